@@ -1,0 +1,311 @@
+// ref_driver.cpp -- TEST INFRASTRUCTURE ONLY (see spiketrain_oracle.h).
+//
+// extern "C" shim over the UNMODIFIED reference headers
+// (/root/reference/proj/include/spiketrain, included read-only via -I by
+// oracle/Makefile).  It exports the orc_* interface under the ref_* prefix so
+// the tests can compare the plain-C restatement with the reference itself,
+// and so bench.py can time the reference's own CPU train_step.  Output goes
+// to oracle/_ref/ only.
+#include <cstring>
+#include <vector>
+
+#include "spiketrain/data.hpp"
+#include "spiketrain/network.hpp"
+#include "spiketrain/objective.hpp"
+#include "spiketrain/optimize.hpp"
+#include "spiketrain/commands.hpp"
+
+#include "spiketrain_oracle.h"
+
+using namespace spiketrain;
+
+namespace {
+
+ActivationDesc act_desc(const orc_net* n) {
+  static const char* names[] = {"custom", "superspike", "triangular", "arctan",
+                                "boxcar"};
+  ActivationDesc d;
+  d.name = names[n->act];
+  d.slope = double(n->slope);
+  d.aux = double(n->aux);
+  return d;
+}
+
+NetworkSpec make_spec(const orc_net* n) {
+  NetworkSpec s;
+  s.input_shape = {std::size_t(n->in)};
+  for (int l = 0; l < n->n_hidden; ++l) {
+    s.layers.push_back(LinearLayer{std::size_t(n->hidden[l]), n->bias != 0});
+    LIFLayer lif;
+    lif.activation = act_desc(n);
+    lif.threshold = double(n->threshold);
+    s.layers.push_back(lif);
+  }
+  s.layers.push_back(LinearLayer{std::size_t(n->classes), n->bias != 0});
+  s.layers.push_back(LILayer{});
+  return s;
+}
+
+NetworkParams<float> params_from_flat(const NetworkParams<float>& shape_src,
+                                      const float* flat) {
+  NetworkParams<float> p;
+  std::size_t off = 0;
+  for (const auto& e : shape_src.entries) {
+    Tensor<float> t(e.tensor.shape());
+    std::memcpy(t.data(), flat + off, t.size() * sizeof(float));
+    off += t.size();
+    p.entries.push_back({e.name, t, e.trainable});
+  }
+  return p;
+}
+
+void params_to_flat(const NetworkParams<float>& p, float* flat) {
+  std::size_t off = 0;
+  for (const auto& e : p.entries) {
+    std::memcpy(flat + off, e.tensor.data(), e.tensor.size() * sizeof(float));
+    off += e.tensor.size();
+  }
+}
+
+NetworkParams<float> skeleton(const orc_net* n) {
+  return init<float>(make_spec(n), RngKey::from_seed(0),
+                     Tensor<float>::zeros({1, 1, std::size_t(n->in)}));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_entry_count(const orc_net* n) {
+  return int(skeleton(n).entries.size());
+}
+
+size_t ref_param_count(const orc_net* n) { return skeleton(n).scalar_count(); }
+
+void ref_entry_layout(const orc_net* n, size_t* offsets, size_t* sizes,
+                      char (*names)[16]) {
+  std::size_t off = 0;
+  int i = 0;
+  for (const auto& e : skeleton(n).entries) {
+    if (offsets) offsets[i] = off;
+    if (sizes) sizes[i] = e.tensor.size();
+    if (names) std::snprintf(names[i], 16, "%s", e.name.c_str());
+    off += e.tensor.size();
+    ++i;
+  }
+}
+
+uint64_t ref_key_from_seed(uint64_t seed) {
+  return RngKey::from_seed(seed).word;
+}
+uint64_t ref_key_child(uint64_t key, uint64_t index) {
+  return RngKey{key}.child(index).word;
+}
+uint64_t ref_key_bits(uint64_t key, uint64_t counter) {
+  return RngKey{key}.bits(counter);
+}
+double ref_uniform01(uint64_t key, uint64_t counter) {
+  return uniform01(RngKey{key}, counter);
+}
+void ref_permutation(uint64_t key, size_t n, uint64_t* out) {
+  const auto p = permutation(RngKey{key}, n);
+  for (size_t i = 0; i < n; ++i) out[i] = p[i];
+}
+void ref_truncated_normal(uint64_t key, size_t n, float mean, float sd,
+                          float* out) {
+  const auto t = rng_truncated_normal<float>(RngKey{key}, Shape{n}, mean, sd);
+  std::memcpy(out, t.data(), n * sizeof(float));
+}
+
+void ref_synth_raster(size_t classes, size_t n, size_t t, size_t f,
+                      uint64_t seed, uint8_t* x, int64_t* y) {
+  const RasterDataset d = synth_raster(classes, n, t, Shape{f}, seed);
+  std::memcpy(x, d.x.data(), d.x.size());
+  for (size_t i = 0; i < n; ++i) y[i] = d.y[i];
+}
+
+void ref_pack_time(const uint8_t* x, size_t n, size_t t, size_t f,
+                   uint8_t* out) {
+  Tensor<std::uint8_t> xt(Shape{n, t, f});
+  std::memcpy(xt.data(), x, n * t * f);
+  const auto p = pack_time(xt, 1);
+  std::memcpy(out, p.data(), p.size());
+}
+
+void ref_unpack_time(const uint8_t* packed, size_t n, size_t t, size_t f,
+                     uint8_t* out) {
+  Tensor<std::uint8_t> pt(Shape{n, (t + 7) / 8, f});
+  std::memcpy(pt.data(), packed, pt.size());
+  const auto u = unpack_time<std::uint8_t>(pt, t, 1);
+  std::memcpy(out, u.data(), u.size());
+}
+
+void ref_init(const orc_net* n, uint64_t key, float* params) {
+  const auto p = init<float>(make_spec(n), RngKey{key},
+                             Tensor<float>::zeros({1, 1, std::size_t(n->in)}));
+  params_to_flat(p, params);
+}
+
+int ref_forward_backward(const orc_net* n, const float* params,
+                         const uint8_t* packed, size_t batch, size_t t_steps,
+                         const int64_t* targets, float* loss, double* acc,
+                         float* grads, uint8_t* spikes, float* vtrace,
+                         float* trace) {
+  (void)vtrace;
+  try {
+    const NetworkSpec spec = make_spec(n);
+    const NetworkParams<float> p = params_from_flat(skeleton(n), params);
+    Tensor<std::uint8_t> px(Shape{batch, (t_steps + 7) / 8, std::size_t(n->in)});
+    std::memcpy(px.data(), packed, px.size());
+    const std::vector<std::int64_t> y(targets, targets + batch);
+    // train_step without the update, mirroring optimize.hpp:157-203.
+    Tensor<float> x = unpack_time<float>(px, t_steps, 1);
+    Tape<float> tape;
+    std::vector<Tape<float>::Id> ids;
+    for (const auto& e : p.entries)
+      ids.push_back(e.trainable ? tape.leaf(e.tensor) : tape.constant(e.tensor));
+    auto fwd = forward_taped(tape, spec, ids, tape.constant(std::move(x)),
+                             std::size_t(n->unroll));
+    auto l = integral_crossentropy_taped(tape, fwd.trace, y);
+    *loss = tape.value(l)[0];
+    *acc = integral_accuracy(tape.value(fwd.trace), y);
+    if (trace)
+      std::memcpy(trace, tape.value(fwd.trace).data(),
+                  tape.value(fwd.trace).size() * sizeof(float));
+    if (grads) {
+      tape.backward(l);
+      std::size_t off = 0;
+      for (std::size_t i = 0; i < ids.size(); ++i) {
+        const Tensor<float> g = tape.grad(ids[i]);
+        std::memcpy(grads + off, g.data(), g.size() * sizeof(float));
+        off += g.size();
+      }
+    }
+    if (spikes) {
+      // Hidden rasters via the prefix-network trick (network_test.cpp:180-185):
+      // the prefix ending at LIF l reuses the identical entries, so its
+      // readout trace is that cell's spike train.
+      std::size_t off = 0;
+      const int per = n->bias ? 3 : 2;
+      for (int h = 0; h < n->n_hidden; ++h) {
+        NetworkSpec prefix;
+        prefix.input_shape = spec.input_shape;
+        prefix.layers.assign(spec.layers.begin(),
+                             spec.layers.begin() + 2 * (h + 1));
+        NetworkParams<float> pp;
+        pp.entries.assign(p.entries.begin(),
+                          p.entries.begin() + per * (h + 1));
+        Tensor<float> xin = unpack_time<float>(px, t_steps, 1);
+        const auto r = apply(prefix, pp, xin, std::size_t(n->unroll));
+        for (std::size_t i = 0; i < r.trace.size(); ++i)
+          spikes[off + i] = r.trace[i] != 0.0f;
+        off += r.trace.size();
+      }
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+void ref_adam(float* p, const float* g, float* m, float* v, size_t n,
+              uint64_t* step, float lr, float beta1, float beta2, float eps) {
+  NetworkParams<float> holder;
+  Tensor<float> pt(Shape{n});
+  std::memcpy(pt.data(), p, n * sizeof(float));
+  holder.entries.push_back({"p", pt, true});
+  auto st = init_optimizer(OptimizerKind::Adam, holder);
+  std::memcpy(st.m[0].data(), m, n * sizeof(float));
+  std::memcpy(st.v[0].data(), v, n * sizeof(float));
+  st.step = *step;
+  Tensor<float> gt(Shape{n});
+  std::memcpy(gt.data(), g, n * sizeof(float));
+  std::vector<Tensor<float>*> ps = {&holder.entries[0].tensor};
+  adam_update(ps, {gt}, st, lr, beta1, beta2, eps);
+  std::memcpy(p, holder.entries[0].tensor.data(), n * sizeof(float));
+  std::memcpy(m, st.m[0].data(), n * sizeof(float));
+  std::memcpy(v, st.v[0].data(), n * sizeof(float));
+  *step = st.step;
+}
+
+namespace {
+
+TrainState<float> make_state(const orc_net* n, const float* params,
+                             const float* m, const float* v, uint64_t step,
+                             float lr) {
+  TrainState<float> st;
+  st.spec = make_spec(n);
+  st.cfg.unroll = std::size_t(n->unroll);
+  st.cfg.lr = double(lr);
+  st.params = params_from_flat(skeleton(n), params);
+  st.opt = init_optimizer(OptimizerKind::Adam, st.params);
+  std::size_t off = 0;
+  for (std::size_t i = 0; i < st.opt.m.size(); ++i) {
+    std::memcpy(st.opt.m[i].data(), m + off, st.opt.m[i].size() * sizeof(float));
+    std::memcpy(st.opt.v[i].data(), v + off, st.opt.v[i].size() * sizeof(float));
+    off += st.opt.m[i].size();
+  }
+  st.opt.step = step;
+  return st;
+}
+
+void unload_state(const TrainState<float>& st, float* params, float* m,
+                  float* v, uint64_t* step) {
+  params_to_flat(st.params, params);
+  std::size_t off = 0;
+  for (std::size_t i = 0; i < st.opt.m.size(); ++i) {
+    std::memcpy(m + off, st.opt.m[i].data(), st.opt.m[i].size() * sizeof(float));
+    std::memcpy(v + off, st.opt.v[i].data(), st.opt.v[i].size() * sizeof(float));
+    off += st.opt.m[i].size();
+  }
+  *step = st.opt.step;
+}
+
+}  // namespace
+
+int ref_train_step(const orc_net* n, float* params, float* m, float* v,
+                   uint64_t* step, const uint8_t* packed, size_t batch,
+                   size_t t_steps, const int64_t* targets, float lr,
+                   float* loss, double* acc) {
+  try {
+    TrainState<float> st = make_state(n, params, m, v, *step, lr);
+    Tensor<std::uint8_t> px(Shape{batch, (t_steps + 7) / 8, std::size_t(n->in)});
+    std::memcpy(px.data(), packed, px.size());
+    const std::vector<std::int64_t> y(targets, targets + batch);
+    const StepResult<float> r = train_step(st, px, t_steps, y);
+    *loss = r.loss;
+    *acc = r.accuracy;
+    unload_state(st, params, m, v, step);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+int ref_train_epochs(const orc_net* n, float* params, float* m, float* v,
+                     uint64_t* step, const uint8_t* packed, const int64_t* y,
+                     size_t count, size_t t_steps, size_t batch, size_t epochs,
+                     uint64_t seed, float lr, double* metrics) {
+  try {
+    TrainState<float> st = make_state(n, params, m, v, *step, lr);
+    st.cfg.batch_size = batch;
+    st.cfg.epochs = epochs;
+    st.cfg.seed = seed;
+    PackedDataset d;
+    d.x = Tensor<std::uint8_t>(Shape{count, (t_steps + 7) / 8, std::size_t(n->in)});
+    std::memcpy(d.x.data(), packed, d.x.size());
+    d.original_t = t_steps;
+    d.y.assign(y, y + count);
+    const auto r = train(st, d);
+    for (std::size_t e = 0; e < r.metrics.size(); ++e) {
+      metrics[2 * e] = r.metrics[e].loss;
+      metrics[2 * e + 1] = r.metrics[e].accuracy;
+    }
+    unload_state(st, params, m, v, step);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+}  // extern "C"

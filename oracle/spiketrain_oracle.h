@@ -1,0 +1,128 @@
+/*
+ * spiketrain_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement of the reference training step (spiketrain, header-only
+ * C++20 under /root/reference/proj/include/spiketrain).  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library, and only as the checker or the timed CPU baseline.
+ * The product path (paper_2402_18994_b200) never links or calls it.
+ *
+ * Two implementations export this interface:
+ *   orc_*  -- oracle/spiketrain_oracle.c, an independent plain-C restatement
+ *             (fp32, same operation order as the reference, so results are
+ *             bit-identical to it on the same libm);
+ *   ref_*  -- oracle/ref_driver.cpp, a thin extern "C" driver that calls the
+ *             reference headers themselves; compiled into oracle/_ref/.
+ * The CPU test-suite pins orc_* against ref_* bit for bit and against the
+ * committed golden vectors in tests/golden/.
+ */
+#ifndef SPIKETRAIN_ORACLE_H
+#define SPIKETRAIN_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_MAX_HIDDEN 8
+
+/* Surrogate catalogue (surrogate.hpp:134-157). */
+enum orc_act {
+  ORC_ACT_CUSTOM = 0,     /* straight-through: g = 1          (surrogate.hpp:45-57) */
+  ORC_ACT_SUPERSPIKE = 1, /* 1/(1+k|x|)^2                     (surrogate.hpp:59-73) */
+  ORC_ACT_TRIANGULAR = 2, /* max(0, 1-|kx|)                   (surrogate.hpp:75-88) */
+  ORC_ACT_ARCTAN = 3,     /* 1/(1+(pi k x/2)^2)               (surrogate.hpp:90-104) */
+  ORC_ACT_BOXCAR = 4      /* h on |x|<=w/2                    (surrogate.hpp:106-120) */
+};
+
+/*
+ * Feed-forward SNN of the shape every BASELINE config uses:
+ *   Linear(in->h0) -> LIF -> Linear(h0->h1) -> LIF ... -> Linear(->classes) -> LI
+ * (network.hpp:23-60, normalised layer ids 0..2*n_hidden+1).  beta is per
+ * neuron (BetaMode::PerNeuron, neuron.hpp:22).
+ */
+typedef struct orc_net {
+  int in;                      /* per-timestep input features            */
+  int n_hidden;                /* number of Linear+LIF blocks            */
+  int hidden[ORC_MAX_HIDDEN];  /* LIF widths                             */
+  int classes;                 /* readout width (Linear + LI)            */
+  int bias;                    /* Linear layers carry a bias entry       */
+  float threshold;             /* LIF threshold theta (network.hpp:47)   */
+  int act;                     /* enum orc_act                           */
+  float slope;                 /* ActivationDesc.slope                   */
+  float aux;                   /* ActivationDesc.aux (boxcar height)     */
+  int unroll;                  /* TrainConfig.unroll (optimize.hpp:130)  */
+} orc_net;
+
+/* Parameter entries in NetworkParams order (network.hpp:231-286). */
+int orc_entry_count(const orc_net* net);
+/* offsets/sizes in floats into the flat parameter vector; names "l{i}.w" ... */
+void orc_entry_layout(const orc_net* net, size_t* offsets, size_t* sizes,
+                      char (*names)[16]);
+size_t orc_param_count(const orc_net* net);
+
+/* SplitMix64 key algebra (rng.hpp:20-48). Keys are the 64-bit `word`. */
+uint64_t orc_key_from_seed(uint64_t seed);
+uint64_t orc_key_child(uint64_t key, uint64_t index);
+uint64_t orc_key_bits(uint64_t key, uint64_t counter);
+double orc_uniform01(uint64_t key, uint64_t counter);
+void orc_permutation(uint64_t key, size_t n, uint64_t* out);
+void orc_truncated_normal(uint64_t key, size_t n, float mean, float stddev,
+                          float* out);
+
+/* synth_raster (commands.hpp:50-86): x [n, t, f] u8, y [n]. */
+void orc_synth_raster(size_t classes, size_t n, size_t t, size_t f,
+                      uint64_t seed, uint8_t* x, int64_t* y);
+/* pack_time / unpack_time along axis 1 (data.hpp:105-149). */
+void orc_pack_time(const uint8_t* x, size_t n, size_t t, size_t f,
+                   uint8_t* out);
+void orc_unpack_time(const uint8_t* packed, size_t n, size_t t, size_t f,
+                     uint8_t* out);
+
+/* init(spec, key, sample) (network.hpp:231-286); key = master.child(0). */
+void orc_init(const orc_net* net, uint64_t key, float* params);
+
+/*
+ * One taped forward + loss + accuracy + reverse sweep (optimize.hpp:152-203),
+ * without the optimizer update.  packed: [B, ceil(T/8), in] MSB-first.
+ * Outputs (all optional except loss/acc):
+ *   grads   [param_count]                 tape.grad of every entry
+ *   spikes  [sum_l B*T*hidden[l]]  u8     hidden spike rasters, layer-major
+ *   vtrace  [sum_l B*T*hidden[l]]  f32    membrane entering each step
+ *   trace   [B*T*classes]          f32    LI readout trace
+ * Returns 0 on success, nonzero on a shape/argument error.
+ */
+int orc_forward_backward(const orc_net* net, const float* params,
+                         const uint8_t* packed, size_t batch, size_t t_steps,
+                         const int64_t* targets, float* loss, double* acc,
+                         float* grads, uint8_t* spikes, float* vtrace,
+                         float* trace);
+
+/* adam_update over a flat buffer (optimize.hpp:86-111); *step is the
+ * optimizer step counter, incremented here before the bias correction. */
+void orc_adam(float* p, const float* g, float* m, float* v, size_t n,
+              uint64_t* step, float lr, float beta1, float beta2, float eps);
+
+/* Full train_step: forward_backward + Adam over trainable entries. */
+int orc_train_step(const orc_net* net, float* params, float* m, float* v,
+                   uint64_t* step, const uint8_t* packed, size_t batch,
+                   size_t t_steps, const int64_t* targets, float lr,
+                   float* loss, double* acc);
+
+/*
+ * train(TrainState&, data) epoch loop (optimize.hpp:260-299): per epoch e the
+ * permutation key master.child(1+e).child(0), drop-remainder batches, one
+ * train_step each.  metrics: [epochs][2] = {mean loss, mean accuracy}.
+ */
+int orc_train_epochs(const orc_net* net, float* params, float* m, float* v,
+                     uint64_t* step, const uint8_t* packed, const int64_t* y,
+                     size_t n, size_t t_steps, size_t batch, size_t epochs,
+                     uint64_t seed, float lr, double* metrics);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

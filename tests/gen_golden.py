@@ -1,0 +1,109 @@
+"""Generate tests/golden/*.npz from the REFERENCE ITSELF (oracle/_ref).
+
+Run here (needs /root/reference to build oracle/_ref):
+    python tests/gen_golden.py
+The fixtures pin the plain-C oracle (oracle/liboracle.so) on machines where the
+reference is absent (the GPU box).  Every array comes from ref_* entry points,
+i.e. from the unmodified spiketrain headers.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle.pyoracle import Lib, Net, State, have_ref  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+TINY = Net(inp=30, hidden=(16, 12), classes=5, act="arctan", unroll=4)
+C1 = Net()  # 700-128-128-20, arctan k=2, nobias, unroll 32
+
+
+def net_dict(n: Net) -> dict:
+    return dict(inp=n.inp, hidden=np.array(n.hidden), classes=n.classes,
+                bias=int(n.bias), threshold=n.threshold, act=n.act,
+                unroll=n.unroll)
+
+
+def tiny(ref: Lib):
+    key = ref.key_child(ref.key_from_seed(5), 0)
+    p = ref.init(TINY, key) * np.float32(3.0)  # scale for activity
+    x, y = ref.synth_raster(5, 12, 19, 30, 3)
+    pk = ref.pack_time(x)
+    out = ref.forward_backward(TINY, p, pk, 19, y, want_spikes=True, want_trace=True)
+    st = State(p.copy())
+    l1, a1 = ref.train_step(TINY, st, pk, 19, y)
+    st2 = State(p.copy())
+    metrics = ref.train_epochs(TINY, st2, pk, y, 19, 4, 3, 7)
+    np.savez_compressed(
+        os.path.join(GOLD, "tiny.npz"), **{f"net_{k}": v for k, v in net_dict(TINY).items()},
+        params=p, packed=pk, y=y, t=19, loss=out["loss"], acc=out["acc"],
+        grads=out["grads"], trace=out["trace"],
+        spikes0=out["spikes"][0], spikes1=out["spikes"][1],
+        step_params=st.params, step_m=st.m, step_v=st.v, step_loss=l1,
+        epochs_params=st2.params, epochs_metrics=metrics, epochs_step=st2.step)
+
+
+def c1(ref: Lib):
+    """C1 shape: init and warm (3 epochs x 4 steps at N=1024, B=256, seed 0)."""
+    master = ref.key_from_seed(0)
+    p_init = ref.init(C1, ref.key_child(master, 0))
+    x, y = ref.synth_raster(20, 1024, 128, 700, 1)
+    pk = ref.pack_time(x)
+    st = State(p_init.copy())
+    metrics = ref.train_epochs(C1, st, pk, y, 128, 256, 3, 0)
+    # "hot": resume the warm state for 9 more epochs (epoch keys restart at 0
+    # on resume, optimize.hpp:258) -> hidden rates of several percent.
+    hot = st.copy()
+    hot_metrics = ref.train_epochs(C1, hot, pk, y, 128, 256, 9, 0)
+    # evaluation batch: first 16 examples of the dataset (labels 0..15)
+    bx, by = pk[:16], y[:16]
+    res = {}
+    for tag, params in (("init", p_init), ("warm", st.params), ("hot", hot.params)):
+        o = ref.forward_backward(C1, params, bx, 128, by, want_spikes=True, want_trace=True)
+        res[tag] = o
+    np.savez_compressed(
+        os.path.join(GOLD, "c1.npz"), **{f"net_{k}": v for k, v in net_dict(C1).items()},
+        params_init=p_init, warm_params=st.params, warm_m=st.m, warm_v=st.v,
+        warm_step=st.step, warm_metrics=metrics, batch_packed=bx, batch_y=by,
+        hot_params=hot.params, hot_step=hot.step, hot_metrics=hot_metrics,
+        dataset_packed_sha=np.frombuffer(__import__("hashlib").sha256(pk.tobytes()).digest(), np.uint8),
+        **{f"{t}_{k}": v for t, o in res.items() for k, v in (
+            ("loss", o["loss"]), ("acc", o["acc"]), ("grads", o["grads"]),
+            ("trace", o["trace"]),
+            ("spikes0_bits", np.packbits(o["spikes"][0])),
+            ("spikes1_bits", np.packbits(o["spikes"][1])))})
+    print("warm metrics", metrics.tolist(), "hot", hot_metrics.tolist())
+    for tag in res:
+        print(tag, "rates", [float(s.mean()) for s in res[tag]["spikes"]])
+
+
+def rng_kats(ref: Lib):
+    k = ref.key_from_seed(42)
+    vals = dict(
+        seed42_word=np.uint64(k),
+        bits=np.array([ref.key_bits(k, i) for i in range(8)], np.uint64),
+        child=np.array([ref.key_child(k, i) for i in range(8)], np.uint64),
+        uniform=np.array([ref.uniform01(k, i) for i in range(8)], np.float64),
+        perm=ref.permutation(ref.key_child(k, 3), 50),
+        tnorm=ref.truncated_normal(ref.key_child(k, 4), 64, 0.5, 0.25))
+    np.savez_compressed(os.path.join(GOLD, "rng.npz"), **vals)
+
+
+if __name__ == "__main__":
+    if not have_ref():
+        Lib.__init__  # noqa: B018
+        from oracle.pyoracle import build
+        build()
+    if not have_ref():
+        sys.exit("oracle/_ref not buildable here (no /root/reference)")
+    os.makedirs(GOLD, exist_ok=True)
+    ref = Lib("ref")
+    rng_kats(ref)
+    tiny(ref)
+    c1(ref)
+    print("golden fixtures written to", GOLD)

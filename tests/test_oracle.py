@@ -1,0 +1,185 @@
+"""Pins the plain-C oracle against the reference (CPU only).
+
+* golden vectors in tests/golden/ were produced by the unmodified reference
+  (tests/gen_golden.py -> oracle/_ref); the oracle must reproduce them BIT FOR
+  BIT (same fp32 operation order, -ffp-contract=off, same libm);
+* known-answer tests restated from the reference's own suite
+  (data_test.cpp:26-44, optimize_test.cpp:82-95, rng_test.cpp);
+* when oracle/_ref is present (this container), randomized configurations are
+  compared live against the reference.
+"""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Lib, Net, State, have_ref
+
+
+def _net(g):
+    return Net(inp=int(g["net_inp"]), hidden=tuple(int(h) for h in g["net_hidden"]),
+               classes=int(g["net_classes"]), bias=bool(g["net_bias"]),
+               threshold=float(g["net_threshold"]), act=str(g["net_act"]),
+               unroll=int(g["net_unroll"]))
+
+
+def test_rng_golden(orc, golden):
+    g = golden("rng")
+    k = orc.key_from_seed(42)
+    assert np.uint64(k) == g["seed42_word"]
+    assert [orc.key_bits(k, i) for i in range(8)] == g["bits"].tolist()
+    assert [orc.key_child(k, i) for i in range(8)] == g["child"].tolist()
+    assert [orc.uniform01(k, i) for i in range(8)] == g["uniform"].tolist()
+    assert np.array_equal(orc.permutation(orc.key_child(k, 3), 50), g["perm"])
+    assert np.array_equal(orc.truncated_normal(orc.key_child(k, 4), 64, 0.5, 0.25),
+                          g["tnorm"])
+
+
+def test_permutation_is_a_permutation(orc):
+    p = orc.permutation(orc.key_from_seed(3), 1000)
+    assert sorted(p.tolist()) == list(range(1000))
+
+
+def test_pack_msb_first_kat(orc):
+    # data_test.cpp:26-38: T=10, spikes at t 0,3,8,9 -> 0x90, 0xC0
+    x = np.zeros((1, 10, 1), np.uint8)
+    x[0, [0, 3, 8, 9], 0] = 1
+    pk = orc.pack_time(x)
+    assert pk.shape == (1, 2, 1)
+    assert pk[0, 0, 0] == 0x90 and pk[0, 1, 0] == 0xC0
+    # data_test.cpp:40-44: trailing pad bits stay zero
+    assert orc.pack_time(np.ones((1, 3, 1), np.uint8))[0, 0, 0] == 0xE0
+
+
+def test_pack_roundtrip(orc):
+    rng = np.random.default_rng(0)
+    for t in (1, 7, 8, 9, 19, 128, 131):
+        x = (rng.random((3, t, 5)) < 0.3).astype(np.uint8)
+        assert np.array_equal(orc.unpack_time(orc.pack_time(x), t), x)
+
+
+def test_adam_first_step_moves_by_lr(orc):
+    # optimize_test.cpp:82-95 (fp32 here)
+    p = np.array([1.0, -2.0], np.float32)
+    g = np.array([0.5, -3.0], np.float32)
+    m, v = np.zeros(2, np.float32), np.zeros(2, np.float32)
+    assert orc.adam(p, g, m, v, 0, lr=1e-3) == 1
+    assert p[0] == pytest.approx(1.0 - 1e-3, rel=1e-6)
+    assert p[1] == pytest.approx(-2.0 + 1e-3, rel=1e-6)
+
+
+def test_adam_matches_scalar_reference(orc):
+    # optimize_test.cpp:24-36 ScalarAdam, 25 steps (fp32 vs f64 textbook)
+    rng = np.random.default_rng(700)
+    p = rng.standard_normal(3).astype(np.float32)
+    pref = p.astype(np.float64)
+    m, v = np.zeros(3, np.float32), np.zeros(3, np.float32)
+    mr, vr = np.zeros(3), np.zeros(3)
+    step = 0
+    for s in range(1, 26):
+        g = rng.standard_normal(3).astype(np.float32)
+        step = orc.adam(p, g, m, v, step, lr=1e-3)
+        mr = 0.9 * mr + 0.1 * g
+        vr = 0.999 * vr + 0.001 * g.astype(np.float64) ** 2
+        pref = pref - 1e-3 * (mr / (1 - 0.9 ** s)) / (np.sqrt(vr / (1 - 0.999 ** s)) + 1e-8)
+        assert np.allclose(p, pref, rtol=0, atol=2e-6)
+    assert step == 25
+
+
+def test_tiny_golden_bit_exact(orc, golden):
+    g = golden("tiny")
+    net = _net(g)
+    t = int(g["t"])
+    out = orc.forward_backward(net, g["params"], g["packed"], t, g["y"],
+                               want_spikes=True, want_trace=True)
+    assert out["loss"] == float(g["loss"])
+    assert out["acc"] == float(g["acc"])
+    assert np.array_equal(out["trace"], g["trace"])
+    assert np.array_equal(out["spikes"][0], g["spikes0"])
+    assert np.array_equal(out["spikes"][1], g["spikes1"])
+    assert np.array_equal(out["grads"], g["grads"])
+    st = State(g["params"].copy())
+    loss, _ = orc.train_step(net, st, g["packed"], t, g["y"])
+    assert loss == float(g["step_loss"])
+    assert np.array_equal(st.params, g["step_params"])
+    assert np.array_equal(st.m, g["step_m"]) and np.array_equal(st.v, g["step_v"])
+    st2 = State(g["params"].copy())
+    metrics = orc.train_epochs(net, st2, g["packed"], g["y"], t, 4, 3, 7)
+    assert np.array_equal(metrics, g["epochs_metrics"])
+    assert np.array_equal(st2.params, g["epochs_params"])
+    assert st2.step == int(g["epochs_step"])
+
+
+@pytest.mark.parametrize("tag", ["init", "warm", "hot"])
+def test_c1_golden_bit_exact(orc, golden, tag):
+    g = golden("c1")
+    net = _net(g)
+    params = g["params_init"] if tag == "init" else g[f"{tag}_params"]
+    out = orc.forward_backward(net, params, g["batch_packed"], 128, g["batch_y"],
+                               want_spikes=True, want_trace=True)
+    assert out["loss"] == float(g[f"{tag}_loss"])
+    assert out["acc"] == float(g[f"{tag}_acc"])
+    assert np.array_equal(out["trace"], g[f"{tag}_trace"])
+    assert np.array_equal(np.packbits(out["spikes"][0]), g[f"{tag}_spikes0_bits"])
+    assert np.array_equal(np.packbits(out["spikes"][1]), g[f"{tag}_spikes1_bits"])
+    assert np.array_equal(out["grads"], g[f"{tag}_grads"])
+
+
+def test_c1_init_params_golden(orc, golden):
+    g = golden("c1")
+    master = orc.key_from_seed(0)
+    p = orc.init(_net(g), orc.key_child(master, 0))
+    assert np.array_equal(p, g["params_init"])
+    names = [e[0] for e in orc.entries(_net(g))]
+    assert names == ["l0.w", "l1.beta", "l2.w", "l3.beta", "l4.w", "l5.beta"]
+    assert p.size == 108820
+
+
+@pytest.mark.slow
+def test_c1_warm_checkpoint_golden(orc, golden):
+    """Re-train the warm checkpoint (12 steps at C1) and match bit for bit."""
+    g = golden("c1")
+    net = _net(g)
+    x, y = orc.synth_raster(20, 1024, 128, 700, 1)
+    pk = orc.pack_time(x)
+    import hashlib
+    assert hashlib.sha256(pk.tobytes()).digest() == g["dataset_packed_sha"].tobytes()
+    st = State(g["params_init"].copy())
+    metrics = orc.train_epochs(net, st, pk, y, 128, 256, 3, 0)
+    assert np.array_equal(metrics, g["warm_metrics"])
+    assert np.array_equal(st.params, g["warm_params"])
+    assert st.step == int(g["warm_step"])
+
+
+CONFIGS = [
+    Net(inp=30, hidden=(16, 12), classes=5, unroll=4),
+    Net(inp=30, hidden=(16,), classes=5, bias=True, act="superspike", unroll=3),
+    Net(inp=40, hidden=(24, 20, 8), classes=4, bias=True, act="triangular", unroll=5),
+    Net(inp=40, hidden=(24, 20), classes=4, act="boxcar", unroll=7),
+    Net(inp=40, hidden=(24, 20), classes=4, act="custom", unroll=1),
+    Net(inp=33, hidden=(64, 32), classes=7, act="arctan", threshold=0.75, unroll=32),
+]
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref needs /root/reference")
+@pytest.mark.parametrize("cfg", range(len(CONFIGS)))
+def test_oracle_vs_reference_live(orc, cfg):
+    ref = Lib("ref")
+    net = CONFIGS[cfg]
+    assert orc.entries(net) == ref.entries(net)
+    key = orc.key_from_seed(100 + cfg)
+    p = orc.init(net, key)
+    assert np.array_equal(p, ref.init(net, key))
+    p = p * np.float32(3.0)
+    B, T = 10, 23
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 9 + cfg)
+    pk = orc.pack_time(x)
+    a = orc.forward_backward(net, p, pk, T, y, want_spikes=True, want_trace=True)
+    b = ref.forward_backward(net, p, pk, T, y, want_spikes=True, want_trace=True)
+    assert a["loss"] == b["loss"] and a["acc"] == b["acc"]
+    assert np.array_equal(a["trace"], b["trace"])
+    for s1, s2 in zip(a["spikes"], b["spikes"]):
+        assert np.array_equal(s1, s2)
+    assert np.array_equal(a["grads"], b["grads"])
+    s1, s2 = State(p.copy()), State(p.copy())
+    m1 = orc.train_epochs(net, s1, pk, y, T, 3, 2, 5)
+    m2 = ref.train_epochs(net, s2, pk, y, T, 3, 2, 5)
+    assert np.array_equal(m1, m2) and np.array_equal(s1.params, s2.params)
