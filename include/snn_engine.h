@@ -1,0 +1,169 @@
+/*
+ * snn_engine.h -- C ABI of the B200-native SNN training engine.
+ *
+ * Drop-in boundary for the reference's training step.  Each entry point cites
+ * the reference interface it replaces (paths relative to
+ * /root/reference/proj/include/spiketrain/).  Plain pointers and sizes only:
+ * no torch, no C++ types.  All compute runs on the GPU through hand-written
+ * sm_100a kernels; there is no CPU fallback -- without a usable B200 every
+ * call that needs the device returns SNN_ERR_CUDA.
+ *
+ * Threading: an engine handle is not thread-safe (the reference Tape is
+ * single-threaded and single-use, autodiff.hpp:12-16).  Distinct handles may
+ * be driven from distinct threads.
+ */
+#ifndef SNN_ENGINE_H
+#define SNN_ENGINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNN_ABI_VERSION 1
+#define SNN_MAX_HIDDEN 8
+
+/* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
+typedef enum snn_status {
+  SNN_OK = 0,
+  SNN_ERR_SHAPE = 1,       /* ShapeError       */
+  SNN_ERR_ARGUMENT = 2,    /* ArgumentError    */
+  SNN_ERR_CONTRACT = 3,    /* ContractError    */
+  SNN_ERR_STATE = 4,       /* StateError       */
+  SNN_ERR_FORMAT = 5,      /* FormatError      */
+  SNN_ERR_IO = 6,          /* IoError          */
+  SNN_ERR_SPEC = 7,        /* SpecError        */
+  SNN_ERR_CONFIG = 8,      /* ConfigError      */
+  SNN_ERR_UNSUPPORTED = 9, /* UnsupportedError */
+  SNN_ERR_CUDA = 10        /* device failure or no B200: nothing ran on the CPU */
+} snn_status;
+
+/* Surrogate catalogue (surrogate.hpp:134-157 make_activation). */
+typedef enum snn_activation {
+  SNN_ACT_CUSTOM = 0,
+  SNN_ACT_SUPERSPIKE = 1,
+  SNN_ACT_TRIANGULAR = 2,
+  SNN_ACT_ARCTAN = 3,
+  SNN_ACT_BOXCAR = 4
+} snn_activation;
+
+/*
+ * NetworkSpec for the supported family (network.hpp:62-65):
+ *   input_shape {input}; layers = [Linear(hidden[i], bias), LIF]*n_hidden,
+ *                                  Linear(classes, bias), LI
+ * LIF: LIFLayer{activation, PerNeuron beta, threshold} (network.hpp:42-48);
+ * LI : LILayer{PerNeuron} (network.hpp:50-54).
+ */
+typedef struct snn_network_desc {
+  int32_t input;
+  int32_t n_hidden;
+  int32_t hidden[SNN_MAX_HIDDEN];
+  int32_t classes;
+  int32_t bias;         /* LinearLayer.bias (network.hpp:25) */
+  float threshold;      /* LIFLayer.threshold, must be > 0  */
+  int32_t activation;   /* snn_activation                   */
+  float slope;          /* ActivationDesc.slope             */
+  float aux;            /* ActivationDesc.aux               */
+} snn_network_desc;
+
+/* TrainConfig subset that reaches the step (optimize.hpp:116-133). */
+typedef struct snn_train_config {
+  int32_t batch_size;   /* examples per step on THIS rank (global = batch_size * world) */
+  int32_t time_steps;   /* original T of the packed data (PackedDataset.original_t) */
+  float lr;             /* TrainConfig.lr, Adam (optimize.hpp:86-111) */
+  float beta1, beta2, eps;
+  uint64_t seed;        /* TrainConfig.seed: init key child(0), epoch keys child(1+e) */
+  int32_t unroll;       /* accepted for API parity; scheduling only (network.hpp:352) */
+} snn_train_config;
+
+typedef struct snn_engine snn_engine;
+
+/* Last error message of a handle (or of the last failed create when NULL). */
+const char* snn_last_error(const snn_engine* e);
+int snn_abi_version(void);
+
+/* Construct: validates the spec like normalize() (network.hpp:125-157),
+ * allocates all device state, initialises parameters exactly like
+ * train(spec, cfg, data) does (init(spec, master.child(0)), optimize.hpp:246-254). */
+snn_status snn_engine_create(const snn_network_desc* net, const snn_train_config* cfg,
+                             int device, snn_engine** out);
+void snn_engine_destroy(snn_engine* e);
+
+/* NetworkParams as one flat f32 vector in entry order l{i}.w, l{i}.b, l{i}.beta
+ * (network.hpp:164-226).  Entry i: name, offset, size, trainable. */
+snn_status snn_param_count(const snn_engine* e, size_t* n);
+snn_status snn_entry_count(const snn_engine* e, int32_t* n);
+snn_status snn_entry_info(const snn_engine* e, int32_t i, char name[16], size_t* offset,
+                          size_t* size, int32_t* trainable);
+snn_status snn_set_params(snn_engine* e, const float* host, size_t n);
+snn_status snn_get_params(snn_engine* e, float* host, size_t n);
+/* Reference init (network.hpp:231-286) from an explicit key word. */
+snn_status snn_init_params(snn_engine* e, uint64_t key_word);
+/* OptimizerState m, v, step (optimize.hpp:28-48), trainable entries in order. */
+snn_status snn_get_opt_state(snn_engine* e, float* m, float* v, uint64_t* step, size_t n);
+snn_status snn_set_opt_state(snn_engine* e, const float* m, const float* v, uint64_t step,
+                             size_t n);
+/* Gradients of the last step (tape.grad of every entry, before the update). */
+snn_status snn_get_grads(snn_engine* e, float* host, size_t n);
+
+/* PackedDataset staged once in HBM (data.hpp:159-163): packed u8
+ * [n][ceil(T/8)][input] MSB-first, labels in [0, classes). */
+snn_status snn_stage_dataset(snn_engine* e, const uint8_t* packed, size_t n,
+                             const int64_t* labels);
+
+/* train_step on rows of the staged dataset (optimize.hpp:152-214).  rows: host
+ * array of batch_size dataset indices.  Updates params + optimizer state in
+ * place and returns StepResult{loss, accuracy} (global over ranks). */
+snn_status snn_train_step(snn_engine* e, const uint32_t* rows, float* loss, double* accuracy);
+
+/* Reference-shaped compatibility entry: train_step(st, packed_x, T, targets)
+ * with a HOST packed batch [batch_size][ceil(T/8)][input] and int64 targets. */
+snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
+                                 const int64_t* targets, float* loss, double* accuracy);
+
+/* Forward + loss + reverse sweep without the optimizer update (gradients are
+ * then readable with snn_get_grads). */
+snn_status snn_forward_backward(snn_engine* e, const uint32_t* rows, float* loss,
+                                double* accuracy);
+
+/* train(TrainState&, data) epoch loop over the staged dataset
+ * (optimize.hpp:260-299): epoch e shuffles with master.child(1+e).child(0),
+ * drop-remainder batches.  metrics: [epochs][2] mean loss, mean accuracy. */
+snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics);
+
+/* Asynchronous stepping for throughput measurement: enqueue one full step
+ * (captured CUDA graph) on the engine stream with batch rows taken from the
+ * device index buffer slot `slot` of the uploaded schedule; no host sync. */
+snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_steps);
+snn_status snn_enqueue_step(snn_engine* e, size_t slot);
+snn_status snn_sync(snn_engine* e);
+snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy);
+/* cudaStream_t of the engine, for CUDA-event timing by the caller. */
+void* snn_stream(snn_engine* e);
+/* Number of kernel launches one step issues. */
+int32_t snn_launches_per_step(const snn_engine* e);
+
+/* Data-parallel training: one engine per GPU/process.  Every rank passes the
+ * same 128-byte ncclUniqueId (rank 0 creates it with snn_nccl_unique_id).
+ * After this call each step allreduces the flat gradient (sum) and uses the
+ * global batch in the loss mean. */
+snn_status snn_nccl_unique_id(uint8_t id[128]);
+snn_status snn_comm_init(snn_engine* e, const uint8_t id[128], int32_t rank, int32_t world);
+
+/* Diagnostics: raw intermediate tensors of the last forward_backward when
+ * enabled (costs extra HBM writes; off by default).
+ *   which 0: projection I of hidden layer `layer`   [B][T][H]
+ *         1: membrane V (entering step t)           [B][T][H]
+ *         2: spikes (0/1 as u8)                     [B][T][H]
+ *         3: readout trace                          [B][T][C]
+ *         4: dS (grad of spikes) of hidden `layer`  [B][T][H]  */
+snn_status snn_debug_enable(snn_engine* e, int32_t on);
+snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* host, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SNN_ENGINE_H */

@@ -1,0 +1,978 @@
+// engine.cu -- host side of the B200 SNN training engine and its C ABI
+// (include/snn_engine.h).  One engine = one GPU = one data-parallel rank.
+//
+// Step schedule (all on one stream, captured once into a CUDA graph):
+//   k_lif_fwd x L          GEMM (tcgen05, TMEM) + LIF scan per (sample, 128 neurons)
+//   k_readout              readout projection + LI + integral CE + LI reverse scan
+//   k_lif_bwd_ro / _gemm   dS (CUDA-core for the readout, tcgen05 otherwise) + LIF reverse scan
+//   k_wgrad x (L+1)        dW = A^T dI on tcgen05, split-K partials
+//   k_reduce, k_loss_partial, [ncclAllReduce], k_adam, k_result
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/snn_engine.h"
+#include "host_rng.hpp"
+#include "kernels.cuh"
+
+using namespace snn;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct SnnError {
+  snn_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(snn_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  throw SnnError{code, buf};
+}
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t err__ = (x);                                                           \
+    if (err__ != cudaSuccess)                                                          \
+      fail(SNN_ERR_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(err__), __FILE__, \
+           __LINE__);                                                                  \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  using comm_t = void*;
+  int (*GetUniqueId)(void*) = nullptr;
+  int (*CommInitRank)(comm_t*, int, void* /*by value 128B*/, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, comm_t, cudaStream_t) = nullptr;
+  int (*CommDestroy)(comm_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool ok = false;
+};
+
+struct UniqueId {
+  char internal[128];
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    const char* env = std::getenv("SNN_NCCL_LIB");
+    void* h = nullptr;
+    if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+      api.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*,
+                                               cudaStream_t)>(dlsym(h, "ncclAllReduce"));
+      api.CommDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+      api.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+      api.CommInitRank = reinterpret_cast<int (*)(void**, int, void*, int)>(
+          dlsym(h, "ncclCommInitRank"));
+      api.ok = api.GetUniqueId && api.AllReduce && api.CommDestroy && api.CommInitRank;
+    }
+  }
+  return api;
+}
+
+// ncclCommInitRank takes ncclUniqueId by value (128 bytes): call through a
+// correctly typed pointer.
+using InitRankFn = int (*)(void**, int, UniqueId, int);
+
+// -------------------------------------------------------------- tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [rows][cols] (cols contiguous), box {64 cols, box_rows}, 128B swizzle.
+CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return m;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count, bool zero = true) {
+    free();
+    n = count;
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    if (zero) CK(cudaMemset(p, 0, count * sizeof(T)));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { free(); }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+struct EntryHost {
+  std::string name;
+  int kind, layer, rows, cols;
+  size_t offset, size;
+};
+
+struct Dataset {
+  DevBuf<uint8_t> x;       // [n][T_pad/8][IN_pad]
+  DevBuf<int32_t> labels;  // [n]
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct snn_engine {
+  snn_network_desc net{};
+  snn_train_config cfg{};
+  int device = 0;
+  std::string err;
+
+  // dimensions
+  int B = 0, T = 0, TT = 0, NT = 0, T_pad = 0, IN = 0, IN_pad = 0, L = 0, C = 0;
+  int H[SNN_MAX_HIDDEN]{}, H_pad[SNN_MAX_HIDDEN]{};
+  int K[kMaxLayers]{}, N[kMaxLayers]{}, K_pad[kMaxLayers]{}, N_pad[kMaxLayers]{};
+  int M_pad_w[kMaxLayers]{}, n_tile_w[kMaxLayers]{}, splits_w[kMaxLayers]{};
+  std::vector<EntryHost> entries;
+  size_t n_params = 0;
+
+  cudaStream_t stream = nullptr;
+  // parameters / optimizer
+  DevBuf<float> params, m, v, comm;  // comm = grads [n_params] + loss_sum + hits
+  DevBuf<float> bc;
+  size_t bc_steps = 0;
+  DevBuf<int64_t> step;
+  DevBuf<__nv_bfloat16> wt[kMaxLayers], wb[kMaxLayers];
+  // activations
+  DevBuf<float> V[SNN_MAX_HIDDEN];
+  DevBuf<uint32_t> s_np[SNN_MAX_HIDDEN], s_tp[SNN_MAX_HIDDEN];
+  DevBuf<__nv_bfloat16> di[kMaxLayers];  // per Linear j: dI of its output
+  DevBuf<float> dbeta[kMaxLayers], dbias[kMaxLayers];
+  DevBuf<float> d3, loss_b;
+  DevBuf<int32_t> correct_b;
+  DevBuf<float> partial[kMaxLayers];
+  DevBuf<float> result_loss;
+  DevBuf<double> result_acc;
+  float* h_loss = nullptr;
+  double* h_acc = nullptr;
+  uint32_t* h_rows = nullptr;
+  // data
+  Dataset data, scratch;
+  DevBuf<uint32_t> rows_cur, sched;
+  size_t sched_steps = 0;
+  // tensor maps
+  CUtensorMap tm_wt[kMaxLayers], tm_wb[kMaxLayers], tm_di_k[kMaxLayers], tm_di_w[kMaxLayers];
+  // debug
+  bool debug = false;
+  DevBuf<float> dbg_i[SNN_MAX_HIDDEN], dbg_ds[SNN_MAX_HIDDEN], dbg_trace;
+  // graphs keyed by (dataset ptr, update flag)
+  std::map<std::pair<const void*, int>, cudaGraphExec_t> graphs;
+  // multi-GPU
+  void* comm_handle = nullptr;
+  int rank = 0, world = 1;
+  bool planes_dirty = true;
+
+  ~snn_engine() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    if (comm_handle && nccl().ok) nccl().CommDestroy(comm_handle);
+    if (h_loss) cudaFreeHost(h_loss);
+    if (h_acc) cudaFreeHost(h_acc);
+    if (h_rows) cudaFreeHost(h_rows);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void clear_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    graphs.clear();
+  }
+
+  int B_global() const { return B * world; }
+
+  // ---------------------------------------------------------------- setup
+  void validate_and_size() {
+    const snn_network_desc& n = net;
+    if (n.input <= 0) fail(SNN_ERR_SPEC, "network: input shape not declared");
+    if (n.n_hidden < 1 || n.n_hidden > SNN_MAX_HIDDEN)
+      fail(SNN_ERR_UNSUPPORTED, "n_hidden=%d outside [1,%d]", n.n_hidden, SNN_MAX_HIDDEN);
+    if (n.classes < 1 || n.classes > kMaxClasses)
+      fail(SNN_ERR_UNSUPPORTED, "classes=%d outside [1,%d]", n.classes, kMaxClasses);
+    for (int l = 0; l < n.n_hidden; ++l)
+      if (n.hidden[l] < 1) fail(SNN_ERR_SPEC, "layer %d: zero width", 2 * l);
+    if (!(n.threshold > 0.0f)) fail(SNN_ERR_UNSUPPORTED, "LIF threshold must be > 0");
+    if (n.activation < 0 || n.activation > 4) fail(SNN_ERR_ARGUMENT, "unknown activation");
+    if (n.activation != SNN_ACT_CUSTOM && !(n.slope > 0.0f))
+      fail(SNN_ERR_ARGUMENT, "activation slope must be positive");
+    if (n.activation == SNN_ACT_BOXCAR && !(n.aux > 0.0f))
+      fail(SNN_ERR_ARGUMENT, "boxcar: width and height must be positive");
+    if (cfg.batch_size < 1) fail(SNN_ERR_ARGUMENT, "train: batch size 0");
+    if (cfg.time_steps < 1) fail(SNN_ERR_ARGUMENT, "apply: zero timesteps");
+    if (cfg.unroll < 1) fail(SNN_ERR_ARGUMENT, "apply: unroll must be >= 1");
+    B = cfg.batch_size;
+    T = cfg.time_steps;
+    TT = T <= 64 ? 64 : 128;
+    NT = (T + TT - 1) / TT;
+    T_pad = NT * TT;
+    IN = n.input;
+    IN_pad = rup(IN, 64);
+    L = n.n_hidden;
+    C = n.classes;
+    for (int l = 0; l < L; ++l) {
+      H[l] = n.hidden[l];
+      H_pad[l] = rup(H[l], 128);
+    }
+    for (int j = 0; j <= L; ++j) {
+      K[j] = j == 0 ? IN : H[j - 1];
+      K_pad[j] = j == 0 ? IN_pad : H_pad[j - 1];
+      N[j] = j < L ? H[j] : C;
+      N_pad[j] = j < L ? H_pad[j] : 64;
+      M_pad_w[j] = rup(K[j], 128);
+      n_tile_w[j] = j < L ? 128 : 64;
+    }
+    const size_t ro_smem = (size_t(H[L - 1]) * C + size_t(T) * C) * sizeof(float);
+    if (ro_smem > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "readout working set too large");
+    // split-K so that each Linear's wgrad launch fills the chip ~2x
+    for (int j = 0; j <= L; ++j) {
+      const int tiles = (M_pad_w[j] / 128) * (N_pad[j] / n_tile_w[j]);
+      int s = std::max(1, 296 / std::max(1, tiles));
+      s = std::min(s, B);
+      splits_w[j] = s;
+    }
+    // parameter entries (network.hpp:210-226 order)
+    entries.clear();
+    size_t off = 0;
+    for (int j = 0; j <= L; ++j) {
+      const int lin = 2 * j, cell = 2 * j + 1;
+      entries.push_back({"l" + std::to_string(lin) + ".w", kEntryW, j, K[j], N[j], off,
+                         size_t(K[j]) * N[j]});
+      off += size_t(K[j]) * N[j];
+      if (n.bias) {
+        entries.push_back({"l" + std::to_string(lin) + ".b", kEntryB, j, 1, N[j], off, size_t(N[j])});
+        off += N[j];
+      }
+      entries.push_back({"l" + std::to_string(cell) + ".beta", kEntryBeta, j, 1, N[j], off,
+                         size_t(N[j])});
+      off += N[j];
+    }
+    n_params = off;
+  }
+
+  void allocate() {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    params.alloc(n_params);
+    m.alloc(n_params);
+    v.alloc(n_params);
+    comm.alloc(n_params + 2);
+    step.alloc(1);
+    grow_bc(1 << 16);
+    for (int j = 0; j < L; ++j) {
+      wt[j].alloc(size_t(3) * N_pad[j] * K_pad[j]);
+      if (j >= 1) wb[j].alloc(size_t(3) * K_pad[j] * N_pad[j]);
+    }
+    const size_t rows = size_t(B) * T_pad;
+    for (int l = 0; l < L; ++l) {
+      V[l].alloc(rows * H_pad[l], false);
+      s_np[l].alloc(rows * (H_pad[l] / 32));
+      s_tp[l].alloc(size_t(H_pad[l]) * (rows / 32));
+    }
+    for (int j = 0; j <= L; ++j) {
+      di[j].alloc(size_t(3) * rows * N_pad[j]);  // zero: padded rows/cols stay zero
+      dbeta[j].alloc(size_t(B) * N[j]);
+      if (net.bias) dbias[j].alloc(size_t(B) * N[j]);
+      partial[j].alloc(size_t(splits_w[j]) * M_pad_w[j] * N_pad[j], false);
+    }
+    d3.alloc(rows * C);
+    loss_b.alloc(B);
+    correct_b.alloc(B);
+    result_loss.alloc(1);
+    result_acc.alloc(1);
+    rows_cur.alloc(B);
+    CK(cudaMallocHost(&h_loss, sizeof(float)));
+    CK(cudaMallocHost(&h_acc, sizeof(double)));
+    CK(cudaMallocHost(&h_rows, sizeof(uint32_t) * B));
+    // tensor maps
+    for (int j = 0; j < L; ++j) {
+      tm_wt[j] = make_map(wt[j].p, uint64_t(3) * N_pad[j], K_pad[j], 128);
+      if (j >= 1) tm_wb[j] = make_map(wb[j].p, uint64_t(3) * K_pad[j], N_pad[j], 128);
+    }
+    for (int j = 0; j <= L; ++j) {
+      tm_di_k[j] = make_map(di[j].p, uint64_t(3) * rows, N_pad[j], TT);
+      tm_di_w[j] = make_map(di[j].p, uint64_t(3) * rows, N_pad[j], 64);
+    }
+    CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(fwd_smem_bytes(TT))));
+    CK(cudaFuncSetAttribute(k_lif_bwd_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(bwd_smem_bytes(TT))));
+    CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(wg_smem_bytes(128))));
+    CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(200 * 1024)));
+  }
+
+  void grow_bc(size_t steps) {
+    if (steps <= bc_steps) return;
+    std::vector<float> h(2 * steps);
+    const float b1 = cfg.beta1, b2 = cfg.beta2;
+    for (size_t s = 0; s < steps; ++s) {
+      // optimize.hpp:96-97: bc = T(1) - std::pow(beta, T(step)) in float
+      h[2 * s] = 1.0f - std::pow(b1, float(s + 1));
+      h[2 * s + 1] = 1.0f - std::pow(b2, float(s + 1));
+    }
+    DevBuf<float> nb;
+    nb.alloc(2 * steps, false);
+    CK(cudaMemcpy(nb.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    std::swap(bc.p, nb.p);
+    std::swap(bc.n, nb.n);
+    bc_steps = steps;
+    clear_graphs();
+  }
+
+  void ensure_bc_capacity() {
+    int64_t s = 0;
+    CK(cudaMemcpy(&s, step.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (size_t(s) + 2 > bc_steps) grow_bc(std::max(bc_steps * 2, size_t(s) + 2));
+  }
+
+  // ---------------------------------------------------------- parameters
+  void init_params_host(uint64_t key) {
+    // network.hpp:231-286: layer i key rng.child(i); W ~ TN(child(0)); beta ~ TN(child(2))
+    std::vector<float> h(n_params, 0.0f);
+    for (const auto& e : entries) {
+      if (e.kind == kEntryW) {
+        const uint64_t lk = hostrng::child(key, uint64_t(2 * e.layer));
+        const float sd = 1.0f / std::sqrt(float(e.rows));
+        hostrng::truncated_normal(hostrng::child(lk, 0), e.size, 0.0f, sd, h.data() + e.offset);
+      } else if (e.kind == kEntryBeta) {
+        const uint64_t lk = hostrng::child(key, uint64_t(2 * e.layer + 1));
+        hostrng::truncated_normal(hostrng::child(lk, 2), e.size, 0.5f, 0.25f, h.data() + e.offset);
+      }
+    }
+    upload_params(h.data());
+  }
+
+  void upload_params(const float* h) {
+    CK(cudaMemcpyAsync(params.p, h, n_params * sizeof(float), cudaMemcpyHostToDevice, stream));
+    refresh_planes();
+  }
+
+  void fill_entries(Entry* out, int* n_out) const {
+    int i = 0;
+    for (const auto& e : entries) {
+      out[i].kind = e.kind;
+      out[i].layer = e.layer;
+      out[i].rows = e.rows;
+      out[i].cols = e.cols;
+      out[i].offset = int64_t(e.offset);
+      ++i;
+    }
+    *n_out = i;
+  }
+
+  AdamArgs adam_args(int update) {
+    AdamArgs a{};
+    fill_entries(a.entries, &a.n_entries);
+    a.n_params = int64_t(n_params);
+    for (int j = 0; j <= L; ++j) {
+      a.planes[j].wt = j < L ? wt[j].p : nullptr;
+      a.planes[j].wb = (j >= 1 && j < L) ? wb[j].p : nullptr;
+      a.planes[j].K_pad = K_pad[j];
+      a.planes[j].N_pad = N_pad[j];
+    }
+    a.params = params.p;
+    a.m = m.p;
+    a.v = v.p;
+    a.grads = comm.p;
+    a.bc = bc.p;
+    a.step = step.p;
+    a.lr = cfg.lr;
+    a.b1 = cfg.beta1;
+    a.b2 = cfg.beta2;
+    a.eps = cfg.eps;
+    a.omb1 = 1.0f - cfg.beta1;
+    a.omb2 = 1.0f - cfg.beta2;
+    a.update = update;
+    return a;
+  }
+
+  void refresh_planes() {
+    AdamArgs a = adam_args(0);
+    const int threads = 256;
+    k_adam<<<unsigned((n_params + threads - 1) / threads), threads, 0, stream>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // ---------------------------------------------------------------- data
+  void stage(Dataset& ds, const uint8_t* packed, size_t n, const int64_t* labels) {
+    const int tp8 = (T + 7) / 8;
+    const int tp8_pad = T_pad / 8;
+    for (size_t i = 0; i < n; ++i)
+      if (labels[i] < 0 || labels[i] >= C)
+        fail(SNN_ERR_ARGUMENT, "target %lld outside [0,%d)", (long long)labels[i], C);
+    std::vector<uint8_t> h(n * size_t(tp8_pad) * IN_pad, 0);
+    for (size_t i = 0; i < n; ++i)
+      for (int g = 0; g < tp8; ++g)
+        std::memcpy(&h[(i * tp8_pad + g) * IN_pad], packed + (i * tp8 + g) * size_t(IN), IN);
+    std::vector<int32_t> lab(n);
+    for (size_t i = 0; i < n; ++i) lab[i] = int32_t(labels[i]);
+    if (ds.n != n) {
+      ds.x.alloc(h.size(), false);
+      ds.labels.alloc(n, false);
+      ds.n = n;
+      clear_graphs();
+    }
+    CK(cudaMemcpyAsync(ds.x.p, h.data(), h.size(), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(ds.labels.p, lab.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // ---------------------------------------------------------------- step
+  int launches_per_step() const { return 3 * L + 6; }
+
+  void enqueue_body(const Dataset& ds, int update) {
+    const size_t rows = size_t(B) * T_pad;
+    // forward
+    for (int l = 0; l < L; ++l) {
+      FwdArgs f{};
+      f.x = ds.x.p;
+      f.rows = rows_cur.p;
+      f.s_in = l > 0 ? s_np[l - 1].p : nullptr;
+      f.beta = params.p + entry_of(kEntryBeta, l).offset;
+      f.bias = net.bias ? params.p + entry_of(kEntryB, l).offset : nullptr;
+      f.v_out = V[l].p;
+      f.s_np = s_np[l].p;
+      f.s_tp = s_tp[l].p;
+      f.dbg_i = debug ? dbg_i[l].p : nullptr;
+      f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
+      f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
+      f.theta = net.threshold;
+      k_lif_fwd<<<dim3(B, H_pad[l] / 128), kFwdThreads, fwd_smem_bytes(TT), stream>>>(tm_wt[l], f);
+    }
+    // readout + loss + LI backward
+    {
+      ReadoutArgs r{};
+      r.s_in = s_np[L - 1].p;
+      r.rows = rows_cur.p;
+      r.labels = ds.labels.p;
+      r.w = params.p + entry_of(kEntryW, L).offset;
+      r.bias = net.bias ? params.p + entry_of(kEntryB, L).offset : nullptr;
+      r.beta = params.p + entry_of(kEntryBeta, L).offset;
+      r.d3 = d3.p;
+      r.d3_planes = di[L].p;
+      r.loss_b = loss_b.p;
+      r.correct_b = correct_b.p;
+      r.dbeta_part = dbeta[L].p;
+      r.dbias_part = net.bias ? dbias[L].p : nullptr;
+      r.dbg_trace = debug ? dbg_trace.p : nullptr;
+      r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
+      r.inv_b = 1.0f / float(B_global());
+      const size_t smem = (size_t(H[L - 1]) * C + size_t(T) * C) * sizeof(float);
+      k_readout<<<B, 128, smem, stream>>>(r);
+    }
+    // hidden backward, top-down
+    for (int l = L - 1; l >= 0; --l) {
+      BwdArgs bw{};
+      bw.v_in = V[l].p;
+      bw.beta = params.p + entry_of(kEntryBeta, l).offset;
+      bw.d3 = d3.p;
+      bw.w3 = params.p + entry_of(kEntryW, L).offset;
+      bw.di_planes = di[l].p;
+      bw.dbeta_part = dbeta[l].p;
+      bw.dbias_part = net.bias ? dbias[l].p : nullptr;
+      bw.dbg_ds = debug ? dbg_ds[l].p : nullptr;
+      bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
+      bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.C = C; bw.act = net.activation;
+      bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
+      if (l == L - 1) {
+        k_lif_bwd_ro<<<dim3(B, H_pad[l] / 128), 128, 0, stream>>>(bw);
+      } else {
+        k_lif_bwd_gemm<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT), stream>>>(
+            tm_wb[l + 1], tm_di_k[l + 1], bw);
+      }
+    }
+    // weight gradients
+    for (int j = 0; j <= L; ++j) {
+      WgradArgs w{};
+      w.x = ds.x.p;
+      w.rows = rows_cur.p;
+      w.s_tp = j > 0 ? s_tp[j - 1].p : nullptr;
+      w.partial = partial[j].p;
+      w.kind = j == 0 ? 0 : 1;
+      w.B = B; w.T_pad = T_pad; w.M_pad = M_pad_w[j]; w.N_pad = N_pad[j];
+      w.n_tile = n_tile_w[j]; w.splits = splits_w[j]; w.x_row_stride = IN_pad;
+      k_wgrad<<<dim3(M_pad_w[j] / 128, N_pad[j] / n_tile_w[j], splits_w[j]), kWgThreads,
+                wg_smem_bytes(n_tile_w[j]), stream>>>(tm_di_w[j], w);
+    }
+    (void)rows;
+    // gradient assembly
+    {
+      ReduceArgs r{};
+      fill_entries(r.entries, &r.n_entries);
+      r.n_params = int64_t(n_params);
+      for (int j = 0; j <= L; ++j) {
+        r.partial[j] = partial[j].p;
+        r.M_pad[j] = M_pad_w[j];
+        r.N_pad[j] = N_pad[j];
+        r.splits[j] = splits_w[j];
+        r.dbeta_part[j] = dbeta[j].p;
+        r.dbias_part[j] = net.bias ? dbias[j].p : nullptr;
+      }
+      r.params = params.p;
+      r.grads = comm.p;
+      r.B = B;
+      k_reduce<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(r);
+    }
+    k_loss_partial<<<1, 32, 0, stream>>>(loss_b.p, correct_b.p, B, comm.p + n_params);
+    if (world > 1) {
+      const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2, /*ncclFloat32*/ 7,
+                                      /*ncclSum*/ 0, comm_handle, stream);
+      if (rc != 0) fail(SNN_ERR_CUDA, "ncclAllReduce failed (%d)", rc);
+    }
+    if (update) {
+      AdamArgs a = adam_args(1);
+      k_adam<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(a);
+    }
+    k_result<<<1, 32, 0, stream>>>(comm.p + n_params, B_global(), step.p, update, result_loss.p,
+                                   result_acc.p);
+  }
+
+  const EntryHost& entry_of(int kind, int layer) const {
+    for (const auto& e : entries)
+      if (e.kind == kind && e.layer == layer) return e;
+    fail(SNN_ERR_ARGUMENT, "no entry kind %d layer %d", kind, layer);
+  }
+
+  cudaGraphExec_t graph_for(const Dataset& ds, int update) {
+    auto key = std::make_pair(static_cast<const void*>(ds.x.p), update);
+    auto it = graphs.find(key);
+    if (it != graphs.end()) return it->second;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_body(ds, update);
+    } catch (...) {
+      cudaStreamEndCapture(stream, &g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(stream, &g));
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    CK(cudaGraphDestroy(g));
+    graphs[key] = ex;
+    return ex;
+  }
+
+  void launch(const Dataset& ds, int update) {
+    if (ds.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    if (update) ensure_bc_capacity();
+    CK(cudaGraphLaunch(graph_for(ds, update), stream));
+  }
+
+  void set_rows_host(const uint32_t* rows, const Dataset& ds) {
+    for (int i = 0; i < B; ++i) {
+      if (rows[i] >= ds.n) fail(SNN_ERR_ARGUMENT, "row %u outside dataset of %zu", rows[i], ds.n);
+      h_rows[i] = rows[i];
+    }
+    CK(cudaMemcpyAsync(rows_cur.p, h_rows, sizeof(uint32_t) * B, cudaMemcpyHostToDevice, stream));
+  }
+
+  void read_result(float* loss, double* acc) {
+    CK(cudaMemcpyAsync(h_loss, result_loss.p, sizeof(float), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h_acc, result_acc.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (loss) *loss = *h_loss;
+    if (acc) *acc = *h_acc;
+  }
+
+  void step_rows(const uint32_t* rows, const Dataset& ds, int update, float* loss, double* acc) {
+    set_rows_host(rows, ds);
+    launch(ds, update);
+    read_result(loss, acc);
+  }
+
+  void set_debug(bool on) {
+    debug = on;
+    const size_t rows = size_t(B) * T_pad;
+    for (int l = 0; l < L; ++l) {
+      if (on) {
+        dbg_i[l].alloc(rows * H_pad[l]);
+        dbg_ds[l].alloc(rows * H_pad[l]);
+      } else {
+        dbg_i[l].free();
+        dbg_ds[l].free();
+      }
+    }
+    if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
+    clear_graphs();
+  }
+};
+
+// =================================================================== C ABI
+namespace {
+
+template <typename F>
+snn_status guard(snn_engine* e, F&& f) {
+  try {
+    if (e) CK(cudaSetDevice(e->device));
+    f();
+    return SNN_OK;
+  } catch (const SnnError& err) {
+    if (e) e->err = err.msg; else g_create_error = err.msg;
+    return err.code;
+  } catch (const std::exception& ex) {
+    if (e) e->err = ex.what(); else g_create_error = ex.what();
+    return SNN_ERR_CUDA;
+  }
+}
+
+void check_n(const snn_engine* e, size_t n) {
+  if (n != e->n_params)
+    fail(SNN_ERR_SHAPE, "expected %zu parameter scalars, got %zu", e->n_params, n);
+}
+
+}  // namespace
+
+extern "C" {
+
+int snn_abi_version(void) { return SNN_ABI_VERSION; }
+
+const char* snn_last_error(const snn_engine* e) {
+  return e ? e->err.c_str() : g_create_error.c_str();
+}
+
+snn_status snn_engine_create(const snn_network_desc* net, const snn_train_config* cfg, int device,
+                             snn_engine** out) {
+  if (!net || !cfg || !out) {
+    g_create_error = "null argument";
+    return SNN_ERR_ARGUMENT;
+  }
+  *out = nullptr;
+  auto e = std::make_unique<snn_engine>();
+  e->net = *net;
+  e->cfg = *cfg;
+  e->device = device;
+  const snn_status st = guard(nullptr, [&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device)
+      fail(SNN_ERR_CUDA, "no CUDA device %d (this engine has no CPU fallback)", device);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(SNN_ERR_CUDA, "device %d is sm_%d%d; this engine is built for sm_100a only", device,
+           prop.major, prop.minor);
+    e->validate_and_size();
+    e->allocate();
+    // train(spec, cfg, data): params from master.child(0) (optimize.hpp:246-254)
+    e->init_params_host(hostrng::child(hostrng::from_seed(cfg->seed), 0));
+  });
+  if (st != SNN_OK) return st;
+  *out = e.release();
+  return SNN_OK;
+}
+
+void snn_engine_destroy(snn_engine* e) { delete e; }
+
+snn_status snn_param_count(const snn_engine* e, size_t* n) {
+  if (!e || !n) return SNN_ERR_ARGUMENT;
+  *n = e->n_params;
+  return SNN_OK;
+}
+
+snn_status snn_entry_count(const snn_engine* e, int32_t* n) {
+  if (!e || !n) return SNN_ERR_ARGUMENT;
+  *n = int32_t(e->entries.size());
+  return SNN_OK;
+}
+
+snn_status snn_entry_info(const snn_engine* e, int32_t i, char name[16], size_t* offset,
+                          size_t* size, int32_t* trainable) {
+  if (!e || i < 0 || size_t(i) >= e->entries.size()) return SNN_ERR_ARGUMENT;
+  const auto& en = e->entries[size_t(i)];
+  if (name) std::snprintf(name, 16, "%s", en.name.c_str());
+  if (offset) *offset = en.offset;
+  if (size) *size = en.size;
+  if (trainable) *trainable = 1;
+  return SNN_OK;
+}
+
+snn_status snn_set_params(snn_engine* e, const float* host, size_t n) {
+  if (!e || !host) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    check_n(e, n);
+    e->upload_params(host);
+  });
+}
+
+snn_status snn_get_params(snn_engine* e, float* host, size_t n) {
+  if (!e || !host) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    check_n(e, n);
+    CK(cudaMemcpyAsync(host, e->params.p, n * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+snn_status snn_init_params(snn_engine* e, uint64_t key_word) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->init_params_host(key_word); });
+}
+
+snn_status snn_get_opt_state(snn_engine* e, float* m, float* v, uint64_t* step, size_t n) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    check_n(e, n);
+    if (m) CK(cudaMemcpyAsync(m, e->m.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+    if (v) CK(cudaMemcpyAsync(v, e->v.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+    int64_t s = 0;
+    CK(cudaMemcpyAsync(&s, e->step.p, 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    if (step) *step = uint64_t(s);
+  });
+}
+
+snn_status snn_set_opt_state(snn_engine* e, const float* m, const float* v, uint64_t step,
+                             size_t n) {
+  if (!e || !m || !v) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    check_n(e, n);
+    const int64_t s = int64_t(step);
+    CK(cudaMemcpyAsync(e->m.p, m, n * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(e->v.p, v, n * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(e->step.p, &s, 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+snn_status snn_get_grads(snn_engine* e, float* host, size_t n) {
+  if (!e || !host) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    check_n(e, n);
+    CK(cudaMemcpyAsync(host, e->comm.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+snn_status snn_stage_dataset(snn_engine* e, const uint8_t* packed, size_t n,
+                             const int64_t* labels) {
+  if (!e || !packed || !labels || n == 0) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->stage(e->data, packed, n, labels); });
+}
+
+snn_status snn_train_step(snn_engine* e, const uint32_t* rows, float* loss, double* accuracy) {
+  if (!e || !rows) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->step_rows(rows, e->data, 1, loss, accuracy); });
+}
+
+snn_status snn_forward_backward(snn_engine* e, const uint32_t* rows, float* loss,
+                                double* accuracy) {
+  if (!e || !rows) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->step_rows(rows, e->data, 0, loss, accuracy); });
+}
+
+snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
+                                 const int64_t* targets, float* loss, double* accuracy) {
+  if (!e || !packed_batch || !targets) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    e->stage(e->scratch, packed_batch, size_t(e->B), targets);
+    std::vector<uint32_t> rows(size_t(e->B));
+    for (int i = 0; i < e->B; ++i) rows[size_t(i)] = uint32_t(i);
+    e->step_rows(rows.data(), e->scratch, 1, loss, accuracy);
+  });
+}
+
+snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    const size_t n = e->data.n;
+    if (n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    const size_t gb = size_t(e->B_global());
+    if (gb > n) fail(SNN_ERR_ARGUMENT, "shuffle: batch size %zu for %zu examples", gb, n);
+    const uint64_t master = hostrng::from_seed(e->cfg.seed);
+    const size_t nb = n / gb;
+    for (size_t ep = 0; ep < epochs; ++ep) {
+      const uint64_t ek = hostrng::child(master, 1 + ep);
+      const std::vector<uint32_t> perm = hostrng::permutation(hostrng::child(ek, 0), n);
+      double ls = 0, as = 0;
+      for (size_t bi = 0; bi < nb; ++bi) {
+        float l;
+        double a;
+        e->step_rows(perm.data() + bi * gb + size_t(e->rank) * e->B, e->data, 1, &l, &a);
+        ls += double(l);
+        as += a;
+      }
+      if (metrics) {
+        metrics[2 * ep] = ls / double(nb ? nb : 1);
+        metrics[2 * ep + 1] = as / double(nb ? nb : 1);
+      }
+    }
+  });
+}
+
+snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_steps) {
+  if (!e || !rows || n_steps == 0) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    for (size_t i = 0; i < n_steps * size_t(e->B); ++i)
+      if (rows[i] >= e->data.n) fail(SNN_ERR_ARGUMENT, "schedule row outside dataset");
+    e->sched.alloc(n_steps * size_t(e->B), false);
+    e->sched_steps = n_steps;
+    CK(cudaMemcpy(e->sched.p, rows, n_steps * e->B * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    e->ensure_bc_capacity();
+    e->grow_bc(e->bc_steps + 0);
+  });
+}
+
+snn_status snn_enqueue_step(snn_engine* e, size_t slot) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (slot >= e->sched_steps) fail(SNN_ERR_ARGUMENT, "schedule slot %zu out of range", slot);
+    CK(cudaMemcpyAsync(e->rows_cur.p, e->sched.p + slot * size_t(e->B), sizeof(uint32_t) * e->B,
+                       cudaMemcpyDeviceToDevice, e->stream));
+    CK(cudaGraphLaunch(e->graph_for(e->data, 1), e->stream));
+  });
+}
+
+snn_status snn_sync(snn_engine* e) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { CK(cudaStreamSynchronize(e->stream)); });
+}
+
+snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->read_result(loss, accuracy); });
+}
+
+void* snn_stream(snn_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
+int32_t snn_launches_per_step(const snn_engine* e) { return e ? e->launches_per_step() : 0; }
+
+snn_status snn_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return SNN_ERR_ARGUMENT;
+  NcclApi& api = nccl();
+  if (!api.ok) {
+    g_create_error = "libnccl.so.2 not loadable";
+    return SNN_ERR_CUDA;
+  }
+  UniqueId u;
+  const int rc = api.GetUniqueId(&u);
+  if (rc != 0) {
+    g_create_error = "ncclGetUniqueId failed";
+    return SNN_ERR_CUDA;
+  }
+  std::memcpy(id, u.internal, 128);
+  return SNN_OK;
+}
+
+snn_status snn_comm_init(snn_engine* e, const uint8_t id[128], int32_t rank, int32_t world) {
+  if (!e || !id || world < 1 || rank < 0 || rank >= world) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (world == 1) {
+      e->world = 1;
+      e->rank = 0;
+      e->clear_graphs();
+      return;
+    }
+    NcclApi& api = nccl();
+    if (!api.ok) fail(SNN_ERR_CUDA, "libnccl.so.2 not loadable");
+    UniqueId u;
+    std::memcpy(u.internal, id, 128);
+    void* comm = nullptr;
+    const int rc = reinterpret_cast<InitRankFn>(api.CommInitRank)(&comm, world, u, rank);
+    if (rc != 0) fail(SNN_ERR_CUDA, "ncclCommInitRank failed (%d)", rc);
+    e->comm_handle = comm;
+    e->rank = rank;
+    e->world = world;
+    e->clear_graphs();
+  });
+}
+
+snn_status snn_debug_enable(snn_engine* e, int32_t on) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->set_debug(on != 0); });
+}
+
+snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* host, size_t bytes) {
+  if (!e || !host) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
+    const int B = e->B, T = e->T, T_pad = e->T_pad;
+    if (which == 3) {
+      const size_t need = size_t(B) * T * e->C * sizeof(float);
+      if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
+      CK(cudaMemcpy(host, e->dbg_trace.p, need, cudaMemcpyDeviceToHost));
+      return;
+    }
+    if (layer < 0 || layer >= e->L) fail(SNN_ERR_ARGUMENT, "layer %d", layer);
+    const int H = e->H[layer], Hp = e->H_pad[layer];
+    const size_t elem = which == 2 ? 1 : 4;
+    const size_t need = size_t(B) * T * H * elem;
+    if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
+    const size_t rows = size_t(B) * T_pad;
+    if (which == 0 || which == 1 || which == 4) {
+      std::vector<float> buf(rows * Hp);
+      const float* src = which == 0 ? e->dbg_i[layer].p : (which == 1 ? e->V[layer].p : e->dbg_ds[layer].p);
+      CK(cudaMemcpy(buf.data(), src, buf.size() * 4, cudaMemcpyDeviceToHost));
+      float* out = static_cast<float*>(host);
+      for (int b = 0; b < B; ++b)
+        for (int t = 0; t < T; ++t)
+          std::memcpy(out + (size_t(b) * T + t) * H, buf.data() + (size_t(b) * T_pad + t) * Hp,
+                      size_t(H) * 4);
+    } else if (which == 2) {
+      const int hw = Hp / 32;
+      std::vector<uint32_t> buf(rows * hw);
+      CK(cudaMemcpy(buf.data(), e->s_np[layer].p, buf.size() * 4, cudaMemcpyDeviceToHost));
+      uint8_t* out = static_cast<uint8_t*>(host);
+      for (int b = 0; b < B; ++b)
+        for (int t = 0; t < T; ++t)
+          for (int n = 0; n < H; ++n)
+            out[(size_t(b) * T + t) * H + n] =
+                (buf[(size_t(b) * T_pad + t) * hw + n / 32] >> (n % 32)) & 1u;
+    } else {
+      fail(SNN_ERR_ARGUMENT, "unknown debug tensor %d", which);
+    }
+  });
+}
+
+}  // extern "C"

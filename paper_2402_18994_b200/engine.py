@@ -1,0 +1,408 @@
+"""Python mirror of the reference's training-step API over the engine's C ABI.
+
+Names follow spiketrain (network.hpp, optimize.hpp, surrogate.hpp, errors.hpp):
+NetworkSpec / LinearLayer / LIFLayer / LILayer / ActivationDesc / TrainConfig,
+train_step, train; errors are raised as the reference's exception classes.
+Every call goes through include/snn_engine.h into libsnn_b200.so (sm_100a).
+There is no CPU fallback: without the library or a B200 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from .build import LIB, build, needs_build
+
+# ----------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """spiketrain::Error (errors.hpp:9-11)."""
+
+
+class ShapeError(Error): ...
+class ArgumentError(Error): ...
+class ContractError(Error): ...
+class StateError(Error): ...
+class FormatError(Error): ...
+class IoError(Error): ...
+class SpecError(Error): ...
+class ConfigError(Error): ...
+class UnsupportedError(Error): ...
+class DeviceError(Error):
+    """No usable B200 / CUDA failure (the engine never falls back to the CPU)."""
+
+
+_STATUS = {1: ShapeError, 2: ArgumentError, 3: ContractError, 4: StateError, 5: FormatError,
+           6: IoError, 7: SpecError, 8: ConfigError, 9: UnsupportedError, 10: DeviceError}
+
+# ------------------------------------------------------------- spec types
+ACTIVATIONS = {"custom": 0, "superspike": 1, "triangular": 2, "arctan": 3, "boxcar": 4}
+
+
+@dataclass
+class ActivationDesc:
+    """surrogate.hpp:134-138; defaults per default_activation_desc (:150-157)."""
+    name: str = "superspike"
+    slope: float = 25.0
+    aux: float = 0.0
+
+
+def default_activation_desc(name: str) -> ActivationDesc:
+    table = {"custom": (0.0, 0.0), "superspike": (25.0, 0.0), "triangular": (0.5, 0.0),
+             "arctan": (2.0, 0.0), "boxcar": (2.0, 0.5)}
+    if name not in table:
+        raise ArgumentError(f"unknown activation: {name}")
+    return ActivationDesc(name, *table[name])
+
+
+@dataclass
+class LinearLayer:
+    out: int
+    bias: bool = True
+
+
+@dataclass
+class LIFLayer:
+    activation: ActivationDesc = field(default_factory=ActivationDesc)
+    threshold: float = 1.0
+    beta_mode: str = "per_neuron"
+
+
+@dataclass
+class LILayer:
+    beta_mode: str = "per_neuron"
+
+
+@dataclass
+class NetworkSpec:
+    input_shape: Sequence[int]
+    layers: list
+
+
+@dataclass
+class TrainConfig:
+    """optimize.hpp:116-133 (the fields the training step consumes)."""
+    epochs: int = 100
+    batch_size: int = 64
+    lr: float = 1e-3
+    seed: int = 0
+    unroll: int = 32
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+class _NetDesc(C.Structure):
+    _fields_ = [("input", C.c_int32), ("n_hidden", C.c_int32), ("hidden", C.c_int32 * 8),
+                ("classes", C.c_int32), ("bias", C.c_int32), ("threshold", C.c_float),
+                ("activation", C.c_int32), ("slope", C.c_float), ("aux", C.c_float)]
+
+
+class _TrainCfg(C.Structure):
+    _fields_ = [("batch_size", C.c_int32), ("time_steps", C.c_int32), ("lr", C.c_float),
+                ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("seed", C.c_uint64), ("unroll", C.c_int32)]
+
+
+def normalize(spec: NetworkSpec) -> dict:
+    """Map a NetworkSpec onto the engine's feed-forward family, validating like
+    normalize() (network.hpp:125-157).  Supported: [Linear, LIF]*k, Linear, LI."""
+    if not spec.input_shape:
+        raise SpecError("network: input shape not declared")
+    if not spec.layers:
+        raise SpecError("network: no layers")
+    last = spec.layers[-1]
+    if not isinstance(last, (LIFLayer, LILayer)):
+        raise SpecError("network must end in a lif or li readout")
+    inp = int(np.prod(spec.input_shape))
+    layers = list(spec.layers)
+    if len(layers) < 4 or len(layers) % 2:
+        raise UnsupportedError("engine supports [Linear, LIF]*k + Linear + LI")
+    hidden, act, thr, bias = [], None, None, None
+    for i in range(0, len(layers) - 2, 2):
+        lin, cell = layers[i], layers[i + 1]
+        if not isinstance(lin, LinearLayer) or not isinstance(cell, LIFLayer):
+            raise UnsupportedError(f"layer {i}: expected Linear + LIF")
+        if cell.beta_mode != "per_neuron":
+            raise UnsupportedError("only BetaMode::PerNeuron")
+        if act is not None and (cell.activation != act or cell.threshold != thr):
+            raise UnsupportedError("all LIF layers must share activation and threshold")
+        if bias is not None and lin.bias != bias:
+            raise UnsupportedError("all Linear layers must share the bias flag")
+        act, thr, bias = cell.activation, cell.threshold, lin.bias
+        hidden.append(int(lin.out))
+    lin, cell = layers[-2], layers[-1]
+    if not isinstance(lin, LinearLayer) or not isinstance(cell, LILayer):
+        raise UnsupportedError("readout must be Linear + LI")
+    if lin.bias != bias:
+        raise UnsupportedError("all Linear layers must share the bias flag")
+    if act.name not in ACTIVATIONS:
+        raise ArgumentError(f"unknown activation: {act.name}")
+    return dict(input=inp, hidden=hidden, classes=int(lin.out), bias=bool(bias),
+                threshold=float(thr), activation=act.name, slope=float(act.slope),
+                aux=float(act.aux))
+
+
+def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False) -> NetworkSpec:
+    """The BASELINE network: 700-H1-H2-20, LIF, arctan k=2, nobias."""
+    layers = []
+    for h in hidden:
+        layers += [LinearLayer(h, bias), LIFLayer(default_activation_desc(act))]
+    layers += [LinearLayer(classes, bias), LILayer()]
+    return NetworkSpec([inp], layers)
+
+
+# ---------------------------------------------------------------- library
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libsnn_b200.so (built in-tree).  Fails loudly if it cannot be built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if needs_build():
+        build()
+    if not os.path.exists(LIB):
+        raise DeviceError(f"{LIB} missing: the CUDA engine is required (no CPU fallback)")
+    L = C.CDLL(LIB, mode=C.RTLD_GLOBAL)
+    L.snn_last_error.restype = C.c_char_p
+    L.snn_last_error.argtypes = [C.c_void_p]
+    L.snn_stream.restype = C.c_void_p
+    L.snn_stream.argtypes = [C.c_void_p]
+    L.snn_launches_per_step.restype = C.c_int32
+    L.snn_launches_per_step.argtypes = [C.c_void_p]
+    for name in ("snn_engine_create", "snn_param_count", "snn_entry_count", "snn_entry_info",
+                 "snn_set_params", "snn_get_params", "snn_init_params", "snn_get_opt_state",
+                 "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
+                 "snn_train_step_packed", "snn_forward_backward", "snn_train_epochs",
+                 "snn_upload_schedule", "snn_enqueue_step", "snn_sync", "snn_read_result",
+                 "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch"):
+        getattr(L, name).restype = C.c_int
+    L.snn_engine_destroy.restype = None
+    L.snn_engine_destroy.argtypes = [C.c_void_p]
+    _lib = L
+    return L
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class Engine:
+    """One training state (TrainState, optimize.hpp:135-141) resident on one GPU."""
+
+    def __init__(self, spec: NetworkSpec, cfg: TrainConfig, time_steps: int, device: int = 0):
+        d = normalize(spec)
+        self.desc = d
+        self.spec, self.cfg, self.time_steps = spec, cfg, int(time_steps)
+        n = _NetDesc()
+        n.input = d["input"]
+        n.n_hidden = len(d["hidden"])
+        if n.n_hidden > 8:
+            raise UnsupportedError("at most 8 hidden layers")
+        for i, h in enumerate(d["hidden"]):
+            n.hidden[i] = h
+        n.classes = d["classes"]
+        n.bias = int(d["bias"])
+        n.threshold = d["threshold"]
+        n.activation = ACTIVATIONS[d["activation"]]
+        n.slope = d["slope"]
+        n.aux = d["aux"]
+        c = _TrainCfg()
+        c.batch_size = int(cfg.batch_size)
+        c.time_steps = int(time_steps)
+        c.lr = float(cfg.lr)
+        c.beta1, c.beta2, c.eps = float(cfg.beta1), float(cfg.beta2), float(cfg.eps)
+        c.seed = int(cfg.seed)
+        c.unroll = int(cfg.unroll)
+        self._L = lib()
+        h = C.c_void_p()
+        self._h = None
+        self._check(self._L.snn_engine_create(C.byref(n), C.byref(c), int(device), C.byref(h)),
+                    create=True)
+        self._h = h
+        cnt = C.c_size_t()
+        self._check(self._L.snn_param_count(self._h, C.byref(cnt)))
+        self.n_params = cnt.value
+        self.batch_size = int(cfg.batch_size)
+
+    # -------------------------------------------------------------- utils
+    def _check(self, rc: int, create: bool = False):
+        if rc == 0:
+            return
+        msg = self._L.snn_last_error(None if create else self._h)
+        msg = msg.decode() if msg else f"status {rc}"
+        raise _STATUS.get(rc, Error)(msg)
+
+    def close(self):
+        if self._h is not None:
+            self._L.snn_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---------------------------------------------------------- parameters
+    def entries(self):
+        cnt = C.c_int32()
+        self._check(self._L.snn_entry_count(self._h, C.byref(cnt)))
+        out = []
+        for i in range(cnt.value):
+            name = C.create_string_buffer(16)
+            off, size, tr = C.c_size_t(), C.c_size_t(), C.c_int32()
+            self._check(self._L.snn_entry_info(self._h, i, name, C.byref(off), C.byref(size),
+                                               C.byref(tr)))
+            out.append((name.value.decode(), off.value, size.value))
+        return out
+
+    def get_params(self) -> np.ndarray:
+        out = np.empty(self.n_params, np.float32)
+        self._check(self._L.snn_get_params(self._h, _p(out, C.c_float), C.c_size_t(out.size)))
+        return out
+
+    def set_params(self, params: np.ndarray):
+        p = np.ascontiguousarray(params, np.float32)
+        self._check(self._L.snn_set_params(self._h, _p(p, C.c_float), C.c_size_t(p.size)))
+
+    def init_params(self, key_word: int):
+        self._check(self._L.snn_init_params(self._h, C.c_uint64(key_word)))
+
+    def get_grads(self) -> np.ndarray:
+        out = np.empty(self.n_params, np.float32)
+        self._check(self._L.snn_get_grads(self._h, _p(out, C.c_float), C.c_size_t(out.size)))
+        return out
+
+    def get_opt_state(self):
+        m = np.empty(self.n_params, np.float32)
+        v = np.empty(self.n_params, np.float32)
+        st = C.c_uint64()
+        self._check(self._L.snn_get_opt_state(self._h, _p(m, C.c_float), _p(v, C.c_float),
+                                              C.byref(st), C.c_size_t(m.size)))
+        return m, v, st.value
+
+    def set_opt_state(self, m, v, step: int):
+        m = np.ascontiguousarray(m, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        self._check(self._L.snn_set_opt_state(self._h, _p(m, C.c_float), _p(v, C.c_float),
+                                              C.c_uint64(step), C.c_size_t(m.size)))
+
+    # ---------------------------------------------------------------- data
+    def stage_dataset(self, packed: np.ndarray, labels: np.ndarray):
+        packed = np.ascontiguousarray(packed, np.uint8)
+        labels = np.ascontiguousarray(labels, np.int64)
+        if packed.ndim != 3 or packed.shape[1] != (self.time_steps + 7) // 8:
+            raise FormatError(f"packed extent {packed.shape} inconsistent with T={self.time_steps}")
+        if packed.shape[0] != labels.shape[0]:
+            raise ArgumentError("label count mismatch")
+        self._check(self._L.snn_stage_dataset(self._h, _p(packed, C.c_uint8),
+                                              C.c_size_t(packed.shape[0]), _p(labels, C.c_int64)))
+        self.n_examples = packed.shape[0]
+
+    # ---------------------------------------------------------------- steps
+    def train_step(self, rows) -> tuple[float, float]:
+        r = np.ascontiguousarray(rows, np.uint32)
+        if r.size != self.batch_size:
+            raise ArgumentError(f"targets: {r.size} rows for batch {self.batch_size}")
+        loss, acc = C.c_float(), C.c_double()
+        self._check(self._L.snn_train_step(self._h, _p(r, C.c_uint32), C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
+
+    def forward_backward(self, rows) -> tuple[float, float]:
+        r = np.ascontiguousarray(rows, np.uint32)
+        if r.size != self.batch_size:
+            raise ArgumentError(f"targets: {r.size} rows for batch {self.batch_size}")
+        loss, acc = C.c_float(), C.c_double()
+        self._check(self._L.snn_forward_backward(self._h, _p(r, C.c_uint32), C.byref(loss),
+                                                 C.byref(acc)))
+        return loss.value, acc.value
+
+    def train_step_packed(self, packed_x: np.ndarray, targets) -> tuple[float, float]:
+        """train_step(st, packed_x, T, targets) (optimize.hpp:152-156)."""
+        packed_x = np.ascontiguousarray(packed_x, np.uint8)
+        t = np.ascontiguousarray(targets, np.int64)
+        if packed_x.shape[0] != self.batch_size or t.size != self.batch_size:
+            raise ArgumentError(f"targets: {t.size} labels for batch {packed_x.shape[0]}")
+        if packed_x.shape[1] != (self.time_steps + 7) // 8:
+            raise FormatError("unpack_time: packed extent inconsistent with T")
+        loss, acc = C.c_float(), C.c_double()
+        self._check(self._L.snn_train_step_packed(self._h, _p(packed_x, C.c_uint8),
+                                                  _p(t, C.c_int64), C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
+
+    def train_epochs(self, epochs: int) -> np.ndarray:
+        metrics = np.zeros((epochs, 2), np.float64)
+        self._check(self._L.snn_train_epochs(self._h, C.c_size_t(epochs), _p(metrics, C.c_double)))
+        return metrics
+
+    # ------------------------------------------------------------- async path
+    def upload_schedule(self, rows: np.ndarray):
+        r = np.ascontiguousarray(rows, np.uint32)
+        self._check(self._L.snn_upload_schedule(self._h, _p(r, C.c_uint32),
+                                                C.c_size_t(r.size // self.batch_size)))
+
+    def enqueue_step(self, slot: int):
+        self._check(self._L.snn_enqueue_step(self._h, C.c_size_t(slot)))
+
+    def sync(self):
+        self._check(self._L.snn_sync(self._h))
+
+    def read_result(self):
+        loss, acc = C.c_float(), C.c_double()
+        self._check(self._L.snn_read_result(self._h, C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
+
+    @property
+    def stream(self) -> int:
+        return int(self._L.snn_stream(self._h) or 0)
+
+    @property
+    def launches_per_step(self) -> int:
+        return int(self._L.snn_launches_per_step(self._h))
+
+    # ---------------------------------------------------------- multi-GPU
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        L = lib()
+        buf = (C.c_uint8 * 128)()
+        rc = L.snn_nccl_unique_id(buf)
+        if rc != 0:
+            raise DeviceError((L.snn_last_error(None) or b"").decode())
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, rank: int, world: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self._L.snn_comm_init(self._h, buf, int(rank), int(world)))
+
+    # ---------------------------------------------------------- diagnostics
+    def debug(self, on: bool = True):
+        self._check(self._L.snn_debug_enable(self._h, int(on)))
+
+    def fetch(self, which: str, layer: int = 0) -> np.ndarray:
+        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4}[which]
+        B, T = self.batch_size, self.time_steps
+        if which == "trace":
+            out = np.empty((B, T, self.desc["classes"]), np.float32)
+        else:
+            H = self.desc["hidden"][layer]
+            out = np.empty((B, T, H), np.uint8 if which == "spikes" else np.float32)
+        self._check(self._L.snn_debug_fetch(self._h, idx, int(layer),
+                                            out.ctypes.data_as(C.c_void_p), C.c_size_t(out.nbytes)))
+        return out
+
+
+def train_step(engine: Engine, packed_x, original_t: int, targets):
+    """Free-function form of optimize.hpp:152-156."""
+    if original_t != engine.time_steps:
+        raise FormatError(f"unpack_time: packed extent inconsistent with T={original_t}")
+    return engine.train_step_packed(packed_x, targets)
