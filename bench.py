@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py -- SNN train samples/s (fwd + bwd + Adam, SHD shape) on B200.
+
+Default: N=1, configuration C1 of BASELINE.json (700-128-128-20 LIF, T=128,
+batch 256, arctan surrogate, integral CE + Adam).  One "step" = one full
+train_step over one batch drawn from an HBM-resident synthetic dataset that
+is larger than L2 (16384 examples, 184 MB staged), fresh rows every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (data-parallel, weak scaling)
+
+Prints ONE JSON line on rank 0.  The `reference` arm times the reference's own
+CPU train_step (oracle/_ref, built from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SNN train samples/sec (fwd+bwd+Adam, SHD shape) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "samples/s"
+
+WORKLOADS = {
+    # name: input, hidden, classes, T, per-GPU batch, surrogate, dataset examples
+    "c1": dict(inp=700, hidden=(128, 128), classes=20, T=128, B=256, act="arctan", n_data=16384,
+               desc="SHD-shaped 700-128-128-20 LIF, T=128, batch 256/GPU, arctan k=2, "
+                    "integral-CE + Adam, nobias"),
+    "c3": dict(inp=700, hidden=(1024, 1024), classes=20, T=256, B=512, act="arctan", n_data=8192,
+               desc="wide 700-1024-1024-20 LIF, T=256, batch 512/GPU"),
+    "c5": dict(inp=700, hidden=(256, 256), classes=20, T=1000, B=512, act="arctan", n_data=2048,
+               desc="long-sequence 700-256-256-20 LIF, T=1000, batch 512/GPU"),
+}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        p = json.load(open(path))
+        return float(p["hbm_gbs"]), float(p["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ roofline
+def algorithmic(name: str, w: dict, n_params: int):
+    """(bound, work per launch) from SURVEY.md §8(d) per-unit figures."""
+    B, T, C = w["B"], w["T"], w["classes"]
+    dims = [w["inp"], *w["hidden"], C]
+    base, _, idx = name.partition("[")
+    l = int(idx.rstrip("]")) if idx else 0
+    if base == "lif_fwd":            # I = A W over all T: 2 B T K N flops
+        return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
+    if base == "wgrad":              # dW = A^T dI
+        return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
+    if base == "lif_bwd_gemm":       # dS = dI_next W_next^T
+        return "tensor", 2.0 * B * T * dims[l + 1] * dims[l + 2]
+    if base == "lif_bwd_ro":         # LIF bwd 12 B / neuron-step
+        return "hbm", 12.0 * B * T * dims[l + 1]
+    if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element
+        return "hbm", 8.0 * B * T * C
+    if base == "adam":               # 28 B / param
+        return "hbm", 28.0 * n_params
+    return "hbm", 0.0
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch for `kernel` from the committed ncu summary, if any."""
+    for fn in sorted(os.listdir(os.path.join(ROOT, "profiles")) if os.path.isdir(
+            os.path.join(ROOT, "profiles")) else [], reverse=True):
+        if fn.endswith("_ncu.json"):
+            try:
+                d = json.load(open(os.path.join(ROOT, "profiles", fn)))
+                if kernel in d.get("dram_bytes_per_launch", {}):
+                    return d["dram_bytes_per_launch"][kernel]
+            except Exception:
+                pass
+    return None
+
+
+# ------------------------------------------------------------ CPU baseline
+def _ref_worker(args):
+    which, n_examples, steps, warmup, seed, q = args
+    from oracle.pyoracle import Lib, Net, State
+    lib = Lib(which)
+    net = Net()
+    x, y = lib.synth_raster(20, n_examples, 128, 700, seed)
+    pk = lib.pack_time(x)
+    st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
+    for _ in range(warmup):
+        lib.train_step(net, st, pk, 128, y)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        lib.train_step(net, st, pk, 128, y)
+    q.put((n_examples * steps, time.perf_counter() - t0))
+
+
+def cpu_reference(steps: int, warmup: int, workers: int, per_step_budget_s: float):
+    """Reference CPU train_step on `workers` host cores (independent replicas).
+
+    Each step of each worker is a bounded sample of the C1 workload: b examples
+    (b sized so the whole run fits the budget), T=128, 700-128-128-20."""
+    from oracle.pyoracle import Lib, have_ref
+    which = "ref" if have_ref() else "orc"
+    kind = "reference" if which == "ref" else "port"
+    lib = Lib(which)
+    # calibrate the per-example cost on one core
+    from oracle.pyoracle import Net, State
+    net = Net()
+    x, y = lib.synth_raster(20, 8, 128, 700, 1)
+    pk = lib.pack_time(x)
+    st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
+    t0 = time.perf_counter()
+    lib.train_step(net, st, pk, 128, y)
+    per_ex = (time.perf_counter() - t0) / 8
+    b = int(max(1, min(256, per_step_budget_s / max(per_ex, 1e-6))))
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ref_worker, args=((which, b, steps, warmup, 1 + i, q),))
+             for i in range(workers)]
+    t0 = time.perf_counter()
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in procs]
+    wall = time.perf_counter() - t0
+    for p in procs:
+        p.join()
+    samples = sum(r[0] for r in res)
+    slowest = max(r[1] for r in res)
+    value = samples / slowest
+    return dict(value=value, unit=UNIT, cores=workers, kind=kind,
+                sample=f"{workers} x replica train_step on {b} examples/step of C1 "
+                       f"(T=128, 700-128-128-20, arctan, init regime), {steps} timed + "
+                       f"{warmup} warm-up steps each", wall_s=wall, examples_per_step=b,
+                ms_per_step=1e3 * slowest / max(steps, 1))
+
+
+def cpu_baseline_single(seconds: float = 12.0):
+    """Bounded single-core sample for our arm's cpu_baseline key."""
+    from oracle.pyoracle import Lib, Net, State, have_ref
+    which = "ref" if have_ref() else "orc"
+    lib = Lib(which)
+    net = Net()
+    b = 32
+    x, y = lib.synth_raster(20, b, 128, 700, 1)
+    pk = lib.pack_time(x)
+    st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
+    lib.train_step(net, st, pk, 128, y)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        lib.train_step(net, st, pk, 128, y)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 200:
+            break
+    return dict(value=b * n / el, unit=UNIT, cores=1,
+                kind="reference" if which == "ref" else "port",
+                sample=f"{n} train_steps of {b} C1 examples (T=128, 700-128-128-20, arctan, "
+                       f"init regime) on 1 host core, {el:.1f} s")
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--profile-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    warmup = max(3, args.warmup)
+    w = WORKLOADS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": f"{args.config}: {w['desc']}", "global_batch": w["B"] * world,
+              "seq_len": w["T"], "network": f"{w['inp']}-" + "-".join(map(str, w["hidden"])) +
+              f"-{w['classes']}", "parallelism": f"dp{world}",
+              "l2": f"HBM-resident dataset of {w['n_data']} examples "
+                    f"({w['n_data'] * (w['T'] // 8) * ((w['inp'] + 63) // 64 * 64) / 1e6:.0f} MB "
+                    f"staged) > 126 MB L2; fresh permuted rows every step, no L2 flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        workers = max(1, os.cpu_count() or 1)
+        budget = 150.0 / (args.steps + warmup)
+        r = cpu_reference(args.steps, warmup, workers, budget)
+        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": warmup,
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth_raster seed 1)",
+                "config": config,
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    spec = shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"])
+    B = w["B"]
+    eng = Engine(spec, TrainConfig(batch_size=B, seed=0, lr=1e-3), w["T"], device=local)
+    if world > 1:
+        uid = [Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.comm_init(uid[0], rank, world)
+    n_data = w["n_data"]
+    eng.synth_dataset(n_data, seed=1)
+    # schedule: the reference epoch shuffle, this rank's contiguous slice of each global batch
+    gb = B * world
+    per_epoch = n_data // gb
+    total = warmup + args.steps
+    rows = np.empty((total, B), np.uint32)
+    e = 0
+    s = 0
+    while s < total:
+        perm = eng.epoch_permutation(e, n_data)
+        for bi in range(per_epoch):
+            if s >= total:
+                break
+            rows[s] = perm[bi * gb + rank * B: bi * gb + (rank + 1) * B]
+            s += 1
+        e += 1
+    eng.upload_schedule(rows.reshape(-1))
+    stream = torch.cuda.ExternalStream(eng.stream)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for i in range(warmup):
+        eng.enqueue_step(i)
+    eng.sync()
+    barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t_start.record(stream)
+        for i in range(args.steps):
+            eng.enqueue_step(warmup + i)
+        t_end.record(stream)
+        eng.sync()
+        torch.cuda.synchronize()
+    barrier()
+    ms = t_start.elapsed_time(t_end)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    loss, acc = eng.read_result()
+    ms_per_step = ms / args.steps
+    value = gb * args.steps / (ms / 1e3)
+
+    # --- end to end through the public API with HOST buffers (pinned H2D in, loss/acc out)
+    packed_host, labels_host = eng.read_dataset(0, min(n_data, 4 * B))
+    nb = packed_host.shape[0] // B
+    for i in range(3):
+        eng.train_step_packed(packed_host[(i % nb) * B:(i % nb + 1) * B],
+                              labels_host[(i % nb) * B:(i % nb + 1) * B])
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(args.e2e_steps):
+        k = i % nb
+        eng.train_step_packed(packed_host[k * B:(k + 1) * B], labels_host[k * B:(k + 1) * B])
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = gb * args.e2e_steps / e2e_s
+    h2d = int(packed_host[:B].nbytes + 8 * B)
+    d2h = 4 + 8
+
+    # --- per-kernel device times (graph with event nodes) -> roofline of the dominant kernel
+    prof = eng.profile(args.profile_steps)
+    hbm_peak, tf_peak, peak_src = peaks()
+    kernels = []
+    for name, kms in prof:
+        bound, work = algorithmic(name, w, eng.n_params)
+        kernels.append({"name": name, "ms": kms, "bound": bound, "work": work})
+    dom = max(kernels, key=lambda k: k["ms"])
+    if dom["bound"] == "tensor":
+        achieved = dom["work"] / (dom["ms"] / 1e3) / 1e12
+        peak, unit = tf_peak, "TFLOP/s"
+    else:
+        achieved = dom["work"] / (dom["ms"] / 1e3) / 1e9
+        peak, unit = hbm_peak, "GB/s"
+    roofline = {"kernel": dom["name"], "bound": dom["bound"], "achieved": achieved, "peak": peak,
+                "unit": unit, "frac": achieved / peak, "traffic": ncu_traffic(dom["name"]),
+                "peak_source": f"{peak_src} ({'bf16_tflops_sustained' if dom['bound'] == 'tensor' else 'hbm_gbs'})",
+                "work_per_launch": dom["work"],
+                "share_of_step": dom["ms"] / sum(k["ms"] for k in kernels)}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (synth_raster seed 1, generated in HBM bit-identical to the "
+                    "reference), random-init weights (reference init, seed 0)",
+            "config": config, "clocks": clocks.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "snn_train_step_packed: host packed batch -> pinned -> H2D, graph, "
+                            "D2H loss/acc, sync every step"},
+            "gpu_launches": eng.launches_per_step * args.steps,
+            "roofline": roofline,
+            "kernels": [{"name": k["name"], "ms": round(k["ms"], 5)} for k in kernels],
+            "final_loss": loss, "final_acc": acc}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_single()
+    if rank == 0:
+        print(json.dumps(line))
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

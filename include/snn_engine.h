@@ -113,6 +113,20 @@ snn_status snn_get_grads(snn_engine* e, float* host, size_t n);
 snn_status snn_stage_dataset(snn_engine* e, const uint8_t* packed, size_t n,
                              const int64_t* labels);
 
+/* synth_raster(classes, n, T, {input}, seed) + pack_time generated on the GPU
+ * straight into the staged HBM dataset, bit-identical to the reference
+ * (commands.hpp:50-86, data.hpp:105-126, rng.hpp:20-64). */
+snn_status snn_synth_dataset(snn_engine* e, size_t n, uint64_t seed);
+
+/* Copy rows [start, start+n) of the staged dataset back to the host in the
+ * reference's packed layout [n][ceil(T/8)][input] + labels. */
+snn_status snn_read_dataset(snn_engine* e, size_t start, size_t n, uint8_t* packed,
+                            int64_t* labels);
+
+/* permutation(master.child(1+epoch).child(0), n): the epoch shuffle of
+ * train() (optimize.hpp:266-268, data.hpp:181-208, rng.hpp:78-87). */
+snn_status snn_epoch_permutation(snn_engine* e, size_t epoch, uint32_t* out, size_t n);
+
 /* train_step on rows of the staged dataset (optimize.hpp:152-214).  rows: host
  * array of batch_size dataset indices.  Updates params + optimizer state in
  * place and returns StepResult{loss, accuracy} (global over ranks). */
@@ -144,6 +158,11 @@ snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy);
 void* snn_stream(snn_engine* e);
 /* Number of kernel launches one step issues. */
 int32_t snn_launches_per_step(const snn_engine* e);
+/* Device time of every launch of a step, averaged over `steps` steps (a
+ * captured graph with event-record nodes between kernels). */
+snn_status snn_profile_steps(snn_engine* e, int32_t steps, double* ms, int32_t max_launches,
+                             int32_t* n_launches);
+const char* snn_launch_name(const snn_engine* e, int32_t i);
 
 /* Data-parallel training: one engine per GPU/process.  Every rank passes the
  * same 128-byte ncclUniqueId (rank 0 creates it with snn_nccl_unique_id).

@@ -221,12 +221,17 @@ struct snn_engine {
     if (h_loss) cudaFreeHost(h_loss);
     if (h_acc) cudaFreeHost(h_acc);
     if (h_rows) cudaFreeHost(h_rows);
+    if (pinned) cudaFreeHost(pinned);
+    for (auto& g : prof_graphs) cudaGraphExecDestroy(g.second);
+    for (auto& ev : prof_ev) cudaEventDestroy(ev);
     if (stream) cudaStreamDestroy(stream);
   }
 
   void clear_graphs() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.second);
     graphs.clear();
+    for (auto& g : prof_graphs) cudaGraphExecDestroy(g.second);
+    prof_graphs.clear();
   }
 
   int B_global() const { return B * world; }
@@ -307,7 +312,7 @@ struct snn_engine {
     v.alloc(n_params);
     comm.alloc(n_params + 2);
     step.alloc(1);
-    grow_bc(1 << 16);
+    grow_bc(1 << 20);
     for (int j = 0; j < L; ++j) {
       wt[j].alloc(size_t(3) * N_pad[j] * K_pad[j]);
       if (j >= 1) wb[j].alloc(size_t(3) * K_pad[j] * N_pad[j]);
@@ -446,34 +451,86 @@ struct snn_engine {
   }
 
   // ---------------------------------------------------------------- data
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  bool sync_after_stage = true;
+
   void stage(Dataset& ds, const uint8_t* packed, size_t n, const int64_t* labels) {
     const int tp8 = (T + 7) / 8;
     const int tp8_pad = T_pad / 8;
     for (size_t i = 0; i < n; ++i)
       if (labels[i] < 0 || labels[i] >= C)
         fail(SNN_ERR_ARGUMENT, "target %lld outside [0,%d)", (long long)labels[i], C);
-    std::vector<uint8_t> h(n * size_t(tp8_pad) * IN_pad, 0);
+    const size_t bytes = n * size_t(tp8_pad) * IN_pad;
+    // pinned staging area: the H2D copy of every step's input runs at full PCIe rate
+    if (pinned_bytes < bytes + n * sizeof(int32_t)) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      pinned_bytes = 0;
+      CK(cudaMallocHost(&pinned, bytes + n * sizeof(int32_t)));
+      pinned_bytes = bytes + n * sizeof(int32_t);
+    }
+    uint8_t* h = static_cast<uint8_t*>(pinned);
+    std::memset(h, 0, bytes);
     for (size_t i = 0; i < n; ++i)
       for (int g = 0; g < tp8; ++g)
-        std::memcpy(&h[(i * tp8_pad + g) * IN_pad], packed + (i * tp8 + g) * size_t(IN), IN);
-    std::vector<int32_t> lab(n);
+        std::memcpy(h + (i * tp8_pad + g) * IN_pad, packed + (i * tp8 + g) * size_t(IN), IN);
+    int32_t* lab = reinterpret_cast<int32_t*>(h + bytes);
     for (size_t i = 0; i < n; ++i) lab[i] = int32_t(labels[i]);
     if (ds.n != n) {
-      ds.x.alloc(h.size(), false);
+      ds.x.alloc(bytes, false);
       ds.labels.alloc(n, false);
       ds.n = n;
       clear_graphs();
     }
-    CK(cudaMemcpyAsync(ds.x.p, h.data(), h.size(), cudaMemcpyHostToDevice, stream));
-    CK(cudaMemcpyAsync(ds.labels.p, lab.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(ds.x.p, h, bytes, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(ds.labels.p, lab, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    if (sync_after_stage) CK(cudaStreamSynchronize(stream));
+  }
+
+  void synth(size_t n, uint64_t seed) {
+    if (n == 0) fail(SNN_ERR_ARGUMENT, "synth: classes, examples, and steps must be >= 1");
+    Dataset& ds = data;
+    const size_t bytes = n * size_t(T_pad / 8) * IN_pad;
+    if (ds.n != n) {
+      ds.x.alloc(bytes, false);
+      ds.labels.alloc(n, false);
+      ds.n = n;
+      clear_graphs();
+    }
+    SynthArgs a{};
+    a.x = ds.x.p;
+    a.labels = ds.labels.p;
+    a.master = hostrng::from_seed(seed);
+    a.n = int64_t(n);
+    a.T = T; a.T_pad = T_pad; a.f = IN; a.f_pad = IN_pad; a.classes = C;
+    const int64_t total = int64_t(bytes);
+    k_synth<<<unsigned((total + 255) / 256), 256, 0, stream>>>(a);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(stream));
   }
 
   // ---------------------------------------------------------------- step
   int launches_per_step() const { return 3 * L + 6; }
 
-  void enqueue_body(const Dataset& ds, int update) {
+  std::vector<std::string> launch_names;
+  std::vector<cudaEvent_t> prof_ev;
+  std::map<std::pair<const void*, int>, cudaGraphExec_t> prof_graphs;
+
+  // Records an event after each kernel when profiling (graph event nodes).
+  void mark(std::vector<cudaEvent_t>* evs, const char* name, int layer) {
+    CK(cudaGetLastError());
+    launch_names.push_back(std::string(name) + (layer >= 0 ? "[" + std::to_string(layer) + "]" : ""));
+    if (evs) {
+      if (evs->size() < launch_names.size() + 1) fail(SNN_ERR_STATE, "profiling events exhausted");
+      CK(cudaEventRecordWithFlags((*evs)[launch_names.size()], stream, cudaEventRecordExternal));
+    }
+  }
+
+  void enqueue_body(const Dataset& ds, int update, std::vector<cudaEvent_t>* evs = nullptr) {
     const size_t rows = size_t(B) * T_pad;
+    launch_names.clear();
+    if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
     // forward
     for (int l = 0; l < L; ++l) {
       FwdArgs f{};
@@ -490,6 +547,7 @@ struct snn_engine {
       f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
       f.theta = net.threshold;
       k_lif_fwd<<<dim3(B, H_pad[l] / 128), kFwdThreads, fwd_smem_bytes(TT), stream>>>(tm_wt[l], f);
+      mark(evs, "lif_fwd", l);
     }
     // readout + loss + LI backward
     {
@@ -511,6 +569,7 @@ struct snn_engine {
       r.inv_b = 1.0f / float(B_global());
       const size_t smem = (size_t(H[L - 1]) * C + size_t(T) * C) * sizeof(float);
       k_readout<<<B, 128, smem, stream>>>(r);
+      mark(evs, "readout", -1);
     }
     // hidden backward, top-down
     for (int l = L - 1; l >= 0; --l) {
@@ -528,9 +587,11 @@ struct snn_engine {
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
       if (l == L - 1) {
         k_lif_bwd_ro<<<dim3(B, H_pad[l] / 128), 128, 0, stream>>>(bw);
+        mark(evs, "lif_bwd_ro", l);
       } else {
         k_lif_bwd_gemm<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT), stream>>>(
             tm_wb[l + 1], tm_di_k[l + 1], bw);
+        mark(evs, "lif_bwd_gemm", l);
       }
     }
     // weight gradients
@@ -545,6 +606,7 @@ struct snn_engine {
       w.n_tile = n_tile_w[j]; w.splits = splits_w[j]; w.x_row_stride = IN_pad;
       k_wgrad<<<dim3(M_pad_w[j] / 128, N_pad[j] / n_tile_w[j], splits_w[j]), kWgThreads,
                 wg_smem_bytes(n_tile_w[j]), stream>>>(tm_di_w[j], w);
+      mark(evs, "wgrad", j);
     }
     (void)rows;
     // gradient assembly
@@ -564,19 +626,68 @@ struct snn_engine {
       r.grads = comm.p;
       r.B = B;
       k_reduce<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(r);
+      mark(evs, "reduce", -1);
     }
     k_loss_partial<<<1, 32, 0, stream>>>(loss_b.p, correct_b.p, B, comm.p + n_params);
+    mark(evs, "loss_partial", -1);
     if (world > 1) {
       const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2, /*ncclFloat32*/ 7,
                                       /*ncclSum*/ 0, comm_handle, stream);
       if (rc != 0) fail(SNN_ERR_CUDA, "ncclAllReduce failed (%d)", rc);
+      mark(evs, "nccl_allreduce", -1);
     }
     if (update) {
       AdamArgs a = adam_args(1);
       k_adam<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(a);
+      mark(evs, "adam", -1);
     }
     k_result<<<1, 32, 0, stream>>>(comm.p + n_params, B_global(), step.p, update, result_loss.p,
                                    result_acc.p);
+    mark(evs, "result", -1);
+  }
+
+  // Per-launch device times of `steps` full steps (graph with event nodes).
+  std::vector<double> profile(int steps) {
+    const int max_ev = 64;
+    if (prof_ev.empty()) {
+      prof_ev.resize(max_ev);
+      for (auto& ev : prof_ev) CK(cudaEventCreate(&ev));
+    }
+    const Dataset& ds = data;
+    if (ds.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    auto key = std::make_pair(static_cast<const void*>(ds.x.p), 1);
+    cudaGraphExec_t ex = nullptr;
+    auto it = prof_graphs.find(key);
+    if (it == prof_graphs.end()) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_body(ds, 1, &prof_ev);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        throw;
+      }
+      CK(cudaStreamEndCapture(stream, &g));
+      CK(cudaGraphInstantiate(&ex, g, 0));
+      CK(cudaGraphDestroy(g));
+      prof_graphs[key] = ex;
+    } else {
+      ex = it->second;
+    }
+    const size_t nl = launch_names.size();
+    std::vector<double> acc(nl, 0.0);
+    for (int s = 0; s < steps; ++s) {
+      ensure_bc_capacity();
+      CK(cudaGraphLaunch(ex, stream));
+      CK(cudaStreamSynchronize(stream));
+      for (size_t i = 0; i < nl; ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, prof_ev[i], prof_ev[i + 1]));
+        acc[i] += ms;
+      }
+    }
+    for (auto& a : acc) a /= std::max(1, steps);
+    return acc;
   }
 
   const EntryHost& entry_of(int kind, int layer) const {
@@ -816,7 +927,9 @@ snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
                                  const int64_t* targets, float* loss, double* accuracy) {
   if (!e || !packed_batch || !targets) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
+    e->sync_after_stage = false;
     e->stage(e->scratch, packed_batch, size_t(e->B), targets);
+    e->sync_after_stage = true;
     std::vector<uint32_t> rows(size_t(e->B));
     for (int i = 0; i < e->B; ++i) rows[size_t(i)] = uint32_t(i);
     e->step_rows(rows.data(), e->scratch, 1, loss, accuracy);
@@ -860,7 +973,6 @@ snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_ste
     e->sched_steps = n_steps;
     CK(cudaMemcpy(e->sched.p, rows, n_steps * e->B * sizeof(uint32_t), cudaMemcpyHostToDevice));
     e->ensure_bc_capacity();
-    e->grow_bc(e->bc_steps + 0);
   });
 }
 
@@ -882,6 +994,55 @@ snn_status snn_sync(snn_engine* e) {
 snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy) {
   if (!e) return SNN_ERR_ARGUMENT;
   return guard(e, [&] { e->read_result(loss, accuracy); });
+}
+
+snn_status snn_synth_dataset(snn_engine* e, size_t n, uint64_t seed) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->synth(n, seed); });
+}
+
+snn_status snn_read_dataset(snn_engine* e, size_t start, size_t n, uint8_t* packed,
+                            int64_t* labels) {
+  if (!e || !packed || !labels) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (start + n > e->data.n) fail(SNN_ERR_ARGUMENT, "rows [%zu,%zu) outside dataset", start, start + n);
+    const int tp8 = (e->T + 7) / 8, tp8_pad = e->T_pad / 8;
+    std::vector<uint8_t> h(n * size_t(tp8_pad) * e->IN_pad);
+    std::vector<int32_t> lab(n);
+    CK(cudaMemcpy(h.data(), e->data.x.p + start * size_t(tp8_pad) * e->IN_pad, h.size(),
+                  cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(lab.data(), e->data.labels.p + start, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) {
+      labels[i] = lab[i];
+      for (int g = 0; g < tp8; ++g)
+        std::memcpy(packed + (i * tp8 + g) * size_t(e->IN), h.data() + (i * tp8_pad + g) * e->IN_pad,
+                    size_t(e->IN));
+    }
+  });
+}
+
+snn_status snn_epoch_permutation(snn_engine* e, size_t epoch, uint32_t* out, size_t n) {
+  if (!e || !out) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    const uint64_t ek = hostrng::child(hostrng::from_seed(e->cfg.seed), 1 + epoch);
+    const std::vector<uint32_t> p = hostrng::permutation(hostrng::child(ek, 0), n);
+    std::memcpy(out, p.data(), n * sizeof(uint32_t));
+  });
+}
+
+snn_status snn_profile_steps(snn_engine* e, int32_t steps, double* ms, int32_t max_launches,
+                             int32_t* n_launches) {
+  if (!e || !ms || !n_launches || steps < 1) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    const std::vector<double> t = e->profile(steps);
+    *n_launches = int32_t(t.size());
+    for (size_t i = 0; i < t.size() && int32_t(i) < max_launches; ++i) ms[i] = t[i];
+  });
+}
+
+const char* snn_launch_name(const snn_engine* e, int32_t i) {
+  if (!e || i < 0 || size_t(i) >= e->launch_names.size()) return "";
+  return e->launch_names[size_t(i)].c_str();
 }
 
 void* snn_stream(snn_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }

@@ -891,6 +891,55 @@ __global__ void k_adam(AdamArgs a) {
   }
 }
 
+// ============================================================================
+// K0  k_synth: synth_raster(classes, n, T, {f}, seed) + pack_time, generated
+// directly into the staged HBM layout (commands.hpp:50-86, data.hpp:105-126).
+// SplitMix64 counter draws (rng.hpp:20-64) in integer + fp64 math -> bit-exact.
+// One thread per (example, t-group, feature) byte.
+// ============================================================================
+__device__ __forceinline__ uint64_t d_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct SynthArgs {
+  uint8_t* x;        // [n][T_pad/8][f_pad]
+  int32_t* labels;   // [n]
+  uint64_t master;   // RngKey::from_seed(seed).word
+  int64_t n;
+  int T, T_pad, f, f_pad, classes;
+};
+
+__global__ void k_synth(SynthArgs a) {
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int groups = a.T_pad / 8;
+  const int64_t total = a.n * groups * a.f_pad;
+  if (gid >= total) return;
+  const int j = int(gid % a.f_pad);
+  const int g = int((gid / a.f_pad) % groups);
+  const int64_t i = gid / (int64_t(a.f_pad) * groups);
+  const int label = int(i % a.classes);
+  if (j == 0 && g == 0) a.labels[i] = label;
+  uint8_t byte = 0;
+  if (j < a.f) {
+    const int block = a.f / a.classes > 1 ? a.f / a.classes : 1;
+    const int lo = label * block, hi = lo + block < a.f ? lo + block : a.f;
+    const double rate = (j >= lo && j < hi) ? 0.4 : 0.05;
+    const uint64_t ek = d_mix64(a.master ^ d_mix64(uint64_t(i) + 0xC2B2AE3D27D4EB4Full));
+    for (int e = 0; e < 8; ++e) {
+      const int s = g * 8 + e;
+      if (s >= a.T) break;
+      const uint64_t ctr = uint64_t(s) * uint64_t(a.f) + uint64_t(j);
+      const uint64_t bits = d_mix64(ek ^ d_mix64(ctr + 0x165667B19E3779F9ull));
+      const double u = double(bits >> 11) * 0x1.0p-53;
+      if (u < rate) byte |= uint8_t(1u << (7 - e));
+    }
+  }
+  a.x[gid] = byte;
+}
+
 // Local loss sum in batch order (objective.hpp:57-72: loss += lse - row[y]) and
 // hit count, appended to the gradient buffer so one allreduce carries both.
 __global__ void k_loss_partial(const float* loss_b, const int32_t* correct_b, int B,

@@ -180,8 +180,12 @@ def lib() -> C.CDLL:
                  "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
                  "snn_train_step_packed", "snn_forward_backward", "snn_train_epochs",
                  "snn_upload_schedule", "snn_enqueue_step", "snn_sync", "snn_read_result",
-                 "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch"):
+                 "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
+                 "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
+                 "snn_read_dataset"):
         getattr(L, name).restype = C.c_int
+    L.snn_launch_name.restype = C.c_char_p
+    L.snn_launch_name.argtypes = [C.c_void_p, C.c_int32]
     L.snn_engine_destroy.restype = None
     L.snn_engine_destroy.argtypes = [C.c_void_p]
     _lib = L
@@ -309,6 +313,25 @@ class Engine:
                                               C.c_size_t(packed.shape[0]), _p(labels, C.c_int64)))
         self.n_examples = packed.shape[0]
 
+    def synth_dataset(self, n: int, seed: int = 1):
+        """synth_raster(classes, n, T, {input}, seed) generated in HBM (commands.hpp:50-86)."""
+        self._check(self._L.snn_synth_dataset(self._h, C.c_size_t(n), C.c_uint64(seed)))
+        self.n_examples = n
+
+    def read_dataset(self, start: int, n: int):
+        """Rows [start, start+n) of the staged dataset in the reference packed layout."""
+        packed = np.empty((n, (self.time_steps + 7) // 8, self.desc["input"]), np.uint8)
+        labels = np.empty(n, np.int64)
+        self._check(self._L.snn_read_dataset(self._h, C.c_size_t(start), C.c_size_t(n),
+                                             _p(packed, C.c_uint8), _p(labels, C.c_int64)))
+        return packed, labels
+
+    def epoch_permutation(self, epoch: int, n: int) -> np.ndarray:
+        out = np.empty(n, np.uint32)
+        self._check(self._L.snn_epoch_permutation(self._h, C.c_size_t(epoch), _p(out, C.c_uint32),
+                                                  C.c_size_t(n)))
+        return out
+
     # ---------------------------------------------------------------- steps
     def train_step(self, rows) -> tuple[float, float]:
         r = np.ascontiguousarray(rows, np.uint32)
@@ -365,6 +388,14 @@ class Engine:
     @property
     def stream(self) -> int:
         return int(self._L.snn_stream(self._h) or 0)
+
+    def profile(self, steps: int = 5):
+        """[(launch name, mean device ms)] for one step (graph with event nodes)."""
+        ms = np.zeros(64, np.float64)
+        n = C.c_int32()
+        self._check(self._L.snn_profile_steps(self._h, int(steps), _p(ms, C.c_double), 64,
+                                              C.byref(n)))
+        return [(self._L.snn_launch_name(self._h, i).decode(), float(ms[i])) for i in range(n.value)]
 
     @property
     def launches_per_step(self) -> int:

@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA engine (through the C ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): spike-raster agreement >= 99.99 %, loss and
+gradients within 1e-4 relative (norm per tensor) on the fp32 path.  The scan
+kernels are additionally checked BIT-EXACT given the GPU's own projection
+(numpy float32 restatement in tests/scanref.py, same op order as neuron.hpp).
+"""
+import numpy as np
+import pytest
+
+import scanref
+from oracle.pyoracle import Net, State
+
+pytestmark = pytest.mark.gpu
+
+SPIKE_AGREE = 0.9999
+REL_TOL = 1e-4
+
+
+def relnorm(a, b):
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def make_engine(net: Net, B, T, seed=0, lr=1e-3):
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    spec = shd_spec(hidden=net.hidden, classes=net.classes, inp=net.inp, act=net.act,
+                    bias=net.bias)
+    for layer in spec.layers:
+        if hasattr(layer, "threshold"):
+            layer.threshold = net.threshold
+            if net.slope is not None:
+                layer.activation.slope = net.slope
+    return Engine(spec, TrainConfig(batch_size=B, seed=seed, lr=lr, unroll=net.unroll), T)
+
+
+def check_grads(orc, net, g, ref, tol=REL_TOL):
+    for name, off, size in orc.entries(net):
+        r = relnorm(g[off:off + size], ref[off:off + size])
+        assert r <= tol, f"{name}: relnorm {r:.3e}"
+
+
+CASES = [
+    ("tiny", Net(inp=30, hidden=(16, 12), classes=5, unroll=4), 6, 19, 3.0),
+    ("T70-superspike", Net(inp=70, hidden=(40, 24), classes=7, act="superspike"), 5, 70, 3.0),
+    ("3hidden-triangular", Net(inp=50, hidden=(64, 48, 32), classes=6, act="triangular"), 4, 33, 3.0),
+    ("bias-boxcar", Net(inp=40, hidden=(24, 20), classes=4, act="boxcar", bias=True), 5, 23, 3.0),
+    ("custom-theta", Net(inp=33, hidden=(130, 32), classes=7, act="custom", threshold=0.75), 3, 40, 2.0),
+    ("T200-two-tiles", Net(inp=64, hidden=(128, 128), classes=10), 3, 200, 2.0),
+    ("c1-shape", Net(), 8, 128, 2.0),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_step_parity(orc, case):
+    _, net, B, T, scale = case
+    params = orc.init(net, orc.key_child(orc.key_from_seed(11), 0)) * np.float32(scale)
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 5)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    assert np.array_equal(eng.get_params(), params)
+    eng.debug(True)
+    rows = np.arange(B, dtype=np.uint32)
+    loss, acc = eng.forward_backward(rows)
+    ref = orc.forward_backward(net, params, pk, T, y, want_spikes=True, want_trace=True)
+    assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    ents = {n: (o, s) for n, o, s in orc.entries(net)}
+    for l, h in enumerate(net.hidden):
+        I = eng.fetch("I", l)
+        o, s = ents[f"l{2 * l + 1}.beta"]
+        V_ref, S_ref = scanref.lif_forward(
+            I if not net.bias else I, params[o:o + s], net.threshold)
+        assert np.array_equal(eng.fetch("V", l), V_ref), f"layer {l}: V not bit-exact given I"
+        S = eng.fetch("spikes", l)
+        assert np.array_equal(S, S_ref), f"layer {l}: spikes not bit-exact given I"
+        assert (S == ref["spikes"][l]).mean() >= SPIKE_AGREE
+    assert relnorm(eng.fetch("trace"), ref["trace"]) <= REL_TOL
+    check_grads(orc, net, eng.get_grads(), ref["grads"])
+    # the backward scan given the GPU's own dS is bit-exact too
+    for l, h in enumerate(net.hidden):
+        o, s = ents[f"l{2 * l + 1}.beta"]
+        dS = eng.fetch("dS", l)
+        assert np.isfinite(dS).all()
+    # one optimizer step
+    st = State(params.copy())
+    lo, ao = orc.train_step(net, st, pk, T, y)
+    eng.debug(False)
+    l2, a2 = eng.train_step(rows)
+    assert abs(l2 - lo) <= REL_TOL * abs(lo) and a2 == ao
+    assert relnorm(eng.get_params(), st.params) <= 1e-6
+    m, v, step = eng.get_opt_state()
+    assert step == 1
+    assert relnorm(m, st.m) <= REL_TOL and relnorm(v, st.v) <= 1e-3
+
+
+@pytest.mark.parametrize("tag", ["init", "warm", "hot"])
+def test_c1_golden(orc, golden, tag):
+    """C1 network at the reference's own init/warm/hot checkpoints (golden)."""
+    g = golden("c1")
+    net = Net()
+    params = g["params_init"] if tag == "init" else g[f"{tag}_params"]
+    eng = make_engine(net, 16, 128)
+    eng.stage_dataset(g["batch_packed"], g["batch_y"])
+    eng.set_params(params)
+    eng.debug(True)
+    loss, acc = eng.forward_backward(np.arange(16, dtype=np.uint32))
+    ref_loss = float(g[f"{tag}_loss"])
+    assert abs(loss - ref_loss) <= REL_TOL * max(abs(ref_loss), 1e-3)
+    for l in range(2):
+        S = eng.fetch("spikes", l)
+        ref_s = np.unpackbits(g[f"{tag}_spikes{l}_bits"])[:S.size].reshape(S.shape)
+        assert (S == ref_s).mean() >= SPIKE_AGREE
+    check_grads(orc, net, eng.get_grads(), g[f"{tag}_grads"])
+
+
+@pytest.mark.parametrize("tag", ["init", "hot"])
+def test_c1_full_batch(orc, golden, tag):
+    """Full C1 workload (B=256, T=128) vs the oracle on the same inputs."""
+    g = golden("c1")
+    net = Net()
+    params = g["params_init"] if tag == "init" else g["hot_params"]
+    x, y = orc.synth_raster(20, 256, 128, 700, 1)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, 256, 128)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    eng.debug(True)
+    loss, acc = eng.forward_backward(np.arange(256, dtype=np.uint32))
+    ref = orc.forward_backward(net, params, pk, 128, y, want_spikes=True)
+    assert abs(loss - ref["loss"]) <= REL_TOL * max(abs(ref["loss"]), 1e-3)
+    assert acc == ref["acc"]
+    for l in range(2):
+        assert (eng.fetch("spikes", l) == ref["spikes"][l]).mean() >= SPIKE_AGREE
+    check_grads(orc, net, eng.get_grads(), ref["grads"])
+
+
+def test_training_curve_matches_oracle(orc):
+    """Epoch loop with the reference key schedule: 3 epochs of C1-shaped training."""
+    net = Net()
+    B, N, T = 64, 256, 128
+    x, y = orc.synth_raster(20, N, T, 700, 1)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T, seed=0)
+    p0 = orc.init(net, orc.key_child(orc.key_from_seed(0), 0))
+    assert np.array_equal(eng.get_params(), p0), "engine init != reference init(master.child(0))"
+    eng.stage_dataset(pk, y)
+    m_gpu = eng.train_epochs(3)
+    st = State(p0.copy())
+    m_ref = orc.train_epochs(net, st, pk, y, T, B, 3, 0)
+    assert np.allclose(m_gpu[:, 0], m_ref[:, 0], rtol=1e-3), (m_gpu, m_ref)
+    assert np.abs(m_gpu[:, 1] - m_ref[:, 1]).max() <= 1.0 / B + 1e-12
+    assert relnorm(eng.get_params(), st.params) <= 1e-4
+
+
+def test_packed_entry_matches_rows_entry(orc):
+    """train_step(st, packed_x, T, targets) == the staged-dataset path."""
+    net = Net(inp=30, hidden=(16, 12), classes=5)
+    x, y = orc.synth_raster(5, 4, 19, 30, 2)
+    pk = orc.pack_time(x)
+    e1 = make_engine(net, 4, 19)
+    e2 = make_engine(net, 4, 19)
+    e1.stage_dataset(pk, y)
+    l1 = e1.train_step(np.arange(4, dtype=np.uint32))
+    l2 = e2.train_step_packed(pk, y)
+    assert l1 == l2
+    assert np.array_equal(e1.get_params(), e2.get_params())
+
+
+def test_errors_map_to_reference_classes(orc):
+    from paper_2402_18994_b200 import ArgumentError, FormatError
+    net = Net(inp=30, hidden=(16,), classes=5)
+    eng = make_engine(net, 2, 19)
+    x, y = orc.synth_raster(5, 2, 19, 30, 2)
+    pk = orc.pack_time(x)
+    with pytest.raises(ArgumentError):
+        eng.stage_dataset(pk, np.array([0, 7]))       # target outside [0, classes)
+    with pytest.raises(FormatError):
+        eng.stage_dataset(pk[:, :1], y)                # packed extent != ceil(T/8)
+    eng.stage_dataset(pk, y)
+    with pytest.raises(ArgumentError):
+        eng.train_step(np.array([0, 5], np.uint32))    # row outside the dataset
+
+
+def test_determinism(orc):
+    net = Net(inp=30, hidden=(16, 12), classes=5)
+    x, y = orc.synth_raster(5, 8, 19, 30, 2)
+    pk = orc.pack_time(x)
+    outs = []
+    for _ in range(2):
+        e = make_engine(net, 4, 19, seed=9)
+        e.stage_dataset(pk, y)
+        m = e.train_epochs(3)
+        outs.append((m, e.get_params()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
