@@ -6,7 +6,7 @@
 //   k_readout              readout projection + LI + integral CE + LI reverse scan
 //   k_lif_bwd_ro / _gemm   dS (CUDA-core for the readout, tcgen05 otherwise) + LIF reverse scan
 //   k_wgrad x (L+1)        dW = A^T dI on tcgen05, split-K partials
-//   k_reduce, k_loss_partial, [ncclAllReduce], k_adam, k_result
+//   k_reduce (+loss, step), [ncclAllReduce], k_adam (+StepResult)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -193,6 +193,8 @@ struct snn_engine {
   DevBuf<float> d3, loss_b;
   DevBuf<int32_t> correct_b;
   DevBuf<float> partial[kMaxLayers];
+  DevBuf<int32_t> vec_index;
+  int n_vec = 0;
   DevBuf<float> result_loss;
   DevBuf<double> result_acc;
   float* h_loss = nullptr;
@@ -276,8 +278,9 @@ struct snn_engine {
       M_pad_w[j] = rup(K[j], 128);
       n_tile_w[j] = j < L ? 128 : 64;
     }
-    const size_t ro_smem = (size_t(H[L - 1]) * C + size_t(T) * C) * sizeof(float);
+    const size_t ro_smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
     if (ro_smem > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "readout working set too large");
+    if (size_t(T) * C * 4 > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "T * classes too large");
     // split-K so that each Linear's wgrad launch fills the chip ~2x
     for (int j = 0; j <= L; ++j) {
       const int tiles = (M_pad_w[j] / 128) * (N_pad[j] / n_tile_w[j]);
@@ -355,6 +358,17 @@ struct snn_engine {
                             int(wg_smem_bytes(128))));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
+    CK(cudaFuncSetAttribute(k_lif_bwd_ro, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(200 * 1024)));
+    {
+      std::vector<int32_t> vi;
+      for (const auto& en : entries)
+        if (en.kind != kEntryW)
+          for (size_t q = 0; q < en.size; ++q) vi.push_back(int32_t(en.offset + q));
+      vec_index.alloc(vi.size(), false);
+      CK(cudaMemcpy(vec_index.p, vi.data(), vi.size() * 4, cudaMemcpyHostToDevice));
+      n_vec = int(vi.size());
+    }
   }
 
   void grow_bc(size_t steps) {
@@ -439,6 +453,9 @@ struct snn_engine {
     a.omb1 = 1.0f - cfg.beta1;
     a.omb2 = 1.0f - cfg.beta2;
     a.update = update;
+    a.B_global = B_global();
+    a.loss_out = result_loss.p;
+    a.acc_out = result_acc.p;
     return a;
   }
 
@@ -511,7 +528,7 @@ struct snn_engine {
   }
 
   // ---------------------------------------------------------------- step
-  int launches_per_step() const { return 3 * L + 6; }
+  int launches_per_step() const { return 3 * L + 4; }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;
@@ -567,7 +584,7 @@ struct snn_engine {
       r.dbg_trace = debug ? dbg_trace.p : nullptr;
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
       r.inv_b = 1.0f / float(B_global());
-      const size_t smem = (size_t(H[L - 1]) * C + size_t(T) * C) * sizeof(float);
+      const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
       k_readout<<<B, 128, smem, stream>>>(r);
       mark(evs, "readout", -1);
     }
@@ -586,7 +603,7 @@ struct snn_engine {
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.C = C; bw.act = net.activation;
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
       if (l == L - 1) {
-        k_lif_bwd_ro<<<dim3(B, H_pad[l] / 128), 128, 0, stream>>>(bw);
+        k_lif_bwd_ro<<<dim3(B, H_pad[l] / 128), 128, size_t(T) * C * 4, stream>>>(bw);
         mark(evs, "lif_bwd_ro", l);
       } else {
         k_lif_bwd_gemm<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT), stream>>>(
@@ -609,7 +626,7 @@ struct snn_engine {
       mark(evs, "wgrad", j);
     }
     (void)rows;
-    // gradient assembly
+    // gradient assembly (+ loss sum, hits, step counter)
     {
       ReduceArgs r{};
       fill_entries(r.entries, &r.n_entries);
@@ -622,14 +639,20 @@ struct snn_engine {
         r.dbeta_part[j] = dbeta[j].p;
         r.dbias_part[j] = net.bias ? dbias[j].p : nullptr;
       }
+      r.vec_index = vec_index.p;
+      r.n_vec = n_vec;
       r.params = params.p;
       r.grads = comm.p;
+      r.loss_b = loss_b.p;
+      r.correct_b = correct_b.p;
+      r.step = step.p;
+      r.update = update;
       r.B = B;
-      k_reduce<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(r);
+      r.w_blocks = int((n_params + 255) / 256);
+      const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
+      k_reduce<<<blocks, 256, 0, stream>>>(r);
       mark(evs, "reduce", -1);
     }
-    k_loss_partial<<<1, 32, 0, stream>>>(loss_b.p, correct_b.p, B, comm.p + n_params);
-    mark(evs, "loss_partial", -1);
     if (world > 1) {
       const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2, /*ncclFloat32*/ 7,
                                       /*ncclSum*/ 0, comm_handle, stream);
@@ -640,10 +663,11 @@ struct snn_engine {
       AdamArgs a = adam_args(1);
       k_adam<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(a);
       mark(evs, "adam", -1);
+    } else {
+      k_result<<<1, 32, 0, stream>>>(comm.p + n_params, B_global(), step.p, 0, result_loss.p,
+                                     result_acc.p);
+      mark(evs, "result", -1);
     }
-    k_result<<<1, 32, 0, stream>>>(comm.p + n_params, B_global(), step.p, update, result_loss.p,
-                                   result_acc.p);
-    mark(evs, "result", -1);
   }
 
   // Per-launch device times of `steps` full steps (graph with event nodes).

@@ -216,39 +216,48 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // ---------------- B-operand producers: activations -> bf16 {0,1} rows t, cols k
+    // ---------------- B-operand producers: activations -> bf16 {0,1} rows t, cols k.
+    // Global loads of stage it+1 are issued before waiting for stage it's slot.
     const int tid = threadIdx.x - 128;
     const size_t kwords = size_t(a.K_pad) / 32;
+    // kind 0: unit = (t-group g, 8-feature chunk q), TT units; kind 1: unit = row t.
+    const bool active = tid < a.TT;
+    const size_t xrow = (a.in_kind == 0) ? size_t(a.rows[b]) : 0;
+    auto fetch = [&](int it) -> uint64_t {
+      if (!active || it >= total) return 0;
+      const int tt = it / KB, kb = it % KB;
+      if (a.in_kind == 0) {
+        const int g = tid >> 3, q = tid & 7;
+        return __ldg(reinterpret_cast<const unsigned long long*>(
+            a.x + (xrow * (a.T_pad / 8) + tt * (a.TT / 8) + g) * size_t(a.K_pad) + kb * 64 + q * 8));
+      }
+      return __ldg(reinterpret_cast<const unsigned long long*>(
+          a.s_in + (size_t(b) * a.T_pad + tt * a.TT + tid) * kwords + kb * 2));
+    };
+    uint64_t cur = fetch(0);
     for (int it = 0; it < total; ++it) {
       const int s = it % kFwdStages, ph = (it / kFwdStages) & 1;
-      const int tt = it / KB, kb = it % KB;
+      const uint64_t nxt = fetch(it + 1);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t Bt = smem_u32(smem + s * stage_bytes + 3 * kPlaneTile);
-      if (a.in_kind == 0) {
-        // dataset bytes: [row][t/8][k], bit 7-(t%8); one u64 = 8 k of one t-group
-        const size_t row = a.rows[b];
-        const int groups = a.TT / 8;
-        for (int u = tid; u < groups * 8; u += 128) {
-          const int g = u >> 3, q = u & 7;
-          const uint64_t w = *reinterpret_cast<const uint64_t*>(
-              a.x + (row * (a.T_pad / 8) + tt * (a.TT / 8) + g) * size_t(a.K_pad) + kb * 64 + q * 8);
+      if (active) {
+        if (a.in_kind == 0) {
+          // dataset bytes [row][t/8][k], bit 7-(t%8): 8 k of one t-group -> 8 rows
+          const int g = tid >> 3, q = tid & 7;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             st_shared_v4(Bt + sw128_off(8 * g + j, q),
-                         expand_bytes01((w >> (7 - j)) & 0x0101010101010101ull));
-        }
-      } else {
-        // neuron-packed spike words: row t, 2 words = 64 k
-        for (int u = tid; u < a.TT * 8; u += 128) {
-          const int r = u >> 3, q = u & 7;
-          const uint32_t* src =
-              a.s_in + (size_t(b) * a.T_pad + tt * a.TT + r) * kwords + kb * 2;
-          const uint32_t word = src[q >> 2];
-          st_shared_v4(Bt + sw128_off(r, q), expand_bits_lsb((word >> (8 * (q & 3))) & 0xFFu));
+                         expand_bytes01((cur >> (7 - j)) & 0x0101010101010101ull));
+        } else {
+          // neuron-packed spike words: row t, 2 words = 64 k
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            st_shared_v4(Bt + sw128_off(tid, q), expand_bits_lsb(uint32_t(cur >> (8 * q)) & 0xFFu));
         }
       }
       fence_async_smem();
       mbar_arrive(&full[s]);
+      cur = nxt;
     }
   } else {
     // ---------------- LIF scan epilogue: thread = neuron (TMEM lane)
@@ -331,89 +340,122 @@ struct ReadoutArgs {
 __device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
 __device__ __forceinline__ float log_cr(float x) { return float(log(double(x))); }
 
+__host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
+  return (size_t(HL) * C + size_t(T) * (HL_pad / 32) + size_t(T) * C) * 4;
+}
+
 __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   extern __shared__ float rsm[];
-  float* w = rsm;                        // [HL][C]
-  float* buf = w + size_t(a.HL) * a.C;   // [T][C]: I3 -> V3 (entering state) -> dI3
-  __shared__ float logits[kMaxClasses];
-  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = a.C;
-  for (int i = tid; i < a.HL * C; i += 128) w[i] = a.w[i];
+  const int hw = a.HL_pad / 32;
+  float* w = rsm;                                                      // [HL][C]
+  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * C);   // [T][hw]
+  float* buf = reinterpret_cast<float*>(spk + size_t(a.T) * hw);       // [T][C] I3 -> V3
+  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < a.HL * C; i += 128) w[i] = __ldg(a.w + i);
+  {
+    const uint32_t* __restrict__ src = a.s_in + size_t(b) * a.T_pad * hw;
+    for (int i = tid; i < a.T * hw; i += 128) spk[i] = __ldg(src + i);
+  }
   __syncthreads();
-  const size_t hw = size_t(a.HL_pad) / 32;
-  // projection: warp w handles t = w, w+4, ...; lane c accumulates class c
+  // projection: warp w handles t = w, w+4, ...; lane c accumulates class c in the
+  // reference's ascending-k order with zero skip
+  const float bias_c = (a.bias != nullptr && lane < C) ? a.bias[lane] : 0.0f;
   for (int t = warp; t < a.T; t += 4) {
-    const uint32_t* srow = a.s_in + (size_t(b) * a.T_pad + t) * hw;
     float acc = 0.0f;
-    for (size_t wi = 0; wi < hw; ++wi) {
-      uint32_t bits = srow[wi];
+    for (int wi = 0; wi < hw; ++wi) {
+      uint32_t bits = spk[t * hw + wi];
       while (bits) {
         const int i = __ffs(bits) - 1;
         bits &= bits - 1;
-        const int k = int(wi) * 32 + i;
-        if (lane < C) acc = __fadd_rn(acc, w[k * C + lane]);
+        if (lane < C) acc = __fadd_rn(acc, w[(wi * 32 + i) * C + lane]);
       }
     }
-    if (lane < C) {
-      if (a.bias != nullptr) acc = __fadd_rn(acc, a.bias[lane]);
-      buf[t * C + lane] = acc;
-    }
+    if (lane < C) buf[t * C + lane] = (a.bias != nullptr) ? __fadd_rn(acc, bias_c) : acc;
   }
   __syncthreads();
-  if (warp == 0) {
-    const bool on = lane < C;
-    const float vb = on ? clip01(a.beta[lane]) : 0.0f;
-    float v = 0.0f, logit = 0.0f;
-    for (int t = 0; t < a.T; ++t) {
-      float I = on ? buf[t * C + lane] : 0.0f;
-      if (on) buf[t * C + lane] = v;  // keep V3 (entering state) for dbeta
-      v = __fadd_rn(__fmul_rn(v, vb), I);
-      logit = __fadd_rn(logit, v);
-      if (on && a.dbg_trace != nullptr) a.dbg_trace[(size_t(b) * a.T + t) * C + lane] = v;
-    }
-    if (on) logits[lane] = logit;
-    __syncwarp();
-    // softmax CE in the reference's sequential order (objective.hpp:53-73)
-    float mx = logits[0];
-    for (int j = 1; j < C; ++j) mx = (mx < logits[j]) ? logits[j] : mx;
-    float z = 0.0f;
-    for (int j = 0; j < C; ++j) z = __fadd_rn(z, exp_cr(__fsub_rn(logits[j], mx)));
-    const int y = a.labels[a.rows[b]];
-    if (lane == 0) {
-      const float lse = __fadd_rn(mx, log_cr(z));
-      a.loss_b[b] = __fsub_rn(lse, logits[y]);
-      int best = 0;
-      for (int j = 1; j < C; ++j)
-        if (logits[j] > logits[best]) best = j;
-      a.correct_b[b] = (best == y) ? 1 : 0;
-    }
-    float delta = 0.0f;
-    if (on) {
-      float d = __fdiv_rn(exp_cr(__fsub_rn(logit, mx)), z);
-      if (lane == y) d = __fsub_rn(d, 1.0f);
-      delta = __fmul_rn(d, a.inv_b);
-    }
-    // LI reverse scan: G_t = delta + G_{t+1} * bc ; dI3_t = G_t ; dbeta += G_t * V3_t
-    float G = 0.0f, db = 0.0f, dbias = 0.0f;
-    for (int t = a.T - 1; t >= 0; --t) {
-      G = (t == a.T - 1) ? delta : __fadd_rn(delta, __fmul_rn(G, vb));
-      if (on) {
-        db = __fadd_rn(db, __fmul_rn(G, buf[t * C + lane]));
-        dbias = __fadd_rn(dbias, G);
-        const size_t row = size_t(b) * a.T_pad + t;
-        a.d3[row * C + lane] = G;
-        __nv_bfloat16 h, m, l;
-        split3(G, h, m, l);
-        const size_t plane = size_t(a.B) * a.T_pad * 64;
-        a.d3_planes[row * 64 + lane] = h;
-        a.d3_planes[plane + row * 64 + lane] = m;
-        a.d3_planes[2 * plane + row * 64 + lane] = l;
+  if (warp != 0) return;
+  const bool on = lane < C;
+  const float vb = on ? clip01(a.beta[lane]) : 0.0f;
+  // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50)
+  float v = 0.0f, logit = 0.0f;
+  for (int t0 = 0; t0 < a.T; t0 += 8) {
+    float I[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) I[e] = (on && t0 + e < a.T) ? buf[(t0 + e) * C + lane] : 0.0f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = t0 + e;
+      if (t < a.T) {
+        if (on) buf[t * C + lane] = v;  // keep V3 (entering state) for dbeta
+        v = __fadd_rn(__fmul_rn(v, vb), I[e]);
+        logit = __fadd_rn(logit, v);
+        if (on && a.dbg_trace != nullptr) a.dbg_trace[(size_t(b) * a.T + t) * C + lane] = v;
       }
     }
-    if (on) {
-      a.dbeta_part[size_t(b) * C + lane] = db;
-      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
+  }
+  // softmax CE in the reference's sequential order (objective.hpp:53-73)
+  float mx = __shfl_sync(0xffffffffu, logit, 0);
+  for (int j = 1; j < C; ++j) {
+    const float lj = __shfl_sync(0xffffffffu, logit, j);
+    mx = (mx < lj) ? lj : mx;
+  }
+  const float ex = on ? exp_cr(__fsub_rn(logit, mx)) : 0.0f;
+  float z = 0.0f;
+  for (int j = 0; j < C; ++j) z = __fadd_rn(z, __shfl_sync(0xffffffffu, ex, j));
+  const int y = a.labels[a.rows[b]];
+  const float logit_y = __shfl_sync(0xffffffffu, logit, y);
+  // argmax, ties to the lowest index (objective.hpp:126-131)
+  float bv = on ? logit : -INFINITY;
+  int bi = on ? lane : 1 << 30;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
     }
+  }
+  if (lane == 0) {
+    a.loss_b[b] = __fsub_rn(__fadd_rn(mx, log_cr(z)), logit_y);
+    a.correct_b[b] = (bi == y) ? 1 : 0;
+  }
+  float delta = 0.0f;
+  if (on) {
+    float d = __fdiv_rn(ex, z);
+    if (lane == y) d = __fsub_rn(d, 1.0f);
+    delta = __fmul_rn(d, a.inv_b);
+  }
+  // LI reverse scan: G_t = delta + G_{t+1} * bc ; dI3_t = G_t ; dbeta += G_t * V3_t
+  float G = 0.0f, db = 0.0f, dbias = 0.0f;
+  const size_t plane = size_t(a.B) * a.T_pad * 64;
+  for (int t1 = a.T; t1 > 0; t1 -= 8) {
+    float V3[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) V3[e] = (on && t1 - 1 - e >= 0) ? buf[(t1 - 1 - e) * C + lane] : 0.0f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = t1 - 1 - e;
+      if (t >= 0) {
+        G = (t == a.T - 1) ? delta : __fadd_rn(delta, __fmul_rn(G, vb));
+        if (on) {
+          db = __fadd_rn(db, __fmul_rn(G, V3[e]));
+          dbias = __fadd_rn(dbias, G);
+          const size_t row = size_t(b) * a.T_pad + t;
+          a.d3[row * C + lane] = G;
+          __nv_bfloat16 h, m, l;
+          split3(G, h, m, l);
+          a.d3_planes[row * 64 + lane] = h;
+          a.d3_planes[plane + row * 64 + lane] = m;
+          a.d3_planes[2 * plane + row * 64 + lane] = l;
+        }
+      }
+    }
+  }
+  if (on) {
+    a.dbeta_part[size_t(b) * C + lane] = db;
+    if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
   }
 }
 
@@ -442,10 +484,9 @@ struct ScanState {
   float G, db, dbias;
 };
 
-__device__ __forceinline__ void bwd_step(const BwdArgs& a, ScanState& st, float vb, int b, int n,
-                                         int t, float dS) {
-  const size_t vi = (size_t(b) * a.T_pad + t) * a.H_pad + n;
-  const float V = a.v_in[vi];
+// One reverse step given the (prefetched) entering membrane V_t and dS_t.
+__device__ __forceinline__ void bwd_step(const BwdArgs& a, ScanState& st, float vb, size_t vi,
+                                         float V, float dS) {
   if (a.dbg_ds != nullptr) a.dbg_ds[vi] = dS;
   const float G = st.G;
   // dI_t = G (grad of the step-t input); three bf16 planes
@@ -464,20 +505,54 @@ __device__ __forceinline__ void bwd_step(const BwdArgs& a, ScanState& st, float 
   st.G = __fadd_rn(__fmul_rn(G, vb), gpre);
 }
 
+// 32 membranes of one 32-step chunk (coalesced across the warp), issued together.
+__device__ __forceinline__ void load_v_chunk(const BwdArgs& a, int b, int n, int c,
+                                             float (&v)[32]) {
+  const float* __restrict__ src = a.v_in + (size_t(b) * a.T_pad + c * 32) * a.H_pad + n;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = (c * 32 + e < a.T) ? __ldg(src + size_t(e) * a.H_pad) : 0.0f;
+}
+
 __global__ void __launch_bounds__(128) k_lif_bwd_ro(BwdArgs a) {
+  extern __shared__ float sd3[];  // this sample's dI3 [T][C]
   const int b = blockIdx.x, n = blockIdx.y * 128 + threadIdx.x;
+  {
+    const float* __restrict__ src = a.d3 + size_t(b) * a.T_pad * a.C;
+    for (int i = threadIdx.x; i < a.T * a.C; i += 128) sd3[i] = src[i];
+  }
   const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
   float w[kMaxClasses];
 #pragma unroll
   for (int c = 0; c < kMaxClasses; ++c) w[c] = (n < a.H && c < a.C) ? a.w3[n * a.C + c] : 0.0f;
+  __syncthreads();
   ScanState st{0.0f, 0.0f, 0.0f};
-  for (int t = a.T - 1; t >= 0; --t) {
-    const float* g = a.d3 + (size_t(b) * a.T_pad + t) * a.C;
-    float dS = 0.0f;
+  const int nch = (a.T + 31) / 32;
+  float vn[32];
+  load_v_chunk(a, b, n, nch - 1, vn);
+  for (int c = nch - 1; c >= 0; --c) {
+    float vr[32];
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c)
-      if (c < a.C) dS = __fadd_rn(dS, __fmul_rn(g[c], w[c]));
-    bwd_step(a, st, vb, b, n, t, dS);
+    for (int e = 0; e < 32; ++e) vr[e] = vn[e];
+    if (c > 0) load_v_chunk(a, b, n, c - 1, vn);
+    // dS_t = sum_c dI3[t][c] * W3[n][c] in ascending c (matmul_nt, ops.hpp:178-199)
+    float ds[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      const int t = c * 32 + e;
+      float acc = 0.0f;
+      if (t < a.T) {
+        const float* g = sd3 + t * a.C;
+#pragma unroll
+        for (int k = 0; k < kMaxClasses; ++k)
+          if (k < a.C) acc = __fadd_rn(acc, __fmul_rn(g[k], w[k]));
+      }
+      ds[e] = acc;
+    }
+#pragma unroll
+    for (int e = 31; e >= 0; --e) {
+      const int t = c * 32 + e;
+      if (t < a.T) bwd_step(a, st, vb, (size_t(b) * a.T_pad + t) * a.H_pad + n, vr[e], ds[e]);
+    }
   }
   if (n < a.H) {
     a.dbeta_part[size_t(b) * a.H + n] = st.db;
@@ -588,18 +663,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int n = nt * 128 + warp * 32 + lane;
     const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
     ScanState st{0.0f, 0.0f, 0.0f};
+    const int nch = (a.T + 31) / 32;   // 32-step chunks holding valid steps
+    float vn[32];
+    load_v_chunk(a, b, n, nch - 1, vn);
     for (int j = 0; j < a.NT; ++j) {
       const int tt = a.NT - 1 - j, buf = j & 1;
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
       for (int c = a.TT / 32 - 1; c >= 0; --c) {
+        const int gc = tt * (a.TT / 32) + c;  // global chunk index
+        if (gc >= nch) continue;
+        float vr[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) vr[e] = vn[e];
+        if (gc > 0) load_v_chunk(a, b, n, gc - 1, vn);
         uint32_t r[32];
         tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + buf * a.TT + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
         for (int e = 31; e >= 0; --e) {
-          const int t = tt * a.TT + c * 32 + e;
-          if (t < a.T) bwd_step(a, st, vb, b, n, t, __uint_as_float(r[e]));
+          const int t = gc * 32 + e;
+          if (t < a.T)
+            bwd_step(a, st, vb, (size_t(b) * a.T_pad + t) * a.H_pad + n, vr[e], __uint_as_float(r[e]));
         }
       }
       tc_fence_before();
@@ -722,30 +807,38 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
     __syncwarp();
   } else if (warp < 4) {
-    // A producers: tile [128 k-rows][64 time cols], K-major SW128
+    // A producers: tile [128 k-rows][64 time cols], K-major SW128.  The loads of
+    // stage it+1 are issued before waiting for stage it's slot.
     const int tid = threadIdx.x;
     const int k = mt * 128 + tid;  // this thread's A row
-    for (int it = 0; it < total; ++it) {
-      const int s = it % kWgStages, ph = (it / kWgStages) & 1;
+    const bool in_row = a.kind != 0 || k < a.x_row_stride;
+    auto fetch = [&](int it) -> uint64_t {
+      if (it >= total || !in_row) return 0;
       const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
-      mbar_wait(&empty[s], ph ^ 1);
-      const uint32_t A = smem_u32(smem + s * stage_bytes);
       if (a.kind == 0) {
         const uint8_t* src = a.x + (size_t(a.rows[bb]) * (a.T_pad / 8) + tq * 8) * a.x_row_stride + k;
-        const bool in_row = k < a.x_row_stride;
+        uint64_t v = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          st_shared_v4(A + sw128_off(tid, j),
-                       expand_bits_msb(in_row ? src[size_t(j) * a.x_row_stride] : 0u));
-      } else {
-        const uint64_t w = *reinterpret_cast<const uint64_t*>(
-            a.s_tp + size_t(k) * (size_t(a.B) * a.T_pad / 32) + size_t(bb) * (a.T_pad / 32) + tq * 2);
+        for (int j = 0; j < 8; ++j) v |= uint64_t(__ldg(src + size_t(j) * a.x_row_stride)) << (8 * j);
+        return v;
+      }
+      return __ldg(reinterpret_cast<const unsigned long long*>(
+          a.s_tp + size_t(k) * (size_t(a.B) * a.T_pad / 32) + size_t(bb) * (a.T_pad / 32) + tq * 2));
+    };
+    uint64_t cur = fetch(0);
+    for (int it = 0; it < total; ++it) {
+      const int s = it % kWgStages, ph = (it / kWgStages) & 1;
+      const uint64_t nxt = fetch(it + 1);
+      mbar_wait(&empty[s], ph ^ 1);
+      const uint32_t A = smem_u32(smem + s * stage_bytes);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          st_shared_v4(A + sw128_off(tid, j), expand_bits_lsb(uint32_t(w >> (8 * j)) & 0xFFu));
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t byte = uint32_t(cur >> (8 * j)) & 0xFFu;
+        st_shared_v4(A + sw128_off(tid, j), a.kind == 0 ? expand_bits_msb(byte) : expand_bits_lsb(byte));
       }
       fence_async_smem();
       mbar_arrive(&full[s]);
+      cur = nxt;
     }
     // epilogue: thread = output row k, n_tile columns
     mbar_wait(&acc_full[0], 0);
@@ -800,33 +893,99 @@ struct ReduceArgs {
   int M_pad[kMaxLayers], N_pad[kMaxLayers], splits[kMaxLayers];
   const float* dbeta_part[kMaxLayers];  // per cell j: [B][N]
   const float* dbias_part[kMaxLayers];  // per Linear j: [B][N]
+  const int32_t* vec_index;             // flat indices of the beta / bias entries
+  int n_vec;
   const float* params;                  // for the clip mask
-  float* grads;
+  float* grads;                         // [n_params] then loss sum, hits
+  const float* loss_b;                  // [B]
+  const int32_t* correct_b;             // [B]
+  int64_t* step;
+  int update;
   int B;
+  int w_blocks;                         // blocks [0, w_blocks) handle W entries
 };
 
-__global__ void k_reduce(ReduceArgs a) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.n_params) return;
+__device__ __forceinline__ int find_entry(const Entry* en, int n, int64_t i) {
   int e = 0;
-  while (e + 1 < a.n_entries && a.entries[e + 1].offset <= i) ++e;
-  const Entry en = a.entries[e];
-  const int64_t li = i - en.offset;
-  const int j = en.layer;
-  float g = 0.0f;
-  if (en.kind == kEntryW) {
+  while (e + 1 < n && en[e + 1].offset <= i) ++e;
+  return e;
+}
+
+// Blocks [0, w_blocks): one thread per flat index, W entries only -- fixed-order
+// sum of the split-K partials.  Next blocks: one warp per beta/bias element --
+// lanes take strided samples, then a fixed-shape tree (deterministic).  Last
+// block: loss sum in batch order (objective.hpp:57-72) + hits, step counter.
+__global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
+  const int tid = threadIdx.x;
+  if (int(blockIdx.x) < a.w_blocks) {
+    const int64_t i = int64_t(blockIdx.x) * 256 + tid;
+    if (i >= a.n_params) return;
+    const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
+    if (en.kind != kEntryW) return;
+    const int64_t li = i - en.offset;
+    const int j = en.layer;
     const int64_t k = li / en.cols, n = li % en.cols;
-    const float* p = a.partial[j] + k * a.N_pad[j] + n;
+    const float* __restrict__ p = a.partial[j] + k * a.N_pad[j] + n;
     const int64_t sstride = int64_t(a.M_pad[j]) * a.N_pad[j];
-    for (int s = 0; s < a.splits[j]; ++s) g = __fadd_rn(g, p[s * sstride]);
-  } else if (en.kind == kEntryB) {
-    for (int b = 0; b < a.B; ++b) g = __fadd_rn(g, a.dbias_part[j][int64_t(b) * en.cols + li]);
-  } else {
-    for (int b = 0; b < a.B; ++b) g = __fadd_rn(g, a.dbeta_part[j][int64_t(b) * en.cols + li]);
-    const float beta = a.params[i];
-    if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
+    const int S = a.splits[j];
+    float g = 0.0f;
+    int s = 0;
+    for (; s + 4 <= S; s += 4) {
+      const float x0 = __ldg(p + s * sstride), x1 = __ldg(p + (s + 1) * sstride);
+      const float x2 = __ldg(p + (s + 2) * sstride), x3 = __ldg(p + (s + 3) * sstride);
+      g = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(g, x0), x1), x2), x3);
+    }
+    for (; s < S; ++s) g = __fadd_rn(g, __ldg(p + s * sstride));
+    a.grads[i] = g;
+    return;
   }
-  a.grads[i] = g;
+  const int vb_blocks = (a.n_vec + 7) / 8;
+  if (int(blockIdx.x) < a.w_blocks + vb_blocks) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int v = (int(blockIdx.x) - a.w_blocks) * 8 + warp;
+    if (v >= a.n_vec) return;
+    const int64_t i = a.vec_index[v];
+    const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
+    const int64_t li = i - en.offset;
+    const float* __restrict__ src =
+        (en.kind == kEntryB ? a.dbias_part[en.layer] : a.dbeta_part[en.layer]) + li;
+    float g = 0.0f;
+    for (int b = lane; b < a.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
+    if (lane == 0) {
+      if (en.kind == kEntryBeta) {
+        const float beta = a.params[i];
+        if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
+      }
+      a.grads[i] = g;
+    }
+    return;
+  }
+  // loss / hits / step
+  __shared__ float sl[1024];
+  __shared__ int sc[1024];
+  float loss = 0.0f;
+  int hits = 0;
+  for (int b0 = 0; b0 < a.B; b0 += 1024) {
+    const int nb = min(1024, a.B - b0);
+    __syncthreads();
+    for (int i = tid; i < nb; i += 256) {
+      sl[i] = a.loss_b[b0 + i];
+      sc[i] = a.correct_b[b0 + i];
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int i = 0; i < nb; ++i) {
+        loss = __fadd_rn(loss, sl[i]);
+        hits += sc[i];
+      }
+  }
+  if (tid == 0) {
+    a.grads[a.n_params] = loss;
+    a.grads[a.n_params + 1] = float(hits);
+    if (a.update) *a.step += 1;
+  }
 }
 
 struct PlaneTarget {
@@ -843,19 +1002,27 @@ struct AdamArgs {
   float* params;
   float* m;
   float* v;
-  const float* grads;
+  const float* grads;        // [n_params] + loss sum + hits (after the allreduce)
   const float* bc;           // [2 * max_steps]: bc1, bc2 per step (host powf)
-  const int64_t* step;       // device step counter (before this update)
+  const int64_t* step;       // device step counter (already advanced by k_reduce)
   float lr, b1, b2, eps, omb1, omb2;
   int update;                // 0: only refresh planes (after set_params)
+  int B_global;
+  float* loss_out;
+  double* acc_out;
 };
 
-__global__ void k_adam(AdamArgs a) {
+__global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a.update && i == 0) {
+    // StepResult{loss, accuracy} (optimize.hpp:143-147, :193-196)
+    *a.loss_out = __fdiv_rn(a.grads[a.n_params], float(a.B_global));
+    *a.acc_out = double(a.grads[a.n_params + 1]) / double(a.B_global);
+  }
   if (i >= a.n_params) return;
   float p = a.params[i];
   if (a.update) {
-    const int64_t s = *a.step;  // steps done so far; this update is s+1
+    const int64_t s = *a.step - 1;  // bias correction of step s+1 (optimize.hpp:95-97)
     const float bc1 = a.bc[2 * s], bc2 = a.bc[2 * s + 1];
     const float g = a.grads[i];
     const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(a.omb1, g));
@@ -867,9 +1034,7 @@ __global__ void k_adam(AdamArgs a) {
     a.v[i] = v;
     a.params[i] = p;
   }
-  int e = 0;
-  while (e + 1 < a.n_entries && a.entries[e + 1].offset <= i) ++e;
-  const Entry en = a.entries[e];
+  const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
   if (en.kind != kEntryW) return;
   const PlaneTarget pt = a.planes[en.layer];
   if (pt.wt == nullptr && pt.wb == nullptr) return;
@@ -938,21 +1103,6 @@ __global__ void k_synth(SynthArgs a) {
     }
   }
   a.x[gid] = byte;
-}
-
-// Local loss sum in batch order (objective.hpp:57-72: loss += lse - row[y]) and
-// hit count, appended to the gradient buffer so one allreduce carries both.
-__global__ void k_loss_partial(const float* loss_b, const int32_t* correct_b, int B,
-                               float* tail) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  float loss = 0.0f;
-  int hits = 0;
-  for (int b = 0; b < B; ++b) {
-    loss = __fadd_rn(loss, loss_b[b]);
-    hits += correct_b[b];
-  }
-  tail[0] = loss;
-  tail[1] = float(hits);
 }
 
 // StepResult{loss / B_global, hits / B_global}; advances the step counter.
