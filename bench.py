@@ -120,9 +120,7 @@ def algorithmic(name: str, w: dict, n_params: int):
         return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
     if base == "wgrad":              # dW = A^T dI
         return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
-    if base == "lif_bwd_gemm":       # dS = dI_next W_next^T
-        return "tensor", 2.0 * B * T * dims[l + 1] * dims[l + 2]
-    if base == "lif_bwd_ro":         # LIF bwd 12 B / neuron-step
+    if base == "lif_bwd":            # LIF reverse scan: 12 B / neuron-step
         return "hbm", 12.0 * B * T * dims[l + 1]
     if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element
         return "hbm", 8.0 * B * T * C

@@ -4,7 +4,7 @@
 // Step schedule (all on one stream, captured once into a CUDA graph):
 //   k_lif_fwd x L          GEMM (tcgen05, TMEM) + LIF scan per (sample, 128 neurons)
 //   k_readout              readout projection + LI + integral CE + LI reverse scan
-//   k_lif_bwd_ro / _gemm   dS (CUDA-core for the readout, tcgen05 otherwise) + LIF reverse scan
+//   k_lif_bwd              dS = dI_next W_next^T on tcgen05 + LIF reverse scan (TMEM epilogue)
 //   k_wgrad x (L+1)        dW = A^T dI on tcgen05, split-K partials
 //   k_reduce (+loss, step), [ncclAllReduce], k_adam (+StepResult)
 #include <cuda.h>
@@ -190,7 +190,7 @@ struct snn_engine {
   DevBuf<uint32_t> s_np[SNN_MAX_HIDDEN], s_tp[SNN_MAX_HIDDEN];
   DevBuf<__nv_bfloat16> di[kMaxLayers];  // per Linear j: dI of its output
   DevBuf<float> dbeta[kMaxLayers], dbias[kMaxLayers];
-  DevBuf<float> d3, loss_b;
+  DevBuf<float> loss_b;
   DevBuf<int32_t> correct_b;
   DevBuf<float> partial[kMaxLayers];
   DevBuf<int32_t> vec_index;
@@ -318,8 +318,8 @@ struct snn_engine {
     grow_bc(1 << 20);
     for (int j = 0; j < L; ++j) {
       wt[j].alloc(size_t(3) * N_pad[j] * K_pad[j]);
-      if (j >= 1) wb[j].alloc(size_t(3) * K_pad[j] * N_pad[j]);
     }
+    for (int j = 1; j <= L; ++j) wb[j].alloc(size_t(3) * K_pad[j] * N_pad[j]);
     const size_t rows = size_t(B) * T_pad;
     for (int l = 0; l < L; ++l) {
       V[l].alloc(rows * H_pad[l], false);
@@ -332,7 +332,6 @@ struct snn_engine {
       if (net.bias) dbias[j].alloc(size_t(B) * N[j]);
       partial[j].alloc(size_t(splits_w[j]) * M_pad_w[j] * N_pad[j], false);
     }
-    d3.alloc(rows * C);
     loss_b.alloc(B);
     correct_b.alloc(B);
     result_loss.alloc(1);
@@ -344,21 +343,21 @@ struct snn_engine {
     // tensor maps
     for (int j = 0; j < L; ++j) {
       tm_wt[j] = make_map(wt[j].p, uint64_t(3) * N_pad[j], K_pad[j], 128);
-      if (j >= 1) tm_wb[j] = make_map(wb[j].p, uint64_t(3) * K_pad[j], N_pad[j], 128);
     }
+    for (int j = 1; j <= L; ++j) tm_wb[j] = make_map(wb[j].p, uint64_t(3) * K_pad[j], N_pad[j], 128);
+    // dI planes [3][N_pad][B*T_pad]: MN-major boxes for the backward GEMM, K-major
+    // boxes (rows = output neurons) for the weight-gradient GEMM
     for (int j = 0; j <= L; ++j) {
-      tm_di_k[j] = make_map(di[j].p, uint64_t(3) * rows, N_pad[j], TT);
-      tm_di_w[j] = make_map(di[j].p, uint64_t(3) * rows, N_pad[j], 64);
+      tm_di_k[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 64);
+      tm_di_w[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, uint32_t(n_tile_w[j]));
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(fwd_smem_bytes(TT))));
-    CK(cudaFuncSetAttribute(k_lif_bwd_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(bwd_smem_bytes(TT))));
+    CK(cudaFuncSetAttribute(k_lif_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(wg_smem_bytes(128))));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(200 * 1024)));
-    CK(cudaFuncSetAttribute(k_lif_bwd_ro, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
     {
       std::vector<int32_t> vi;
@@ -436,7 +435,7 @@ struct snn_engine {
     a.n_params = int64_t(n_params);
     for (int j = 0; j <= L; ++j) {
       a.planes[j].wt = j < L ? wt[j].p : nullptr;
-      a.planes[j].wb = (j >= 1 && j < L) ? wb[j].p : nullptr;
+      a.planes[j].wb = j >= 1 ? wb[j].p : nullptr;
       a.planes[j].K_pad = K_pad[j];
       a.planes[j].N_pad = N_pad[j];
     }
@@ -575,7 +574,6 @@ struct snn_engine {
       r.w = params.p + entry_of(kEntryW, L).offset;
       r.bias = net.bias ? params.p + entry_of(kEntryB, L).offset : nullptr;
       r.beta = params.p + entry_of(kEntryBeta, L).offset;
-      r.d3 = d3.p;
       r.d3_planes = di[L].p;
       r.loss_b = loss_b.p;
       r.correct_b = correct_b.p;
@@ -588,28 +586,22 @@ struct snn_engine {
       k_readout<<<B, 128, smem, stream>>>(r);
       mark(evs, "readout", -1);
     }
-    // hidden backward, top-down
+    // hidden backward, top-down: dS on tcgen05 (readout-fed layer: K = classes)
     for (int l = L - 1; l >= 0; --l) {
       BwdArgs bw{};
       bw.v_in = V[l].p;
       bw.beta = params.p + entry_of(kEntryBeta, l).offset;
-      bw.d3 = d3.p;
-      bw.w3 = params.p + entry_of(kEntryW, L).offset;
       bw.di_planes = di[l].p;
       bw.dbeta_part = dbeta[l].p;
       bw.dbias_part = net.bias ? dbias[l].p : nullptr;
       bw.dbg_ds = debug ? dbg_ds[l].p : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
-      bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.C = C; bw.act = net.activation;
+      bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
+      bw.stages = std::min(2, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
-      if (l == L - 1) {
-        k_lif_bwd_ro<<<dim3(B, H_pad[l] / 128), 128, size_t(T) * C * 4, stream>>>(bw);
-        mark(evs, "lif_bwd_ro", l);
-      } else {
-        k_lif_bwd_gemm<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT), stream>>>(
-            tm_wb[l + 1], tm_di_k[l + 1], bw);
-        mark(evs, "lif_bwd_gemm", l);
-      }
+      k_lif_bwd<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT, bw.stages), stream>>>(
+          tm_wb[l + 1], tm_di_k[l + 1], bw);
+      mark(evs, "lif_bwd", l);
     }
     // weight gradients
     for (int j = 0; j <= L; ++j) {

@@ -326,8 +326,7 @@ struct ReadoutArgs {
   const float* w;           // readout W [HL][C] f32 (master)
   const float* bias;        // [C] or nullptr
   const float* beta;        // [C]
-  float* d3;                // dL/dI3 f32 [B][T_pad][C]
-  __nv_bfloat16* d3_planes; // [3][B*T_pad][64]
+  __nv_bfloat16* d3_planes; // [3][64][B*T_pad] (class rows, (b,t) contiguous)
   float* loss_b;            // [B] lse - logit_y
   int32_t* correct_b;       // [B]
   float* dbeta_part;        // [B][C]
@@ -339,6 +338,34 @@ struct ReadoutArgs {
 
 __device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
 __device__ __forceinline__ float log_cr(float x) { return float(log(double(x))); }
+
+// Phase 2 of the readout: write dI3 as three bf16 planes [3][64][B*T_pad]
+// (class rows, (b,t) contiguous) -- all 128 threads, 16-byte stores.
+__device__ __forceinline__ void readout_store_planes(const ReadoutArgs& a, const float* buf, int b) {
+  const int C = a.C;
+  const int chunks = (a.T + 7) / 8;
+  const size_t cols = size_t(a.B) * a.T_pad;
+  const size_t plane = size_t(64) * cols;
+  for (int u = threadIdx.x; u < C * chunks; u += blockDim.x) {
+    const int c = u / chunks, t0 = (u % chunks) * 8;
+    uint32_t hp[4], mp[4], lp[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float g0 = t0 + e < a.T ? buf[(t0 + e) * C + c] : 0.0f;
+      const float g1 = t0 + e + 1 < a.T ? buf[(t0 + e + 1) * C + c] : 0.0f;
+      __nv_bfloat16 h0, m0, l0, h1, m1, l1;
+      split3(g0, h0, m0, l0);
+      split3(g1, h1, m1, l1);
+      hp[e / 2] = uint32_t(__bfloat16_as_ushort(h0)) | (uint32_t(__bfloat16_as_ushort(h1)) << 16);
+      mp[e / 2] = uint32_t(__bfloat16_as_ushort(m0)) | (uint32_t(__bfloat16_as_ushort(m1)) << 16);
+      lp[e / 2] = uint32_t(__bfloat16_as_ushort(l0)) | (uint32_t(__bfloat16_as_ushort(l1)) << 16);
+    }
+    const size_t off = size_t(c) * cols + size_t(b) * a.T_pad + t0;
+    *reinterpret_cast<uint4*>(a.d3_planes + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+    *reinterpret_cast<uint4*>(a.d3_planes + plane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
+    *reinterpret_cast<uint4*>(a.d3_planes + 2 * plane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+  }
+}
 
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
   return (size_t(HL) * C + size_t(T) * (HL_pad / 32) + size_t(T) * C) * 4;
@@ -374,7 +401,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     if (lane < C) buf[t * C + lane] = (a.bias != nullptr) ? __fadd_rn(acc, bias_c) : acc;
   }
   __syncthreads();
-  if (warp != 0) return;
+  if (warp == 0) {
   const bool on = lane < C;
   const float vb = on ? clip01(a.beta[lane]) : 0.0f;
   // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50)
@@ -429,7 +456,6 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   }
   // LI reverse scan: G_t = delta + G_{t+1} * bc ; dI3_t = G_t ; dbeta += G_t * V3_t
   float G = 0.0f, db = 0.0f, dbias = 0.0f;
-  const size_t plane = size_t(a.B) * a.T_pad * 64;
   for (int t1 = a.T; t1 > 0; t1 -= 8) {
     float V3[8];
 #pragma unroll
@@ -439,17 +465,9 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
       const int t = t1 - 1 - e;
       if (t >= 0) {
         G = (t == a.T - 1) ? delta : __fadd_rn(delta, __fmul_rn(G, vb));
-        if (on) {
-          db = __fadd_rn(db, __fmul_rn(G, V3[e]));
-          dbias = __fadd_rn(dbias, G);
-          const size_t row = size_t(b) * a.T_pad + t;
-          a.d3[row * C + lane] = G;
-          __nv_bfloat16 h, m, l;
-          split3(G, h, m, l);
-          a.d3_planes[row * 64 + lane] = h;
-          a.d3_planes[plane + row * 64 + lane] = m;
-          a.d3_planes[2 * plane + row * 64 + lane] = l;
-        }
+        db = __fadd_rn(db, __fmul_rn(G, V3[e]));
+        dbias = __fadd_rn(dbias, G);
+        if (on) buf[t * C + lane] = G;
       }
     }
   }
@@ -457,55 +475,55 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     a.dbeta_part[size_t(b) * C + lane] = db;
     if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
   }
+  }  // warp 0
+  __syncthreads();
+  readout_store_planes(a, buf, b);
 }
 
 // ============================================================================
-// K3  LIF reverse scan (App. A.2):
-//   dI_t = G ; ds = dS_t - theta*G ; G = bc*G + g(V_t - theta)*ds ; dbeta += G_{t+1} V_t
-// Variant "ro": dS comes from the readout, dS_t[n] = sum_c dI3[t][c] W3[n][c]
-// computed here in the reference's order (matmul_nt, ops.hpp:178-199).
-// Variant "gemm": dS^T[n][t] = sum_k W[n][k] dI_next[t][k] on tcgen05 (6 plane
-// products), scan epilogue from TMEM.
+// K3  k_lif_bwd: LIF reverse scan (App. A.2) with dS from the tensor core.
+//   dS^T[n][t] = sum_k Wb[n][k] dI_next^T[k][t]  (tcgen05, 6 bf16 plane products
+//   ~ fp32), for the readout-fed layer k = classes (dI3 planes from k_readout).
+//   Then per neuron (TMEM lane), t descending:
+//     dI_t = G ; ds = dS_t - theta*G ; G = bc*G + g(V_t - theta)*ds ; dbeta += G V_t
+// The scan runs in 32-step chunks split into three phases: surrogates (independent),
+// the recurrence (short dependent chain), plane split + 64-byte vector stores.
+// grid (B, H_pad/128); block 192: w0-3 scan, w4 TMA, w5 MMA.
 // ============================================================================
 struct BwdArgs {
   const float* v_in;           // V_l [B][T_pad][H_pad]
   const float* beta;           // [H]
-  const float* d3;             // ro: dI3 [B][T_pad][C]
-  const float* w3;             // ro: W3 [H][C]
-  __nv_bfloat16* di_planes;    // out: dI_l planes [3][B*T_pad][H_pad]
+  __nv_bfloat16* di_planes;    // out: dI_l planes [3][H_pad][B*T_pad]
   float* dbeta_part;           // [B][H]
   float* dbias_part;           // [B][H] or nullptr
   float* dbg_ds;               // optional [B][T_pad][H_pad]
-  int B, T, T_pad, TT, NT, K_pad, H, H_pad, C, act;
+  int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
   float theta, slope, aux;
 };
 
-struct ScanState {
-  float G, db, dbias;
-};
-
-// One reverse step given the (prefetched) entering membrane V_t and dS_t.
-__device__ __forceinline__ void bwd_step(const BwdArgs& a, ScanState& st, float vb, size_t vi,
-                                         float V, float dS) {
-  if (a.dbg_ds != nullptr) a.dbg_ds[vi] = dS;
-  const float G = st.G;
-  // dI_t = G (grad of the step-t input); three bf16 planes
-  __nv_bfloat16 h, m, l;
-  split3(G, h, m, l);
-  const size_t plane = size_t(a.B) * a.T_pad * a.H_pad;
-  a.di_planes[vi] = h;
-  a.di_planes[plane + vi] = m;
-  a.di_planes[2 * plane + vi] = l;
-  st.dbias = __fadd_rn(st.dbias, G);
-  st.db = __fadd_rn(st.db, __fmul_rn(G, V));
-  const float rg = -G;
-  const float gs = __fadd_rn(dS, __fmul_rn(rg, a.theta));
-  const float pre = __fadd_rn(V, -a.theta);
-  const float gpre = __fmul_rn(gs, surrogate(a.act, a.slope, a.aux, pre));
-  st.G = __fadd_rn(__fmul_rn(G, vb), gpre);
+// Surrogate with divisions replaced by correctly rounded reciprocals / exact
+// halvings -- bit-identical to the divisions of surrogate.hpp.
+__device__ __forceinline__ float surrogate_fast(int act, float k, float aux, float x) {
+  switch (act) {
+    case 1: {
+      const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
+      return __frcp_rn(__fmul_rn(d, d));
+    }
+    case 2: {
+      const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
+      return 0.0f < r ? r : 0.0f;
+    }
+    case 3: {
+      const float u = __fmul_rn(__fmul_rn(__fmul_rn(3.14159265358979f, k), x), 0.5f);
+      return __frcp_rn(__fadd_rn(1.0f, __fmul_rn(u, u)));
+    }
+    case 4:
+      return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
+    default:
+      return 1.0f;
+  }
 }
 
-// 32 membranes of one 32-step chunk (coalesced across the warp), issued together.
 __device__ __forceinline__ void load_v_chunk(const BwdArgs& a, int b, int n, int c,
                                              float (&v)[32]) {
   const float* __restrict__ src = a.v_in + (size_t(b) * a.T_pad + c * 32) * a.H_pad + n;
@@ -513,72 +531,25 @@ __device__ __forceinline__ void load_v_chunk(const BwdArgs& a, int b, int n, int
   for (int e = 0; e < 32; ++e) v[e] = (c * 32 + e < a.T) ? __ldg(src + size_t(e) * a.H_pad) : 0.0f;
 }
 
-__global__ void __launch_bounds__(128) k_lif_bwd_ro(BwdArgs a) {
-  extern __shared__ float sd3[];  // this sample's dI3 [T][C]
-  const int b = blockIdx.x, n = blockIdx.y * 128 + threadIdx.x;
-  {
-    const float* __restrict__ src = a.d3 + size_t(b) * a.T_pad * a.C;
-    for (int i = threadIdx.x; i < a.T * a.C; i += 128) sd3[i] = src[i];
-  }
-  const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
-  float w[kMaxClasses];
-#pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) w[c] = (n < a.H && c < a.C) ? a.w3[n * a.C + c] : 0.0f;
-  __syncthreads();
-  ScanState st{0.0f, 0.0f, 0.0f};
-  const int nch = (a.T + 31) / 32;
-  float vn[32];
-  load_v_chunk(a, b, n, nch - 1, vn);
-  for (int c = nch - 1; c >= 0; --c) {
-    float vr[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) vr[e] = vn[e];
-    if (c > 0) load_v_chunk(a, b, n, c - 1, vn);
-    // dS_t = sum_c dI3[t][c] * W3[n][c] in ascending c (matmul_nt, ops.hpp:178-199)
-    float ds[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      const int t = c * 32 + e;
-      float acc = 0.0f;
-      if (t < a.T) {
-        const float* g = sd3 + t * a.C;
-#pragma unroll
-        for (int k = 0; k < kMaxClasses; ++k)
-          if (k < a.C) acc = __fadd_rn(acc, __fmul_rn(g[k], w[k]));
-      }
-      ds[e] = acc;
-    }
-#pragma unroll
-    for (int e = 31; e >= 0; --e) {
-      const int t = c * 32 + e;
-      if (t < a.T) bwd_step(a, st, vb, (size_t(b) * a.T_pad + t) * a.H_pad + n, vr[e], ds[e]);
-    }
-  }
-  if (n < a.H) {
-    a.dbeta_part[size_t(b) * a.H + n] = st.db;
-    if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * a.H + n] = st.dbias;
-  }
-}
-
-constexpr int kBwdStages = 2;
-constexpr int kBwdThreads = 192;  // w0-3 scan, w4 TMA, w5 MMA
+constexpr int kBwdThreads = 192;
 __host__ __device__ constexpr uint32_t bwd_stage_bytes(int TT) {
   return 3 * kPlaneTile + 3 * uint32_t(TT) * 128u;
 }
-__host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT) {
-  return kBwdStages * bwd_stage_bytes(TT) + 1024 + 256;
+__host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
+  return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256;
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
-    k_lif_bwd_gemm(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
-                   BwdArgs a) {
+    k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
+              BwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  const int S = a.stages;
   const uint32_t stage_bytes = bwd_stage_bytes(a.TT);
-  const uint32_t btile = uint32_t(a.TT) * 128u;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBwdStages * stage_bytes);
-  uint64_t* empty = full + kBwdStages;
-  uint64_t* acc_full = empty + kBwdStages;
+  const uint32_t btile = uint32_t(a.TT) * 128u;  // one plane: 64 k-rows x TT t (MN-major)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -589,7 +560,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tmem_cols = (a.TT >= 128) ? 256u : 128u;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kBwdStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -606,14 +577,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int rows_total = a.B * a.T_pad;
+  const int cols_total = a.B * a.T_pad;
 
   if (warp == 4) {
     if (elect_one()) {
       tma_prefetch(&tm_w);
       tma_prefetch(&tm_di);
       for (int it = 0; it < total; ++it) {
-        const int s = it % kBwdStages, ph = (it / kBwdStages) & 1;
+        const int s = it % S, ph = (it / S) & 1;
         const int tt = a.NT - 1 - it / KB, kb = it % KB;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile + 3 * btile);
@@ -621,17 +592,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint8_t* Bt = A + 3 * kPlaneTile;
         for (int p = 0; p < 3; ++p) {
           tma_load_2d(A + p * kPlaneTile, &tm_w, &full[s], kb * 64, p * a.H_pad + nt * 128);
-          tma_load_2d(Bt + p * btile, &tm_di, &full[s], kb * 64,
-                      p * rows_total + b * a.T_pad + tt * a.TT);
+          for (int h = 0; h < a.TT / 64; ++h)
+            tma_load_2d(Bt + p * btile + h * 8192, &tm_di, &full[s],
+                        b * a.T_pad + tt * a.TT + h * 64, p * a.K_pad + kb * 64);
         }
       }
     }
     __syncwarp();
   } else if (warp == 5) {
-    const uint32_t idesc = idesc_bf16(128, a.TT, false, false);
+    // A: K-major W planes; B: MN-major dI planes (t contiguous), LBO = 64-t block
+    const uint32_t idesc = idesc_bf16(128, a.TT, false, true);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
-        const int s = it % kBwdStages, ph = (it / kBwdStages) & 1;
+        const int s = it % S, ph = (it / S) & 1;
         const int j = it / KB, kb = it % KB, buf = j & 1;
         if (kb == 0 && j >= 2) {
           mbar_wait(&acc_empty[buf], ((j - 2) >> 1) & 1);
@@ -650,7 +623,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int q = 0; q < 6; ++q) {
             const uint64_t ad = sdesc_sw128(A + pa[q] * kPlaneTile + ks * 32, 16, 1024);
-            const uint64_t bd = sdesc_sw128(Bt + pb[q] * btile + ks * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(Bt + pb[q] * btile + ks * 2048, 8192, 1024);
             umma_bf16(d, ad, bd, idesc, (kb | ks | q) != 0);
           }
         }
@@ -662,8 +635,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   } else if (warp < 4) {
     const int n = nt * 128 + warp * 32 + lane;
     const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
-    ScanState st{0.0f, 0.0f, 0.0f};
-    const int nch = (a.T + 31) / 32;   // 32-step chunks holding valid steps
+    const float theta = a.theta, ntheta = -a.theta;
+    const size_t plane = size_t(a.H_pad) * cols_total;
+    __nv_bfloat16* __restrict__ drow = a.di_planes + size_t(n) * cols_total + size_t(b) * a.T_pad;
+    float G = 0.0f, db = 0.0f, dbias = 0.0f;
+    const int nch = (a.T + 31) / 32;
     float vn[32];
     load_v_chunk(a, b, n, nch - 1, vn);
     for (int j = 0; j < a.NT; ++j) {
@@ -671,28 +647,73 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
       for (int c = a.TT / 32 - 1; c >= 0; --c) {
-        const int gc = tt * (a.TT / 32) + c;  // global chunk index
+        const int gc = tt * (a.TT / 32) + c;
         if (gc >= nch) continue;
-        float vr[32];
+        float vr[32], x[32], sg[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) vr[e] = vn[e];
         if (gc > 0) load_v_chunk(a, b, n, gc - 1, vn);
-        uint32_t r[32];
-        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + buf * a.TT + c * 32, r);
-        tmem_ld_wait();
+        {
+          uint32_t r[32];
+          tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + buf * a.TT + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r[e]);
+        }
+        const int nvalid = min(32, a.T - gc * 32);
+        if (a.dbg_ds != nullptr) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < nvalid) a.dbg_ds[(size_t(b) * a.T_pad + gc * 32 + e) * a.H_pad + n] = x[e];
+        }
+        // phase A: surrogates g(V_t - theta), independent across t
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          sg[e] = surrogate_fast(a.act, a.slope, a.aux, __fadd_rn(vr[e], ntheta));
+        // phase B: the recurrence; x[e] <- dI_t = G (grad of the step-t input)
 #pragma unroll
         for (int e = 31; e >= 0; --e) {
-          const int t = gc * 32 + e;
-          if (t < a.T)
-            bwd_step(a, st, vb, (size_t(b) * a.T_pad + t) * a.H_pad + n, vr[e], __uint_as_float(r[e]));
+          if (e < nvalid) {
+            const float g = G;
+            const float gs = __fadd_rn(x[e], __fmul_rn(-g, theta));
+            G = __fadd_rn(__fmul_rn(g, vb), __fmul_rn(gs, sg[e]));
+            x[e] = g;
+          } else {
+            x[e] = 0.0f;
+          }
+        }
+        // phase C: dbeta / dbias partial sums (t descending) and the bf16 planes
+#pragma unroll
+        for (int e = 31; e >= 0; --e) {
+          db = __fadd_rn(db, __fmul_rn(x[e], vr[e]));
+          dbias = __fadd_rn(dbias, x[e]);
+        }
+        uint32_t ph_[16], pm_[16], pl_[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          __nv_bfloat16 h0, m0, l0, h1, m1, l1;
+          split3(x[e], h0, m0, l0);
+          split3(x[e + 1], h1, m1, l1);
+          ph_[e / 2] = uint32_t(__bfloat16_as_ushort(h0)) | (uint32_t(__bfloat16_as_ushort(h1)) << 16);
+          pm_[e / 2] = uint32_t(__bfloat16_as_ushort(m0)) | (uint32_t(__bfloat16_as_ushort(m1)) << 16);
+          pl_[e / 2] = uint32_t(__bfloat16_as_ushort(l0)) | (uint32_t(__bfloat16_as_ushort(l1)) << 16);
+        }
+        uint4* dh = reinterpret_cast<uint4*>(drow + gc * 32);
+        uint4* dm = reinterpret_cast<uint4*>(drow + plane + gc * 32);
+        uint4* dl = reinterpret_cast<uint4*>(drow + 2 * plane + gc * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          dh[q] = make_uint4(ph_[4 * q], ph_[4 * q + 1], ph_[4 * q + 2], ph_[4 * q + 3]);
+          dm[q] = make_uint4(pm_[4 * q], pm_[4 * q + 1], pm_[4 * q + 2], pm_[4 * q + 3]);
+          dl[q] = make_uint4(pl_[4 * q], pl_[4 * q + 1], pl_[4 * q + 2], pl_[4 * q + 3]);
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
     }
     if (n < a.H) {
-      a.dbeta_part[size_t(b) * a.H + n] = st.db;
-      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * a.H + n] = st.dbias;
+      a.dbeta_part[size_t(b) * a.H + n] = db;
+      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * a.H + n] = dbias;
     }
   }
   __syncthreads();
@@ -714,13 +735,14 @@ struct WgradArgs {
   const uint32_t* rows;    // kind 0: [B]
   const uint32_t* s_tp;    // kind 1: time-packed spikes [K_pad][B*T_pad/32]
   float* partial;          // [splits][M_pad][N_pad]
+  // B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
   int kind, B, T_pad, M_pad, N_pad, n_tile, splits, x_row_stride;
 };
 
 constexpr int kWgStages = 3;
 constexpr int kWgThreads = 192;
 __host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile) {
-  return kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // A 16 KB + 3 planes x (n/64 boxes x 8 KB)
+  return kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // A 16 KB + 3 planes x (n_tile x 128 B)
 }
 __host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile) {
   return kWgStages * wg_stage_bytes(n_tile) + 1024 + 256;
@@ -765,8 +787,6 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int rows_total = a.B * a.T_pad;
-
   if (warp == 4) {
     if (elect_one()) {
       tma_prefetch(&tm_di);
@@ -777,14 +797,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         mbar_arrive_expect_tx(&full[s], 3 * ptile);
         uint8_t* Bp = smem + s * stage_bytes + kPlaneTile;
         for (int p = 0; p < 3; ++p)
-          for (int h = 0; h < a.n_tile / 64; ++h)
-            tma_load_2d(Bp + p * ptile + h * 8192, &tm_di, &full[s], ntile * a.n_tile + h * 64,
-                        p * rows_total + bb * a.T_pad + tq * 64);
+          tma_load_2d(Bp + p * ptile, &tm_di, &full[s], bb * a.T_pad + tq * 64,
+                      p * a.N_pad + ntile * a.n_tile);
       }
     }
     __syncwarp();
   } else if (warp == 5) {
-    const uint32_t idesc = idesc_bf16(128, a.n_tile, false, true);
+    const uint32_t idesc = idesc_bf16(128, a.n_tile, false, false);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
         const int s = it % kWgStages, ph = (it / kWgStages) & 1;
@@ -797,7 +816,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
           const uint64_t ad = sdesc_sw128(A + ks * 32, 16, 1024);
 #pragma unroll
           for (int p = 2; p >= 0; --p) {
-            const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 2048, 8192, 1024);
+            const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
             umma_bf16(tmem, ad, bd, idesc, (it | ks | (2 - p)) != 0);
           }
         }
