@@ -215,6 +215,13 @@ struct snn_engine {
   void* comm_handle = nullptr;
   int rank = 0, world = 1;
   bool planes_dirty = true;
+  // pipeline depths (smem per CTA decides how many CTAs share an SM)
+  int fwd_stages = env_int("SNN_FWD_STAGES", 1);
+  int bwd_stages = env_int("SNN_BWD_STAGES", 1);
+  static int env_int(const char* k, int d) {
+    const char* v = std::getenv(k);
+    return (v && *v) ? std::max(1, std::atoi(v)) : d;
+  }
 
   ~snn_engine() {
     if (device >= 0) cudaSetDevice(device);
@@ -352,7 +359,7 @@ struct snn_engine {
       tm_di_w[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, uint32_t(n_tile_w[j]));
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(fwd_smem_bytes(TT))));
+                            int(fwd_smem_bytes(TT, kFwdStagesMax))));
     CK(cudaFuncSetAttribute(k_lif_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -562,7 +569,9 @@ struct snn_engine {
       f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
       f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
       f.theta = net.threshold;
-      k_lif_fwd<<<dim3(B, H_pad[l] / 128), kFwdThreads, fwd_smem_bytes(TT), stream>>>(tm_wt[l], f);
+      f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
+      k_lif_fwd<<<dim3(B, H_pad[l] / 128), kFwdThreads, fwd_smem_bytes(TT, f.stages), stream>>>(
+          tm_wt[l], f);
       mark(evs, "lif_fwd", l);
     }
     // readout + loss + LI backward
@@ -597,7 +606,7 @@ struct snn_engine {
       bw.dbg_ds = debug ? dbg_ds[l].p : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
-      bw.stages = std::min(2, NT * (N_pad[l + 1] / 64));
+      bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
       k_lif_bwd<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT, bw.stages), stream>>>(
           tm_wb[l + 1], tm_di_k[l + 1], bw);

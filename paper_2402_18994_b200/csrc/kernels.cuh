@@ -120,29 +120,34 @@ struct FwdArgs {
   uint32_t* s_np;         // [B][T_pad][H_pad/32]
   uint32_t* s_tp;         // [H_pad][B*T_pad/32]
   float* dbg_i;           // optional [B][T_pad][H_pad] raw projection
-  int B, T, T_pad, TT, NT, K_pad, H, H_pad, in_kind;
+  int B, T, T_pad, TT, NT, K_pad, H, H_pad, in_kind, stages;
   float theta;
 };
 
-constexpr int kFwdStages = 3;
+constexpr int kFwdStagesMax = 3;
 constexpr int kFwdThreads = 320;
 constexpr uint32_t kPlaneTile = 128 * 128;  // 128 rows x 64 bf16 = 16 KB
 
 __host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT) {
   return 3 * kPlaneTile + uint32_t(TT) * 128u;
 }
-__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT) {
-  return kFwdStages * fwd_stage_bytes(TT) + 1024 + 256;
+__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int stages) {
+  return uint32_t(stages) * fwd_stage_bytes(TT) + 1024 + 256;
+}
+// TMEM columns: one TT-wide accumulator, doubled when several t-tiles pipeline.
+__host__ __device__ constexpr uint32_t acc_cols(int TT, int NT) {
+  return NT > 1 ? (TT >= 128 ? 256u : 128u) : (TT >= 128 ? 128u : 64u);
 }
 
-__global__ void __launch_bounds__(kFwdThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 2)
     k_lif_fwd(const __grid_constant__ CUtensorMap tm_w, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const uint32_t stage_bytes = fwd_stage_bytes(a.TT);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kFwdStages * stage_bytes);
-  uint64_t* empty = full + kFwdStages;
-  uint64_t* acc_full = empty + kFwdStages;
+  const int S = a.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -150,10 +155,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int b = blockIdx.x, nt = blockIdx.y;
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
-  const uint32_t tmem_cols = (a.TT >= 128) ? 256u : 128u;  // 2 accumulator buffers
+  const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
+  const int nbuf = a.NT > 1 ? 2 : 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kFwdStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1 + 128);
       mbar_init(&empty[s], 1);
     }
@@ -164,7 +170,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0) {
-    if (tmem_cols == 256) tmem_alloc<256>(tmem_slot); else tmem_alloc<128>(tmem_slot);
+    if (tmem_cols == 256) tmem_alloc<256>(tmem_slot);
+    else if (tmem_cols == 128) tmem_alloc<128>(tmem_slot);
+    else tmem_alloc<64>(tmem_slot);
   }
   tc_fence_before();
   __syncthreads();
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (elect_one()) {
       tma_prefetch(&tm_w);
       for (int it = 0; it < total; ++it) {
-        const int s = it % kFwdStages, ph = (it / kFwdStages) & 1, kb = it % KB;
+        const int s = it % S, ph = (it / S) & 1, kb = it % KB;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile);
         uint8_t* A = smem + s * stage_bytes;
@@ -190,10 +198,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t idesc = idesc_bf16(128, a.TT, false, false);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
-        const int s = it % kFwdStages, ph = (it / kFwdStages) & 1;
-        const int tt = it / KB, kb = it % KB, buf = tt & 1;
-        if (kb == 0 && tt >= 2) {
-          mbar_wait(&acc_empty[buf], ((tt - 2) >> 1) & 1);
+        const int s = it % S, ph = (it / S) & 1;
+        const int tt = it / KB, kb = it % KB, buf = tt % nbuf;
+        if (kb == 0 && tt >= nbuf) {
+          mbar_wait(&acc_empty[buf], ((tt - nbuf) / nbuf) & 1);
           tc_fence_after();
         }
         mbar_wait(&full[s], ph);
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     };
     uint64_t cur = fetch(0);
     for (int it = 0; it < total; ++it) {
-      const int s = it % kFwdStages, ph = (it / kFwdStages) & 1;
+      const int s = it % S, ph = (it / S) & 1;
       const uint64_t nxt = fetch(it + 1);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t Bt = smem_u32(smem + s * stage_bytes + 3 * kPlaneTile);
@@ -269,8 +277,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const size_t tp_words = size_t(a.B) * a.T_pad / 32;
     float v = 0.0f;
     for (int tt = 0; tt < a.NT; ++tt) {
-      const int buf = tt & 1;
-      mbar_wait(&acc_full[buf], (tt >> 1) & 1);
+      const int buf = tt % nbuf;
+      mbar_wait(&acc_full[buf], (tt / nbuf) & 1);
       tc_fence_after();
       for (int c = 0; c < a.TT / 32; ++c) {
         uint32_t r[32];
@@ -310,7 +318,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    if (tmem_cols == 256) tmem_dealloc<256>(tmem); else tmem_dealloc<128>(tmem);
+    if (tmem_cols == 256) tmem_dealloc<256>(tmem);
+    else if (tmem_cols == 128) tmem_dealloc<128>(tmem);
+    else tmem_dealloc<64>(tmem);
   }
 }
 
@@ -339,20 +349,150 @@ struct ReadoutArgs {
 __device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
 __device__ __forceinline__ float log_cr(float x) { return float(log(double(x))); }
 
-// Phase 2 of the readout: write dI3 as three bf16 planes [3][64][B*T_pad]
-// (class rows, (b,t) contiguous) -- all 128 threads, 16-byte stores.
-__device__ __forceinline__ void readout_store_planes(const ReadoutArgs& a, const float* buf, int b) {
-  const int C = a.C;
-  const int chunks = (a.T + 7) / 8;
+// readout scratch: W [HL][C] | spike words [T][HL_pad/32] | per-(t, class) column
+// buffer [T][32] (one column per lane, so the serial loops need no predicates)
+__host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
+  return (size_t(HL) * C + size_t(T) * (HL_pad / 32) + size_t(T) * 32) * 4;
+}
+
+__global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
+  extern __shared__ float rsm[];
+  const int C = a.C, T = a.T;
+  const int hw = a.HL_pad / 32;
+  float* w = rsm;                                                      // [HL][C]
+  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * C);   // [T][hw]
+  float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][32]
+  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < a.HL * C; i += 128) w[i] = __ldg(a.w + i);
+  {
+    const uint32_t* __restrict__ src = a.s_in + size_t(b) * a.T_pad * hw;
+    for (int i = tid; i < T * hw; i += 128) spk[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  // projection (ops.hpp:163-172 order: ascending k, zero skip); warp w: t = w, w+4, ...
+  const int cl = lane < C ? lane : 0;
+  const float bias_c = (a.bias != nullptr && lane < C) ? a.bias[lane] : 0.0f;
+  for (int t = warp; t < T; t += 4) {
+    float acc = 0.0f;
+    for (int wi = 0; wi < hw; ++wi) {
+      uint32_t bits = spk[t * hw + wi];
+      while (bits) {
+        const int i = __ffs(bits) - 1;
+        bits &= bits - 1;
+        acc = __fadd_rn(acc, w[(wi * 32 + i) * C + cl]);
+      }
+    }
+    if (a.bias != nullptr) acc = __fadd_rn(acc, bias_c);
+    buf[t * 32 + lane] = lane < C ? acc : 0.0f;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float* col = buf + lane;
+    const float vb = lane < C ? clip01(a.beta[lane]) : 0.0f;
+    // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50); col[t] <- V3_t
+    float v = 0.0f, logit = 0.0f;
+    int t = 0;
+    for (; t + 8 <= T; t += 8) {
+      float I[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * 32];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        col[(t + e) * 32] = v;
+        v = __fadd_rn(__fmul_rn(v, vb), I[e]);
+        logit = __fadd_rn(logit, v);
+      }
+    }
+    for (; t < T; ++t) {
+      const float I = col[t * 32];
+      col[t * 32] = v;
+      v = __fadd_rn(__fmul_rn(v, vb), I);
+      logit = __fadd_rn(logit, v);
+    }
+    const float v_final = v;
+    // softmax CE, sequential order of objective.hpp:53-73
+    float mx = __shfl_sync(0xffffffffu, logit, 0);
+    for (int j = 1; j < C; ++j) {
+      const float lj = __shfl_sync(0xffffffffu, logit, j);
+      mx = (mx < lj) ? lj : mx;
+    }
+    const float ex = lane < C ? exp_cr(__fsub_rn(logit, mx)) : 0.0f;
+    float z = 0.0f;
+    for (int j = 0; j < C; ++j) z = __fadd_rn(z, __shfl_sync(0xffffffffu, ex, j));
+    const int y = a.labels[a.rows[b]];
+    const float logit_y = __shfl_sync(0xffffffffu, logit, y);
+    // argmax, ties to the lowest index (objective.hpp:126-131)
+    float bv = lane < C ? logit : -INFINITY;
+    int bi = lane < C ? lane : 1 << 30;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      a.loss_b[b] = __fsub_rn(__fadd_rn(mx, log_cr(z)), logit_y);
+      a.correct_b[b] = (bi == y) ? 1 : 0;
+    }
+    float delta = 0.0f;
+    if (lane < C) {
+      float d = __fdiv_rn(ex, z);
+      if (lane == y) d = __fsub_rn(d, 1.0f);
+      delta = __fmul_rn(d, a.inv_b);
+    }
+    if (a.dbg_trace != nullptr && lane < C) {
+      for (int s = 0; s < T; ++s)
+        a.dbg_trace[(size_t(b) * T + s) * C + lane] = s + 1 < T ? col[(s + 1) * 32] : v_final;
+    }
+    // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
+    float G = delta, db = 0.0f, dbias = 0.0f;
+    t = T - 1;
+    {
+      const float V3 = col[t * 32];
+      db = __fmul_rn(G, V3);
+      dbias = G;
+      col[t * 32] = G;
+    }
+    --t;
+    for (; t >= 7; t -= 8) {
+      float V3[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * 32];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        G = __fadd_rn(delta, __fmul_rn(G, vb));
+        db = __fadd_rn(db, __fmul_rn(G, V3[e]));
+        dbias = __fadd_rn(dbias, G);
+        col[(t - e) * 32] = G;
+      }
+    }
+    for (; t >= 0; --t) {
+      const float V3 = col[t * 32];
+      G = __fadd_rn(delta, __fmul_rn(G, vb));
+      db = __fadd_rn(db, __fmul_rn(G, V3));
+      dbias = __fadd_rn(dbias, G);
+      col[t * 32] = G;
+    }
+    if (lane < C) {
+      a.dbeta_part[size_t(b) * C + lane] = db;
+      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
+    }
+  }
+  __syncthreads();
+  // dI3 as three bf16 planes [3][64][B*T_pad] (class rows, (b,t) contiguous)
+  const int chunks = (T + 7) / 8;
   const size_t cols = size_t(a.B) * a.T_pad;
   const size_t plane = size_t(64) * cols;
-  for (int u = threadIdx.x; u < C * chunks; u += blockDim.x) {
+  for (int u = tid; u < C * chunks; u += 128) {
     const int c = u / chunks, t0 = (u % chunks) * 8;
     uint32_t hp[4], mp[4], lp[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const float g0 = t0 + e < a.T ? buf[(t0 + e) * C + c] : 0.0f;
-      const float g1 = t0 + e + 1 < a.T ? buf[(t0 + e + 1) * C + c] : 0.0f;
+      const float g0 = t0 + e < T ? buf[(t0 + e) * 32 + c] : 0.0f;
+      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * 32 + c] : 0.0f;
       __nv_bfloat16 h0, m0, l0, h1, m1, l1;
       split3(g0, h0, m0, l0);
       split3(g1, h1, m1, l1);
@@ -365,119 +505,6 @@ __device__ __forceinline__ void readout_store_planes(const ReadoutArgs& a, const
     *reinterpret_cast<uint4*>(a.d3_planes + plane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
     *reinterpret_cast<uint4*>(a.d3_planes + 2 * plane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
   }
-}
-
-__host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (size_t(HL) * C + size_t(T) * (HL_pad / 32) + size_t(T) * C) * 4;
-}
-
-__global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
-  extern __shared__ float rsm[];
-  const int C = a.C;
-  const int hw = a.HL_pad / 32;
-  float* w = rsm;                                                      // [HL][C]
-  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * C);   // [T][hw]
-  float* buf = reinterpret_cast<float*>(spk + size_t(a.T) * hw);       // [T][C] I3 -> V3
-  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < a.HL * C; i += 128) w[i] = __ldg(a.w + i);
-  {
-    const uint32_t* __restrict__ src = a.s_in + size_t(b) * a.T_pad * hw;
-    for (int i = tid; i < a.T * hw; i += 128) spk[i] = __ldg(src + i);
-  }
-  __syncthreads();
-  // projection: warp w handles t = w, w+4, ...; lane c accumulates class c in the
-  // reference's ascending-k order with zero skip
-  const float bias_c = (a.bias != nullptr && lane < C) ? a.bias[lane] : 0.0f;
-  for (int t = warp; t < a.T; t += 4) {
-    float acc = 0.0f;
-    for (int wi = 0; wi < hw; ++wi) {
-      uint32_t bits = spk[t * hw + wi];
-      while (bits) {
-        const int i = __ffs(bits) - 1;
-        bits &= bits - 1;
-        if (lane < C) acc = __fadd_rn(acc, w[(wi * 32 + i) * C + lane]);
-      }
-    }
-    if (lane < C) buf[t * C + lane] = (a.bias != nullptr) ? __fadd_rn(acc, bias_c) : acc;
-  }
-  __syncthreads();
-  if (warp == 0) {
-  const bool on = lane < C;
-  const float vb = on ? clip01(a.beta[lane]) : 0.0f;
-  // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50)
-  float v = 0.0f, logit = 0.0f;
-  for (int t0 = 0; t0 < a.T; t0 += 8) {
-    float I[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) I[e] = (on && t0 + e < a.T) ? buf[(t0 + e) * C + lane] : 0.0f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int t = t0 + e;
-      if (t < a.T) {
-        if (on) buf[t * C + lane] = v;  // keep V3 (entering state) for dbeta
-        v = __fadd_rn(__fmul_rn(v, vb), I[e]);
-        logit = __fadd_rn(logit, v);
-        if (on && a.dbg_trace != nullptr) a.dbg_trace[(size_t(b) * a.T + t) * C + lane] = v;
-      }
-    }
-  }
-  // softmax CE in the reference's sequential order (objective.hpp:53-73)
-  float mx = __shfl_sync(0xffffffffu, logit, 0);
-  for (int j = 1; j < C; ++j) {
-    const float lj = __shfl_sync(0xffffffffu, logit, j);
-    mx = (mx < lj) ? lj : mx;
-  }
-  const float ex = on ? exp_cr(__fsub_rn(logit, mx)) : 0.0f;
-  float z = 0.0f;
-  for (int j = 0; j < C; ++j) z = __fadd_rn(z, __shfl_sync(0xffffffffu, ex, j));
-  const int y = a.labels[a.rows[b]];
-  const float logit_y = __shfl_sync(0xffffffffu, logit, y);
-  // argmax, ties to the lowest index (objective.hpp:126-131)
-  float bv = on ? logit : -INFINITY;
-  int bi = on ? lane : 1 << 30;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-    if (ov > bv || (ov == bv && oi < bi)) {
-      bv = ov;
-      bi = oi;
-    }
-  }
-  if (lane == 0) {
-    a.loss_b[b] = __fsub_rn(__fadd_rn(mx, log_cr(z)), logit_y);
-    a.correct_b[b] = (bi == y) ? 1 : 0;
-  }
-  float delta = 0.0f;
-  if (on) {
-    float d = __fdiv_rn(ex, z);
-    if (lane == y) d = __fsub_rn(d, 1.0f);
-    delta = __fmul_rn(d, a.inv_b);
-  }
-  // LI reverse scan: G_t = delta + G_{t+1} * bc ; dI3_t = G_t ; dbeta += G_t * V3_t
-  float G = 0.0f, db = 0.0f, dbias = 0.0f;
-  for (int t1 = a.T; t1 > 0; t1 -= 8) {
-    float V3[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) V3[e] = (on && t1 - 1 - e >= 0) ? buf[(t1 - 1 - e) * C + lane] : 0.0f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int t = t1 - 1 - e;
-      if (t >= 0) {
-        G = (t == a.T - 1) ? delta : __fadd_rn(delta, __fmul_rn(G, vb));
-        db = __fadd_rn(db, __fmul_rn(G, V3[e]));
-        dbias = __fadd_rn(dbias, G);
-        if (on) buf[t * C + lane] = G;
-      }
-    }
-  }
-  if (on) {
-    a.dbeta_part[size_t(b) * C + lane] = db;
-    if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
-  }
-  }  // warp 0
-  __syncthreads();
-  readout_store_planes(a, buf, b);
 }
 
 // ============================================================================
@@ -539,7 +566,7 @@ __host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
   return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256;
 }
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 2)
     k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
               BwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -557,7 +584,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int b = blockIdx.x, nt = blockIdx.y;
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
-  const uint32_t tmem_cols = (a.TT >= 128) ? 256u : 128u;
+  const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
+  const int nbuf = a.NT > 1 ? 2 : 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -571,7 +599,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0) {
-    if (tmem_cols == 256) tmem_alloc<256>(tmem_slot); else tmem_alloc<128>(tmem_slot);
+    if (tmem_cols == 256) tmem_alloc<256>(tmem_slot);
+    else if (tmem_cols == 128) tmem_alloc<128>(tmem_slot);
+    else tmem_alloc<64>(tmem_slot);
   }
   tc_fence_before();
   __syncthreads();
@@ -605,9 +635,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1;
-        const int j = it / KB, kb = it % KB, buf = j & 1;
-        if (kb == 0 && j >= 2) {
-          mbar_wait(&acc_empty[buf], ((j - 2) >> 1) & 1);
+        const int j = it / KB, kb = it % KB, buf = j % nbuf;
+        if (kb == 0 && j >= nbuf) {
+          mbar_wait(&acc_empty[buf], ((j - nbuf) / nbuf) & 1);
           tc_fence_after();
         }
         mbar_wait(&full[s], ph);
@@ -643,8 +673,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     float vn[32];
     load_v_chunk(a, b, n, nch - 1, vn);
     for (int j = 0; j < a.NT; ++j) {
-      const int tt = a.NT - 1 - j, buf = j & 1;
-      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      const int tt = a.NT - 1 - j, buf = j % nbuf;
+      mbar_wait(&acc_full[buf], (j / nbuf) & 1);
       tc_fence_after();
       for (int c = a.TT / 32 - 1; c >= 0; --c) {
         const int gc = tt * (a.TT / 32) + c;
@@ -719,7 +749,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    if (tmem_cols == 256) tmem_dealloc<256>(tmem); else tmem_dealloc<128>(tmem);
+    if (tmem_cols == 256) tmem_dealloc<256>(tmem);
+    else if (tmem_cols == 128) tmem_dealloc<128>(tmem);
+    else tmem_dealloc<64>(tmem);
   }
 }
 
