@@ -209,6 +209,7 @@ struct snn_engine {
   // debug
   bool debug = false;
   DevBuf<float> dbg_i[SNN_MAX_HIDDEN], dbg_ds[SNN_MAX_HIDDEN], dbg_trace;
+  DevBuf<long long> dbg_clk;
   // graphs keyed by (dataset ptr, update flag)
   std::map<std::pair<const void*, int>, cudaGraphExec_t> graphs;
   // multi-GPU
@@ -218,6 +219,7 @@ struct snn_engine {
   // pipeline depths (smem per CTA decides how many CTAs share an SM)
   int fwd_stages = env_int("SNN_FWD_STAGES", 1);
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
+  int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
     return (v && *v) ? std::max(1, std::atoi(v)) : d;
@@ -589,6 +591,8 @@ struct snn_engine {
       r.dbeta_part = dbeta[L].p;
       r.dbias_part = net.bias ? dbias[L].p : nullptr;
       r.dbg_trace = debug ? dbg_trace.p : nullptr;
+      r.dbg_clk = debug ? dbg_clk.p : nullptr;
+      r.exp_mode = exp_mode;
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
       r.inv_b = 1.0f / float(B_global());
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
@@ -782,6 +786,7 @@ struct snn_engine {
       }
     }
     if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
+    if (on) dbg_clk.alloc(size_t(B) * 8); else dbg_clk.free();
     clear_graphs();
   }
 };
@@ -1124,6 +1129,12 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
   return guard(e, [&] {
     if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
     const int B = e->B, T = e->T, T_pad = e->T_pad;
+    if (which == 5) {
+      const size_t need = size_t(B) * 8 * sizeof(long long);
+      if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
+      CK(cudaMemcpy(host, e->dbg_clk.p, need, cudaMemcpyDeviceToHost));
+      return;
+    }
     if (which == 3) {
       const size_t need = size_t(B) * T * e->C * sizeof(float);
       if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);

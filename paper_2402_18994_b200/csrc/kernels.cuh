@@ -342,6 +342,8 @@ struct ReadoutArgs {
   float* dbeta_part;        // [B][C]
   float* dbias_part;        // [B][C] or nullptr
   float* dbg_trace;         // optional [B][T][C]
+  long long* dbg_clk;       // optional [B][8] phase timestamps (clock64)
+  int exp_mode;             // 0: exp/log evaluated in fp64 then rounded; 1: expf/logf
   int B, T, T_pad, HL, HL_pad, C;
   float inv_b;              // 1/B_global (objective.hpp:104)
 };
@@ -363,32 +365,46 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * C);   // [T][hw]
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][32]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * 8 + (k)] = clock64();
+  RO_CLK(0)
+  __shared__ int s_label;
+  if (tid == 0) s_label = a.labels[a.rows[b]];
+  const float beta_l = lane < C ? a.beta[lane] : 0.0f;
   for (int i = tid; i < a.HL * C; i += 128) w[i] = __ldg(a.w + i);
   {
     const uint32_t* __restrict__ src = a.s_in + size_t(b) * a.T_pad * hw;
     for (int i = tid; i < T * hw; i += 128) spk[i] = __ldg(src + i);
   }
   __syncthreads();
-  // projection (ops.hpp:163-172 order: ascending k, zero skip); warp w: t = w, w+4, ...
-  const int cl = lane < C ? lane : 0;
-  const float bias_c = (a.bias != nullptr && lane < C) ? a.bias[lane] : 0.0f;
-  for (int t = warp; t < T; t += 4) {
-    float acc = 0.0f;
+  RO_CLK(1)
+  // projection (ops.hpp:163-172 order: ascending k, zero skip): one lane per
+  // time step, all classes per lane (acc in registers), W rows from smem.
+  for (int t = tid; t < T; t += 128) {
+    float acc[kMaxClasses];
+#pragma unroll
+    for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0f;
     for (int wi = 0; wi < hw; ++wi) {
       uint32_t bits = spk[t * hw + wi];
       while (bits) {
         const int i = __ffs(bits) - 1;
         bits &= bits - 1;
-        acc = __fadd_rn(acc, w[(wi * 32 + i) * C + cl]);
+        const float* wr = w + (wi * 32 + i) * C;
+#pragma unroll
+        for (int c = 0; c < kMaxClasses; ++c)
+          if (c < C) acc[c] = __fadd_rn(acc[c], wr[c]);
       }
     }
-    if (a.bias != nullptr) acc = __fadd_rn(acc, bias_c);
-    buf[t * 32 + lane] = lane < C ? acc : 0.0f;
+#pragma unroll
+    for (int c = 0; c < kMaxClasses; ++c) {
+      if (c < C && a.bias != nullptr) acc[c] = __fadd_rn(acc[c], a.bias[c]);
+      buf[t * 32 + c] = c < C ? acc[c] : 0.0f;
+    }
   }
   __syncthreads();
+  RO_CLK(2)
   if (warp == 0) {
     float* col = buf + lane;
-    const float vb = lane < C ? clip01(a.beta[lane]) : 0.0f;
+    const float vb = lane < C ? clip01(beta_l) : 0.0f;
     // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50); col[t] <- V3_t
     float v = 0.0f, logit = 0.0f;
     int t = 0;
@@ -410,16 +426,18 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
       logit = __fadd_rn(logit, v);
     }
     const float v_final = v;
+    RO_CLK(3)
     // softmax CE, sequential order of objective.hpp:53-73
     float mx = __shfl_sync(0xffffffffu, logit, 0);
     for (int j = 1; j < C; ++j) {
       const float lj = __shfl_sync(0xffffffffu, logit, j);
       mx = (mx < lj) ? lj : mx;
     }
-    const float ex = lane < C ? exp_cr(__fsub_rn(logit, mx)) : 0.0f;
+    const float xd = __fsub_rn(logit, mx);
+    const float ex = lane < C ? (a.exp_mode ? expf(xd) : exp_cr(xd)) : 0.0f;
     float z = 0.0f;
     for (int j = 0; j < C; ++j) z = __fadd_rn(z, __shfl_sync(0xffffffffu, ex, j));
-    const int y = a.labels[a.rows[b]];
+    const int y = s_label;
     const float logit_y = __shfl_sync(0xffffffffu, logit, y);
     // argmax, ties to the lowest index (objective.hpp:126-131)
     float bv = lane < C ? logit : -INFINITY;
@@ -434,7 +452,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
       }
     }
     if (lane == 0) {
-      a.loss_b[b] = __fsub_rn(__fadd_rn(mx, log_cr(z)), logit_y);
+      a.loss_b[b] = __fsub_rn(__fadd_rn(mx, a.exp_mode ? logf(z) : log_cr(z)), logit_y);
       a.correct_b[b] = (bi == y) ? 1 : 0;
     }
     float delta = 0.0f;
@@ -447,6 +465,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
       for (int s = 0; s < T; ++s)
         a.dbg_trace[(size_t(b) * T + s) * C + lane] = s + 1 < T ? col[(s + 1) * 32] : v_final;
     }
+    RO_CLK(4)
     // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
     float G = delta, db = 0.0f, dbias = 0.0f;
     t = T - 1;
@@ -480,8 +499,10 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
       a.dbeta_part[size_t(b) * C + lane] = db;
       if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
     }
+    RO_CLK(5)
   }
   __syncthreads();
+  RO_CLK(6)
   // dI3 as three bf16 planes [3][64][B*T_pad] (class rows, (b,t) contiguous)
   const int chunks = (T + 7) / 8;
   const size_t cols = size_t(a.B) * a.T_pad;
@@ -505,6 +526,9 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     *reinterpret_cast<uint4*>(a.d3_planes + plane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
     *reinterpret_cast<uint4*>(a.d3_planes + 2 * plane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
   }
+  __syncthreads();
+  RO_CLK(7)
+#undef RO_CLK
 }
 
 // ============================================================================
@@ -558,12 +582,14 @@ __device__ __forceinline__ void load_v_chunk(const BwdArgs& a, int b, int n, int
   for (int e = 0; e < 32; ++e) v[e] = (c * 32 + e < a.T) ? __ldg(src + size_t(e) * a.H_pad) : 0.0f;
 }
 
-constexpr int kBwdThreads = 192;
+constexpr int kBwdSeg = 2;                        // time segments per t-tile
+constexpr int kBwdScanThreads = 128 * kBwdSeg;
+constexpr int kBwdThreads = kBwdScanThreads + 64;  // + TMA warp + MMA warp
 __host__ __device__ constexpr uint32_t bwd_stage_bytes(int TT) {
   return 3 * kPlaneTile + 3 * uint32_t(TT) * 128u;
 }
 __host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
-  return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256;
+  return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256 + 3 * 4 * kBwdScanThreads;
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 2)
@@ -579,6 +605,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // segment exchange: affine maps (A, Bc) and segment-start G per (segment, neuron)
+  float* xA = reinterpret_cast<float*>(smem + S * stage_bytes + 256);
+  float* xB = xA + kBwdScanThreads;
+  float* xG = xB + kBwdScanThreads;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x, nt = blockIdx.y;
@@ -594,7 +624,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], kBwdScanThreads);
     }
     fence_barrier_init();
   }
@@ -609,7 +639,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   const uint32_t tmem = *tmem_slot;
   const int cols_total = a.B * a.T_pad;
 
-  if (warp == 4) {
+  const int tma_warp = kBwdScanThreads / 32, mma_warp = tma_warp + 1;
+  if (warp == tma_warp) {
     if (elect_one()) {
       tma_prefetch(&tm_w);
       tma_prefetch(&tm_di);
@@ -629,7 +660,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == mma_warp) {
     // A: K-major W planes; B: MN-major dI planes (t contiguous), LBO = 64-t block
     const uint32_t idesc = idesc_bf16(128, a.TT, false, true);
     if (elect_one()) {
@@ -662,65 +693,94 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
-    const int n = nt * 128 + warp * 32 + lane;
+  } else {
+    // Scan warps: quadrant q (TMEM lanes 32q..32q+31 = neurons), time segment sg
+    // of each t-tile.  G' = (bc - theta g) G + g dS is linear in G, so each
+    // segment first composes its affine map, the maps are chained through smem,
+    // then every segment replays its steps in the reference operation order.
+    const int q = warp & 3, sg = warp >> 2;
+    const int sidx = sg * 128 + q * 32 + lane;
+    const int n = nt * 128 + q * 32 + lane;
     const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
     const float theta = a.theta, ntheta = -a.theta;
     const size_t plane = size_t(a.H_pad) * cols_total;
     __nv_bfloat16* __restrict__ drow = a.di_planes + size_t(n) * cols_total + size_t(b) * a.T_pad;
-    float G = 0.0f, db = 0.0f, dbias = 0.0f;
-    const int nch = (a.T + 31) / 32;
-    float vn[32];
-    load_v_chunk(a, b, n, nch - 1, vn);
+    const float* __restrict__ vrow = a.v_in + size_t(b) * a.T_pad * a.H_pad + n;
+    const int seg_len = a.TT / kBwdSeg;  // multiple of 16
+    float Gcarry = 0.0f, db = 0.0f, dbias = 0.0f;
     for (int j = 0; j < a.NT; ++j) {
       const int tt = a.NT - 1 - j, buf = j % nbuf;
+      const int t_lo = tt * a.TT + sg * seg_len;               // first step of my segment
+      const int t_hi = min(t_lo + seg_len, a.T);                // one past the last valid
+      const uint32_t tcol = tmem + (uint32_t(q * 32) << 16) + buf * a.TT + sg * seg_len;
       mbar_wait(&acc_full[buf], (j / nbuf) & 1);
       tc_fence_after();
-      for (int c = a.TT / 32 - 1; c >= 0; --c) {
-        const int gc = tt * (a.TT / 32) + c;
-        if (gc >= nch) continue;
-        float vr[32], x[32], sg[32];
+      // ---- pass 1: compose the segment's affine map, t descending
+      float A = 1.0f, Bc = 0.0f;
+      for (int c0 = seg_len - 16; c0 >= 0; c0 -= 16) {
+        if (t_lo + c0 >= t_hi) continue;
+        uint32_t r[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                     : "r"(tcol + c0));
+        float vr[16];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) vr[e] = vn[e];
-        if (gc > 0) load_v_chunk(a, b, n, gc - 1, vn);
-        {
-          uint32_t r[32];
-          tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + buf * a.TT + c * 32, r);
-          tmem_ld_wait();
+        for (int e = 0; e < 16; ++e) vr[e] = (t_lo + c0 + e < t_hi) ? __ldg(vrow + size_t(t_lo + c0 + e) * a.H_pad) : 0.0f;
+        tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r[e]);
+        for (int e = 15; e >= 0; --e) {
+          if (t_lo + c0 + e < t_hi) {
+            const float g = surrogate_fast(a.act, a.slope, a.aux, __fadd_rn(vr[e], ntheta));
+            const float at = vb - theta * g;
+            Bc = at * Bc + g * __uint_as_float(r[e]);
+            A = at * A;
+          }
         }
-        const int nvalid = min(32, a.T - gc * 32);
+      }
+      xA[sidx] = A;
+      xB[sidx] = Bc;
+      if (sg == kBwdSeg - 1) xG[sidx] = Gcarry;
+      asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      // chain the maps: segment s starts from the G leaving segment s+1
+      float G = xG[(kBwdSeg - 1) * 128 + q * 32 + lane];
+      for (int s2 = kBwdSeg - 1; s2 > sg; --s2) G = xA[s2 * 128 + q * 32 + lane] * G + xB[s2 * 128 + q * 32 + lane];
+      asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      // ---- pass 3: exact-order replay of my segment
+      for (int c0 = seg_len - 16; c0 >= 0; c0 -= 16) {
+        if (t_lo + c0 >= t_hi) continue;
+        uint32_t r[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                     : "r"(tcol + c0));
+        float vr[16], x[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vr[e] = (t_lo + c0 + e < t_hi) ? __ldg(vrow + size_t(t_lo + c0 + e) * a.H_pad) : 0.0f;
+        tmem_ld_wait();
         if (a.dbg_ds != nullptr) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e < nvalid) a.dbg_ds[(size_t(b) * a.T_pad + gc * 32 + e) * a.H_pad + n] = x[e];
+          for (int e = 0; e < 16; ++e)
+            if (t_lo + c0 + e < t_hi)
+              a.dbg_ds[(size_t(b) * a.T_pad + t_lo + c0 + e) * a.H_pad + n] = __uint_as_float(r[e]);
         }
-        // phase A: surrogates g(V_t - theta), independent across t
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          sg[e] = surrogate_fast(a.act, a.slope, a.aux, __fadd_rn(vr[e], ntheta));
-        // phase B: the recurrence; x[e] <- dI_t = G (grad of the step-t input)
-#pragma unroll
-        for (int e = 31; e >= 0; --e) {
-          if (e < nvalid) {
-            const float g = G;
-            const float gs = __fadd_rn(x[e], __fmul_rn(-g, theta));
-            G = __fadd_rn(__fmul_rn(g, vb), __fmul_rn(gs, sg[e]));
-            x[e] = g;
+        for (int e = 15; e >= 0; --e) {
+          if (t_lo + c0 + e < t_hi) {
+            const float g = surrogate_fast(a.act, a.slope, a.aux, __fadd_rn(vr[e], ntheta));
+            const float gi = G;
+            const float gs = __fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gi, theta));
+            G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
+            x[e] = gi;
+            db = __fadd_rn(db, __fmul_rn(gi, vr[e]));
+            dbias = __fadd_rn(dbias, gi);
           } else {
             x[e] = 0.0f;
           }
         }
-        // phase C: dbeta / dbias partial sums (t descending) and the bf16 planes
+        uint32_t ph_[8], pm_[8], pl_[8];
 #pragma unroll
-        for (int e = 31; e >= 0; --e) {
-          db = __fadd_rn(db, __fmul_rn(x[e], vr[e]));
-          dbias = __fadd_rn(dbias, x[e]);
-        }
-        uint32_t ph_[16], pm_[16], pl_[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
+        for (int e = 0; e < 16; e += 2) {
           __nv_bfloat16 h0, m0, l0, h1, m1, l1;
           split3(x[e], h0, m0, l0);
           split3(x[e + 1], h1, m1, l1);
@@ -728,22 +788,38 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           pm_[e / 2] = uint32_t(__bfloat16_as_ushort(m0)) | (uint32_t(__bfloat16_as_ushort(m1)) << 16);
           pl_[e / 2] = uint32_t(__bfloat16_as_ushort(l0)) | (uint32_t(__bfloat16_as_ushort(l1)) << 16);
         }
-        uint4* dh = reinterpret_cast<uint4*>(drow + gc * 32);
-        uint4* dm = reinterpret_cast<uint4*>(drow + plane + gc * 32);
-        uint4* dl = reinterpret_cast<uint4*>(drow + 2 * plane + gc * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          dh[q] = make_uint4(ph_[4 * q], ph_[4 * q + 1], ph_[4 * q + 2], ph_[4 * q + 3]);
-          dm[q] = make_uint4(pm_[4 * q], pm_[4 * q + 1], pm_[4 * q + 2], pm_[4 * q + 3]);
-          dl[q] = make_uint4(pl_[4 * q], pl_[4 * q + 1], pl_[4 * q + 2], pl_[4 * q + 3]);
-        }
+        uint4* dh = reinterpret_cast<uint4*>(drow + t_lo + c0);
+        uint4* dm = reinterpret_cast<uint4*>(drow + plane + t_lo + c0);
+        uint4* dl = reinterpret_cast<uint4*>(drow + 2 * plane + t_lo + c0);
+        dh[0] = make_uint4(ph_[0], ph_[1], ph_[2], ph_[3]);
+        dh[1] = make_uint4(ph_[4], ph_[5], ph_[6], ph_[7]);
+        dm[0] = make_uint4(pm_[0], pm_[1], pm_[2], pm_[3]);
+        dm[1] = make_uint4(pm_[4], pm_[5], pm_[6], pm_[7]);
+        dl[0] = make_uint4(pl_[0], pl_[1], pl_[2], pl_[3]);
+        dl[1] = make_uint4(pl_[4], pl_[5], pl_[6], pl_[7]);
       }
+      // the earliest segment's final G carries into the previous t-tile
+      if (sg == 0) xG[(kBwdSeg - 1) * 128 + q * 32 + lane] = G;
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
+      asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      Gcarry = xG[(kBwdSeg - 1) * 128 + q * 32 + lane];
     }
-    if (n < a.H) {
-      a.dbeta_part[size_t(b) * a.H + n] = db;
-      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * a.H + n] = dbias;
+    // combine the per-segment dbeta / dbias partials in a fixed order
+    if (sg > 0) {
+      xA[sidx] = db;
+      xB[sidx] = dbias;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+    if (sg == 0) {
+      for (int s2 = 1; s2 < kBwdSeg; ++s2) {
+        db = __fadd_rn(db, xA[s2 * 128 + q * 32 + lane]);
+        dbias = __fadd_rn(dbias, xB[s2 * 128 + q * 32 + lane]);
+      }
+      if (n < a.H) {
+        a.dbeta_part[size_t(b) * a.H + n] = db;
+        if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * a.H + n] = dbias;
+      }
     }
   }
   __syncthreads();
@@ -981,10 +1057,12 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     const int S = a.splits[j];
     float g = 0.0f;
     int s = 0;
-    for (; s + 4 <= S; s += 4) {
-      const float x0 = __ldg(p + s * sstride), x1 = __ldg(p + (s + 1) * sstride);
-      const float x2 = __ldg(p + (s + 2) * sstride), x3 = __ldg(p + (s + 3) * sstride);
-      g = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(g, x0), x1), x2), x3);
+    for (; s + 8 <= S; s += 8) {
+      float x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = __ldg(p + (s + q) * sstride);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) g = __fadd_rn(g, x[q]);
     }
     for (; s < S; ++s) g = __fadd_rn(g, __ldg(p + s * sstride));
     a.grads[i] = g;

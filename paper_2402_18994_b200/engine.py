@@ -420,9 +420,11 @@ class Engine:
         self._check(self._L.snn_debug_enable(self._h, int(on)))
 
     def fetch(self, which: str, layer: int = 0) -> np.ndarray:
-        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4}[which]
+        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5}[which]
         B, T = self.batch_size, self.time_steps
-        if which == "trace":
+        if which == "clk":
+            out = np.empty((B, 8), np.int64)
+        elif which == "trace":
             out = np.empty((B, T, self.desc["classes"]), np.float32)
         else:
             H = self.desc["hidden"][layer]
