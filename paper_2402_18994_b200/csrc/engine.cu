@@ -568,6 +568,7 @@ struct snn_engine {
       f.s_np = s_np[l].p;
       f.s_tp = s_tp[l].p;
       f.dbg_i = debug ? dbg_i[l].p : nullptr;
+      f.dbg_clk = debug ? dbg_clk.p + size_t(1 + l) * B * 8 * 8 : nullptr;
       f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
       f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
       f.theta = net.threshold;
@@ -608,6 +609,7 @@ struct snn_engine {
       bw.dbeta_part = dbeta[l].p;
       bw.dbias_part = net.bias ? dbias[l].p : nullptr;
       bw.dbg_ds = debug ? dbg_ds[l].p : nullptr;
+      bw.dbg_clk = debug ? dbg_clk.p + size_t(1 + L + l) * B * 8 * 8 : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
@@ -786,7 +788,8 @@ struct snn_engine {
       }
     }
     if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
-    if (on) dbg_clk.alloc(size_t(B) * 8); else dbg_clk.free();
+    // clock stamps: slot 0 readout [B][8], slots 1..L fwd, L+1..2L bwd ([B*8 ctas][8] each)
+    if (on) dbg_clk.alloc(size_t(1 + 2 * L) * B * 8 * 8); else dbg_clk.free();
     clear_graphs();
   }
 };
@@ -1130,7 +1133,7 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
     if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
     const int B = e->B, T = e->T, T_pad = e->T_pad;
     if (which == 5) {
-      const size_t need = size_t(B) * 8 * sizeof(long long);
+      const size_t need = size_t(1 + 2 * e->L) * B * 8 * 8 * sizeof(long long);
       if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
       CK(cudaMemcpy(host, e->dbg_clk.p, need, cudaMemcpyDeviceToHost));
       return;

@@ -149,6 +149,7 @@ struct FwdArgs {
   uint32_t* s_np;         // [B][T_pad][H_pad/32]
   uint32_t* s_tp;         // [H_pad][B*T_pad/32]
   float* dbg_i;           // optional [B][T_pad][H_pad] raw projection
+  long long* dbg_clk;     // optional [gridDim.x*gridDim.y][8] phase timestamps
   int B, T, T_pad, TT, NT, K_pad, H, H_pad, in_kind, stages;
   float theta;
 };
@@ -168,6 +169,36 @@ __host__ __device__ constexpr uint32_t acc_cols(int TT, int NT) {
   return NT > 1 ? (TT >= 128 ? 256u : 128u) : (TT >= 128 ? 128u : 64u);
 }
 
+// 32 LIF steps of one neuron (neuron.hpp:127-136 op order, bit-exact):
+//   pre = v - theta ; s = pre >= 0 ; v = ((v * bc) + I) - s * theta
+// kGeneral adds bias, a debug copy of I and a valid-step count (< 32 only in the
+// last chunk).  V is stored before each step (membrane entering step t).
+template <bool kGeneral>
+__device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, float* dp, int hpad,
+                                          int nvalid, float vb, float bn, float theta, int lane,
+                                          float& v, uint32_t& myword, uint32_t& tmask) {
+  const float ntheta = -theta;
+  myword = 0u;
+  tmask = 0u;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    float I = __uint_as_float(r[j]);
+    if (kGeneral) {
+      I = __fadd_rn(I, bn);
+      if (dp != nullptr && j < nvalid) dp[size_t(j) * hpad] = I;
+    }
+    vp[size_t(j) * hpad] = v;
+    const float pre = __fadd_rn(v, ntheta);
+    const bool sp = kGeneral ? (pre >= 0.0f && j < nvalid) : (pre >= 0.0f);
+    const float m = __fmul_rn(v, vb);
+    const float ai = __fadd_rn(m, I);
+    v = __fsub_rn(ai, sp ? theta : 0.0f);
+    const uint32_t bal = __ballot_sync(0xffffffffu, sp);
+    myword = (lane == j) ? bal : myword;
+    tmask |= uint32_t(sp) << j;
+  }
+}
+
 __global__ void __launch_bounds__(kFwdThreads, 2)
     k_lif_fwd(const __grid_constant__ CUtensorMap tm_w, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -182,6 +213,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x, nt = blockIdx.y;
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * 8 : nullptr;
+  if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
@@ -301,7 +334,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     const int n = nt * 128 + warp * 32 + lane;
     const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
     const float bn = (a.bias != nullptr && n < a.H) ? a.bias[n] : 0.0f;
-    const float theta = a.theta, ntheta = -a.theta;
     const size_t hw = size_t(a.H_pad) / 32;
     const size_t tp_words = size_t(a.B) * a.T_pad / 32;
     float v = 0.0f;
@@ -309,42 +341,36 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       const int buf = tt % nbuf;
       mbar_wait(&acc_full[buf], (tt / nbuf) & 1);
       tc_fence_after();
+      if (clk != nullptr && threadIdx.x == 0 && tt == 0) clk[1] = clock64();
       for (int c = 0; c < a.TT / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + buf * a.TT + c * 32, r);
         tmem_ld_wait();
         const int t0 = tt * a.TT + c * 32;
-        uint32_t myword = 0, tmask = 0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int t = t0 + j;
-          const bool valid = t < a.T;
-          float I = __uint_as_float(r[j]);
-          if (a.bias != nullptr) I = __fadd_rn(I, bn);
-          const size_t vi = (size_t(b) * a.T_pad + t) * a.H_pad + n;
-          if (valid) {
-            a.v_out[vi] = v;
-            if (a.dbg_i != nullptr) a.dbg_i[vi] = I;
-          }
-          const float pre = __fadd_rn(v, ntheta);
-          const bool sp = valid && (pre >= 0.0f);
-          const float m = __fmul_rn(v, vb);
-          const float ai = __fadd_rn(m, I);
-          const float rr = __fmul_rn(sp ? 1.0f : 0.0f, theta);
-          v = __fsub_rn(ai, rr);
-          const uint32_t bal = __ballot_sync(0xffffffffu, sp);
-          if (lane == j) myword = bal;
-          tmask |= uint32_t(sp) << j;
+        if (t0 >= a.T) {
+          // padded steps: no spikes (V rows beyond T are never read)
+          a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + warp] = 0u;
+          a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = 0u;
+          continue;
         }
+        float* vp = a.v_out + (size_t(b) * a.T_pad + t0) * a.H_pad + n;
+        uint32_t myword, tmask;
+        if (a.bias != nullptr || a.dbg_i != nullptr || t0 + 32 > a.T)
+          lif_chunk<true>(r, vp, a.dbg_i != nullptr ? a.dbg_i + (vp - a.v_out) : nullptr, a.H_pad,
+                          a.T - t0, vb, bn, a.theta, lane, v, myword, tmask);
+        else
+          lif_chunk<false>(r, vp, nullptr, a.H_pad, 32, vb, 0.0f, a.theta, lane, v, myword, tmask);
         a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + warp] = myword;
         a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = tmask;
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
     }
+    if (clk != nullptr && threadIdx.x == 0) clk[2] = clock64();
   }
 
   __syncthreads();
+  if (clk != nullptr && threadIdx.x == 0) clk[3] = clock64();
   if (warp == 0) {
     tc_fence_after();
     if (tmem_cols == 256) tmem_dealloc<256>(tmem);
@@ -572,6 +598,7 @@ struct BwdArgs {
   float* dbeta_part;           // [B][H]
   float* dbias_part;           // [B][H] or nullptr
   float* dbg_ds;               // optional [B][T_pad][H_pad]
+  long long* dbg_clk;          // optional [gridDim.x*gridDim.y][8] phase timestamps
   int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
   float theta, slope, aux;
 };
@@ -607,6 +634,55 @@ __device__ __forceinline__ void load_v_chunk(const BwdArgs& a, int b, int n, int
   for (int e = 0; e < 32; ++e) v[e] = (c * 32 + e < a.T) ? __ldg(src + size_t(e) * a.H_pad) : 0.0f;
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void load_v16(const float* __restrict__ p, int hpad, int nval,
+                                         float (&v)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = e < nval ? __ldg(p + size_t(e) * hpad) : 0.0f;
+}
+// affine map of 16 reverse steps: G' = (bc - theta g) G + g dS
+template <bool kTail>
+__device__ __forceinline__ void bwd_compose(const uint32_t (&r)[16], const float (&vr)[16], int nval,
+                                            float vb, float theta, const BwdArgs& a, float& A,
+                                            float& Bc) {
+#pragma unroll
+  for (int e = 15; e >= 0; --e) {
+    if (kTail && e >= nval) continue;
+    const float g = surrogate_fast(a.act, a.slope, a.aux, __fsub_rn(vr[e], theta));
+    const float at = vb - theta * g;
+    Bc = at * Bc + g * __uint_as_float(r[e]);
+    A = at * A;
+  }
+}
+// 16 reverse steps in the reference order: dI_t = G ; gs = dS + (-G) theta ;
+// G = G bc + gs g ; dbeta += G V ; dbias += G
+template <bool kTail>
+__device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float (&vr)[16], int nval,
+                                           float vb, float theta, const BwdArgs& a, float& G,
+                                           float& db, float& dbias, float (&x)[16]) {
+#pragma unroll
+  for (int e = 15; e >= 0; --e) {
+    if (kTail && e >= nval) {
+      x[e] = 0.0f;
+      continue;
+    }
+    const float g = surrogate_fast(a.act, a.slope, a.aux, __fsub_rn(vr[e], theta));
+    const float gi = G;
+    const float gs = __fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gi, theta));
+    G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
+    x[e] = gi;
+    db = __fadd_rn(db, __fmul_rn(gi, vr[e]));
+    dbias = __fadd_rn(dbias, gi);
+  }
+}
+
 constexpr int kBwdSeg = 2;                        // time segments per t-tile
 constexpr int kBwdScanThreads = 128 * kBwdSeg;
 constexpr int kBwdThreads = kBwdScanThreads + 64;  // + TMA warp + MMA warp
@@ -637,6 +713,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x, nt = blockIdx.y;
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * 8 : nullptr;
+  if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
@@ -740,69 +818,49 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const uint32_t tcol = tmem + (uint32_t(q * 32) << 16) + buf * a.TT + sg * seg_len;
       mbar_wait(&acc_full[buf], (j / nbuf) & 1);
       tc_fence_after();
+      if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[1] = clock64();
       // ---- pass 1: compose the segment's affine map, t descending
       float A = 1.0f, Bc = 0.0f;
+      const float* vseg = vrow + size_t(t_lo) * a.H_pad;
       for (int c0 = seg_len - 16; c0 >= 0; c0 -= 16) {
-        if (t_lo + c0 >= t_hi) continue;
+        const int nval = t_hi - (t_lo + c0);
+        if (nval <= 0) continue;
         uint32_t r[16];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                     : "r"(tcol + c0));
+        tmem_ld16(tcol + c0, r);
         float vr[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) vr[e] = (t_lo + c0 + e < t_hi) ? __ldg(vrow + size_t(t_lo + c0 + e) * a.H_pad) : 0.0f;
+        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
         tmem_ld_wait();
-#pragma unroll
-        for (int e = 15; e >= 0; --e) {
-          if (t_lo + c0 + e < t_hi) {
-            const float g = surrogate_fast(a.act, a.slope, a.aux, __fadd_rn(vr[e], ntheta));
-            const float at = vb - theta * g;
-            Bc = at * Bc + g * __uint_as_float(r[e]);
-            A = at * A;
-          }
-        }
+        if (nval >= 16) bwd_compose<false>(r, vr, 16, vb, theta, a, A, Bc);
+        else bwd_compose<true>(r, vr, nval, vb, theta, a, A, Bc);
       }
       xA[sidx] = A;
       xB[sidx] = Bc;
       if (sg == kBwdSeg - 1) xG[sidx] = Gcarry;
       asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[2] = clock64();
       // chain the maps: segment s starts from the G leaving segment s+1
       float G = xG[(kBwdSeg - 1) * 128 + q * 32 + lane];
       for (int s2 = kBwdSeg - 1; s2 > sg; --s2) G = xA[s2 * 128 + q * 32 + lane] * G + xB[s2 * 128 + q * 32 + lane];
       asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[3] = clock64();
       // ---- pass 3: exact-order replay of my segment
       for (int c0 = seg_len - 16; c0 >= 0; c0 -= 16) {
-        if (t_lo + c0 >= t_hi) continue;
+        const int nval = t_hi - (t_lo + c0);
+        if (nval <= 0) continue;
         uint32_t r[16];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                     : "r"(tcol + c0));
-        float vr[16], x[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) vr[e] = (t_lo + c0 + e < t_hi) ? __ldg(vrow + size_t(t_lo + c0 + e) * a.H_pad) : 0.0f;
+        tmem_ld16(tcol + c0, r);
+        float vr[16];
+        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
         tmem_ld_wait();
         if (a.dbg_ds != nullptr) {
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            if (t_lo + c0 + e < t_hi)
+            if (e < nval)
               a.dbg_ds[(size_t(b) * a.T_pad + t_lo + c0 + e) * a.H_pad + n] = __uint_as_float(r[e]);
         }
-#pragma unroll
-        for (int e = 15; e >= 0; --e) {
-          if (t_lo + c0 + e < t_hi) {
-            const float g = surrogate_fast(a.act, a.slope, a.aux, __fadd_rn(vr[e], ntheta));
-            const float gi = G;
-            const float gs = __fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gi, theta));
-            G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
-            x[e] = gi;
-            db = __fadd_rn(db, __fmul_rn(gi, vr[e]));
-            dbias = __fadd_rn(dbias, gi);
-          } else {
-            x[e] = 0.0f;
-          }
-        }
+        float x[16];
+        if (nval >= 16) bwd_replay<false>(r, vr, 16, vb, theta, a, G, db, dbias, x);
+        else bwd_replay<true>(r, vr, nval, vb, theta, a, G, db, dbias, x);
         uint32_t ph_[8], pm_[8], pl_[8];
 #pragma unroll
         for (int e = 0; e < 16; e += 2) split3_pack(x[e], x[e + 1], ph_[e / 2], pm_[e / 2], pl_[e / 2]);
@@ -816,6 +874,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         dl[0] = make_uint4(pl_[0], pl_[1], pl_[2], pl_[3]);
         dl[1] = make_uint4(pl_[4], pl_[5], pl_[6], pl_[7]);
       }
+      if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[4] = clock64();
       // the earliest segment's final G carries into the previous t-tile
       if (sg == 0) xG[(kBwdSeg - 1) * 128 + q * 32 + lane] = G;
       tc_fence_before();
@@ -823,6 +882,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
       Gcarry = xG[(kBwdSeg - 1) * 128 + q * 32 + lane];
     }
+    if (clk != nullptr && threadIdx.x == 0) clk[5] = clock64();
     // combine the per-segment dbeta / dbias partials in a fixed order
     if (sg > 0) {
       xA[sidx] = db;
@@ -841,6 +901,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     }
   }
   __syncthreads();
+  if (clk != nullptr && threadIdx.x == 0) clk[6] = clock64();
   if (warp == 0) {
     tc_fence_after();
     if (tmem_cols == 256) tmem_dealloc<256>(tmem);

@@ -1,3 +1,4 @@
+"""Phase timestamps (clock64) of the readout, forward and backward kernels (debug mode)."""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -5,12 +6,15 @@ sys.path.insert(0, ROOT)
 from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
 eng = Engine(shd_spec(), TrainConfig(batch_size=256, seed=0), 128)
 eng.synth_dataset(16384, seed=1)
-eng.debug(True)  # clocks + debug tensors
+eng.debug(True)
 rows = np.arange(256, dtype=np.uint32)
 for _ in range(3):
     eng.forward_backward(rows)
 clk = eng.fetch("clk")
-d = np.diff(clk, axis=1)
-print("phase cycles (median over CTAs):", np.median(d, axis=0).astype(int).tolist())
-print("phase cycles (max):", d.max(axis=0).tolist())
-print("start spread:", int(clk[:, 0].max() - clk[:, 0].min()), "end spread", int(clk[:, 7].max() - clk[:, 0].min()))
+L = 2
+names = ["readout"] + [f"fwd{l}" for l in range(L)] + [f"bwd{l}" for l in range(L)]
+for s, name in enumerate(names):
+    c = clk[s, :256]
+    n = 8 if name == "readout" else (4 if name.startswith("fwd") else 7)
+    d = np.diff(c[:, :n], axis=1)
+    print(f"{name:8s} phase cycles median {np.median(d, axis=0).astype(int).tolist()} max {d.max(axis=0).tolist()} total med {int(np.median(c[:, n-1]-c[:, 0]))}")
