@@ -118,8 +118,8 @@ def algorithmic(name: str, w: dict, n_params: int):
     l = int(idx.rstrip("]")) if idx else 0
     if base == "lif_fwd":            # I = A W over all T: 2 B T K N flops
         return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
-    if base == "wgrad":              # dW = A^T dI
-        return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
+    if base == "wgrad":              # dW = A^T dI, every Linear layer in one launch
+        return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(len(dims) - 1))
     if base == "lif_bwd":            # LIF reverse scan: 12 B / neuron-step
         return "hbm", 12.0 * B * T * dims[l + 1]
     if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element

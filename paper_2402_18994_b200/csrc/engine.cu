@@ -206,6 +206,7 @@ struct snn_engine {
   size_t sched_steps = 0;
   // tensor maps
   CUtensorMap tm_wt[kMaxLayers], tm_wb[kMaxLayers], tm_di_k[kMaxLayers], tm_di_w[kMaxLayers];
+  WgradMaps wg_maps;
   // debug
   bool debug = false;
   DevBuf<float> dbg_i[SNN_MAX_HIDDEN], dbg_ds[SNN_MAX_HIDDEN], dbg_trace;
@@ -220,6 +221,8 @@ struct snn_engine {
   int fwd_stages = env_int("SNN_FWD_STAGES", 1);
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
+  int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 1));
+  int wg_samples_per_split = env_int("SNN_WG_SPLIT_SAMPLES", 8);
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
     return (v && *v) ? std::max(1, std::atoi(v)) : d;
@@ -290,13 +293,9 @@ struct snn_engine {
     const size_t ro_smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
     if (ro_smem > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "readout working set too large");
     if (size_t(T) * C * 4 > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "T * classes too large");
-    // split-K so that each Linear's wgrad launch fills the chip ~2x
-    for (int j = 0; j <= L; ++j) {
-      const int tiles = (M_pad_w[j] / 128) * (N_pad[j] / n_tile_w[j]);
-      int s = std::max(1, 296 / std::max(1, tiles));
-      s = std::min(s, B);
-      splits_w[j] = s;
-    }
+    // split-K over samples: >= wg_samples_per_split samples per split keeps the
+    // partials small; the merged launch fills the chip across layers
+    for (int j = 0; j <= L; ++j) splits_w[j] = std::max(1, B / wg_samples_per_split);
     // parameter entries (network.hpp:210-226 order)
     entries.clear();
     size_t off = 0;
@@ -359,13 +358,14 @@ struct snn_engine {
     for (int j = 0; j <= L; ++j) {
       tm_di_k[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 64);
       tm_di_w[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, uint32_t(n_tile_w[j]));
+      wg_maps.m[j] = tm_di_w[j];
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(fwd_smem_bytes(TT, kFwdStagesMax))));
     CK(cudaFuncSetAttribute(k_lif_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(wg_smem_bytes(128))));
+                            int(wg_smem_bytes(128, kWgStagesMax))));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
     {
@@ -536,7 +536,7 @@ struct snn_engine {
   }
 
   // ---------------------------------------------------------------- step
-  int launches_per_step() const { return 3 * L + 4; }
+  int launches_per_step() const { return 2 * L + 5; }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;
@@ -618,21 +618,28 @@ struct snn_engine {
           tm_wb[l + 1], tm_di_k[l + 1], bw);
       mark(evs, "lif_bwd", l);
     }
-    // weight gradients
-    for (int j = 0; j <= L; ++j) {
+    // weight gradients: one launch over every Linear layer (split-K partials)
+    {
       WgradArgs w{};
+      w.n_layers = L + 1;
+      w.stages = wg_stages;
       w.x = ds.x.p;
       w.rows = rows_cur.p;
-      w.s_tp = j > 0 ? s_tp[j - 1].p : nullptr;
-      w.partial = partial[j].p;
-      w.kind = j == 0 ? 0 : 1;
-      w.B = B; w.T_pad = T_pad; w.M_pad = M_pad_w[j]; w.N_pad = N_pad[j];
-      w.n_tile = n_tile_w[j]; w.splits = splits_w[j]; w.x_row_stride = IN_pad;
-      k_wgrad<<<dim3(M_pad_w[j] / 128, N_pad[j] / n_tile_w[j], splits_w[j]), kWgThreads,
-                wg_smem_bytes(n_tile_w[j]), stream>>>(tm_di_w[j], w);
-      mark(evs, "wgrad", j);
+      w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
+      int blocks = 0;
+      for (int j = 0; j <= L; ++j) {
+        WgradLayer& g = w.layer[j];
+        g.s_tp = j > 0 ? s_tp[j - 1].p : nullptr;
+        g.partial = partial[j].p;
+        g.kind = j == 0 ? 0 : 1;
+        g.M_pad = M_pad_w[j]; g.N_pad = N_pad[j]; g.n_tile = n_tile_w[j]; g.splits = splits_w[j];
+        g.m_tiles = M_pad_w[j] / 128; g.n_tiles = N_pad[j] / n_tile_w[j];
+        g.block_start = blocks;
+        blocks += g.m_tiles * g.n_tiles * g.splits;
+      }
+      k_wgrad<<<blocks, kWgThreads, wg_smem_bytes(128, wg_stages), stream>>>(wg_maps, w);
+      mark(evs, "wgrad", -1);
     }
-    (void)rows;
     // gradient assembly (+ loss sum, hits, step counter)
     {
       ReduceArgs r{};

@@ -31,6 +31,7 @@ namespace snn {
 using namespace sm100;
 
 constexpr int kMaxClasses = 32;
+constexpr int kMaxLayers = 9;  // Linear layers (hidden + readout)
 
 // ------------------------------------------------------------ small helpers
 // clip(beta,0,1) = std::min(1, std::max(0, beta)) exactly (ops.hpp clip).
@@ -917,45 +918,61 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 // writes f32 partials; k_reduce sums them in fixed order (deterministic).
 // grid (M_pad/128, N_pad/N_TILE, splits); block 192.
 // ============================================================================
-struct WgradArgs {
-  const uint8_t* x;        // kind 0: staged dataset
-  const uint32_t* rows;    // kind 0: [B]
+struct WgradLayer {
   const uint32_t* s_tp;    // kind 1: time-packed spikes [K_pad][B*T_pad/32]
   float* partial;          // [splits][M_pad][N_pad]
-  // B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
-  int kind, B, T_pad, M_pad, N_pad, n_tile, splits, x_row_stride;
+  int kind, M_pad, N_pad, n_tile, splits, m_tiles, n_tiles, block_start;
+};
+// B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
+struct WgradArgs {
+  WgradLayer layer[kMaxLayers];
+  int n_layers, stages;
+  const uint8_t* x;        // kind 0: staged dataset
+  const uint32_t* rows;    // kind 0: [B]
+  int B, T_pad, x_row_stride;
+};
+struct WgradMaps {
+  CUtensorMap m[kMaxLayers];
 };
 
-constexpr int kWgStages = 3;
+constexpr int kWgStagesMax = 3;
 constexpr int kWgThreads = 192;
 __host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile) {
   return kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // A 16 KB + 3 planes x (n_tile x 128 B)
 }
-__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile) {
-  return kWgStages * wg_stage_bytes(n_tile) + 1024 + 256;
+__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int stages) {
+  return uint32_t(stages) * wg_stage_bytes(n_tile) + 1024 + 256;
 }
 
+// One launch for every Linear layer: block -> (layer, m-tile, n-tile, split).
 __global__ void __launch_bounds__(kWgThreads, 1)
-    k_wgrad(const __grid_constant__ CUtensorMap tm_di, WgradArgs a) {
+    k_wgrad(const __grid_constant__ WgradMaps maps, WgradArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  int li = 0;
+  while (li + 1 < args.n_layers && int(blockIdx.x) >= args.layer[li + 1].block_start) ++li;
+  const WgradLayer a = args.layer[li];
+  const CUtensorMap* tm_di = &maps.m[li];
+  const int local = int(blockIdx.x) - a.block_start;
+  const int mt = local % a.m_tiles, ntile = (local / a.m_tiles) % a.n_tiles;
+  const int split = local / (a.m_tiles * a.n_tiles);
+  const int S = args.stages;
   const uint32_t stage_bytes = wg_stage_bytes(a.n_tile);
-  const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: 64 rows x n_tile cols
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgStages * stage_bytes);
-  uint64_t* empty = full + kWgStages;
-  uint64_t* acc_full = empty + kWgStages;
+  const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: n_tile rows x 64 cols
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* acc_full = empty + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x, ntile = blockIdx.y, split = blockIdx.z;
-  const int tq_per_b = a.T_pad / 64;
-  const int b0 = int((long long)a.B * split / a.splits);
-  const int b1 = int((long long)a.B * (split + 1) / a.splits);
+  const int tq_per_b = args.T_pad / 64;
+  const int b0 = int((long long)args.B * split / a.splits);
+  const int b1 = int((long long)args.B * (split + 1) / a.splits);
   const int total = (b1 - b0) * tq_per_b;
   const uint32_t tmem_cols = a.n_tile <= 32 ? 32u : (a.n_tile <= 64 ? 64u : (a.n_tile <= 128 ? 128u : 256u));
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kWgStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1 + 128);
       mbar_init(&empty[s], 1);
     }
@@ -976,15 +993,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (warp == 4) {
     if (elect_one()) {
-      tma_prefetch(&tm_di);
+      tma_prefetch(tm_di);
       for (int it = 0; it < total; ++it) {
-        const int s = it % kWgStages, ph = (it / kWgStages) & 1;
+        const int s = it % S, ph = (it / S) & 1;
         const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * ptile);
         uint8_t* Bp = smem + s * stage_bytes + kPlaneTile;
         for (int p = 0; p < 3; ++p)
-          tma_load_2d(Bp + p * ptile, &tm_di, &full[s], bb * a.T_pad + tq * 64,
+          tma_load_2d(Bp + p * ptile, tm_di, &full[s], bb * args.T_pad + tq * 64,
                       p * a.N_pad + ntile * a.n_tile);
       }
     }
@@ -993,7 +1010,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     const uint32_t idesc = idesc_bf16(128, a.n_tile, false, false);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
-        const int s = it % kWgStages, ph = (it / kWgStages) & 1;
+        const int s = it % S, ph = (it / S) & 1;
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t A = smem_u32(smem + s * stage_bytes);
@@ -1017,23 +1034,24 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     // stage it+1 are issued before waiting for stage it's slot.
     const int tid = threadIdx.x;
     const int k = mt * 128 + tid;  // this thread's A row
-    const bool in_row = a.kind != 0 || k < a.x_row_stride;
+    const bool in_row = a.kind != 0 || k < args.x_row_stride;
     auto fetch = [&](int it) -> uint64_t {
       if (it >= total || !in_row) return 0;
       const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
       if (a.kind == 0) {
-        const uint8_t* src = a.x + (size_t(a.rows[bb]) * (a.T_pad / 8) + tq * 8) * a.x_row_stride + k;
+        const uint8_t* src =
+            args.x + (size_t(args.rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride + k;
         uint64_t v = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v |= uint64_t(__ldg(src + size_t(j) * a.x_row_stride)) << (8 * j);
+        for (int j = 0; j < 8; ++j) v |= uint64_t(__ldg(src + size_t(j) * args.x_row_stride)) << (8 * j);
         return v;
       }
       return __ldg(reinterpret_cast<const unsigned long long*>(
-          a.s_tp + size_t(k) * (size_t(a.B) * a.T_pad / 32) + size_t(bb) * (a.T_pad / 32) + tq * 2));
+          a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) + size_t(bb) * (args.T_pad / 32) + tq * 2));
     };
     uint64_t cur = fetch(0);
     for (int it = 0; it < total; ++it) {
-      const int s = it % kWgStages, ph = (it / kWgStages) & 1;
+      const int s = it % S, ph = (it / S) & 1;
       const uint64_t nxt = fetch(it + 1);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t A = smem_u32(smem + s * stage_bytes);
@@ -1089,7 +1107,6 @@ struct Entry {
 };
 
 constexpr int kMaxEntries = 3 * 9;
-constexpr int kMaxLayers = 9;
 
 struct ReduceArgs {
   Entry entries[kMaxEntries];
