@@ -146,6 +146,9 @@ snn_status snn_forward_backward(snn_engine* e, const uint32_t* rows, float* loss
  * (optimize.hpp:260-299): epoch e shuffles with master.child(1+e).child(0),
  * drop-remainder batches.  metrics: [epochs][2] mean loss, mean accuracy. */
 snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics);
+/* Same loop for epochs [first_epoch, first_epoch + epochs) of the key schedule. */
+snn_status snn_train_epochs_from(snn_engine* e, size_t first_epoch, size_t epochs,
+                                 double* metrics);
 
 /* Asynchronous stepping for throughput measurement: enqueue one full step
  * (captured CUDA graph) on the engine stream with batch rows taken from the

@@ -1,0 +1,277 @@
+// spiketrain_b200.hpp -- header-only C++ mirror of the reference's training API
+// (spiketrain: network.hpp, optimize.hpp, surrogate.hpp, errors.hpp, data.hpp)
+// implemented over the engine's C ABI (snn_engine.h).  Code written against
+// spiketrain::train_step / train can switch namespaces and link
+// libsnn_b200.so; the numerics run on the B200, never on the CPU.
+//
+// Mirrored (reference file:line):
+//   errors        errors.hpp:9-64         exception classes <- snn_status
+//   ActivationDesc surrogate.hpp:134-157   name/slope/aux + default_activation_desc
+//   LinearLayer / LIFLayer / LILayer / NetworkSpec   network.hpp:23-65
+//   TrainConfig   optimize.hpp:116-133
+//   TrainState    optimize.hpp:135-141   (params live on the device)
+//   StepResult    optimize.hpp:143-147
+//   train_step    optimize.hpp:152-214
+//   train         optimize.hpp:237-299   (same key schedule; callback may stop)
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <variant>
+#include <vector>
+
+#include "snn_engine.h"
+
+namespace spiketrain_b200 {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ShapeError : Error { using Error::Error; };
+struct ArgumentError : Error { using Error::Error; };
+struct ContractError : Error { using Error::Error; };
+struct StateError : Error { using Error::Error; };
+struct FormatError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct SpecError : Error { using Error::Error; };
+struct ConfigError : Error { using Error::Error; };
+struct UnsupportedError : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };
+
+inline void check(snn_status st, const snn_engine* e) {
+  if (st == SNN_OK) return;
+  const std::string msg = snn_last_error(e);
+  switch (st) {
+    case SNN_ERR_SHAPE: throw ShapeError(msg);
+    case SNN_ERR_ARGUMENT: throw ArgumentError(msg);
+    case SNN_ERR_CONTRACT: throw ContractError(msg);
+    case SNN_ERR_STATE: throw StateError(msg);
+    case SNN_ERR_FORMAT: throw FormatError(msg);
+    case SNN_ERR_IO: throw IoError(msg);
+    case SNN_ERR_SPEC: throw SpecError(msg);
+    case SNN_ERR_CONFIG: throw ConfigError(msg);
+    case SNN_ERR_UNSUPPORTED: throw UnsupportedError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+// -------------------------------------------------------------- spec types
+struct ActivationDesc {
+  std::string name = "superspike";
+  double slope = 25.0;
+  double aux = 0.0;
+};
+
+inline ActivationDesc default_activation_desc(const std::string& name) {
+  if (name == "custom") return {"custom", 0.0, 0.0};
+  if (name == "superspike") return {"superspike", 25.0, 0.0};
+  if (name == "triangular") return {"triangular", 0.5, 0.0};
+  if (name == "arctan") return {"arctan", 2.0, 0.0};
+  if (name == "boxcar") return {"boxcar", 2.0, 0.5};
+  throw ArgumentError("unknown activation: " + name);
+}
+
+struct LinearLayer {
+  std::size_t out = 0;
+  bool bias = true;
+};
+struct LIFLayer {
+  std::vector<std::size_t> shape;
+  ActivationDesc activation = {"superspike", 25.0, 0.0};
+  double threshold = 1.0;
+};
+struct LILayer {
+  std::vector<std::size_t> shape;
+};
+using Layer = std::variant<LinearLayer, LIFLayer, LILayer>;
+
+struct NetworkSpec {
+  std::vector<std::size_t> input_shape;
+  std::vector<Layer> layers;
+};
+
+struct TrainConfig {
+  std::size_t epochs = 100;
+  std::size_t batch_size = 64;
+  double lr = 1e-3;
+  std::uint64_t seed = 0;
+  std::size_t unroll = 32;
+};
+
+struct PackedDataset {
+  std::vector<std::uint8_t> x;  // [N, ceil(T/8), input...] MSB-first
+  std::size_t n = 0;
+  std::size_t original_t = 0;
+  std::vector<std::int64_t> y;
+};
+
+struct StepResult {
+  float loss = 0;
+  double accuracy = 0;
+};
+
+struct EpochMetrics {
+  std::size_t epoch = 0;
+  double loss = 0;
+  double accuracy = 0;
+  double wall_ms = 0;
+};
+using EpochCallback = std::function<bool(const EpochMetrics&)>;
+
+namespace detail {
+
+inline int activation_id(const std::string& n) {
+  if (n == "custom") return SNN_ACT_CUSTOM;
+  if (n == "superspike") return SNN_ACT_SUPERSPIKE;
+  if (n == "triangular") return SNN_ACT_TRIANGULAR;
+  if (n == "arctan") return SNN_ACT_ARCTAN;
+  if (n == "boxcar") return SNN_ACT_BOXCAR;
+  throw ArgumentError("unknown activation: " + n);
+}
+
+// normalize() subset (network.hpp:125-157): [Linear, LIF]*k, Linear, LI
+inline snn_network_desc describe(const NetworkSpec& s) {
+  if (s.input_shape.empty()) throw SpecError("network: input shape not declared");
+  if (s.layers.empty()) throw SpecError("network: no layers");
+  if (!std::holds_alternative<LIFLayer>(s.layers.back()) &&
+      !std::holds_alternative<LILayer>(s.layers.back()))
+    throw SpecError("network must end in a lif or li readout");
+  if (s.layers.size() < 4 || s.layers.size() % 2)
+    throw UnsupportedError("engine supports [Linear, LIF]*k + Linear + LI");
+  snn_network_desc d{};
+  std::size_t in = 1;
+  for (auto v : s.input_shape) in *= v;
+  d.input = int32_t(in);
+  d.n_hidden = int32_t(s.layers.size() / 2 - 1);
+  if (d.n_hidden > SNN_MAX_HIDDEN) throw UnsupportedError("too many hidden layers");
+  for (int i = 0; i < d.n_hidden; ++i) {
+    const auto* lin = std::get_if<LinearLayer>(&s.layers[2 * i]);
+    const auto* lif = std::get_if<LIFLayer>(&s.layers[2 * i + 1]);
+    if (!lin || !lif) throw UnsupportedError("expected Linear + LIF pairs");
+    d.hidden[i] = int32_t(lin->out);
+    d.bias = lin->bias;
+    d.threshold = float(lif->threshold);
+    d.activation = activation_id(lif->activation.name);
+    d.slope = float(lif->activation.slope);
+    d.aux = float(lif->activation.aux);
+  }
+  const auto* lin = std::get_if<LinearLayer>(&s.layers[s.layers.size() - 2]);
+  if (!lin || !std::holds_alternative<LILayer>(s.layers.back()))
+    throw UnsupportedError("readout must be Linear + LI");
+  d.classes = int32_t(lin->out);
+  return d;
+}
+
+}  // namespace detail
+
+// TrainState: NetworkSpec + TrainConfig + device-resident params/optimizer state.
+class TrainState {
+ public:
+  TrainState(const NetworkSpec& spec, const TrainConfig& cfg, std::size_t original_t,
+             int device = 0)
+      : spec_(spec), cfg_(cfg), t_(original_t) {
+    const snn_network_desc d = detail::describe(spec);
+    snn_train_config c{};
+    c.batch_size = int32_t(cfg.batch_size);
+    c.time_steps = int32_t(original_t);
+    c.lr = float(cfg.lr);
+    c.beta1 = 0.9f;
+    c.beta2 = 0.999f;
+    c.eps = 1e-8f;
+    c.seed = cfg.seed;
+    c.unroll = int32_t(cfg.unroll);
+    snn_engine* e = nullptr;
+    check(snn_engine_create(&d, &c, device, &e), nullptr);
+    eng_.reset(e);
+    check(snn_param_count(e, &n_params_), e);
+  }
+
+  snn_engine* engine() const { return eng_.get(); }
+  const NetworkSpec& spec() const { return spec_; }
+  const TrainConfig& cfg() const { return cfg_; }
+  std::size_t original_t() const { return t_; }
+  std::size_t scalar_count() const { return n_params_; }
+
+  // NetworkParams flat view (entry order of network.hpp:210-226)
+  std::vector<float> params() const {
+    std::vector<float> p(n_params_);
+    check(snn_get_params(eng_.get(), p.data(), p.size()), eng_.get());
+    return p;
+  }
+  void set_params(const std::vector<float>& p) {
+    check(snn_set_params(eng_.get(), p.data(), p.size()), eng_.get());
+  }
+  std::uint64_t optimizer_step() const {
+    std::uint64_t s = 0;
+    check(snn_get_opt_state(eng_.get(), nullptr, nullptr, &s, n_params_), eng_.get());
+    return s;
+  }
+
+ private:
+  struct Deleter {
+    void operator()(snn_engine* e) const { snn_engine_destroy(e); }
+  };
+  NetworkSpec spec_;
+  TrainConfig cfg_;
+  std::size_t t_;
+  std::size_t n_params_ = 0;
+  std::unique_ptr<snn_engine, Deleter> eng_;
+};
+
+// optimize.hpp:152-156: one fused step on a packed host batch.
+inline StepResult train_step(TrainState& st, const std::vector<std::uint8_t>& packed_x,
+                             std::size_t original_t, const std::vector<std::int64_t>& targets) {
+  if (original_t != st.original_t())
+    throw FormatError("unpack_time: packed extent inconsistent with T=" + std::to_string(original_t));
+  if (targets.size() != st.cfg().batch_size)
+    throw ArgumentError("targets: " + std::to_string(targets.size()) + " labels for batch " +
+                        std::to_string(st.cfg().batch_size));
+  StepResult r;
+  check(snn_train_step_packed(st.engine(), packed_x.data(), targets.data(), &r.loss, &r.accuracy),
+        st.engine());
+  return r;
+}
+
+struct TrainResult {
+  std::vector<float> params;
+  std::vector<EpochMetrics> metrics;
+  std::uint64_t step = 0;
+};
+
+// optimize.hpp:260-299: epoch loop over the dataset staged once in HBM.
+inline TrainResult train(TrainState& st, const PackedDataset& data,
+                         const EpochCallback& on_epoch = nullptr) {
+  check(snn_stage_dataset(st.engine(), data.x.data(), data.n, data.y.data()), st.engine());
+  TrainResult out;
+  for (std::size_t e = 0; e < st.cfg().epochs; ++e) {
+    const auto t0 = std::chrono::steady_clock::now();
+    double m[2];
+    // one epoch with the reference's epoch key (the engine keeps the epoch index)
+    check(snn_train_epochs_from(st.engine(), e, 1, m), st.engine());
+    EpochMetrics em;
+    em.epoch = e;
+    em.loss = m[0];
+    em.accuracy = m[1];
+    em.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    out.metrics.push_back(em);
+    if (on_epoch && on_epoch(em)) break;
+  }
+  out.params = st.params();
+  out.step = st.optimizer_step();
+  return out;
+}
+
+// optimize.hpp:237-256: fresh state (init from master.child(0)) + epoch loop.
+inline TrainResult train(const NetworkSpec& spec, const TrainConfig& cfg, const PackedDataset& data,
+                         const EpochCallback& on_epoch = nullptr, int device = 0) {
+  if (cfg.batch_size == 0) throw ArgumentError("train: batch size 0");
+  TrainState st(spec, cfg, data.original_t, device);
+  return train(st, data, on_epoch);
+}
+
+}  // namespace spiketrain_b200

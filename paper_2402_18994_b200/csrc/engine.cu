@@ -976,7 +976,8 @@ snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
   });
 }
 
-snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics) {
+snn_status snn_train_epochs_from(snn_engine* e, size_t first_epoch, size_t epochs,
+                                 double* metrics) {
   if (!e) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
     const size_t n = e->data.n;
@@ -985,7 +986,8 @@ snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics) {
     if (gb > n) fail(SNN_ERR_ARGUMENT, "shuffle: batch size %zu for %zu examples", gb, n);
     const uint64_t master = hostrng::from_seed(e->cfg.seed);
     const size_t nb = n / gb;
-    for (size_t ep = 0; ep < epochs; ++ep) {
+    for (size_t k = 0; k < epochs; ++k) {
+      const size_t ep = first_epoch + k;
       const uint64_t ek = hostrng::child(master, 1 + ep);
       const std::vector<uint32_t> perm = hostrng::permutation(hostrng::child(ek, 0), n);
       double ls = 0, as = 0;
@@ -997,11 +999,15 @@ snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics) {
         as += a;
       }
       if (metrics) {
-        metrics[2 * ep] = ls / double(nb ? nb : 1);
-        metrics[2 * ep + 1] = as / double(nb ? nb : 1);
+        metrics[2 * k] = ls / double(nb ? nb : 1);
+        metrics[2 * k + 1] = as / double(nb ? nb : 1);
       }
     }
   });
+}
+
+snn_status snn_train_epochs(snn_engine* e, size_t epochs, double* metrics) {
+  return snn_train_epochs_from(e, 0, epochs, metrics);
 }
 
 snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_steps) {

@@ -195,3 +195,48 @@ def test_determinism(orc):
         outs.append((m, e.get_params()))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+BIG = [
+    ("c3-shape", Net(inp=700, hidden=(1024, 1024), classes=20), 2, 256, 1.0),
+    ("c5-shape", Net(inp=700, hidden=(256, 256), classes=20), 2, 1000, 1.5),
+]
+
+
+@pytest.mark.parametrize("case", BIG, ids=[c[0] for c in BIG])
+def test_baseline_shapes(orc, case):
+    """Config C3 (700-1024-1024-20, T=256) and C5 (700-256-256-20, T=1000) shapes."""
+    _, net, B, T, scale = case
+    params = orc.init(net, orc.key_child(orc.key_from_seed(0), 0)) * np.float32(scale)
+    x, y = orc.synth_raster(20, B, T, 700, 1)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    eng.debug(True)
+    loss, acc = eng.forward_backward(np.arange(B, dtype=np.uint32))
+    ref = orc.forward_backward(net, params, pk, T, y, want_spikes=True)
+    assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    for l in range(2):
+        assert (eng.fetch("spikes", l) == ref["spikes"][l]).mean() >= SPIKE_AGREE
+    check_grads(orc, net, eng.get_grads(), ref["grads"])
+
+
+def test_device_synth_is_bit_exact(orc):
+    """synth_raster + pack_time generated in HBM == the reference's host version."""
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    for T, n in ((128, 40), (19, 7), (1000, 3)):
+        eng = Engine(shd_spec(), TrainConfig(batch_size=1), T)
+        eng.synth_dataset(n, seed=1)
+        pk, y = eng.read_dataset(0, n)
+        x_ref, y_ref = orc.synth_raster(20, n, T, 700, 1)
+        assert np.array_equal(pk, orc.pack_time(x_ref))
+        assert np.array_equal(y, y_ref)
+
+
+def test_epoch_permutation_matches_reference(orc):
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    eng = Engine(shd_spec(), TrainConfig(batch_size=1, seed=7), 8)
+    for e in (0, 3):
+        ref = orc.permutation(orc.key_child(orc.key_child(orc.key_from_seed(7), 1 + e), 0), 500)
+        assert np.array_equal(eng.epoch_permutation(e, 500), ref)
