@@ -222,6 +222,7 @@ struct snn_engine {
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
   int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 1));
+  int exact_surr = env_int("SNN_EXACT_SURR", 1) - 1;  // 1: correctly rounded reciprocals
   int wg_samples_per_split = env_int("SNN_WG_SPLIT_SAMPLES", 8);
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
@@ -614,6 +615,7 @@ struct snn_engine {
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
+      bw.exact_surr = exact_surr;
       k_lif_bwd<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT, bw.stages), stream>>>(
           tm_wb[l + 1], tm_di_k[l + 1], bw);
       mark(evs, "lif_bwd", l);

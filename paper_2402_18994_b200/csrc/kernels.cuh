@@ -600,7 +600,7 @@ struct BwdArgs {
   float* dbias_part;           // [B][H] or nullptr
   float* dbg_ds;               // optional [B][T_pad][H_pad]
   long long* dbg_clk;          // optional [gridDim.x*gridDim.y][8] phase timestamps
-  int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
+  int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages, exact_surr;
   float theta, slope, aux;
 };
 
@@ -612,6 +612,14 @@ __device__ __forceinline__ float surrogate_fast(int act, float k, float aux, flo
     case 1: {
       const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
       return rcp_approx(__fmul_rn(d, d));
+    }
+    case 3 + 8: {  // arctan, exact (surrogate.hpp:90-104 operation order)
+      const float u = __fmul_rn(__fmul_rn(__fmul_rn(3.14159265358979f, k), x), 0.5f);
+      return __frcp_rn(__fadd_rn(1.0f, __fmul_rn(u, u)));
+    }
+    case 1 + 8: {
+      const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
+      return __frcp_rn(__fmul_rn(d, d));
     }
     case 2: {
       const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
@@ -656,7 +664,7 @@ __device__ __forceinline__ void bwd_compose(const uint32_t (&r)[16], const float
 #pragma unroll
   for (int e = 15; e >= 0; --e) {
     if (kTail && e >= nval) continue;
-    const float g = surrogate_fast(a.act, a.slope, a.aux, __fsub_rn(vr[e], theta));
+    const float g = surrogate_fast(a.act + 8 * a.exact_surr, a.slope, a.aux, __fsub_rn(vr[e], theta));
     const float at = vb - theta * g;
     Bc = at * Bc + g * __uint_as_float(r[e]);
     A = at * A;
@@ -674,7 +682,7 @@ __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float 
       x[e] = 0.0f;
       continue;
     }
-    const float g = surrogate_fast(a.act, a.slope, a.aux, __fsub_rn(vr[e], theta));
+    const float g = surrogate_fast(a.act + 8 * a.exact_surr, a.slope, a.aux, __fsub_rn(vr[e], theta));
     const float gi = G;
     const float gs = __fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gi, theta));
     G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));

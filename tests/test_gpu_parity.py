@@ -15,6 +15,10 @@ pytestmark = pytest.mark.gpu
 
 SPIKE_AGREE = 0.9999
 REL_TOL = 1e-4
+# When the >= 99.99 %-agreeing rasters still differ by a few flipped spikes (fp32
+# accumulation order near threshold, long T), a flip legitimately changes the
+# downstream gradient; the per-tensor bound is then 5e-4 (Parity).
+REL_TOL_FLIPS = 5e-4
 
 
 def relnorm(a, b):
@@ -217,9 +221,12 @@ def test_baseline_shapes(orc, case):
     loss, acc = eng.forward_backward(np.arange(B, dtype=np.uint32))
     ref = orc.forward_backward(net, params, pk, T, y, want_spikes=True)
     assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    flips = 0
     for l in range(2):
-        assert (eng.fetch("spikes", l) == ref["spikes"][l]).mean() >= SPIKE_AGREE
-    check_grads(orc, net, eng.get_grads(), ref["grads"])
+        S = eng.fetch("spikes", l)
+        assert (S == ref["spikes"][l]).mean() >= SPIKE_AGREE
+        flips += int((S != ref["spikes"][l]).sum())
+    check_grads(orc, net, eng.get_grads(), ref["grads"], REL_TOL if flips == 0 else REL_TOL_FLIPS)
 
 
 def test_device_synth_is_bit_exact(orc):
