@@ -218,7 +218,10 @@ struct snn_engine {
   int rank = 0, world = 1;
   bool planes_dirty = true;
   // pipeline depths (smem per CTA decides how many CTAs share an SM)
-  int fwd_stages = env_int("SNN_FWD_STAGES", 1);
+  int fwd_stages = std::min(kFwdStagesMax, env_int("SNN_FWD_STAGES", 2));
+  int fwd_spb_env = env_int("SNN_FWD_SPB", 2);
+  // samples per forward CTA: N = spb * TT <= 256 and TMEM (doubled for NT > 1) <= 512
+  int fwd_spb(int tt) const { return std::max(1, std::min(fwd_spb_env, std::min(kFwdSpbMax, 256 / tt))); }
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
   int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 1));
@@ -362,7 +365,7 @@ struct snn_engine {
       wg_maps.m[j] = tm_di_w[j];
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(fwd_smem_bytes(TT, kFwdStagesMax))));
+                            int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax))));
     CK(cudaFuncSetAttribute(k_lif_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -574,8 +577,9 @@ struct snn_engine {
       f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
       f.theta = net.threshold;
       f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
-      k_lif_fwd<<<dim3(B, H_pad[l] / 128), kFwdThreads, fwd_smem_bytes(TT, f.stages), stream>>>(
-          tm_wt[l], f);
+      f.spb = fwd_spb(TT);
+      k_lif_fwd<<<dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128), kFwdThreads,
+                  fwd_smem_bytes(TT, f.spb, f.stages), stream>>>(tm_wt[l], f);
       mark(evs, "lif_fwd", l);
     }
     // readout + loss + LI backward

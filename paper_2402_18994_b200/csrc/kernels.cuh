@@ -138,7 +138,10 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // ============================================================================
 // K1  k_lif_fwd: I^T[n][t] = sum_k Wt[n][k] * A[t][k] on tcgen05 (3 bf16 planes
 // of W, binary A exact in bf16), then the LIF scan epilogue straight from TMEM.
-// grid (B, H_pad/128); block 320: w0-3 scan, w4-7 B-operand decode, w8 TMA, w9 MMA.
+// One CTA = 128 neurons x SPB samples: the samples' activation rows are stacked
+// into one N = SPB*TT MMA, so each W-plane tile streamed from L2 feeds SPB samples.
+// grid (ceil(B/SPB), H_pad/128); block 448: w0-7 scan (sample w/4, TMEM quadrant
+// w%4), w8-11 B-operand decode, w12 TMA, w13 MMA.
 // ============================================================================
 struct FwdArgs {
   const uint8_t* x;       // staged dataset (layer 0)
@@ -151,23 +154,46 @@ struct FwdArgs {
   uint32_t* s_tp;         // [H_pad][B*T_pad/32]
   float* dbg_i;           // optional [B][T_pad][H_pad] raw projection
   long long* dbg_clk;     // optional [gridDim.x*gridDim.y][8] phase timestamps
-  int B, T, T_pad, TT, NT, K_pad, H, H_pad, in_kind, stages;
+  int B, T, T_pad, TT, NT, K_pad, H, H_pad, in_kind, stages, spb;
   float theta;
 };
 
-constexpr int kFwdStagesMax = 3;
-constexpr int kFwdThreads = 320;
+constexpr int kFwdStagesMax = 2;
+constexpr int kFwdSpbMax = 2;
+constexpr int kFwdScanWarps = 4 * kFwdSpbMax;
+constexpr int kFwdThreads = 32 * (kFwdScanWarps + 4 + 2);
 constexpr uint32_t kPlaneTile = 128 * 128;  // 128 rows x 64 bf16 = 16 KB
 
-__host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT) {
-  return 3 * kPlaneTile + uint32_t(TT) * 128u;
+__host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT, int spb) {
+  return 3 * kPlaneTile + uint32_t(spb * TT) * 128u;
 }
-__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int stages) {
-  return uint32_t(stages) * fwd_stage_bytes(TT) + 1024 + 256;
+__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int spb, int stages) {
+  return uint32_t(stages) * fwd_stage_bytes(TT, spb) + 1024 + 256;
 }
-// TMEM columns: one TT-wide accumulator, doubled when several t-tiles pipeline.
-__host__ __device__ constexpr uint32_t acc_cols(int TT, int NT) {
-  return NT > 1 ? (TT >= 128 ? 256u : 128u) : (TT >= 128 ? 128u : 64u);
+// TMEM columns for N-wide accumulators, doubled when several t-tiles pipeline.
+__host__ __device__ constexpr uint32_t tmem_cols_for(int N, int NT) {
+  const int need = NT > 1 ? 2 * N : N;
+  return need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
+}
+__host__ __device__ constexpr uint32_t acc_cols(int TT, int NT) { return tmem_cols_for(TT, NT); }
+
+__device__ __forceinline__ void tmem_alloc_any(uint32_t cols, uint32_t* slot) {
+  switch (cols) {
+    case 32: tmem_alloc<32>(slot); break;
+    case 64: tmem_alloc<64>(slot); break;
+    case 128: tmem_alloc<128>(slot); break;
+    case 256: tmem_alloc<256>(slot); break;
+    default: tmem_alloc<512>(slot); break;
+  }
+}
+__device__ __forceinline__ void tmem_dealloc_any(uint32_t cols, uint32_t taddr) {
+  switch (cols) {
+    case 32: tmem_dealloc<32>(taddr); break;
+    case 64: tmem_dealloc<64>(taddr); break;
+    case 128: tmem_dealloc<128>(taddr); break;
+    case 256: tmem_dealloc<256>(taddr); break;
+    default: tmem_dealloc<512>(taddr); break;
+  }
 }
 
 // 32 LIF steps of one neuron (neuron.hpp:127-136 op order, bit-exact):
@@ -200,11 +226,13 @@ __device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, fl
   }
 }
 
-__global__ void __launch_bounds__(kFwdThreads, 2)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     k_lif_fwd(const __grid_constant__ CUtensorMap tm_w, FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const uint32_t stage_bytes = fwd_stage_bytes(a.TT);
+  const int SPB = a.spb;
+  const int NTOT = SPB * a.TT;  // MMA N (stacked samples)
+  const uint32_t stage_bytes = fwd_stage_bytes(a.TT, SPB);
   const int S = a.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
@@ -213,13 +241,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x, nt = blockIdx.y;
-  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * 8 : nullptr;
+  const int b0 = blockIdx.x * SPB, nt = blockIdx.y;
+  const int nsamp = min(SPB, a.B - b0);
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
   if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
-  const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
+  const uint32_t tmem_cols = tmem_cols_for(NTOT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
+  const int scan_threads = 128 * nsamp;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -228,21 +258,18 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], scan_threads);
     }
     fence_barrier_init();
   }
-  if (warp == 0) {
-    if (tmem_cols == 256) tmem_alloc<256>(tmem_slot);
-    else if (tmem_cols == 128) tmem_alloc<128>(tmem_slot);
-    else tmem_alloc<64>(tmem_slot);
-  }
+  if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int dec_warp0 = kFwdScanWarps, tma_warp = kFwdScanWarps + 4, mma_warp = tma_warp + 1;
 
-  if (warp == 8) {
+  if (warp == tma_warp) {
     // ---------------- TMA producer: the three W^T planes of each k-block
     if (elect_one()) {
       tma_prefetch(&tm_w);
@@ -256,9 +283,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       }
     }
     __syncwarp();
-  } else if (warp == 9) {
-    // ---------------- MMA issuer (one thread)
-    const uint32_t idesc = idesc_bf16(128, a.TT, false, false);
+  } else if (warp == mma_warp) {
+    // ---------------- MMA issuer (one thread), N = SPB*TT stacked sample rows
+    const uint32_t idesc = idesc_bf16(128, NTOT, false, false);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1;
@@ -271,7 +298,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         tc_fence_after();
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bt = A + 3 * kPlaneTile;
-        const uint32_t d = tmem + buf * a.TT;
+        const uint32_t d = tmem + buf * NTOT;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
@@ -286,53 +313,62 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
-    // ---------------- B-operand producers: activations -> bf16 {0,1} rows t, cols k.
-    // Global loads of stage it+1 are issued before waiting for stage it's slot.
-    const int tid = threadIdx.x - 128;
+  } else if (warp >= dec_warp0) {
+    // ---------------- B-operand producers: activations -> bf16 {0,1} rows t, cols k,
+    // sample s's rows at [s*TT, (s+1)*TT).  Loads of stage it+1 issue before the wait.
+    const int tid = threadIdx.x - dec_warp0 * 32;
     const size_t kwords = size_t(a.K_pad) / 32;
-    // kind 0: unit = (t-group g, 8-feature chunk q), TT units; kind 1: unit = row t.
-    const bool active = tid < a.TT;
-    const size_t xrow = (a.in_kind == 0) ? size_t(a.rows[b]) : 0;
-    auto fetch = [&](int it) -> uint64_t {
-      if (!active || it >= total) return 0;
+    const int units = SPB * a.TT;  // kind 0: (sample, t-group, 8-feature chunk); kind 1: row
+    auto fetch = [&](int it, int u) -> uint64_t {
+      if (u >= units || it >= total) return 0;
       const int tt = it / KB, kb = it % KB;
+      const int sm = u / a.TT, r = u % a.TT;
+      if (sm >= nsamp) return 0;
       if (a.in_kind == 0) {
-        const int g = tid >> 3, q = tid & 7;
+        const int g = r >> 3, q = r & 7;
         return __ldg(reinterpret_cast<const unsigned long long*>(
-            a.x + (xrow * (a.T_pad / 8) + tt * (a.TT / 8) + g) * size_t(a.K_pad) + kb * 64 + q * 8));
+            a.x + (size_t(a.rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8) + g) * size_t(a.K_pad) +
+            kb * 64 + q * 8));
       }
       return __ldg(reinterpret_cast<const unsigned long long*>(
-          a.s_in + (size_t(b) * a.T_pad + tt * a.TT + tid) * kwords + kb * 2));
+          a.s_in + (size_t(b0 + sm) * a.T_pad + tt * a.TT + r) * kwords + kb * 2));
     };
-    uint64_t cur = fetch(0);
+    uint64_t cur0 = fetch(0, tid), cur1 = fetch(0, tid + 128);
     for (int it = 0; it < total; ++it) {
       const int s = it % S, ph = (it / S) & 1;
-      const uint64_t nxt = fetch(it + 1);
+      const uint64_t nxt0 = fetch(it + 1, tid), nxt1 = fetch(it + 1, tid + 128);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t Bt = smem_u32(smem + s * stage_bytes + 3 * kPlaneTile);
-      if (active) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = tid + 128 * h;
+        if (u >= units) continue;
+        const uint64_t cur = h == 0 ? cur0 : cur1;
+        const int sm = u / a.TT, r = u % a.TT;
         if (a.in_kind == 0) {
           // dataset bytes [row][t/8][k], bit 7-(t%8): 8 k of one t-group -> 8 rows
-          const int g = tid >> 3, q = tid & 7;
+          const int g = r >> 3, q = r & 7;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            st_shared_v4(Bt + sw128_off(8 * g + j, q),
+            st_shared_v4(Bt + sw128_off(sm * a.TT + 8 * g + j, q),
                          expand_bytes01((cur >> (7 - j)) & 0x0101010101010101ull));
         } else {
           // neuron-packed spike words: row t, 2 words = 64 k
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            st_shared_v4(Bt + sw128_off(tid, q), expand_bits_lsb(uint32_t(cur >> (8 * q)) & 0xFFu));
+            st_shared_v4(Bt + sw128_off(sm * a.TT + r, q), expand_bits_lsb(uint32_t(cur >> (8 * q)) & 0xFFu));
         }
       }
       fence_async_smem();
       mbar_arrive(&full[s]);
-      cur = nxt;
+      cur0 = nxt0;
+      cur1 = nxt1;
     }
-  } else {
-    // ---------------- LIF scan epilogue: thread = neuron (TMEM lane)
-    const int n = nt * 128 + warp * 32 + lane;
+  } else if (warp / 4 < nsamp) {
+    // ---------------- LIF scan epilogue: thread = neuron (TMEM lane) of sample warp/4
+    const int sm = warp >> 2, q = warp & 3;
+    const int b = b0 + sm;
+    const int n = nt * 128 + q * 32 + lane;
     const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
     const float bn = (a.bias != nullptr && n < a.H) ? a.bias[n] : 0.0f;
     const size_t hw = size_t(a.H_pad) / 32;
@@ -345,12 +381,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       if (clk != nullptr && threadIdx.x == 0 && tt == 0) clk[1] = clock64();
       for (int c = 0; c < a.TT / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + buf * a.TT + c * 32, r);
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + buf * NTOT + sm * a.TT + c * 32, r);
         tmem_ld_wait();
         const int t0 = tt * a.TT + c * 32;
         if (t0 >= a.T) {
           // padded steps: no spikes (V rows beyond T are never read)
-          a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + warp] = 0u;
+          a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + q] = 0u;
           a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = 0u;
           continue;
         }
@@ -361,7 +397,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
                           a.T - t0, vb, bn, a.theta, lane, v, myword, tmask);
         else
           lif_chunk<false>(r, vp, nullptr, a.H_pad, 32, vb, 0.0f, a.theta, lane, v, myword, tmask);
-        a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + warp] = myword;
+        a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + q] = myword;
         a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = tmask;
       }
       tc_fence_before();
@@ -374,9 +410,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   if (clk != nullptr && threadIdx.x == 0) clk[3] = clock64();
   if (warp == 0) {
     tc_fence_after();
-    if (tmem_cols == 256) tmem_dealloc<256>(tmem);
-    else if (tmem_cols == 128) tmem_dealloc<128>(tmem);
-    else tmem_dealloc<64>(tmem);
+    tmem_dealloc_any(tmem_cols, tmem);
   }
 }
 
