@@ -131,6 +131,12 @@ __device__ __forceinline__ float rcp_approx(float y) {
   return r;
 }
 
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
@@ -244,9 +250,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int b0 = blockIdx.x * SPB, nt = blockIdx.y;
   const int nsamp = min(SPB, a.B - b0);
   long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
-  if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[0] = clock64();
+    clk[6] = globaltimer();
+  }
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
+  // k-block order rotated per CTA: concurrent CTAs stream different W tiles
+  const int rot = int(blockIdx.x) % KB;
   const uint32_t tmem_cols = tmem_cols_for(NTOT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
   const int scan_threads = 128 * nsamp;
@@ -274,7 +285,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (elect_one()) {
       tma_prefetch(&tm_w);
       for (int it = 0; it < total; ++it) {
-        const int s = it % S, ph = (it / S) & 1, kb = it % KB;
+        const int s = it % S, ph = (it / S) & 1, kb = (it % KB + rot) % KB;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile);
         uint8_t* A = smem + s * stage_bytes;
@@ -289,7 +300,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1;
-        const int tt = it / KB, kb = it % KB, buf = tt % nbuf;
+        const int tt = it / KB, kb = it % KB, buf = tt % nbuf;  // kb: position in the tile
         if (kb == 0 && tt >= nbuf) {
           mbar_wait(&acc_empty[buf], ((tt - nbuf) / nbuf) & 1);
           tc_fence_after();
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int units = SPB * a.TT;  // kind 0: (sample, t-group, 8-feature chunk); kind 1: row
     auto fetch = [&](int it, int u) -> uint64_t {
       if (u >= units || it >= total) return 0;
-      const int tt = it / KB, kb = it % KB;
+      const int tt = it / KB, kb = (it % KB + rot) % KB;
       const int sm = u / a.TT, r = u % a.TT;
       if (sm >= nsamp) return 0;
       if (a.in_kind == 0) {
@@ -407,7 +418,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
 
   __syncthreads();
-  if (clk != nullptr && threadIdx.x == 0) clk[3] = clock64();
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[3] = clock64();
+    clk[7] = globaltimer();
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc_any(tmem_cols, tmem);
@@ -728,7 +742,7 @@ __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float 
 
 constexpr int kBwdSeg = 2;                        // time segments per t-tile
 constexpr int kBwdScanThreads = 128 * kBwdSeg;
-constexpr int kBwdThreads = kBwdScanThreads + 64;  // + TMA warp + MMA warp
+constexpr int kBwdThreads = kBwdScanThreads + 32;  // + control warp (lane 0 TMA, lane 1 MMA)
 __host__ __device__ constexpr uint32_t bwd_stage_bytes(int TT) {
   return 3 * kPlaneTile + 3 * uint32_t(TT) * 128u;
 }
@@ -785,9 +799,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   const uint32_t tmem = *tmem_slot;
   const int cols_total = a.B * a.T_pad;
 
-  const int tma_warp = kBwdScanThreads / 32, mma_warp = tma_warp + 1;
-  if (warp == tma_warp) {
-    if (elect_one()) {
+  const int ctl_warp = kBwdScanThreads / 32;
+  if (warp == ctl_warp) {
+    if (lane == 0) {
       tma_prefetch(&tm_w);
       tma_prefetch(&tm_di);
       for (int it = 0; it < total; ++it) {
@@ -804,12 +818,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
                         b * a.T_pad + tt * a.TT + h * 64, p * a.K_pad + kb * 64);
         }
       }
-    }
-    __syncwarp();
-  } else if (warp == mma_warp) {
+    } else if (lane == 1) {
     // A: K-major W planes; B: MN-major dI planes (t contiguous), LBO = 64-t block
     const uint32_t idesc = idesc_bf16(128, a.TT, false, true);
-    if (elect_one()) {
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1;
         const int j = it / KB, kb = it % KB, buf = j % nbuf;
@@ -862,16 +873,23 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       mbar_wait(&acc_full[buf], (j / nbuf) & 1);
       tc_fence_after();
       if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[1] = clock64();
-      // ---- pass 1: compose the segment's affine map, t descending
+      // ---- pass 1: compose the segment's affine map, t descending.  The membranes
+      // of the next 16-step sub-chunk are loaded while this one is processed.
       float A = 1.0f, Bc = 0.0f;
       const float* vseg = vrow + size_t(t_lo) * a.H_pad;
-      for (int c0 = seg_len - 16; c0 >= 0; c0 -= 16) {
+      const int top = seg_len - 16;
+      float vr[16], vn[16];
+      load_v16(vseg + size_t(top) * a.H_pad, a.H_pad, t_hi - (t_lo + top), vn);
+      for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vr[e] = vn[e];
+        // next: c0 - 16, or (end of pass 1) the top sub-chunk again for pass 3
+        const int cn = c0 >= 16 ? c0 - 16 : top;
+        load_v16(vseg + size_t(cn) * a.H_pad, a.H_pad, t_hi - (t_lo + cn), vn);
         if (nval <= 0) continue;
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
-        float vr[16];
-        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
         tmem_ld_wait();
         if (nval >= 16) bwd_compose<false>(r, vr, 16, vb, theta, a, A, Bc);
         else bwd_compose<true>(r, vr, nval, vb, theta, a, A, Bc);
@@ -887,13 +905,14 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
       if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[3] = clock64();
       // ---- pass 3: exact-order replay of my segment
-      for (int c0 = seg_len - 16; c0 >= 0; c0 -= 16) {
+      for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vr[e] = vn[e];
+        if (c0 >= 16) load_v16(vseg + size_t(c0 - 16) * a.H_pad, a.H_pad, t_hi - (t_lo + c0 - 16), vn);
         if (nval <= 0) continue;
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
-        float vr[16];
-        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
         tmem_ld_wait();
         if (a.dbg_ds != nullptr) {
 #pragma unroll

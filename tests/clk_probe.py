@@ -18,3 +18,9 @@ for s, name in enumerate(names):
     n = 8 if name == "readout" else (4 if name.startswith("fwd") else 7)
     d = np.diff(c[:, :n], axis=1)
     print(f"{name:8s} phase cycles median {np.median(d, axis=0).astype(int).tolist()} max {d.max(axis=0).tolist()} total med {int(np.median(c[:, n-1]-c[:, 0]))}")
+for s, name in ((1, "fwd0"), (2, "fwd1")):
+    c = clk[s]
+    valid = c[:, 6] > 0
+    st, en = c[valid, 6], c[valid, 7]
+    t0 = st.min()
+    print(f"{name}: CTAs {valid.sum()}  start spread {(st.max()-t0)/1e3:.1f} us  end spread {(en.min()-t0)/1e3:.1f}..{(en.max()-t0)/1e3:.1f} us  per-CTA median {np.median(en-st)/1e3:.1f} us")
