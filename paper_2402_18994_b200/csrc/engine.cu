@@ -225,7 +225,6 @@ struct snn_engine {
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
   int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 1));
-  int exact_surr = env_int("SNN_EXACT_SURR", 1) - 1;  // 1: correctly rounded reciprocals
   int wg_samples_per_split = env_int("SNN_WG_SPLIT_SAMPLES", 8);
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
@@ -366,8 +365,9 @@ struct snn_engine {
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax))));
-    CK(cudaFuncSetAttribute(k_lif_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(bwd_smem_bytes(TT, 2))));
+    for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(wg_smem_bytes(128, kWgStagesMax))));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -539,6 +539,17 @@ struct snn_engine {
     CK(cudaStreamSynchronize(stream));
   }
 
+  void launch_bwd(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
+                  const BwdArgs& bw) {
+    switch (act) {
+      case 1: k_lif_bwd<1><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
+      case 2: k_lif_bwd<2><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
+      case 3: k_lif_bwd<3><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
+      case 4: k_lif_bwd<4><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
+      default: k_lif_bwd<0><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
+    }
+  }
+
   // ---------------------------------------------------------------- step
   int launches_per_step() const { return 2 * L + 5; }
 
@@ -619,9 +630,8 @@ struct snn_engine {
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
-      bw.exact_surr = exact_surr;
-      k_lif_bwd<<<dim3(B, H_pad[l] / 128), kBwdThreads, bwd_smem_bytes(TT, bw.stages), stream>>>(
-          tm_wb[l + 1], tm_di_k[l + 1], bw);
+      launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages),
+                 tm_wb[l + 1], tm_di_k[l + 1], bw);
       mark(evs, "lif_bwd", l);
     }
     // weight gradients: one launch over every Linear layer (split-K partials)

@@ -648,39 +648,29 @@ struct BwdArgs {
   float* dbias_part;           // [B][H] or nullptr
   float* dbg_ds;               // optional [B][T_pad][H_pad]
   long long* dbg_clk;          // optional [gridDim.x*gridDim.y][8] phase timestamps
-  int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages, exact_surr;
+  int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
   float theta, slope, aux;
 };
 
-// Surrogate for the backward sweep with the divisions of surrogate.hpp
-// evaluated as approximate reciprocals (<= 1 ulp; the backward is checked to
-// the 1e-4 gradient tolerance, the bit-exact parts are the forward scans).
-__device__ __forceinline__ float surrogate_fast(int act, float k, float aux, float x) {
-  switch (act) {
-    case 1: {
-      const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
-      return rcp_approx(__fmul_rn(d, d));
-    }
-    case 3 + 8: {  // arctan, exact (surrogate.hpp:90-104 operation order)
-      const float u = __fmul_rn(__fmul_rn(__fmul_rn(3.14159265358979f, k), x), 0.5f);
-      return __frcp_rn(__fadd_rn(1.0f, __fmul_rn(u, u)));
-    }
-    case 1 + 8: {
-      const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
-      return __frcp_rn(__fmul_rn(d, d));
-    }
-    case 2: {
-      const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
-      return 0.0f < r ? r : 0.0f;
-    }
-    case 3: {
-      const float u = __fmul_rn(k * 1.57079632679489662f, x);
-      return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
-    }
-    case 4:
-      return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
-    default:
-      return 1.0f;
+// Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
+// the unrolled step bodies stay branch-free; divisions evaluated as approximate
+// reciprocals (<= 1 ulp; the backward is checked to the 1e-4 gradient bound,
+// the bit-exact parts are the forward scans).
+template <int kAct>
+__device__ __forceinline__ float surrogate_t(float k, float aux, float x) {
+  if constexpr (kAct == 1) {  // superspike 1/(1+k|x|)^2
+    const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
+    return rcp_approx(__fmul_rn(d, d));
+  } else if constexpr (kAct == 2) {  // triangular max(0, 1-|kx|)
+    const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
+    return 0.0f < r ? r : 0.0f;
+  } else if constexpr (kAct == 3) {  // arctan 1/(1+(pi k x/2)^2)
+    const float u = __fmul_rn(k * 1.57079632679489662f, x);
+    return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
+  } else if constexpr (kAct == 4) {  // boxcar
+    return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
+  } else {  // custom straight-through
+    return 1.0f;
   }
 }
 
@@ -705,14 +695,14 @@ __device__ __forceinline__ void load_v16(const float* __restrict__ p, int hpad, 
   for (int e = 0; e < 16; ++e) v[e] = e < nval ? __ldg(p + size_t(e) * hpad) : 0.0f;
 }
 // affine map of 16 reverse steps: G' = (bc - theta g) G + g dS
-template <bool kTail>
+template <int kAct, bool kTail>
 __device__ __forceinline__ void bwd_compose(const uint32_t (&r)[16], const float (&vr)[16], int nval,
                                             float vb, float theta, const BwdArgs& a, float& A,
                                             float& Bc) {
 #pragma unroll
   for (int e = 15; e >= 0; --e) {
     if (kTail && e >= nval) continue;
-    const float g = surrogate_fast(a.act + 8 * a.exact_surr, a.slope, a.aux, __fsub_rn(vr[e], theta));
+    const float g = surrogate_t<kAct>(a.slope, a.aux, __fsub_rn(vr[e], theta));
     const float at = vb - theta * g;
     Bc = at * Bc + g * __uint_as_float(r[e]);
     A = at * A;
@@ -720,7 +710,7 @@ __device__ __forceinline__ void bwd_compose(const uint32_t (&r)[16], const float
 }
 // 16 reverse steps in the reference order: dI_t = G ; gs = dS + (-G) theta ;
 // G = G bc + gs g ; dbeta += G V ; dbias += G
-template <bool kTail>
+template <int kAct, bool kTail>
 __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float (&vr)[16], int nval,
                                            float vb, float theta, const BwdArgs& a, float& G,
                                            float& db, float& dbias, float (&x)[16]) {
@@ -730,7 +720,7 @@ __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float 
       x[e] = 0.0f;
       continue;
     }
-    const float g = surrogate_fast(a.act + 8 * a.exact_surr, a.slope, a.aux, __fsub_rn(vr[e], theta));
+    const float g = surrogate_t<kAct>(a.slope, a.aux, __fsub_rn(vr[e], theta));
     const float gi = G;
     const float gs = __fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gi, theta));
     G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
@@ -750,6 +740,7 @@ __host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
   return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256 + 3 * 4 * kBwdScanThreads;
 }
 
+template <int kAct>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
               BwdArgs a) {
@@ -891,8 +882,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
         tmem_ld_wait();
-        if (nval >= 16) bwd_compose<false>(r, vr, 16, vb, theta, a, A, Bc);
-        else bwd_compose<true>(r, vr, nval, vb, theta, a, A, Bc);
+        if (nval >= 16) bwd_compose<kAct, false>(r, vr, 16, vb, theta, a, A, Bc);
+        else bwd_compose<kAct, true>(r, vr, nval, vb, theta, a, A, Bc);
       }
       xA[sidx] = A;
       xB[sidx] = Bc;
@@ -921,8 +912,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               a.dbg_ds[(size_t(b) * a.T_pad + t_lo + c0 + e) * a.H_pad + n] = __uint_as_float(r[e]);
         }
         float x[16];
-        if (nval >= 16) bwd_replay<false>(r, vr, 16, vb, theta, a, G, db, dbias, x);
-        else bwd_replay<true>(r, vr, nval, vb, theta, a, G, db, dbias, x);
+        if (nval >= 16) bwd_replay<kAct, false>(r, vr, 16, vb, theta, a, G, db, dbias, x);
+        else bwd_replay<kAct, true>(r, vr, nval, vb, theta, a, G, db, dbias, x);
         uint32_t ph_[8], pm_[8], pl_[8];
 #pragma unroll
         for (int e = 0; e < 16; e += 2) split3_pack(x[e], x[e + 1], ph_[e / 2], pm_[e / 2], pl_[e / 2]);
