@@ -456,9 +456,12 @@ __device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x)));
 __device__ __forceinline__ float log_cr(float x) { return float(log(double(x))); }
 
 // readout scratch: W [HL][C] | spike words [T][HL_pad/32] | per-(t, class) column
-// buffer [T][32] (one column per lane, so the serial loops need no predicates)
+// buffer [T][33] (one column per lane; stride 33 keeps both the per-step rows
+// written by the projection and the per-class columns read by the scans free
+// of bank conflicts)
+constexpr int kRoStride = 33;
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (size_t(HL) * C + size_t(T) * (HL_pad / 32) + size_t(T) * 32) * 4;
+  return (((size_t(HL) * C + 3) & ~size_t(3)) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
 }
 
 __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
@@ -466,18 +469,25 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   const int C = a.C, T = a.T;
   const int hw = a.HL_pad / 32;
   float* w = rsm;                                                      // [HL][C]
-  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * C);   // [T][hw]
-  float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][32]
+  uint32_t* spk = reinterpret_cast<uint32_t*>(w + ((size_t(a.HL) * C + 3) & ~size_t(3)));  // [T][hw]
+  float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * 8 + (k)] = clock64();
   RO_CLK(0)
   __shared__ int s_label;
   if (tid == 0) s_label = a.labels[a.rows[b]];
   const float beta_l = lane < C ? a.beta[lane] : 0.0f;
-  for (int i = tid; i < a.HL * C; i += 128) w[i] = __ldg(a.w + i);
   {
-    const uint32_t* __restrict__ src = a.s_in + size_t(b) * a.T_pad * hw;
-    for (int i = tid; i < T * hw; i += 128) spk[i] = __ldg(src + i);
+    // W rows (HL*C floats, 16-byte aligned when C % 4 == 0) and the spike words
+    const int nw = a.HL * C;
+    if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
+      const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
+      for (int i = tid; i < nw / 4; i += 128) reinterpret_cast<float4*>(w)[i] = __ldg(src + i);
+    } else {
+      for (int i = tid; i < nw; i += 128) w[i] = __ldg(a.w + i);
+    }
+    const uint4* __restrict__ ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
+    for (int i = tid; i < T * hw / 4; i += 128) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
   }
   __syncthreads();
   RO_CLK(1)
@@ -501,7 +511,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
 #pragma unroll
     for (int c = 0; c < kMaxClasses; ++c) {
       if (c < C && a.bias != nullptr) acc[c] = __fadd_rn(acc[c], a.bias[c]);
-      buf[t * 32 + c] = c < C ? acc[c] : 0.0f;
+      buf[t * kRoStride + c] = c < C ? acc[c] : 0.0f;
     }
   }
   __syncthreads();
@@ -515,17 +525,17 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     for (; t + 8 <= T; t += 8) {
       float I[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * 32];
+      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * kRoStride];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        col[(t + e) * 32] = v;
+        col[(t + e) * kRoStride] = v;
         v = __fadd_rn(__fmul_rn(v, vb), I[e]);
         logit = __fadd_rn(logit, v);
       }
     }
     for (; t < T; ++t) {
-      const float I = col[t * 32];
-      col[t * 32] = v;
+      const float I = col[t * kRoStride];
+      col[t * kRoStride] = v;
       v = __fadd_rn(__fmul_rn(v, vb), I);
       logit = __fadd_rn(logit, v);
     }
@@ -567,37 +577,37 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     }
     if (a.dbg_trace != nullptr && lane < C) {
       for (int s = 0; s < T; ++s)
-        a.dbg_trace[(size_t(b) * T + s) * C + lane] = s + 1 < T ? col[(s + 1) * 32] : v_final;
+        a.dbg_trace[(size_t(b) * T + s) * C + lane] = s + 1 < T ? col[(s + 1) * kRoStride] : v_final;
     }
     RO_CLK(4)
     // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
     float G = delta, db = 0.0f, dbias = 0.0f;
     t = T - 1;
     {
-      const float V3 = col[t * 32];
+      const float V3 = col[t * kRoStride];
       db = __fmul_rn(G, V3);
       dbias = G;
-      col[t * 32] = G;
+      col[t * kRoStride] = G;
     }
     --t;
     for (; t >= 7; t -= 8) {
       float V3[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * 32];
+      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * kRoStride];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         G = __fadd_rn(delta, __fmul_rn(G, vb));
         db = __fadd_rn(db, __fmul_rn(G, V3[e]));
         dbias = __fadd_rn(dbias, G);
-        col[(t - e) * 32] = G;
+        col[(t - e) * kRoStride] = G;
       }
     }
     for (; t >= 0; --t) {
-      const float V3 = col[t * 32];
+      const float V3 = col[t * kRoStride];
       G = __fadd_rn(delta, __fmul_rn(G, vb));
       db = __fadd_rn(db, __fmul_rn(G, V3));
       dbias = __fadd_rn(dbias, G);
-      col[t * 32] = G;
+      col[t * kRoStride] = G;
     }
     if (lane < C) {
       a.dbeta_part[size_t(b) * C + lane] = db;
@@ -616,8 +626,8 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     uint32_t hp[4], mp[4], lp[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const float g0 = t0 + e < T ? buf[(t0 + e) * 32 + c] : 0.0f;
-      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * 32 + c] : 0.0f;
+      const float g0 = t0 + e < T ? buf[(t0 + e) * kRoStride + c] : 0.0f;
+      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * kRoStride + c] : 0.0f;
       split3_pack(g0, g1, hp[e / 2], mp[e / 2], lp[e / 2]);
     }
     const size_t off = size_t(c) * cols + size_t(b) * a.T_pad + t0;
