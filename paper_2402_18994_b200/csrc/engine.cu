@@ -225,6 +225,7 @@ struct snn_engine {
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
   int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 1));
+  int pdl = env_int("SNN_PDL", 2) - 1;  // programmatic dependent launch between step kernels
   int wg_samples_per_split = env_int("SNN_WG_SPLIT_SAMPLES", 8);
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
@@ -539,14 +540,31 @@ struct snn_engine {
     CK(cudaStreamSynchronize(stream));
   }
 
+  // Every step kernel is launched with programmatic stream serialization (PDL):
+  // its prologue overlaps the previous kernel; griddepcontrol.wait orders data.
+  template <typename... KArgs, typename... Args>
+  void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  }
+
   void launch_bwd(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
                   const BwdArgs& bw) {
     switch (act) {
-      case 1: k_lif_bwd<1><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
-      case 2: k_lif_bwd<2><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
-      case 3: k_lif_bwd<3><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
-      case 4: k_lif_bwd<4><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
-      default: k_lif_bwd<0><<<grid, kBwdThreads, smem, stream>>>(tw, td, bw); break;
+      case 1: launch(k_lif_bwd<1>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
+      case 2: launch(k_lif_bwd<2>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
+      case 3: launch(k_lif_bwd<3>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
+      case 4: launch(k_lif_bwd<4>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
+      default: launch(k_lif_bwd<0>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
     }
   }
 
@@ -589,8 +607,8 @@ struct snn_engine {
       f.theta = net.threshold;
       f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
       f.spb = fwd_spb(TT);
-      k_lif_fwd<<<dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128), kFwdThreads,
-                  fwd_smem_bytes(TT, f.spb, f.stages), stream>>>(tm_wt[l], f);
+      launch(k_lif_fwd, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128), dim3(kFwdThreads),
+             fwd_smem_bytes(TT, f.spb, f.stages), tm_wt[l], f);
       mark(evs, "lif_fwd", l);
     }
     // readout + loss + LI backward
@@ -613,7 +631,7 @@ struct snn_engine {
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
       r.inv_b = 1.0f / float(B_global());
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
-      k_readout<<<B, 128, smem, stream>>>(r);
+      launch(k_readout, dim3(B), dim3(128), smem, r);
       mark(evs, "readout", -1);
     }
     // hidden backward, top-down: dS on tcgen05 (readout-fed layer: K = classes)
@@ -653,7 +671,7 @@ struct snn_engine {
         g.block_start = blocks;
         blocks += g.m_tiles * g.n_tiles * g.splits;
       }
-      k_wgrad<<<blocks, kWgThreads, wg_smem_bytes(128, wg_stages), stream>>>(wg_maps, w);
+      launch(k_wgrad, dim3(blocks), dim3(kWgThreads), wg_smem_bytes(128, wg_stages), wg_maps, w);
       mark(evs, "wgrad", -1);
     }
     // gradient assembly (+ loss sum, hits, step counter)
@@ -680,7 +698,7 @@ struct snn_engine {
       r.B = B;
       r.w_blocks = int((n_params + 255) / 256);
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
-      k_reduce<<<blocks, 256, 0, stream>>>(r);
+      launch(k_reduce, dim3(blocks), dim3(256), 0, r);
       mark(evs, "reduce", -1);
     }
     if (world > 1) {
@@ -691,11 +709,11 @@ struct snn_engine {
     }
     if (update) {
       AdamArgs a = adam_args(1);
-      k_adam<<<unsigned((n_params + 255) / 256), 256, 0, stream>>>(a);
+      launch(k_adam, dim3(unsigned((n_params + 255) / 256)), dim3(256), 0, a);
       mark(evs, "adam", -1);
     } else {
-      k_result<<<1, 32, 0, stream>>>(comm.p + n_params, B_global(), step.p, 0, result_loss.p,
-                                     result_acc.p);
+      launch(k_result, dim3(1), dim3(32), 0, (const float*)(comm.p + n_params), B_global(), step.p,
+             0, result_loss.p, result_acc.p);
       mark(evs, "result", -1);
     }
   }

@@ -274,9 +274,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
+  if (threadIdx.x == 32 * (kFwdScanWarps + 4)) tma_prefetch(&tm_w);
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // activations / planes of the previous kernels are visible from here
   const uint32_t tmem = *tmem_slot;
   const int dec_warp0 = kFwdScanWarps, tma_warp = kFwdScanWarps + 4, mma_warp = tma_warp + 1;
 
@@ -473,6 +476,8 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * 8 + (k)] = clock64();
+  pdl_launch_dependents();
+  pdl_wait();
   RO_CLK(0)
   __shared__ int s_label;
   if (tid == 0) s_label = a.labels[a.rows[b]];
@@ -794,9 +799,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     else if (tmem_cols == 128) tmem_alloc<128>(tmem_slot);
     else tmem_alloc<64>(tmem_slot);
   }
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = *tmem_slot;
   const int cols_total = a.B * a.T_pad;
 
@@ -1049,9 +1056,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
       default: tmem_alloc<256>(tmem_slot); break;
     }
   }
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = *tmem_slot;
   if (warp == 4) {
     if (elect_one()) {
@@ -1201,6 +1210,8 @@ __device__ __forceinline__ int find_entry(const Entry* en, int n, int64_t i) {
 // lanes take strided samples, then a fixed-shape tree (deterministic).  Last
 // block: loss sum in batch order (objective.hpp:57-72) + hits, step counter.
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int tid = threadIdx.x;
   if (int(blockIdx.x) < a.w_blocks) {
     const int64_t i = int64_t(blockIdx.x) * 256 + tid;
@@ -1300,6 +1311,8 @@ struct AdamArgs {
 };
 
 __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a.update && i == 0) {
     // StepResult{loss, accuracy} (optimize.hpp:143-147, :193-196)
@@ -1395,6 +1408,7 @@ __global__ void k_synth(SynthArgs a) {
 // StepResult{loss / B_global, hits / B_global}; advances the step counter.
 __global__ void k_result(const float* tail, int B_global, int64_t* step, int do_step,
                          float* loss_out, double* acc_out) {
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   *loss_out = __fdiv_rn(tail[0], float(B_global));
   *acc_out = double(tail[1]) / double(B_global);
