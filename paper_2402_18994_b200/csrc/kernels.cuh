@@ -275,7 +275,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
   if (threadIdx.x == 32 * (kFwdScanWarps + 4)) tma_prefetch(&tm_w);
-  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -420,6 +419,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (clk != nullptr && threadIdx.x == 0) clk[2] = clock64();
   }
 
+  pdl_launch_dependents();
   __syncthreads();
   if (clk != nullptr && threadIdx.x == 0) {
     clk[3] = clock64();
@@ -476,7 +476,6 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * 8 + (k)] = clock64();
-  pdl_launch_dependents();
   pdl_wait();
   RO_CLK(0)
   __shared__ int s_label;
@@ -620,6 +619,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     }
     RO_CLK(5)
   }
+  pdl_launch_dependents();
   __syncthreads();
   RO_CLK(6)
   // dI3 as three bf16 planes [3][64][B*T_pad] (class rows, (b,t) contiguous)
@@ -799,7 +799,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     else if (tmem_cols == 128) tmem_alloc<128>(tmem_slot);
     else tmem_alloc<64>(tmem_slot);
   }
-  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -970,6 +969,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       }
     }
   }
+  pdl_launch_dependents();
   __syncthreads();
   if (clk != nullptr && threadIdx.x == 0) clk[6] = clock64();
   if (warp == 0) {
@@ -1056,7 +1056,6 @@ __global__ void __launch_bounds__(kWgThreads, 1)
       default: tmem_alloc<256>(tmem_slot); break;
     }
   }
-  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1153,6 +1152,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
     tc_fence_before();
   }
+  pdl_launch_dependents();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -1210,7 +1210,6 @@ __device__ __forceinline__ int find_entry(const Entry* en, int n, int64_t i) {
 // lanes take strided samples, then a fixed-shape tree (deterministic).  Last
 // block: loss sum in batch order (objective.hpp:57-72) + hits, step counter.
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
-  pdl_launch_dependents();
   pdl_wait();
   const int tid = threadIdx.x;
   if (int(blockIdx.x) < a.w_blocks) {
@@ -1311,7 +1310,6 @@ struct AdamArgs {
 };
 
 __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
-  pdl_launch_dependents();
   pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a.update && i == 0) {
