@@ -174,7 +174,8 @@ struct snn_engine {
   int B = 0, T = 0, TT = 0, NT = 0, T_pad = 0, IN = 0, IN_pad = 0, L = 0, C = 0;
   int H[SNN_MAX_HIDDEN]{}, H_pad[SNN_MAX_HIDDEN]{};
   int K[kMaxLayers]{}, N[kMaxLayers]{}, K_pad[kMaxLayers]{}, N_pad[kMaxLayers]{};
-  int M_pad_w[kMaxLayers]{}, n_tile_w[kMaxLayers]{}, splits_w[kMaxLayers]{};
+  int M_pad_w[kMaxLayers]{}, n_tile_w[kMaxLayers]{}, splits_w[kMaxLayers]{}, mg_w[kMaxLayers]{};
+  int wg_mg_max = 1;
   std::vector<EntryHost> entries;
   size_t n_params = 0;
 
@@ -224,9 +225,8 @@ struct snn_engine {
   int fwd_spb(int tt) const { return std::max(1, std::min(fwd_spb_env, std::min(kFwdSpbMax, 256 / tt))); }
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
-  int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 1));
-  int pdl = env_int("SNN_PDL", 2) - 1;  // programmatic dependent launch between step kernels
-  int wg_samples_per_split = env_int("SNN_WG_SPLIT_SAMPLES", 8);
+  int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 2));
+  int pdl = env_int("SNN_PDL", 1) - 1;  // programmatic dependent launch (measured slower: off)
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
     return (v && *v) ? std::max(1, std::atoi(v)) : d;
@@ -297,9 +297,37 @@ struct snn_engine {
     const size_t ro_smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
     if (ro_smem > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "readout working set too large");
     if (size_t(T) * C * 4 > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "T * classes too large");
-    // split-K over samples: >= wg_samples_per_split samples per split keeps the
-    // partials small; the merged launch fills the chip across layers
-    for (int j = 0; j <= L; ++j) splits_w[j] = std::max(1, B / wg_samples_per_split);
+    // weight-gradient work split: each CTA owns mg M-tiles (shared dI stages, TMEM
+    // mg*n_tile <= 512 columns) of one n-tile and a contiguous range of samples;
+    // splits are chosen per layer so the whole launch is ~one CTA per SM with
+    // equal tensor work per CTA
+    {
+      int sms = 148;
+      int dev_sms = 0;
+      if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
+          dev_sms > 0)
+        sms = dev_sms;
+      // smem: stages * (mg * 16 KB + 48 KB) must fit 227 KB
+      wg_mg_max = std::min(kWgMgMax, (int(227 * 1024 / wg_stages) - 1280 - 3 * 128 * 128) / int(kPlaneTile));
+      wg_mg_max = std::max(1, wg_mg_max);
+      double total_cost = 0, cost[kMaxLayers], units[kMaxLayers];
+      for (int j = 0; j <= L; ++j) {
+        const int m_tiles = M_pad_w[j] / 128, n_tiles = N_pad[j] / n_tile_w[j];
+        const int mg_cap = std::min(wg_mg_max, std::min(m_tiles, 512 / n_tile_w[j]));
+        const int groups = (m_tiles + mg_cap - 1) / mg_cap;
+        mg_w[j] = (m_tiles + groups - 1) / groups;  // balanced groups (6 tiles -> 3 + 3)
+        const int m_groups = (m_tiles + mg_w[j] - 1) / mg_w[j];
+        units[j] = double(m_groups) * n_tiles;
+        cost[j] = double(m_tiles) * n_tiles * n_tile_w[j];  // tensor time per sample
+        total_cost += cost[j];
+      }
+      for (int j = 0; j <= L; ++j) {
+        const double share = double(sms) * cost[j] / total_cost;  // CTAs for layer j
+        splits_w[j] = std::max(1, std::min(B, int(share / units[j] + 0.5)));
+      }
+      if (const char* v = std::getenv("SNN_WG_SPLIT_SAMPLES"))
+        for (int j = 0; j <= L; ++j) splits_w[j] = std::max(1, B / std::max(1, std::atoi(v)));
+    }
     // parameter entries (network.hpp:210-226 order)
     entries.clear();
     size_t off = 0;
@@ -370,7 +398,7 @@ struct snn_engine {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(wg_smem_bytes(128, kWgStagesMax))));
+                            int(wg_smem_bytes(128, wg_mg_max, wg_stages))));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
     {
@@ -668,10 +696,12 @@ struct snn_engine {
         g.kind = j == 0 ? 0 : 1;
         g.M_pad = M_pad_w[j]; g.N_pad = N_pad[j]; g.n_tile = n_tile_w[j]; g.splits = splits_w[j];
         g.m_tiles = M_pad_w[j] / 128; g.n_tiles = N_pad[j] / n_tile_w[j];
+        g.mg = mg_w[j]; g.m_groups = (g.m_tiles + g.mg - 1) / g.mg;
         g.block_start = blocks;
-        blocks += g.m_tiles * g.n_tiles * g.splits;
+        blocks += g.m_groups * g.n_tiles * g.splits;
       }
-      launch(k_wgrad, dim3(blocks), dim3(kWgThreads), wg_smem_bytes(128, wg_stages), wg_maps, w);
+      launch(k_wgrad, dim3(blocks), dim3(kWgThreads), wg_smem_bytes(128, wg_mg_max, wg_stages),
+             wg_maps, w);
       mark(evs, "wgrad", -1);
     }
     // gradient assembly (+ loss sum, hits, step counter)

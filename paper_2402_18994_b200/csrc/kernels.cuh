@@ -991,6 +991,7 @@ struct WgradLayer {
   const uint32_t* s_tp;    // kind 1: time-packed spikes [K_pad][B*T_pad/32]
   float* partial;          // [splits][M_pad][N_pad]
   int kind, M_pad, N_pad, n_tile, splits, m_tiles, n_tiles, block_start;
+  int mg, m_groups;        // m-tiles per CTA (share every dI stage), groups
 };
 // B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
 struct WgradArgs {
@@ -1004,16 +1005,19 @@ struct WgradMaps {
   CUtensorMap m[kMaxLayers];
 };
 
-constexpr int kWgStagesMax = 3;
+constexpr int kWgStagesMax = 2;
+constexpr int kWgMgMax = 4;
 constexpr int kWgThreads = 192;
-__host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile) {
-  return kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // A 16 KB + 3 planes x (n_tile x 128 B)
+__host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile, int mg) {
+  return uint32_t(mg) * kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // mg A tiles + 3 B planes
 }
-__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int stages) {
-  return uint32_t(stages) * wg_stage_bytes(n_tile) + 1024 + 256;
+__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages) {
+  return uint32_t(stages) * wg_stage_bytes(n_tile, mg) + 1024 + 256;
 }
 
-// One launch for every Linear layer: block -> (layer, m-tile, n-tile, split).
+// One launch for every Linear layer: block -> (layer, m-group, n-tile, split).
+// A CTA accumulates mg M-tiles (mg x n_tile TMEM columns) so each dI stage
+// loaded by TMA feeds mg MMAs.
 __global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad(const __grid_constant__ WgradMaps maps, WgradArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -1023,10 +1027,12 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const WgradLayer a = args.layer[li];
   const CUtensorMap* tm_di = &maps.m[li];
   const int local = int(blockIdx.x) - a.block_start;
-  const int mt = local % a.m_tiles, ntile = (local / a.m_tiles) % a.n_tiles;
-  const int split = local / (a.m_tiles * a.n_tiles);
+  const int mgi = local % a.m_groups, ntile = (local / a.m_groups) % a.n_tiles;
+  const int split = local / (a.m_groups * a.n_tiles);
+  const int mt0 = mgi * a.mg;
+  const int nm = min(a.mg, a.m_tiles - mt0);  // M-tiles of this CTA
   const int S = args.stages;
-  const uint32_t stage_bytes = wg_stage_bytes(a.n_tile);
+  const uint32_t stage_bytes = wg_stage_bytes(a.n_tile, a.mg);
   const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: n_tile rows x 64 cols
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
@@ -1038,7 +1044,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const int b0 = int((long long)args.B * split / a.splits);
   const int b1 = int((long long)args.B * (split + 1) / a.splits);
   const int total = (b1 - b0) * tq_per_b;
-  const uint32_t tmem_cols = a.n_tile <= 32 ? 32u : (a.n_tile <= 64 ? 64u : (a.n_tile <= 128 ? 128u : 256u));
+  const uint32_t tmem_cols = tmem_cols_for(a.mg * a.n_tile, 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -1048,14 +1054,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     mbar_init(&acc_full[0], 1);
     fence_barrier_init();
   }
-  if (warp == 0) {
-    switch (tmem_cols) {
-      case 32: tmem_alloc<32>(tmem_slot); break;
-      case 64: tmem_alloc<64>(tmem_slot); break;
-      case 128: tmem_alloc<128>(tmem_slot); break;
-      default: tmem_alloc<256>(tmem_slot); break;
-    }
-  }
+  if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1069,7 +1068,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * ptile);
-        uint8_t* Bp = smem + s * stage_bytes + kPlaneTile;
+        uint8_t* Bp = smem + s * stage_bytes + a.mg * kPlaneTile;
         for (int p = 0; p < 3; ++p)
           tma_load_2d(Bp + p * ptile, tm_di, &full[s], bb * args.T_pad + tq * 64,
                       p * a.N_pad + ntile * a.n_tile);
@@ -1084,14 +1083,16 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t A = smem_u32(smem + s * stage_bytes);
-        const uint32_t Bp = A + kPlaneTile;
+        const uint32_t Bp = A + a.mg * kPlaneTile;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t ad = sdesc_sw128(A + ks * 32, 16, 1024);
+          for (int m = 0; m < nm; ++m) {
+            const uint64_t ad = sdesc_sw128(A + m * kPlaneTile + ks * 32, 16, 1024);
 #pragma unroll
-          for (int p = 2; p >= 0; --p) {
-            const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
-            umma_bf16(tmem, ad, bd, idesc, (it | ks | (2 - p)) != 0);
+            for (int p = 2; p >= 0; --p) {
+              const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
+              umma_bf16(tmem + m * a.n_tile, ad, bd, idesc, (it | ks | (2 - p)) != 0);
+            }
           }
         }
         umma_commit(&empty[s]);
@@ -1100,13 +1101,12 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
     __syncwarp();
   } else if (warp < 4) {
-    // A producers: tile [128 k-rows][64 time cols], K-major SW128.  The loads of
-    // stage it+1 are issued before waiting for stage it's slot.
+    // A producers: nm tiles [128 k-rows][64 time cols], K-major SW128; thread =
+    // row tid of every tile.  Loads of stage it+1 issue before stage it's wait.
     const int tid = threadIdx.x;
-    const int k = mt * 128 + tid;  // this thread's A row
-    const bool in_row = a.kind != 0 || k < args.x_row_stride;
-    auto fetch = [&](int it) -> uint64_t {
-      if (it >= total || !in_row) return 0;
+    auto fetch = [&](int it, int m) -> uint64_t {
+      const int k = (mt0 + m) * 128 + tid;
+      if (it >= total || m >= nm || (a.kind == 0 && k >= args.x_row_stride)) return 0;
       const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
       if (a.kind == 0) {
         const uint8_t* src =
@@ -1119,35 +1119,47 @@ __global__ void __launch_bounds__(kWgThreads, 1)
       return __ldg(reinterpret_cast<const unsigned long long*>(
           a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) + size_t(bb) * (args.T_pad / 32) + tq * 2));
     };
-    uint64_t cur = fetch(0);
+    uint64_t cur[kWgMgMax], nxt[kWgMgMax];
+#pragma unroll
+    for (int m = 0; m < kWgMgMax; ++m) cur[m] = fetch(0, m);
     for (int it = 0; it < total; ++it) {
       const int s = it % S, ph = (it / S) & 1;
-      const uint64_t nxt = fetch(it + 1);
+#pragma unroll
+      for (int m = 0; m < kWgMgMax; ++m) nxt[m] = fetch(it + 1, m);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t A = smem_u32(smem + s * stage_bytes);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t byte = uint32_t(cur >> (8 * j)) & 0xFFu;
-        st_shared_v4(A + sw128_off(tid, j), a.kind == 0 ? expand_bits_msb(byte) : expand_bits_lsb(byte));
+      for (int m = 0; m < kWgMgMax; ++m) {
+        if (m >= nm) break;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t byte = uint32_t(cur[m] >> (8 * j)) & 0xFFu;
+          st_shared_v4(A + m * kPlaneTile + sw128_off(tid, j),
+                       a.kind == 0 ? expand_bits_msb(byte) : expand_bits_lsb(byte));
+        }
       }
       fence_async_smem();
       mbar_arrive(&full[s]);
-      cur = nxt;
+#pragma unroll
+      for (int m = 0; m < kWgMgMax; ++m) cur[m] = nxt[m];
     }
-    // epilogue: thread = output row k, n_tile columns
+    // epilogue: thread = output row of each M-tile, n_tile columns
     mbar_wait(&acc_full[0], 0);
     tc_fence_after();
-    float* dst = a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile;
-    for (int c = 0; c < a.n_tile / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c * 32, r);
-      tmem_ld_wait();
+    for (int m = 0; m < nm; ++m) {
+      const int k = (mt0 + m) * 128 + tid;
+      float* dst = a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile;
+      for (int c = 0; c < a.n_tile / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + m * a.n_tile + c * 32, r);
+        tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 v4 = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-        if (total == 0) v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        *reinterpret_cast<float4*>(dst + c * 32 + j) = v4;
+        for (int j = 0; j < 32; j += 4) {
+          float4 v4 = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                  __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          if (total == 0) v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(dst + c * 32 + j) = v4;
+        }
       }
     }
     tc_fence_before();
@@ -1156,12 +1168,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    switch (tmem_cols) {
-      case 32: tmem_dealloc<32>(tmem); break;
-      case 64: tmem_dealloc<64>(tmem); break;
-      case 128: tmem_dealloc<128>(tmem); break;
-      default: tmem_dealloc<256>(tmem); break;
-    }
+    tmem_dealloc_any(tmem_cols, tmem);
   }
 }
 
