@@ -307,8 +307,10 @@ struct snn_engine {
       if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
           dev_sms > 0)
         sms = dev_sms;
-      // smem: stages * (mg * 16 KB + 48 KB) must fit 227 KB
-      wg_mg_max = std::min(kWgMgMax, (int(227 * 1024 / wg_stages) - 1280 - 3 * 128 * 128) / int(kPlaneTile));
+      // smem: stages * (mg * 16 KB + 48 KB + dataset run) must fit 227 KB
+      const int xrun = (8 * IN_pad + 1023) / 1024 * 1024;
+      wg_mg_max = std::min(kWgMgMax, (int((227 * 1024 - 1280) / wg_stages) - 3 * 128 * 128 - xrun) /
+                                         int(kPlaneTile));
       wg_mg_max = std::max(1, wg_mg_max);
       double total_cost = 0, cost[kMaxLayers], units[kMaxLayers];
       for (int j = 0; j <= L; ++j) {
@@ -393,12 +395,12 @@ struct snn_engine {
       wg_maps.m[j] = tm_di_w[j];
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax))));
+                            int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(wg_smem_bytes(128, wg_mg_max, wg_stages))));
+                            int(wg_smem_bytes(128, wg_mg_max, wg_stages, IN_pad))));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
     {
@@ -636,7 +638,7 @@ struct snn_engine {
       f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
       f.spb = fwd_spb(TT);
       launch(k_lif_fwd, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128), dim3(kFwdThreads),
-             fwd_smem_bytes(TT, f.spb, f.stages), tm_wt[l], f);
+             fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), tm_wt[l], f);
       mark(evs, "lif_fwd", l);
     }
     // readout + loss + LI backward
@@ -700,8 +702,8 @@ struct snn_engine {
         g.block_start = blocks;
         blocks += g.m_groups * g.n_tiles * g.splits;
       }
-      launch(k_wgrad, dim3(blocks), dim3(kWgThreads), wg_smem_bytes(128, wg_mg_max, wg_stages),
-             wg_maps, w);
+      launch(k_wgrad, dim3(blocks), dim3(kWgThreads),
+             wg_smem_bytes(128, wg_mg_max, wg_stages, IN_pad), wg_maps, w);
       mark(evs, "wgrad", -1);
     }
     // gradient assembly (+ loss sum, hits, step counter)

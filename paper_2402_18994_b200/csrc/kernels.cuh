@@ -173,8 +173,13 @@ constexpr uint32_t kPlaneTile = 128 * 128;  // 128 rows x 64 bf16 = 16 KB
 __host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT, int spb) {
   return 3 * kPlaneTile + uint32_t(spb * TT) * 128u;
 }
-__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int spb, int stages) {
-  return uint32_t(stages) * fwd_stage_bytes(TT, spb) + 1024 + 256;
+// dataset run of one sample for one t-tile: TT/8 rows of K_pad bytes (layer 0)
+__host__ __device__ constexpr uint32_t fwd_xrun_bytes(int TT, int K_pad) {
+  return uint32_t(TT / 8) * uint32_t(K_pad);
+}
+__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int spb, int stages, int x_kpad) {
+  return uint32_t(stages) * fwd_stage_bytes(TT, spb) +
+         2u * ((uint32_t(spb) * fwd_xrun_bytes(TT, x_kpad) + 1023) & ~1023u) + 1024 + 256;
 }
 // TMEM columns for N-wide accumulators, doubled when several t-tiles pipeline.
 __host__ __device__ constexpr uint32_t tmem_cols_for(int N, int NT) {
@@ -240,11 +245,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int NTOT = SPB * a.TT;  // MMA N (stacked samples)
   const uint32_t stage_bytes = fwd_stage_bytes(a.TT, SPB);
   const int S = a.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  // layer 0: each sample's dataset run for the current t-tile is bulk-copied
+  // into xbuf[tt % 2] (double-buffered across t-tiles)
+  const uint32_t xrun = a.in_kind == 0 ? fwd_xrun_bytes(a.TT, a.K_pad) : 0u;
+  const uint32_t xbuf_bytes = (uint32_t(SPB) * xrun + 1023) & ~1023u;
+  uint8_t* xbuf = smem + S * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * xbuf_bytes);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* xfull = acc_empty + 2;
+  uint64_t* xempty = xfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = blockIdx.x * SPB, nt = blockIdx.y;
@@ -270,6 +282,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], scan_threads);
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], 128);
     }
     fence_barrier_init();
   }
@@ -288,6 +302,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tma_prefetch(&tm_w);
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1, kb = (it % KB + rot) % KB;
+        if (a.in_kind == 0 && it % KB == 0) {
+          const int tt = it / KB, xb = tt & 1;
+          if (tt >= 2) mbar_wait(&xempty[xb], ((tt - 2) >> 1) & 1);
+          mbar_arrive_expect_tx(&xfull[xb], uint32_t(nsamp) * xrun);
+          for (int sm = 0; sm < nsamp; ++sm)
+            bulk_load(xbuf + xb * xbuf_bytes + sm * xrun,
+                      a.x + (size_t(a.rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(a.K_pad),
+                      xrun, &xfull[xb]);
+        }
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile);
         uint8_t* A = smem + s * stage_bytes;
@@ -333,45 +356,44 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const size_t kwords = size_t(a.K_pad) / 32;
     const int units = SPB * a.TT;  // kind 0: (sample, t-group, 8-feature chunk); kind 1: row
     auto fetch = [&](int it, int u) -> uint64_t {
-      if (u >= units || it >= total) return 0;
+      if (a.in_kind == 0 || u >= units || it >= total) return 0;
       const int tt = it / KB, kb = (it % KB + rot) % KB;
       const int sm = u / a.TT, r = u % a.TT;
       if (sm >= nsamp) return 0;
-      if (a.in_kind == 0) {
-        const int g = r >> 3, q = r & 7;
-        return __ldg(reinterpret_cast<const unsigned long long*>(
-            a.x + (size_t(a.rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8) + g) * size_t(a.K_pad) +
-            kb * 64 + q * 8));
-      }
       return __ldg(reinterpret_cast<const unsigned long long*>(
           a.s_in + (size_t(b0 + sm) * a.T_pad + tt * a.TT + r) * kwords + kb * 2));
     };
     uint64_t cur0 = fetch(0, tid), cur1 = fetch(0, tid + 128);
     for (int it = 0; it < total; ++it) {
       const int s = it % S, ph = (it / S) & 1;
+      const int tt = it / KB, kb = (it % KB + rot) % KB;
       const uint64_t nxt0 = fetch(it + 1, tid), nxt1 = fetch(it + 1, tid + 128);
+      if (a.in_kind == 0 && it % KB == 0) mbar_wait(&xfull[tt & 1], (tt >> 1) & 1);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t Bt = smem_u32(smem + s * stage_bytes + 3 * kPlaneTile);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int u = tid + 128 * h;
         if (u >= units) continue;
-        const uint64_t cur = h == 0 ? cur0 : cur1;
         const int sm = u / a.TT, r = u % a.TT;
         if (a.in_kind == 0) {
-          // dataset bytes [row][t/8][k], bit 7-(t%8): 8 k of one t-group -> 8 rows
+          // dataset bytes [t/8][k] (bulk-copied), bit 7-(t%8): 8 k of one t-group -> 8 rows
           const int g = r >> 3, q = r & 7;
+          const uint64_t cur = sm < nsamp ? *reinterpret_cast<const uint64_t*>(
+              xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * a.K_pad + kb * 64 + q * 8) : 0ull;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             st_shared_v4(Bt + sw128_off(sm * a.TT + 8 * g + j, q),
                          expand_bytes01((cur >> (7 - j)) & 0x0101010101010101ull));
         } else {
           // neuron-packed spike words: row t, 2 words = 64 k
+          const uint64_t cur = h == 0 ? cur0 : cur1;
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             st_shared_v4(Bt + sw128_off(sm * a.TT + r, q), expand_bits_lsb(uint32_t(cur >> (8 * q)) & 0xFFu));
         }
       }
+      if (a.in_kind == 0 && it % KB == KB - 1) mbar_arrive(&xempty[tt & 1]);
       fence_async_smem();
       mbar_arrive(&full[s]);
       cur0 = nxt0;
@@ -1011,8 +1033,8 @@ constexpr int kWgThreads = 192;
 __host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile, int mg) {
   return uint32_t(mg) * kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // mg A tiles + 3 B planes
 }
-__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages) {
-  return uint32_t(stages) * wg_stage_bytes(n_tile, mg) + 1024 + 256;
+__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages, int x_row_stride) {
+  return uint32_t(stages) * (wg_stage_bytes(n_tile, mg) + ((8u * x_row_stride + 1023) & ~1023u)) + 1024 + 256;
 }
 
 // One launch for every Linear layer: block -> (layer, m-group, n-tile, split).
@@ -1034,9 +1056,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const int S = args.stages;
   const uint32_t stage_bytes = wg_stage_bytes(a.n_tile, a.mg);
   const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: n_tile rows x 64 cols
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  // kind 0: the dataset bytes of one (sample, 64-step block) are one contiguous
+  // run of 8 * x_row_stride bytes -> one bulk copy per stage into xbuf
+  const uint32_t xbytes = a.kind == 0 ? 8u * uint32_t(args.x_row_stride) : 0u;
+  uint8_t* xbuf = smem + S * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + S * ((xbytes + 1023) & ~1023u));
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;
+  uint64_t* xfull = empty + S;
+  uint64_t* acc_full = xfull + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1050,6 +1077,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1 + 128);
       mbar_init(&empty[s], 1);
+      mbar_init(&xfull[s], 1);
     }
     mbar_init(&acc_full[0], 1);
     fence_barrier_init();
@@ -1067,6 +1095,12 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int s = it % S, ph = (it / S) & 1;
         const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
         mbar_wait(&empty[s], ph ^ 1);
+        if (a.kind == 0) {
+          mbar_arrive_expect_tx(&xfull[s], xbytes);
+          bulk_load(xbuf + s * ((xbytes + 1023) & ~1023u),
+                    args.x + (size_t(args.rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride,
+                    xbytes, &xfull[s]);
+        }
         mbar_arrive_expect_tx(&full[s], 3 * ptile);
         uint8_t* Bp = smem + s * stage_bytes + a.mg * kPlaneTile;
         for (int p = 0; p < 3; ++p)
@@ -1102,20 +1136,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     __syncwarp();
   } else if (warp < 4) {
     // A producers: nm tiles [128 k-rows][64 time cols], K-major SW128; thread =
-    // row tid of every tile.  Loads of stage it+1 issue before stage it's wait.
+    // row tid of every tile.  kind 0 decodes the bulk-copied dataset bytes from
+    // smem; kind 1 loads time-packed spike words (L2-resident) one stage ahead.
     const int tid = threadIdx.x;
     auto fetch = [&](int it, int m) -> uint64_t {
       const int k = (mt0 + m) * 128 + tid;
-      if (it >= total || m >= nm || (a.kind == 0 && k >= args.x_row_stride)) return 0;
+      if (a.kind == 0 || it >= total || m >= nm) return 0;
       const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
-      if (a.kind == 0) {
-        const uint8_t* src =
-            args.x + (size_t(args.rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride + k;
-        uint64_t v = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v |= uint64_t(__ldg(src + size_t(j) * args.x_row_stride)) << (8 * j);
-        return v;
-      }
       return __ldg(reinterpret_cast<const unsigned long long*>(
           a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) + size_t(bb) * (args.T_pad / 32) + tq * 2));
     };
@@ -1127,6 +1154,21 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
       for (int m = 0; m < kWgMgMax; ++m) nxt[m] = fetch(it + 1, m);
       mbar_wait(&empty[s], ph ^ 1);
+      if (a.kind == 0) {
+        mbar_wait(&xfull[s], ph);
+        const uint8_t* xs = xbuf + s * ((xbytes + 1023) & ~1023u);
+#pragma unroll
+        for (int m = 0; m < kWgMgMax; ++m) {
+          if (m >= nm) break;
+          const int k = (mt0 + m) * 128 + tid;
+          uint64_t v = 0;
+          if (k < args.x_row_stride) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v |= uint64_t(xs[j * args.x_row_stride + k]) << (8 * j);
+          }
+          cur[m] = v;
+        }
+      }
       const uint32_t A = smem_u32(smem + s * stage_bytes);
 #pragma unroll
       for (int m = 0; m < kWgMgMax; ++m) {
