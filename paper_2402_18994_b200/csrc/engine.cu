@@ -175,6 +175,7 @@ struct snn_engine {
   int H[SNN_MAX_HIDDEN]{}, H_pad[SNN_MAX_HIDDEN]{};
   int K[kMaxLayers]{}, N[kMaxLayers]{}, K_pad[kMaxLayers]{}, N_pad[kMaxLayers]{};
   int M_pad_w[kMaxLayers]{}, n_tile_w[kMaxLayers]{}, splits_w[kMaxLayers]{}, mg_w[kMaxLayers]{};
+  int wg_stages_l[kMaxLayers]{};
   int wg_mg_max = 1;
   std::vector<EntryHost> entries;
   size_t n_params = 0;
@@ -225,7 +226,7 @@ struct snn_engine {
   int fwd_spb(int tt) const { return std::max(1, std::min(fwd_spb_env, std::min(kFwdSpbMax, 256 / tt))); }
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
-  int wg_stages = std::min(kWgStagesMax, env_int("SNN_WG_STAGES", 2));
+  int wg_stages_cap = env_int("SNN_WG_STAGES", kWgStagesMax);
   int pdl = env_int("SNN_PDL", 1) - 1;  // programmatic dependent launch (measured slower: off)
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
@@ -298,29 +299,38 @@ struct snn_engine {
     if (ro_smem > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "readout working set too large");
     if (size_t(T) * C * 4 > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "T * classes too large");
     // weight-gradient work split: each CTA owns mg M-tiles (shared dI stages, TMEM
-    // mg*n_tile <= 512 columns) of one n-tile and a contiguous range of samples;
-    // splits are chosen per layer so the whole launch is ~one CTA per SM with
-    // equal tensor work per CTA
+    // mg*n_tile <= 512 columns) of one n-tile and a contiguous range of samples.
+    // Pipeline depth per layer = what fits the smem budget (small stages -> more
+    // stages in flight).  Splits balance CTAs by modelled time: iterations x
+    // max(MMA cycles per iteration, load latency / stages).
     {
       int sms = 148;
       int dev_sms = 0;
       if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
           dev_sms > 0)
         sms = dev_sms;
-      // smem: stages * (mg * 16 KB + 48 KB + dataset run) must fit 227 KB
-      const int xrun = (8 * IN_pad + 1023) / 1024 * 1024;
-      wg_mg_max = std::min(kWgMgMax, (int((227 * 1024 - 1280) / wg_stages) - 3 * 128 * 128 - xrun) /
-                                         int(kPlaneTile));
-      wg_mg_max = std::max(1, wg_mg_max);
+      const double budget = double(kWgBarrierOffset);
+      const double xrun = double(wg_xrun_bytes(IN_pad));
+      // mg cap: 2 stages of (mg A tiles + 3 B planes + dataset run) must fit
+      wg_mg_max = std::max(1, std::min(kWgMgMax, int((budget / 2 - 3 * 128 * 128 - xrun) / kPlaneTile)));
       double total_cost = 0, cost[kMaxLayers], units[kMaxLayers];
+      const double iters = double(B) * (T_pad / 64);
       for (int j = 0; j <= L; ++j) {
         const int m_tiles = M_pad_w[j] / 128, n_tiles = N_pad[j] / n_tile_w[j];
-        const int mg_cap = std::min(wg_mg_max, std::min(m_tiles, 512 / n_tile_w[j]));
+        // mg: TMEM columns (mg * n_tile <= 512), the 2-stage smem cap, and the epilogue
+        // staging of mg f32 tiles (mg * 128 * n_tile * 4 bytes) within the budget
+        const int mg_epi = int(budget / (128.0 * n_tile_w[j] * 4));
+        const int mg_cap = std::max(1, std::min(std::min(wg_mg_max, mg_epi),
+                                                std::min(m_tiles, 512 / n_tile_w[j])));
         const int groups = (m_tiles + mg_cap - 1) / mg_cap;
         mg_w[j] = (m_tiles + groups - 1) / groups;  // balanced groups (6 tiles -> 3 + 3)
+        const double stage = double(wg_stage_bytes(n_tile_w[j], mg_w[j])) + (j == 0 ? xrun : 0.0);
+        wg_stages_l[j] = std::max(1, std::min(std::min(kWgStagesMax, wg_stages_cap), int(budget / stage)));
         const int m_groups = (m_tiles + mg_w[j] - 1) / mg_w[j];
         units[j] = double(m_groups) * n_tiles;
-        cost[j] = double(m_tiles) * n_tiles * n_tile_w[j];  // tensor time per sample
+        const double mma = 12.0 * mg_w[j] * (n_tile_w[j] / 2.0);     // cycles per iteration
+        const double per_it = std::max(mma, 3000.0 / wg_stages_l[j]);  // latency floor
+        cost[j] = units[j] * iters * per_it;
         total_cost += cost[j];
       }
       for (int j = 0; j <= L; ++j) {
@@ -400,7 +410,7 @@ struct snn_engine {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(wg_smem_bytes(128, wg_mg_max, wg_stages, IN_pad))));
+                            int(kWgSmemLaunch)));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
     {
@@ -686,10 +696,10 @@ struct snn_engine {
     {
       WgradArgs w{};
       w.n_layers = L + 1;
-      w.stages = wg_stages;
       w.x = ds.x.p;
       w.rows = rows_cur.p;
       w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
+      w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * B * 8 * 8 : nullptr;
       int blocks = 0;
       for (int j = 0; j <= L; ++j) {
         WgradLayer& g = w.layer[j];
@@ -699,11 +709,11 @@ struct snn_engine {
         g.M_pad = M_pad_w[j]; g.N_pad = N_pad[j]; g.n_tile = n_tile_w[j]; g.splits = splits_w[j];
         g.m_tiles = M_pad_w[j] / 128; g.n_tiles = N_pad[j] / n_tile_w[j];
         g.mg = mg_w[j]; g.m_groups = (g.m_tiles + g.mg - 1) / g.mg;
+        g.stages = wg_stages_l[j];
         g.block_start = blocks;
         blocks += g.m_groups * g.n_tiles * g.splits;
       }
-      launch(k_wgrad, dim3(blocks), dim3(kWgThreads),
-             wg_smem_bytes(128, wg_mg_max, wg_stages, IN_pad), wg_maps, w);
+      launch(k_wgrad, dim3(blocks), dim3(kWgThreads), kWgSmemLaunch, wg_maps, w);
       mark(evs, "wgrad", -1);
     }
     // gradient assembly (+ loss sum, hits, step counter)
@@ -868,7 +878,7 @@ struct snn_engine {
     }
     if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
     // clock stamps: slot 0 readout [B][8], slots 1..L fwd, L+1..2L bwd ([B*8 ctas][8] each)
-    if (on) dbg_clk.alloc(size_t(1 + 2 * L) * B * 8 * 8); else dbg_clk.free();
+    if (on) dbg_clk.alloc(size_t(2 + 2 * L) * B * 8 * 8); else dbg_clk.free();
     clear_graphs();
   }
 };
@@ -1218,7 +1228,7 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
     if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
     const int B = e->B, T = e->T, T_pad = e->T_pad;
     if (which == 5) {
-      const size_t need = size_t(1 + 2 * e->L) * B * 8 * 8 * sizeof(long long);
+      const size_t need = size_t(2 + 2 * e->L) * B * 8 * 8 * sizeof(long long);
       if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
       CK(cudaMemcpy(host, e->dbg_clk.p, need, cudaMemcpyDeviceToHost));
       return;

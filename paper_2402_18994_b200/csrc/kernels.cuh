@@ -1014,28 +1014,38 @@ struct WgradLayer {
   float* partial;          // [splits][M_pad][N_pad]
   int kind, M_pad, N_pad, n_tile, splits, m_tiles, n_tiles, block_start;
   int mg, m_groups;        // m-tiles per CTA (share every dI stage), groups
+  int stages;              // pipeline depth for this layer's stage size
 };
 // B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
 struct WgradArgs {
   WgradLayer layer[kMaxLayers];
-  int n_layers, stages;
+  int n_layers;
   const uint8_t* x;        // kind 0: staged dataset
   const uint32_t* rows;    // kind 0: [B]
+  long long* dbg_clk;      // optional [blocks][8] phase timestamps
   int B, T_pad, x_row_stride;
 };
 struct WgradMaps {
   CUtensorMap m[kMaxLayers];
 };
 
-constexpr int kWgStagesMax = 2;
+constexpr int kWgStagesMax = 6;
 constexpr int kWgMgMax = 4;
 constexpr int kWgThreads = 192;
 __host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile, int mg) {
   return uint32_t(mg) * kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // mg A tiles + 3 B planes
 }
-__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages, int x_row_stride) {
-  return uint32_t(stages) * (wg_stage_bytes(n_tile, mg) + ((8u * x_row_stride + 1023) & ~1023u)) + 1024 + 256;
+__host__ __device__ constexpr uint32_t wg_xrun_bytes(int x_row_stride) {
+  return (8u * uint32_t(x_row_stride) + 1023) & ~1023u;
 }
+__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages, int x_row_stride) {
+  return uint32_t(stages) * (wg_stage_bytes(n_tile, mg) + wg_xrun_bytes(x_row_stride)) + 1024 + 256;
+}
+// the launch always requests the full carve-out: barriers at kWgBarrierOffset
+constexpr uint32_t kWgSmemLaunch = 227 * 1024;
+
+// barriers at a fixed offset past the largest per-layer stage footprint
+constexpr uint32_t kWgBarrierOffset = 227 * 1024 - 2048;
 
 // One launch for every Linear layer: block -> (layer, m-group, n-tile, split).
 // A CTA accumulates mg M-tiles (mg x n_tile TMEM columns) so each dI stage
@@ -1044,6 +1054,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad(const __grid_constant__ WgradMaps maps, WgradArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  long long* clk = args.dbg_clk != nullptr ? args.dbg_clk + size_t(blockIdx.x) * 8 : nullptr;
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[0] = clock64();
+    clk[6] = globaltimer();
+  }
   int li = 0;
   while (li + 1 < args.n_layers && int(blockIdx.x) >= args.layer[li + 1].block_start) ++li;
   const WgradLayer a = args.layer[li];
@@ -1053,14 +1068,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const int split = local / (a.m_groups * a.n_tiles);
   const int mt0 = mgi * a.mg;
   const int nm = min(a.mg, a.m_tiles - mt0);  // M-tiles of this CTA
-  const int S = args.stages;
+  const int S = a.stages;
   const uint32_t stage_bytes = wg_stage_bytes(a.n_tile, a.mg);
   const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: n_tile rows x 64 cols
   // kind 0: the dataset bytes of one (sample, 64-step block) are one contiguous
   // run of 8 * x_row_stride bytes -> one bulk copy per stage into xbuf
   const uint32_t xbytes = a.kind == 0 ? 8u * uint32_t(args.x_row_stride) : 0u;
   uint8_t* xbuf = smem + S * stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + S * ((xbytes + 1023) & ~1023u));
+  // barriers live at the end of the (max-sized) dynamic smem, past every layer's stages
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgBarrierOffset);
   uint64_t* empty = full + S;
   uint64_t* xfull = empty + S;
   uint64_t* acc_full = xfull + S;
@@ -1087,6 +1103,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   __syncthreads();
   tc_fence_after();
   pdl_wait();
+  if (clk != nullptr && threadIdx.x == 0) clk[1] = clock64();
   const uint32_t tmem = *tmem_slot;
   if (warp == 4) {
     if (elect_one()) {
@@ -1116,6 +1133,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int s = it % S, ph = (it / S) & 1;
         mbar_wait(&full[s], ph);
         tc_fence_after();
+        if (clk != nullptr && it == 0) clk[2] = clock64();
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bp = A + a.mg * kPlaneTile;
 #pragma unroll
@@ -1132,6 +1150,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         umma_commit(&empty[s]);
       }
       umma_commit(&acc_full[0]);
+      if (clk != nullptr) clk[3] = clock64();
     }
     __syncwarp();
   } else if (warp < 4) {
@@ -1185,29 +1204,39 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
       for (int m = 0; m < kWgMgMax; ++m) cur[m] = nxt[m];
     }
-    // epilogue: thread = output row of each M-tile, n_tile columns
+    // epilogue: TMEM -> smem (row per thread; chunk order rotated per row to
+    // spread banks) -> one 1-D bulk store per output row (coalesced, async)
     mbar_wait(&acc_full[0], 0);
     tc_fence_after();
+    if (clk != nullptr && threadIdx.x == 0) clk[4] = clock64();
+    const uint32_t row_bytes = uint32_t(a.n_tile) * 4u;
     for (int m = 0; m < nm; ++m) {
-      const int k = (mt0 + m) * 128 + tid;
-      float* dst = a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile;
+      uint8_t* srow = smem + (size_t(m) * 128 + tid) * row_bytes;  // stages are free now
       for (int c = 0; c < a.n_tile / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + m * a.n_tile + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 v4 = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                  __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-          if (total == 0) v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          *reinterpret_cast<float4*>(dst + c * 32 + j) = v4;
+        for (int jj = 0; jj < 8; ++jj) {
+          const int j = (jj + tid) & 7;  // rotate the 16-byte chunk order per row
+          uint4 v4 = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          if (total == 0) v4 = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(srow + c * 128 + j * 16) = v4;
         }
       }
+      fence_async_smem();
+      const int k = (mt0 + m) * 128 + tid;
+      bulk_store(a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile, srow, row_bytes);
     }
+    bulk_commit_wait_all();
     tc_fence_before();
   }
   pdl_launch_dependents();
   __syncthreads();
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[5] = clock64();
+    clk[7] = globaltimer();
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc_any(tmem_cols, tmem);

@@ -24,3 +24,12 @@ for s, name in ((1, "fwd0"), (2, "fwd1")):
     st, en = c[valid, 6], c[valid, 7]
     t0 = st.min()
     print(f"{name}: CTAs {valid.sum()}  start spread {(st.max()-t0)/1e3:.1f} us  end spread {(en.min()-t0)/1e3:.1f}..{(en.max()-t0)/1e3:.1f} us  per-CTA median {np.median(en-st)/1e3:.1f} us")
+c = clk[1 + 2 * L]
+valid = c[:, 6] > 0
+c = c[valid]
+d = np.stack([c[:, 1] - c[:, 0], c[:, 2] - c[:, 1], c[:, 3] - c[:, 2], c[:, 4] - c[:, 3], c[:, 5] - c[:, 4]], 1)
+print("wgrad CTAs", valid.sum(), "[prologue, first-stage, mma-loop, commit->epi, epilogue] median", np.median(d, 0).astype(int).tolist(), "max", d.max(0).tolist())
+gt = c[:, 6:8]; t0 = gt[:, 0].min()
+print(f"wgrad start spread {(gt[:,0].max()-t0)/1e3:.1f} us, end {(gt[:,1].min()-t0)/1e3:.1f}..{(gt[:,1].max()-t0)/1e3:.1f} us; clock {np.median((c[:,5]-c[:,0])/((gt[:,1]-gt[:,0])*1e-3)):.0f} MHz")
+for blk in (0, 60, 119, 125, 140, 147):
+    if blk < len(c): print("  cta", blk, (c[blk, 1:6] - c[blk, 0:5]).tolist())
