@@ -305,8 +305,7 @@ def main():
         if dist is not None:
             dist.barrier()
 
-    for i in range(warmup):
-        eng.enqueue_step(i)
+    eng.enqueue_steps(0, warmup)
     eng.sync()
     barrier()
     torch.cuda.synchronize()
@@ -314,8 +313,7 @@ def main():
     t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         t_start.record(stream)
-        for i in range(args.steps):
-            eng.enqueue_step(warmup + i)
+        eng.enqueue_steps(warmup, args.steps)
         t_end.record(stream)
         eng.sync()
         torch.cuda.synchronize()

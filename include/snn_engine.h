@@ -151,10 +151,14 @@ snn_status snn_train_epochs_from(snn_engine* e, size_t first_epoch, size_t epoch
                                  double* metrics);
 
 /* Asynchronous stepping for throughput measurement: enqueue one full step
- * (captured CUDA graph) on the engine stream with batch rows taken from the
- * device index buffer slot `slot` of the uploaded schedule; no host sync. */
+ * (captured CUDA graph) on the engine stream with batch rows taken from slot
+ * `slot` of the uploaded device-resident schedule; no host sync.  The slot is
+ * a device counter the step advances, so consecutive slots need no host->device
+ * traffic.  snn_enqueue_steps enqueues slots [first_slot, first_slot + n_steps)
+ * as multi-step graphs (8 steps per graph launch). */
 snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_steps);
 snn_status snn_enqueue_step(snn_engine* e, size_t slot);
+snn_status snn_enqueue_steps(snn_engine* e, size_t first_slot, size_t n_steps);
 snn_status snn_sync(snn_engine* e);
 snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy);
 /* cudaStream_t of the engine, for CUDA-event timing by the caller. */

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 #include <vector>
@@ -186,6 +187,10 @@ struct snn_engine {
   DevBuf<float> bc;
   size_t bc_steps = 0;
   DevBuf<int64_t> step;
+  int64_t host_step = 0;               // host mirror of *step (advanced per update launch)
+  DevBuf<int64_t> sched_slot;          // schedule mode: slot of the next step (device counter)
+  DevBuf<unsigned int> tail_done;      // completion counter of k_reduce_adam
+  size_t slot_expected = ~size_t(0);   // host mirror of *sched_slot
   DevBuf<__nv_bfloat16> wt[kMaxLayers], wb[kMaxLayers];
   // activations
   DevBuf<float> V[SNN_MAX_HIDDEN];
@@ -213,8 +218,9 @@ struct snn_engine {
   bool debug = false;
   DevBuf<float> dbg_i[SNN_MAX_HIDDEN], dbg_ds[SNN_MAX_HIDDEN], dbg_trace;
   DevBuf<long long> dbg_clk;
-  // graphs keyed by (dataset ptr, update flag)
-  std::map<std::pair<const void*, int>, cudaGraphExec_t> graphs;
+  // graphs keyed by (dataset ptr, update flag, mode): mode 0 = rows_cur, mode g >= 1 =
+  // g consecutive schedule steps (rows from sched[*sched_slot])
+  std::map<std::tuple<const void*, int, int>, cudaGraphExec_t> graphs;
   // multi-GPU
   void* comm_handle = nullptr;
   int rank = 0, world = 1;
@@ -367,6 +373,8 @@ struct snn_engine {
     v.alloc(n_params);
     comm.alloc(n_params + 2);
     step.alloc(1);
+    sched_slot.alloc(1);
+    tail_done.alloc(1);
     grow_bc(1 << 20);
     for (int j = 0; j < L; ++j) {
       wt[j].alloc(size_t(3) * N_pad[j] * K_pad[j]);
@@ -426,6 +434,7 @@ struct snn_engine {
 
   void grow_bc(size_t steps) {
     if (steps <= bc_steps) return;
+    if (stream) CK(cudaStreamSynchronize(stream));  // graphs in flight hold the old table
     std::vector<float> h(2 * steps);
     const float b1 = cfg.beta1, b2 = cfg.beta2;
     for (size_t s = 0; s < steps; ++s) {
@@ -442,10 +451,10 @@ struct snn_engine {
     clear_graphs();
   }
 
-  void ensure_bc_capacity() {
-    int64_t s = 0;
-    CK(cudaMemcpy(&s, step.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    if (size_t(s) + 2 > bc_steps) grow_bc(std::max(bc_steps * 2, size_t(s) + 2));
+  // bias-correction table must cover the next `more` update steps
+  void ensure_bc_capacity(size_t more = 1) {
+    const size_t need = size_t(host_step) + more + 1;
+    if (need > bc_steps) grow_bc(std::max(bc_steps * 2, need));
   }
 
   // ---------------------------------------------------------- parameters
@@ -609,7 +618,8 @@ struct snn_engine {
   }
 
   // ---------------------------------------------------------------- step
-  int launches_per_step() const { return 2 * L + 5; }
+  // L fwd + readout + L bwd + wgrad + tail (fused reduce+Adam on one rank; reduce, adam otherwise)
+  int launches_per_step() const { return 2 * L + (world == 1 ? 4 : 5); }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;
@@ -625,15 +635,19 @@ struct snn_engine {
     }
   }
 
-  void enqueue_body(const Dataset& ds, int update, std::vector<cudaEvent_t>* evs = nullptr) {
-    const size_t rows = size_t(B) * T_pad;
+  // One step.  sched_mode: rows = sched[*sched_slot] (advanced by the step tail).
+  void enqueue_body(const Dataset& ds, int update, std::vector<cudaEvent_t>* evs = nullptr,
+                    bool sched_mode = false) {
     launch_names.clear();
+    const uint32_t* rows_p = sched_mode ? sched.p : rows_cur.p;
+    const int64_t* slot_p = sched_mode ? sched_slot.p : nullptr;
     if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
     // forward
     for (int l = 0; l < L; ++l) {
       FwdArgs f{};
       f.x = ds.x.p;
-      f.rows = rows_cur.p;
+      f.rows = rows_p;
+      f.rows_slot = slot_p;
       f.s_in = l > 0 ? s_np[l - 1].p : nullptr;
       f.beta = params.p + entry_of(kEntryBeta, l).offset;
       f.bias = net.bias ? params.p + entry_of(kEntryB, l).offset : nullptr;
@@ -655,7 +669,8 @@ struct snn_engine {
     {
       ReadoutArgs r{};
       r.s_in = s_np[L - 1].p;
-      r.rows = rows_cur.p;
+      r.rows = rows_p;
+      r.rows_slot = slot_p;
       r.labels = ds.labels.p;
       r.w = params.p + entry_of(kEntryW, L).offset;
       r.bias = net.bias ? params.p + entry_of(kEntryB, L).offset : nullptr;
@@ -697,7 +712,8 @@ struct snn_engine {
       WgradArgs w{};
       w.n_layers = L + 1;
       w.x = ds.x.p;
-      w.rows = rows_cur.p;
+      w.rows = rows_p;
+      w.rows_slot = slot_p;
       w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
       w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * B * 8 * 8 : nullptr;
       int blocks = 0;
@@ -740,6 +756,14 @@ struct snn_engine {
       r.B = B;
       r.w_blocks = int((n_params + 255) / 256);
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
+      if (update && world == 1) {
+        // single rank: no allreduce between reduction and update -> one kernel
+        AdamArgs a = adam_args(1);
+        launch(k_reduce_adam, dim3(blocks), dim3(256), 0, r, a, tail_done.p,
+               sched_mode ? sched_slot.p : (int64_t*)nullptr);
+        mark(evs, "reduce_adam", -1);
+        return;
+      }
       launch(k_reduce, dim3(blocks), dim3(256), 0, r);
       mark(evs, "reduce", -1);
     }
@@ -751,6 +775,7 @@ struct snn_engine {
     }
     if (update) {
       AdamArgs a = adam_args(1);
+      a.rows_slot = sched_mode ? sched_slot.p : nullptr;
       launch(k_adam, dim3(unsigned((n_params + 255) / 256)), dim3(256), 0, a);
       mark(evs, "adam", -1);
     } else {
@@ -771,6 +796,7 @@ struct snn_engine {
     if (ds.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
     auto key = std::make_pair(static_cast<const void*>(ds.x.p), 1);
     cudaGraphExec_t ex = nullptr;
+    ensure_bc_capacity(64 + 4 * size_t(steps));
     auto it = prof_graphs.find(key);
     if (it == prof_graphs.end()) {
       cudaGraph_t g;
@@ -793,12 +819,12 @@ struct snn_engine {
     // keep the GPU busy (boost clocks) around every profiled step: the event
     // graph runs between plain step graphs, one sync per 4 steps
     cudaGraphExec_t plain = graph_for(ds, 1);
-    ensure_bc_capacity();
     for (int w = 0; w < 64; ++w) CK(cudaGraphLaunch(plain, stream));
+    host_step += 64;
     for (int s = 0; s < steps; ++s) {
-      ensure_bc_capacity();
       CK(cudaGraphLaunch(ex, stream));
       for (int w = 0; w < 3; ++w) CK(cudaGraphLaunch(plain, stream));
+      host_step += 4;
       CK(cudaStreamSynchronize(stream));
       for (size_t i = 0; i < nl; ++i) {
         float ms = 0;
@@ -816,14 +842,16 @@ struct snn_engine {
     fail(SNN_ERR_ARGUMENT, "no entry kind %d layer %d", kind, layer);
   }
 
-  cudaGraphExec_t graph_for(const Dataset& ds, int update) {
-    auto key = std::make_pair(static_cast<const void*>(ds.x.p), update);
+  // mode 0: one step on rows_cur; mode g >= 1: g schedule steps back to back
+  cudaGraphExec_t graph_for(const Dataset& ds, int update, int mode = 0) {
+    auto key = std::make_tuple(static_cast<const void*>(ds.x.p), update, mode);
     auto it = graphs.find(key);
     if (it != graphs.end()) return it->second;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     try {
-      enqueue_body(ds, update);
+      if (mode == 0) enqueue_body(ds, update);
+      for (int i = 0; i < mode; ++i) enqueue_body(ds, update, nullptr, true);
     } catch (...) {
       cudaStreamEndCapture(stream, &g);
       throw;
@@ -840,6 +868,25 @@ struct snn_engine {
     if (ds.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
     if (update) ensure_bc_capacity();
     CK(cudaGraphLaunch(graph_for(ds, update), stream));
+    if (update) ++host_step;
+  }
+
+  // `n` schedule steps starting at `slot`: graphs of kSchedGraphSteps steps, then singles
+  static constexpr int kSchedGraphSteps = 8;
+  void launch_sched(size_t slot, size_t n) {
+    if (data.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    if (slot + n > sched_steps) fail(SNN_ERR_ARGUMENT, "schedule slots [%zu, %zu) out of range", slot, slot + n);
+    ensure_bc_capacity(n);
+    if (slot != slot_expected) {
+      const int64_t s = int64_t(slot);  // pageable source: staged before the call returns
+      CK(cudaMemcpyAsync(sched_slot.p, &s, sizeof(s), cudaMemcpyHostToDevice, stream));
+    }
+    size_t done = 0;
+    for (; done + kSchedGraphSteps <= n; done += kSchedGraphSteps)
+      CK(cudaGraphLaunch(graph_for(data, 1, kSchedGraphSteps), stream));
+    for (; done < n; ++done) CK(cudaGraphLaunch(graph_for(data, 1, 1), stream));
+    slot_expected = slot + n;
+    host_step += int64_t(n);
   }
 
   void set_rows_host(const uint32_t* rows, const Dataset& ds) {
@@ -1002,6 +1049,7 @@ snn_status snn_get_opt_state(snn_engine* e, float* m, float* v, uint64_t* step, 
     int64_t s = 0;
     CK(cudaMemcpyAsync(&s, e->step.p, 8, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    e->host_step = s;
     if (step) *step = uint64_t(s);
   });
 }
@@ -1016,6 +1064,8 @@ snn_status snn_set_opt_state(snn_engine* e, const float* m, const float* v, uint
     CK(cudaMemcpyAsync(e->v.p, v, n * 4, cudaMemcpyHostToDevice, e->stream));
     CK(cudaMemcpyAsync(e->step.p, &s, 8, cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    e->host_step = s;
+    e->ensure_bc_capacity();
   });
 }
 
@@ -1097,21 +1147,29 @@ snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_ste
   return guard(e, [&] {
     for (size_t i = 0; i < n_steps * size_t(e->B); ++i)
       if (rows[i] >= e->data.n) fail(SNN_ERR_ARGUMENT, "schedule row outside dataset");
+    CK(cudaStreamSynchronize(e->stream));
     e->sched.alloc(n_steps * size_t(e->B), false);
     e->sched_steps = n_steps;
+    e->slot_expected = ~size_t(0);
     CK(cudaMemcpy(e->sched.p, rows, n_steps * e->B * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    e->ensure_bc_capacity();
+    e->clear_graphs();  // schedule-mode graphs bake the schedule pointer
+    if (e->data.n > 0) {  // capture both schedule graphs now, outside any timed region
+      e->graph_for(e->data, 1, 1);
+      e->graph_for(e->data, 1, snn_engine::kSchedGraphSteps);
+    }
   });
 }
 
 snn_status snn_enqueue_step(snn_engine* e, size_t slot) {
   if (!e) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
-    if (slot >= e->sched_steps) fail(SNN_ERR_ARGUMENT, "schedule slot %zu out of range", slot);
-    CK(cudaMemcpyAsync(e->rows_cur.p, e->sched.p + slot * size_t(e->B), sizeof(uint32_t) * e->B,
-                       cudaMemcpyDeviceToDevice, e->stream));
-    CK(cudaGraphLaunch(e->graph_for(e->data, 1), e->stream));
+    e->launch_sched(slot, 1);
   });
+}
+
+snn_status snn_enqueue_steps(snn_engine* e, size_t first_slot, size_t n_steps) {
+  if (!e) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] { e->launch_sched(first_slot, n_steps); });
 }
 
 snn_status snn_sync(snn_engine* e) {

@@ -32,6 +32,14 @@ using namespace sm100;
 
 constexpr int kMaxClasses = 32;
 constexpr int kMaxLayers = 9;  // Linear layers (hidden + readout)
+// debug phase-timestamp record per CTA; [14]/[15] = globaltimer start/end
+constexpr int kClkStride = 16;
+
+// The step's dataset rows: a fixed [B] buffer, or (schedule mode) slot *slot of
+// a device-resident schedule [steps][B] whose slot counter the step tail advances.
+__device__ __forceinline__ const uint32_t* batch_rows(const uint32_t* rows, const int64_t* slot, int B) {
+  return slot != nullptr ? rows + size_t(*slot) * size_t(B) : rows;
+}
 
 // ------------------------------------------------------------ small helpers
 // clip(beta,0,1) = std::min(1, std::max(0, beta)) exactly (ops.hpp clip).
@@ -152,6 +160,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 struct FwdArgs {
   const uint8_t* x;       // staged dataset (layer 0)
   const uint32_t* rows;   // [B] dataset row per sample (layer 0)
+  const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
   const uint32_t* s_in;   // neuron-packed spikes of the previous layer (layer > 0)
   const float* beta;      // [H]
   const float* bias;      // [H] or nullptr
@@ -261,10 +270,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = blockIdx.x * SPB, nt = blockIdx.y;
   const int nsamp = min(SPB, a.B - b0);
-  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * kClkStride : nullptr;
   if (clk != nullptr && threadIdx.x == 0) {
     clk[0] = clock64();
     clk[6] = globaltimer();
+    clk[14] = clk[6];
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    clk[4] = smid;
   }
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
@@ -300,6 +313,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // ---------------- TMA producer: the three W^T planes of each k-block
     if (elect_one()) {
       tma_prefetch(&tm_w);
+      const uint32_t* rows = batch_rows(a.rows, a.rows_slot, a.B);
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1, kb = (it % KB + rot) % KB;
         if (a.in_kind == 0 && it % KB == 0) {
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mbar_arrive_expect_tx(&xfull[xb], uint32_t(nsamp) * xrun);
           for (int sm = 0; sm < nsamp; ++sm)
             bulk_load(xbuf + xb * xbuf_bytes + sm * xrun,
-                      a.x + (size_t(a.rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(a.K_pad),
+                      a.x + (size_t(rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(a.K_pad),
                       xrun, &xfull[xb]);
         }
         mbar_wait(&empty[s], ph ^ 1);
@@ -446,6 +460,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (clk != nullptr && threadIdx.x == 0) {
     clk[3] = clock64();
     clk[7] = globaltimer();
+    clk[15] = clk[7];
   }
   if (warp == 0) {
     tc_fence_after();
@@ -461,6 +476,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 struct ReadoutArgs {
   const uint32_t* s_in;     // neuron-packed spikes of the last hidden layer
   const uint32_t* rows;     // [B]
+  const int64_t* rows_slot; // schedule mode: rows += *rows_slot * B (else nullptr)
   const int32_t* labels;    // dataset labels [N]
   const float* w;           // readout W [HL][C] f32 (master)
   const float* bias;        // [C] or nullptr
@@ -497,11 +513,12 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   uint32_t* spk = reinterpret_cast<uint32_t*>(w + ((size_t(a.HL) * C + 3) & ~size_t(3)));  // [T][hw]
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-#define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * 8 + (k)] = clock64();
+#define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
   pdl_wait();
   RO_CLK(0)
+  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
   __shared__ int s_label;
-  if (tid == 0) s_label = a.labels[a.rows[b]];
+  if (tid == 0) s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
   const float beta_l = lane < C ? a.beta[lane] : 0.0f;
   {
     // W rows (HL*C floats, 16-byte aligned when C % 4 == 0) and the spike words
@@ -664,6 +681,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   }
   __syncthreads();
   RO_CLK(7)
+  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 15] = globaltimer();
 #undef RO_CLK
 }
 
@@ -798,8 +816,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x, nt = blockIdx.y;
-  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * 8 : nullptr;
-  if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * kClkStride : nullptr;
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[0] = clock64();
+    clk[14] = globaltimer();
+  }
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
@@ -993,7 +1014,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   }
   pdl_launch_dependents();
   __syncthreads();
-  if (clk != nullptr && threadIdx.x == 0) clk[6] = clock64();
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[6] = clock64();
+    clk[15] = globaltimer();
+  }
   if (warp == 0) {
     tc_fence_after();
     if (tmem_cols == 256) tmem_dealloc<256>(tmem);
@@ -1022,7 +1046,8 @@ struct WgradArgs {
   int n_layers;
   const uint8_t* x;        // kind 0: staged dataset
   const uint32_t* rows;    // kind 0: [B]
-  long long* dbg_clk;      // optional [blocks][8] phase timestamps
+  const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
+  long long* dbg_clk;      // optional [blocks][kClkStride] phase timestamps
   int B, T_pad, x_row_stride;
 };
 struct WgradMaps {
@@ -1054,7 +1079,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     k_wgrad(const __grid_constant__ WgradMaps maps, WgradArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  long long* clk = args.dbg_clk != nullptr ? args.dbg_clk + size_t(blockIdx.x) * 8 : nullptr;
+  long long* clk = args.dbg_clk != nullptr ? args.dbg_clk + size_t(blockIdx.x) * kClkStride : nullptr;
   if (clk != nullptr && threadIdx.x == 0) {
     clk[0] = clock64();
     clk[6] = globaltimer();
@@ -1108,6 +1133,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   if (warp == 4) {
     if (elect_one()) {
       tma_prefetch(tm_di);
+      const uint32_t* rows = batch_rows(args.rows, args.rows_slot, args.B);
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1;
         const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
@@ -1115,7 +1141,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         if (a.kind == 0) {
           mbar_arrive_expect_tx(&xfull[s], xbytes);
           bulk_load(xbuf + s * ((xbytes + 1023) & ~1023u),
-                    args.x + (size_t(args.rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride,
+                    args.x + (size_t(rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride,
                     xbytes, &xfull[s]);
         }
         mbar_arrive_expect_tx(&full[s], 3 * ptile);
@@ -1236,6 +1262,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   if (clk != nullptr && threadIdx.x == 0) {
     clk[5] = clock64();
     clk[7] = globaltimer();
+    clk[14] = clk[6];
+    clk[15] = clk[7];
   }
   if (warp == 0) {
     tc_fence_after();
@@ -1385,37 +1413,27 @@ struct AdamArgs {
   int B_global;
   float* loss_out;
   double* acc_out;
+  int64_t* rows_slot;        // schedule mode: advanced once per update (else nullptr)
 };
 
-__global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
-  pdl_wait();
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (a.update && i == 0) {
-    // StepResult{loss, accuracy} (optimize.hpp:143-147, :193-196)
-    *a.loss_out = __fdiv_rn(a.grads[a.n_params], float(a.B_global));
-    *a.acc_out = double(a.grads[a.n_params + 1]) / double(a.B_global);
-  }
-  if (i >= a.n_params) return;
+// Adam on one flat parameter (optimize.hpp:88-110); bias corrections of step s+1.
+__device__ __forceinline__ float adam_one(const AdamArgs& a, int64_t i, float g, float bc1, float bc2) {
   float p = a.params[i];
-  if (a.update) {
-    const int64_t s = *a.step - 1;  // bias correction of step s+1 (optimize.hpp:95-97)
-    const float bc1 = a.bc[2 * s], bc2 = a.bc[2 * s + 1];
-    const float g = a.grads[i];
-    const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(a.omb1, g));
-    const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(a.omb2, g), g));
-    const float mhat = __fdiv_rn(m, bc1);
-    const float vhat = __fdiv_rn(v, bc2);
-    p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
-    a.m[i] = m;
-    a.v[i] = v;
-    a.params[i] = p;
-  }
-  const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
-  if (en.kind != kEntryW) return;
-  const PlaneTarget pt = a.planes[en.layer];
+  const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(a.omb1, g));
+  const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(a.omb2, g), g));
+  const float mhat = __fdiv_rn(m, bc1);
+  const float vhat = __fdiv_rn(v, bc2);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
+  a.m[i] = m;
+  a.v[i] = v;
+  a.params[i] = p;
+  return p;
+}
+
+// bf16 operand planes of W element (k, n) of Linear `layer` from its f32 master.
+__device__ __forceinline__ void refresh_planes(const AdamArgs& a, int layer, int64_t k, int64_t n, float p) {
+  const PlaneTarget pt = a.planes[layer];
   if (pt.wt == nullptr && pt.wb == nullptr) return;
-  const int64_t li = i - en.offset;
-  const int64_t k = li / en.cols, n = li % en.cols;
   __nv_bfloat16 h, mi, lo;
   split3(p, h, mi, lo);
   if (pt.wt != nullptr) {
@@ -1429,6 +1447,126 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
     pt.wb[idx] = h;
     pt.wb[plane + idx] = mi;
     pt.wb[2 * plane + idx] = lo;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
+  pdl_wait();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a.update && i == 0) {
+    // StepResult{loss, accuracy} (optimize.hpp:143-147, :193-196)
+    *a.loss_out = __fdiv_rn(a.grads[a.n_params], float(a.B_global));
+    *a.acc_out = double(a.grads[a.n_params + 1]) / double(a.B_global);
+    if (a.rows_slot != nullptr) *a.rows_slot += 1;
+  }
+  if (i >= a.n_params) return;
+  float p = a.params[i];
+  if (a.update) {
+    const int64_t s = *a.step - 1;  // bias correction of step s+1 (optimize.hpp:95-97)
+    p = adam_one(a, i, a.grads[i], a.bc[2 * s], a.bc[2 * s + 1]);
+  }
+  const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
+  if (en.kind != kEntryW) return;
+  const int64_t li = i - en.offset;
+  refresh_planes(a, en.layer, li / en.cols, li % en.cols, p);
+}
+
+// Single-rank step tail: k_reduce + k_adam in one launch (no allreduce between
+// them).  Same block roles and the same fixed-order sums as k_reduce, each
+// gradient consumed by Adam in the thread that produced it.  Every block reads
+// the step counter first; the last block to finish (completion counter) advances
+// it and the schedule slot, so no block can observe the advanced value.
+__global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, unsigned int* done,
+                                                     int64_t* rows_slot) {
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const int64_t s = *reinterpret_cast<volatile const int64_t*>(r.step);  // this step's bias corrections: table entry s (optimize.hpp:95-97)
+  const float bc1 = a.bc[2 * s], bc2 = a.bc[2 * s + 1];
+  const int vb_blocks = (r.n_vec + 7) / 8;
+  if (int(blockIdx.x) < r.w_blocks) {
+    const int64_t i = int64_t(blockIdx.x) * 256 + tid;
+    if (i < r.n_params) {
+      const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
+      if (en.kind == kEntryW) {
+        const int64_t li = i - en.offset;
+        const int j = en.layer;
+        const int64_t k = li / en.cols, n = li % en.cols;
+        const float* __restrict__ p = r.partial[j] + k * r.N_pad[j] + n;
+        const int64_t sstride = int64_t(r.M_pad[j]) * r.N_pad[j];
+        const int S = r.splits[j];
+        float g = 0.0f;
+        int q0 = 0;
+        for (; q0 + 16 <= S; q0 += 16) {
+          float x[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) x[q] = __ldg(p + (q0 + q) * sstride);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) g = __fadd_rn(g, x[q]);
+        }
+        for (; q0 < S; ++q0) g = __fadd_rn(g, __ldg(p + q0 * sstride));
+        r.grads[i] = g;
+        refresh_planes(a, j, k, n, adam_one(a, i, g, bc1, bc2));
+      }
+    }
+  } else if (int(blockIdx.x) < r.w_blocks + vb_blocks) {
+    const int warp = tid >> 5, lane = tid & 31;
+    const int v = (int(blockIdx.x) - r.w_blocks) * 8 + warp;
+    if (v < r.n_vec) {
+      const int64_t i = r.vec_index[v];
+      const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
+      const int64_t li = i - en.offset;
+      const float* __restrict__ src =
+          (en.kind == kEntryB ? r.dbias_part[en.layer] : r.dbeta_part[en.layer]) + li;
+      float g = 0.0f;
+      for (int b = lane; b < r.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
+      if (lane == 0) {
+        if (en.kind == kEntryBeta) {
+          const float beta = r.params[i];
+          if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
+        }
+        r.grads[i] = g;
+        adam_one(a, i, g, bc1, bc2);
+      }
+    }
+  } else {
+    // loss sum in batch order (objective.hpp:57-72) + hits -> StepResult
+    __shared__ float sl[1024];
+    __shared__ int sc[1024];
+    float loss = 0.0f;
+    int hits = 0;
+    for (int b0 = 0; b0 < r.B; b0 += 1024) {
+      const int nb = min(1024, r.B - b0);
+      __syncthreads();
+      for (int i = tid; i < nb; i += 256) {
+        sl[i] = r.loss_b[b0 + i];
+        sc[i] = r.correct_b[b0 + i];
+      }
+      __syncthreads();
+      if (tid == 0)
+        for (int i = 0; i < nb; ++i) {
+          loss = __fadd_rn(loss, sl[i]);
+          hits += sc[i];
+        }
+    }
+    if (tid == 0) {
+      r.grads[r.n_params] = loss;
+      r.grads[r.n_params + 1] = float(hits);
+      *a.loss_out = __fdiv_rn(loss, float(a.B_global));
+      *a.acc_out = double(hits) / double(a.B_global);
+    }
+  }
+  // completion: the last block advances the step (and schedule slot) counters
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *done = 0u;
+      *r.step = s + 1;
+      if (rows_slot != nullptr) *rows_slot += 1;
+      __threadfence();
+    }
   }
 }
 

@@ -179,7 +179,7 @@ def lib() -> C.CDLL:
                  "snn_set_params", "snn_get_params", "snn_init_params", "snn_get_opt_state",
                  "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
                  "snn_train_step_packed", "snn_forward_backward", "snn_train_epochs",
-                 "snn_upload_schedule", "snn_enqueue_step", "snn_sync", "snn_read_result",
+                 "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_sync", "snn_read_result",
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
                  "snn_read_dataset"):
@@ -377,6 +377,10 @@ class Engine:
     def enqueue_step(self, slot: int):
         self._check(self._L.snn_enqueue_step(self._h, C.c_size_t(slot)))
 
+    def enqueue_steps(self, first_slot: int, n_steps: int):
+        """Schedule slots [first_slot, first_slot + n_steps), 8 steps per graph launch."""
+        self._check(self._L.snn_enqueue_steps(self._h, C.c_size_t(first_slot), C.c_size_t(n_steps)))
+
     def sync(self):
         self._check(self._L.snn_sync(self._h))
 
@@ -423,7 +427,7 @@ class Engine:
         idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5}[which]
         B, T = self.batch_size, self.time_steps
         if which == "clk":
-            out = np.empty((2 + 2 * len(self.desc["hidden"]), B * 8, 8), np.int64)
+            out = np.empty((2 + 2 * len(self.desc["hidden"]), B * 4, 16), np.int64)
         elif which == "trace":
             out = np.empty((B, T, self.desc["classes"]), np.float32)
         else:

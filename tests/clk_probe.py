@@ -33,3 +33,21 @@ gt = c[:, 6:8]; t0 = gt[:, 0].min()
 print(f"wgrad start spread {(gt[:,0].max()-t0)/1e3:.1f} us, end {(gt[:,1].min()-t0)/1e3:.1f}..{(gt[:,1].max()-t0)/1e3:.1f} us; clock {np.median((c[:,5]-c[:,0])/((gt[:,1]-gt[:,0])*1e-3)):.0f} MHz")
 for blk in (0, 60, 119, 125, 140, 147):
     if blk < len(c): print("  cta", blk, (c[blk, 1:6] - c[blk, 0:5]).tolist())
+c = clk[1][:128]
+g = c[:, 1] - c[:, 0]
+sm = c[:, 4]
+order = np.argsort(g)
+print("fwd0 GEMM-phase cycles by CTA (fastest 6 / slowest 10): ", [(int(i), int(sm[i]), int(g[i])) for i in order[:6]], [(int(i), int(sm[i]), int(g[i])) for i in order[-10:]])
+print("  slow (> 1.5x median) CTA ids:", sorted(np.where(g > 1.5 * np.median(g))[0].tolist()))
+print("  smids of slow:", sorted(sm[g > 1.5 * np.median(g)].tolist()))
+
+# timeline of one replay (globaltimer slots 14/15), kernels in launch order
+order = [f"fwd{l}" for l in range(L)] + ["readout"] + [f"bwd{l}" for l in reversed(range(L))] + ["wgrad"]
+slot = {"readout": 0, "wgrad": 1 + 2 * L, **{f"fwd{l}": 1 + l for l in range(L)}, **{f"bwd{l}": 1 + L + l for l in range(L)}}
+t0 = None
+for name in order:
+    c = clk[slot[name]]
+    v = c[:, 14] > 0
+    st, en = c[v, 14], c[v, 15]
+    if t0 is None: t0 = st.min()
+    print(f"TL {name:8s} ctas {v.sum():4d} start {(st.min()-t0)/1e3:7.1f} .. {(st.max()-t0)/1e3:7.1f}  end {(en.min()-t0)/1e3:7.1f} .. {(en.max()-t0)/1e3:7.1f} us  span {(en.max()-st.min())/1e3:6.1f}  cta med {np.median(en-st)/1e3:5.1f}")

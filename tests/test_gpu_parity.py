@@ -247,3 +247,34 @@ def test_epoch_permutation_matches_reference(orc):
     for e in (0, 3):
         ref = orc.permutation(orc.key_child(orc.key_child(orc.key_from_seed(7), 1 + e), 0), 500)
         assert np.array_equal(eng.epoch_permutation(e, 500), ref)
+
+
+def test_schedule_steps_match_train_step(orc):
+    """Device-resident schedule (8-step graphs, device slot counter, fused step
+    tail) == host-driven train_step on the same rows, bit for bit; a slot jump
+    re-seeds the device counter."""
+    net = Net(inp=30, hidden=(16, 12), classes=5)
+    B, T, N = 4, 19, 40
+    x, y = orc.synth_raster(5, N, T, 30, 2)
+    pk = orc.pack_time(x)
+    rng = np.random.default_rng(3)
+    sched = rng.integers(0, N, size=(24, B)).astype(np.uint32)
+    order = list(range(0, 11)) + [17] + list(range(18, 21)) + [4]   # 8-graph + singles, jumps
+    ref = make_engine(net, B, T, seed=5)
+    ref.stage_dataset(pk, y)
+    for s in order:
+        last_ref = ref.train_step(sched[s])
+    eng = make_engine(net, B, T, seed=5)
+    eng.stage_dataset(pk, y)
+    eng.upload_schedule(sched.reshape(-1))
+    eng.enqueue_steps(0, 11)
+    eng.enqueue_step(17)
+    eng.enqueue_steps(18, 3)
+    eng.enqueue_steps(4, 1)
+    eng.sync()
+    assert eng.read_result() == last_ref
+    assert np.array_equal(eng.get_params(), ref.get_params())
+    m1, v1, s1 = eng.get_opt_state()
+    m2, v2, s2 = ref.get_opt_state()
+    assert s1 == s2 == len(order)
+    assert np.array_equal(m1, m2) and np.array_equal(v1, v2)
