@@ -324,8 +324,8 @@ struct snn_engine {
       for (int j = 0; j <= L; ++j) {
         const int m_tiles = M_pad_w[j] / 128, n_tiles = N_pad[j] / n_tile_w[j];
         // mg: TMEM columns (mg * n_tile <= 512), the 2-stage smem cap, and the epilogue
-        // staging of mg f32 tiles (mg * 128 * n_tile * 4 bytes) within the budget
-        const int mg_epi = int(budget / (128.0 * n_tile_w[j] * 4));
+        // staging of mg f32 tiles (mg * 128 padded rows) within the budget
+        const int mg_epi = int(budget / (128.0 * wg_epi_row_stride(n_tile_w[j])));
         const int mg_cap = std::max(1, std::min(std::min(wg_mg_max, mg_epi),
                                                 std::min(m_tiles, 512 / n_tile_w[j])));
         const int groups = (m_tiles + mg_cap - 1) / mg_cap;
@@ -759,8 +759,10 @@ struct snn_engine {
       if (update && world == 1) {
         // single rank: no allreduce between reduction and update -> one kernel
         AdamArgs a = adam_args(1);
+        long long* tclk = debug && size_t(blocks) <= size_t(B) * 64 / kClkStride
+                              ? dbg_clk.p + size_t(2 + 2 * L) * B * 8 * 8 : nullptr;
         launch(k_reduce_adam, dim3(blocks), dim3(256), 0, r, a, tail_done.p,
-               sched_mode ? sched_slot.p : (int64_t*)nullptr);
+               sched_mode ? sched_slot.p : (int64_t*)nullptr, tclk);
         mark(evs, "reduce_adam", -1);
         return;
       }
@@ -925,7 +927,7 @@ struct snn_engine {
     }
     if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
     // clock stamps: slot 0 readout [B][8], slots 1..L fwd, L+1..2L bwd ([B*8 ctas][8] each)
-    if (on) dbg_clk.alloc(size_t(2 + 2 * L) * B * 8 * 8); else dbg_clk.free();
+    if (on) dbg_clk.alloc(size_t(3 + 2 * L) * B * 8 * 8); else dbg_clk.free();
     clear_graphs();
   }
 };
@@ -1286,7 +1288,7 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
     if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
     const int B = e->B, T = e->T, T_pad = e->T_pad;
     if (which == 5) {
-      const size_t need = size_t(2 + 2 * e->L) * B * 8 * 8 * sizeof(long long);
+      const size_t need = size_t(3 + 2 * e->L) * B * 8 * 8 * sizeof(long long);
       if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
       CK(cudaMemcpy(host, e->dbg_clk.p, need, cudaMemcpyDeviceToHost));
       return;

@@ -81,13 +81,18 @@ __device__ __forceinline__ uint4 expand_bytes01(uint64_t m) {
   r.x = w[0]; r.y = w[1]; r.z = w[2]; r.w = w[3];
   return r;
 }
-// 8 bits (bit e = element e) -> 8 bf16.
+// 8 bits (bit e = element e) -> 8 bf16 (0 or 1.0).  The multiply spreads bit i
+// of a nibble to bit 8i (the four shifted copies do not overlap, so no carries),
+// x0xFF turns each byte into a 0x00/0xFF mask, PRMT duplicates mask bytes into
+// bf16 halves, AND applies the 1.0 pattern 0x3F80.
 __device__ __forceinline__ uint4 expand_bits_lsb(uint32_t byte) {
+  const uint32_t ml = (((byte & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+  const uint32_t mh = ((((byte >> 4) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
   uint4 r;
-  r.x = ((byte >> 0) & 1u) * 0x3F80u | ((byte >> 1) & 1u) * 0x3F800000u;
-  r.y = ((byte >> 2) & 1u) * 0x3F80u | ((byte >> 3) & 1u) * 0x3F800000u;
-  r.z = ((byte >> 4) & 1u) * 0x3F80u | ((byte >> 5) & 1u) * 0x3F800000u;
-  r.w = ((byte >> 6) & 1u) * 0x3F80u | ((byte >> 7) & 1u) * 0x3F800000u;
+  r.x = __byte_perm(ml, 0u, 0x1100u) & 0x3F803F80u;
+  r.y = __byte_perm(ml, 0u, 0x3322u) & 0x3F803F80u;
+  r.z = __byte_perm(mh, 0u, 0x1100u) & 0x3F803F80u;
+  r.w = __byte_perm(mh, 0u, 0x3322u) & 0x3F803F80u;
   return r;
 }
 // 8 bits MSB-first (bit 7-e = element e) -> 8 bf16 (dataset time bits).
@@ -1056,7 +1061,14 @@ struct WgradMaps {
 
 constexpr int kWgStagesMax = 6;
 constexpr int kWgMgMax = 4;
-constexpr int kWgThreads = 192;
+#ifndef SNN_WG_EXP
+#define SNN_WG_EXP 0  // timing experiments (tests/clk_probe.py only): 1 no decode, 2 one dI plane, 3 no MMA
+#endif
+// A-operand producers: kWgProdWarps warps; thread p decodes row p % 128 of every
+// M-tile, time half p / 128 (64 steps per stage = 2 halves of 32)
+constexpr int kWgProdWarps = 8;
+constexpr int kWgProd = 32 * kWgProdWarps;
+constexpr int kWgThreads = kWgProd + 64;  // + TMA warp + MMA warp
 __host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile, int mg) {
   return uint32_t(mg) * kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // mg A tiles + 3 B planes
 }
@@ -1066,6 +1078,8 @@ __host__ __device__ constexpr uint32_t wg_xrun_bytes(int x_row_stride) {
 __host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages, int x_row_stride) {
   return uint32_t(stages) * (wg_stage_bytes(n_tile, mg) + wg_xrun_bytes(x_row_stride)) + 1024 + 256;
 }
+// epilogue staging row stride (f32 row of n_tile + 16 bytes of bank padding)
+__host__ __device__ constexpr uint32_t wg_epi_row_stride(int n_tile) { return uint32_t(n_tile) * 4u + 16u; }
 // the launch always requests the full carve-out: barriers at kWgBarrierOffset
 constexpr uint32_t kWgSmemLaunch = 227 * 1024;
 
@@ -1116,7 +1130,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1 + 128);
+      mbar_init(&full[s], 1 + kWgProd);
       mbar_init(&empty[s], 1);
       mbar_init(&xfull[s], 1);
     }
@@ -1130,7 +1144,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   pdl_wait();
   if (clk != nullptr && threadIdx.x == 0) clk[1] = clock64();
   const uint32_t tmem = *tmem_slot;
-  if (warp == 4) {
+  if (warp == kWgProdWarps) {
     if (elect_one()) {
       tma_prefetch(tm_di);
       const uint32_t* rows = batch_rows(args.rows, args.rows_slot, args.B);
@@ -1144,15 +1158,20 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     args.x + (size_t(rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride,
                     xbytes, &xfull[s]);
         }
-        mbar_arrive_expect_tx(&full[s], 3 * ptile);
+#if SNN_WG_EXP == 2
+        constexpr int kLoadPlanes = 1;  // timing experiment only
+#else
+        constexpr int kLoadPlanes = 3;
+#endif
+        mbar_arrive_expect_tx(&full[s], kLoadPlanes * ptile);
         uint8_t* Bp = smem + s * stage_bytes + a.mg * kPlaneTile;
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < kLoadPlanes; ++p)
           tma_load_2d(Bp + p * ptile, tm_di, &full[s], bb * args.T_pad + tq * 64,
                       p * a.N_pad + ntile * a.n_tile);
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == kWgProdWarps + 1) {
     const uint32_t idesc = idesc_bf16(128, a.n_tile, false, false);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
@@ -1163,7 +1182,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bp = A + a.mg * kPlaneTile;
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
+        for (int ks = 0; ks < (SNN_WG_EXP == 3 ? 0 : 4); ++ks) {
           for (int m = 0; m < nm; ++m) {
             const uint64_t ad = sdesc_sw128(A + m * kPlaneTile + ks * 32, 16, 1024);
 #pragma unroll
@@ -1179,19 +1198,20 @@ __global__ void __launch_bounds__(kWgThreads, 1)
       if (clk != nullptr) clk[3] = clock64();
     }
     __syncwarp();
-  } else if (warp < 4) {
-    // A producers: nm tiles [128 k-rows][64 time cols], K-major SW128; thread =
-    // row tid of every tile.  kind 0 decodes the bulk-copied dataset bytes from
-    // smem; kind 1 loads time-packed spike words (L2-resident) one stage ahead.
-    const int tid = threadIdx.x;
-    auto fetch = [&](int it, int m) -> uint64_t {
-      const int k = (mt0 + m) * 128 + tid;
-      if (a.kind == 0 || it >= total || m >= nm) return 0;
+  } else {
+    // A producers: nm tiles [128 k-rows][64 time cols], K-major SW128.  Thread p:
+    // row p % 128 of every tile, 16-byte chunks 4h..4h+3 (h = p / 128: 32 steps).
+    // kind 0 decodes the bulk-copied dataset bytes from smem; kind 1 loads the
+    // time-packed spike word (L2-resident) one stage ahead.
+    const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
+    auto fetch = [&](int it, int m) -> uint32_t {
+      const int k = (mt0 + m) * 128 + row;
+      if (a.kind == 0 || it >= total || m >= nm) return 0u;
       const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
-      return __ldg(reinterpret_cast<const unsigned long long*>(
-          a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) + size_t(bb) * (args.T_pad / 32) + tq * 2));
+      return __ldg(a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) +
+                   size_t(bb) * (args.T_pad / 32) + tq * 2 + h);
     };
-    uint64_t cur[kWgMgMax], nxt[kWgMgMax];
+    uint32_t cur[kWgMgMax], nxt[kWgMgMax];
 #pragma unroll
     for (int m = 0; m < kWgMgMax; ++m) cur[m] = fetch(0, m);
     for (int it = 0; it < total; ++it) {
@@ -1201,27 +1221,27 @@ __global__ void __launch_bounds__(kWgThreads, 1)
       mbar_wait(&empty[s], ph ^ 1);
       if (a.kind == 0) {
         mbar_wait(&xfull[s], ph);
-        const uint8_t* xs = xbuf + s * ((xbytes + 1023) & ~1023u);
+        const uint8_t* xs = xbuf + s * ((xbytes + 1023) & ~1023u) + 4 * h * args.x_row_stride;
 #pragma unroll
         for (int m = 0; m < kWgMgMax; ++m) {
           if (m >= nm) break;
-          const int k = (mt0 + m) * 128 + tid;
-          uint64_t v = 0;
+          const int k = (mt0 + m) * 128 + row;
+          uint32_t v = 0;
           if (k < args.x_row_stride) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v |= uint64_t(xs[j * args.x_row_stride + k]) << (8 * j);
+            for (int j = 0; j < 4; ++j) v |= uint32_t(xs[j * args.x_row_stride + k]) << (8 * j);
           }
           cur[m] = v;
         }
       }
       const uint32_t A = smem_u32(smem + s * stage_bytes);
 #pragma unroll
-      for (int m = 0; m < kWgMgMax; ++m) {
+      for (int m = 0; m < (SNN_WG_EXP == 1 ? 0 : kWgMgMax); ++m) {
         if (m >= nm) break;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t byte = uint32_t(cur[m] >> (8 * j)) & 0xFFu;
-          st_shared_v4(A + m * kPlaneTile + sw128_off(tid, j),
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t byte = (cur[m] >> (8 * j)) & 0xFFu;
+          st_shared_v4(A + m * kPlaneTile + sw128_off(row, 4 * h + j),
                        a.kind == 0 ? expand_bits_msb(byte) : expand_bits_lsb(byte));
         }
       }
@@ -1230,31 +1250,39 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
       for (int m = 0; m < kWgMgMax; ++m) cur[m] = nxt[m];
     }
-    // epilogue: TMEM -> smem (row per thread; chunk order rotated per row to
-    // spread banks) -> one 1-D bulk store per output row (coalesced, async)
+    // epilogue: TMEM -> smem (row per thread, rows padded by 16 bytes so the 8
+    // rows of a quarter-warp hit distinct banks) -> one 1-D bulk store per row.
+    // Warp w reads TMEM lanes 32 (w % 4)..; the two halves split the columns.
     mbar_wait(&acc_full[0], 0);
     tc_fence_after();
     if (clk != nullptr && threadIdx.x == 0) clk[4] = clock64();
     const uint32_t row_bytes = uint32_t(a.n_tile) * 4u;
+    const uint32_t row_stride = wg_epi_row_stride(a.n_tile);
+    const int nc = a.n_tile / 32, c0 = h * nc / 2, c1 = (h + 1) * nc / 2;
     for (int m = 0; m < nm; ++m) {
-      uint8_t* srow = smem + (size_t(m) * 128 + tid) * row_bytes;  // stages are free now
-      for (int c = 0; c < a.n_tile / 32; ++c) {
+      uint8_t* srow = smem + (size_t(m) * 128 + row) * row_stride;  // stages are free now
+      for (int c = c0; c < c1; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + m * a.n_tile + c * 32, r);
+        tmem_ld32(tmem + (uint32_t((warp & 3) * 32) << 16) + m * a.n_tile + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int j = (jj + tid) & 7;  // rotate the 16-byte chunk order per row
+        for (int j = 0; j < 8; ++j) {
           uint4 v4 = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
           if (total == 0) v4 = make_uint4(0u, 0u, 0u, 0u);
           *reinterpret_cast<uint4*>(srow + c * 128 + j * 16) = v4;
         }
       }
-      fence_async_smem();
-      const int k = (mt0 + m) * 128 + tid;
-      bulk_store(a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile, srow, row_bytes);
     }
-    bulk_commit_wait_all();
+    fence_async_smem();
+    asm volatile("bar.sync 1, %0;" ::"r"(kWgProd) : "memory");
+    if (h == 0) {
+      for (int m = 0; m < nm; ++m) {
+        const int k = (mt0 + m) * 128 + row;
+        bulk_store(a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile,
+                   smem + (size_t(m) * 128 + row) * row_stride, row_bytes);
+      }
+      bulk_commit_wait_all();
+    }
     tc_fence_before();
   }
   pdl_launch_dependents();
@@ -1477,14 +1505,18 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
 // the step counter first; the last block to finish (completion counter) advances
 // it and the schedule slot, so no block can observe the advanced value.
 __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, unsigned int* done,
-                                                     int64_t* rows_slot) {
+                                                     int64_t* rows_slot, long long* dbg_clk) {
   pdl_wait();
   const int tid = threadIdx.x;
+  if (dbg_clk != nullptr && tid == 0) dbg_clk[size_t(blockIdx.x) * kClkStride + 14] = globaltimer();
   const int64_t s = *reinterpret_cast<volatile const int64_t*>(r.step);  // this step's bias corrections: table entry s (optimize.hpp:95-97)
   const float bc1 = a.bc[2 * s], bc2 = a.bc[2 * s + 1];
+  // block 0: the serial batch-order loss sum (scheduled first, overlaps the rest);
+  // blocks [1, 1 + vb_blocks): beta / bias; then one thread per W element
   const int vb_blocks = (r.n_vec + 7) / 8;
-  if (int(blockIdx.x) < r.w_blocks) {
-    const int64_t i = int64_t(blockIdx.x) * 256 + tid;
+  const int wb0 = 1 + vb_blocks;
+  if (blockIdx.x >= unsigned(wb0)) {
+    const int64_t i = int64_t(blockIdx.x - wb0) * 256 + tid;
     if (i < r.n_params) {
       const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
       if (en.kind == kEntryW) {
@@ -1508,9 +1540,9 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
         refresh_planes(a, j, k, n, adam_one(a, i, g, bc1, bc2));
       }
     }
-  } else if (int(blockIdx.x) < r.w_blocks + vb_blocks) {
+  } else if (blockIdx.x >= 1u) {
     const int warp = tid >> 5, lane = tid & 31;
-    const int v = (int(blockIdx.x) - r.w_blocks) * 8 + warp;
+    const int v = (int(blockIdx.x) - 1) * 8 + warp;
     if (v < r.n_vec) {
       const int64_t i = r.vec_index[v];
       const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
@@ -1559,6 +1591,7 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
   }
   // completion: the last block advances the step (and schedule slot) counters
   __syncthreads();
+  if (dbg_clk != nullptr && tid == 0) dbg_clk[size_t(blockIdx.x) * kClkStride + 15] = globaltimer();
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(done, 1u) == gridDim.x - 1) {

@@ -166,9 +166,10 @@ def lib() -> C.CDLL:
         return _lib
     if needs_build():
         build()
-    if not os.path.exists(LIB):
-        raise DeviceError(f"{LIB} missing: the CUDA engine is required (no CPU fallback)")
-    L = C.CDLL(LIB, mode=C.RTLD_GLOBAL)
+    lib = os.environ.get("SNN_B200_LIB") or LIB  # A/B builds of the same sources
+    if not os.path.exists(lib):
+        raise DeviceError(f"{lib} missing: the CUDA engine is required (no CPU fallback)")
+    L = C.CDLL(lib, mode=C.RTLD_GLOBAL)
     L.snn_last_error.restype = C.c_char_p
     L.snn_last_error.argtypes = [C.c_void_p]
     L.snn_stream.restype = C.c_void_p
@@ -427,7 +428,7 @@ class Engine:
         idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5}[which]
         B, T = self.batch_size, self.time_steps
         if which == "clk":
-            out = np.empty((2 + 2 * len(self.desc["hidden"]), B * 4, 16), np.int64)
+            out = np.empty((3 + 2 * len(self.desc["hidden"]), B * 4, 16), np.int64)
         elif which == "trace":
             out = np.empty((B, T, self.desc["classes"]), np.float32)
         else:

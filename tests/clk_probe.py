@@ -9,7 +9,7 @@ eng.synth_dataset(16384, seed=1)
 eng.debug(True)
 rows = np.arange(256, dtype=np.uint32)
 for _ in range(3):
-    eng.forward_backward(rows)
+    eng.train_step(rows)
 clk = eng.fetch("clk")
 L = 2
 names = ["readout"] + [f"fwd{l}" for l in range(L)] + [f"bwd{l}" for l in range(L)]
@@ -42,8 +42,8 @@ print("  slow (> 1.5x median) CTA ids:", sorted(np.where(g > 1.5 * np.median(g))
 print("  smids of slow:", sorted(sm[g > 1.5 * np.median(g)].tolist()))
 
 # timeline of one replay (globaltimer slots 14/15), kernels in launch order
-order = [f"fwd{l}" for l in range(L)] + ["readout"] + [f"bwd{l}" for l in reversed(range(L))] + ["wgrad"]
-slot = {"readout": 0, "wgrad": 1 + 2 * L, **{f"fwd{l}": 1 + l for l in range(L)}, **{f"bwd{l}": 1 + L + l for l in range(L)}}
+order = [f"fwd{l}" for l in range(L)] + ["readout"] + [f"bwd{l}" for l in reversed(range(L))] + ["wgrad", "tail"]
+slot = {"readout": 0, "wgrad": 1 + 2 * L, "tail": 2 + 2 * L, **{f"fwd{l}": 1 + l for l in range(L)}, **{f"bwd{l}": 1 + L + l for l in range(L)}}
 t0 = None
 for name in order:
     c = clk[slot[name]]
