@@ -260,6 +260,8 @@ struct snn_engine {
   }
 
   int B_global() const { return B * world; }
+  // debug clock stamps: one region per kernel of the step, kClkStride per CTA
+  size_t clk_region() const { return std::max<size_t>(size_t(B) * 64, size_t(4096) * kClkStride); }
 
   // ---------------------------------------------------------------- setup
   void validate_and_size() {
@@ -307,8 +309,11 @@ struct snn_engine {
     // weight-gradient work split: each CTA owns mg M-tiles (shared dI stages, TMEM
     // mg*n_tile <= 512 columns) of one n-tile and a contiguous range of samples.
     // Pipeline depth per layer = what fits the smem budget (small stages -> more
-    // stages in flight).  Splits balance CTAs by modelled time: iterations x
-    // max(MMA cycles per iteration, load latency / stages).
+    // stages in flight).  Splits minimise the modelled finish time of the slowest
+    // CTA, fixed + iterations x per-iteration cycles, calibrated on B200 phase
+    // clocks (tests/clk_probe.py): fixed = prologue + first stage (~8K) + epilogue
+    // (f32 partial bytes at ~22 B/clk); per iteration = 600 + max(MMA issue,
+    // 600 per A tile decoded).  Binary search on the finish time tau.
     {
       int sms = 148;
       int dev_sms = 0;
@@ -319,7 +324,7 @@ struct snn_engine {
       const double xrun = double(wg_xrun_bytes(IN_pad));
       // mg cap: 2 stages of (mg A tiles + 3 B planes + dataset run) must fit
       wg_mg_max = std::max(1, std::min(kWgMgMax, int((budget / 2 - 3 * 128 * 128 - xrun) / kPlaneTile)));
-      double total_cost = 0, cost[kMaxLayers], units[kMaxLayers];
+      double fixed[kMaxLayers], per_unit[kMaxLayers], units[kMaxLayers];
       const double iters = double(B) * (T_pad / 64);
       for (int j = 0; j <= L; ++j) {
         const int m_tiles = M_pad_w[j] / 128, n_tiles = N_pad[j] / n_tile_w[j];
@@ -334,15 +339,25 @@ struct snn_engine {
         wg_stages_l[j] = std::max(1, std::min(std::min(kWgStagesMax, wg_stages_cap), int(budget / stage)));
         const int m_groups = (m_tiles + mg_w[j] - 1) / mg_w[j];
         units[j] = double(m_groups) * n_tiles;
-        const double mma = 12.0 * mg_w[j] * (n_tile_w[j] / 2.0);     // cycles per iteration
-        const double per_it = std::max(mma, 3000.0 / wg_stages_l[j]);  // latency floor
-        cost[j] = units[j] * iters * per_it;
-        total_cost += cost[j];
+        const double mma = 12.0 * mg_w[j] * (n_tile_w[j] / 2.0);  // tcgen05 issue cycles
+        const double per_it = 600.0 + std::max(mma, 600.0 * mg_w[j]);
+        fixed[j] = 8000.0 + mg_w[j] * n_tile_w[j] * 512.0 / 22.0;
+        per_unit[j] = iters * per_it;  // all samples through one CTA
       }
-      for (int j = 0; j <= L; ++j) {
-        const double share = double(sms) * cost[j] / total_cost;  // CTAs for layer j
-        splits_w[j] = std::max(1, std::min(B, int(share / units[j] + 0.5)));
+      auto splits_for = [&](double tau, int j) {
+        const double room = tau - fixed[j];
+        if (room <= 0) return B;
+        return std::max(1, std::min(B, int(std::ceil(per_unit[j] / room))));
+      };
+      double lo = 0, hi = 1e12;
+      for (int j = 0; j <= L; ++j) lo = std::max(lo, fixed[j]);
+      for (int rep = 0; rep < 100; ++rep) {
+        const double mid = 0.5 * (lo + hi);
+        double ctas = 0;
+        for (int j = 0; j <= L; ++j) ctas += units[j] * splits_for(mid, j);
+        if (ctas <= sms) hi = mid; else lo = mid;
       }
+      for (int j = 0; j <= L; ++j) splits_w[j] = splits_for(hi, j);
       if (const char* v = std::getenv("SNN_WG_SPLIT_SAMPLES"))
         for (int j = 0; j <= L; ++j) splits_w[j] = std::max(1, B / std::max(1, std::atoi(v)));
     }
@@ -655,7 +670,7 @@ struct snn_engine {
       f.s_np = s_np[l].p;
       f.s_tp = s_tp[l].p;
       f.dbg_i = debug ? dbg_i[l].p : nullptr;
-      f.dbg_clk = debug ? dbg_clk.p + size_t(1 + l) * B * 8 * 8 : nullptr;
+      f.dbg_clk = debug ? dbg_clk.p + size_t(1 + l) * clk_region() : nullptr;
       f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
       f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
       f.theta = net.threshold;
@@ -698,7 +713,7 @@ struct snn_engine {
       bw.dbeta_part = dbeta[l].p;
       bw.dbias_part = net.bias ? dbias[l].p : nullptr;
       bw.dbg_ds = debug ? dbg_ds[l].p : nullptr;
-      bw.dbg_clk = debug ? dbg_clk.p + size_t(1 + L + l) * B * 8 * 8 : nullptr;
+      bw.dbg_clk = debug ? dbg_clk.p + size_t(1 + L + l) * clk_region() : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
@@ -715,7 +730,7 @@ struct snn_engine {
       w.rows = rows_p;
       w.rows_slot = slot_p;
       w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
-      w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * B * 8 * 8 : nullptr;
+      w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * clk_region() : nullptr;
       int blocks = 0;
       for (int j = 0; j <= L; ++j) {
         WgradLayer& g = w.layer[j];
@@ -754,13 +769,13 @@ struct snn_engine {
       r.step = step.p;
       r.update = update;
       r.B = B;
-      r.w_blocks = int((n_params + 255) / 256);
+      r.w_blocks = int((n_params + kRedElemsPerBlock - 1) / kRedElemsPerBlock);
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
       if (update && world == 1) {
         // single rank: no allreduce between reduction and update -> one kernel
         AdamArgs a = adam_args(1);
-        long long* tclk = debug && size_t(blocks) <= size_t(B) * 64 / kClkStride
-                              ? dbg_clk.p + size_t(2 + 2 * L) * B * 8 * 8 : nullptr;
+        long long* tclk = debug && size_t(blocks) * kClkStride <= clk_region()
+                              ? dbg_clk.p + size_t(2 + 2 * L) * clk_region() : nullptr;
         launch(k_reduce_adam, dim3(blocks), dim3(256), 0, r, a, tail_done.p,
                sched_mode ? sched_slot.p : (int64_t*)nullptr, tclk);
         mark(evs, "reduce_adam", -1);
@@ -927,7 +942,7 @@ struct snn_engine {
     }
     if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
     // clock stamps: slot 0 readout [B][8], slots 1..L fwd, L+1..2L bwd ([B*8 ctas][8] each)
-    if (on) dbg_clk.alloc(size_t(3 + 2 * L) * B * 8 * 8); else dbg_clk.free();
+    if (on) dbg_clk.alloc(size_t(3 + 2 * L) * clk_region()); else dbg_clk.free();
     clear_graphs();
   }
 };
@@ -1288,7 +1303,7 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
     if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
     const int B = e->B, T = e->T, T_pad = e->T_pad;
     if (which == 5) {
-      const size_t need = size_t(3 + 2 * e->L) * B * 8 * 8 * sizeof(long long);
+      const size_t need = size_t(3 + 2 * e->L) * e->clk_region() * sizeof(long long);
       if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
       CK(cudaMemcpy(host, e->dbg_clk.p, need, cudaMemcpyDeviceToHost));
       return;

@@ -1339,35 +1339,51 @@ __device__ __forceinline__ int find_entry(const Entry* en, int n, int64_t i) {
   return e;
 }
 
-// Blocks [0, w_blocks): one thread per flat index, W entries only -- fixed-order
-// sum of the split-K partials.  Next blocks: one warp per beta/bias element --
+// W gradient element of the split-K partials, summed by a pair of lanes: lane q
+// sums splits [q*S/2, (q+1)*S/2) in order, then q0 + q1 -- a fixed order
+// (deterministic), twice the loads in flight of one thread per element while
+// the grid still fits one wave.  Both lanes of the pair must call it (they share
+// the element and every branch before the call); both return the total.
+__device__ __forceinline__ float sum_partials_pair(const ReduceArgs& r, const Entry& en, int64_t li,
+                                                   int q) {
+  const int j = en.layer;
+  const int64_t k = li / en.cols, n = li % en.cols;
+  const float* __restrict__ p = r.partial[j] + k * r.N_pad[j] + n;
+  const int64_t sstride = int64_t(r.M_pad[j]) * r.N_pad[j];
+  const int S = r.splits[j];
+  const int s0 = q * S / 2, s1 = (q + 1) * S / 2;
+  float g = 0.0f;
+  int s = s0;
+  for (; s + 8 <= s1; s += 8) {
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(p + (s + u) * sstride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) g = __fadd_rn(g, x[u]);
+  }
+  for (; s < s1; ++s) g = __fadd_rn(g, __ldg(p + s * sstride));
+  const unsigned pair = 0x3u << (threadIdx.x & 30);
+  const float g0 = __shfl_sync(pair, g, 0, 2);
+  const float g1 = __shfl_sync(pair, g, 1, 2);
+  return __fadd_rn(g0, g1);
+}
+constexpr int kRedElemsPerBlock = 128;  // W elements per 256-thread block (lane pairs)
+
+// Blocks [0, w_blocks): one pair of lanes per flat index, W entries only --
+// fixed-order sum of the split-K partials (sum_partials_pair).  Next blocks: one warp per beta/bias element --
 // lanes take strided samples, then a fixed-shape tree (deterministic).  Last
 // block: loss sum in batch order (objective.hpp:57-72) + hits, step counter.
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
   pdl_wait();
   const int tid = threadIdx.x;
   if (int(blockIdx.x) < a.w_blocks) {
-    const int64_t i = int64_t(blockIdx.x) * 256 + tid;
+    // pairs stay converged: out-of-range / non-W pairs skip as a whole
+    const int64_t i = int64_t(blockIdx.x) * kRedElemsPerBlock + (tid >> 1);
     if (i >= a.n_params) return;
     const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
     if (en.kind != kEntryW) return;
-    const int64_t li = i - en.offset;
-    const int j = en.layer;
-    const int64_t k = li / en.cols, n = li % en.cols;
-    const float* __restrict__ p = a.partial[j] + k * a.N_pad[j] + n;
-    const int64_t sstride = int64_t(a.M_pad[j]) * a.N_pad[j];
-    const int S = a.splits[j];
-    float g = 0.0f;
-    int s = 0;
-    for (; s + 8 <= S; s += 8) {
-      float x[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) x[q] = __ldg(p + (s + q) * sstride);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) g = __fadd_rn(g, x[q]);
-    }
-    for (; s < S; ++s) g = __fadd_rn(g, __ldg(p + s * sstride));
-    a.grads[i] = g;
+    const float g = sum_partials_pair(a, en, i - en.offset, tid & 1);
+    if ((tid & 1) == 0) a.grads[i] = g;
     return;
   }
   const int vb_blocks = (a.n_vec + 7) / 8;
@@ -1516,28 +1532,16 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
   const int vb_blocks = (r.n_vec + 7) / 8;
   const int wb0 = 1 + vb_blocks;
   if (blockIdx.x >= unsigned(wb0)) {
-    const int64_t i = int64_t(blockIdx.x - wb0) * 256 + tid;
+    const int64_t i = int64_t(blockIdx.x - wb0) * kRedElemsPerBlock + (tid >> 1);
     if (i < r.n_params) {
       const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
       if (en.kind == kEntryW) {
         const int64_t li = i - en.offset;
-        const int j = en.layer;
-        const int64_t k = li / en.cols, n = li % en.cols;
-        const float* __restrict__ p = r.partial[j] + k * r.N_pad[j] + n;
-        const int64_t sstride = int64_t(r.M_pad[j]) * r.N_pad[j];
-        const int S = r.splits[j];
-        float g = 0.0f;
-        int q0 = 0;
-        for (; q0 + 16 <= S; q0 += 16) {
-          float x[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) x[q] = __ldg(p + (q0 + q) * sstride);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) g = __fadd_rn(g, x[q]);
+        const float g = sum_partials_pair(r, en, li, tid & 1);
+        if ((tid & 1) == 0) {
+          r.grads[i] = g;
+          refresh_planes(a, en.layer, li / en.cols, li % en.cols, adam_one(a, i, g, bc1, bc2));
         }
-        for (; q0 < S; ++q0) g = __fadd_rn(g, __ldg(p + q0 * sstride));
-        r.grads[i] = g;
-        refresh_planes(a, j, k, n, adam_one(a, i, g, bc1, bc2));
       }
     }
   } else if (blockIdx.x >= 1u) {
