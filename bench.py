@@ -124,7 +124,7 @@ def algorithmic(name: str, w: dict, n_params: int):
         return "hbm", 12.0 * B * T * dims[l + 1]
     if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element
         return "hbm", 8.0 * B * T * C
-    if base == "adam":               # 28 B / param
+    if base in ("adam", "reduce_adam"):  # Adam: 28 B / param (split-K sums are overhead)
         return "hbm", 28.0 * n_params
     return "hbm", 0.0
 

@@ -634,7 +634,7 @@ struct snn_engine {
 
   // ---------------------------------------------------------------- step
   // L fwd + readout + L bwd + wgrad + tail (fused reduce+Adam on one rank; reduce, adam otherwise)
-  int launches_per_step() const { return 2 * L + (world == 1 ? 4 : 5); }
+  int launches_per_step() const { return 2 * L + (world == 1 ? 3 : 4); }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;

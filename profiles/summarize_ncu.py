@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 NAMES = {"k_lif_fwd": "lif_fwd", "k_readout": "readout", "k_lif_bwd": "lif_bwd",
-         "k_wgrad": "wgrad", "k_reduce": "reduce", "k_adam": "adam"}
+         "k_wgrad": "wgrad", "k_reduce_adam": "reduce_adam", "k_reduce": "reduce", "k_adam": "adam"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6}
 
 
@@ -32,11 +32,12 @@ def main(rep, tag):
     out = {"report": rep, "kernels": [], "dram_bytes_per_launch": {}}
     counters = {}
     for r in rows[2:]:
-        kname = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+        kname = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0]
+        kname = kname.replace("void ", "").strip()
         base = NAMES.get(kname, kname)
         idx = counters.get(base, 0)
         counters[base] = idx + 1
-        name = base if base in ("readout", "wgrad", "reduce", "adam") else f"{base}[{idx}]"
+        name = base if base in ("readout", "wgrad", "reduce", "adam", "reduce_adam") else f"{base}[{idx}]"
         dur, du = val(r, "gpu__time_duration.sum")
         rd, ru = val(r, "dram__bytes_read.sum")
         wr, wu = val(r, "dram__bytes_write.sum")
@@ -62,6 +63,12 @@ def main(rep, tag):
                 ent[k] = val(r, k)[0]
         out["kernels"].append(ent)
         out["dram_bytes_per_launch"][name] = dram
+    # backward launches run top-down: the first lif_bwd launch is the last hidden layer
+    nb = counters.get("lif_bwd", 0)
+    for k in out["kernels"]:
+        if k["name"].startswith("lif_bwd["):
+            k["name"] = f"lif_bwd[{nb - 1 - int(k['name'][8:-1])}]"
+    out["dram_bytes_per_launch"] = {k["name"]: k["dram_bytes"] for k in out["kernels"]}
     json.dump(out, open(f"profiles/{tag}_ncu.json", "w"), indent=1)
     for k in out["kernels"]:
         tp = k.get("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")

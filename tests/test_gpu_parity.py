@@ -278,3 +278,14 @@ def test_schedule_steps_match_train_step(orc):
     m2, v2, s2 = ref.get_opt_state()
     assert s1 == s2 == len(order)
     assert np.array_equal(m1, m2) and np.array_equal(v1, v2)
+
+
+def test_launch_count_matches_captured_step(orc):
+    """bench.py's gpu_launches claim: launches_per_step == kernels in one captured step."""
+    net = Net(inp=30, hidden=(16, 12, 8), classes=5)
+    x, y = orc.synth_raster(5, 8, 19, 30, 2)
+    eng = make_engine(net, 4, 19)
+    eng.stage_dataset(orc.pack_time(x), y)
+    names = [n for n, _ in eng.profile(1)]
+    assert len(names) == eng.launches_per_step, names
+    assert names[-1] == "reduce_adam"
