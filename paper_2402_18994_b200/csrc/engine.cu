@@ -213,6 +213,7 @@ struct snn_engine {
   size_t sched_steps = 0;
   // tensor maps
   CUtensorMap tm_wt[kMaxLayers], tm_wb[kMaxLayers], tm_di_k[kMaxLayers], tm_di_w[kMaxLayers];
+  CUtensorMap tm_di_out[kMaxLayers];  // hidden dI planes, 128-row boxes (K3 TMA stores)
   WgradMaps wg_maps;
   // debug
   bool debug = false;
@@ -425,6 +426,7 @@ struct snn_engine {
     for (int j = 0; j <= L; ++j) {
       tm_di_k[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 64);
       tm_di_w[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, uint32_t(n_tile_w[j]));
+      if (j < L) tm_di_out[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 128);
       wg_maps.m[j] = tm_di_w[j];
     }
     CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -622,13 +624,13 @@ struct snn_engine {
   }
 
   void launch_bwd(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
-                  const BwdArgs& bw) {
+                  const CUtensorMap& to, const BwdArgs& bw) {
     switch (act) {
-      case 1: launch(k_lif_bwd<1>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
-      case 2: launch(k_lif_bwd<2>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
-      case 3: launch(k_lif_bwd<3>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
-      case 4: launch(k_lif_bwd<4>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
-      default: launch(k_lif_bwd<0>, grid, dim3(kBwdThreads), smem, tw, td, bw); break;
+      case 1: launch(k_lif_bwd<1>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 2: launch(k_lif_bwd<2>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 3: launch(k_lif_bwd<3>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 4: launch(k_lif_bwd<4>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      default: launch(k_lif_bwd<0>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
     }
   }
 
@@ -719,7 +721,7 @@ struct snn_engine {
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
       launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages),
-                 tm_wb[l + 1], tm_di_k[l + 1], bw);
+                 tm_wb[l + 1], tm_di_k[l + 1], tm_di_out[l], bw);
       mark(evs, "lif_bwd", l);
     }
     // weight gradients: one launch over every Linear layer (split-K partials)

@@ -790,6 +790,9 @@ __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float 
   }
 }
 
+#ifndef SNN_BWD_EXP
+#define SNN_BWD_EXP 0  // timing experiments only (tests/clk_probe.py): 1 = skip the dI plane stores
+#endif
 constexpr int kBwdSeg = 2;                        // time segments per t-tile
 constexpr int kBwdScanThreads = 128 * kBwdSeg;
 constexpr int kBwdThreads = kBwdScanThreads + 32;  // + control warp (lane 0 TMA, lane 1 MMA)
@@ -803,7 +806,7 @@ __host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
 template <int kAct>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
-              BwdArgs a) {
+              const __grid_constant__ CUtensorMap tm_out, BwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int S = a.stages;
@@ -919,6 +922,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     __nv_bfloat16* __restrict__ drow = a.di_planes + size_t(n) * cols_total + size_t(b) * a.T_pad;
     const float* __restrict__ vrow = a.v_in + size_t(b) * a.T_pad * a.H_pad + n;
     const int seg_len = a.TT / kBwdSeg;  // multiple of 16
+    // one t-tile: dI planes are staged in the (then idle) operand stages in the
+    // SW128 layout of tm_out -- [plane][64-step half][128 rows][128 B] -- and
+    // written by 6 TMA stores (long rows instead of 32-byte pieces of 128 rows)
+    const bool stage_out = a.NT == 1;
     float Gcarry = 0.0f, db = 0.0f, dbias = 0.0f;
     for (int j = 0; j < a.NT; ++j) {
       const int tt = a.NT - 1 - j, buf = j % nbuf;
@@ -981,6 +988,24 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         uint32_t ph_[8], pm_[8], pl_[8];
 #pragma unroll
         for (int e = 0; e < 16; e += 2) split3_pack(x[e], x[e + 1], ph_[e / 2], pm_[e / 2], pl_[e / 2]);
+#if SNN_BWD_EXP == 1
+        if (ph_[0] == 0x12345u && pm_[1] == 0x777u) {  // timing experiment: stores never taken
+#else
+        if (stage_out) {
+          const int tl = sg * seg_len + c0;  // step within the tile (multiple of 16)
+          const uint32_t row = uint32_t(q * 32 + lane);
+          const uint32_t base = smem_u32(smem) + uint32_t(tl >> 6) * 16384u + row * 128u;
+          const uint32_t j0 = uint32_t(tl & 63) >> 3;
+          const uint32_t o0 = ((j0 ^ (row & 7u)) << 4), o1 = (((j0 + 1u) ^ (row & 7u)) << 4);
+          const uint32_t pstride = uint32_t(a.TT / 64) * 16384u;
+          st_shared_v4(base + o0, make_uint4(ph_[0], ph_[1], ph_[2], ph_[3]));
+          st_shared_v4(base + o1, make_uint4(ph_[4], ph_[5], ph_[6], ph_[7]));
+          st_shared_v4(base + pstride + o0, make_uint4(pm_[0], pm_[1], pm_[2], pm_[3]));
+          st_shared_v4(base + pstride + o1, make_uint4(pm_[4], pm_[5], pm_[6], pm_[7]));
+          st_shared_v4(base + 2 * pstride + o0, make_uint4(pl_[0], pl_[1], pl_[2], pl_[3]));
+          st_shared_v4(base + 2 * pstride + o1, make_uint4(pl_[4], pl_[5], pl_[6], pl_[7]));
+        } else {
+#endif
         uint4* dh = reinterpret_cast<uint4*>(drow + t_lo + c0);
         uint4* dm = reinterpret_cast<uint4*>(drow + plane + t_lo + c0);
         uint4* dl = reinterpret_cast<uint4*>(drow + 2 * plane + t_lo + c0);
@@ -990,14 +1015,23 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         dm[1] = make_uint4(pm_[4], pm_[5], pm_[6], pm_[7]);
         dl[0] = make_uint4(pl_[0], pl_[1], pl_[2], pl_[3]);
         dl[1] = make_uint4(pl_[4], pl_[5], pl_[6], pl_[7]);
+        }
       }
       if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[4] = clock64();
       // the earliest segment's final G carries into the previous t-tile
       if (sg == 0) xG[(kBwdSeg - 1) * 128 + q * 32 + lane] = G;
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
+      if (stage_out) fence_async_smem();  // staged planes -> visible to the TMA stores
       asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
       Gcarry = xG[(kBwdSeg - 1) * 128 + q * 32 + lane];
+      if (stage_out && threadIdx.x == 0) {
+        for (int p = 0; p < 3; ++p)
+          for (int h = 0; h < a.TT / 64; ++h)
+            tma_store_2d(&tm_out, smem + (p * (a.TT / 64) + h) * 16384, b * a.T_pad + h * 64,
+                         p * a.H_pad + nt * 128);
+        bulk_commit();
+      }
     }
     if (clk != nullptr && threadIdx.x == 0) clk[5] = clock64();
     // combine the per-segment dbeta / dbias partials in a fixed order
@@ -1018,6 +1052,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     }
   }
   pdl_launch_dependents();
+  if (threadIdx.x == 0) bulk_wait_read_all();  // staged planes read before smem is released
   __syncthreads();
   if (clk != nullptr && threadIdx.x == 0) {
     clk[6] = clock64();
