@@ -262,7 +262,7 @@ struct snn_engine {
 
   int B_global() const { return B * world; }
   // debug clock stamps: one region per kernel of the step, kClkStride per CTA
-  size_t clk_region() const { return std::max<size_t>(size_t(B) * 64, size_t(4096) * kClkStride); }
+  size_t clk_region() const { return size_t(std::max(4096, 4 * B)) * kClkStride; }
 
   // ---------------------------------------------------------------- setup
   void validate_and_size() {

@@ -33,7 +33,7 @@ using namespace sm100;
 constexpr int kMaxClasses = 32;
 constexpr int kMaxLayers = 9;  // Linear layers (hidden + readout)
 // debug phase-timestamp record per CTA; [14]/[15] = globaltimer start/end
-constexpr int kClkStride = 16;
+constexpr int kClkStride = 48;  // [16, 48): per-k-block stamps (forward MMA thread)
 
 // The step's dataset rows: a fixed [B] buffer, or (schedule mode) slot *slot of
 // a device-resident schedule [steps][B] whose slot counter the step tail advances.
@@ -72,13 +72,14 @@ __device__ __forceinline__ float surrogate(int act, float k, float aux, float x)
 
 // 8 bytes each 0/1 (byte e = element e) -> 8 bf16 {0,1} packed into 4 u32.
 __device__ __forceinline__ uint4 expand_bytes01(uint64_t m) {
+  // bytes are 0/1: x0xFF -> 0x00/0xFF masks (no carries), PRMT duplicates each
+  // mask byte into a bf16 half, AND applies 1.0 = 0x3F80
+  const uint32_t ml = uint32_t(m) * 0xFFu, mh = uint32_t(m >> 32) * 0xFFu;
   uint4 r;
-  uint32_t w[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    w[i] = (uint32_t((m >> (16 * i)) & 1u) * 0x3F80u) |
-           (uint32_t((m >> (16 * i + 8)) & 1u) * 0x3F800000u);
-  r.x = w[0]; r.y = w[1]; r.z = w[2]; r.w = w[3];
+  r.x = __byte_perm(ml, 0u, 0x1100u) & 0x3F803F80u;
+  r.y = __byte_perm(ml, 0u, 0x3322u) & 0x3F803F80u;
+  r.z = __byte_perm(mh, 0u, 0x1100u) & 0x3F803F80u;
+  r.w = __byte_perm(mh, 0u, 0x3322u) & 0x3F803F80u;
   return r;
 }
 // 8 bits (bit e = element e) -> 8 bf16 (0 or 1.0).  The multiply spreads bit i
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tc_fence_after();
         }
         mbar_wait(&full[s], ph);
+        if (clk != nullptr && it < 32) clk[16 + it] = clock64();
         tc_fence_after();
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bt = A + 3 * kPlaneTile;

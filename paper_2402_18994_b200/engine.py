@@ -428,7 +428,7 @@ class Engine:
         idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5}[which]
         B, T = self.batch_size, self.time_steps
         if which == "clk":
-            out = np.empty((3 + 2 * len(self.desc["hidden"]), max(B * 4, 4096), 16), np.int64)
+            out = np.empty((3 + 2 * len(self.desc["hidden"]), max(B * 4, 4096), 48), np.int64)
         elif which == "trace":
             out = np.empty((B, T, self.desc["classes"]), np.float32)
         else:

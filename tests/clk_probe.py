@@ -4,10 +4,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
-eng = Engine(shd_spec(), TrainConfig(batch_size=256, seed=0), 128)
+BATCH = int(os.environ.get("PROBE_B", "256"))
+eng = Engine(shd_spec(), TrainConfig(batch_size=BATCH, seed=0), 128)
 eng.synth_dataset(16384, seed=1)
 eng.debug(True)
-rows = np.arange(256, dtype=np.uint32)
+rows = np.arange(BATCH, dtype=np.uint32)
 for _ in range(3):
     eng.train_step(rows)
 clk = eng.fetch("clk")
@@ -51,3 +52,8 @@ for name in order:
     st, en = c[v, 14], c[v, 15]
     if t0 is None: t0 = st.min()
     print(f"TL {name:8s} ctas {v.sum():4d} start {(st.min()-t0)/1e3:7.1f} .. {(st.max()-t0)/1e3:7.1f}  end {(en.min()-t0)/1e3:7.1f} .. {(en.max()-t0)/1e3:7.1f} us  span {(en.max()-st.min())/1e3:6.1f}  cta med {np.median(en-st)/1e3:5.1f}")
+
+# forward layer-0 per-k-block stage readiness (MMA thread), cycles from CTA start
+c = clk[1][:max(1, BATCH // 2)]
+for blk in sorted({0, min(64, BATCH // 2 - 1)}):
+    print(f"fwd0 cta {blk}: kblock ready", (c[blk, 16:16 + 11] - c[blk, 0]).tolist(), " scan start", int(c[blk, 1] - c[blk, 0]))
