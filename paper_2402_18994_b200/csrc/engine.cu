@@ -191,7 +191,9 @@ struct snn_engine {
   DevBuf<int64_t> sched_slot;          // schedule mode: slot of the next step (device counter)
   DevBuf<unsigned int> tail_done;      // completion counter of k_reduce_adam
   size_t slot_expected = ~size_t(0);   // host mirror of *sched_slot
-  DevBuf<__nv_bfloat16> wt[kMaxLayers], wb[kMaxLayers];
+  // bf16 operand planes of every Linear W [3][K_pad][N_pad] (hi/mid/lo split of the
+  // f32 master): MN-major A of the forward GEMM, K-major A of the backward dS GEMM
+  DevBuf<__nv_bfloat16> wb[kMaxLayers];
   // activations
   DevBuf<float> V[SNN_MAX_HIDDEN];
   DevBuf<uint32_t> s_np[SNN_MAX_HIDDEN], s_tp[SNN_MAX_HIDDEN];
@@ -393,9 +395,8 @@ struct snn_engine {
     tail_done.alloc(1);
     grow_bc(1 << 20);
     for (int j = 0; j < L; ++j) {
-      wt[j].alloc(size_t(3) * N_pad[j] * K_pad[j]);
     }
-    for (int j = 1; j <= L; ++j) wb[j].alloc(size_t(3) * K_pad[j] * N_pad[j]);
+    for (int j = 0; j <= L; ++j) wb[j].alloc(size_t(3) * K_pad[j] * N_pad[j]);
     const size_t rows = size_t(B) * T_pad;
     for (int l = 0; l < L; ++l) {
       V[l].alloc(rows * H_pad[l], false);
@@ -418,7 +419,7 @@ struct snn_engine {
     CK(cudaMallocHost(&h_rows, sizeof(uint32_t) * B));
     // tensor maps
     for (int j = 0; j < L; ++j) {
-      tm_wt[j] = make_map(wt[j].p, uint64_t(3) * N_pad[j], K_pad[j], 128);
+      tm_wt[j] = make_map(wb[j].p, uint64_t(3) * K_pad[j], N_pad[j], 64);  // 64x64 MN-major boxes
     }
     for (int j = 1; j <= L; ++j) tm_wb[j] = make_map(wb[j].p, uint64_t(3) * K_pad[j], N_pad[j], 128);
     // dI planes [3][N_pad][B*T_pad]: MN-major boxes for the backward GEMM, K-major
@@ -514,8 +515,7 @@ struct snn_engine {
     fill_entries(a.entries, &a.n_entries);
     a.n_params = int64_t(n_params);
     for (int j = 0; j <= L; ++j) {
-      a.planes[j].wt = j < L ? wt[j].p : nullptr;
-      a.planes[j].wb = j >= 1 ? wb[j].p : nullptr;
+      a.planes[j].wb = wb[j].p;
       a.planes[j].K_pad = K_pad[j];
       a.planes[j].N_pad = N_pad[j];
     }

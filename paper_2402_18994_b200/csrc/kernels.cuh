@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int dec_warp0 = kFwdScanWarps, tma_warp = kFwdScanWarps + 4, mma_warp = tma_warp + 1;
 
   if (warp == tma_warp) {
-    // ---------------- TMA producer: the three W^T planes of each k-block
+    // ---------------- TMA producer: the three W planes of each k-block
     if (elect_one()) {
       tma_prefetch(&tm_w);
       const uint32_t* rows = batch_rows(a.rows, a.rows_slot, a.B);
@@ -334,14 +334,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile);
         uint8_t* A = smem + s * stage_bytes;
+        // W planes [3][K_pad][H_pad] read MN-major: per plane two 64-neuron x 64-k boxes
         for (int p = 0; p < 3; ++p)
-          tma_load_2d(A + p * kPlaneTile, &tm_w, &full[s], kb * 64, p * a.H_pad + nt * 128);
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(A + p * kPlaneTile + h * 8192, &tm_w, &full[s], nt * 128 + h * 64,
+                        p * a.K_pad + kb * 64);
       }
     }
     __syncwarp();
   } else if (warp == mma_warp) {
-    // ---------------- MMA issuer (one thread), N = SPB*TT stacked sample rows
-    const uint32_t idesc = idesc_bf16(128, NTOT, false, false);
+    // ---------------- MMA issuer (one thread), N = SPB*TT stacked sample rows;
+    // A (W^T) MN-major: LBO = 8 KB between the 64-neuron halves, 16 k-rows per step
+    const uint32_t idesc = idesc_bf16(128, NTOT, true, false);
     if (elect_one()) {
       for (int it = 0; it < total; ++it) {
         const int s = it % S, ph = (it / S) & 1;
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
 #pragma unroll
           for (int p = 2; p >= 0; --p) {
-            const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 32, 16, 1024);
+            const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 2048, 8192, 1024);
             umma_bf16(d, ad, bd, idesc, (kb | ks | (2 - p)) != 0);
           }
         }
@@ -1391,12 +1395,20 @@ __device__ __forceinline__ float sum_partials_pair(const ReduceArgs& r, const En
   const int s0 = q * S / 2, s1 = (q + 1) * S / 2;
   float g = 0.0f;
   int s = s0;
-  for (; s + 8 <= s1; s += 8) {
+  for (; s + 16 <= s1; s += 16) {
+    float x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = __ldg(p + (s + u) * sstride);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) g = __fadd_rn(g, x[u]);
+  }
+  if (s + 8 <= s1) {
     float x[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = __ldg(p + (s + u) * sstride);
 #pragma unroll
     for (int u = 0; u < 8; ++u) g = __fadd_rn(g, x[u]);
+    s += 8;
   }
   for (; s < s1; ++s) g = __fadd_rn(g, __ldg(p + s * sstride));
   const unsigned pair = 0x3u << (threadIdx.x & 30);
@@ -1473,8 +1485,7 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
 }
 
 struct PlaneTarget {
-  __nv_bfloat16* wt;  // forward A planes [3][N_pad][K_pad] or nullptr
-  __nv_bfloat16* wb;  // backward A planes [3][K_pad][N_pad] or nullptr
+  __nv_bfloat16* wb;  // operand planes [3][K_pad][N_pad] (forward MN-major A, backward K-major A)
   int K_pad, N_pad;
 };
 
@@ -1498,10 +1509,12 @@ struct AdamArgs {
 };
 
 // Adam on one flat parameter (optimize.hpp:88-110); bias corrections of step s+1.
-__device__ __forceinline__ float adam_one(const AdamArgs& a, int64_t i, float g, float bc1, float bc2) {
-  float p = a.params[i];
-  const float m = __fadd_rn(__fmul_rn(a.b1, a.m[i]), __fmul_rn(a.omb1, g));
-  const float v = __fadd_rn(__fmul_rn(a.b2, a.v[i]), __fmul_rn(__fmul_rn(a.omb2, g), g));
+// p0 / m0 / v0: the current parameter and moments (loaded by the caller, early).
+__device__ __forceinline__ float adam_apply(const AdamArgs& a, int64_t i, float g, float p0, float m0,
+                                            float v0, float bc1, float bc2) {
+  float p = p0;
+  const float m = __fadd_rn(__fmul_rn(a.b1, m0), __fmul_rn(a.omb1, g));
+  const float v = __fadd_rn(__fmul_rn(a.b2, v0), __fmul_rn(__fmul_rn(a.omb2, g), g));
   const float mhat = __fdiv_rn(m, bc1);
   const float vhat = __fdiv_rn(v, bc2);
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
@@ -1510,25 +1523,21 @@ __device__ __forceinline__ float adam_one(const AdamArgs& a, int64_t i, float g,
   a.params[i] = p;
   return p;
 }
+__device__ __forceinline__ float adam_one(const AdamArgs& a, int64_t i, float g, float bc1, float bc2) {
+  return adam_apply(a, i, g, a.params[i], a.m[i], a.v[i], bc1, bc2);
+}
 
-// bf16 operand planes of W element (k, n) of Linear `layer` from its f32 master.
+// bf16 operand planes of W element (k, n) of Linear `layer` from its f32 master
+// (consecutive n -> consecutive addresses: coalesced).
 __device__ __forceinline__ void refresh_planes(const AdamArgs& a, int layer, int64_t k, int64_t n, float p) {
   const PlaneTarget pt = a.planes[layer];
-  if (pt.wt == nullptr && pt.wb == nullptr) return;
+  if (pt.wb == nullptr) return;
   __nv_bfloat16 h, mi, lo;
   split3(p, h, mi, lo);
-  if (pt.wt != nullptr) {
-    const int64_t plane = int64_t(pt.N_pad) * pt.K_pad, idx = n * pt.K_pad + k;
-    pt.wt[idx] = h;
-    pt.wt[plane + idx] = mi;
-    pt.wt[2 * plane + idx] = lo;
-  }
-  if (pt.wb != nullptr) {
-    const int64_t plane = int64_t(pt.K_pad) * pt.N_pad, idx = k * pt.N_pad + n;
-    pt.wb[idx] = h;
-    pt.wb[plane + idx] = mi;
-    pt.wb[2 * plane + idx] = lo;
-  }
+  const int64_t plane = int64_t(pt.K_pad) * pt.N_pad, idx = k * pt.N_pad + n;
+  pt.wb[idx] = h;
+  pt.wb[plane + idx] = mi;
+  pt.wb[2 * plane + idx] = lo;
 }
 
 __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
@@ -1574,10 +1583,17 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
       const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
       if (en.kind == kEntryW) {
         const int64_t li = i - en.offset;
+        // Adam's operands are independent of the sum: issue them first
+        float p0 = 0.0f, m0 = 0.0f, v0 = 0.0f;
+        if ((tid & 1) == 0) {
+          p0 = a.params[i];
+          m0 = a.m[i];
+          v0 = a.v[i];
+        }
         const float g = sum_partials_pair(r, en, li, tid & 1);
         if ((tid & 1) == 0) {
           r.grads[i] = g;
-          refresh_planes(a, en.layer, li / en.cols, li % en.cols, adam_one(a, i, g, bc1, bc2));
+          refresh_planes(a, en.layer, li / en.cols, li % en.cols, adam_apply(a, i, g, p0, m0, v0, bc1, bc2));
         }
       }
     }
