@@ -755,6 +755,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void load_v16(const float* __restrict__ p, int hpad, int nval,
                                          float (&v)[16]) {
 #pragma unroll
@@ -837,7 +850,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   }
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
-  const uint32_t tmem_cols = acc_cols(a.TT, a.NT);
+  // one t-tile: TT more columns cache the membranes V between the two scan passes
+  const bool vcache = a.NT == 1;
+  const uint32_t tmem_cols = vcache ? acc_cols(2 * a.TT, 1) : acc_cols(a.TT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
 
   if (threadIdx.x == 0) {
@@ -851,11 +866,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     }
     fence_barrier_init();
   }
-  if (warp == 0) {
-    if (tmem_cols == 256) tmem_alloc<256>(tmem_slot);
-    else if (tmem_cols == 128) tmem_alloc<128>(tmem_slot);
-    else tmem_alloc<64>(tmem_slot);
-  }
+  if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -946,15 +957,17 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       float A = 1.0f, Bc = 0.0f;
       const float* vseg = vrow + size_t(t_lo) * a.H_pad;
       const int top = seg_len - 16;
+      const uint32_t vcol = tmem + (uint32_t(q * 32) << 16) + a.TT + sg * seg_len;  // V cache
       float vr[16], vn[16];
       load_v16(vseg + size_t(top) * a.H_pad, a.H_pad, t_hi - (t_lo + top), vn);
       for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
 #pragma unroll
         for (int e = 0; e < 16; ++e) vr[e] = vn[e];
-        // next: c0 - 16, or (end of pass 1) the top sub-chunk again for pass 3
+        // next: c0 - 16, or (end of pass 1, no V cache) the top sub-chunk for pass 3
         const int cn = c0 >= 16 ? c0 - 16 : top;
-        load_v16(vseg + size_t(cn) * a.H_pad, a.H_pad, t_hi - (t_lo + cn), vn);
+        if (c0 >= 16 || !vcache) load_v16(vseg + size_t(cn) * a.H_pad, a.H_pad, t_hi - (t_lo + cn), vn);
+        if (vcache) tmem_st16(vcol + c0, vr);
         if (nval <= 0) continue;
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
@@ -962,6 +975,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         if (nval >= 16) bwd_compose<kAct, false>(r, vr, 16, vb, theta, a, A, Bc);
         else bwd_compose<kAct, true>(r, vr, nval, vb, theta, a, A, Bc);
       }
+      if (vcache) tmem_st_wait();
       xA[sidx] = A;
       xB[sidx] = Bc;
       if (sg == kBwdSeg - 1) xG[sidx] = Gcarry;
@@ -975,13 +989,23 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       // ---- pass 3: exact-order replay of my segment
       for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) vr[e] = vn[e];
-        if (c0 >= 16) load_v16(vseg + size_t(c0 - 16) * a.H_pad, a.H_pad, t_hi - (t_lo + c0 - 16), vn);
-        if (nval <= 0) continue;
         uint32_t r[16];
-        tmem_ld16(tcol + c0, r);
-        tmem_ld_wait();
+        if (vcache) {
+          if (nval <= 0) continue;
+          uint32_t vv[16];
+          tmem_ld16(vcol + c0, vv);
+          tmem_ld16(tcol + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) vr[e] = __uint_as_float(vv[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) vr[e] = vn[e];
+          if (c0 >= 16) load_v16(vseg + size_t(c0 - 16) * a.H_pad, a.H_pad, t_hi - (t_lo + c0 - 16), vn);
+          if (nval <= 0) continue;
+          tmem_ld16(tcol + c0, r);
+          tmem_ld_wait();
+        }
         if (a.dbg_ds != nullptr) {
 #pragma unroll
           for (int e = 0; e < 16; ++e)
@@ -1066,9 +1090,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   }
   if (warp == 0) {
     tc_fence_after();
-    if (tmem_cols == 256) tmem_dealloc<256>(tmem);
-    else if (tmem_cols == 128) tmem_dealloc<128>(tmem);
-    else tmem_dealloc<64>(tmem);
+    tmem_dealloc_any(tmem_cols, tmem);
   }
 }
 
