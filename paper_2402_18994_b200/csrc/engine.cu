@@ -231,6 +231,7 @@ struct snn_engine {
   // pipeline depths (smem per CTA decides how many CTAs share an SM)
   int fwd_stages = std::min(kFwdStagesMax, env_int("SNN_FWD_STAGES", 2));
   int fwd_spb_env = env_int("SNN_FWD_SPB", 2);
+  int fwd_fuse = env_int("SNN_FWD_FUSE", 2) - 1;  // 1: one launch per hidden layer
   // samples per forward CTA: N = spb * TT <= 256 and TMEM (doubled for NT > 1) <= 512
   int fwd_spb(int tt) const { return std::max(1, std::min(fwd_spb_env, std::min(kFwdSpbMax, 256 / tt))); }
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
@@ -635,8 +636,23 @@ struct snn_engine {
   }
 
   // ---------------------------------------------------------------- step
-  // L fwd + readout + L bwd + wgrad + tail (fused reduce+Adam on one rank; reduce, adam otherwise)
-  int launches_per_step() const { return 2 * L + (world == 1 ? 3 : 4); }
+  // Forward launch groups (first layer, layer count): consecutive hidden layers run
+  // in one launch when each fits one 128-neuron tile and the step one t-tile --
+  // the next layer's GEMM then consumes the spikes straight from shared memory.
+  std::vector<std::pair<int, int>> fwd_groups() const {
+    std::vector<std::pair<int, int>> g;
+    for (int l = 0; l < L;) {
+      int nl = 1;
+      if (fwd_fuse && NT == 1 && H_pad[l] == 128 && K_pad[l] >= 128 && fwd_stages >= 2)
+        while (l + nl < L && nl < kFwdFuseMax && H_pad[l + nl] == 128 && K_pad[l + nl] == 128) ++nl;
+      g.emplace_back(l, nl);
+      l += nl;
+    }
+    return g;
+  }
+  // forward groups + readout + L bwd + wgrad + tail (fused reduce+Adam on one rank;
+  // reduce, adam otherwise)
+  int launches_per_step() const { return int(fwd_groups().size()) + L + (world == 1 ? 3 : 4); }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;
@@ -659,27 +675,35 @@ struct snn_engine {
     const uint32_t* rows_p = sched_mode ? sched.p : rows_cur.p;
     const int64_t* slot_p = sched_mode ? sched_slot.p : nullptr;
     if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
-    // forward
-    for (int l = 0; l < L; ++l) {
+    // forward: one launch per group of consecutive hidden layers (fwd_groups)
+    for (const auto& grp : fwd_groups()) {
+      const int l = grp.first, nl = grp.second;
       FwdArgs f{};
+      FwdMaps fm{};
       f.x = ds.x.p;
       f.rows = rows_p;
       f.rows_slot = slot_p;
       f.s_in = l > 0 ? s_np[l - 1].p : nullptr;
-      f.beta = params.p + entry_of(kEntryBeta, l).offset;
-      f.bias = net.bias ? params.p + entry_of(kEntryB, l).offset : nullptr;
-      f.v_out = V[l].p;
-      f.s_np = s_np[l].p;
-      f.s_tp = s_tp[l].p;
-      f.dbg_i = debug ? dbg_i[l].p : nullptr;
+      for (int i = 0; i < nl; ++i) {
+        FwdLayer& ly = f.lay[i];
+        ly.beta = params.p + entry_of(kEntryBeta, l + i).offset;
+        ly.bias = net.bias ? params.p + entry_of(kEntryB, l + i).offset : nullptr;
+        ly.v_out = V[l + i].p;
+        ly.s_np = s_np[l + i].p;
+        ly.s_tp = s_tp[l + i].p;
+        ly.dbg_i = debug ? dbg_i[l + i].p : nullptr;
+        ly.K_pad = K_pad[l + i]; ly.H = H[l + i]; ly.H_pad = H_pad[l + i];
+        fm.m[i] = tm_wt[l + i];
+      }
+      f.n_layers = nl;
       f.dbg_clk = debug ? dbg_clk.p + size_t(1 + l) * clk_region() : nullptr;
       f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
-      f.K_pad = K_pad[l]; f.H = H[l]; f.H_pad = H_pad[l]; f.in_kind = l == 0 ? 0 : 1;
+      f.in_kind = l == 0 ? 0 : 1;
       f.theta = net.threshold;
       f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
       f.spb = fwd_spb(TT);
       launch(k_lif_fwd, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128), dim3(kFwdThreads),
-             fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), tm_wt[l], f);
+             fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
       mark(evs, "lif_fwd", l);
     }
     // readout + loss + LI backward

@@ -163,19 +163,33 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // grid (ceil(B/SPB), H_pad/128); block 448: w0-7 scan (sample w/4, TMEM quadrant
 // w%4), w8-11 B-operand decode, w12 TMA, w13 MMA.
 // ============================================================================
-struct FwdArgs {
-  const uint8_t* x;       // staged dataset (layer 0)
-  const uint32_t* rows;   // [B] dataset row per sample (layer 0)
-  const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
-  const uint32_t* s_in;   // neuron-packed spikes of the previous layer (layer > 0)
+// One hidden LIF layer of a forward launch.
+struct FwdLayer {
   const float* beta;      // [H]
   const float* bias;      // [H] or nullptr
   float* v_out;           // [B][T_pad][H_pad]
   uint32_t* s_np;         // [B][T_pad][H_pad/32]
   uint32_t* s_tp;         // [H_pad][B*T_pad/32]
   float* dbg_i;           // optional [B][T_pad][H_pad] raw projection
-  long long* dbg_clk;     // optional [gridDim.x*gridDim.y][8] phase timestamps
-  int B, T, T_pad, TT, NT, K_pad, H, H_pad, in_kind, stages, spb;
+  int K_pad, H, H_pad;
+};
+// A launch runs n_layers consecutive hidden layers.  n_layers > 1 (fused) needs
+// one t-tile, one 128-neuron tile per layer and K_pad = 128 for layers >= 1: the
+// scan warps write each next layer's binary B operand straight into the idle
+// stages and the next GEMM runs in the same CTA.
+constexpr int kFwdFuseMax = SNN_MAX_HIDDEN;
+struct FwdMaps {
+  CUtensorMap m[kFwdFuseMax];  // W planes of each layer (MN-major 64x64 boxes)
+};
+struct FwdArgs {
+  const uint8_t* x;       // staged dataset (first layer = layer 0)
+  const uint32_t* rows;   // [B] dataset row per sample (layer 0)
+  const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
+  const uint32_t* s_in;   // neuron-packed spikes of the previous layer (first layer > 0)
+  FwdLayer lay[kFwdFuseMax];
+  int n_layers;
+  long long* dbg_clk;     // optional [gridDim.x*gridDim.y][kClkStride] phase timestamps
+  int B, T, T_pad, TT, NT, in_kind, stages, spb;
   float theta;
 };
 
@@ -253,7 +267,9 @@ __device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, fl
 }
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    k_lif_fwd(const __grid_constant__ CUtensorMap tm_w, FwdArgs a) {
+    k_lif_fwd(const __grid_constant__ FwdMaps maps, FwdArgs a) {
+  const CUtensorMap& tm_w = maps.m[0];
+  const int K_pad0 = a.lay[0].K_pad;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int SPB = a.spb;
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int S = a.stages;
   // layer 0: each sample's dataset run for the current t-tile is bulk-copied
   // into xbuf[tt % 2] (double-buffered across t-tiles)
-  const uint32_t xrun = a.in_kind == 0 ? fwd_xrun_bytes(a.TT, a.K_pad) : 0u;
+  const uint32_t xrun = a.in_kind == 0 ? fwd_xrun_bytes(a.TT, K_pad0) : 0u;
   const uint32_t xbuf_bytes = (uint32_t(SPB) * xrun + 1023) & ~1023u;
   uint8_t* xbuf = smem + S * stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * xbuf_bytes);
@@ -271,7 +287,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* xfull = acc_empty + 2;
   uint64_t* xempty = xfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 2);
+  uint64_t* lfull = xempty + 2;  // fused layers: W planes of k-block 0 / 1 landed
+  uint64_t* bready = lfull + 2;  // fused layers: next layer's B tiles written by the scan
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b0 = blockIdx.x * SPB, nt = blockIdx.y;
@@ -285,7 +303,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     clk[4] = smid;
   }
-  const int KB = a.K_pad / 64;
+  const int KB = K_pad0 / 64;
   const int total = a.NT * KB;
   // k-block order rotated per CTA: concurrent CTAs stream different W tiles
   const int rot = int(blockIdx.x) % KB;
@@ -303,7 +321,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&acc_empty[i], scan_threads);
       mbar_init(&xfull[i], 1);
       mbar_init(&xempty[i], 128);
+      mbar_init(&lfull[i], 1);
     }
+    mbar_init(bready, scan_threads);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
@@ -328,7 +348,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mbar_arrive_expect_tx(&xfull[xb], uint32_t(nsamp) * xrun);
           for (int sm = 0; sm < nsamp; ++sm)
             bulk_load(xbuf + xb * xbuf_bytes + sm * xrun,
-                      a.x + (size_t(rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(a.K_pad),
+                      a.x + (size_t(rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(K_pad0),
                       xrun, &xfull[xb]);
         }
         mbar_wait(&empty[s], ph ^ 1);
@@ -338,7 +358,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int p = 0; p < 3; ++p)
           for (int h = 0; h < 2; ++h)
             tma_load_2d(A + p * kPlaneTile + h * 8192, &tm_w, &full[s], nt * 128 + h * 64,
-                        p * a.K_pad + kb * 64);
+                        p * K_pad0 + kb * 64);
+      }
+      // fused layers: once the previous GEMM is complete the stages are idle; the
+      // next layer's W planes land in stage kb's A part while the scan runs
+      for (int li = 1; li < a.n_layers; ++li) {
+        mbar_wait(&acc_full[0], (li - 1) & 1);
+        const int KBl = a.lay[li].K_pad / 64;
+        for (int kb = 0; kb < KBl; ++kb) {
+          mbar_arrive_expect_tx(&lfull[kb], 3 * kPlaneTile);
+          for (int p = 0; p < 3; ++p)
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(smem + kb * stage_bytes + p * kPlaneTile + h * 8192, &maps.m[li], &lfull[kb],
+                          nt * 128 + h * 64, p * a.lay[li].K_pad + kb * 64);
+        }
       }
     }
     __syncwarp();
@@ -372,13 +405,35 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         umma_commit(&empty[s]);
         if (kb == KB - 1) umma_commit(&acc_full[buf]);
       }
+      // fused layers: A = W planes in stage kb, B = spikes the scan wrote (one t-tile)
+      for (int li = 1; li < a.n_layers; ++li) {
+        mbar_wait(bready, (li - 1) & 1);
+        tc_fence_after();
+        const int KBl = a.lay[li].K_pad / 64;
+        for (int kb = 0; kb < KBl; ++kb) {
+          mbar_wait(&lfull[kb], (li - 1) & 1);
+          tc_fence_after();
+          const uint32_t A = smem_u32(smem + kb * stage_bytes);
+          const uint32_t Bt = A + 3 * kPlaneTile;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
+#pragma unroll
+            for (int p = 2; p >= 0; --p) {
+              const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 2048, 8192, 1024);
+              umma_bf16(tmem, ad, bd, idesc, (kb | ks | (2 - p)) != 0);
+            }
+          }
+        }
+        umma_commit(&acc_full[0]);
+      }
     }
     __syncwarp();
   } else if (warp >= dec_warp0) {
     // ---------------- B-operand producers: activations -> bf16 {0,1} rows t, cols k,
     // sample s's rows at [s*TT, (s+1)*TT).  Loads of stage it+1 issue before the wait.
     const int tid = threadIdx.x - dec_warp0 * 32;
-    const size_t kwords = size_t(a.K_pad) / 32;
+    const size_t kwords = size_t(K_pad0) / 32;
     const int units = SPB * a.TT;  // kind 0: (sample, t-group, 8-feature chunk); kind 1: row
     auto fetch = [&](int it, int u) -> uint64_t {
       if (a.in_kind == 0 || u >= units || it >= total) return 0;
@@ -405,7 +460,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           // dataset bytes [t/8][k] (bulk-copied), bit 7-(t%8): 8 k of one t-group -> 8 rows
           const int g = r >> 3, q = r & 7;
           const uint64_t cur = sm < nsamp ? *reinterpret_cast<const uint64_t*>(
-              xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * a.K_pad + kb * 64 + q * 8) : 0ull;
+              xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * K_pad0 + kb * 64 + q * 8) : 0ull;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             st_shared_v4(Bt + sw128_off(sm * a.TT + 8 * g + j, q),
@@ -429,39 +484,56 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int sm = warp >> 2, q = warp & 3;
     const int b = b0 + sm;
     const int n = nt * 128 + q * 32 + lane;
-    const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
-    const float bn = (a.bias != nullptr && n < a.H) ? a.bias[n] : 0.0f;
-    const size_t hw = size_t(a.H_pad) / 32;
     const size_t tp_words = size_t(a.B) * a.T_pad / 32;
-    float v = 0.0f;
-    for (int tt = 0; tt < a.NT; ++tt) {
-      const int buf = tt % nbuf;
-      mbar_wait(&acc_full[buf], (tt / nbuf) & 1);
-      tc_fence_after();
-      if (clk != nullptr && threadIdx.x == 0 && tt == 0) clk[1] = clock64();
-      for (int c = 0; c < a.TT / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + buf * NTOT + sm * a.TT + c * 32, r);
-        tmem_ld_wait();
-        const int t0 = tt * a.TT + c * 32;
-        if (t0 >= a.T) {
-          // padded steps: no spikes (V rows beyond T are never read)
-          a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + q] = 0u;
-          a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = 0u;
-          continue;
+    for (int li = 0; li < a.n_layers; ++li) {
+      const FwdLayer& ly = a.lay[li];
+      const float vb = clip01(n < ly.H ? ly.beta[n] : 0.0f);
+      const float bn = (ly.bias != nullptr && n < ly.H) ? ly.bias[n] : 0.0f;
+      const size_t hw = size_t(ly.H_pad) / 32;
+      // fused: lane j writes the next layer's B row t0+j (its quadrant's 32 spikes
+      // of that step, from the ballot word) into stage q/2's B part
+      const bool feed = li + 1 < a.n_layers;
+      const uint32_t feed_b = smem_u32(smem + (q >> 1) * stage_bytes + 3 * kPlaneTile);
+      float v = 0.0f;
+      for (int tt = 0; tt < a.NT; ++tt) {
+        const int g = li * a.NT + tt;  // accumulator use (fused: one per layer)
+        const int buf = g % nbuf;
+        mbar_wait(&acc_full[buf], (g / nbuf) & 1);
+        tc_fence_after();
+        if (clk != nullptr && threadIdx.x == 0 && tt == 0 && li == 0) clk[1] = clock64();
+        for (int c = 0; c < a.TT / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + (uint32_t(q * 32) << 16) + buf * NTOT + sm * a.TT + c * 32, r);
+          tmem_ld_wait();
+          const int t0 = tt * a.TT + c * 32;
+          uint32_t myword = 0u, tmask = 0u;
+          if (t0 < a.T) {
+            float* vp = ly.v_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
+            if (ly.bias != nullptr || ly.dbg_i != nullptr || t0 + 32 > a.T)
+              lif_chunk<true>(r, vp, ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
+                              a.T - t0, vb, bn, a.theta, lane, v, myword, tmask);
+            else
+              lif_chunk<false>(r, vp, nullptr, ly.H_pad, 32, vb, 0.0f, a.theta, lane, v, myword, tmask);
+          }
+          // padded steps (t >= T): no spikes; V rows beyond T are never read
+          ly.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + q] = myword;
+          ly.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = tmask;
+          if (feed) {
+            const uint32_t row = uint32_t(sm * a.TT + c * 32 + lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              st_shared_v4(feed_b + sw128_off(row, uint32_t((q & 1) * 4 + i)),
+                           expand_bits_lsb((myword >> (8 * i)) & 0xFFu));
+          }
         }
-        float* vp = a.v_out + (size_t(b) * a.T_pad + t0) * a.H_pad + n;
-        uint32_t myword, tmask;
-        if (a.bias != nullptr || a.dbg_i != nullptr || t0 + 32 > a.T)
-          lif_chunk<true>(r, vp, a.dbg_i != nullptr ? a.dbg_i + (vp - a.v_out) : nullptr, a.H_pad,
-                          a.T - t0, vb, bn, a.theta, lane, v, myword, tmask);
-        else
-          lif_chunk<false>(r, vp, nullptr, a.H_pad, 32, vb, 0.0f, a.theta, lane, v, myword, tmask);
-        a.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + q] = myword;
-        a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t0 / 32] = tmask;
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[buf]);
+      if (feed) {
+        fence_async_smem();  // B tiles -> visible to the tensor core
+        tc_fence_before();   // TMEM reads of this layer done before the next MMA
+        mbar_arrive(bready);
+      }
     }
     if (clk != nullptr && threadIdx.x == 0) clk[2] = clock64();
   }
