@@ -667,16 +667,23 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     }
     const float v_final = v;
     RO_CLK(3)
-    // softmax CE, sequential order of objective.hpp:53-73
-    float mx = __shfl_sync(0xffffffffu, logit, 0);
-    for (int j = 1; j < C; ++j) {
-      const float lj = __shfl_sync(0xffffffffu, logit, j);
-      mx = (mx < lj) ? lj : mx;
-    }
+    // softmax CE, sequential order of objective.hpp:53-73.  The class values are
+    // gathered with independent shuffles first; only the max / sum chains are serial.
+    float lg[kMaxClasses];
+#pragma unroll
+    for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, logit, j);
+    float mx = lg[0];
+#pragma unroll
+    for (int j = 1; j < kMaxClasses; ++j)
+      if (j < C) mx = (mx < lg[j]) ? lg[j] : mx;
     const float xd = __fsub_rn(logit, mx);
     const float ex = lane < C ? (a.exp_mode ? expf(xd) : exp_cr(xd)) : 0.0f;
+#pragma unroll
+    for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, ex, j);
     float z = 0.0f;
-    for (int j = 0; j < C; ++j) z = __fadd_rn(z, __shfl_sync(0xffffffffu, ex, j));
+#pragma unroll
+    for (int j = 0; j < kMaxClasses; ++j)
+      if (j < C) z = __fadd_rn(z, lg[j]);
     const int y = s_label;
     const float logit_y = __shfl_sync(0xffffffffu, logit, y);
     // argmax, ties to the lowest index (objective.hpp:126-131)
