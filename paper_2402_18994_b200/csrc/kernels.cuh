@@ -585,15 +585,16 @@ __device__ __forceinline__ float log_cr(float x) { return float(log(double(x)));
 // of bank conflicts)
 constexpr int kRoStride = 33;
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (((size_t(HL) * C + 3) & ~size_t(3)) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
+  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
 }
 
 __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   extern __shared__ float rsm[];
   const int C = a.C, T = a.T;
   const int hw = a.HL_pad / 32;
-  float* w = rsm;                                                      // [HL][C]
-  uint32_t* spk = reinterpret_cast<uint32_t*>(w + ((size_t(a.HL) * C + 3) & ~size_t(3)));  // [T][hw]
+  const int Cp = (C + 3) & ~3;
+  float* w = rsm;                                                      // [HL][Cp]
+  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * Cp);  // [T][hw]
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
@@ -604,35 +605,70 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   if (tid == 0) s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
   const float beta_l = lane < C ? a.beta[lane] : 0.0f;
   {
-    // W rows (HL*C floats, 16-byte aligned when C % 4 == 0) and the spike words
+    // W rows padded to Cp floats (zeros in the padding) and the spike words
     const int nw = a.HL * C;
-    if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
+    if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
       const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
       for (int i = tid; i < nw / 4; i += 128) reinterpret_cast<float4*>(w)[i] = __ldg(src + i);
     } else {
-      for (int i = tid; i < nw; i += 128) w[i] = __ldg(a.w + i);
+      for (int i = tid; i < a.HL * Cp; i += 128) {
+        const int k = i / Cp, c = i % Cp;
+        w[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
+      }
     }
     const uint4* __restrict__ ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
     for (int i = tid; i < T * hw / 4; i += 128) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
   }
   __syncthreads();
   RO_CLK(1)
-  // projection (ops.hpp:163-172 order: ascending k, zero skip): one lane per
-  // time step, all classes per lane (acc in registers), W rows from smem.
+  // projection (ops.hpp:163-172 order: ascending k, zero skip): one lane per time
+  // step, all classes per lane (acc in registers).  W rows live in smem padded to
+  // Cp = C rounded up to 4 floats; the row of the next spike is loaded while the
+  // current one is added, so a burst of spikes costs the add chain, not one smem
+  // round trip per spike.
   for (int t = tid; t < T; t += 128) {
     float acc[kMaxClasses];
 #pragma unroll
     for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0f;
-    for (int wi = 0; wi < hw; ++wi) {
-      uint32_t bits = spk[t * hw + wi];
-      while (bits) {
-        const int i = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const float* wr = w + (wi * 32 + i) * C;
-#pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c)
-          if (c < C) acc[c] = __fadd_rn(acc[c], wr[c]);
+    const uint32_t* words = spk + t * hw;
+    int wi = 0;
+    uint32_t bits = words[0];
+    auto next_k = [&]() -> int {
+      while (bits == 0u) {
+        if (++wi >= hw) return -1;
+        bits = words[wi];
       }
+      const int i = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      return wi * 32 + i;
+    };
+    float4 cur[kMaxClasses / 4];
+    int k = next_k();
+    if (k >= 0) {
+      const float4* wr = reinterpret_cast<const float4*>(w + k * Cp);
+#pragma unroll
+      for (int j = 0; j < kMaxClasses / 4; ++j)
+        if (4 * j < C) cur[j] = wr[j];
+    }
+    while (k >= 0) {
+      const int kn = next_k();
+      float4 nxt[kMaxClasses / 4];
+      if (kn >= 0) {
+        const float4* wr = reinterpret_cast<const float4*>(w + kn * Cp);
+#pragma unroll
+        for (int j = 0; j < kMaxClasses / 4; ++j)
+          if (4 * j < C) nxt[j] = wr[j];
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxClasses / 4; ++j) {
+        if (4 * j + 0 < C) acc[4 * j + 0] = __fadd_rn(acc[4 * j + 0], cur[j].x);
+        if (4 * j + 1 < C) acc[4 * j + 1] = __fadd_rn(acc[4 * j + 1], cur[j].y);
+        if (4 * j + 2 < C) acc[4 * j + 2] = __fadd_rn(acc[4 * j + 2], cur[j].z);
+        if (4 * j + 3 < C) acc[4 * j + 3] = __fadd_rn(acc[4 * j + 3], cur[j].w);
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxClasses / 4; ++j) cur[j] = nxt[j];
+      k = kn;
     }
 #pragma unroll
     for (int c = 0; c < kMaxClasses; ++c) {

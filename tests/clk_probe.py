@@ -22,6 +22,8 @@ for s, name in enumerate(names):
 for s, name in ((1, "fwd0"), (2, "fwd1")):
     c = clk[s]
     valid = c[:, 6] > 0
+    if not valid.any():
+        continue
     st, en = c[valid, 6], c[valid, 7]
     t0 = st.min()
     print(f"{name}: CTAs {valid.sum()}  start spread {(st.max()-t0)/1e3:.1f} us  end spread {(en.min()-t0)/1e3:.1f}..{(en.max()-t0)/1e3:.1f} us  per-CTA median {np.median(en-st)/1e3:.1f} us")
@@ -49,6 +51,9 @@ t0 = None
 for name in order:
     c = clk[slot[name]]
     v = c[:, 14] > 0
+    if not v.any():
+        print(f"TL {name:8s} (fused into another launch)")
+        continue
     st, en = c[v, 14], c[v, 15]
     if t0 is None: t0 = st.min()
     print(f"TL {name:8s} ctas {v.sum():4d} start {(st.min()-t0)/1e3:7.1f} .. {(st.max()-t0)/1e3:7.1f}  end {(en.min()-t0)/1e3:7.1f} .. {(en.max()-t0)/1e3:7.1f} us  span {(en.max()-st.min())/1e3:6.1f}  cta med {np.median(en-st)/1e3:5.1f}")
