@@ -727,7 +727,7 @@ struct snn_engine {
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
       r.inv_b = 1.0f / float(B_global());
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
-      launch(k_readout, dim3(B), dim3(128), smem, r);
+      launch(k_readout, dim3(B), dim3(kRoThreads), smem, r);
       mark(evs, "readout", -1);
     }
     // hidden backward, top-down: dS on tcgen05 (readout-fed layer: K = classes)

@@ -584,11 +584,12 @@ __device__ __forceinline__ float log_cr(float x) { return float(log(double(x)));
 // written by the projection and the per-class columns read by the scans free
 // of bank conflicts)
 constexpr int kRoStride = 33;
+constexpr int kRoThreads = 256;  // projection: 2 lanes per time step (class groups split)
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
   return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
 }
 
-__global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
+__global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   extern __shared__ float rsm[];
   const int C = a.C, T = a.T;
   const int hw = a.HL_pad / 32;
@@ -609,27 +610,30 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
     const int nw = a.HL * C;
     if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
       const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
-      for (int i = tid; i < nw / 4; i += 128) reinterpret_cast<float4*>(w)[i] = __ldg(src + i);
+      for (int i = tid; i < nw / 4; i += kRoThreads) reinterpret_cast<float4*>(w)[i] = __ldg(src + i);
     } else {
-      for (int i = tid; i < a.HL * Cp; i += 128) {
+      for (int i = tid; i < a.HL * Cp; i += kRoThreads) {
         const int k = i / Cp, c = i % Cp;
         w[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
       }
     }
     const uint4* __restrict__ ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
-    for (int i = tid; i < T * hw / 4; i += 128) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
+    for (int i = tid; i < T * hw / 4; i += kRoThreads) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
   }
   __syncthreads();
   RO_CLK(1)
-  // projection (ops.hpp:163-172 order: ascending k, zero skip): one lane per time
-  // step, all classes per lane (acc in registers).  W rows live in smem padded to
+  // projection (ops.hpp:163-172 order: ascending k, zero skip): a lane pair per
+  // time step, lane h of the pair owning the 4-class groups j = 2jj + h (acc in
+  // registers; the pair walks the same spike bits).  W rows live in smem padded to
   // Cp = C rounded up to 4 floats; the row of the next spike is loaded while the
   // current one is added, so a burst of spikes costs the add chain, not one smem
   // round trip per spike.
-  for (int t = tid; t < T; t += 128) {
-    float acc[kMaxClasses];
+  constexpr int kGroups = kMaxClasses / 8;  // 4-class groups per lane
+  const int h = tid & 1;
+  for (int t = tid >> 1; t < T; t += kRoThreads / 2) {
+    float acc[kGroups][4];
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0f;
+    for (int jj = 0; jj < kGroups; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0.0f;
     const uint32_t* words = spk + t * hw;
     int wi = 0;
     uint32_t bits = words[0];
@@ -642,39 +646,44 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
       bits &= bits - 1u;
       return wi * 32 + i;
     };
-    float4 cur[kMaxClasses / 4];
+    float4 cur[kGroups];
     int k = next_k();
     if (k >= 0) {
-      const float4* wr = reinterpret_cast<const float4*>(w + k * Cp);
+      const float4* wr = reinterpret_cast<const float4*>(w + k * Cp) + h;
 #pragma unroll
-      for (int j = 0; j < kMaxClasses / 4; ++j)
-        if (4 * j < C) cur[j] = wr[j];
+      for (int jj = 0; jj < kGroups; ++jj)
+        if (4 * (2 * jj + h) < C) cur[jj] = wr[2 * jj];
     }
     while (k >= 0) {
       const int kn = next_k();
-      float4 nxt[kMaxClasses / 4];
+      float4 nxt[kGroups];
       if (kn >= 0) {
-        const float4* wr = reinterpret_cast<const float4*>(w + kn * Cp);
+        const float4* wr = reinterpret_cast<const float4*>(w + kn * Cp) + h;
 #pragma unroll
-        for (int j = 0; j < kMaxClasses / 4; ++j)
-          if (4 * j < C) nxt[j] = wr[j];
+        for (int jj = 0; jj < kGroups; ++jj)
+          if (4 * (2 * jj + h) < C) nxt[jj] = wr[2 * jj];
       }
 #pragma unroll
-      for (int j = 0; j < kMaxClasses / 4; ++j) {
-        if (4 * j + 0 < C) acc[4 * j + 0] = __fadd_rn(acc[4 * j + 0], cur[j].x);
-        if (4 * j + 1 < C) acc[4 * j + 1] = __fadd_rn(acc[4 * j + 1], cur[j].y);
-        if (4 * j + 2 < C) acc[4 * j + 2] = __fadd_rn(acc[4 * j + 2], cur[j].z);
-        if (4 * j + 3 < C) acc[4 * j + 3] = __fadd_rn(acc[4 * j + 3], cur[j].w);
+      for (int jj = 0; jj < kGroups; ++jj) {
+        const int c0 = 4 * (2 * jj + h);
+        if (c0 + 0 < C) acc[jj][0] = __fadd_rn(acc[jj][0], cur[jj].x);
+        if (c0 + 1 < C) acc[jj][1] = __fadd_rn(acc[jj][1], cur[jj].y);
+        if (c0 + 2 < C) acc[jj][2] = __fadd_rn(acc[jj][2], cur[jj].z);
+        if (c0 + 3 < C) acc[jj][3] = __fadd_rn(acc[jj][3], cur[jj].w);
       }
 #pragma unroll
-      for (int j = 0; j < kMaxClasses / 4; ++j) cur[j] = nxt[j];
+      for (int jj = 0; jj < kGroups; ++jj) cur[jj] = nxt[jj];
       k = kn;
     }
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) {
-      if (c < C && a.bias != nullptr) acc[c] = __fadd_rn(acc[c], a.bias[c]);
-      buf[t * kRoStride + c] = c < C ? acc[c] : 0.0f;
-    }
+    for (int jj = 0; jj < kGroups; ++jj)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = 4 * (2 * jj + h) + e;
+        float vout = 0.0f;
+        if (c < C) vout = a.bias != nullptr ? __fadd_rn(acc[jj][e], a.bias[c]) : acc[jj][e];
+        buf[t * kRoStride + c] = vout;  // c < 32: classes >= C are zero
+      }
   }
   __syncthreads();
   RO_CLK(2)
@@ -791,7 +800,7 @@ __global__ void __launch_bounds__(128) k_readout(ReadoutArgs a) {
   const int chunks = (T + 7) / 8;
   const size_t cols = size_t(a.B) * a.T_pad;
   const size_t plane = size_t(64) * cols;
-  for (int u = tid; u < C * chunks; u += 128) {
+  for (int u = tid; u < C * chunks; u += kRoThreads) {
     const int c = u / chunks, t0 = (u % chunks) * 8;
     uint32_t hp[4], mp[4], lp[4];
 #pragma unroll
