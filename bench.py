@@ -110,14 +110,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ roofline
-def algorithmic(name: str, w: dict, n_params: int):
-    """(bound, work per launch) from SURVEY.md §8(d) per-unit figures."""
+def algorithmic(name: str, w: dict, n_params: int, fwd_groups=None):
+    """(bound, work per launch) from SURVEY.md §8(d) per-unit figures.  fwd_groups:
+    Engine.forward_launches -- a fused forward launch does every layer it covers."""
     B, T, C = w["B"], w["T"], w["classes"]
     dims = [w["inp"], *w["hidden"], C]
     base, _, idx = name.partition("[")
     l = int(idx.rstrip("]")) if idx else 0
-    if base == "lif_fwd":            # I = A W over all T: 2 B T K N flops
-        return "tensor", 2.0 * B * T * dims[l] * dims[l + 1]
+    if base == "lif_fwd":            # I = A W over all T: 2 B T K N flops per layer
+        n = dict(fwd_groups or []).get(l, 1)
+        return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(l, l + n))
     if base == "wgrad":              # dW = A^T dI, every Linear layer in one launch
         return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(len(dims) - 1))
     if base == "lif_bwd":            # LIF reverse scan: 12 B / neuron-step (SURVEY §8d)
@@ -352,7 +354,7 @@ def main():
     hbm_peak, tf_peak, peak_src = peaks()
     kernels = []
     for name, kms in prof:
-        bound, work = algorithmic(name, w, eng.n_params)
+        bound, work = algorithmic(name, w, eng.n_params, eng.forward_launches)
         kernels.append({"name": name, "ms": kms, "bound": bound, "work": work})
     dom = max(kernels, key=lambda k: k["ms"])
     if dom["bound"] == "tensor":

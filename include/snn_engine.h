@@ -159,6 +159,10 @@ snn_status snn_train_epochs_from(snn_engine* e, size_t first_epoch, size_t epoch
 snn_status snn_upload_schedule(snn_engine* e, const uint32_t* rows, size_t n_steps);
 snn_status snn_enqueue_step(snn_engine* e, size_t slot);
 snn_status snn_enqueue_steps(snn_engine* e, size_t first_slot, size_t n_steps);
+/* Forward launches of one step: launch i runs hidden layers [first, first + count)
+ * (narrow layers are fused into one launch).  Returns count, or 0 when i is out of
+ * range; *first may be NULL. */
+int32_t snn_forward_launch_layers(const snn_engine* e, int32_t i, int32_t* first);
 snn_status snn_sync(snn_engine* e);
 snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy);
 /* cudaStream_t of the engine, for CUDA-event timing by the caller. */

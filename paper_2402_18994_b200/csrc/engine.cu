@@ -1278,6 +1278,14 @@ void* snn_stream(snn_engine* e) { return e ? static_cast<void*>(e->stream) : nul
 
 int32_t snn_launches_per_step(const snn_engine* e) { return e ? e->launches_per_step() : 0; }
 
+int32_t snn_forward_launch_layers(const snn_engine* e, int32_t i, int32_t* first) {
+  if (!e || i < 0) return 0;
+  const auto g = e->fwd_groups();
+  if (size_t(i) >= g.size()) return 0;
+  if (first) *first = g[size_t(i)].first;
+  return g[size_t(i)].second;
+}
+
 snn_status snn_nccl_unique_id(uint8_t id[128]) {
   if (!id) return SNN_ERR_ARGUMENT;
   NcclApi& api = nccl();

@@ -176,6 +176,8 @@ def lib() -> C.CDLL:
     L.snn_stream.argtypes = [C.c_void_p]
     L.snn_launches_per_step.restype = C.c_int32
     L.snn_launches_per_step.argtypes = [C.c_void_p]
+    L.snn_forward_launch_layers.restype = C.c_int32
+    L.snn_forward_launch_layers.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
     for name in ("snn_engine_create", "snn_param_count", "snn_entry_count", "snn_entry_info",
                  "snn_set_params", "snn_get_params", "snn_init_params", "snn_get_opt_state",
                  "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
@@ -405,6 +407,17 @@ class Engine:
     @property
     def launches_per_step(self) -> int:
         return int(self._L.snn_launches_per_step(self._h))
+
+    @property
+    def forward_launches(self) -> list[tuple[int, int]]:
+        """[(first hidden layer, layer count)] per forward launch of a step."""
+        out, i, first = [], 0, C.c_int32()
+        while True:
+            n = int(self._L.snn_forward_launch_layers(self._h, i, C.byref(first)))
+            if n == 0:
+                return out
+            out.append((int(first.value), n))
+            i += 1
 
     # ---------------------------------------------------------- multi-GPU
     @staticmethod

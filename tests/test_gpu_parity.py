@@ -310,4 +310,6 @@ def test_launch_count_matches_captured_step(orc):
         names = [n for n, _ in eng.profile(1)]
         assert len(names) == eng.launches_per_step, names
         assert sum(n.startswith("lif_fwd") for n in names) == n_fwd, names
+        groups = eng.forward_launches
+        assert len(groups) == n_fwd and sum(c for _, c in groups) == len(net.hidden), groups
         assert names[-1] == "reduce_adam"
