@@ -163,6 +163,15 @@ snn_status snn_enqueue_steps(snn_engine* e, size_t first_slot, size_t n_steps);
  * (narrow layers are fused into one launch).  Returns count, or 0 when i is out of
  * range; *first may be NULL. */
 int32_t snn_forward_launch_layers(const snn_engine* e, int32_t i, int32_t* first);
+/* Evaluation.  snn_evaluate mirrors cmd_eval
+ * (commands.hpp:144-169): integral accuracy over `n` dataset rows walked in
+ * batches of the engine batch size (last batch short), forward only; mean_loss
+ * (optional) is the mean integral-CE loss over the rows.  snn_apply mirrors
+ * apply (network.hpp:435-448) for one batch of B rows: the readout trace
+ * [B][T][classes] (n = B*T*classes floats). */
+snn_status snn_evaluate(snn_engine* e, const uint32_t* rows, size_t n, double* accuracy,
+                        double* mean_loss);
+snn_status snn_apply(snn_engine* e, const uint32_t* rows, float* trace, size_t n);
 snn_status snn_sync(snn_engine* e);
 snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy);
 /* cudaStream_t of the engine, for CUDA-event timing by the caller. */

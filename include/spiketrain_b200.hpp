@@ -237,6 +237,25 @@ inline StepResult train_step(TrainState& st, const std::vector<std::uint8_t>& pa
   return r;
 }
 
+// cmd_eval (commands.hpp:144-169) on the dataset staged in the engine (train() /
+// snn_stage_dataset): integral accuracy over all `n_rows` rows, walked in batches
+// of the engine batch size, forward only.
+inline double evaluate(TrainState& st, std::size_t n_rows) {
+  std::vector<std::uint32_t> rows(n_rows);
+  for (std::size_t i = 0; i < n_rows; ++i) rows[i] = std::uint32_t(i);
+  double acc = 0.0;
+  check(snn_evaluate(st.engine(), rows.data(), rows.size(), &acc, nullptr), st.engine());
+  return acc;
+}
+
+// apply (network.hpp:435-448) for one batch of staged rows: readout trace [B][T][C].
+inline std::vector<float> apply(TrainState& st, const std::vector<std::uint32_t>& rows,
+                                std::size_t classes) {
+  std::vector<float> trace(st.cfg().batch_size * st.original_t() * classes);
+  check(snn_apply(st.engine(), rows.data(), trace.data(), trace.size()), st.engine());
+  return trace;
+}
+
 struct TrainResult {
   std::vector<float> params;
   std::vector<EpochMetrics> metrics;

@@ -207,6 +207,18 @@ class Lib:
             out["trace"] = trace
         return out
 
+    def eval_accuracy(self, net: Net, params, packed, y, t, batch) -> float:
+        """cmd_eval (commands.hpp:144-169): batches of `batch` rows (the last one
+        short), integral_accuracy per batch (objective.hpp:118-134, computed by the
+        oracle in the reference order) accumulated as correct += acc * nb, / n."""
+        n = packed.shape[0]
+        correct = 0.0
+        for lo in range(0, n, batch):
+            hi = min(n, lo + batch)
+            r = self.forward_backward(net, params, packed[lo:hi], t, y[lo:hi], want_grads=False)
+            correct += r["acc"] * float(hi - lo)
+        return correct / float(n)
+
     def adam(self, p, g, m, v, step, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
         st = C.c_uint64(step)
         self._f("adam")(_ptr(p, C.c_float), _ptr(g, C.c_float), _ptr(m, C.c_float),

@@ -220,6 +220,10 @@ struct snn_engine {
   // debug
   bool debug = false;
   DevBuf<float> dbg_i[SNN_MAX_HIDDEN], dbg_ds[SNN_MAX_HIDDEN], dbg_trace;
+  // evaluation graphs (update flag): kEval = forward + readout, kEvalTrace = + the
+  // readout trace [B][T][C] into eval_trace (apply, network.hpp:435-448)
+  static constexpr int kEval = 2, kEvalTrace = 3;
+  DevBuf<float> eval_trace;
   DevBuf<long long> dbg_clk;
   // graphs keyed by (dataset ptr, update flag, mode): mode 0 = rows_cur, mode g >= 1 =
   // g consecutive schedule steps (rows from sched[*sched_slot])
@@ -721,7 +725,7 @@ struct snn_engine {
       r.correct_b = correct_b.p;
       r.dbeta_part = dbeta[L].p;
       r.dbias_part = net.bias ? dbias[L].p : nullptr;
-      r.dbg_trace = debug ? dbg_trace.p : nullptr;
+      r.dbg_trace = update == kEvalTrace ? eval_trace.p : (debug ? dbg_trace.p : nullptr);
       r.dbg_clk = debug ? dbg_clk.p : nullptr;
       r.exp_mode = exp_mode;
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
@@ -730,6 +734,7 @@ struct snn_engine {
       launch(k_readout, dim3(B), dim3(kRoThreads), smem, r);
       mark(evs, "readout", -1);
     }
+    if (update >= kEval) return;  // evaluation: forward + readout only (apply, cmd_eval)
     // hidden backward, top-down: dS on tcgen05 (readout-fed layer: K = classes)
     for (int l = L - 1; l >= 0; --l) {
       BwdArgs bw{};
@@ -1213,6 +1218,71 @@ snn_status snn_enqueue_step(snn_engine* e, size_t slot) {
 snn_status snn_enqueue_steps(snn_engine* e, size_t first_slot, size_t n_steps) {
   if (!e) return SNN_ERR_ARGUMENT;
   return guard(e, [&] { e->launch_sched(first_slot, n_steps); });
+}
+
+// cmd_eval (commands.hpp:144-169): accuracy over `n` dataset rows in batches of the
+// engine batch size B, the last batch short (its padding rows are not counted);
+// per batch integral_accuracy = hits / nb (objective.hpp:118-134), accumulated as
+// correct += acc * nb and divided by n, in the reference's double arithmetic.
+snn_status snn_evaluate(snn_engine* e, const uint32_t* rows, size_t n, double* accuracy,
+                        double* mean_loss) {
+  if (!e || !rows || n == 0) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (e->data.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    for (size_t i = 0; i < n; ++i)
+      if (rows[i] >= e->data.n) fail(SNN_ERR_ARGUMENT, "row %u outside dataset of %zu", rows[i], e->data.n);
+    const size_t B = size_t(e->B), nb = (n + B - 1) / B;
+    uint32_t* h_rows = nullptr;
+    int32_t* h_hit = nullptr;
+    float* h_loss = nullptr;
+    CK(cudaMallocHost(&h_rows, nb * B * sizeof(uint32_t)));
+    CK(cudaMallocHost(&h_hit, nb * B * sizeof(int32_t)));
+    CK(cudaMallocHost(&h_loss, nb * B * sizeof(float)));
+    struct Free {
+      void* p[3];
+      ~Free() { for (void* q : p) if (q) cudaFreeHost(q); }
+    } fr{{h_rows, h_hit, h_loss}};
+    for (size_t i = 0; i < nb * B; ++i) h_rows[i] = i < n ? rows[i] : rows[0];
+    cudaGraphExec_t g = e->graph_for(e->data, snn_engine::kEval);
+    for (size_t i = 0; i < nb; ++i) {
+      CK(cudaMemcpyAsync(e->rows_cur.p, h_rows + i * B, B * sizeof(uint32_t), cudaMemcpyHostToDevice, e->stream));
+      CK(cudaGraphLaunch(g, e->stream));
+      CK(cudaMemcpyAsync(h_hit + i * B, e->correct_b.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
+      CK(cudaMemcpyAsync(h_loss + i * B, e->loss_b.p, B * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    }
+    CK(cudaStreamSynchronize(e->stream));
+    double correct = 0.0, loss = 0.0;
+    for (size_t i = 0; i < nb; ++i) {
+      const size_t cnt = std::min(B, n - i * B);
+      size_t hits = 0;
+      for (size_t j = 0; j < cnt; ++j) {
+        hits += h_hit[i * B + j] != 0;
+        loss += double(h_loss[i * B + j]);
+      }
+      correct += double(hits) / double(cnt) * double(cnt);
+    }
+    if (accuracy) *accuracy = correct / double(n);
+    if (mean_loss) *mean_loss = loss / double(n);
+  });
+}
+
+// apply (network.hpp:435-448) on one batch of B dataset rows: the readout (LI)
+// trace [B][T][C], forward only.
+snn_status snn_apply(snn_engine* e, const uint32_t* rows, float* trace, size_t n) {
+  if (!e || !rows || !trace) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (e->data.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    const size_t need = size_t(e->B) * e->T * e->C;
+    if (n != need) fail(SNN_ERR_SHAPE, "trace holds %zu floats, need %zu", n, need);
+    if (e->eval_trace.n != need) {
+      e->eval_trace.alloc(need);
+      e->clear_graphs();
+    }
+    e->set_rows_host(rows, e->data);
+    CK(cudaGraphLaunch(e->graph_for(e->data, snn_engine::kEvalTrace), e->stream));
+    CK(cudaMemcpyAsync(trace, e->eval_trace.p, need * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
 }
 
 snn_status snn_sync(snn_engine* e) {

@@ -182,7 +182,7 @@ def lib() -> C.CDLL:
                  "snn_set_params", "snn_get_params", "snn_init_params", "snn_get_opt_state",
                  "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
                  "snn_train_step_packed", "snn_forward_backward", "snn_train_epochs",
-                 "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_sync", "snn_read_result",
+                 "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_evaluate", "snn_apply", "snn_sync", "snn_read_result",
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
                  "snn_read_dataset"):
@@ -383,6 +383,23 @@ class Engine:
     def enqueue_steps(self, first_slot: int, n_steps: int):
         """Schedule slots [first_slot, first_slot + n_steps), 8 steps per graph launch."""
         self._check(self._L.snn_enqueue_steps(self._h, C.c_size_t(first_slot), C.c_size_t(n_steps)))
+
+    # ------------------------------------------------------------ evaluation
+    def evaluate(self, rows) -> tuple[float, float]:
+        """cmd_eval (commands.hpp:144-169) over dataset `rows`: (accuracy, mean loss)."""
+        r = np.ascontiguousarray(rows, np.uint32)
+        acc, loss = C.c_double(), C.c_double()
+        self._check(self._L.snn_evaluate(self._h, _p(r, C.c_uint32), C.c_size_t(r.size),
+                                         C.byref(acc), C.byref(loss)))
+        return acc.value, loss.value
+
+    def apply(self, rows) -> np.ndarray:
+        """apply (network.hpp:435-448) on one batch of rows: readout trace [B, T, C]."""
+        r = np.ascontiguousarray(rows, np.uint32)
+        out = np.empty((self.batch_size, self.time_steps, self.desc["classes"]), np.float32)
+        self._check(self._L.snn_apply(self._h, _p(r, C.c_uint32), _p(out, C.c_float),
+                                      C.c_size_t(out.size)))
+        return out
 
     def sync(self):
         self._check(self._L.snn_sync(self._h))

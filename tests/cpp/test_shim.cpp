@@ -70,6 +70,25 @@ int main() {
     std::printf("toy: loss %.4f -> %.4f, acc %.3f, steps %llu\n", r.metrics.front().loss,
                 r.metrics.back().loss, r.metrics.back().accuracy, (unsigned long long)r.step);
   }
+  // cmd_eval after training (commands.hpp:144-169): the trained toy separates its
+  // own data; evaluation is forward only (no optimizer step)
+  {
+    const auto data = toy_data(16, 16, rng::from_seed(703));
+    st::TrainConfig cfg;
+    cfg.epochs = 30;
+    cfg.batch_size = 8;
+    cfg.lr = 5e-3;
+    cfg.seed = 1;
+    cfg.unroll = 8;
+    st::TrainState state(toy_spec(), cfg, data.original_t);
+    st::train(state, data);
+    const auto step = state.optimizer_step();
+    const double acc = st::evaluate(state, data.n);
+    CHECK(acc >= 0.75 && acc <= 1.0);
+    CHECK(state.optimizer_step() == step);
+    CHECK(st::evaluate(state, data.n) == acc);
+    std::printf("toy eval accuracy %.3f\n", acc);
+  }
   // "training is deterministic in the seed" (optimize_test.cpp:170-191)
   {
     const auto data = toy_data(8, 16, rng::from_seed(702));

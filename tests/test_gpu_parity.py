@@ -313,3 +313,48 @@ def test_launch_count_matches_captured_step(orc):
         groups = eng.forward_launches
         assert len(groups) == n_fwd and sum(c for _, c in groups) == len(net.hidden), groups
         assert names[-1] == "reduce_adam"
+
+
+def test_apply_trace_matches_oracle(orc):
+    """apply (network.hpp:435-448): the readout trace of one batch, forward only."""
+    net = Net(inp=40, hidden=(24, 20), classes=6, act="superspike")
+    B, T = 5, 30
+    params = orc.init(net, orc.key_child(orc.key_from_seed(4), 0)) * np.float32(3.0)
+    x, y = orc.synth_raster(net.classes, 12, T, net.inp, 3)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    rows = np.array([7, 0, 11, 3, 3], np.uint32)
+    tr = eng.apply(rows)
+    ref = orc.forward_backward(net, params, pk[rows], T, y[rows], want_grads=False, want_trace=True)
+    assert relnorm(tr, ref["trace"]) <= REL_TOL
+    assert np.array_equal(eng.get_params(), params)        # forward only: no update
+    assert eng.get_opt_state()[2] == 0
+
+
+def test_evaluate_matches_cmd_eval(orc):
+    """cmd_eval (commands.hpp:144-169) after some training: accuracy equals the
+    reference's batched walk exactly, and is independent of the batch split
+    (commands_test.cpp:199-238: 24 examples as one batch vs 4 x 5 + a tail of 4)."""
+    net = Net(inp=40, hidden=(24, 20), classes=4)
+    T, N = 25, 24
+    x, y = orc.synth_raster(net.classes, N, T, net.inp, 6)
+    pk = orc.pack_time(x)
+    trainer = make_engine(net, N, T, seed=2)
+    trainer.stage_dataset(pk, y)
+    for _ in range(6):
+        trainer.train_step(np.arange(N, dtype=np.uint32))
+    params = trainer.get_params()
+    accs = {}
+    for B in (24, 5):
+        eng = make_engine(net, B, T)
+        eng.stage_dataset(pk, y)
+        eng.set_params(params)
+        acc, loss = eng.evaluate(np.arange(N, dtype=np.uint32))
+        ref = orc.eval_accuracy(net, params, pk, y, T, B)
+        assert acc == ref, (B, acc, ref)
+        assert np.isfinite(loss) and loss > 0
+        accs[B] = acc
+    assert accs[24] == accs[5]
+    assert 0.0 <= accs[24] <= 1.0
