@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 1
+#define SNN_ABI_VERSION 2
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -76,6 +76,11 @@ typedef struct snn_train_config {
   float beta1, beta2, eps;
   uint64_t seed;        /* TrainConfig.seed: init key child(0), epoch keys child(1+e) */
   int32_t unroll;       /* accepted for API parity; scheduling only (network.hpp:352) */
+  /* TrainConfig options on the step (optimize.hpp:113-131); zero = Adam + integral CE */
+  int32_t optimizer;    /* 0 Adam, 1 SGD with momentum (optimize.hpp:69-84) */
+  float momentum;       /* SGD momentum (TrainConfig default 0.9) */
+  int32_t loss;         /* 0 integral CE (objective.hpp:88-114), 1 spike-rate MSE (:139-183) */
+  float rate_hi, rate_lo; /* rate-MSE targets on / off the true class (defaults 0.9 / 0.1) */
 } snn_train_config;
 
 typedef struct snn_engine snn_engine;

@@ -95,10 +95,19 @@ struct NetworkSpec {
   std::vector<Layer> layers;
 };
 
+enum class OptimizerKind { Adam, Sgd };                       // optimize.hpp:22
+enum class LossKind { IntegralCrossentropy, SpikeRateMse };  // optimize.hpp:23
+
+// optimize.hpp:116-133 (the fields the training step consumes)
 struct TrainConfig {
   std::size_t epochs = 100;
   std::size_t batch_size = 64;
   double lr = 1e-3;
+  OptimizerKind optimizer = OptimizerKind::Adam;
+  double momentum = 0.9;  // SGD only
+  LossKind loss = LossKind::IntegralCrossentropy;
+  double rate_hi = 0.9;  // rate-MSE targets
+  double rate_lo = 0.1;
   std::uint64_t seed = 0;
   std::size_t unroll = 32;
 };
@@ -185,6 +194,11 @@ class TrainState {
     c.eps = 1e-8f;
     c.seed = cfg.seed;
     c.unroll = int32_t(cfg.unroll);
+    c.optimizer = cfg.optimizer == OptimizerKind::Sgd ? 1 : 0;
+    c.momentum = float(cfg.momentum);
+    c.loss = cfg.loss == LossKind::SpikeRateMse ? 1 : 0;
+    c.rate_hi = float(cfg.rate_hi);
+    c.rate_lo = float(cfg.rate_lo);
     snn_engine* e = nullptr;
     check(snn_engine_create(&d, &c, device, &e), nullptr);
     eng_.reset(e);

@@ -31,6 +31,26 @@ class _Net(C.Structure):
                 ("slope", C.c_float), ("aux", C.c_float), ("unroll", C.c_int)]
 
 
+class _Opts(C.Structure):
+    _fields_ = [("optimizer", C.c_int), ("momentum", C.c_float), ("loss", C.c_int),
+                ("rate_hi", C.c_float), ("rate_lo", C.c_float)]
+
+
+@dataclass
+class Opts:
+    """TrainConfig options on the step (optimize.hpp:113-131): optimizer 'adam' |
+    'sgd' (+ momentum), loss 'ce' (integral CE) | 'rate_mse' (+ rate targets)."""
+    optimizer: str = "adam"
+    momentum: float = 0.9
+    loss: str = "ce"
+    rate_hi: float = 0.9
+    rate_lo: float = 0.1
+
+    def c(self) -> _Opts:
+        return _Opts(1 if self.optimizer == "sgd" else 0, self.momentum,
+                     1 if self.loss == "rate_mse" else 0, self.rate_hi, self.rate_lo)
+
+
 @dataclass
 class Net:
     """Linear->LIF stack + Linear->LI readout (network.hpp:23-60)."""
@@ -93,7 +113,9 @@ class Lib:
         f("param_count").restype = C.c_size_t
         f("entry_count").restype = C.c_int
         f("forward_backward").restype = C.c_int
+        f("forward_backward_ex").restype = C.c_int
         f("train_step").restype = C.c_int
+        f("train_step_ex").restype = C.c_int
         f("train_epochs").restype = C.c_int
         self._f = f
 
@@ -168,8 +190,9 @@ class Lib:
 
     def forward_backward(self, net: Net, params, packed, t, targets,
                          want_grads=True, want_spikes=False, want_trace=False,
-                         want_v=False):
+                         want_v=False, opts: "Opts | None" = None):
         n = net.c()
+        oc = opts.c() if opts is not None else None
         B = packed.shape[0]
         params = np.ascontiguousarray(params, np.float32)
         packed = np.ascontiguousarray(packed, np.uint8)
@@ -181,8 +204,9 @@ class Lib:
         spikes = np.zeros(nsp, np.uint8) if want_spikes else None
         vtr = np.zeros(nsp, np.float32) if want_v else None
         trace = np.zeros((B, t, net.classes), np.float32) if want_trace else None
-        rc = self._f("forward_backward")(
-            C.byref(n), _ptr(params, C.c_float), _ptr(packed, C.c_uint8),
+        rc = self._f("forward_backward_ex")(
+            C.byref(n), C.byref(oc) if oc is not None else None, _ptr(params, C.c_float),
+            _ptr(packed, C.c_uint8),
             C.c_size_t(B), C.c_size_t(t), _ptr(targets, C.c_int64), C.byref(loss),
             C.byref(acc), _ptr(grads, C.c_float), _ptr(spikes, C.c_uint8),
             _ptr(vtr, C.c_float), _ptr(trace, C.c_float))
@@ -226,15 +250,18 @@ class Lib:
                         C.c_float(lr), C.c_float(b1), C.c_float(b2), C.c_float(eps))
         return st.value
 
-    def train_step(self, net: Net, state: "State", packed, t, targets, lr=1e-3):
+    def train_step(self, net: Net, state: "State", packed, t, targets, lr=1e-3,
+                   opts: "Opts | None" = None):
         n = net.c()
+        oc = opts.c() if opts is not None else None
         packed = np.ascontiguousarray(packed, np.uint8)
         targets = np.ascontiguousarray(targets, np.int64)
         loss = C.c_float()
         acc = C.c_double()
         st = C.c_uint64(state.step)
-        rc = self._f("train_step")(
-            C.byref(n), _ptr(state.params, C.c_float), _ptr(state.m, C.c_float),
+        rc = self._f("train_step_ex")(
+            C.byref(n), C.byref(oc) if oc is not None else None,
+            _ptr(state.params, C.c_float), _ptr(state.m, C.c_float),
             _ptr(state.v, C.c_float), C.byref(st), _ptr(packed, C.c_uint8),
             C.c_size_t(packed.shape[0]), C.c_size_t(t), _ptr(targets, C.c_int64),
             C.c_float(lr), C.byref(loss), C.byref(acc))

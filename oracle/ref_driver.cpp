@@ -146,11 +146,26 @@ void ref_init(const orc_net* n, uint64_t key, float* params) {
   params_to_flat(p, params);
 }
 
+int ref_forward_backward_ex(const orc_net* n, const orc_train_opts* opts,
+                            const float* params, const uint8_t* packed, size_t batch,
+                            size_t t_steps, const int64_t* targets, float* loss,
+                            double* acc, float* grads, uint8_t* spikes, float* vtrace,
+                            float* trace);
+
 int ref_forward_backward(const orc_net* n, const float* params,
                          const uint8_t* packed, size_t batch, size_t t_steps,
                          const int64_t* targets, float* loss, double* acc,
                          float* grads, uint8_t* spikes, float* vtrace,
                          float* trace) {
+  return ref_forward_backward_ex(n, nullptr, params, packed, batch, t_steps, targets,
+                                 loss, acc, grads, spikes, vtrace, trace);
+}
+
+int ref_forward_backward_ex(const orc_net* n, const orc_train_opts* opts,
+                            const float* params, const uint8_t* packed, size_t batch,
+                            size_t t_steps, const int64_t* targets, float* loss,
+                            double* acc, float* grads, uint8_t* spikes, float* vtrace,
+                            float* trace) {
   (void)vtrace;
   try {
     const NetworkSpec spec = make_spec(n);
@@ -166,7 +181,9 @@ int ref_forward_backward(const orc_net* n, const float* params,
       ids.push_back(e.trainable ? tape.leaf(e.tensor) : tape.constant(e.tensor));
     auto fwd = forward_taped(tape, spec, ids, tape.constant(std::move(x)),
                              std::size_t(n->unroll));
-    auto l = integral_crossentropy_taped(tape, fwd.trace, y);
+    auto l = (opts && opts->loss == 1)
+                 ? spike_rate_mse_taped(tape, fwd.trace, y, opts->rate_hi, opts->rate_lo)
+                 : integral_crossentropy_taped(tape, fwd.trace, y);
     *loss = tape.value(l)[0];
     *acc = integral_accuracy(tape.value(fwd.trace), y);
     if (trace)
@@ -232,17 +249,27 @@ namespace {
 
 TrainState<float> make_state(const orc_net* n, const float* params,
                              const float* m, const float* v, uint64_t step,
-                             float lr) {
+                             float lr, const orc_train_opts* opts = nullptr) {
   TrainState<float> st;
   st.spec = make_spec(n);
   st.cfg.unroll = std::size_t(n->unroll);
   st.cfg.lr = double(lr);
+  const OptimizerKind kind =
+      (opts && opts->optimizer == 1) ? OptimizerKind::Sgd : OptimizerKind::Adam;
+  if (opts) {
+    st.cfg.optimizer = kind;
+    st.cfg.momentum = double(opts->momentum);
+    st.cfg.loss = opts->loss == 1 ? LossKind::SpikeRateMse : LossKind::IntegralCrossentropy;
+    st.cfg.rate_hi = double(opts->rate_hi);
+    st.cfg.rate_lo = double(opts->rate_lo);
+  }
   st.params = params_from_flat(skeleton(n), params);
-  st.opt = init_optimizer(OptimizerKind::Adam, st.params);
+  st.opt = init_optimizer(kind, st.params);
   std::size_t off = 0;
   for (std::size_t i = 0; i < st.opt.m.size(); ++i) {
     std::memcpy(st.opt.m[i].data(), m + off, st.opt.m[i].size() * sizeof(float));
-    std::memcpy(st.opt.v[i].data(), v + off, st.opt.v[i].size() * sizeof(float));
+    if (i < st.opt.v.size())
+      std::memcpy(st.opt.v[i].data(), v + off, st.opt.v[i].size() * sizeof(float));
     off += st.opt.m[i].size();
   }
   st.opt.step = step;
@@ -255,7 +282,8 @@ void unload_state(const TrainState<float>& st, float* params, float* m,
   std::size_t off = 0;
   for (std::size_t i = 0; i < st.opt.m.size(); ++i) {
     std::memcpy(m + off, st.opt.m[i].data(), st.opt.m[i].size() * sizeof(float));
-    std::memcpy(v + off, st.opt.v[i].data(), st.opt.v[i].size() * sizeof(float));
+    if (i < st.opt.v.size())
+      std::memcpy(v + off, st.opt.v[i].data(), st.opt.v[i].size() * sizeof(float));
     off += st.opt.m[i].size();
   }
   *step = st.opt.step;
@@ -263,12 +291,25 @@ void unload_state(const TrainState<float>& st, float* params, float* m,
 
 }  // namespace
 
+int ref_train_step_ex(const orc_net* n, const orc_train_opts* opts, float* params,
+                      float* m, float* v, uint64_t* step, const uint8_t* packed,
+                      size_t batch, size_t t_steps, const int64_t* targets, float lr,
+                      float* loss, double* acc);
+
 int ref_train_step(const orc_net* n, float* params, float* m, float* v,
                    uint64_t* step, const uint8_t* packed, size_t batch,
                    size_t t_steps, const int64_t* targets, float lr,
                    float* loss, double* acc) {
+  return ref_train_step_ex(n, nullptr, params, m, v, step, packed, batch, t_steps,
+                           targets, lr, loss, acc);
+}
+
+int ref_train_step_ex(const orc_net* n, const orc_train_opts* opts, float* params,
+                      float* m, float* v, uint64_t* step, const uint8_t* packed,
+                      size_t batch, size_t t_steps, const int64_t* targets, float lr,
+                      float* loss, double* acc) {
   try {
-    TrainState<float> st = make_state(n, params, m, v, *step, lr);
+    TrainState<float> st = make_state(n, params, m, v, *step, lr, opts);
     Tensor<std::uint8_t> px(Shape{batch, (t_steps + 7) / 8, std::size_t(n->in)});
     std::memcpy(px.data(), packed, px.size());
     const std::vector<std::int64_t> y(targets, targets + batch);

@@ -259,11 +259,26 @@ static void matmul_rows(const float* a, size_t rows, size_t k, const float* w,
   }
 }
 
+static const orc_train_opts k_default_opts = {0, 0.9f, 0, 0.9f, 0.1f};
+
 int orc_forward_backward(const orc_net* net, const float* params,
                          const uint8_t* packed, size_t B, size_t T,
                          const int64_t* targets, float* loss_out,
                          double* acc_out, float* grads, uint8_t* spikes_out,
                          float* vtrace_out, float* trace_out) {
+  return orc_forward_backward_ex(net, NULL, params, packed, B, T, targets, loss_out,
+                                 acc_out, grads, spikes_out, vtrace_out, trace_out);
+}
+
+int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
+                            const float* params, const uint8_t* packed, size_t B,
+                            size_t T, const int64_t* targets, float* loss_out,
+                            double* acc_out, float* grads, uint8_t* spikes_out,
+                            float* vtrace_out, float* trace_out) {
+  if (!opts) opts = &k_default_opts;
+  if (opts->loss == 1 && (opts->rate_hi < 0.0f || opts->rate_hi > 1.0f ||
+                          opts->rate_lo < 0.0f || opts->rate_lo > 1.0f))
+    return 3; /* spike_rate_mse: rates must lie in [0,1] (objective.hpp:144-145) */
   const int L = net->n_hidden;
   const size_t C = (size_t)net->classes;
   if (B == 0 || T == 0 || L < 1 || L > ORC_MAX_HIDDEN || net->unroll < 1)
@@ -358,30 +373,53 @@ int orc_forward_backward(const orc_net* net, const float* params,
     float z = 0.0f;
     for (size_t j = 0; j < C; ++j) z += expf(row[j] - m);
     const float lse = m + logf(z);
-    loss += lse - row[(size_t)targets[b]];
+    if (opts->loss == 0) loss += lse - row[(size_t)targets[b]];
     for (size_t j = 0; j < C; ++j) probs[b * C + j] = expf(row[j] - m) / z;
     size_t best = 0;
     for (size_t j = 1; j < C; ++j)
       if (row[j] > row[best]) best = j;
     if (best == (size_t)targets[b]) ++hits;
   }
-  *loss_out = loss / (float)B;
+  if (opts->loss == 1) {
+    /* spike_rate_mse (objective.hpp:139-158): one running sum over (b, j) */
+    for (size_t b = 0; b < B; ++b)
+      for (size_t j = 0; j < C; ++j) {
+        const float r = logits[b * C + j] / (float)T;
+        const float target = (size_t)targets[b] == j ? opts->rate_hi : opts->rate_lo;
+        const float d = r - target;
+        loss += d * d;
+      }
+    *loss_out = loss / (float)(B * C);
+  } else {
+    *loss_out = loss / (float)B;
+  }
   *acc_out = (double)hits / (double)B;
 
   if (grads) {
     memset(grads, 0, orc_param_count(net) * sizeof(float));
     const size_t U = (size_t)net->unroll;
     const size_t nblk = (T + U - 1) / U;
-    /* CE backward: d = (p - onehot) * (1/B) on every timestep. */
-    const float gs = 1.0f / (float)B;
     float* delta = (float*)malloc(B * C * sizeof(float));
-    for (size_t b = 0; b < B; ++b)
-      for (size_t c = 0; c < C; ++c) {
-        float d = probs[b * C + c];
-        if ((size_t)targets[b] == c) d -= 1.0f;
-        d *= gs;
-        delta[b * C + c] = d;
-      }
+    if (opts->loss == 1) {
+      /* rate-MSE backward (objective.hpp:170-181): gs*(r - target) on every step */
+      const float gs = 1.0f * 2.0f / ((float)(B * C) * (float)T);
+      for (size_t b = 0; b < B; ++b)
+        for (size_t c = 0; c < C; ++c) {
+          const float r = logits[b * C + c] / (float)T;
+          const float target = (size_t)targets[b] == c ? opts->rate_hi : opts->rate_lo;
+          delta[b * C + c] = gs * (r - target);
+        }
+    } else {
+      /* CE backward: d = (p - onehot) * (1/B) on every timestep. */
+      const float gs = 1.0f / (float)B;
+      for (size_t b = 0; b < B; ++b)
+        for (size_t c = 0; c < C; ++c) {
+          float d = probs[b * C + c];
+          if ((size_t)targets[b] == c) d -= 1.0f;
+          d *= gs;
+          delta[b * C + c] = d;
+        }
+    }
     /* LI reverse scan: Gout_t = delta + Gout_{t+1}*bc; dI = Gout. */
     float* dI = (float*)malloc(M * C * sizeof(float));
     {
@@ -523,15 +561,37 @@ void orc_adam(float* p, const float* g, float* m, float* v, size_t n,
   }
 }
 
+/* sgd_update (optimize.hpp:69-84). */
+void orc_sgd(float* p, const float* g, float* m, size_t n, uint64_t* step,
+             float lr, float momentum) {
+  *step += 1;
+  for (size_t k = 0; k < n; ++k) {
+    m[k] = momentum * m[k] + g[k];
+    p[k] -= lr * m[k];
+  }
+}
+
 int orc_train_step(const orc_net* net, float* params, float* m, float* v,
                    uint64_t* step, const uint8_t* packed, size_t batch,
                    size_t t_steps, const int64_t* targets, float lr,
                    float* loss, double* acc) {
+  return orc_train_step_ex(net, NULL, params, m, v, step, packed, batch, t_steps,
+                           targets, lr, loss, acc);
+}
+
+int orc_train_step_ex(const orc_net* net, const orc_train_opts* opts,
+                      float* params, float* m, float* v, uint64_t* step,
+                      const uint8_t* packed, size_t batch, size_t t_steps,
+                      const int64_t* targets, float lr, float* loss, double* acc) {
+  if (!opts) opts = &k_default_opts;
   const size_t np = orc_param_count(net);
   float* g = (float*)malloc(np * sizeof(float));
-  const int rc = orc_forward_backward(net, params, packed, batch, t_steps,
-                                      targets, loss, acc, g, NULL, NULL, NULL);
-  if (rc == 0) orc_adam(params, g, m, v, np, step, lr, 0.9f, 0.999f, 1e-8f);
+  const int rc = orc_forward_backward_ex(net, opts, params, packed, batch, t_steps,
+                                         targets, loss, acc, g, NULL, NULL, NULL);
+  if (rc == 0) {
+    if (opts->optimizer == 1) orc_sgd(params, g, m, np, step, lr, opts->momentum);
+    else orc_adam(params, g, m, v, np, step, lr, 0.9f, 0.999f, 1e-8f);
+  }
   free(g);
   return rc;
 }

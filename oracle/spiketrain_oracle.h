@@ -100,6 +100,29 @@ int orc_forward_backward(const orc_net* net, const float* params,
                          float* grads, uint8_t* spikes, float* vtrace,
                          float* trace);
 
+/* TrainConfig options on the same path (optimize.hpp:113-131), all off by default. */
+typedef struct orc_train_opts {
+  int optimizer;   /* 0 Adam (optimize.hpp:86-111), 1 SGD + momentum (:69-84)       */
+  float momentum;  /* SGD momentum (TrainConfig.momentum, default 0.9)              */
+  int loss;        /* 0 integral CE (objective.hpp:88-114), 1 spike-rate MSE (:139-183) */
+  float rate_hi;   /* rate-MSE target on the true class (default 0.9)               */
+  float rate_lo;   /* rate-MSE target elsewhere (default 0.1)                       */
+} orc_train_opts;
+
+/* forward_backward / train_step with TrainConfig options (NULL = defaults). */
+int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
+                            const float* params, const uint8_t* packed,
+                            size_t batch, size_t t_steps, const int64_t* targets,
+                            float* loss, double* acc, float* grads,
+                            uint8_t* spikes, float* vtrace, float* trace);
+int orc_train_step_ex(const orc_net* net, const orc_train_opts* opts,
+                      float* params, float* m, float* v, uint64_t* step,
+                      const uint8_t* packed, size_t batch, size_t t_steps,
+                      const int64_t* targets, float lr, float* loss, double* acc);
+/* sgd_update over a flat buffer (optimize.hpp:69-84): m doubles as momentum. */
+void orc_sgd(float* p, const float* g, float* m, size_t n, uint64_t* step,
+             float lr, float momentum);
+
 /* adam_update over a flat buffer (optimize.hpp:86-111); *step is the
  * optimizer step counter, incremented here before the bias correction. */
 void orc_adam(float* p, const float* g, float* m, float* v, size_t n,

@@ -200,6 +200,7 @@ struct snn_engine {
   DevBuf<__nv_bfloat16> di[kMaxLayers];  // per Linear j: dI of its output
   DevBuf<float> dbeta[kMaxLayers], dbias[kMaxLayers];
   DevBuf<float> loss_b;
+  DevBuf<float> loss_terms;  // rate-MSE: [B][C] squared rate gaps
   DevBuf<int32_t> correct_b;
   DevBuf<float> partial[kMaxLayers];
   DevBuf<int32_t> vec_index;
@@ -290,6 +291,11 @@ struct snn_engine {
     if (cfg.batch_size < 1) fail(SNN_ERR_ARGUMENT, "train: batch size 0");
     if (cfg.time_steps < 1) fail(SNN_ERR_ARGUMENT, "apply: zero timesteps");
     if (cfg.unroll < 1) fail(SNN_ERR_ARGUMENT, "apply: unroll must be >= 1");
+    if (cfg.optimizer != 0 && cfg.optimizer != 1) fail(SNN_ERR_ARGUMENT, "train_step: unknown optimizer");
+    if (cfg.loss != 0 && cfg.loss != 1) fail(SNN_ERR_ARGUMENT, "train_step: unknown loss kind");
+    if (cfg.loss == 1 && !(cfg.rate_hi >= 0.0f && cfg.rate_hi <= 1.0f && cfg.rate_lo >= 0.0f &&
+                           cfg.rate_lo <= 1.0f))
+      fail(SNN_ERR_ARGUMENT, "spike_rate_mse: rates must lie in [0,1]");
     B = cfg.batch_size;
     T = cfg.time_steps;
     TT = T <= 64 ? 64 : 128;
@@ -415,6 +421,7 @@ struct snn_engine {
       partial[j].alloc(size_t(splits_w[j]) * M_pad_w[j] * N_pad[j], false);
     }
     loss_b.alloc(B);
+    if (cfg.loss == 1) loss_terms.alloc(size_t(B) * C);
     correct_b.alloc(B);
     result_loss.alloc(1);
     result_acc.alloc(1);
@@ -538,6 +545,10 @@ struct snn_engine {
     a.omb2 = 1.0f - cfg.beta2;
     a.update = update;
     a.B_global = B_global();
+    // StepResult.loss = numerator / (B) for CE, / T(b * c) for rate-MSE (objective.hpp:158)
+    a.loss_denom = cfg.loss == 1 ? float(int64_t(B_global()) * C) : float(B_global());
+    a.opt_kind = cfg.optimizer;
+    a.momentum = cfg.momentum;
     a.loss_out = result_loss.p;
     a.acc_out = result_acc.p;
     return a;
@@ -730,6 +741,12 @@ struct snn_engine {
       r.exp_mode = exp_mode;
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
       r.inv_b = 1.0f / float(B_global());
+      r.loss_kind = cfg.loss;
+      r.rate_hi = cfg.rate_hi;
+      r.rate_lo = cfg.rate_lo;
+      // gs = g * T(2) / (T(b * c) * T(t)) with g = 1 (objective.hpp:172), in float
+      r.mse_gs = 1.0f * 2.0f / (float(int64_t(B_global()) * C) * float(T));
+      r.loss_terms = cfg.loss == 1 ? loss_terms.p : nullptr;
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
       launch(k_readout, dim3(B), dim3(kRoThreads), smem, r);
       mark(evs, "readout", -1);
@@ -800,6 +817,8 @@ struct snn_engine {
       r.step = step.p;
       r.update = update;
       r.B = B;
+      r.loss_terms = cfg.loss == 1 ? loss_terms.p : nullptr;
+      r.n_loss_terms = cfg.loss == 1 ? B * C : B;
       r.w_blocks = int((n_params + kRedElemsPerBlock - 1) / kRedElemsPerBlock);
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
       if (update && world == 1) {
@@ -827,7 +846,8 @@ struct snn_engine {
       launch(k_adam, dim3(unsigned((n_params + 255) / 256)), dim3(256), 0, a);
       mark(evs, "adam", -1);
     } else {
-      launch(k_result, dim3(1), dim3(32), 0, (const float*)(comm.p + n_params), B_global(), step.p,
+      launch(k_result, dim3(1), dim3(32), 0, (const float*)(comm.p + n_params), B_global(),
+             cfg.loss == 1 ? float(int64_t(B_global()) * C) : float(B_global()), step.p,
              0, result_loss.p, result_acc.p);
       mark(evs, "result", -1);
     }

@@ -574,6 +574,10 @@ struct ReadoutArgs {
   int exp_mode;             // 0: exp/log evaluated in fp64 then rounded; 1: expf/logf
   int B, T, T_pad, HL, HL_pad, C;
   float inv_b;              // 1/B_global (objective.hpp:104)
+  int loss_kind;            // 0 integral CE, 1 spike-rate MSE (objective.hpp:139-183)
+  float rate_hi, rate_lo;   // rate-MSE targets
+  float mse_gs;             // 2 / (float(B_global*C) * float(T)) (objective.hpp:172)
+  float* loss_terms;        // rate-MSE: [B][C] squared rate gaps (summed in order by the tail)
 };
 
 __device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
@@ -722,7 +726,7 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     for (int j = 1; j < kMaxClasses; ++j)
       if (j < C) mx = (mx < lg[j]) ? lg[j] : mx;
     const float xd = __fsub_rn(logit, mx);
-    const float ex = lane < C ? (a.exp_mode ? expf(xd) : exp_cr(xd)) : 0.0f;
+    const float ex = (lane < C && a.loss_kind == 0) ? (a.exp_mode ? expf(xd) : exp_cr(xd)) : 0.0f;
 #pragma unroll
     for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, ex, j);
     float z = 0.0f;
@@ -744,14 +748,24 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
       }
     }
     if (lane == 0) {
-      a.loss_b[b] = __fsub_rn(__fadd_rn(mx, a.exp_mode ? logf(z) : log_cr(z)), logit_y);
+      if (a.loss_kind == 0)
+        a.loss_b[b] = __fsub_rn(__fadd_rn(mx, a.exp_mode ? logf(z) : log_cr(z)), logit_y);
       a.correct_b[b] = (bi == y) ? 1 : 0;
     }
     float delta = 0.0f;
     if (lane < C) {
-      float d = __fdiv_rn(ex, z);
-      if (lane == y) d = __fsub_rn(d, 1.0f);
-      delta = __fmul_rn(d, a.inv_b);
+      if (a.loss_kind == 1) {
+        // spike_rate_mse (objective.hpp:139-183): r = counts / T, d = r - target;
+        // the loss term d*d and the cotangent gs*d on every step
+        const float r = __fdiv_rn(logit, float(T));
+        const float d = __fsub_rn(r, lane == y ? a.rate_hi : a.rate_lo);
+        a.loss_terms[size_t(b) * C + lane] = __fmul_rn(d, d);
+        delta = __fmul_rn(a.mse_gs, d);
+      } else {
+        float d = __fdiv_rn(ex, z);
+        if (lane == y) d = __fsub_rn(d, 1.0f);
+        delta = __fmul_rn(d, a.inv_b);
+      }
     }
     if (a.dbg_trace != nullptr && lane < C) {
       for (int s = 0; s < T; ++s)
@@ -1512,8 +1526,10 @@ struct ReduceArgs {
   int n_vec;
   const float* params;                  // for the clip mask
   float* grads;                         // [n_params] then loss sum, hits
-  const float* loss_b;                  // [B]
+  const float* loss_b;                  // [B] (integral CE: one term per sample)
   const int32_t* correct_b;             // [B]
+  const float* loss_terms;              // rate-MSE: [B][C] terms, else nullptr
+  int n_loss_terms;                     // B (CE) or B*C (rate-MSE), summed in order
   int64_t* step;
   int update;
   int B;
@@ -1564,6 +1580,35 @@ __device__ __forceinline__ float sum_partials_pair(const ReduceArgs& r, const En
 }
 constexpr int kRedElemsPerBlock = 128;  // W elements per 256-thread block (lane pairs)
 
+// Loss numerator in the reference order -- one running float sum over the
+// per-sample CE terms (objective.hpp:57-72) or the per-(sample, class) rate-MSE
+// terms (objective.hpp:150-157) -- and the hit count.  Whole block calls; thread
+// 0 holds the results.
+__device__ __forceinline__ void loss_and_hits(const ReduceArgs& r, float& loss, int& hits) {
+  __shared__ float sl[1024];
+  __shared__ int sc[1024];
+  const int tid = threadIdx.x;
+  const float* terms = r.loss_terms != nullptr ? r.loss_terms : r.loss_b;
+  loss = 0.0f;
+  hits = 0;
+  for (int b0 = 0; b0 < r.n_loss_terms; b0 += 1024) {
+    const int nb = min(1024, r.n_loss_terms - b0);
+    __syncthreads();
+    for (int i = tid; i < nb; i += blockDim.x) sl[i] = terms[b0 + i];
+    __syncthreads();
+    if (tid == 0)
+      for (int i = 0; i < nb; ++i) loss = __fadd_rn(loss, sl[i]);
+  }
+  for (int b0 = 0; b0 < r.B; b0 += 1024) {
+    const int nb = min(1024, r.B - b0);
+    __syncthreads();
+    for (int i = tid; i < nb; i += blockDim.x) sc[i] = r.correct_b[b0 + i];
+    __syncthreads();
+    if (tid == 0)
+      for (int i = 0; i < nb; ++i) hits += sc[i];
+  }
+}
+
 // Blocks [0, w_blocks): one pair of lanes per flat index, W entries only --
 // fixed-order sum of the split-K partials (sum_partials_pair).  Next blocks: one warp per beta/bias element --
 // lanes take strided samples, then a fixed-shape tree (deterministic).  Last
@@ -1605,24 +1650,9 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     return;
   }
   // loss / hits / step
-  __shared__ float sl[1024];
-  __shared__ int sc[1024];
-  float loss = 0.0f;
-  int hits = 0;
-  for (int b0 = 0; b0 < a.B; b0 += 1024) {
-    const int nb = min(1024, a.B - b0);
-    __syncthreads();
-    for (int i = tid; i < nb; i += 256) {
-      sl[i] = a.loss_b[b0 + i];
-      sc[i] = a.correct_b[b0 + i];
-    }
-    __syncthreads();
-    if (tid == 0)
-      for (int i = 0; i < nb; ++i) {
-        loss = __fadd_rn(loss, sl[i]);
-        hits += sc[i];
-      }
-  }
+  float loss;
+  int hits;
+  loss_and_hits(a, loss, hits);
   if (tid == 0) {
     a.grads[a.n_params] = loss;
     a.grads[a.n_params + 1] = float(hits);
@@ -1652,12 +1682,23 @@ struct AdamArgs {
   float* loss_out;
   double* acc_out;
   int64_t* rows_slot;        // schedule mode: advanced once per update (else nullptr)
+  float loss_denom;          // float(B_global) (CE) or float(B_global * C) (rate-MSE)
+  int opt_kind;              // 0 Adam, 1 SGD + momentum (optimize.hpp:69-84)
+  float momentum;
 };
 
 // Adam on one flat parameter (optimize.hpp:88-110); bias corrections of step s+1.
 // p0 / m0 / v0: the current parameter and moments (loaded by the caller, early).
 __device__ __forceinline__ float adam_apply(const AdamArgs& a, int64_t i, float g, float p0, float m0,
                                             float v0, float bc1, float bc2) {
+  if (a.opt_kind == 1) {
+    // sgd_update (optimize.hpp:69-84): m doubles as the momentum buffer
+    const float m = __fadd_rn(__fmul_rn(a.momentum, m0), g);
+    const float p = __fsub_rn(p0, __fmul_rn(a.lr, m));
+    a.m[i] = m;
+    a.params[i] = p;
+    return p;
+  }
   float p = p0;
   const float m = __fadd_rn(__fmul_rn(a.b1, m0), __fmul_rn(a.omb1, g));
   const float v = __fadd_rn(__fmul_rn(a.b2, v0), __fmul_rn(__fmul_rn(a.omb2, g), g));
@@ -1691,7 +1732,7 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a.update && i == 0) {
     // StepResult{loss, accuracy} (optimize.hpp:143-147, :193-196)
-    *a.loss_out = __fdiv_rn(a.grads[a.n_params], float(a.B_global));
+    *a.loss_out = __fdiv_rn(a.grads[a.n_params], a.loss_denom);
     *a.acc_out = double(a.grads[a.n_params + 1]) / double(a.B_global);
     if (a.rows_slot != nullptr) *a.rows_slot += 1;
   }
@@ -1767,28 +1808,13 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
     }
   } else {
     // loss sum in batch order (objective.hpp:57-72) + hits -> StepResult
-    __shared__ float sl[1024];
-    __shared__ int sc[1024];
-    float loss = 0.0f;
-    int hits = 0;
-    for (int b0 = 0; b0 < r.B; b0 += 1024) {
-      const int nb = min(1024, r.B - b0);
-      __syncthreads();
-      for (int i = tid; i < nb; i += 256) {
-        sl[i] = r.loss_b[b0 + i];
-        sc[i] = r.correct_b[b0 + i];
-      }
-      __syncthreads();
-      if (tid == 0)
-        for (int i = 0; i < nb; ++i) {
-          loss = __fadd_rn(loss, sl[i]);
-          hits += sc[i];
-        }
-    }
+    float loss;
+    int hits;
+    loss_and_hits(r, loss, hits);
     if (tid == 0) {
       r.grads[r.n_params] = loss;
       r.grads[r.n_params + 1] = float(hits);
-      *a.loss_out = __fdiv_rn(loss, float(a.B_global));
+      *a.loss_out = __fdiv_rn(loss, a.loss_denom);
       *a.acc_out = double(hits) / double(a.B_global);
     }
   }
@@ -1856,11 +1882,11 @@ __global__ void k_synth(SynthArgs a) {
 }
 
 // StepResult{loss / B_global, hits / B_global}; advances the step counter.
-__global__ void k_result(const float* tail, int B_global, int64_t* step, int do_step,
-                         float* loss_out, double* acc_out) {
+__global__ void k_result(const float* tail, int B_global, float loss_denom, int64_t* step,
+                         int do_step, float* loss_out, double* acc_out) {
   pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  *loss_out = __fdiv_rn(tail[0], float(B_global));
+  *loss_out = __fdiv_rn(tail[0], loss_denom);
   *acc_out = double(tail[1]) / double(B_global);
   if (do_step) *step += 1;
 }

@@ -93,6 +93,11 @@ class TrainConfig:
     beta1: float = 0.9
     beta2: float = 0.999
     eps: float = 1e-8
+    optimizer: str = "adam"              # OptimizerKind: "adam" | "sgd" (optimize.hpp:22)
+    momentum: float = 0.9                # SGD only
+    loss: str = "integral_crossentropy"  # LossKind: | "spike_rate_mse" (optimize.hpp:23)
+    rate_hi: float = 0.9                 # rate-MSE targets
+    rate_lo: float = 0.1
 
 
 class _NetDesc(C.Structure):
@@ -104,7 +109,9 @@ class _NetDesc(C.Structure):
 class _TrainCfg(C.Structure):
     _fields_ = [("batch_size", C.c_int32), ("time_steps", C.c_int32), ("lr", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("seed", C.c_uint64), ("unroll", C.c_int32)]
+                ("seed", C.c_uint64), ("unroll", C.c_int32), ("optimizer", C.c_int32),
+                ("momentum", C.c_float), ("loss", C.c_int32), ("rate_hi", C.c_float),
+                ("rate_lo", C.c_float)]
 
 
 def normalize(spec: NetworkSpec) -> dict:
@@ -226,6 +233,14 @@ class Engine:
         c.beta1, c.beta2, c.eps = float(cfg.beta1), float(cfg.beta2), float(cfg.eps)
         c.seed = int(cfg.seed)
         c.unroll = int(cfg.unroll)
+        if cfg.optimizer not in ("adam", "sgd"):
+            raise ArgumentError(f"train_step: unknown optimizer {cfg.optimizer!r}")
+        if cfg.loss not in ("integral_crossentropy", "spike_rate_mse"):
+            raise ArgumentError(f"train_step: unknown loss kind {cfg.loss!r}")
+        c.optimizer = 1 if cfg.optimizer == "sgd" else 0
+        c.momentum = float(cfg.momentum)
+        c.loss = 1 if cfg.loss == "spike_rate_mse" else 0
+        c.rate_hi, c.rate_lo = float(cfg.rate_hi), float(cfg.rate_lo)
         self._L = lib()
         h = C.c_void_p()
         self._h = None

@@ -94,6 +94,31 @@ def rng_kats(ref: Lib):
     np.savez_compressed(os.path.join(GOLD, "rng.npz"), **vals)
 
 
+OPTS_NET = Net(inp=40, hidden=(24, 20), classes=6, act="superspike", unroll=7)
+OPTS = {"rate_mse": dict(loss="rate_mse", rate_hi=0.8, rate_lo=0.05),
+        "sgd": dict(optimizer="sgd", momentum=0.8)}
+
+
+def opts_fixture(ref: Lib):
+    """TrainConfig options on the step: spike-rate MSE loss (objective.hpp:139-183)
+    and SGD with momentum (optimize.hpp:69-84), 3 train_steps each."""
+    from oracle.pyoracle import Opts
+    key = ref.key_child(ref.key_from_seed(21), 0)
+    p = ref.init(OPTS_NET, key) * np.float32(3.0)
+    x, y = ref.synth_raster(6, 7, 30, 40, 13)
+    pk = ref.pack_time(x)
+    vals = dict(params=p, packed=pk, y=y, t=30, **net_dict(OPTS_NET))
+    for name, kw in OPTS.items():
+        o = Opts(**kw)
+        fb = ref.forward_backward(OPTS_NET, p, pk, 30, y, opts=o)
+        st = State(p.copy())
+        losses = [ref.train_step(OPTS_NET, st, pk, 30, y, opts=o)[0] for _ in range(3)]
+        vals.update({f"{name}_loss": np.float32(fb["loss"]), f"{name}_grads": fb["grads"],
+                     f"{name}_step_losses": np.array(losses, np.float32),
+                     f"{name}_params3": st.params, f"{name}_m3": st.m, f"{name}_v3": st.v})
+    np.savez_compressed(os.path.join(GOLD, "opts.npz"), **vals)
+
+
 if __name__ == "__main__":
     if not have_ref():
         Lib.__init__  # noqa: B018
@@ -103,7 +128,13 @@ if __name__ == "__main__":
         sys.exit("oracle/_ref not buildable here (no /root/reference)")
     os.makedirs(GOLD, exist_ok=True)
     ref = Lib("ref")
-    rng_kats(ref)
-    tiny(ref)
-    c1(ref)
+    only = sys.argv[1] if len(sys.argv) > 1 else None  # e.g. "opts": one fixture
+    if only in (None, "rng"):
+        rng_kats(ref)
+    if only in (None, "tiny"):
+        tiny(ref)
+    if only in (None, "c1"):
+        c1(ref)
+    if only in (None, "opts"):
+        opts_fixture(ref)
     print("golden fixtures written to", GOLD)

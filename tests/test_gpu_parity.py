@@ -358,3 +358,67 @@ def test_evaluate_matches_cmd_eval(orc):
         accs[B] = acc
     assert accs[24] == accs[5]
     assert 0.0 <= accs[24] <= 1.0
+
+
+OPTION_CASES = [
+    ("rate_mse", dict(loss="spike_rate_mse", rate_hi=0.8, rate_lo=0.05)),
+    ("sgd", dict(optimizer="sgd", momentum=0.8)),
+    ("sgd+rate_mse", dict(optimizer="sgd", momentum=0.5, loss="spike_rate_mse", rate_hi=0.7,
+                          rate_lo=0.2)),
+]
+
+
+@pytest.mark.parametrize("case", OPTION_CASES, ids=[c[0] for c in OPTION_CASES])
+def test_step_options_match_oracle(orc, case):
+    """TrainConfig options on the step: spike-rate MSE (objective.hpp:139-183) and
+    SGD + momentum (optimize.hpp:69-84), against the oracle (pinned to the reference
+    by tests/golden/opts.npz)."""
+    from oracle.pyoracle import Opts
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    name, kw = case
+    o = Opts(optimizer=kw.get("optimizer", "adam"), momentum=kw.get("momentum", 0.9),
+             loss="rate_mse" if kw.get("loss") == "spike_rate_mse" else "ce",
+             rate_hi=kw.get("rate_hi", 0.9), rate_lo=kw.get("rate_lo", 0.1))
+    net = Net(inp=40, hidden=(24, 20), classes=6, act="superspike")
+    B, T = 5, 30
+    params = orc.init(net, orc.key_child(orc.key_from_seed(8), 0)) * np.float32(3.0)
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 4)
+    pk = orc.pack_time(x)
+    eng = Engine(shd_spec(hidden=net.hidden, classes=net.classes, inp=net.inp, act=net.act),
+                 TrainConfig(batch_size=B, **kw), T)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    rows = np.arange(B, dtype=np.uint32)
+    loss, acc = eng.forward_backward(rows)
+    ref = orc.forward_backward(net, params, pk, T, y, opts=o)
+    assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"]) and acc == ref["acc"]
+    check_grads(orc, net, eng.get_grads(), ref["grads"])
+    st = State(params.copy())
+    for _ in range(3):
+        lo, ao = orc.train_step(net, st, pk, T, y, opts=o)
+        l2, a2 = eng.train_step(rows)
+        assert abs(l2 - lo) <= REL_TOL * abs(lo) and a2 == ao
+    m, v, step = eng.get_opt_state()
+    assert step == 3
+    if o.optimizer == "sgd":
+        # p -= lr * m is linear in the gradient: the accumulated update carries the
+        # gradient tolerance (1e-4 per step, 3 steps)
+        assert relnorm(eng.get_params() - params, st.params - params) <= 1e-3
+        assert relnorm(m, st.m) <= 1e-3 and not v.any()
+    else:
+        assert relnorm(eng.get_params(), st.params) <= 1e-4
+
+
+def test_rate_mse_golden_loss_bit_exact(golden):
+    """Rate-MSE loss on the reference-made fixture: logits are bit-exact and the
+    (b, c) terms are summed in the reference's single running order."""
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    g = golden("opts")
+    hidden = tuple(int(h) for h in g["hidden"])
+    T, B = int(g["t"]), int(g["y"].size)
+    eng = Engine(shd_spec(hidden=hidden, classes=int(g["classes"]), inp=int(g["inp"]), act=str(g["act"])),
+                 TrainConfig(batch_size=B, loss="spike_rate_mse", rate_hi=0.8, rate_lo=0.05), T)
+    eng.stage_dataset(g["packed"], g["y"])
+    eng.set_params(g["params"])
+    loss, _ = eng.forward_backward(np.arange(B, dtype=np.uint32))
+    assert np.float32(loss) == g["rate_mse_loss"]

@@ -8,6 +8,8 @@
 * when oracle/_ref is present (this container), randomized configurations are
   compared live against the reference.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -183,3 +185,51 @@ def test_oracle_vs_reference_live(orc, cfg):
     m1 = orc.train_epochs(net, s1, pk, y, T, 3, 2, 5)
     m2 = ref.train_epochs(net, s2, pk, y, T, 3, 2, 5)
     assert np.array_equal(m1, m2) and np.array_equal(s1.params, s2.params)
+
+
+def _opts_case():
+    from oracle.pyoracle import Opts
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "opts.npz"))
+    net = Net(inp=int(g["inp"]), hidden=tuple(int(h) for h in g["hidden"]), classes=int(g["classes"]),
+              bias=bool(g["bias"]), threshold=float(g["threshold"]), act=str(g["act"]),
+              unroll=int(g["unroll"]))
+    opts = {"rate_mse": Opts(loss="rate_mse", rate_hi=0.8, rate_lo=0.05),
+            "sgd": Opts(optimizer="sgd", momentum=0.8)}
+    return g, net, opts
+
+
+@pytest.mark.parametrize("name", ["rate_mse", "sgd"])
+def test_opts_golden_bit_exact(orc, name):
+    """Spike-rate MSE loss (objective.hpp:139-183) and SGD + momentum
+    (optimize.hpp:69-84): the C restatement equals fixtures made by the reference."""
+    g, net, opts = _opts_case()
+    o, T = opts[name], int(g["t"])
+    fb = orc.forward_backward(net, g["params"], g["packed"], T, g["y"], opts=o)
+    assert fb["loss"] == g[f"{name}_loss"]
+    assert np.array_equal(fb["grads"], g[f"{name}_grads"])
+    st = State(g["params"].copy())
+    losses = [orc.train_step(net, st, g["packed"], T, g["y"], opts=o)[0] for _ in range(3)]
+    assert np.array_equal(np.array(losses, np.float32), g[f"{name}_step_losses"])
+    assert np.array_equal(st.params, g[f"{name}_params3"])
+    assert np.array_equal(st.m, g[f"{name}_m3"]) and np.array_equal(st.v, g[f"{name}_v3"])
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref needs /root/reference")
+@pytest.mark.parametrize("cfg", range(3))
+def test_opts_vs_reference_live(orc, cfg):
+    from oracle.pyoracle import Opts
+    net = CONFIGS[cfg]
+    ref = Lib("ref")
+    p = orc.init(net, orc.key_from_seed(300 + cfg)) * np.float32(3.0)
+    B, T = 6, 21
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 31 + cfg)
+    pk = orc.pack_time(x)
+    for o in (Opts(loss="rate_mse", rate_hi=0.7, rate_lo=0.2), Opts(optimizer="sgd", momentum=0.5),
+              Opts(optimizer="sgd", loss="rate_mse")):
+        a = orc.forward_backward(net, p, pk, T, y, opts=o)
+        b = ref.forward_backward(net, p, pk, T, y, opts=o)
+        assert a["loss"] == b["loss"] and np.array_equal(a["grads"], b["grads"])
+        s1, s2 = State(p.copy()), State(p.copy())
+        for _ in range(2):
+            assert orc.train_step(net, s1, pk, T, y, opts=o) == ref.train_step(net, s2, pk, T, y, opts=o)
+        assert np.array_equal(s1.params, s2.params) and np.array_equal(s1.m, s2.m)
