@@ -377,8 +377,9 @@ def main():
             "config": config, "clocks": clocks.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "path": "snn_train_step_packed: host packed batch -> pinned -> H2D, graph, "
-                            "D2H loss/acc, sync every step"},
+                    "path": "snn_train_step_packed: host packed batch (reference layout) -> "
+                            "pinned (parallel copy, chunks pipelined with their DMA) -> H2D -> "
+                            "device re-layout, step graph, D2H loss/acc, sync every step"},
             "gpu_launches": eng.launches_per_step * args.steps,
             "roofline": roofline,
             "kernels": [{"name": k["name"], "ms": round(k["ms"], 5)} for k in kernels],

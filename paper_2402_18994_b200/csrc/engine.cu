@@ -13,7 +13,12 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -163,6 +168,82 @@ struct Dataset {
   size_t n = 0;
 };
 
+// Host memcpy split over a few persistent worker threads (the caller takes part).
+// A host batch (e.g. 2.87 MB at C1) is copied into pinned memory at several times
+// one core's memcpy rate; the engine pipelines the chunks with their DMA.  Workers
+// spin on an atomic job counter for ~2 ms after each job (steps arrive every few
+// hundred us while training) and sleep on a condition variable otherwise.
+class CopyPool {
+ public:
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_.store(true);
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    dst_ = static_cast<uint8_t*>(dst);
+    src_ = static_cast<const uint8_t*>(src);
+    bytes_ = bytes;
+    pending_.store(int(th_.size()), std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> lk(mu_);  // orders the job fields before the counter
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    if (sleepers_.load() > 0) cv_.notify_all();
+    part(0);
+    while (pending_.load(std::memory_order_acquire) > 0) cpu_relax();
+  }
+
+ private:
+  static void cpu_relax() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  void part(int i) {
+    const size_t parts = th_.size() + 1;
+    const size_t per = ((bytes_ + parts - 1) / parts + 63) & ~size_t(63);
+    const size_t lo = std::min(bytes_, per * size_t(i)), hi = std::min(bytes_, lo + per);
+    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void run(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      // spin ~2 ms for the next job, then sleep
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int k = 0; gen_.load(std::memory_order_acquire) == seen && !stop_.load(); ++k) {
+        cpu_relax();
+        if ((k & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+          std::unique_lock<std::mutex> lk(mu_);
+          sleepers_.fetch_add(1);
+          cv_.wait(lk, [&] { return stop_.load() || gen_.load() != seen; });
+          sleepers_.fetch_sub(1);
+          break;
+        }
+      }
+      if (stop_.load()) return;
+      seen = gen_.load(std::memory_order_acquire);
+      part(i + 1);
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t bytes_ = 0;
+  std::atomic<int> pending_{0}, sleepers_{0};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<bool> stop_{false};
+};
+
 }  // namespace
 
 struct snn_engine {
@@ -237,6 +318,7 @@ struct snn_engine {
   int fwd_stages = std::min(kFwdStagesMax, env_int("SNN_FWD_STAGES", 2));
   int fwd_spb_env = env_int("SNN_FWD_SPB", 2);
   int fwd_fuse = env_int("SNN_FWD_FUSE", 2) - 1;  // 1: one launch per hidden layer
+  int copy_chunks = env_int("SNN_COPY_CHUNKS", 4);  // host batch: copy / DMA pipeline depth
   // samples per forward CTA: N = spb * TT <= 256 and TMEM (doubled for NT > 1) <= 512
   int fwd_spb(int tt) const { return std::max(1, std::min(fwd_spb_env, std::min(kFwdSpbMax, 256 / tt))); }
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
@@ -598,6 +680,55 @@ struct snn_engine {
     CK(cudaMemcpyAsync(ds.x.p, h, bytes, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(ds.labels.p, lab, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
     if (sync_after_stage) CK(cudaStreamSynchronize(stream));
+  }
+
+  // A host batch in the reference layout [n][ceil(T/8)][IN] (train_step_packed):
+  // copied verbatim into pinned memory by the copy pool in chunks whose DMA
+  // overlaps the next chunk's copy, then re-laid into [n][T_pad/8][IN_pad] on the
+  // device (k_relayout) -- no host memset or per-row copies.
+  std::unique_ptr<CopyPool> copy_pool;
+  DevBuf<uint8_t> raw_in;
+  void stage_batch(Dataset& ds, const uint8_t* packed, size_t n, const int64_t* labels) {
+    const int tp8 = (T + 7) / 8, tp8_pad = T_pad / 8;
+    for (size_t i = 0; i < n; ++i)
+      if (labels[i] < 0 || labels[i] >= C)
+        fail(SNN_ERR_ARGUMENT, "target %lld outside [0,%d)", (long long)labels[i], C);
+    const size_t raw = n * size_t(tp8) * IN, lab_off = (raw + 15) & ~size_t(15);
+    if (pinned_bytes < lab_off + n * sizeof(int32_t)) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      pinned_bytes = 0;
+      CK(cudaMallocHost(&pinned, lab_off + n * sizeof(int32_t)));
+      pinned_bytes = lab_off + n * sizeof(int32_t);
+    }
+    if (raw_in.n < raw) raw_in.alloc(raw, false);
+    if (ds.n != n) {
+      ds.x.alloc(n * size_t(tp8_pad) * IN_pad, false);
+      ds.labels.alloc(n, false);
+      ds.n = n;
+      clear_graphs();
+    }
+    if (!copy_pool) {
+      const unsigned hc = std::thread::hardware_concurrency();
+      const int dflt = int(std::min(7u, hc > 2 ? hc / 2 - 1 : 0u));
+      const char* ev = std::getenv("SNN_COPY_THREADS");  // extra copy threads
+      copy_pool.reset(new CopyPool(ev && *ev ? std::max(0, std::atoi(ev)) : dflt));
+    }
+    uint8_t* h = static_cast<uint8_t*>(pinned);
+    const size_t chunks = raw >= (size_t(1) << 20) ? size_t(copy_chunks) : 1;
+    const size_t per = ((raw + chunks - 1) / chunks + 15) & ~size_t(15);
+    for (size_t off = 0; off < raw; off += per) {
+      const size_t len = std::min(per, raw - off);
+      copy_pool->copy(h + off, packed + off, len);
+      CK(cudaMemcpyAsync(raw_in.p + off, h + off, len, cudaMemcpyHostToDevice, stream));
+    }
+    int32_t* lab = reinterpret_cast<int32_t*>(h + lab_off);
+    for (size_t i = 0; i < n; ++i) lab[i] = int32_t(labels[i]);
+    CK(cudaMemcpyAsync(ds.labels.p, lab, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    const size_t out = n * size_t(tp8_pad) * IN_pad;
+    k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, stream>>>(raw_in.p, ds.x.p, int64_t(n), tp8,
+                                                                   tp8_pad, IN, IN_pad);
+    CK(cudaGetLastError());
   }
 
   void synth(size_t n, uint64_t seed) {
@@ -1167,9 +1298,7 @@ snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
                                  const int64_t* targets, float* loss, double* accuracy) {
   if (!e || !packed_batch || !targets) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
-    e->sync_after_stage = false;
-    e->stage(e->scratch, packed_batch, size_t(e->B), targets);
-    e->sync_after_stage = true;
+    e->stage_batch(e->scratch, packed_batch, size_t(e->B), targets);
     std::vector<uint32_t> rows(size_t(e->B));
     for (int i = 0; i < e->B; ++i) rows[size_t(i)] = uint32_t(i);
     e->step_rows(rows.data(), e->scratch, 1, loss, accuracy);

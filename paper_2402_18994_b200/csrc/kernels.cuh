@@ -1881,6 +1881,27 @@ __global__ void k_synth(SynthArgs a) {
   a.x[gid] = byte;
 }
 
+// Host-batch layout [n][tp8][IN] (reference packed, data.hpp:105-126) -> the
+// staged layout [n][tp8_pad][IN_pad], zero padded.  One thread per 4 output bytes.
+__global__ void k_relayout(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t n,
+                           int tp8, int tp8_pad, int IN, int IN_pad) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = n * tp8_pad * IN_pad;
+  if (q * 4 >= total) return;
+  uint32_t word = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int64_t o = q * 4 + e;
+    const int k = int(o % IN_pad);
+    const int64_t rg = o / IN_pad;
+    const int g = int(rg % tp8_pad);
+    const int64_t i = rg / tp8_pad;
+    const uint32_t v = (k < IN && g < tp8) ? in[(i * tp8 + g) * IN + k] : 0u;
+    word |= v << (8 * e);
+  }
+  reinterpret_cast<uint32_t*>(out)[q] = word;  // IN_pad is a multiple of 64
+}
+
 // StepResult{loss / B_global, hits / B_global}; advances the step counter.
 __global__ void k_result(const float* tail, int B_global, float loss_denom, int64_t* step,
                          int do_step, float* loss_out, double* acc_out) {
