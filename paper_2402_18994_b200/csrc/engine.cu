@@ -708,19 +708,28 @@ struct snn_engine {
       ds.n = n;
       clear_graphs();
     }
-    if (!copy_pool) {
-      const unsigned hc = std::thread::hardware_concurrency();
-      const int dflt = int(std::min(7u, hc > 2 ? hc / 2 - 1 : 0u));
-      const char* ev = std::getenv("SNN_COPY_THREADS");  // extra copy threads
-      copy_pool.reset(new CopyPool(ev && *ev ? std::max(0, std::atoi(ev)) : dflt));
-    }
     uint8_t* h = static_cast<uint8_t*>(pinned);
-    const size_t chunks = raw >= (size_t(1) << 20) ? size_t(copy_chunks) : 1;
-    const size_t per = ((raw + chunks - 1) / chunks + 15) & ~size_t(15);
-    for (size_t off = 0; off < raw; off += per) {
-      const size_t len = std::min(per, raw - off);
-      copy_pool->copy(h + off, packed + off, len);
-      CK(cudaMemcpyAsync(raw_in.p + off, h + off, len, cudaMemcpyHostToDevice, stream));
+    // a caller batch that already lives in pinned (page-locked) memory is DMA'd as is
+    cudaPointerAttributes pa{};
+    const bool caller_pinned = cudaPointerGetAttributes(&pa, packed) == cudaSuccess &&
+                               pa.type == cudaMemoryTypeHost;
+    if (!caller_pinned) cudaGetLastError();  // clear a pageable-pointer query error
+    if (caller_pinned) {
+      CK(cudaMemcpyAsync(raw_in.p, packed, raw, cudaMemcpyHostToDevice, stream));
+    } else {
+      if (!copy_pool) {  // created on the first pageable batch
+        const unsigned hc = std::thread::hardware_concurrency();
+        const int dflt = int(std::min(7u, hc > 2 ? hc / 2 - 1 : 0u));
+        const char* ev = std::getenv("SNN_COPY_THREADS");  // extra copy threads
+        copy_pool.reset(new CopyPool(ev && *ev ? std::max(0, std::atoi(ev)) : dflt));
+      }
+      const size_t chunks = raw >= (size_t(1) << 20) ? size_t(copy_chunks) : 1;
+      const size_t per = ((raw + chunks - 1) / chunks + 15) & ~size_t(15);
+      for (size_t off = 0; off < raw; off += per) {
+        const size_t len = std::min(per, raw - off);
+        copy_pool->copy(h + off, packed + off, len);
+        CK(cudaMemcpyAsync(raw_in.p + off, h + off, len, cudaMemcpyHostToDevice, stream));
+      }
     }
     int32_t* lab = reinterpret_cast<int32_t*>(h + lab_off);
     for (size_t i = 0; i < n; ++i) lab[i] = int32_t(labels[i]);
@@ -1298,10 +1307,27 @@ snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
                                  const int64_t* targets, float* loss, double* accuracy) {
   if (!e || !packed_batch || !targets) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
+    static const bool trace = std::getenv("SNN_E2E_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     e->stage_batch(e->scratch, packed_batch, size_t(e->B), targets);
+    const auto t1 = std::chrono::steady_clock::now();
     std::vector<uint32_t> rows(size_t(e->B));
     for (int i = 0; i < e->B; ++i) rows[size_t(i)] = uint32_t(i);
-    e->step_rows(rows.data(), e->scratch, 1, loss, accuracy);
+    e->set_rows_host(rows.data(), e->scratch);
+    e->launch(e->scratch, 1);
+    const auto t2 = std::chrono::steady_clock::now();
+    e->read_result(loss, accuracy);
+    const auto t3 = std::chrono::steady_clock::now();
+    if (trace) {  // host-side phase times of the e2e call (diagnostics)
+      static double acc[3];
+      static int calls;
+      acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+      acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
+      acc[2] += std::chrono::duration<double, std::micro>(t3 - t2).count();
+      if (++calls % 200 == 0)
+        std::fprintf(stderr, "e2e host us/step: stage %.1f  launch %.1f  wait+result %.1f\n", acc[0] / calls,
+                     acc[1] / calls, acc[2] / calls);
+    }
   });
 }
 

@@ -31,3 +31,8 @@ eng.synth_dataset(4096, seed=1)
 pk, y = eng.read_dataset(0, 256)
 eng.train_step_packed(pk, y)
 print(f"train_step_packed {t(lambda: eng.train_step_packed(pk, y), 100):.1f} us/step")
+import ctypes
+t0 = time.perf_counter()
+for _ in range(400):
+    eng.train_step_packed(pk, y)
+print(f"python loop {(time.perf_counter() - t0) / 400 * 1e6:.1f} us/step")

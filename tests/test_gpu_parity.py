@@ -422,3 +422,18 @@ def test_rate_mse_golden_loss_bit_exact(golden):
     eng.set_params(g["params"])
     loss, _ = eng.forward_backward(np.arange(B, dtype=np.uint32))
     assert np.float32(loss) == g["rate_mse_loss"]
+
+
+def test_packed_entry_pinned_caller_buffer(orc):
+    """A caller batch in pinned memory is DMA'd directly; results equal the
+    pageable-buffer path (staged through the copy pool) bit for bit."""
+    import torch
+    net = Net(inp=30, hidden=(16, 12), classes=5)
+    x, y = orc.synth_raster(5, 4, 19, 30, 2)
+    pk = orc.pack_time(x)
+    pinned = torch.empty(pk.shape, dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[...] = pk
+    e1, e2 = make_engine(net, 4, 19), make_engine(net, 4, 19)
+    for _ in range(2):
+        assert e1.train_step_packed(pk, y) == e2.train_step_packed(pinned.numpy(), y)
+    assert np.array_equal(e1.get_params(), e2.get_params())
