@@ -805,9 +805,9 @@ struct snn_engine {
     }
     return g;
   }
-  // forward groups + readout + L bwd + wgrad + tail (fused reduce+Adam on one rank;
-  // reduce, adam otherwise)
-  int launches_per_step() const { return int(fwd_groups().size()) + L + (world == 1 ? 3 : 4); }
+  // forward groups + readout + L bwd + wgrad + tail (fused reduce+Adam without a
+  // communicator; reduce, adam with one -- the allreduce between them is NCCL's)
+  int launches_per_step() const { return int(fwd_groups().size()) + L + (comm_handle == nullptr ? 3 : 4); }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;
@@ -961,8 +961,8 @@ struct snn_engine {
       r.n_loss_terms = cfg.loss == 1 ? B * C : B;
       r.w_blocks = int((n_params + kRedElemsPerBlock - 1) / kRedElemsPerBlock);
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
-      if (update && world == 1) {
-        // single rank: no allreduce between reduction and update -> one kernel
+      if (update && comm_handle == nullptr) {
+        // no communicator: no allreduce between reduction and update -> one kernel
         AdamArgs a = adam_args(1);
         long long* tclk = debug && size_t(blocks) * kClkStride <= clk_region()
                               ? dbg_clk.p + size_t(2 + 2 * L) * clk_region() : nullptr;
@@ -974,7 +974,7 @@ struct snn_engine {
       launch(k_reduce, dim3(blocks), dim3(256), 0, r);
       mark(evs, "reduce", -1);
     }
-    if (world > 1) {
+    if (comm_handle != nullptr) {
       const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2, /*ncclFloat32*/ 7,
                                       /*ncclSum*/ 0, comm_handle, stream);
       if (rc != 0) fail(SNN_ERR_CUDA, "ncclAllReduce failed (%d)", rc);
@@ -1551,12 +1551,8 @@ snn_status snn_nccl_unique_id(uint8_t id[128]) {
 snn_status snn_comm_init(snn_engine* e, const uint8_t id[128], int32_t rank, int32_t world) {
   if (!e || !id || world < 1 || rank < 0 || rank >= world) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
-    if (world == 1) {
-      e->world = 1;
-      e->rank = 0;
-      e->clear_graphs();
-      return;
-    }
+    // world == 1 still creates a (single-rank) communicator: the step then runs the
+    // multi-rank tail (k_reduce -> ncclAllReduce -> k_adam), testable on one GPU
     NcclApi& api = nccl();
     if (!api.ok) fail(SNN_ERR_CUDA, "libnccl.so.2 not loadable");
     UniqueId u;

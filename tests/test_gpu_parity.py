@@ -437,3 +437,29 @@ def test_packed_entry_pinned_caller_buffer(orc):
     for _ in range(2):
         assert e1.train_step_packed(pk, y) == e2.train_step_packed(pinned.numpy(), y)
     assert np.array_equal(e1.get_params(), e2.get_params())
+
+
+def test_single_rank_nccl_tail_matches_fused_tail(orc):
+    """The multi-rank tail (k_reduce -> ncclAllReduce -> k_adam) on a one-rank NCCL
+    communicator gives bit-identical training to the fused single-rank tail."""
+    from paper_2402_18994_b200 import DeviceError, Engine
+    net = Net(inp=30, hidden=(16, 12), classes=5)
+    x, y = orc.synth_raster(5, 8, 19, 30, 2)
+    pk = orc.pack_time(x)
+    e1, e2 = make_engine(net, 4, 19, seed=3), make_engine(net, 4, 19, seed=3)
+    try:
+        e2.comm_init(Engine.nccl_unique_id(), 0, 1)
+    except DeviceError as err:
+        pytest.skip(f"NCCL unavailable: {err}")
+    assert e2.launches_per_step == e1.launches_per_step + 1
+    for eng in (e1, e2):
+        eng.stage_dataset(pk, y)
+    for i in range(4):
+        rows = np.arange(4 * (i % 2), 4 * (i % 2) + 4, dtype=np.uint32)
+        assert e1.train_step(rows) == e2.train_step(rows)
+    assert np.array_equal(e1.get_params(), e2.get_params())
+    m1, v1, s1 = e1.get_opt_state()
+    m2, v2, s2 = e2.get_opt_state()
+    assert s1 == s2 == 4 and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+    assert e1.forward_backward(np.arange(4, dtype=np.uint32)) == e2.forward_backward(np.arange(4, dtype=np.uint32))
+    assert np.array_equal(e1.get_grads(), e2.get_grads())
