@@ -107,6 +107,15 @@ snn_status snn_get_params(snn_engine* e, float* host, size_t n);
 /* Reference init (network.hpp:231-286) from an explicit key word. */
 snn_status snn_init_params(snn_engine* e, uint64_t key_word);
 /* OptimizerState m, v, step (optimize.hpp:28-48), trainable entries in order. */
+/* Checkpoints in the reference .spkc format (optimize.hpp:300-436), bit-exact:
+ * parameters, optimizer kind / step / m (/ v for Adam) and the caller's config
+ * text with its FNV-1a hash.  Load checks the entries against the network and
+ * copies the stored config text into config_out (NUL-terminated, truncated to
+ * config_cap) and its full length into *config_len (either may be NULL). */
+snn_status snn_save_checkpoint(snn_engine* e, const char* path, const char* config_text,
+                               size_t config_len);
+snn_status snn_load_checkpoint(snn_engine* e, const char* path, char* config_out,
+                               size_t config_cap, size_t* config_len);
 snn_status snn_get_opt_state(snn_engine* e, float* m, float* v, uint64_t* step, size_t n);
 snn_status snn_set_opt_state(snn_engine* e, const float* m, const float* v, uint64_t step,
                              size_t n);

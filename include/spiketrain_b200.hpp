@@ -270,6 +270,20 @@ inline std::vector<float> apply(TrainState& st, const std::vector<std::uint32_t>
   return trace;
 }
 
+// write_checkpoint / read_checkpoint (optimize.hpp:334-436) of the engine state in
+// the reference .spkc format (bit-exact); read returns the stored config text.
+inline void write_checkpoint(TrainState& st, const std::string& path, const std::string& config_text) {
+  check(snn_save_checkpoint(st.engine(), path.c_str(), config_text.data(), config_text.size()),
+        st.engine());
+}
+inline std::string read_checkpoint(TrainState& st, const std::string& path) {
+  std::string cfg((1u << 20) + 1, '\0');
+  std::size_t n = 0;
+  check(snn_load_checkpoint(st.engine(), path.c_str(), cfg.data(), cfg.size(), &n), st.engine());
+  cfg.resize(n);
+  return cfg;
+}
+
 struct TrainResult {
   std::vector<float> params;
   std::vector<EpochMetrics> metrics;

@@ -243,6 +243,19 @@ class Lib:
             correct += r["acc"] * float(hi - lo)
         return correct / float(n)
 
+    def write_checkpoint(self, net: Net, params, m, v, step: int, optimizer: str,
+                         config_text: str, path: str) -> None:
+        """Reference write_checkpoint (optimize.hpp:334-366); ref library only."""
+        n = net.c()
+        f = self._f("write_checkpoint")
+        f.restype = C.c_int
+        rc = f(C.byref(n), _ptr(np.ascontiguousarray(params, np.float32), C.c_float),
+               _ptr(np.ascontiguousarray(m, np.float32), C.c_float),
+               _ptr(np.ascontiguousarray(v, np.float32), C.c_float), C.c_uint64(step),
+               C.c_int(1 if optimizer == "sgd" else 0), config_text.encode(), path.encode())
+        if rc != 0:
+            raise ValueError("write_checkpoint failed")
+
     def adam(self, p, g, m, v, step, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
         st = C.c_uint64(step)
         self._f("adam")(_ptr(p, C.c_float), _ptr(g, C.c_float), _ptr(m, C.c_float),

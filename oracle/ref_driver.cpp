@@ -349,4 +349,27 @@ int ref_train_epochs(const orc_net* n, float* params, float* m, float* v,
   }
 }
 
+// write_checkpoint (optimize.hpp:334-366) of a flat parameter / optimizer state:
+// optimizer 0 = Adam (m and v), 1 = SGD (m only).  Golden .spkc fixtures.
+int ref_write_checkpoint(const orc_net* n, const float* params, const float* m,
+                         const float* v, uint64_t step, int optimizer,
+                         const char* config_text, const char* path) {
+  try {
+    const NetworkParams<float> p = params_from_flat(skeleton(n), params);
+    OptimizerState<float> st =
+        init_optimizer(optimizer == 1 ? OptimizerKind::Sgd : OptimizerKind::Adam, p);
+    std::size_t off = 0;
+    for (std::size_t i = 0; i < st.m.size(); ++i) {
+      std::memcpy(st.m[i].data(), m + off, st.m[i].size() * sizeof(float));
+      if (i < st.v.size()) std::memcpy(st.v[i].data(), v + off, st.v[i].size() * sizeof(float));
+      off += st.m[i].size();
+    }
+    st.step = step;
+    write_checkpoint(path, p, st, std::string(config_text));
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 }  // extern "C"

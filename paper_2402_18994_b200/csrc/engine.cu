@@ -1248,6 +1248,160 @@ snn_status snn_init_params(snn_engine* e, uint64_t key_word) {
   return guard(e, [&] { e->init_params_host(key_word); });
 }
 
+// ------------------------------------------------------------- checkpoints
+// .spkc (optimize.hpp:300-436): "SPKC", u32 version 1, u64 fnv1a(config), u64
+// config length, config bytes, u8 scalar width, u32 entry count, entries (u16
+// name length, name, u8 trainable, u32 ndim, u64 dims, payload), u8 optimizer
+// kind, u64 step, m payloads, v payloads (Adam only).  Little-endian, bit-exact.
+namespace {
+uint64_t fnv1a(const char* s, size_t n) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= static_cast<unsigned char>(s[i]);
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+struct Reader {
+  const std::vector<uint8_t>& b;
+  size_t off = 0;
+  void take(void* dst, size_t n) {
+    if (off + n > b.size()) fail(SNN_ERR_IO, "short read at byte offset %zu", off);
+    std::memcpy(dst, b.data() + off, n);
+    off += n;
+  }
+  uint8_t u8() { uint8_t v; take(&v, 1); return v; }
+  uint16_t u16() { uint16_t v; take(&v, 2); return v; }
+  uint32_t u32() { uint32_t v; take(&v, 4); return v; }
+  uint64_t u64() { uint64_t v; take(&v, 8); return v; }
+};
+void put_bytes(std::vector<uint8_t>& o, const void* p, size_t n) {
+  const uint8_t* c = static_cast<const uint8_t*>(p);
+  o.insert(o.end(), c, c + n);
+}
+void put_u8(std::vector<uint8_t>& o, uint8_t v) { put_bytes(o, &v, 1); }
+void put_u16(std::vector<uint8_t>& o, uint16_t v) { put_bytes(o, &v, 2); }
+void put_u32(std::vector<uint8_t>& o, uint32_t v) { put_bytes(o, &v, 4); }
+void put_u64(std::vector<uint8_t>& o, uint64_t v) { put_bytes(o, &v, 8); }
+}  // namespace
+
+snn_status snn_save_checkpoint(snn_engine* e, const char* path, const char* config_text,
+                               size_t config_len) {
+  if (!e || !path || (!config_text && config_len)) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    const size_t n = e->n_params;
+    std::vector<float> p(n), m(n), v(n);
+    int64_t step = 0;
+    CK(cudaMemcpyAsync(p.data(), e->params.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(m.data(), e->m.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(v.data(), e->v.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(&step, e->step.p, 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    std::vector<uint8_t> o;
+    put_bytes(o, "SPKC", 4);
+    put_u32(o, 1);
+    put_u64(o, fnv1a(config_text, config_len));
+    put_u64(o, config_len);
+    put_bytes(o, config_text, config_len);
+    put_u8(o, 4);
+    put_u32(o, uint32_t(e->entries.size()));
+    for (const auto& en : e->entries) {
+      put_u16(o, uint16_t(en.name.size()));
+      put_bytes(o, en.name.data(), en.name.size());
+      put_u8(o, 1);  // every entry trainable (BetaMode::PerNeuron, network.hpp:231-286)
+      if (en.kind == kEntryW) {
+        put_u32(o, 2);
+        put_u64(o, uint64_t(en.rows));
+        put_u64(o, uint64_t(en.cols));
+      } else {
+        put_u32(o, 1);
+        put_u64(o, uint64_t(en.cols));
+      }
+      put_bytes(o, p.data() + en.offset, en.size * 4);
+    }
+    put_u8(o, e->cfg.optimizer == 1 ? 1 : 0);
+    put_u64(o, uint64_t(step));
+    for (const auto& en : e->entries) put_bytes(o, m.data() + en.offset, en.size * 4);
+    if (e->cfg.optimizer != 1)
+      for (const auto& en : e->entries) put_bytes(o, v.data() + en.offset, en.size * 4);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(SNN_ERR_IO, "cannot open for writing: %s", path);
+    const size_t w = std::fwrite(o.data(), 1, o.size(), f);
+    const int rc = std::fclose(f);
+    if (w != o.size() || rc != 0) fail(SNN_ERR_IO, "short write: %s", path);
+  });
+}
+
+snn_status snn_load_checkpoint(snn_engine* e, const char* path, char* config_out,
+                               size_t config_cap, size_t* config_len) {
+  if (!e || !path) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(SNN_ERR_IO, "cannot open for reading: %s", path);
+    std::vector<uint8_t> b;
+    uint8_t buf[1 << 16];
+    for (size_t r; (r = std::fread(buf, 1, sizeof(buf), f)) > 0;) b.insert(b.end(), buf, buf + r);
+    std::fclose(f);
+    Reader rd{b};
+    char magic[4];
+    rd.take(magic, 4);
+    if (std::memcmp(magic, "SPKC", 4) != 0) fail(SNN_ERR_FORMAT, "bad magic at byte offset 0");
+    const uint32_t version = rd.u32();
+    if (version != 1) fail(SNN_ERR_FORMAT, "unsupported checkpoint version %u at byte offset 4", version);
+    const uint64_t hash = rd.u64();
+    const uint64_t clen = rd.u64();
+    if (clen > (1u << 20)) fail(SNN_ERR_FORMAT, "implausible config length at byte offset 16");
+    std::string cfg(clen, '\0');
+    rd.take(cfg.data(), clen);
+    if (fnv1a(cfg.data(), cfg.size()) != hash)
+      fail(SNN_ERR_FORMAT, "config hash mismatch (stored %llu)", (unsigned long long)hash);
+    const uint8_t width = rd.u8();
+    if (width != 4) fail(SNN_ERR_FORMAT, "checkpoint scalar width %u, expected 4", unsigned(width));
+    const uint32_t ne = rd.u32();
+    if (ne != e->entries.size())
+      fail(SNN_ERR_SHAPE, "checkpoint holds %u entries, the network %zu", ne, e->entries.size());
+    const size_t n = e->n_params;
+    std::vector<float> p(n), m(n, 0.0f), v(n, 0.0f);
+    for (const auto& en : e->entries) {
+      const uint16_t nl = rd.u16();
+      std::string name(nl, '\0');
+      rd.take(name.data(), nl);
+      const uint8_t trainable = rd.u8();
+      const uint32_t nd = rd.u32();
+      if (nd > 16) fail(SNN_ERR_FORMAT, "implausible tensor rank at byte offset %zu", rd.off - 4);
+      std::vector<uint64_t> dims(nd);
+      for (auto& d : dims) d = rd.u64();
+      const bool w2 = en.kind == kEntryW;
+      const bool shape_ok = w2 ? (nd == 2 && dims[0] == uint64_t(en.rows) && dims[1] == uint64_t(en.cols))
+                               : (nd == 1 && dims[0] == uint64_t(en.cols));
+      if (name != en.name || !shape_ok || trainable != 1)
+        fail(SNN_ERR_SHAPE, "checkpoint entry %s does not match network entry %s", name.c_str(),
+             en.name.c_str());
+      rd.take(p.data() + en.offset, en.size * 4);
+    }
+    const uint8_t kind = rd.u8();
+    if (int(kind) != (e->cfg.optimizer == 1 ? 1 : 0))
+      fail(SNN_ERR_ARGUMENT, "checkpoint optimizer kind %u differs from the engine's", unsigned(kind));
+    const int64_t step = int64_t(rd.u64());
+    for (const auto& en : e->entries) rd.take(m.data() + en.offset, en.size * 4);
+    if (kind == 0)
+      for (const auto& en : e->entries) rd.take(v.data() + en.offset, en.size * 4);
+    e->upload_params(p.data());
+    CK(cudaMemcpyAsync(e->m.p, m.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(e->v.p, v.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(e->step.p, &step, 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    e->host_step = step;
+    e->ensure_bc_capacity();
+    if (config_len) *config_len = cfg.size();
+    if (config_out && config_cap) {
+      const size_t c = std::min(config_cap - 1, cfg.size());
+      std::memcpy(config_out, cfg.data(), c);
+      config_out[c] = '\0';
+    }
+  });
+}
+
 snn_status snn_get_opt_state(snn_engine* e, float* m, float* v, uint64_t* step, size_t n) {
   if (!e) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {

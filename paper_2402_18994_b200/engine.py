@@ -189,7 +189,7 @@ def lib() -> C.CDLL:
                  "snn_set_params", "snn_get_params", "snn_init_params", "snn_get_opt_state",
                  "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
                  "snn_train_step_packed", "snn_forward_backward", "snn_train_epochs",
-                 "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_evaluate", "snn_apply", "snn_sync", "snn_read_result",
+                 "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_evaluate", "snn_apply", "snn_save_checkpoint", "snn_load_checkpoint", "snn_sync", "snn_read_result",
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
                  "snn_read_dataset"):
@@ -415,6 +415,20 @@ class Engine:
         self._check(self._L.snn_apply(self._h, _p(r, C.c_uint32), _p(out, C.c_float),
                                       C.c_size_t(out.size)))
         return out
+
+    # ------------------------------------------------------------ checkpoints
+    def save_checkpoint(self, path: str, config_text: str = ""):
+        """write_checkpoint (optimize.hpp:334-366) of the device state, .spkc bit-exact."""
+        cfg = config_text.encode()
+        self._check(self._L.snn_save_checkpoint(self._h, os.fsencode(path), cfg, C.c_size_t(len(cfg))))
+
+    def load_checkpoint(self, path: str) -> str:
+        """read_checkpoint (optimize.hpp:376-436) into the engine; returns the config text."""
+        n = C.c_size_t()
+        buf = C.create_string_buffer((1 << 20) + 1)  # the format caps config text at 1 MiB
+        self._check(self._L.snn_load_checkpoint(self._h, os.fsencode(path), buf,
+                                                C.c_size_t(len(buf)), C.byref(n)))
+        return buf.raw[:n.value].decode()
 
     def sync(self):
         self._check(self._L.snn_sync(self._h))

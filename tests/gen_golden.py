@@ -119,6 +119,30 @@ def opts_fixture(ref: Lib):
     np.savez_compressed(os.path.join(GOLD, "opts.npz"), **vals)
 
 
+CKPT_NET = Net(inp=30, hidden=(16, 12), classes=5, bias=True, act="arctan", unroll=4)
+CKPT_CONFIG = "# spiketrain run config (fixture)\nnet = 30-16-12-5 lif arctan bias\nlr = 1e-3\n"
+
+
+def checkpoint_fixture(ref: Lib):
+    """.spkc files written by the reference (optimize.hpp:334-366) after 2 steps with
+    Adam and with SGD, plus the state they hold (ckpt.npz)."""
+    from oracle.pyoracle import Opts
+    key = ref.key_child(ref.key_from_seed(17), 0)
+    p = ref.init(CKPT_NET, key) * np.float32(3.0)
+    x, y = ref.synth_raster(5, 6, 19, 30, 8)
+    pk = ref.pack_time(x)
+    vals = dict(config=np.frombuffer(CKPT_CONFIG.encode(), np.uint8), **net_dict(CKPT_NET))
+    for opt in ("adam", "sgd"):
+        st = State(p.copy())
+        for _ in range(2):
+            ref.train_step(CKPT_NET, st, pk, 19, y, opts=Opts(optimizer=opt, momentum=0.9))
+        ref.write_checkpoint(CKPT_NET, st.params, st.m, st.v, st.step, opt, CKPT_CONFIG,
+                             os.path.join(GOLD, f"ckpt_{opt}.spkc"))
+        vals.update({f"{opt}_params": st.params, f"{opt}_m": st.m, f"{opt}_v": st.v,
+                     f"{opt}_step": np.int64(st.step)})
+    np.savez_compressed(os.path.join(GOLD, "ckpt.npz"), **vals)
+
+
 if __name__ == "__main__":
     if not have_ref():
         Lib.__init__  # noqa: B018
@@ -137,4 +161,6 @@ if __name__ == "__main__":
         c1(ref)
     if only in (None, "opts"):
         opts_fixture(ref)
+    if only in (None, "ckpt"):
+        checkpoint_fixture(ref)
     print("golden fixtures written to", GOLD)

@@ -463,3 +463,58 @@ def test_single_rank_nccl_tail_matches_fused_tail(orc):
     assert s1 == s2 == 4 and np.array_equal(m1, m2) and np.array_equal(v1, v2)
     assert e1.forward_backward(np.arange(4, dtype=np.uint32)) == e2.forward_backward(np.arange(4, dtype=np.uint32))
     assert np.array_equal(e1.get_grads(), e2.get_grads())
+
+
+CKPT_NET = Net(inp=30, hidden=(16, 12), classes=5, bias=True, act="arctan", unroll=4)
+
+
+@pytest.mark.parametrize("opt", ["adam", "sgd"])
+def test_checkpoint_matches_reference_file(golden, tmp_path, opt):
+    """.spkc files written by the reference itself (tests/golden/ckpt_*.spkc):
+    the engine loads them exactly and writes the same bytes back."""
+    import os
+    from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+    g = golden("ckpt")
+    spec = shd_spec(hidden=CKPT_NET.hidden, classes=CKPT_NET.classes, inp=CKPT_NET.inp,
+                    act=CKPT_NET.act, bias=True)
+    eng = Engine(spec, TrainConfig(batch_size=4, optimizer=opt, momentum=0.9), 19)
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"ckpt_{opt}.spkc")
+    cfg = eng.load_checkpoint(src)
+    assert cfg.encode() == g["config"].tobytes()
+    assert np.array_equal(eng.get_params(), g[f"{opt}_params"])
+    m, v, step = eng.get_opt_state()
+    assert step == int(g[f"{opt}_step"])
+    assert np.array_equal(m, g[f"{opt}_m"]) and (opt == "sgd" or np.array_equal(v, g[f"{opt}_v"]))
+    out = tmp_path / "out.spkc"
+    eng.save_checkpoint(str(out), cfg)
+    assert out.read_bytes() == open(src, "rb").read()
+
+
+def test_checkpoint_resume_is_bit_exact(orc, tmp_path):
+    """optimize_test.cpp:257-290: training resumed from a checkpoint continues
+    bit-identically; errors map to the reference classes."""
+    from paper_2402_18994_b200 import FormatError, IoError, ShapeError
+    x, y = orc.synth_raster(5, 8, 19, 30, 2)
+    pk = orc.pack_time(x)
+    a = make_engine(CKPT_NET, 4, 19, seed=6)
+    a.stage_dataset(pk, y)
+    rows = [np.arange(4 * (i % 2), 4 * (i % 2) + 4, dtype=np.uint32) for i in range(5)]
+    for r in rows[:3]:
+        a.train_step(r)
+    path = str(tmp_path / "mid.spkc")
+    a.save_checkpoint(path, "resume test")
+    b = make_engine(CKPT_NET, 4, 19, seed=99)
+    b.stage_dataset(pk, y)
+    assert b.load_checkpoint(path) == "resume test"
+    for r in rows[3:]:
+        assert a.train_step(r) == b.train_step(r)
+    assert np.array_equal(a.get_params(), b.get_params())
+    with pytest.raises(IoError):
+        b.load_checkpoint(str(tmp_path / "missing.spkc"))
+    bad = tmp_path / "bad.spkc"
+    bad.write_bytes(b"XXXX" + open(path, "rb").read()[4:])
+    with pytest.raises(FormatError):
+        b.load_checkpoint(str(bad))
+    other = make_engine(Net(inp=30, hidden=(16, 12), classes=5), 4, 19)  # no bias entries
+    with pytest.raises(ShapeError):
+        other.load_checkpoint(path)
