@@ -28,7 +28,10 @@ class _Net(C.Structure):
     _fields_ = [("in_", C.c_int), ("n_hidden", C.c_int),
                 ("hidden", C.c_int * 8), ("classes", C.c_int),
                 ("bias", C.c_int), ("threshold", C.c_float), ("act", C.c_int),
-                ("slope", C.c_float), ("aux", C.c_float), ("unroll", C.c_int)]
+                ("slope", C.c_float), ("aux", C.c_float), ("unroll", C.c_int),
+                ("beta_mode", C.c_int * 9), ("fixed_beta", C.c_float * 9)]
+
+BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 
 
 class _Opts(C.Structure):
@@ -63,6 +66,10 @@ class Net:
     slope: float | None = None
     aux: float | None = None
     unroll: int = 32
+    # BetaMode per cell (hidden LIF layers, then the LI readout): "per_neuron" |
+    # "scalar" (LearnableScalar) | "fixed"; fixed_beta per cell (default 0.5)
+    beta_mode: tuple = ()
+    fixed_beta: tuple = ()
 
     def c(self) -> _Net:
         s, a = DEFAULT_SLOPE[self.act]
@@ -78,6 +85,9 @@ class Net:
         n.slope = s if self.slope is None else self.slope
         n.aux = a if self.aux is None else self.aux
         n.unroll = self.unroll
+        for i in range(len(self.hidden) + 1):
+            n.beta_mode[i] = BETA_MODES[self.beta_mode[i]] if i < len(self.beta_mode) else 0
+            n.fixed_beta[i] = self.fixed_beta[i] if i < len(self.fixed_beta) else 0.5
         return n
 
 

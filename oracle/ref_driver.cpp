@@ -31,6 +31,11 @@ ActivationDesc act_desc(const orc_net* n) {
   return d;
 }
 
+BetaMode beta_mode(const orc_net* n, int l) {
+  return n->beta_mode[l] == 1 ? BetaMode::LearnableScalar
+                              : n->beta_mode[l] == 2 ? BetaMode::Fixed : BetaMode::PerNeuron;
+}
+
 NetworkSpec make_spec(const orc_net* n) {
   NetworkSpec s;
   s.input_shape = {std::size_t(n->in)};
@@ -39,10 +44,15 @@ NetworkSpec make_spec(const orc_net* n) {
     LIFLayer lif;
     lif.activation = act_desc(n);
     lif.threshold = double(n->threshold);
+    lif.beta_mode = beta_mode(n, l);
+    lif.fixed_beta = double(n->fixed_beta[l]);
     s.layers.push_back(lif);
   }
   s.layers.push_back(LinearLayer{std::size_t(n->classes), n->bias != 0});
-  s.layers.push_back(LILayer{});
+  LILayer li;
+  li.beta_mode = beta_mode(n, n->n_hidden);
+  li.fixed_beta = double(n->fixed_beta[n->n_hidden]);
+  s.layers.push_back(li);
   return s;
 }
 
@@ -193,9 +203,14 @@ int ref_forward_backward_ex(const orc_net* n, const orc_train_opts* opts,
       tape.backward(l);
       std::size_t off = 0;
       for (std::size_t i = 0; i < ids.size(); ++i) {
-        const Tensor<float> g = tape.grad(ids[i]);
-        std::memcpy(grads + off, g.data(), g.size() * sizeof(float));
-        off += g.size();
+        const std::size_t sz = p.entries[i].tensor.size();
+        if (p.entries[i].trainable) {
+          const Tensor<float> g = tape.grad(ids[i]);
+          std::memcpy(grads + off, g.data(), sz * sizeof(float));
+        } else {
+          std::memset(grads + off, 0, sz * sizeof(float));  // constant: no gradient
+        }
+        off += sz;
       }
     }
     if (spikes) {
@@ -265,12 +280,16 @@ TrainState<float> make_state(const orc_net* n, const float* params,
   }
   st.params = params_from_flat(skeleton(n), params);
   st.opt = init_optimizer(kind, st.params);
-  std::size_t off = 0;
-  for (std::size_t i = 0; i < st.opt.m.size(); ++i) {
-    std::memcpy(st.opt.m[i].data(), m + off, st.opt.m[i].size() * sizeof(float));
-    if (i < st.opt.v.size())
-      std::memcpy(st.opt.v[i].data(), v + off, st.opt.v[i].size() * sizeof(float));
-    off += st.opt.m[i].size();
+  // flat m/v span every entry (zeros for constants); the state holds trainable ones
+  std::size_t off = 0, ti = 0;
+  for (const auto& e : st.params.entries) {
+    if (e.trainable) {
+      std::memcpy(st.opt.m[ti].data(), m + off, e.tensor.size() * sizeof(float));
+      if (ti < st.opt.v.size())
+        std::memcpy(st.opt.v[ti].data(), v + off, e.tensor.size() * sizeof(float));
+      ++ti;
+    }
+    off += e.tensor.size();
   }
   st.opt.step = step;
   return st;
@@ -279,12 +298,15 @@ TrainState<float> make_state(const orc_net* n, const float* params,
 void unload_state(const TrainState<float>& st, float* params, float* m,
                   float* v, uint64_t* step) {
   params_to_flat(st.params, params);
-  std::size_t off = 0;
-  for (std::size_t i = 0; i < st.opt.m.size(); ++i) {
-    std::memcpy(m + off, st.opt.m[i].data(), st.opt.m[i].size() * sizeof(float));
-    if (i < st.opt.v.size())
-      std::memcpy(v + off, st.opt.v[i].data(), st.opt.v[i].size() * sizeof(float));
-    off += st.opt.m[i].size();
+  std::size_t off = 0, ti = 0;
+  for (const auto& e : st.params.entries) {
+    if (e.trainable) {
+      std::memcpy(m + off, st.opt.m[ti].data(), e.tensor.size() * sizeof(float));
+      if (ti < st.opt.v.size())
+        std::memcpy(v + off, st.opt.v[ti].data(), e.tensor.size() * sizeof(float));
+      ++ti;
+    }
+    off += e.tensor.size();
   }
   *step = st.opt.step;
 }
@@ -358,11 +380,14 @@ int ref_write_checkpoint(const orc_net* n, const float* params, const float* m,
     const NetworkParams<float> p = params_from_flat(skeleton(n), params);
     OptimizerState<float> st =
         init_optimizer(optimizer == 1 ? OptimizerKind::Sgd : OptimizerKind::Adam, p);
-    std::size_t off = 0;
-    for (std::size_t i = 0; i < st.m.size(); ++i) {
-      std::memcpy(st.m[i].data(), m + off, st.m[i].size() * sizeof(float));
-      if (i < st.v.size()) std::memcpy(st.v[i].data(), v + off, st.v[i].size() * sizeof(float));
-      off += st.m[i].size();
+    std::size_t off = 0, ti = 0;
+    for (const auto& e : p.entries) {
+      if (e.trainable) {
+        std::memcpy(st.m[ti].data(), m + off, e.tensor.size() * sizeof(float));
+        if (ti < st.v.size()) std::memcpy(st.v[ti].data(), v + off, e.tensor.size() * sizeof(float));
+        ++ti;
+      }
+      off += e.tensor.size();
     }
     st.step = step;
     write_checkpoint(path, p, st, std::string(config_text));

@@ -132,6 +132,11 @@ int orc_entry_count(const orc_net* net) {
   return (net->n_hidden + 1) * (net->bias ? 3 : 2);
 }
 
+/* beta entry size of cell l (l == n_hidden: the readout) */
+static size_t beta_size(const orc_net* net, int l, size_t h) {
+  return net->beta_mode[l] == 0 ? h : 1;
+}
+
 static int layer_in(const orc_net* net, int l) {
   return l == 0 ? net->in : net->hidden[l - 1];
 }
@@ -145,7 +150,7 @@ void orc_entry_layout(const orc_net* net, size_t* offsets, size_t* sizes,
   int e = 0;
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    const size_t sz[3] = {k * h, h, h};
+    const size_t sz[3] = {k * h, h, beta_size(net, l, h)};
     const char* leaf[3] = {"w", "b", "beta"};
     const int lid[3] = {2 * l, 2 * l, 2 * l + 1};
     for (int q = 0; q < 3; ++q) {
@@ -163,7 +168,7 @@ size_t orc_param_count(const orc_net* net) {
   size_t n = 0;
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    n += k * h + h + (net->bias ? h : 0);
+    n += k * h + beta_size(net, l, h) + (net->bias ? h : 0);
   }
   return n;
 }
@@ -185,7 +190,7 @@ static void layer_offsets(const orc_net* net, layer_off* lo) {
       lo[l].b = (size_t)-1;
     }
     lo[l].beta = off;
-    off += h;
+    off += beta_size(net, l, h);
   }
 }
 
@@ -201,8 +206,11 @@ void orc_init(const orc_net* net, uint64_t key, float* params) {
                          params + lo[l].w);
     if (net->bias) memset(params + lo[l].b, 0, h * sizeof(float));
     const uint64_t lk_cell = orc_key_child(key, (uint64_t)(2 * l + 1));
-    orc_truncated_normal(orc_key_child(lk_cell, 2), h, 0.5f, 0.25f,
-                         params + lo[l].beta);
+    if (net->beta_mode[l] == 2) /* Fixed: Tensor::scalar(fixed_beta) */
+      params[lo[l].beta] = net->fixed_beta[l];
+    else /* PerNeuron [h] or LearnableScalar [] from the same key */
+      orc_truncated_normal(orc_key_child(lk_cell, 2), beta_size(net, l, h), 0.5f, 0.25f,
+                           params + lo[l].beta);
   }
 }
 
@@ -310,10 +318,11 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
     act[l + 1] = (float*)malloc(M * H * sizeof(float));
     vst[l] = (float*)malloc(M * H * sizeof(float));
     const float* beta = params + lo[l].beta;
+    const size_t bs = net->beta_mode[l] == 0 ? 1 : 0; /* scalar beta broadcasts */
     /* lif_step_taped (neuron.hpp:127-136), per timestep */
     for (size_t b = 0; b < B; ++b)
       for (size_t n = 0; n < H; ++n) {
-        const float vb = clip01(beta[n]);
+        const float vb = clip01(beta[n * bs]);
         float v = 0.0f;
         for (size_t t = 0; t < T; ++t) {
           const size_t idx = (b * T + t) * H + n;
@@ -343,9 +352,10 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
   float* v3 = (float*)malloc(M * C * sizeof(float));
   {
     const float* beta = params + lo[L].beta;
+    const size_t bs = net->beta_mode[L] == 0 ? 1 : 0;
     for (size_t b = 0; b < B; ++b)
       for (size_t c = 0; c < C; ++c) {
-        const float vb = clip01(beta[c]);
+        const float vb = clip01(beta[c * bs]);
         float v = 0.0f;
         for (size_t t = 0; t < T; ++t) {
           const size_t idx = (b * T + t) * C + c;
@@ -425,10 +435,12 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
     {
       const float* beta = params + lo[L].beta;
       float* gbeta = grads + lo[L].beta;
+      const int mode = net->beta_mode[L];
+      const size_t bs = mode == 0 ? 1 : 0;
       float* gvb = (float*)malloc(C * sizeof(float));
       for (size_t b = 0; b < B; ++b)
         for (size_t c = 0; c < C; ++c) {
-          const float vb = clip01(beta[c]);
+          const float vb = clip01(beta[c * bs]);
           float G = 0.0f;
           for (size_t t = T; t-- > 0;) {
             const size_t idx = (b * T + t) * C + c;
@@ -437,14 +449,16 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
           }
         }
       /* d(clip01(beta)) per step, summed over b; beta grad in reverse t. */
-      for (size_t t = T; t-- > 0;) {
+      /* (mul_bcast backward, autodiff.hpp:191-205: pg[i % inner] += g*a in
+       * row-major order -- a scalar beta sums every (b, c) of the step) */
+      for (size_t t = T; t-- > 0 && mode != 2;) {
         for (size_t c = 0; c < C; ++c) gvb[c] = 0.0f;
         for (size_t b = 0; b < B; ++b)
           for (size_t c = 0; c < C; ++c) {
             const size_t idx = (b * T + t) * C + c;
-            gvb[c] += dI[idx] * v3[idx];
+            gvb[c * bs] += dI[idx] * v3[idx];
           }
-        for (size_t c = 0; c < C; ++c)
+        for (size_t c = 0; c < (bs ? C : 1); ++c)
           if (beta[c] > 0.0f && beta[c] < 1.0f) gbeta[c] += gvb[c];
       }
       free(gvb);
@@ -498,11 +512,13 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
       const int hl = l - 1; /* hidden layer whose spikes fed Linear l */
       const float* beta = params + lo[hl].beta;
       float* gbeta = grads + lo[hl].beta;
+      const int mode = net->beta_mode[hl];
+      const size_t bs = mode == 0 ? 1 : 0;
       const float* V = vst[hl];
       float* dIh = (float*)malloc(M * H * sizeof(float));
       for (size_t b = 0; b < B; ++b)
         for (size_t n = 0; n < H; ++n) {
-          const float vb = clip01(beta[n]);
+          const float vb = clip01(beta[n * bs]);
           float G = 0.0f; /* grad of v_{t+1} */
           for (size_t t = T; t-- > 0;) {
             const size_t idx = (b * T + t) * H + n;
@@ -516,14 +532,14 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
         }
       {
         float* gvb = (float*)malloc(H * sizeof(float));
-        for (size_t t = T - 1; t-- > 0;) {
+        for (size_t t = T - 1; t-- > 0 && mode != 2;) {
           for (size_t n = 0; n < H; ++n) gvb[n] = 0.0f;
           for (size_t b = 0; b < B; ++b)
             for (size_t n = 0; n < H; ++n) {
               const size_t idx = (b * T + t) * H + n;
-              gvb[n] += dIh[idx] * V[idx];
+              gvb[n * bs] += dIh[idx] * V[idx];
             }
-          for (size_t n = 0; n < H; ++n)
+          for (size_t n = 0; n < (bs ? H : 1); ++n)
             if (beta[n] > 0.0f && beta[n] < 1.0f) gbeta[n] += gvb[n];
         }
         free(gvb);

@@ -54,6 +54,12 @@ typedef struct orc_net {
   float slope;                 /* ActivationDesc.slope                   */
   float aux;                   /* ActivationDesc.aux (boxcar height)     */
   int unroll;                  /* TrainConfig.unroll (optimize.hpp:130)  */
+  /* BetaMode per cell (neuron.hpp:24, network.hpp:45-53): index l < n_hidden =
+   * LIF layer l, index n_hidden = the LI readout.  0 PerNeuron (entry [H]),
+   * 1 LearnableScalar (entry [] = 1 value), 2 Fixed (entry [] = fixed_beta,
+   * not trainable).  Zero-initialised = PerNeuron everywhere.             */
+  int beta_mode[ORC_MAX_HIDDEN + 1];
+  float fixed_beta[ORC_MAX_HIDDEN + 1];
 } orc_net;
 
 /* Parameter entries in NetworkParams order (network.hpp:231-286). */

@@ -143,6 +143,27 @@ def checkpoint_fixture(ref: Lib):
     np.savez_compressed(os.path.join(GOLD, "ckpt.npz"), **vals)
 
 
+BETA_NET = Net(inp=40, hidden=(24, 20), classes=6, act="superspike", bias=True,
+               beta_mode=("scalar", "fixed", "scalar"), fixed_beta=(0.5, 0.3, 0.5), unroll=9)
+
+
+def beta_modes_fixture(ref: Lib):
+    """BetaMode::LearnableScalar / Fixed cells (neuron.hpp:56-76): init, one
+    forward/backward and 3 Adam steps, from the reference."""
+    key = ref.key_child(ref.key_from_seed(23), 0)
+    p0 = ref.init(BETA_NET, key)
+    p = p0 * np.float32(2.0)
+    x, y = ref.synth_raster(6, 5, 30, 40, 3)
+    pk = ref.pack_time(x)
+    fb = ref.forward_backward(BETA_NET, p, pk, 30, y, want_trace=True)
+    st = State(p.copy())
+    losses = [ref.train_step(BETA_NET, st, pk, 30, y)[0] for _ in range(3)]
+    np.savez_compressed(os.path.join(GOLD, "betamodes.npz"), init=p0, params=p, packed=pk, y=y,
+                        loss=np.float32(fb["loss"]), grads=fb["grads"], trace=fb["trace"],
+                        step_losses=np.array(losses, np.float32), params3=st.params, m3=st.m,
+                        v3=st.v)
+
+
 if __name__ == "__main__":
     if not have_ref():
         Lib.__init__  # noqa: B018
@@ -163,4 +184,6 @@ if __name__ == "__main__":
         opts_fixture(ref)
     if only in (None, "ckpt"):
         checkpoint_fixture(ref)
+    if only in (None, "betamodes"):
+        beta_modes_fixture(ref)
     print("golden fixtures written to", GOLD)

@@ -233,3 +233,45 @@ def test_opts_vs_reference_live(orc, cfg):
         for _ in range(2):
             assert orc.train_step(net, s1, pk, T, y, opts=o) == ref.train_step(net, s2, pk, T, y, opts=o)
         assert np.array_equal(s1.params, s2.params) and np.array_equal(s1.m, s2.m)
+
+
+BETA_NET = Net(inp=40, hidden=(24, 20), classes=6, act="superspike", bias=True,
+               beta_mode=("scalar", "fixed", "scalar"), fixed_beta=(0.5, 0.3, 0.5), unroll=9)
+
+
+def test_beta_modes_golden_bit_exact(orc, golden):
+    """LearnableScalar / Fixed beta (neuron.hpp:56-76, autodiff.hpp:191-205 for the
+    broadcast gradient): the C restatement equals reference-made fixtures."""
+    g = golden("betamodes")
+    assert np.array_equal(orc.init(BETA_NET, orc.key_child(orc.key_from_seed(23), 0)), g["init"])
+    fb = orc.forward_backward(BETA_NET, g["params"], g["packed"], 30, g["y"], want_trace=True)
+    assert fb["loss"] == g["loss"] and np.array_equal(fb["grads"], g["grads"])
+    assert np.array_equal(fb["trace"], g["trace"])
+    st = State(g["params"].copy())
+    losses = [orc.train_step(BETA_NET, st, g["packed"], 30, g["y"])[0] for _ in range(3)]
+    assert np.array_equal(np.array(losses, np.float32), g["step_losses"])
+    assert np.array_equal(st.params, g["params3"]) and np.array_equal(st.m, g["m3"])
+    assert np.array_equal(st.v, g["v3"])
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref needs /root/reference")
+@pytest.mark.parametrize("modes", [("scalar", "scalar", "fixed"), ("fixed", "per_neuron", "scalar")])
+def test_beta_modes_vs_reference_live(orc, modes):
+    from oracle.pyoracle import Opts
+    ref = Lib("ref")
+    net = Net(inp=30, hidden=(16, 12), classes=5, beta_mode=modes, fixed_beta=(0.6, 0.4, 0.8), unroll=5)
+    assert orc.entries(net) == ref.entries(net)
+    key = orc.key_from_seed(41)
+    p = orc.init(net, key)
+    assert np.array_equal(p, ref.init(net, key))
+    p = p * np.float32(2.5)
+    x, y = orc.synth_raster(5, 6, 23, 30, 12)
+    pk = orc.pack_time(x)
+    a = orc.forward_backward(net, p, pk, 23, y)
+    b = ref.forward_backward(net, p, pk, 23, y)
+    assert a["loss"] == b["loss"] and np.array_equal(a["grads"], b["grads"])
+    for o in (Opts(), Opts(optimizer="sgd")):
+        s1, s2 = State(p.copy()), State(p.copy())
+        for _ in range(2):
+            assert orc.train_step(net, s1, pk, 23, y, opts=o) == ref.train_step(net, s2, pk, 23, y, opts=o)
+        assert np.array_equal(s1.params, s2.params) and np.array_equal(s1.m, s2.m)
