@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 2
+#define SNN_ABI_VERSION 3
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -66,6 +66,12 @@ typedef struct snn_network_desc {
   int32_t activation;   /* snn_activation                   */
   float slope;          /* ActivationDesc.slope             */
   float aux;            /* ActivationDesc.aux               */
+  /* BetaMode per cell (neuron.hpp:24; LIFLayer/LILayer.beta_mode): index l <
+   * n_hidden = LIF layer l, index n_hidden = the LI readout.  0 PerNeuron (entry
+   * [H]), 1 LearnableScalar (entry [], one value), 2 Fixed (entry [] = fixed_beta,
+   * not trainable).  Zero = PerNeuron everywhere. */
+  int32_t beta_mode[SNN_MAX_HIDDEN + 1];
+  float fixed_beta[SNN_MAX_HIDDEN + 1];
 } snn_network_desc;
 
 /* TrainConfig subset that reaches the step (optimize.hpp:116-133). */

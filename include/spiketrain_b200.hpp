@@ -80,13 +80,19 @@ struct LinearLayer {
   std::size_t out = 0;
   bool bias = true;
 };
+enum class BetaMode { PerNeuron, LearnableScalar, Fixed };  // neuron.hpp:24
+
 struct LIFLayer {
   std::vector<std::size_t> shape;
   ActivationDesc activation = {"superspike", 25.0, 0.0};
+  BetaMode beta_mode = BetaMode::PerNeuron;
+  double fixed_beta = 0.5;
   double threshold = 1.0;
 };
 struct LILayer {
   std::vector<std::size_t> shape;
+  BetaMode beta_mode = BetaMode::PerNeuron;
+  double fixed_beta = 0.5;
 };
 using Layer = std::variant<LinearLayer, LIFLayer, LILayer>;
 
@@ -168,11 +174,16 @@ inline snn_network_desc describe(const NetworkSpec& s) {
     d.activation = activation_id(lif->activation.name);
     d.slope = float(lif->activation.slope);
     d.aux = float(lif->activation.aux);
+    d.beta_mode[i] = int32_t(lif->beta_mode);
+    d.fixed_beta[i] = float(lif->fixed_beta);
   }
   const auto* lin = std::get_if<LinearLayer>(&s.layers[s.layers.size() - 2]);
   if (!lin || !std::holds_alternative<LILayer>(s.layers.back()))
     throw UnsupportedError("readout must be Linear + LI");
   d.classes = int32_t(lin->out);
+  const auto& li = std::get<LILayer>(s.layers.back());
+  d.beta_mode[d.n_hidden] = int32_t(li.beta_mode);
+  d.fixed_beta[d.n_hidden] = float(li.fixed_beta);
   return d;
 }
 

@@ -160,6 +160,9 @@ struct EntryHost {
   std::string name;
   int kind, layer, rows, cols;
   size_t offset, size;
+  int beta_mode = 0;  // beta entries: 0 per neuron [H], 1 scalar [], 2 fixed [] (constant)
+  bool trainable() const { return !(kind == kEntryBeta && beta_mode == 2); }
+  int ndim() const { return kind == kEntryW ? 2 : (kind == kEntryBeta && beta_mode != 0 ? 0 : 1); }
 };
 
 struct Dataset {
@@ -368,6 +371,8 @@ struct snn_engine {
     if (n.activation < 0 || n.activation > 4) fail(SNN_ERR_ARGUMENT, "unknown activation");
     if (n.activation != SNN_ACT_CUSTOM && !(n.slope > 0.0f))
       fail(SNN_ERR_ARGUMENT, "activation slope must be positive");
+    for (int l = 0; l <= n.n_hidden; ++l)
+      if (n.beta_mode[l] < 0 || n.beta_mode[l] > 2) fail(SNN_ERR_ARGUMENT, "unknown beta mode");
     if (n.activation == SNN_ACT_BOXCAR && !(n.aux > 0.0f))
       fail(SNN_ERR_ARGUMENT, "boxcar: width and height must be positive");
     if (cfg.batch_size < 1) fail(SNN_ERR_ARGUMENT, "train: batch size 0");
@@ -469,9 +474,11 @@ struct snn_engine {
         entries.push_back({"l" + std::to_string(lin) + ".b", kEntryB, j, 1, N[j], off, size_t(N[j])});
         off += N[j];
       }
-      entries.push_back({"l" + std::to_string(cell) + ".beta", kEntryBeta, j, 1, N[j], off,
-                         size_t(N[j])});
-      off += N[j];
+      // BetaMode (neuron.hpp:56-76): per-neuron [N] or one value (scalar / fixed)
+      const int bm = n.beta_mode[j];
+      const size_t bsz = bm == 0 ? size_t(N[j]) : 1;
+      entries.push_back({"l" + std::to_string(cell) + ".beta", kEntryBeta, j, 1, N[j], off, bsz, bm});
+      off += bsz;
     }
     n_params = off;
   }
@@ -580,7 +587,10 @@ struct snn_engine {
         hostrng::truncated_normal(hostrng::child(lk, 0), e.size, 0.0f, sd, h.data() + e.offset);
       } else if (e.kind == kEntryBeta) {
         const uint64_t lk = hostrng::child(key, uint64_t(2 * e.layer + 1));
-        hostrng::truncated_normal(hostrng::child(lk, 2), e.size, 0.5f, 0.25f, h.data() + e.offset);
+        if (e.beta_mode == 2)
+          h[e.offset] = net.fixed_beta[e.layer];  // Tensor::scalar(fixed_beta)
+        else  // per-neuron [H] or LearnableScalar [] from the same key
+          hostrng::truncated_normal(hostrng::child(lk, 2), e.size, 0.5f, 0.25f, h.data() + e.offset);
       }
     }
     upload_params(h.data());
@@ -598,6 +608,7 @@ struct snn_engine {
       out[i].layer = e.layer;
       out[i].rows = e.rows;
       out[i].cols = e.cols;
+      out[i].beta_mode = e.beta_mode;
       out[i].offset = int64_t(e.offset);
       ++i;
     }
@@ -842,6 +853,7 @@ struct snn_engine {
       for (int i = 0; i < nl; ++i) {
         FwdLayer& ly = f.lay[i];
         ly.beta = params.p + entry_of(kEntryBeta, l + i).offset;
+        ly.beta_stride = net.beta_mode[l + i] == 0 ? 1 : 0;
         ly.bias = net.bias ? params.p + entry_of(kEntryB, l + i).offset : nullptr;
         ly.v_out = V[l + i].p;
         ly.s_np = s_np[l + i].p;
@@ -871,6 +883,7 @@ struct snn_engine {
       r.w = params.p + entry_of(kEntryW, L).offset;
       r.bias = net.bias ? params.p + entry_of(kEntryB, L).offset : nullptr;
       r.beta = params.p + entry_of(kEntryBeta, L).offset;
+    r.beta_stride = net.beta_mode[L] == 0 ? 1 : 0;
       r.d3_planes = di[L].p;
       r.loss_b = loss_b.p;
       r.correct_b = correct_b.p;
@@ -897,6 +910,7 @@ struct snn_engine {
       BwdArgs bw{};
       bw.v_in = V[l].p;
       bw.beta = params.p + entry_of(kEntryBeta, l).offset;
+      bw.beta_stride = net.beta_mode[l] == 0 ? 1 : 0;
       bw.di_planes = di[l].p;
       bw.dbeta_part = dbeta[l].p;
       bw.dbias_part = net.bias ? dbias[l].p : nullptr;
@@ -1308,22 +1322,24 @@ snn_status snn_save_checkpoint(snn_engine* e, const char* path, const char* conf
     for (const auto& en : e->entries) {
       put_u16(o, uint16_t(en.name.size()));
       put_bytes(o, en.name.data(), en.name.size());
-      put_u8(o, 1);  // every entry trainable (BetaMode::PerNeuron, network.hpp:231-286)
-      if (en.kind == kEntryW) {
-        put_u32(o, 2);
+      put_u8(o, en.trainable() ? 1 : 0);  // Fixed beta is not trainable (neuron.hpp:32)
+      put_u32(o, uint32_t(en.ndim()));
+      if (en.ndim() == 2) {
         put_u64(o, uint64_t(en.rows));
         put_u64(o, uint64_t(en.cols));
-      } else {
-        put_u32(o, 1);
+      } else if (en.ndim() == 1) {
         put_u64(o, uint64_t(en.cols));
       }
       put_bytes(o, p.data() + en.offset, en.size * 4);
     }
     put_u8(o, e->cfg.optimizer == 1 ? 1 : 0);
     put_u64(o, uint64_t(step));
-    for (const auto& en : e->entries) put_bytes(o, m.data() + en.offset, en.size * 4);
+    // optimizer state covers the trainable entries only (init_optimizer, optimize.hpp:37-48)
+    for (const auto& en : e->entries)
+      if (en.trainable()) put_bytes(o, m.data() + en.offset, en.size * 4);
     if (e->cfg.optimizer != 1)
-      for (const auto& en : e->entries) put_bytes(o, v.data() + en.offset, en.size * 4);
+      for (const auto& en : e->entries)
+        if (en.trainable()) put_bytes(o, v.data() + en.offset, en.size * 4);
     FILE* f = std::fopen(path, "wb");
     if (!f) fail(SNN_ERR_IO, "cannot open for writing: %s", path);
     const size_t w = std::fwrite(o.data(), 1, o.size(), f);
@@ -1371,10 +1387,10 @@ snn_status snn_load_checkpoint(snn_engine* e, const char* path, char* config_out
       if (nd > 16) fail(SNN_ERR_FORMAT, "implausible tensor rank at byte offset %zu", rd.off - 4);
       std::vector<uint64_t> dims(nd);
       for (auto& d : dims) d = rd.u64();
-      const bool w2 = en.kind == kEntryW;
-      const bool shape_ok = w2 ? (nd == 2 && dims[0] == uint64_t(en.rows) && dims[1] == uint64_t(en.cols))
-                               : (nd == 1 && dims[0] == uint64_t(en.cols));
-      if (name != en.name || !shape_ok || trainable != 1)
+      const bool shape_ok = int(nd) == en.ndim() &&
+                            (nd == 0 || (nd == 1 && dims[0] == uint64_t(en.cols)) ||
+                             (nd == 2 && dims[0] == uint64_t(en.rows) && dims[1] == uint64_t(en.cols)));
+      if (name != en.name || !shape_ok || trainable != (en.trainable() ? 1 : 0))
         fail(SNN_ERR_SHAPE, "checkpoint entry %s does not match network entry %s", name.c_str(),
              en.name.c_str());
       rd.take(p.data() + en.offset, en.size * 4);
@@ -1383,9 +1399,11 @@ snn_status snn_load_checkpoint(snn_engine* e, const char* path, char* config_out
     if (int(kind) != (e->cfg.optimizer == 1 ? 1 : 0))
       fail(SNN_ERR_ARGUMENT, "checkpoint optimizer kind %u differs from the engine's", unsigned(kind));
     const int64_t step = int64_t(rd.u64());
-    for (const auto& en : e->entries) rd.take(m.data() + en.offset, en.size * 4);
+    for (const auto& en : e->entries)
+      if (en.trainable()) rd.take(m.data() + en.offset, en.size * 4);
     if (kind == 0)
-      for (const auto& en : e->entries) rd.take(v.data() + en.offset, en.size * 4);
+      for (const auto& en : e->entries)
+        if (en.trainable()) rd.take(v.data() + en.offset, en.size * 4);
     e->upload_params(p.data());
     CK(cudaMemcpyAsync(e->m.p, m.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
     CK(cudaMemcpyAsync(e->v.p, v.data(), n * 4, cudaMemcpyHostToDevice, e->stream));

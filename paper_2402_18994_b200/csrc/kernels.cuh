@@ -165,7 +165,8 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // ============================================================================
 // One hidden LIF layer of a forward launch.
 struct FwdLayer {
-  const float* beta;      // [H]
+  const float* beta;      // [H], or one value (beta_stride 0: scalar / fixed BetaMode)
+  int beta_stride;
   const float* bias;      // [H] or nullptr
   float* v_out;           // [B][T_pad][H_pad]
   uint32_t* s_np;         // [B][T_pad][H_pad/32]
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const size_t tp_words = size_t(a.B) * a.T_pad / 32;
     for (int li = 0; li < a.n_layers; ++li) {
       const FwdLayer& ly = a.lay[li];
-      const float vb = clip01(n < ly.H ? ly.beta[n] : 0.0f);
+      const float vb = clip01(n < ly.H ? ly.beta[n * ly.beta_stride] : 0.0f);
       const float bn = (ly.bias != nullptr && n < ly.H) ? ly.bias[n] : 0.0f;
       const size_t hw = size_t(ly.H_pad) / 32;
       // fused: lane j writes the next layer's B row t0+j (its quadrant's 32 spikes
@@ -563,7 +564,8 @@ struct ReadoutArgs {
   const int32_t* labels;    // dataset labels [N]
   const float* w;           // readout W [HL][C] f32 (master)
   const float* bias;        // [C] or nullptr
-  const float* beta;        // [C]
+  const float* beta;        // [C] (or one value: beta_stride 0)
+  int beta_stride;
   __nv_bfloat16* d3_planes; // [3][64][B*T_pad] (class rows, (b,t) contiguous)
   float* loss_b;            // [B] lse - logit_y
   int32_t* correct_b;       // [B]
@@ -608,7 +610,7 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
   __shared__ int s_label;
   if (tid == 0) s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
-  const float beta_l = lane < C ? a.beta[lane] : 0.0f;
+  const float beta_l = lane < C ? a.beta[lane * a.beta_stride] : 0.0f;
   {
     // W rows padded to Cp floats (zeros in the padding) and the spike words
     const int nw = a.HL * C;
@@ -846,7 +848,8 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
 // ============================================================================
 struct BwdArgs {
   const float* v_in;           // V_l [B][T_pad][H_pad]
-  const float* beta;           // [H]
+  const float* beta;           // [H] (or one value: beta_stride 0)
+  int beta_stride;
   __nv_bfloat16* di_planes;    // out: dI_l planes [3][H_pad][B*T_pad]
   float* dbeta_part;           // [B][H]
   float* dbias_part;           // [B][H] or nullptr
@@ -1071,7 +1074,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     const int q = warp & 3, sg = warp >> 2;
     const int sidx = sg * 128 + q * 32 + lane;
     const int n = nt * 128 + q * 32 + lane;
-    const float vb = clip01(n < a.H ? a.beta[n] : 0.0f);
+    const float vb = clip01(n < a.H ? a.beta[n * a.beta_stride] : 0.0f);
     const float theta = a.theta, ntheta = -a.theta;
     const size_t plane = size_t(a.H_pad) * cols_total;
     __nv_bfloat16* __restrict__ drow = a.di_planes + size_t(n) * cols_total + size_t(b) * a.T_pad;
@@ -1508,7 +1511,8 @@ enum EntryKind : int32_t { kEntryW = 0, kEntryB = 1, kEntryBeta = 2 };
 
 struct Entry {
   int32_t kind, layer;    // layer = Linear index j (W, b) or cell index (beta)
-  int32_t rows, cols;     // W: [K][N]; b/beta: [1][N]
+  int32_t rows, cols;     // W: [K][N]; b/beta: [1][N] (beta: N = cell width, also when scalar)
+  int32_t beta_mode;      // beta: 0 per neuron, 1 learnable scalar, 2 fixed (no gradient)
   int64_t offset;         // into the flat vector
 };
 
@@ -1637,7 +1641,13 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     const float* __restrict__ src =
         (en.kind == kEntryB ? a.dbias_part[en.layer] : a.dbeta_part[en.layer]) + li;
     float g = 0.0f;
-    for (int b = lane; b < a.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
+    if (en.kind == kEntryBeta && en.beta_mode != 0) {
+      // scalar beta: every (b, n) partial; fixed beta: no gradient
+      if (en.beta_mode == 1)
+        for (int q = lane; q < a.B * en.cols; q += 32) g = __fadd_rn(g, __ldg(src + q));
+    } else {
+      for (int b = lane; b < a.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
     if (lane == 0) {
@@ -1794,7 +1804,14 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
       const float* __restrict__ src =
           (en.kind == kEntryB ? r.dbias_part[en.layer] : r.dbeta_part[en.layer]) + li;
       float g = 0.0f;
-      for (int b = lane; b < r.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
+      if (en.kind == kEntryBeta && en.beta_mode != 0) {
+        // scalar beta: every (b, n) partial (mul_bcast backward, autodiff.hpp:191-205);
+        // fixed beta is a tape constant -- no gradient, so Adam / SGD leave it as is
+        if (en.beta_mode == 1)
+          for (int q = lane; q < r.B * en.cols; q += 32) g = __fadd_rn(g, __ldg(src + q));
+      } else {
+        for (int b = lane; b < r.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
+      }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
       if (lane == 0) {

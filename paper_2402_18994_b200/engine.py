@@ -68,12 +68,14 @@ class LinearLayer:
 class LIFLayer:
     activation: ActivationDesc = field(default_factory=ActivationDesc)
     threshold: float = 1.0
-    beta_mode: str = "per_neuron"
+    beta_mode: str = "per_neuron"   # BetaMode: "per_neuron" | "scalar" | "fixed" (neuron.hpp:24)
+    fixed_beta: float = 0.5
 
 
 @dataclass
 class LILayer:
     beta_mode: str = "per_neuron"
+    fixed_beta: float = 0.5
 
 
 @dataclass
@@ -103,7 +105,11 @@ class TrainConfig:
 class _NetDesc(C.Structure):
     _fields_ = [("input", C.c_int32), ("n_hidden", C.c_int32), ("hidden", C.c_int32 * 8),
                 ("classes", C.c_int32), ("bias", C.c_int32), ("threshold", C.c_float),
-                ("activation", C.c_int32), ("slope", C.c_float), ("aux", C.c_float)]
+                ("activation", C.c_int32), ("slope", C.c_float), ("aux", C.c_float),
+                ("beta_mode", C.c_int32 * 9), ("fixed_beta", C.c_float * 9)]
+
+
+BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 
 
 class _TrainCfg(C.Structure):
@@ -128,19 +134,21 @@ def normalize(spec: NetworkSpec) -> dict:
     layers = list(spec.layers)
     if len(layers) < 4 or len(layers) % 2:
         raise UnsupportedError("engine supports [Linear, LIF]*k + Linear + LI")
-    hidden, act, thr, bias = [], None, None, None
+    hidden, act, thr, bias, modes, fixed = [], None, None, None, [], []
     for i in range(0, len(layers) - 2, 2):
         lin, cell = layers[i], layers[i + 1]
         if not isinstance(lin, LinearLayer) or not isinstance(cell, LIFLayer):
             raise UnsupportedError(f"layer {i}: expected Linear + LIF")
-        if cell.beta_mode != "per_neuron":
-            raise UnsupportedError("only BetaMode::PerNeuron")
+        if cell.beta_mode not in BETA_MODES:
+            raise ArgumentError(f"unknown beta mode: {cell.beta_mode}")
         if act is not None and (cell.activation != act or cell.threshold != thr):
             raise UnsupportedError("all LIF layers must share activation and threshold")
         if bias is not None and lin.bias != bias:
             raise UnsupportedError("all Linear layers must share the bias flag")
         act, thr, bias = cell.activation, cell.threshold, lin.bias
         hidden.append(int(lin.out))
+        modes.append(cell.beta_mode)
+        fixed.append(float(cell.fixed_beta))
     lin, cell = layers[-2], layers[-1]
     if not isinstance(lin, LinearLayer) or not isinstance(cell, LILayer):
         raise UnsupportedError("readout must be Linear + LI")
@@ -148,9 +156,12 @@ def normalize(spec: NetworkSpec) -> dict:
         raise UnsupportedError("all Linear layers must share the bias flag")
     if act.name not in ACTIVATIONS:
         raise ArgumentError(f"unknown activation: {act.name}")
+    if cell.beta_mode not in BETA_MODES:
+        raise ArgumentError(f"unknown beta mode: {cell.beta_mode}")
     return dict(input=inp, hidden=hidden, classes=int(lin.out), bias=bool(bias),
                 threshold=float(thr), activation=act.name, slope=float(act.slope),
-                aux=float(act.aux))
+                aux=float(act.aux), beta_mode=modes + [cell.beta_mode],
+                fixed_beta=fixed + [float(cell.fixed_beta)])
 
 
 def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False) -> NetworkSpec:
@@ -226,6 +237,9 @@ class Engine:
         n.activation = ACTIVATIONS[d["activation"]]
         n.slope = d["slope"]
         n.aux = d["aux"]
+        for i, (bm, fb) in enumerate(zip(d["beta_mode"], d["fixed_beta"])):
+            n.beta_mode[i] = BETA_MODES[bm]
+            n.fixed_beta[i] = fb
         c = _TrainCfg()
         c.batch_size = int(cfg.batch_size)
         c.time_steps = int(time_steps)

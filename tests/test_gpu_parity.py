@@ -518,3 +518,44 @@ def test_checkpoint_resume_is_bit_exact(orc, tmp_path):
     other = make_engine(Net(inp=30, hidden=(16, 12), classes=5), 4, 19)  # no bias entries
     with pytest.raises(ShapeError):
         other.load_checkpoint(path)
+
+
+BETA_NET = Net(inp=40, hidden=(24, 20), classes=6, act="superspike", bias=True,
+               beta_mode=("scalar", "fixed", "scalar"), fixed_beta=(0.5, 0.3, 0.5), unroll=9)
+
+
+def beta_engine(net, B, T, **kw):
+    from paper_2402_18994_b200 import (Engine, LIFLayer, LILayer, LinearLayer, NetworkSpec,
+                                       TrainConfig, default_activation_desc)
+    layers = []
+    for i, h in enumerate(net.hidden):
+        layers += [LinearLayer(h, net.bias),
+                   LIFLayer(default_activation_desc(net.act), beta_mode=net.beta_mode[i],
+                            fixed_beta=net.fixed_beta[i])]
+    layers += [LinearLayer(net.classes, net.bias),
+               LILayer(beta_mode=net.beta_mode[-1], fixed_beta=net.fixed_beta[-1])]
+    return Engine(NetworkSpec([net.inp], layers), TrainConfig(batch_size=B, **kw), T)
+
+
+def test_beta_modes_match_reference_fixture(orc, golden):
+    """BetaMode::LearnableScalar / Fixed cells (neuron.hpp:56-76): init bit-exact,
+    loss / gradients / 3 Adam steps against the reference-made fixture."""
+    g = golden("betamodes")
+    T, B = 30, int(g["y"].size)
+    eng = beta_engine(BETA_NET, B, T, seed=23)
+    assert np.array_equal(eng.get_params(), g["init"])
+    eng.stage_dataset(g["packed"], g["y"])
+    eng.set_params(g["params"])
+    rows = np.arange(B, dtype=np.uint32)
+    loss, _ = eng.forward_backward(rows)
+    assert abs(loss - g["loss"]) <= REL_TOL * abs(g["loss"])
+    check_grads(orc, BETA_NET, eng.get_grads(), g["grads"])
+    for i in range(3):
+        l2, _ = eng.train_step(rows)
+        assert abs(l2 - g["step_losses"][i]) <= REL_TOL * abs(g["step_losses"][i])
+    assert relnorm(eng.get_params(), g["params3"]) <= 1e-4
+    o = {n: (off, sz) for n, off, sz in orc.entries(BETA_NET)}
+    off, sz = o["l3.beta"]                    # fixed: untouched, no optimizer state
+    assert sz == 1 and eng.get_params()[off] == g["params"][off] == g["params3"][off]
+    m, v, _ = eng.get_opt_state()
+    assert m[off] == 0 and v[off] == 0
