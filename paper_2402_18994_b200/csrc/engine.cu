@@ -425,6 +425,7 @@ struct snn_engine {
       const double xrun = double(wg_xrun_bytes(IN_pad));
       // mg cap: 2 stages of (mg A tiles + 3 B planes + dataset run) must fit
       wg_mg_max = std::max(1, std::min(kWgMgMax, int((budget / 2 - 3 * 128 * 128 - xrun) / kPlaneTile)));
+      wg_mg_max = std::min(wg_mg_max, env_int("SNN_WG_MG", kWgMgMax));  // M-tiles per CTA cap
       double fixed[kMaxLayers], per_unit[kMaxLayers], units[kMaxLayers];
       const double iters = double(B) * (T_pad / 64);
       for (int j = 0; j <= L; ++j) {
