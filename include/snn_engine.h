@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 3
+#define SNN_ABI_VERSION 4
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -87,6 +87,14 @@ typedef struct snn_train_config {
   float momentum;       /* SGD momentum (TrainConfig default 0.9) */
   int32_t loss;         /* 0 integral CE (objective.hpp:88-114), 1 spike-rate MSE (:139-183) */
   float rate_hi, rate_lo; /* rate-MSE targets on / off the true class (defaults 0.9 / 0.1) */
+  /* shift_augment in the epoch loop (optimize.hpp:131-132, 276-278, data.hpp:216-227):
+   * when max_shift > 0 every batch of snn_train_epochs is rolled along the feature
+   * axis by sum_i randint(child(epoch_key, 1 + b), i, -max_shift, max_shift).
+   * Axes 0 / 1 are rejected like train() does; with max_shift > 0 only the feature
+   * axis (2 or -1) is supported. */
+  int32_t max_shift;
+  int32_t n_shift_axes; /* 0..4 */
+  int32_t shift_axes[4];
 } snn_train_config;
 
 typedef struct snn_engine snn_engine;

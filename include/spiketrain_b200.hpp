@@ -114,6 +114,8 @@ struct TrainConfig {
   LossKind loss = LossKind::IntegralCrossentropy;
   double rate_hi = 0.9;  // rate-MSE targets
   double rate_lo = 0.1;
+  std::int64_t max_shift = 0;     // shift augmentation on packed batches
+  std::vector<long> shift_axes;   // feature axis only (2 or -1)
   std::uint64_t seed = 0;
   std::size_t unroll = 32;
 };
@@ -210,6 +212,10 @@ class TrainState {
     c.loss = cfg.loss == LossKind::SpikeRateMse ? 1 : 0;
     c.rate_hi = float(cfg.rate_hi);
     c.rate_lo = float(cfg.rate_lo);
+    if (cfg.shift_axes.size() > 4) throw ArgumentError("train: at most 4 shift axes");
+    c.max_shift = int32_t(cfg.max_shift);
+    c.n_shift_axes = int32_t(cfg.shift_axes.size());
+    for (std::size_t i = 0; i < cfg.shift_axes.size(); ++i) c.shift_axes[i] = int32_t(cfg.shift_axes[i]);
     snn_engine* e = nullptr;
     check(snn_engine_create(&d, &c, device, &e), nullptr);
     eng_.reset(e);

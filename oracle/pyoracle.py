@@ -36,7 +36,8 @@ BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 
 class _Opts(C.Structure):
     _fields_ = [("optimizer", C.c_int), ("momentum", C.c_float), ("loss", C.c_int),
-                ("rate_hi", C.c_float), ("rate_lo", C.c_float)]
+                ("rate_hi", C.c_float), ("rate_lo", C.c_float), ("max_shift", C.c_int),
+                ("n_shift_axes", C.c_int), ("shift_axes", C.c_int * 4)]
 
 
 @dataclass
@@ -48,10 +49,16 @@ class Opts:
     loss: str = "ce"
     rate_hi: float = 0.9
     rate_lo: float = 0.1
+    max_shift: int = 0          # shift_augment (epoch loop only)
+    shift_axes: tuple = ()
 
     def c(self) -> _Opts:
-        return _Opts(1 if self.optimizer == "sgd" else 0, self.momentum,
-                     1 if self.loss == "rate_mse" else 0, self.rate_hi, self.rate_lo)
+        o = _Opts(1 if self.optimizer == "sgd" else 0, self.momentum,
+                  1 if self.loss == "rate_mse" else 0, self.rate_hi, self.rate_lo,
+                  self.max_shift, len(self.shift_axes))
+        for i, a in enumerate(self.shift_axes):
+            o.shift_axes[i] = a
+        return o
 
 
 @dataclass
@@ -127,6 +134,7 @@ class Lib:
         f("train_step").restype = C.c_int
         f("train_step_ex").restype = C.c_int
         f("train_epochs").restype = C.c_int
+        f("train_epochs_ex").restype = C.c_int
         self._f = f
 
     # ---- rng -----------------------------------------------------------
@@ -294,14 +302,15 @@ class Lib:
         return loss.value, acc.value
 
     def train_epochs(self, net: Net, state: "State", packed, y, t, batch, epochs,
-                     seed, lr=1e-3):
+                     seed, lr=1e-3, opts: "Opts" = None):
         n = net.c()
         packed = np.ascontiguousarray(packed, np.uint8)
         y = np.ascontiguousarray(y, np.int64)
         metrics = np.zeros((epochs, 2), np.float64)
         st = C.c_uint64(state.step)
-        rc = self._f("train_epochs")(
-            C.byref(n), _ptr(state.params, C.c_float), _ptr(state.m, C.c_float),
+        o = (opts or Opts()).c()
+        rc = self._f("train_epochs_ex")(
+            C.byref(n), C.byref(o), _ptr(state.params, C.c_float), _ptr(state.m, C.c_float),
             _ptr(state.v, C.c_float), C.byref(st), _ptr(packed, C.c_uint8),
             _ptr(y, C.c_int64), C.c_size_t(packed.shape[0]), C.c_size_t(t),
             C.c_size_t(batch), C.c_size_t(epochs), C.c_uint64(seed), C.c_float(lr),

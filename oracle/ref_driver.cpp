@@ -345,12 +345,33 @@ int ref_train_step_ex(const orc_net* n, const orc_train_opts* opts, float* param
   }
 }
 
+int ref_train_epochs_ex(const orc_net* n, const orc_train_opts* opts, float* params,
+                        float* m, float* v, uint64_t* step, const uint8_t* packed,
+                        const int64_t* y, size_t count, size_t t_steps, size_t batch,
+                        size_t epochs, uint64_t seed, float lr, double* metrics);
+
 int ref_train_epochs(const orc_net* n, float* params, float* m, float* v,
                      uint64_t* step, const uint8_t* packed, const int64_t* y,
                      size_t count, size_t t_steps, size_t batch, size_t epochs,
                      uint64_t seed, float lr, double* metrics) {
+  return ref_train_epochs_ex(n, nullptr, params, m, v, step, packed, y, count, t_steps, batch,
+                             epochs, seed, lr, metrics);
+}
+
+int ref_train_epochs_ex(const orc_net* n, const orc_train_opts* opts, float* params,
+                        float* m, float* v, uint64_t* step, const uint8_t* packed,
+                        const int64_t* y, size_t count, size_t t_steps, size_t batch,
+                        size_t epochs, uint64_t seed, float lr, double* metrics) {
   try {
-    TrainState<float> st = make_state(n, params, m, v, *step, lr);
+    TrainState<float> st = make_state(n, params, m, v, *step, lr, opts);
+    if (opts) {
+      // train(spec, cfg, data)'s axis check (optimize.hpp:241-245); the resume
+      // overload train(st, data) called below does not repeat it
+      for (int i = 0; i < opts->n_shift_axes; ++i)
+        if (opts->shift_axes[i] == 0 || opts->shift_axes[i] == 1) return 4;
+      st.cfg.max_shift = opts->max_shift;
+      for (int i = 0; i < opts->n_shift_axes; ++i) st.cfg.shift_axes.push_back(opts->shift_axes[i]);
+    }
     st.cfg.batch_size = batch;
     st.cfg.epochs = epochs;
     st.cfg.seed = seed;

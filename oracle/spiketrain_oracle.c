@@ -267,7 +267,7 @@ static void matmul_rows(const float* a, size_t rows, size_t k, const float* w,
   }
 }
 
-static const orc_train_opts k_default_opts = {0, 0.9f, 0, 0.9f, 0.1f};
+static const orc_train_opts k_default_opts = {0, 0.9f, 0, 0.9f, 0.1f, 0, 0, {0, 0, 0, 0}};
 
 int orc_forward_backward(const orc_net* net, const float* params,
                          const uint8_t* packed, size_t B, size_t T,
@@ -616,6 +616,25 @@ int orc_train_epochs(const orc_net* net, float* params, float* m, float* v,
                      uint64_t* step, const uint8_t* packed, const int64_t* y,
                      size_t n, size_t t_steps, size_t batch, size_t epochs,
                      uint64_t seed, float lr, double* metrics) {
+  return orc_train_epochs_ex(net, NULL, params, m, v, step, packed, y, n, t_steps, batch,
+                             epochs, seed, lr, metrics);
+}
+
+int orc_train_epochs_ex(const orc_net* net, const orc_train_opts* opts, float* params,
+                        float* m, float* v, uint64_t* step, const uint8_t* packed,
+                        const int64_t* y, size_t n, size_t t_steps, size_t batch,
+                        size_t epochs, uint64_t seed, float lr, double* metrics) {
+  if (!opts) opts = &k_default_opts;
+  /* train() rejects the batch / packed-time axes by number (optimize.hpp:241-245);
+   * max_shift <= 0 never reaches shift_augment (optimize.hpp:276).  With a flat
+   * feature axis the only rolls that stay on features are 2 and -1; -2 / -3
+   * (which the reference would apply to time / batch) are refused here. */
+  if (opts->n_shift_axes < 0 || opts->n_shift_axes > 4) return 4;
+  for (int i = 0; i < opts->n_shift_axes; ++i) {
+    const int ax = opts->shift_axes[i];
+    if (ax == 0 || ax == 1) return 4;
+    if (opts->max_shift > 0 && ax != 2 && ax != -1) return 4;
+  }
   if (batch == 0 || batch > n) return 1;
   const size_t ex = ((t_steps + 7) / 8) * (size_t)net->in;
   const uint64_t master = orc_key_from_seed(seed);
@@ -634,10 +653,31 @@ int orc_train_epochs(const orc_net* net, float* params, float* m, float* v,
         memcpy(bx + i * ex, packed + src * ex, ex);
         by[i] = y[src];
       }
+      if (opts->max_shift > 0 && opts->n_shift_axes > 0) {
+        /* shift_augment (data.hpp:216-227): roll(bx, shifts, axes), every axis the
+         * feature axis, out[(k + s) mod in] = in[k] (ops.hpp:423-453) */
+        const uint64_t bk = orc_key_child(ek, 1 + bi);
+        const uint64_t range = (uint64_t)(2 * (int64_t)opts->max_shift);
+        int64_t sh = 0;
+        for (int ax = 0; ax < opts->n_shift_axes; ++ax)
+          sh += -(int64_t)opts->max_shift + (int64_t)(orc_key_bits(bk, (uint64_t)ax) % range);
+        const int64_t in = net->in;
+        sh %= in;
+        if (sh < 0) sh += in;
+        if (sh) {
+          uint8_t* row = (uint8_t*)malloc((size_t)in);
+          for (size_t r = 0; r < batch * ((t_steps + 7) / 8); ++r) {
+            uint8_t* p = bx + r * (size_t)in;
+            for (int64_t k = 0; k < in; ++k) row[(k + sh) % in] = p[k];
+            memcpy(p, row, (size_t)in);
+          }
+          free(row);
+        }
+      }
       float l;
       double a;
-      rc = orc_train_step(net, params, m, v, step, bx, batch, t_steps, by, lr,
-                          &l, &a);
+      rc = orc_train_step_ex(net, opts, params, m, v, step, bx, batch, t_steps, by, lr,
+                             &l, &a);
       ls += (double)l;
       as += a;
     }

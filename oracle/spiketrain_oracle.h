@@ -113,6 +113,12 @@ typedef struct orc_train_opts {
   int loss;        /* 0 integral CE (objective.hpp:88-114), 1 spike-rate MSE (:139-183) */
   float rate_hi;   /* rate-MSE target on the true class (default 0.9)               */
   float rate_lo;   /* rate-MSE target elsewhere (default 0.1)                       */
+  /* shift_augment in the epoch loop (data.hpp:216-227, optimize.hpp:278-280):
+   * per batch b and listed axis i a roll by randint(epoch_key.child(1+b), i,
+   * -max_shift, max_shift); axes must name the feature axis (2 or -1).      */
+  int max_shift;
+  int n_shift_axes;
+  int shift_axes[4];
 } orc_train_opts;
 
 /* forward_backward / train_step with TrainConfig options (NULL = defaults). */
@@ -125,6 +131,11 @@ int orc_train_step_ex(const orc_net* net, const orc_train_opts* opts,
                       float* params, float* m, float* v, uint64_t* step,
                       const uint8_t* packed, size_t batch, size_t t_steps,
                       const int64_t* targets, float lr, float* loss, double* acc);
+/* train() epoch loop with TrainConfig options, shift augmentation included. */
+int orc_train_epochs_ex(const orc_net* net, const orc_train_opts* opts, float* params,
+                        float* m, float* v, uint64_t* step, const uint8_t* packed,
+                        const int64_t* y, size_t n, size_t t_steps, size_t batch,
+                        size_t epochs, uint64_t seed, float lr, double* metrics);
 /* sgd_update over a flat buffer (optimize.hpp:69-84): m doubles as momentum. */
 void orc_sgd(float* p, const float* g, float* m, size_t n, uint64_t* step,
              float lr, float momentum);

@@ -297,6 +297,8 @@ struct snn_engine {
   // data
   Dataset data, scratch;
   DevBuf<uint32_t> rows_cur, sched;
+  DevBuf<int32_t> xshift;  // shift_augment roll of the current batch (0 = none)
+  int32_t xshift_host = 0;
   size_t sched_steps = 0;
   // tensor maps
   CUtensorMap tm_wt[kMaxLayers], tm_wb[kMaxLayers], tm_di_k[kMaxLayers], tm_di_w[kMaxLayers];
@@ -383,6 +385,16 @@ struct snn_engine {
     if (cfg.loss == 1 && !(cfg.rate_hi >= 0.0f && cfg.rate_hi <= 1.0f && cfg.rate_lo >= 0.0f &&
                            cfg.rate_lo <= 1.0f))
       fail(SNN_ERR_ARGUMENT, "spike_rate_mse: rates must lie in [0,1]");
+    // train()'s axis check (optimize.hpp:241-245); max_shift <= 0 never shifts (:276)
+    if (cfg.n_shift_axes < 0 || cfg.n_shift_axes > 4) fail(SNN_ERR_ARGUMENT, "train: 0..4 shift axes");
+    for (int i = 0; i < cfg.n_shift_axes; ++i) {
+      const int ax = cfg.shift_axes[i];
+      if (ax == 0 || ax == 1)
+        fail(SNN_ERR_ARGUMENT, "train: shift axes must name feature axes (>= 2); axis %d is the "
+             "batch/packed-time axis", ax);
+      if (cfg.max_shift > 0 && ax != 2 && ax != -1)
+        fail(SNN_ERR_UNSUPPORTED, "shift axis %d: only the (flat) feature axis 2 / -1 is supported", ax);
+    }
     B = cfg.batch_size;
     T = cfg.time_steps;
     TT = T <= 64 ? 64 : 128;
@@ -516,6 +528,7 @@ struct snn_engine {
     result_loss.alloc(1);
     result_acc.alloc(1);
     rows_cur.alloc(B);
+    xshift.alloc(1);
     CK(cudaMallocHost(&h_loss, sizeof(float)));
     CK(cudaMallocHost(&h_acc, sizeof(double)));
     CK(cudaMallocHost(&h_rows, sizeof(uint32_t) * B));
@@ -532,8 +545,9 @@ struct snn_engine {
       if (j < L) tm_di_out[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 128);
       wg_maps.m[j] = tm_di_w[j];
     }
-    CK(cudaFuncSetAttribute(k_lif_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
+    for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
@@ -752,6 +766,14 @@ struct snn_engine {
     CK(cudaGetLastError());
   }
 
+  // Roll of the next batches along the features (read by the layer-0 forward and
+  // the input wgrad from device memory, so captured graphs stay valid).
+  void set_shift(int32_t s) {
+    if (s == xshift_host) return;
+    CK(cudaMemcpyAsync(xshift.p, &s, sizeof(s), cudaMemcpyHostToDevice, stream));  // pageable: staged before return
+    xshift_host = s;
+  }
+
   void synth(size_t n, uint64_t seed) {
     if (n == 0) fail(SNN_ERR_ARGUMENT, "synth: classes, examples, and steps must be >= 1");
     Dataset& ds = data;
@@ -867,10 +889,14 @@ struct snn_engine {
       f.dbg_clk = debug ? dbg_clk.p + size_t(1 + l) * clk_region() : nullptr;
       f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
       f.in_kind = l == 0 ? 0 : 1;
+      f.xshift = l == 0 ? xshift.p : nullptr;
+      f.in_features = IN;
       f.theta = net.threshold;
       f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
       f.spb = fwd_spb(TT);
-      launch(k_lif_fwd, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128), dim3(kFwdThreads),
+      const bool shifting = l == 0 && cfg.max_shift > 0 && cfg.n_shift_axes > 0;
+      launch(shifting ? k_lif_fwd<true> : k_lif_fwd<false>, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128),
+             dim3(kFwdThreads),
              fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
       mark(evs, "lif_fwd", l);
     }
@@ -933,6 +959,8 @@ struct snn_engine {
       w.rows = rows_p;
       w.rows_slot = slot_p;
       w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
+      w.xshift = xshift.p;
+      w.in_features = IN;
       w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * clk_region() : nullptr;
       int blocks = 0;
       for (int j = 0; j <= L; ++j) {
@@ -1514,6 +1542,12 @@ snn_status snn_train_epochs_from(snn_engine* e, size_t first_epoch, size_t epoch
     if (gb > n) fail(SNN_ERR_ARGUMENT, "shuffle: batch size %zu for %zu examples", gb, n);
     const uint64_t master = hostrng::from_seed(e->cfg.seed);
     const size_t nb = n / gb;
+    struct ShiftReset {  // an interrupted epoch must not leave later steps rolled
+      snn_engine* e;
+      ~ShiftReset() {
+        try { e->set_shift(0); } catch (...) {}
+      }
+    } shift_reset{e};
     for (size_t k = 0; k < epochs; ++k) {
       const size_t ep = first_epoch + k;
       const uint64_t ek = hostrng::child(master, 1 + ep);
@@ -1522,10 +1556,12 @@ snn_status snn_train_epochs_from(snn_engine* e, size_t first_epoch, size_t epoch
       for (size_t bi = 0; bi < nb; ++bi) {
         float l;
         double a;
+        e->set_shift(hostrng::batch_roll(ek, bi, e->cfg.max_shift, e->cfg.n_shift_axes, e->IN));
         e->step_rows(perm.data() + bi * gb + size_t(e->rank) * e->B, e->data, 1, &l, &a);
         ls += double(l);
         as += a;
       }
+      e->set_shift(0);
       if (metrics) {
         metrics[2 * k] = ls / double(nb ? nb : 1);
         metrics[2 * k + 1] = as / double(nb ? nb : 1);

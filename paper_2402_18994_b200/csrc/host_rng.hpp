@@ -35,6 +35,23 @@ inline std::vector<uint32_t> permutation(uint64_t key, size_t n) {
   return p;
 }
 
+// randint (rng.hpp:68-75): lo + bits(counter) % (hi - lo).
+inline int64_t randint(uint64_t key, uint64_t c, int64_t lo, int64_t hi) {
+  return lo + int64_t(bits(key, c) % uint64_t(hi - lo));
+}
+
+// shift_augment of batch b (data.hpp:216-227 with key child(epoch_key, 1 + b),
+// optimize.hpp:276-278): n_axes rolls of the same flat feature axis compose to
+// one roll by the sum of the per-axis draws, reduced into [0, in).
+inline int32_t batch_roll(uint64_t epoch_key, uint64_t b, int64_t max_shift, int n_axes, int64_t in) {
+  if (max_shift <= 0 || n_axes == 0) return 0;
+  const uint64_t k = child(epoch_key, 1 + b);
+  int64_t s = 0;
+  for (int i = 0; i < n_axes; ++i) s += randint(k, uint64_t(i), -max_shift, max_shift);
+  s %= in;
+  return int32_t(s < 0 ? s + in : s);
+}
+
 // Truncated normal, +-2 sigma, per-element child keys (rng.hpp:92-97, :123-144).
 inline void truncated_normal(uint64_t key, size_t n, float mean, float sd, float* out) {
   for (size_t i = 0; i < n; ++i) {

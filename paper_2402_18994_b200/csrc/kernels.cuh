@@ -190,7 +190,8 @@ struct FwdArgs {
   FwdLayer lay[kFwdFuseMax];
   int n_layers;
   long long* dbg_clk;     // optional [gridDim.x*gridDim.y][kClkStride] phase timestamps
-  int B, T, T_pad, TT, NT, in_kind, stages, spb;
+  const int32_t* xshift;  // layer 0: batch roll along the features, [0, in_features) (shift_augment)
+  int B, T, T_pad, TT, NT, in_kind, stages, spb, in_features;
   float theta;
 };
 
@@ -267,6 +268,9 @@ __device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, fl
   }
 }
 
+// kShift: layer-0 launches of an epoch loop with shift_augment (reads a.xshift);
+// the default instantiation has no roll code in the decode loop.
+template <bool kShift>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     k_lif_fwd(const __grid_constant__ FwdMaps maps, FwdArgs a) {
   const CUtensorMap& tm_w = maps.m[0];
@@ -435,6 +439,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // sample s's rows at [s*TT, (s+1)*TT).  Loads of stage it+1 issue before the wait.
     const int tid = threadIdx.x - dec_warp0 * 32;
     const size_t kwords = size_t(K_pad0) / 32;
+    // shift_augment (data.hpp:216-227): feature k of the rolled batch is feature
+    // (k - xsh) mod in of the staged one; padding features stay zero
+    const int xsh = kShift ? *a.xshift : 0;
     const int units = SPB * a.TT;  // kind 0: (sample, t-group, 8-feature chunk); kind 1: row
     auto fetch = [&](int it, int u) -> uint64_t {
       if (a.in_kind == 0 || u >= units || it >= total) return 0;
@@ -460,8 +467,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (a.in_kind == 0) {
           // dataset bytes [t/8][k] (bulk-copied), bit 7-(t%8): 8 k of one t-group -> 8 rows
           const int g = r >> 3, q = r & 7;
-          const uint64_t cur = sm < nsamp ? *reinterpret_cast<const uint64_t*>(
-              xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * K_pad0 + kb * 64 + q * 8) : 0ull;
+          const uint8_t* xr = xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * K_pad0;
+          uint64_t cur = 0ull;
+          if (sm < nsamp) {
+            if (!kShift || xsh == 0) {
+              cur = *reinterpret_cast<const uint64_t*>(xr + kb * 64 + q * 8);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int k = kb * 64 + q * 8 + i;
+                if (k < a.in_features)
+                  cur |= uint64_t(xr[k >= xsh ? k - xsh : k - xsh + a.in_features]) << (8 * i);
+              }
+            }
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             st_shared_v4(Bt + sw128_off(sm * a.TT + 8 * g + j, q),
@@ -1257,7 +1276,8 @@ struct WgradArgs {
   const uint32_t* rows;    // kind 0: [B]
   const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
   long long* dbg_clk;      // optional [blocks][kClkStride] phase timestamps
-  int B, T_pad, x_row_stride;
+  const int32_t* xshift;   // kind 0: batch roll along the features (shift_augment)
+  int B, T_pad, x_row_stride, in_features;
 };
 struct WgradMaps {
   CUtensorMap m[kMaxLayers];
@@ -1416,6 +1436,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                    size_t(bb) * (args.T_pad / 32) + tq * 2 + h);
     };
     uint32_t cur[kWgMgMax], nxt[kWgMgMax];
+    const int xsh = (a.kind == 0 && args.xshift != nullptr) ? *args.xshift : 0;
 #pragma unroll
     for (int m = 0; m < kWgMgMax; ++m) cur[m] = fetch(0, m);
     for (int it = 0; it < total; ++it) {
@@ -1430,10 +1451,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         for (int m = 0; m < kWgMgMax; ++m) {
           if (m >= nm) break;
           const int k = (mt0 + m) * 128 + row;
+          // rolled feature k reads staged feature (k - xsh) mod in (shift_augment)
+          int src = k;
+          if (xsh != 0)
+            src = k >= args.in_features ? args.x_row_stride : (k >= xsh ? k - xsh : k - xsh + args.in_features);
           uint32_t v = 0;
-          if (k < args.x_row_stride) {
+          if (src < args.x_row_stride) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v |= uint32_t(xs[j * args.x_row_stride + k]) << (8 * j);
+            for (int j = 0; j < 4; ++j) v |= uint32_t(xs[j * args.x_row_stride + src]) << (8 * j);
           }
           cur[m] = v;
         }

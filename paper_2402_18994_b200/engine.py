@@ -100,6 +100,11 @@ class TrainConfig:
     loss: str = "integral_crossentropy"  # LossKind: | "spike_rate_mse" (optimize.hpp:23)
     rate_hi: float = 0.9                 # rate-MSE targets
     rate_lo: float = 0.1
+    max_shift: int = 0                   # shift augmentation on packed batches
+    shift_axes: tuple = ()               # feature axis only (2 or -1); 0 / 1 rejected
+
+
+ABI_VERSION = 4  # SNN_ABI_VERSION in include/snn_engine.h
 
 
 class _NetDesc(C.Structure):
@@ -117,7 +122,8 @@ class _TrainCfg(C.Structure):
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("seed", C.c_uint64), ("unroll", C.c_int32), ("optimizer", C.c_int32),
                 ("momentum", C.c_float), ("loss", C.c_int32), ("rate_hi", C.c_float),
-                ("rate_lo", C.c_float)]
+                ("rate_lo", C.c_float), ("max_shift", C.c_int32), ("n_shift_axes", C.c_int32),
+                ("shift_axes", C.c_int32 * 4)]
 
 
 def normalize(spec: NetworkSpec) -> dict:
@@ -188,6 +194,8 @@ def lib() -> C.CDLL:
     if not os.path.exists(lib):
         raise DeviceError(f"{lib} missing: the CUDA engine is required (no CPU fallback)")
     L = C.CDLL(lib, mode=C.RTLD_GLOBAL)
+    if L.snn_abi_version() != ABI_VERSION:  # struct layouts below must match the library
+        raise DeviceError(f"{lib}: ABI {L.snn_abi_version()} != {ABI_VERSION}; rebuild")
     L.snn_last_error.restype = C.c_char_p
     L.snn_last_error.argtypes = [C.c_void_p]
     L.snn_stream.restype = C.c_void_p
@@ -255,6 +263,12 @@ class Engine:
         c.momentum = float(cfg.momentum)
         c.loss = 1 if cfg.loss == "spike_rate_mse" else 0
         c.rate_hi, c.rate_lo = float(cfg.rate_hi), float(cfg.rate_lo)
+        axes = tuple(int(a) for a in cfg.shift_axes)
+        if len(axes) > 4:
+            raise ArgumentError("train: at most 4 shift axes")
+        c.max_shift, c.n_shift_axes = int(cfg.max_shift), len(axes)
+        for i, a in enumerate(axes):
+            c.shift_axes[i] = a
         self._L = lib()
         h = C.c_void_p()
         self._h = None

@@ -119,6 +119,29 @@ def opts_fixture(ref: Lib):
     np.savez_compressed(os.path.join(GOLD, "opts.npz"), **vals)
 
 
+SHIFT_NET = Net(inp=40, hidden=(24,), classes=5, bias=True, act="superspike", unroll=3)
+SHIFT_OPTS = {"one_axis": dict(max_shift=3, shift_axes=(2,)),
+              "two_axes": dict(max_shift=5, shift_axes=(2, -1))}
+
+
+def shift_fixture(ref: Lib):
+    """shift_augment inside the epoch loop (data.hpp:216-227 called from
+    optimize.hpp:241-280): every batch rolled along the feature axis by the sum
+    of per-axis randint(child(epoch_key, 1 + b), axis, -max_shift, max_shift)."""
+    from oracle.pyoracle import Opts
+    key = ref.key_child(ref.key_from_seed(33), 0)
+    p = ref.init(SHIFT_NET, key) * np.float32(3.0)
+    x, y = ref.synth_raster(5, 14, 20, 40, 17)
+    pk = ref.pack_time(x)
+    vals = dict(params=p, packed=pk, y=y, t=20, **net_dict(SHIFT_NET))
+    for name, kw in SHIFT_OPTS.items():
+        st = State(p.copy())
+        metrics = ref.train_epochs(SHIFT_NET, st, pk, y, 20, 4, 2, 9, opts=Opts(**kw))
+        vals.update({f"{name}_metrics": metrics, f"{name}_params": st.params,
+                     f"{name}_m": st.m, f"{name}_v": st.v, f"{name}_step": np.uint64(st.step)})
+    np.savez_compressed(os.path.join(GOLD, "shift.npz"), **vals)
+
+
 CKPT_NET = Net(inp=30, hidden=(16, 12), classes=5, bias=True, act="arctan", unroll=4)
 CKPT_CONFIG = "# spiketrain run config (fixture)\nnet = 30-16-12-5 lif arctan bias\nlr = 1e-3\n"
 
@@ -184,6 +207,8 @@ if __name__ == "__main__":
         opts_fixture(ref)
     if only in (None, "ckpt"):
         checkpoint_fixture(ref)
+    if only in (None, "shift"):
+        shift_fixture(ref)
     if only in (None, "betamodes"):
         beta_modes_fixture(ref)
     print("golden fixtures written to", GOLD)

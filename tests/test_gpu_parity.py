@@ -26,7 +26,7 @@ def relnorm(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def make_engine(net: Net, B, T, seed=0, lr=1e-3):
+def make_engine(net: Net, B, T, seed=0, lr=1e-3, **cfg):
     from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
     spec = shd_spec(hidden=net.hidden, classes=net.classes, inp=net.inp, act=net.act,
                     bias=net.bias)
@@ -35,7 +35,7 @@ def make_engine(net: Net, B, T, seed=0, lr=1e-3):
             layer.threshold = net.threshold
             if net.slope is not None:
                 layer.activation.slope = net.slope
-    return Engine(spec, TrainConfig(batch_size=B, seed=seed, lr=lr, unroll=net.unroll), T)
+    return Engine(spec, TrainConfig(batch_size=B, seed=seed, lr=lr, unroll=net.unroll, **cfg), T)
 
 
 def check_grads(orc, net, g, ref, tol=REL_TOL):
@@ -559,3 +559,64 @@ def test_beta_modes_match_reference_fixture(orc, golden):
     assert sz == 1 and eng.get_params()[off] == g["params"][off] == g["params3"][off]
     m, v, _ = eng.get_opt_state()
     assert m[off] == 0 and v[off] == 0
+
+
+SHIFTS = {"one_axis": dict(max_shift=3, shift_axes=(2,)), "two_axes": dict(max_shift=5, shift_axes=(2, -1))}
+
+
+@pytest.mark.parametrize("name", list(SHIFTS))
+def test_shift_augment_matches_reference_fixture(orc, golden, name):
+    """Epoch loop with shift_augment (data.hpp:216-227, optimize.hpp:276-278): two
+    epochs against the reference's own run (tests/golden/shift.npz)."""
+    g = golden("shift")
+    net = Net(inp=int(g["inp"]), hidden=tuple(int(h) for h in g["hidden"]), classes=int(g["classes"]),
+              bias=bool(g["bias"]), threshold=float(g["threshold"]), act=str(g["act"]),
+              unroll=int(g["unroll"]))
+    eng = make_engine(net, 4, int(g["t"]), seed=9, **SHIFTS[name])
+    eng.stage_dataset(g["packed"], g["y"])
+    eng.set_params(g["params"])
+    m = eng.train_epochs(2)
+    ref = g[f"{name}_metrics"]
+    assert np.allclose(m[:, 0], ref[:, 0], rtol=1e-4), (m, ref)
+    assert np.array_equal(m[:, 1], ref[:, 1])
+    assert relnorm(eng.get_params(), g[f"{name}_params"]) <= 1e-4
+    assert eng.get_opt_state()[2] == int(g[f"{name}_step"])
+    # a following plain step is unshifted again
+    st = State(eng.get_params().copy())
+    rows = np.arange(4, dtype=np.uint32)
+    fb = orc.forward_backward(net, st.params, g["packed"][:4], int(g["t"]), g["y"][:4])
+    loss, _ = eng.forward_backward(rows)
+    assert abs(loss - fb["loss"]) <= REL_TOL * abs(fb["loss"])
+
+
+def test_shift_augment_c1_shape_matches_oracle(orc):
+    """C1 shape (700 inputs, 11 padding features) with rolls up to +-40 over 2 epochs."""
+    from oracle.pyoracle import Opts
+    net = Net()
+    B, N, T = 64, 192, 128
+    x, y = orc.synth_raster(20, N, T, 700, 4)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T, seed=3, max_shift=40, shift_axes=(2, -1))
+    eng.stage_dataset(pk, y)
+    p0 = eng.get_params()
+    m_gpu = eng.train_epochs(2)
+    st = State(p0.copy())
+    m_ref = orc.train_epochs(net, st, pk, y, T, B, 2, 3, opts=Opts(max_shift=40, shift_axes=(2, -1)))
+    assert np.allclose(m_gpu[:, 0], m_ref[:, 0], rtol=1e-3), (m_gpu, m_ref)
+    assert np.abs(m_gpu[:, 1] - m_ref[:, 1]).max() <= 1.0 / B + 1e-12
+    assert relnorm(eng.get_params(), st.params) <= 1e-4
+
+
+def test_shift_axes_validation():
+    """train() rejects axes 0 / 1 (optimize.hpp:241-245); other non-feature rolls
+    are refused as unsupported; max_shift <= 0 accepts any other axis."""
+    from paper_2402_18994_b200 import ArgumentError, UnsupportedError
+    net = Net(inp=30, hidden=(16,), classes=5)
+    for axes in ((0,), (1,), (2, 1)):
+        with pytest.raises(ArgumentError):
+            make_engine(net, 2, 16, max_shift=2, shift_axes=axes)
+    with pytest.raises(ArgumentError):
+        make_engine(net, 2, 16, max_shift=0, shift_axes=(1,))
+    with pytest.raises(UnsupportedError):
+        make_engine(net, 2, 16, max_shift=2, shift_axes=(-2,))
+    make_engine(net, 2, 16, max_shift=0, shift_axes=(3,))

@@ -275,3 +275,73 @@ def test_beta_modes_vs_reference_live(orc, modes):
         for _ in range(2):
             assert orc.train_step(net, s1, pk, 23, y, opts=o) == ref.train_step(net, s2, pk, 23, y, opts=o)
         assert np.array_equal(s1.params, s2.params) and np.array_equal(s1.m, s2.m)
+
+
+def _shift_case():
+    from oracle.pyoracle import Opts
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "shift.npz"))
+    net = Net(inp=int(g["inp"]), hidden=tuple(int(h) for h in g["hidden"]), classes=int(g["classes"]),
+              bias=bool(g["bias"]), threshold=float(g["threshold"]), act=str(g["act"]),
+              unroll=int(g["unroll"]))
+    opts = {"one_axis": Opts(max_shift=3, shift_axes=(2,)),
+            "two_axes": Opts(max_shift=5, shift_axes=(2, -1))}
+    return g, net, opts
+
+
+@pytest.mark.parametrize("name", ["one_axis", "two_axes"])
+def test_shift_augment_golden_bit_exact(orc, name):
+    """shift_augment in the epoch loop (data.hpp:216-227, optimize.hpp:241-280):
+    the C restatement reproduces the reference's 2-epoch run bit for bit."""
+    g, net, opts = _shift_case()
+    st = State(g["params"].copy())
+    metrics = orc.train_epochs(net, st, g["packed"], g["y"], int(g["t"]), 4, 2, 9, opts=opts[name])
+    assert np.array_equal(metrics, g[f"{name}_metrics"])
+    assert np.array_equal(st.params, g[f"{name}_params"])
+    assert np.array_equal(st.m, g[f"{name}_m"]) and np.array_equal(st.v, g[f"{name}_v"])
+    assert st.step == int(g[f"{name}_step"])
+    # the shift is not a no-op: an unshifted run ends elsewhere
+    st0 = State(g["params"].copy())
+    orc.train_epochs(net, st0, g["packed"], g["y"], int(g["t"]), 4, 2, 9)
+    assert not np.array_equal(st0.params, st.params)
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+def test_shift_augment_live_vs_reference(orc):
+    """Same check against the reference's own train() on other shapes."""
+    from oracle.pyoracle import Opts
+    ref = Lib("ref")
+    net = Net(inp=33, hidden=(16, 9), classes=4, bias=False, act="arctan", unroll=2)
+    p = orc.init(net, orc.key_from_seed(5)) * np.float32(3.0)
+    x, y = orc.synth_raster(4, 11, 17, 33, 3)
+    pk = orc.pack_time(x)
+    for o in (Opts(max_shift=7, shift_axes=(-1,)), Opts(max_shift=40, shift_axes=(2, 2, -1)),
+              Opts(max_shift=0, shift_axes=(2,))):
+        s1, s2 = State(p.copy()), State(p.copy())
+        m1 = orc.train_epochs(net, s1, pk, y, 17, 3, 2, 11, opts=o)
+        m2 = ref.train_epochs(net, s2, pk, y, 17, 3, 2, 11, opts=o)
+        assert np.array_equal(m1, m2) and np.array_equal(s1.params, s2.params)
+
+
+@pytest.mark.parametrize("axes,max_shift", [((0,), 2), ((1,), 2), ((2, 1), 2), ((1,), 0)])
+def test_shift_augment_rejects_batch_and_time_axes(orc, axes, max_shift):
+    """train() refuses axes 0 / 1 even when no shift happens (optimize.hpp:241-245)."""
+    from oracle.pyoracle import Opts
+    g, net, _ = _shift_case()
+    libs = [orc] + ([Lib("ref")] if have_ref() else [])
+    for lib in libs:
+        with pytest.raises(ValueError):
+            lib.train_epochs(net, State(g["params"].copy()), g["packed"], g["y"], int(g["t"]), 4, 1,
+                             9, opts=Opts(max_shift=max_shift, shift_axes=axes))
+
+
+def test_shift_augment_nonpositive_max_shift_is_identity(orc):
+    """max_shift <= 0 never reaches shift_augment (optimize.hpp:276): same run as none."""
+    from oracle.pyoracle import Opts
+    g, net, _ = _shift_case()
+    base = State(g["params"].copy())
+    orc.train_epochs(net, base, g["packed"], g["y"], int(g["t"]), 4, 1, 9)
+    for o in (Opts(max_shift=0, shift_axes=(2,)), Opts(max_shift=-3, shift_axes=(2,)),
+              Opts(max_shift=0, shift_axes=(3,))):
+        st = State(g["params"].copy())
+        orc.train_epochs(net, st, g["packed"], g["y"], int(g["t"]), 4, 1, 9, opts=o)
+        assert np.array_equal(st.params, base.params)
