@@ -29,7 +29,8 @@ class _Net(C.Structure):
                 ("hidden", C.c_int * 8), ("classes", C.c_int),
                 ("bias", C.c_int), ("threshold", C.c_float), ("act", C.c_int),
                 ("slope", C.c_float), ("aux", C.c_float), ("unroll", C.c_int),
-                ("beta_mode", C.c_int * 9), ("fixed_beta", C.c_float * 9)]
+                ("beta_mode", C.c_int * 9), ("fixed_beta", C.c_float * 9),
+                ("monitor", C.c_int * 8)]
 
 BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 
@@ -37,7 +38,9 @@ BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 class _Opts(C.Structure):
     _fields_ = [("optimizer", C.c_int), ("momentum", C.c_float), ("loss", C.c_int),
                 ("rate_hi", C.c_float), ("rate_lo", C.c_float), ("max_shift", C.c_int),
-                ("n_shift_axes", C.c_int), ("shift_axes", C.c_int * 4)]
+                ("n_shift_axes", C.c_int), ("shift_axes", C.c_int * 4),
+                ("f_min", C.c_float), ("f_max", C.c_float), ("lambda_low", C.c_float),
+                ("lambda_high", C.c_float)]
 
 
 @dataclass
@@ -51,11 +54,17 @@ class Opts:
     rate_lo: float = 0.1
     max_shift: int = 0          # shift_augment (epoch loop only)
     shift_axes: tuple = ()
+    f_min: float = 0.0          # activity regularizer (both lambdas 0 = off)
+    f_max: float = 1.0
+    lambda_low: float = 0.0
+    lambda_high: float = 0.0
 
     def c(self) -> _Opts:
         o = _Opts(1 if self.optimizer == "sgd" else 0, self.momentum,
                   1 if self.loss == "rate_mse" else 0, self.rate_hi, self.rate_lo,
                   self.max_shift, len(self.shift_axes))
+        o.f_min, o.f_max = self.f_min, self.f_max
+        o.lambda_low, o.lambda_high = self.lambda_low, self.lambda_high
         for i, a in enumerate(self.shift_axes):
             o.shift_axes[i] = a
         return o
@@ -77,6 +86,8 @@ class Net:
     # "scalar" (LearnableScalar) | "fixed"; fixed_beta per cell (default 0.5)
     beta_mode: tuple = ()
     fixed_beta: tuple = ()
+    # hidden LIF layers followed by a MonitorLayer (indices into hidden)
+    monitor: tuple = ()
 
     def c(self) -> _Net:
         s, a = DEFAULT_SLOPE[self.act]
@@ -95,6 +106,8 @@ class Net:
         for i in range(len(self.hidden) + 1):
             n.beta_mode[i] = BETA_MODES[self.beta_mode[i]] if i < len(self.beta_mode) else 0
             n.fixed_beta[i] = self.fixed_beta[i] if i < len(self.fixed_beta) else 0.5
+        for i in self.monitor:
+            n.monitor[i] = 1
         return n
 
 

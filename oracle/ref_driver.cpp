@@ -47,6 +47,7 @@ NetworkSpec make_spec(const orc_net* n) {
     lif.beta_mode = beta_mode(n, l);
     lif.fixed_beta = double(n->fixed_beta[l]);
     s.layers.push_back(lif);
+    if (n->monitor[l]) s.layers.push_back(MonitorLayer{});
   }
   s.layers.push_back(LinearLayer{std::size_t(n->classes), n->bias != 0});
   LILayer li;
@@ -194,6 +195,10 @@ int ref_forward_backward_ex(const orc_net* n, const orc_train_opts* opts,
     auto l = (opts && opts->loss == 1)
                  ? spike_rate_mse_taped(tape, fwd.trace, y, opts->rate_hi, opts->rate_lo)
                  : integral_crossentropy_taped(tape, fwd.trace, y);
+    if (opts && (opts->lambda_low != 0.0f || opts->lambda_high != 0.0f))  // optimize.hpp:185-191
+      for (auto& [name, counts] : fwd.monitors)
+        l = tape.add(l, activity_regularizer_taped(tape, counts, t_steps, opts->f_min, opts->f_max,
+                                                   opts->lambda_low, opts->lambda_high));
     *loss = tape.value(l)[0];
     *acc = integral_accuracy(tape.value(fwd.trace), y);
     if (trace)
@@ -219,11 +224,12 @@ int ref_forward_backward_ex(const orc_net* n, const orc_train_opts* opts,
       // readout trace is that cell's spike train.
       std::size_t off = 0;
       const int per = n->bias ? 3 : 2;
+      std::size_t end = 0;  // one past LIF h in spec.layers (monitors take slots too)
       for (int h = 0; h < n->n_hidden; ++h) {
+        end += 2 + ((h > 0 && n->monitor[h - 1]) ? 1 : 0);
         NetworkSpec prefix;
         prefix.input_shape = spec.input_shape;
-        prefix.layers.assign(spec.layers.begin(),
-                             spec.layers.begin() + 2 * (h + 1));
+        prefix.layers.assign(spec.layers.begin(), spec.layers.begin() + std::ptrdiff_t(end));
         NetworkParams<float> pp;
         pp.entries.assign(p.entries.begin(),
                           p.entries.begin() + per * (h + 1));
@@ -277,6 +283,10 @@ TrainState<float> make_state(const orc_net* n, const float* params,
     st.cfg.loss = opts->loss == 1 ? LossKind::SpikeRateMse : LossKind::IntegralCrossentropy;
     st.cfg.rate_hi = double(opts->rate_hi);
     st.cfg.rate_lo = double(opts->rate_lo);
+    st.cfg.f_min = double(opts->f_min);
+    st.cfg.f_max = double(opts->f_max);
+    st.cfg.lambda_low = double(opts->lambda_low);
+    st.cfg.lambda_high = double(opts->lambda_high);
   }
   st.params = params_from_flat(skeleton(n), params);
   st.opt = init_optimizer(kind, st.params);

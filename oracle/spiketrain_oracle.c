@@ -137,6 +137,14 @@ static size_t beta_size(const orc_net* net, int l, size_t h) {
   return net->beta_mode[l] == 0 ? h : 1;
 }
 
+/* normalised layer ids (network.hpp:125-157): Linear l, its LIF (or the LI
+ * readout) right after, and a monitor after a LIF takes the next id */
+static int lin_id(const orc_net* net, int l) {
+  int id = 2 * l;
+  for (int j = 0; j < l && j < net->n_hidden; ++j) id += net->monitor[j] ? 1 : 0;
+  return id;
+}
+
 static int layer_in(const orc_net* net, int l) {
   return l == 0 ? net->in : net->hidden[l - 1];
 }
@@ -152,7 +160,7 @@ void orc_entry_layout(const orc_net* net, size_t* offsets, size_t* sizes,
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
     const size_t sz[3] = {k * h, h, beta_size(net, l, h)};
     const char* leaf[3] = {"w", "b", "beta"};
-    const int lid[3] = {2 * l, 2 * l, 2 * l + 1};
+    const int lid[3] = {lin_id(net, l), lin_id(net, l), lin_id(net, l) + 1};
     for (int q = 0; q < 3; ++q) {
       if (q == 1 && !net->bias) continue;
       if (offsets) offsets[e] = off;
@@ -200,12 +208,12 @@ void orc_init(const orc_net* net, uint64_t key, float* params) {
   layer_offsets(net, lo);
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    const uint64_t lk_lin = orc_key_child(key, (uint64_t)(2 * l));
+    const uint64_t lk_lin = orc_key_child(key, (uint64_t)lin_id(net, l));
     const float sd = 1.0f / sqrtf((float)k);
     orc_truncated_normal(orc_key_child(lk_lin, 0), k * h, 0.0f, sd,
                          params + lo[l].w);
     if (net->bias) memset(params + lo[l].b, 0, h * sizeof(float));
-    const uint64_t lk_cell = orc_key_child(key, (uint64_t)(2 * l + 1));
+    const uint64_t lk_cell = orc_key_child(key, (uint64_t)(lin_id(net, l) + 1));
     if (net->beta_mode[l] == 2) /* Fixed: Tensor::scalar(fixed_beta) */
       params[lo[l].beta] = net->fixed_beta[l];
     else /* PerNeuron [h] or LearnableScalar [] from the same key */
@@ -267,7 +275,38 @@ static void matmul_rows(const float* a, size_t rows, size_t k, const float* w,
   }
 }
 
-static const orc_train_opts k_default_opts = {0, 0.9f, 0, 0.9f, 0.1f, 0, 0, {0, 0, 0, 0}};
+static const orc_train_opts k_default_opts = {0, 0.9f, 0, 0.9f, 0.1f, 0, 0, {0, 0, 0, 0},
+                                              0.0f, 1.0f, 0.0f, 0.0f};
+
+/* Activity regularizer of one monitor (objective.hpp:186-227) over the spike
+ * raster s [B, T, H]: counts = sum over t (monitor_activity, neuron.hpp:106-114,
+ * integer-valued so the per-block sums are exact), the value in the reference's
+ * running order over i = b*H + n, and d loss / d count per (b, n). */
+static float activity_reg(const orc_train_opts* o, const float* s, size_t B, size_t T, size_t H,
+                          float* dcount) {
+  const size_t n = B * H;
+  float low = 0.0f, high = 0.0f;
+  const float gs = 1.0f * 2.0f / ((float)n * (float)T);
+  for (size_t b = 0; b < B; ++b)
+    for (size_t j = 0; j < H; ++j) {
+      float c = 0.0f;
+      for (size_t t = 0; t < T; ++t) c += s[(b * T + t) * H + j];
+      const float r = c / (float)T;
+      const float dl = o->f_min - r > 0.0f ? o->f_min - r : 0.0f;
+      const float dh = r - o->f_max > 0.0f ? r - o->f_max : 0.0f;
+      low += dl * dl;
+      high += dh * dh;
+      if (dcount) dcount[b * H + j] = gs * (o->lambda_high * dh - o->lambda_low * dl);
+    }
+  return o->lambda_low * (low / (float)n) + o->lambda_high * (high / (float)n);
+}
+
+static int reg_active(const orc_net* net, const orc_train_opts* o) {
+  if (o->lambda_low == 0.0f && o->lambda_high == 0.0f) return 0;
+  for (int l = 0; l < net->n_hidden; ++l)
+    if (net->monitor[l]) return 1;
+  return 0;
+}
 
 int orc_forward_backward(const orc_net* net, const float* params,
                          const uint8_t* packed, size_t B, size_t T,
@@ -287,6 +326,9 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
   if (opts->loss == 1 && (opts->rate_hi < 0.0f || opts->rate_hi > 1.0f ||
                           opts->rate_lo < 0.0f || opts->rate_lo > 1.0f))
     return 3; /* spike_rate_mse: rates must lie in [0,1] (objective.hpp:144-145) */
+  const int reg = reg_active(net, opts);
+  if (reg && (opts->f_min > opts->f_max || opts->f_min < 0.0f || opts->f_max > 1.0f))
+    return 3; /* activity_regularizer: need 0 <= f_min <= f_max <= 1 (objective.hpp:191-192) */
   const int L = net->n_hidden;
   const size_t C = (size_t)net->classes;
   if (B == 0 || T == 0 || L < 1 || L > ORC_MAX_HIDDEN || net->unroll < 1)
@@ -403,6 +445,16 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
   } else {
     *loss_out = loss / (float)B;
   }
+  /* loss = add(loss, activity_regularizer(monitor)) per monitor in layer order
+   * (optimize.hpp:185-191) */
+  float* dcount[ORC_MAX_HIDDEN] = {0};
+  if (reg)
+    for (int l = 0; l < L; ++l) {
+      if (!net->monitor[l]) continue;
+      const size_t H = (size_t)net->hidden[l];
+      dcount[l] = (float*)malloc(B * H * sizeof(float));
+      *loss_out = *loss_out + activity_reg(opts, act[l + 1], B, T, H, dcount[l]);
+    }
   *acc_out = (double)hits / (double)B;
 
   if (grads) {
@@ -510,6 +562,10 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
         }
       }
       const int hl = l - 1; /* hidden layer whose spikes fed Linear l */
+      if (dcount[hl]) /* the monitor's sum_axis1 adds d loss / d count on every step */
+        for (size_t b = 0; b < B; ++b)
+          for (size_t t = 0; t < T; ++t)
+            for (size_t kk = 0; kk < H; ++kk) dS[(b * T + t) * H + kk] += dcount[hl][b * H + kk];
       const float* beta = params + lo[hl].beta;
       float* gbeta = grads + lo[hl].beta;
       const int mode = net->beta_mode[hl];
@@ -554,6 +610,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
 
   for (int l = 0; l <= L; ++l) free(act[l]);
   for (int l = 0; l < L; ++l) free(vst[l]);
+  for (int l = 0; l < L; ++l) free(dcount[l]);
   free(i3);
   free(trace);
   free(v3);

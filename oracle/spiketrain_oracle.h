@@ -60,6 +60,11 @@ typedef struct orc_net {
    * not trainable).  Zero-initialised = PerNeuron everywhere.             */
   int beta_mode[ORC_MAX_HIDDEN + 1];
   float fixed_beta[ORC_MAX_HIDDEN + 1];
+  /* MonitorLayer after LIF layer l (network.hpp:57, :139-144): spike counts
+   * over time (neuron.hpp:106-114) that feed the activity regularizer.  A
+   * monitor takes a normalised layer id, so every later layer's id -- its
+   * init key child(id) and entry names -- moves up by one.                 */
+  int monitor[ORC_MAX_HIDDEN];
 } orc_net;
 
 /* Parameter entries in NetworkParams order (network.hpp:231-286). */
@@ -119,6 +124,9 @@ typedef struct orc_train_opts {
   int max_shift;
   int n_shift_axes;
   int shift_axes[4];
+  /* activity regularizer on every monitor (objective.hpp:186-227, optimize.hpp:185-191);
+   * both lambdas zero = off (defaults f_min 0, f_max 1)                    */
+  float f_min, f_max, lambda_low, lambda_high;
 } orc_train_opts;
 
 /* forward_backward / train_step with TrainConfig options (NULL = defaults). */

@@ -119,6 +119,36 @@ def opts_fixture(ref: Lib):
     np.savez_compressed(os.path.join(GOLD, "opts.npz"), **vals)
 
 
+ACT_NET = Net(inp=40, hidden=(24, 20), classes=5, act="superspike", unroll=4, monitor=(0, 1))
+ACT_OPTS = {"both": dict(lambda_low=0.5, lambda_high=2.0, f_min=0.1, f_max=0.3),
+            "high": dict(lambda_high=1.5, f_max=0.05)}
+
+
+def activity_fixture(ref: Lib):
+    """MonitorLayer after both LIF layers (network.hpp:57, :415-420) and the
+    activity regularizer (objective.hpp:186-227, optimize.hpp:185-191).  The
+    monitors shift the normalised layer ids, so entry names and init keys are
+    part of the fixture."""
+    from oracle.pyoracle import Opts
+    key = ref.key_child(ref.key_from_seed(41), 0)
+    p_init = ref.init(ACT_NET, key)
+    p = p_init * np.float32(3.0)
+    x, y = ref.synth_raster(5, 7, 30, 40, 23)
+    pk = ref.pack_time(x)
+    names = np.array([n for n, _, _ in ref.entries(ACT_NET)])
+    vals = dict(params_init=p_init, params=p, packed=pk, y=y, t=30, names=names,
+                monitor=np.array(ACT_NET.monitor), **net_dict(ACT_NET))
+    for name, kw in ACT_OPTS.items():
+        o = Opts(**kw)
+        fb = ref.forward_backward(ACT_NET, p, pk, 30, y, opts=o)
+        st = State(p.copy())
+        losses = [ref.train_step(ACT_NET, st, pk, 30, y, opts=o)[0] for _ in range(3)]
+        vals.update({f"{name}_loss": np.float32(fb["loss"]), f"{name}_grads": fb["grads"],
+                     f"{name}_step_losses": np.array(losses, np.float32),
+                     f"{name}_params3": st.params})
+    np.savez_compressed(os.path.join(GOLD, "activity.npz"), **vals)
+
+
 SHIFT_NET = Net(inp=40, hidden=(24,), classes=5, bias=True, act="superspike", unroll=3)
 SHIFT_OPTS = {"one_axis": dict(max_shift=3, shift_axes=(2,)),
               "two_axes": dict(max_shift=5, shift_axes=(2, -1))}
@@ -207,6 +237,8 @@ if __name__ == "__main__":
         opts_fixture(ref)
     if only in (None, "ckpt"):
         checkpoint_fixture(ref)
+    if only in (None, "activity"):
+        activity_fixture(ref)
     if only in (None, "shift"):
         shift_fixture(ref)
     if only in (None, "betamodes"):

@@ -345,3 +345,69 @@ def test_shift_augment_nonpositive_max_shift_is_identity(orc):
         st = State(g["params"].copy())
         orc.train_epochs(net, st, g["packed"], g["y"], int(g["t"]), 4, 1, 9, opts=o)
         assert np.array_equal(st.params, base.params)
+
+
+def _activity_case():
+    from oracle.pyoracle import Opts
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "activity.npz"))
+    net = Net(inp=int(g["inp"]), hidden=tuple(int(h) for h in g["hidden"]), classes=int(g["classes"]),
+              bias=bool(g["bias"]), threshold=float(g["threshold"]), act=str(g["act"]),
+              unroll=int(g["unroll"]), monitor=tuple(int(m) for m in g["monitor"]))
+    opts = {"both": Opts(lambda_low=0.5, lambda_high=2.0, f_min=0.1, f_max=0.3),
+            "high": Opts(lambda_high=1.5, f_max=0.05)}
+    return g, net, opts
+
+
+def test_monitor_layer_ids_golden(orc):
+    """Monitors take normalised layer ids: entry names and init keys of every later
+    layer move up (network.hpp:231-286), exactly as the reference's."""
+    g, net, _ = _activity_case()
+    assert [n for n, _, _ in orc.entries(net)] == [str(n) for n in g["names"]]
+    assert np.array_equal(orc.init(net, orc.key_child(orc.key_from_seed(41), 0)), g["params_init"])
+
+
+@pytest.mark.parametrize("name", ["both", "high"])
+def test_activity_regularizer_golden_bit_exact(orc, name):
+    """Activity regularizer on two monitors (objective.hpp:186-227): loss, grads and
+    three train_steps equal the reference's fixture bit for bit."""
+    g, net, opts = _activity_case()
+    o, T = opts[name], int(g["t"])
+    fb = orc.forward_backward(net, g["params"], g["packed"], T, g["y"], opts=o)
+    assert fb["loss"] == g[f"{name}_loss"]
+    assert np.array_equal(fb["grads"], g[f"{name}_grads"])
+    plain = orc.forward_backward(net, g["params"], g["packed"], T, g["y"])
+    assert fb["loss"] != plain["loss"] and not np.array_equal(fb["grads"], plain["grads"])
+    st = State(g["params"].copy())
+    losses = [orc.train_step(net, st, g["packed"], T, g["y"], opts=o)[0] for _ in range(3)]
+    assert np.array_equal(np.array(losses, np.float32), g[f"{name}_step_losses"])
+    assert np.array_equal(st.params, g[f"{name}_params3"])
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+def test_activity_regularizer_live_vs_reference(orc):
+    from oracle.pyoracle import Opts
+    ref = Lib("ref")
+    net = Net(inp=40, hidden=(24, 20, 8), classes=4, bias=True, monitor=(0, 2), act="boxcar", unroll=5)
+    key = orc.key_child(orc.key_from_seed(4), 0)
+    p = orc.init(net, key)
+    assert np.array_equal(p, ref.init(net, key)) and orc.entries(net) == ref.entries(net)
+    p = p * np.float32(3.0)
+    x, y = orc.synth_raster(4, 7, 21, 40, 2)
+    pk = orc.pack_time(x)
+    for o in (Opts(lambda_low=0.5, lambda_high=2.0, f_min=0.1, f_max=0.3),
+              Opts(lambda_low=3.0, f_min=0.9, loss="rate_mse"), Opts(lambda_low=1.0, optimizer="sgd")):
+        a = orc.forward_backward(net, p, pk, 21, y, opts=o)
+        b = ref.forward_backward(net, p, pk, 21, y, opts=o)
+        assert a["loss"] == b["loss"] and np.array_equal(a["grads"], b["grads"])
+
+
+def test_activity_regularizer_rejects_bad_band(orc):
+    """need 0 <= f_min <= f_max <= 1 once a lambda is set (objective.hpp:191-192)."""
+    from oracle.pyoracle import Opts
+    g, net, _ = _activity_case()
+    for o in (Opts(lambda_low=1.0, f_min=0.5, f_max=0.2), Opts(lambda_high=1.0, f_max=1.5)):
+        with pytest.raises(ValueError):
+            orc.forward_backward(net, g["params"], g["packed"], int(g["t"]), g["y"], opts=o)
+    # lambdas zero: the band is never checked (the regularizer is not called)
+    orc.forward_backward(net, g["params"], g["packed"], int(g["t"]), g["y"],
+                         opts=Opts(f_min=0.5, f_max=0.2))
