@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 4
+#define SNN_ABI_VERSION 5
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -72,6 +72,11 @@ typedef struct snn_network_desc {
    * not trainable).  Zero = PerNeuron everywhere. */
   int32_t beta_mode[SNN_MAX_HIDDEN + 1];
   float fixed_beta[SNN_MAX_HIDDEN + 1];
+  /* MonitorLayer after hidden LIF l (network.hpp:57, :139-144): its spike counts
+   * feed the activity regularizer and are readable with snn_monitor_counts.  A
+   * monitor takes a normalised layer id, so the entry names and init keys of
+   * every later layer move up by one (network.hpp:231-286). */
+  int32_t monitor[SNN_MAX_HIDDEN];
 } snn_network_desc;
 
 /* TrainConfig subset that reaches the step (optimize.hpp:116-133). */
@@ -95,6 +100,10 @@ typedef struct snn_train_config {
   int32_t max_shift;
   int32_t n_shift_axes; /* 0..4 */
   int32_t shift_axes[4];
+  /* activity regularizer on every monitor (objective.hpp:186-227, optimize.hpp:185-191):
+   * squared hinge on the rates count/T outside [f_min, f_max]; both lambdas 0 = off
+   * (then the band is not checked, like the reference). */
+  float f_min, f_max, lambda_low, lambda_high;
 } snn_train_config;
 
 typedef struct snn_engine snn_engine;
@@ -200,6 +209,10 @@ int32_t snn_forward_launch_layers(const snn_engine* e, int32_t i, int32_t* first
 snn_status snn_evaluate(snn_engine* e, const uint32_t* rows, size_t n, double* accuracy,
                         double* mean_loss);
 snn_status snn_apply(snn_engine* e, const uint32_t* rows, float* trace, size_t n);
+/* ApplyResult.monitors (network.hpp:435-448, neuron.hpp:106-114): spike counts
+ * [B][hidden[layer]] of the monitor after hidden LIF `layer`, from the last
+ * forward (snn_apply, a step, or an evaluation batch). */
+snn_status snn_monitor_counts(snn_engine* e, int32_t layer, float* counts, size_t n);
 snn_status snn_sync(snn_engine* e);
 snn_status snn_read_result(snn_engine* e, float* loss, double* accuracy);
 /* cudaStream_t of the engine, for CUDA-event timing by the caller. */

@@ -94,7 +94,8 @@ struct LILayer {
   BetaMode beta_mode = BetaMode::PerNeuron;
   double fixed_beta = 0.5;
 };
-using Layer = std::variant<LinearLayer, LIFLayer, LILayer>;
+struct MonitorLayer {};  // network.hpp:57: spike counts of the LIF before it
+using Layer = std::variant<LinearLayer, LIFLayer, LILayer, MonitorLayer>;
 
 struct NetworkSpec {
   std::vector<std::size_t> input_shape;
@@ -114,6 +115,10 @@ struct TrainConfig {
   LossKind loss = LossKind::IntegralCrossentropy;
   double rate_hi = 0.9;  // rate-MSE targets
   double rate_lo = 0.1;
+  double f_min = 0.0;  // activity regularizer; zero lambdas disable it
+  double f_max = 1.0;
+  double lambda_low = 0.0;
+  double lambda_high = 0.0;
   std::int64_t max_shift = 0;     // shift augmentation on packed batches
   std::vector<long> shift_axes;   // feature axis only (2 or -1)
   std::uint64_t seed = 0;
@@ -151,13 +156,26 @@ inline int activation_id(const std::string& n) {
   throw ArgumentError("unknown activation: " + n);
 }
 
-// normalize() subset (network.hpp:125-157): [Linear, LIF]*k, Linear, LI
-inline snn_network_desc describe(const NetworkSpec& s) {
-  if (s.input_shape.empty()) throw SpecError("network: input shape not declared");
-  if (s.layers.empty()) throw SpecError("network: no layers");
-  if (!std::holds_alternative<LIFLayer>(s.layers.back()) &&
-      !std::holds_alternative<LILayer>(s.layers.back()))
+// normalize() subset (network.hpp:125-157): [Linear, LIF, (Monitor)]*k, Linear, LI
+inline snn_network_desc describe(const NetworkSpec& spec) {
+  if (spec.input_shape.empty()) throw SpecError("network: input shape not declared");
+  if (spec.layers.empty()) throw SpecError("network: no layers");
+  if (!std::holds_alternative<LIFLayer>(spec.layers.back()) &&
+      !std::holds_alternative<LILayer>(spec.layers.back()))
     throw SpecError("network must end in a lif or li readout");
+  // monitors: must follow a LIF (network.hpp:139-144); recorded per hidden block
+  NetworkSpec s;
+  s.input_shape = spec.input_shape;
+  std::vector<int> monitor;
+  for (std::size_t i = 0; i < spec.layers.size(); ++i) {
+    if (std::holds_alternative<MonitorLayer>(spec.layers[i])) {
+      if (i == 0 || !std::holds_alternative<LIFLayer>(spec.layers[i - 1]))
+        throw SpecError("layer " + std::to_string(i) + ": monitor must follow a lif layer");
+      monitor.push_back(int(s.layers.size() / 2) - 1);
+      continue;
+    }
+    s.layers.push_back(spec.layers[i]);
+  }
   if (s.layers.size() < 4 || s.layers.size() % 2)
     throw UnsupportedError("engine supports [Linear, LIF]*k + Linear + LI");
   snn_network_desc d{};
@@ -186,6 +204,7 @@ inline snn_network_desc describe(const NetworkSpec& s) {
   const auto& li = std::get<LILayer>(s.layers.back());
   d.beta_mode[d.n_hidden] = int32_t(li.beta_mode);
   d.fixed_beta[d.n_hidden] = float(li.fixed_beta);
+  for (int m : monitor) d.monitor[m] = 1;
   return d;
 }
 
@@ -216,6 +235,10 @@ class TrainState {
     c.max_shift = int32_t(cfg.max_shift);
     c.n_shift_axes = int32_t(cfg.shift_axes.size());
     for (std::size_t i = 0; i < cfg.shift_axes.size(); ++i) c.shift_axes[i] = int32_t(cfg.shift_axes[i]);
+    c.f_min = float(cfg.f_min);
+    c.f_max = float(cfg.f_max);
+    c.lambda_low = float(cfg.lambda_low);
+    c.lambda_high = float(cfg.lambda_high);
     snn_engine* e = nullptr;
     check(snn_engine_create(&d, &c, device, &e), nullptr);
     eng_.reset(e);
@@ -285,6 +308,14 @@ inline std::vector<float> apply(TrainState& st, const std::vector<std::uint32_t>
   std::vector<float> trace(st.cfg().batch_size * st.original_t() * classes);
   check(snn_apply(st.engine(), rows.data(), trace.data(), trace.size()), st.engine());
   return trace;
+}
+
+// ApplyResult.monitors entry of the monitor after hidden LIF `layer`: spike counts
+// [B][H] of the last forward (apply / step / evaluation batch).
+inline std::vector<float> monitor_counts(TrainState& st, int layer, std::size_t hidden) {
+  std::vector<float> c(st.cfg().batch_size * hidden);
+  check(snn_monitor_counts(st.engine(), int32_t(layer), c.data(), c.size()), st.engine());
+  return c;
 }
 
 // write_checkpoint / read_checkpoint (optimize.hpp:334-436) of the engine state in

@@ -285,6 +285,9 @@ struct snn_engine {
   DevBuf<float> dbeta[kMaxLayers], dbias[kMaxLayers];
   DevBuf<float> loss_b;
   DevBuf<float> loss_terms;  // rate-MSE: [B][C] squared rate gaps
+  DevBuf<unsigned int> hist;  // activity regularizer: [n_mon][T+1] spike-count histograms
+  DevBuf<float> mon_counts;   // snn_monitor_counts output staging [B][H]
+  std::vector<int> mon_layers;  // monitored hidden layers feeding the regularizer, in order
   DevBuf<int32_t> correct_b;
   DevBuf<float> partial[kMaxLayers];
   DevBuf<int32_t> vec_index;
@@ -385,6 +388,16 @@ struct snn_engine {
     if (cfg.loss == 1 && !(cfg.rate_hi >= 0.0f && cfg.rate_hi <= 1.0f && cfg.rate_lo >= 0.0f &&
                            cfg.rate_lo <= 1.0f))
       fail(SNN_ERR_ARGUMENT, "spike_rate_mse: rates must lie in [0,1]");
+    for (int l = 0; l < SNN_MAX_HIDDEN; ++l)
+      if (n.monitor[l] != 0 && (n.monitor[l] != 1 || l >= n.n_hidden))
+        fail(SNN_ERR_SPEC, "monitor must follow a lif layer");
+    {
+      bool mon = false;
+      for (int l = 0; l < n.n_hidden; ++l) mon = mon || n.monitor[l] != 0;
+      if (mon && (cfg.lambda_low != 0.0f || cfg.lambda_high != 0.0f) &&
+          !(cfg.f_min <= cfg.f_max && cfg.f_min >= 0.0f && cfg.f_max <= 1.0f))
+        fail(SNN_ERR_ARGUMENT, "activity_regularizer: need 0 <= f_min <= f_max <= 1");
+    }
     // train()'s axis check (optimize.hpp:241-245); max_shift <= 0 never shifts (:276)
     if (cfg.n_shift_axes < 0 || cfg.n_shift_axes > 4) fail(SNN_ERR_ARGUMENT, "train: 0..4 shift axes");
     for (int i = 0; i < cfg.n_shift_axes; ++i) {
@@ -479,7 +492,7 @@ struct snn_engine {
     entries.clear();
     size_t off = 0;
     for (int j = 0; j <= L; ++j) {
-      const int lin = 2 * j, cell = 2 * j + 1;
+      const int lin = lin_id(j), cell = lin + 1;
       entries.push_back({"l" + std::to_string(lin) + ".w", kEntryW, j, K[j], N[j], off,
                          size_t(K[j]) * N[j]});
       off += size_t(K[j]) * N[j];
@@ -502,7 +515,7 @@ struct snn_engine {
     params.alloc(n_params);
     m.alloc(n_params);
     v.alloc(n_params);
-    comm.alloc(n_params + 2);
+    comm.alloc(n_params + 2 + L);  // grads, loss sum, hits, one regularizer value per monitor
     step.alloc(1);
     sched_slot.alloc(1);
     tail_done.alloc(1);
@@ -524,6 +537,11 @@ struct snn_engine {
     }
     loss_b.alloc(B);
     if (cfg.loss == 1) loss_terms.alloc(size_t(B) * C);
+    mon_layers.clear();
+    if (reg_on())
+      for (int l = 0; l < L; ++l)
+        if (net.monitor[l]) mon_layers.push_back(l);
+    if (!mon_layers.empty()) hist.alloc(mon_layers.size() * size_t(T + 1));
     correct_b.alloc(B);
     result_loss.alloc(1);
     result_acc.alloc(1);
@@ -548,7 +566,9 @@ struct snn_engine {
     for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
-    for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>})
+    for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>,
+                    k_lif_bwd<0, true>, k_lif_bwd<1, true>, k_lif_bwd<2, true>, k_lif_bwd<3, true>,
+                    k_lif_bwd<4, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -592,16 +612,30 @@ struct snn_engine {
   }
 
   // ---------------------------------------------------------- parameters
+  // normalised layer id of Linear j (network.hpp:125-157): its cell follows, and
+  // a monitor after LIF i < j takes one more id
+  int lin_id(int j) const {
+    int id = 2 * j;
+    for (int i = 0; i < j && i < L; ++i) id += net.monitor[i] ? 1 : 0;
+    return id;
+  }
+  bool reg_on() const {
+    if (cfg.lambda_low == 0.0f && cfg.lambda_high == 0.0f) return false;
+    for (int l = 0; l < L; ++l)
+      if (net.monitor[l]) return true;
+    return false;
+  }
+
   void init_params_host(uint64_t key) {
     // network.hpp:231-286: layer i key rng.child(i); W ~ TN(child(0)); beta ~ TN(child(2))
     std::vector<float> h(n_params, 0.0f);
     for (const auto& e : entries) {
       if (e.kind == kEntryW) {
-        const uint64_t lk = hostrng::child(key, uint64_t(2 * e.layer));
+        const uint64_t lk = hostrng::child(key, uint64_t(lin_id(e.layer)));
         const float sd = 1.0f / std::sqrt(float(e.rows));
         hostrng::truncated_normal(hostrng::child(lk, 0), e.size, 0.0f, sd, h.data() + e.offset);
       } else if (e.kind == kEntryBeta) {
-        const uint64_t lk = hostrng::child(key, uint64_t(2 * e.layer + 1));
+        const uint64_t lk = hostrng::child(key, uint64_t(lin_id(e.layer) + 1));
         if (e.beta_mode == 2)
           h[e.offset] = net.fixed_beta[e.layer];  // Tensor::scalar(fixed_beta)
         else  // per-neuron [H] or LearnableScalar [] from the same key
@@ -657,6 +691,7 @@ struct snn_engine {
     a.loss_denom = cfg.loss == 1 ? float(int64_t(B_global()) * C) : float(B_global());
     a.opt_kind = cfg.optimizer;
     a.momentum = cfg.momentum;
+    a.n_mon = int(mon_layers.size());
     a.loss_out = result_loss.p;
     a.acc_out = result_acc.p;
     return a;
@@ -815,6 +850,16 @@ struct snn_engine {
 
   void launch_bwd(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
                   const CUtensorMap& to, const BwdArgs& bw) {
+    if (bw.hist != nullptr) {  // monitored layer with the activity regularizer on
+      switch (act) {
+        case 1: launch(k_lif_bwd<1, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+        case 2: launch(k_lif_bwd<2, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+        case 3: launch(k_lif_bwd<3, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+        case 4: launch(k_lif_bwd<4, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+        default: launch(k_lif_bwd<0, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      }
+      return;
+    }
     switch (act) {
       case 1: launch(k_lif_bwd<1>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       case 2: launch(k_lif_bwd<2>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
@@ -947,6 +992,14 @@ struct snn_engine {
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
+      for (size_t m = 0; m < mon_layers.size(); ++m)
+        if (mon_layers[m] == l) {  // activity_regularizer_taped backward (objective.hpp:208-227)
+          bw.s_tp = s_tp[l].p;
+          bw.hist = hist.p + m * size_t(T + 1);
+          bw.reg_gs = 1.0f * 2.0f / (float(int64_t(B_global()) * H[l]) * float(T));
+          bw.f_min = cfg.f_min; bw.f_max = cfg.f_max;
+          bw.lambda_low = cfg.lambda_low; bw.lambda_high = cfg.lambda_high;
+        }
       launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages),
                  tm_wb[l + 1], tm_di_k[l + 1], tm_di_out[l], bw);
       mark(evs, "lif_bwd", l);
@@ -1003,6 +1056,14 @@ struct snn_engine {
       r.loss_terms = cfg.loss == 1 ? loss_terms.p : nullptr;
       r.n_loss_terms = cfg.loss == 1 ? B * C : B;
       r.w_blocks = int((n_params + kRedElemsPerBlock - 1) / kRedElemsPerBlock);
+      r.hist = hist.p;
+      r.n_mon = int(mon_layers.size());
+      r.hist_stride = T + 1;
+      r.reg_T = T;
+      for (size_t m = 0; m < mon_layers.size(); ++m)
+        r.mon_n[m] = float(int64_t(B_global()) * H[mon_layers[m]]);
+      r.f_min = cfg.f_min; r.f_max = cfg.f_max;
+      r.lambda_low = cfg.lambda_low; r.lambda_high = cfg.lambda_high;
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
       if (update && comm_handle == nullptr) {
         // no communicator: no allreduce between reduction and update -> one kernel
@@ -1018,7 +1079,7 @@ struct snn_engine {
       mark(evs, "reduce", -1);
     }
     if (comm_handle != nullptr) {
-      const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2, /*ncclFloat32*/ 7,
+      const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2 + mon_layers.size(), /*ncclFloat32*/ 7,
                                       /*ncclSum*/ 0, comm_handle, stream);
       if (rc != 0) fail(SNN_ERR_CUDA, "ncclAllReduce failed (%d)", rc);
       mark(evs, "nccl_allreduce", -1);
@@ -1031,7 +1092,7 @@ struct snn_engine {
     } else {
       launch(k_result, dim3(1), dim3(32), 0, (const float*)(comm.p + n_params), B_global(),
              cfg.loss == 1 ? float(int64_t(B_global()) * C) : float(B_global()), step.p,
-             0, result_loss.p, result_acc.p);
+             0, result_loss.p, result_acc.p, int(mon_layers.size()));
       mark(evs, "result", -1);
     }
   }
@@ -1665,6 +1726,22 @@ snn_status snn_apply(snn_engine* e, const uint32_t* rows, float* trace, size_t n
     e->set_rows_host(rows, e->data);
     CK(cudaGraphLaunch(e->graph_for(e->data, snn_engine::kEvalTrace), e->stream));
     CK(cudaMemcpyAsync(trace, e->eval_trace.p, need * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  });
+}
+
+snn_status snn_monitor_counts(snn_engine* e, int32_t layer, float* counts, size_t n) {
+  if (!e || !counts) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (layer < 0 || layer >= e->L || !e->net.monitor[layer])
+      fail(SNN_ERR_ARGUMENT, "hidden layer %d has no monitor", int(layer));
+    const size_t need = size_t(e->B) * e->H[layer];
+    if (n != need) fail(SNN_ERR_SHAPE, "counts holds %zu floats, need %zu", n, need);
+    if (e->mon_counts.n < need) e->mon_counts.alloc(need, false);
+    k_spike_counts<<<unsigned((need + 255) / 256), 256, 0, e->stream>>>(e->s_tp[layer].p, e->B, e->T_pad,
+                                                                         e->H[layer], e->mon_counts.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(counts, e->mon_counts.p, need * sizeof(float), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
   });
 }

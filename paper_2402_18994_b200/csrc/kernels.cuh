@@ -876,7 +876,20 @@ struct BwdArgs {
   long long* dbg_clk;          // optional [gridDim.x*gridDim.y][8] phase timestamps
   int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
   float theta, slope, aux;
+  // activity regularizer on a monitored layer (kReg launches only)
+  const uint32_t* s_tp;        // this layer's spikes, time-packed [H_pad][B*T_pad/32]
+  unsigned int* hist;          // [T+1] (sample, neuron) count histogram for the loss value
+  float reg_gs, f_min, f_max, lambda_low, lambda_high;  // reg_gs = 2 / (B_global*H * T)
 };
+
+// d loss / d count of one (sample, neuron) (objective.hpp:208-227): with g = 1,
+// gs (lambda_high dh - lambda_low dl), r = count / T -- the same float ops.
+__device__ __forceinline__ float activity_dcount(const BwdArgs& a, int count) {
+  const float r = __fdiv_rn(float(count), float(a.T));
+  const float xl = __fsub_rn(a.f_min, r), xh = __fsub_rn(r, a.f_max);
+  const float dl = xl > 0.0f ? xl : 0.0f, dh = xh > 0.0f ? xh : 0.0f;
+  return __fmul_rn(a.reg_gs, __fsub_rn(__fmul_rn(a.lambda_high, dh), __fmul_rn(a.lambda_low, dl)));
+}
 
 // Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
 // the unrolled step bodies stay branch-free; divisions evaluated as approximate
@@ -969,6 +982,14 @@ __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float 
   }
 }
 
+// dS of 16 steps + the monitor's per-(sample, neuron) term (two gradient
+// contributions to the stacked spikes: commutative, so the reference's order
+// does not matter)
+__device__ __forceinline__ void add_dcount(uint32_t (&r)[16], float term) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__fadd_rn(__uint_as_float(r[e]), term));
+}
+
 #ifndef SNN_BWD_EXP
 #define SNN_BWD_EXP 0  // timing experiments only (tests/clk_probe.py): 1 = skip the dI plane stores
 #endif
@@ -982,7 +1003,9 @@ __host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
   return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256 + 3 * 4 * kBwdScanThreads;
 }
 
-template <int kAct>
+// kReg: the layer feeds a monitor and the activity regularizer is on -- every
+// step's dS gains d loss / d count of its (sample, neuron) (sum_axis1 backward).
+template <int kAct, bool kReg = false>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
               const __grid_constant__ CUtensorMap tm_out, BwdArgs a) {
@@ -1104,6 +1127,22 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     // written by 6 TMA stores (long rows instead of 32-byte pieces of 128 rows)
     const bool stage_out = a.NT == 1;
     float Gcarry = 0.0f, db = 0.0f, dbias = 0.0f;
+    float rterm = 0.0f;
+    if constexpr (kReg) {
+      // spike count over the window (monitor_activity, neuron.hpp:106-114)
+      int count = -1;
+      if (n < a.H) {
+        const int wpb = a.T_pad / 32;
+        const uint32_t* w = a.s_tp + size_t(n) * (size_t(a.B) * wpb) + size_t(b) * wpb;
+        count = 0;
+        for (int i = 0; i < wpb; ++i) count += __popc(__ldg(w + i));
+        rterm = activity_dcount(a, count);
+      }
+      if (sg == 0) {  // one histogram entry per (sample, neuron), warp-aggregated
+        const unsigned peers = __match_any_sync(0xffffffffu, count);
+        if (count >= 0 && lane == __ffs(peers) - 1) atomicAdd(a.hist + count, unsigned(__popc(peers)));
+      }
+    }
     for (int j = 0; j < a.NT; ++j) {
       const int tt = a.NT - 1 - j, buf = j % nbuf;
       const int t_lo = tt * a.TT + sg * seg_len;               // first step of my segment
@@ -1132,6 +1171,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
         tmem_ld_wait();
+        if constexpr (kReg) add_dcount(r, rterm);
         if (nval >= 16) bwd_compose<kAct, false>(r, vr, 16, vb, theta, a, A, Bc);
         else bwd_compose<kAct, true>(r, vr, nval, vb, theta, a, A, Bc);
       }
@@ -1166,6 +1206,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           tmem_ld16(tcol + c0, r);
           tmem_ld_wait();
         }
+        if constexpr (kReg) add_dcount(r, rterm);
         if (a.dbg_ds != nullptr) {
 #pragma unroll
           for (int e = 0; e < 16; ++e)
@@ -1563,7 +1604,57 @@ struct ReduceArgs {
   int update;
   int B;
   int w_blocks;                         // blocks [0, w_blocks) handle W entries
+  // activity regularizer: one count histogram [T+1] per monitor (k_lif_bwd<., true>)
+  unsigned int* hist;                   // [n_mon][hist_stride], zeroed after reading
+  int n_mon, hist_stride, reg_T;
+  float mon_n[kMaxLayers];              // float(B_global * H) of each monitor
+  float f_min, f_max, lambda_low, lambda_high;
 };
+
+// 8 KB of static shared scratch shared by the tail's block-wide helpers
+__device__ __forceinline__ uint32_t* tail_scratch() {
+  __shared__ __align__(16) uint32_t buf[2048];
+  return buf;
+}
+
+// Regularizer value of monitor m (objective.hpp:189-205) from its count histogram:
+// lambda_low * (low / n) + lambda_high * (high / n), low / high summed per count
+// value in double with a fixed-shape tree (deterministic; the reference's running
+// float sum over (b, n) differs by rounding only), then the histogram is zeroed
+// for the next step.  Whole block calls; thread 0 holds the value.
+__device__ __forceinline__ float activity_value(const ReduceArgs& r, int m) {
+  double* s_lo = reinterpret_cast<double*>(tail_scratch());
+  double* s_hi = s_lo + 256;
+  const int tid = threadIdx.x;
+  __syncthreads();  // the scratch may still be read by the previous helper
+  unsigned int* h = r.hist + size_t(m) * r.hist_stride;
+  double lo = 0.0, hi = 0.0;
+  for (int c = tid; c <= r.reg_T; c += blockDim.x) {
+    const unsigned k = h[c];
+    if (k == 0u) continue;
+    const float rate = __fdiv_rn(float(c), float(r.reg_T));
+    const float xl = __fsub_rn(r.f_min, rate), xh = __fsub_rn(rate, r.f_max);
+    const float dl = xl > 0.0f ? xl : 0.0f, dh = xh > 0.0f ? xh : 0.0f;
+    lo += double(k) * double(__fmul_rn(dl, dl));
+    hi += double(k) * double(__fmul_rn(dh, dh));
+  }
+  s_lo[tid] = lo;
+  s_hi[tid] = hi;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (tid < w) {
+      s_lo[tid] += s_lo[tid + w];
+      s_hi[tid] += s_hi[tid + w];
+    }
+    __syncthreads();
+  }
+  const float n = r.mon_n[m];
+  const float v = __fadd_rn(__fmul_rn(r.lambda_low, __fdiv_rn(float(s_lo[0]), n)),
+                            __fmul_rn(r.lambda_high, __fdiv_rn(float(s_hi[0]), n)));
+  __syncthreads();
+  for (int c = tid; c <= r.reg_T; c += blockDim.x) h[c] = 0u;
+  return v;
+}
 
 __device__ __forceinline__ int find_entry(const Entry* en, int n, int64_t i) {
   int e = 0;
@@ -1614,8 +1705,8 @@ constexpr int kRedElemsPerBlock = 128;  // W elements per 256-thread block (lane
 // terms (objective.hpp:150-157) -- and the hit count.  Whole block calls; thread
 // 0 holds the results.
 __device__ __forceinline__ void loss_and_hits(const ReduceArgs& r, float& loss, int& hits) {
-  __shared__ float sl[1024];
-  __shared__ int sc[1024];
+  float* sl = reinterpret_cast<float*>(tail_scratch());
+  int* sc = reinterpret_cast<int*>(tail_scratch() + 1024);
   const int tid = threadIdx.x;
   const float* terms = r.loss_terms != nullptr ? r.loss_terms : r.loss_b;
   loss = 0.0f;
@@ -1684,7 +1775,8 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     }
     return;
   }
-  // loss / hits / step
+  // loss / hits / step; activity regularizer values after them (summed over ranks
+  // by the allreduce, added to the loss by k_adam / k_result)
   float loss;
   int hits;
   loss_and_hits(a, loss, hits);
@@ -1692,6 +1784,10 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     a.grads[a.n_params] = loss;
     a.grads[a.n_params + 1] = float(hits);
     if (a.update) *a.step += 1;
+  }
+  for (int m = 0; m < a.n_mon; ++m) {
+    const float v = activity_value(a, m);
+    if (tid == 0) a.grads[a.n_params + 2 + m] = v;
   }
 }
 
@@ -1720,6 +1816,7 @@ struct AdamArgs {
   float loss_denom;          // float(B_global) (CE) or float(B_global * C) (rate-MSE)
   int opt_kind;              // 0 Adam, 1 SGD + momentum (optimize.hpp:69-84)
   float momentum;
+  int n_mon;                 // activity regularizer values at grads[n_params + 2 + m]
 };
 
 // Adam on one flat parameter (optimize.hpp:88-110); bias corrections of step s+1.
@@ -1767,7 +1864,9 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a.update && i == 0) {
     // StepResult{loss, accuracy} (optimize.hpp:143-147, :193-196)
-    *a.loss_out = __fdiv_rn(a.grads[a.n_params], a.loss_denom);
+    float l = __fdiv_rn(a.grads[a.n_params], a.loss_denom);
+    for (int m = 0; m < a.n_mon; ++m) l = __fadd_rn(l, a.grads[a.n_params + 2 + m]);  // optimize.hpp:185-191
+    *a.loss_out = l;
     *a.acc_out = double(a.grads[a.n_params + 1]) / double(a.B_global);
     if (a.rows_slot != nullptr) *a.rows_slot += 1;
   }
@@ -1853,10 +1952,18 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
     float loss;
     int hits;
     loss_and_hits(r, loss, hits);
+    float l = __fdiv_rn(loss, a.loss_denom);
+    for (int m = 0; m < r.n_mon; ++m) {  // loss = add(loss, regularizer) per monitor (optimize.hpp:185-191)
+      const float v = activity_value(r, m);
+      if (tid == 0) {
+        r.grads[r.n_params + 2 + m] = v;
+        l = __fadd_rn(l, v);
+      }
+    }
     if (tid == 0) {
       r.grads[r.n_params] = loss;
       r.grads[r.n_params + 1] = float(hits);
-      *a.loss_out = __fdiv_rn(loss, a.loss_denom);
+      *a.loss_out = l;
       *a.acc_out = double(hits) / double(a.B_global);
     }
   }
@@ -1944,12 +2051,27 @@ __global__ void k_relayout(const uint8_t* __restrict__ in, uint8_t* __restrict__
   reinterpret_cast<uint32_t*>(out)[q] = word;  // IN_pad is a multiple of 64
 }
 
+// monitor_activity (neuron.hpp:106-114): counts[b][n] = spikes of (b, n) over the
+// window, from the time-packed raster of the last forward.
+__global__ void k_spike_counts(const uint32_t* __restrict__ s_tp, int B, int T_pad, int H,
+                               float* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(B) * H) return;
+  const int b = int(i / H), n = int(i % H), wpb = T_pad / 32;
+  const uint32_t* w = s_tp + size_t(n) * (size_t(B) * wpb) + size_t(b) * wpb;
+  int c = 0;
+  for (int k = 0; k < wpb; ++k) c += __popc(__ldg(w + k));
+  out[i] = float(c);
+}
+
 // StepResult{loss / B_global, hits / B_global}; advances the step counter.
 __global__ void k_result(const float* tail, int B_global, float loss_denom, int64_t* step,
-                         int do_step, float* loss_out, double* acc_out) {
+                         int do_step, float* loss_out, double* acc_out, int n_mon) {
   pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  *loss_out = __fdiv_rn(tail[0], loss_denom);
+  float l = __fdiv_rn(tail[0], loss_denom);
+  for (int m = 0; m < n_mon; ++m) l = __fadd_rn(l, tail[2 + m]);
+  *loss_out = l;
   *acc_out = double(tail[1]) / double(B_global);
   if (do_step) *step += 1;
 }

@@ -79,6 +79,12 @@ class LILayer:
 
 
 @dataclass
+class MonitorLayer:
+    """Spike counts of the LIF layer before it (network.hpp:57); feeds the activity
+    regularizer and ApplyResult.monitors.  Takes a normalised layer id."""
+
+
+@dataclass
 class NetworkSpec:
     input_shape: Sequence[int]
     layers: list
@@ -102,16 +108,21 @@ class TrainConfig:
     rate_lo: float = 0.1
     max_shift: int = 0                   # shift augmentation on packed batches
     shift_axes: tuple = ()               # feature axis only (2 or -1); 0 / 1 rejected
+    f_min: float = 0.0                   # activity regularizer; zero lambdas disable it
+    f_max: float = 1.0
+    lambda_low: float = 0.0
+    lambda_high: float = 0.0
 
 
-ABI_VERSION = 4  # SNN_ABI_VERSION in include/snn_engine.h
+ABI_VERSION = 5  # SNN_ABI_VERSION in include/snn_engine.h
 
 
 class _NetDesc(C.Structure):
     _fields_ = [("input", C.c_int32), ("n_hidden", C.c_int32), ("hidden", C.c_int32 * 8),
                 ("classes", C.c_int32), ("bias", C.c_int32), ("threshold", C.c_float),
                 ("activation", C.c_int32), ("slope", C.c_float), ("aux", C.c_float),
-                ("beta_mode", C.c_int32 * 9), ("fixed_beta", C.c_float * 9)]
+                ("beta_mode", C.c_int32 * 9), ("fixed_beta", C.c_float * 9),
+                ("monitor", C.c_int32 * 8)]
 
 
 BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
@@ -123,7 +134,8 @@ class _TrainCfg(C.Structure):
                 ("seed", C.c_uint64), ("unroll", C.c_int32), ("optimizer", C.c_int32),
                 ("momentum", C.c_float), ("loss", C.c_int32), ("rate_hi", C.c_float),
                 ("rate_lo", C.c_float), ("max_shift", C.c_int32), ("n_shift_axes", C.c_int32),
-                ("shift_axes", C.c_int32 * 4)]
+                ("shift_axes", C.c_int32 * 4), ("f_min", C.c_float), ("f_max", C.c_float),
+                ("lambda_low", C.c_float), ("lambda_high", C.c_float)]
 
 
 def normalize(spec: NetworkSpec) -> dict:
@@ -137,7 +149,15 @@ def normalize(spec: NetworkSpec) -> dict:
     if not isinstance(last, (LIFLayer, LILayer)):
         raise SpecError("network must end in a lif or li readout")
     inp = int(np.prod(spec.input_shape))
-    layers = list(spec.layers)
+    layers, monitor = [], []
+    for i, layer in enumerate(spec.layers):
+        if isinstance(layer, MonitorLayer):  # network.hpp:139-144
+            if not layers or not isinstance(layers[-1], LIFLayer) or (monitor and monitor[-1] == len(layers)):
+                raise SpecError(f"layer {i}: monitor must follow a lif layer")
+            monitor.append(len(layers))
+            continue
+        layers.append(layer)
+    monitor = [m // 2 - 1 for m in monitor]  # index of the hidden LIF block
     if len(layers) < 4 or len(layers) % 2:
         raise UnsupportedError("engine supports [Linear, LIF]*k + Linear + LI")
     hidden, act, thr, bias, modes, fixed = [], None, None, None, [], []
@@ -167,7 +187,7 @@ def normalize(spec: NetworkSpec) -> dict:
     return dict(input=inp, hidden=hidden, classes=int(lin.out), bias=bool(bias),
                 threshold=float(thr), activation=act.name, slope=float(act.slope),
                 aux=float(act.aux), beta_mode=modes + [cell.beta_mode],
-                fixed_beta=fixed + [float(cell.fixed_beta)])
+                fixed_beta=fixed + [float(cell.fixed_beta)], monitor=monitor)
 
 
 def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False) -> NetworkSpec:
@@ -194,7 +214,9 @@ def lib() -> C.CDLL:
     if not os.path.exists(lib):
         raise DeviceError(f"{lib} missing: the CUDA engine is required (no CPU fallback)")
     L = C.CDLL(lib, mode=C.RTLD_GLOBAL)
-    if L.snn_abi_version() != ABI_VERSION:  # struct layouts below must match the library
+    # struct layouts below must match the library (SNN_B200_ABI_ANY: timing A/B of an
+    # older build whose structs are a prefix of these -- never for results)
+    if L.snn_abi_version() != ABI_VERSION and not os.environ.get("SNN_B200_ABI_ANY"):
         raise DeviceError(f"{lib}: ABI {L.snn_abi_version()} != {ABI_VERSION}; rebuild")
     L.snn_last_error.restype = C.c_char_p
     L.snn_last_error.argtypes = [C.c_void_p]
@@ -211,8 +233,9 @@ def lib() -> C.CDLL:
                  "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_evaluate", "snn_apply", "snn_save_checkpoint", "snn_load_checkpoint", "snn_sync", "snn_read_result",
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
-                 "snn_read_dataset"):
-        getattr(L, name).restype = C.c_int
+                 "snn_read_dataset", "snn_monitor_counts"):
+        if hasattr(L, name) or not os.environ.get("SNN_B200_ABI_ANY"):
+            getattr(L, name).restype = C.c_int
     L.snn_launch_name.restype = C.c_char_p
     L.snn_launch_name.argtypes = [C.c_void_p, C.c_int32]
     L.snn_engine_destroy.restype = None
@@ -248,6 +271,8 @@ class Engine:
         for i, (bm, fb) in enumerate(zip(d["beta_mode"], d["fixed_beta"])):
             n.beta_mode[i] = BETA_MODES[bm]
             n.fixed_beta[i] = fb
+        for m in d["monitor"]:
+            n.monitor[m] = 1
         c = _TrainCfg()
         c.batch_size = int(cfg.batch_size)
         c.time_steps = int(time_steps)
@@ -267,6 +292,8 @@ class Engine:
         if len(axes) > 4:
             raise ArgumentError("train: at most 4 shift axes")
         c.max_shift, c.n_shift_axes = int(cfg.max_shift), len(axes)
+        c.f_min, c.f_max = float(cfg.f_min), float(cfg.f_max)
+        c.lambda_low, c.lambda_high = float(cfg.lambda_low), float(cfg.lambda_high)
         for i, a in enumerate(axes):
             c.shift_axes[i] = a
         self._L = lib()
@@ -442,6 +469,16 @@ class Engine:
         out = np.empty((self.batch_size, self.time_steps, self.desc["classes"]), np.float32)
         self._check(self._L.snn_apply(self._h, _p(r, C.c_uint32), _p(out, C.c_float),
                                       C.c_size_t(out.size)))
+        return out
+
+    def monitor_counts(self, layer: int) -> np.ndarray:
+        """ApplyResult.monitors entry of the monitor after hidden LIF `layer`: spike
+        counts [B, H] of the last forward (neuron.hpp:106-114)."""
+        if layer not in self.desc["monitor"]:
+            raise ArgumentError(f"hidden layer {layer} has no monitor")
+        out = np.empty((self.batch_size, self.desc["hidden"][layer]), np.float32)
+        self._check(self._L.snn_monitor_counts(self._h, C.c_int32(layer), _p(out, C.c_float),
+                                               C.c_size_t(out.size)))
         return out
 
     # ------------------------------------------------------------ checkpoints

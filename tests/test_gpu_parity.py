@@ -35,6 +35,10 @@ def make_engine(net: Net, B, T, seed=0, lr=1e-3, **cfg):
             layer.threshold = net.threshold
             if net.slope is not None:
                 layer.activation.slope = net.slope
+    if net.monitor:  # MonitorLayer after the listed hidden LIF layers
+        from paper_2402_18994_b200 import MonitorLayer
+        for m in sorted(net.monitor, reverse=True):
+            spec.layers.insert(2 * m + 2, MonitorLayer())
     return Engine(spec, TrainConfig(batch_size=B, seed=seed, lr=lr, unroll=net.unroll, **cfg), T)
 
 
@@ -620,3 +624,104 @@ def test_shift_axes_validation():
     with pytest.raises(UnsupportedError):
         make_engine(net, 2, 16, max_shift=2, shift_axes=(-2,))
     make_engine(net, 2, 16, max_shift=0, shift_axes=(3,))
+
+
+ACT_OPTS = {"both": dict(lambda_low=0.5, lambda_high=2.0, f_min=0.1, f_max=0.3),
+            "high": dict(lambda_high=1.5, f_max=0.05)}
+
+
+def _act_net(g):
+    return Net(inp=int(g["inp"]), hidden=tuple(int(h) for h in g["hidden"]), classes=int(g["classes"]),
+               bias=bool(g["bias"]), threshold=float(g["threshold"]), act=str(g["act"]),
+               unroll=int(g["unroll"]), monitor=tuple(int(m) for m in g["monitor"]))
+
+
+@pytest.mark.parametrize("name", list(ACT_OPTS))
+def test_activity_regularizer_matches_reference_fixture(orc, golden, name):
+    """MonitorLayer + activity regularizer (objective.hpp:186-227, optimize.hpp:185-191)
+    against the reference's own numbers: init and entry names with the shifted
+    layer ids, loss and grads of one step, three train_steps."""
+    g = golden("activity")
+    net = _act_net(g)
+    T = int(g["t"])
+    eng = make_engine(net, 7, T, seed=41, **ACT_OPTS[name])
+    assert np.array_equal(eng.get_params(), g["params_init"]), "init keys with monitors"
+    assert [e[0] for e in eng.entries()] == [str(n) for n in g["names"]]
+    eng.stage_dataset(g["packed"], g["y"])
+    eng.set_params(g["params"])
+    rows = np.arange(7, dtype=np.uint32)
+    loss, _ = eng.forward_backward(rows)
+    assert abs(loss - g[f"{name}_loss"]) <= REL_TOL * abs(g[f"{name}_loss"])
+    check_grads(orc, net, eng.get_grads(), g[f"{name}_grads"])
+    losses = [eng.train_step(rows)[0] for _ in range(3)]
+    assert np.allclose(losses, g[f"{name}_step_losses"], rtol=REL_TOL, atol=0)
+    assert relnorm(eng.get_params(), g[f"{name}_params3"]) <= 1e-4
+
+
+def test_activity_regularizer_c1_shape_matches_oracle(orc):
+    """C1 shape (B=64) with monitors on both LIF layers, both hinge sides active."""
+    from oracle.pyoracle import Opts
+    net = Net(monitor=(0, 1))
+    B, T = 64, 128
+    params = orc.init(net, orc.key_child(orc.key_from_seed(2), 0)) * np.float32(2.0)
+    x, y = orc.synth_raster(20, B, T, 700, 6)
+    pk = orc.pack_time(x)
+    # strong enough that the regularizer moves the gradient ~50x the parity bar
+    kw = dict(lambda_low=3000.0, lambda_high=4500.0, f_min=0.05, f_max=0.2)
+    eng = make_engine(net, B, T, **kw)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    rows = np.arange(B, dtype=np.uint32)
+    loss, _ = eng.forward_backward(rows)
+    ref = orc.forward_backward(net, params, pk, T, y, opts=Opts(**kw), want_spikes=True)
+    plain = orc.forward_backward(net, params, pk, T, y)
+    assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    assert ref["loss"] > plain["loss"] and relnorm(ref["grads"], plain["grads"]) > 3e-3, "regularizer inactive"
+    check_grads(orc, net, eng.get_grads(), ref["grads"])
+    # ApplyResult.monitors: spike counts of the same forward
+    for l in range(2):
+        assert np.array_equal(eng.monitor_counts(l), ref["spikes"][l].sum(axis=1).astype(np.float32))
+    # the update path (fused tail) reports the same loss, and the histogram resets per step
+    l1, _ = eng.train_step(rows)
+    assert abs(l1 - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    l2, _ = eng.forward_backward(rows)
+    ref2 = orc.forward_backward(net, eng.get_params(), pk, T, y, opts=Opts(**kw))
+    assert abs(l2 - ref2["loss"]) <= REL_TOL * abs(ref2["loss"])
+
+
+def test_activity_regularizer_nccl_tail_matches_fused_tail(orc):
+    """Regularizer values travel through the allreduce buffer on the multi-rank tail."""
+    from paper_2402_18994_b200 import DeviceError, Engine
+    net = Net(inp=30, hidden=(16, 12), classes=5, monitor=(1,))
+    x, y = orc.synth_raster(5, 8, 19, 30, 2)
+    pk = orc.pack_time(x)
+    kw = dict(lambda_low=0.5, lambda_high=0.5, f_min=0.2, f_max=0.4)
+    e1, e2 = make_engine(net, 4, 19, seed=3, **kw), make_engine(net, 4, 19, seed=3, **kw)
+    try:
+        e2.comm_init(Engine.nccl_unique_id(), 0, 1)
+    except DeviceError as err:
+        pytest.skip(f"NCCL unavailable: {err}")
+    for eng in (e1, e2):
+        eng.stage_dataset(pk, y)
+    for i in range(3):
+        rows = np.arange(4 * (i % 2), 4 * (i % 2) + 4, dtype=np.uint32)
+        assert e1.train_step(rows) == e2.train_step(rows)
+    assert np.array_equal(e1.get_params(), e2.get_params())
+
+
+def test_monitor_spec_errors():
+    from paper_2402_18994_b200 import (ArgumentError, Engine, LIFLayer, LILayer, LinearLayer,
+                                       MonitorLayer, NetworkSpec, SpecError, TrainConfig)
+    bad = NetworkSpec([30], [LinearLayer(16), MonitorLayer(), LIFLayer(), LinearLayer(5), LILayer()])
+    with pytest.raises(SpecError):
+        Engine(bad, TrainConfig(batch_size=2), 16)
+    twice = NetworkSpec([30], [LinearLayer(16), LIFLayer(), MonitorLayer(), MonitorLayer(),
+                               LinearLayer(5), LILayer()])
+    with pytest.raises(SpecError):
+        Engine(twice, TrainConfig(batch_size=2), 16)
+    ok = NetworkSpec([30], [LinearLayer(16), LIFLayer(), MonitorLayer(), LinearLayer(5), LILayer()])
+    with pytest.raises(ArgumentError):
+        Engine(ok, TrainConfig(batch_size=2, lambda_low=1.0, f_min=0.6, f_max=0.3), 16)
+    eng = Engine(ok, TrainConfig(batch_size=2, f_min=0.6, f_max=0.3), 16)  # lambdas 0: unchecked
+    with pytest.raises(ArgumentError):
+        eng.monitor_counts(1)
