@@ -250,6 +250,8 @@ def main():
               "l2": f"HBM-resident dataset of {w['n_data']} examples "
                     f"({w['n_data'] * (w['T'] // 8) * ((w['inp'] + 63) // 64 * 64) / 1e6:.0f} MB "
                     f"staged) > 126 MB L2; fresh permuted rows every step, no L2 flush"}
+    if world > 1:
+        config["dp_tail"] = os.environ.get("SNN_DP_TAIL", "peer")  # gradient exchange (parallel.py)
 
     if args.impl == "reference":
         if rank != 0:
@@ -280,9 +282,9 @@ def main():
     B = w["B"]
     eng = Engine(spec, TrainConfig(batch_size=B, seed=0, lr=1e-3), w["T"], device=local)
     if world > 1:
-        uid = [Engine.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        eng.comm_init(uid[0], rank, world)
+        # gradient exchange: peer-memory tail (default) or NCCL (SNN_DP_TAIL=nccl)
+        from paper_2402_18994_b200.parallel import setup_data_parallel
+        setup_data_parallel(eng, rank, world, dist, os.environ.get("SNN_DP_TAIL", "peer"))
     n_data = w["n_data"]
     eng.synth_dataset(n_data, seed=1)
     # schedule: the reference epoch shuffle, this rank's contiguous slice of each global batch

@@ -318,9 +318,20 @@ struct snn_engine {
   // graphs keyed by (dataset ptr, update flag, mode): mode 0 = rows_cur, mode g >= 1 =
   // g consecutive schedule steps (rows from sched[*sched_slot])
   std::map<std::tuple<const void*, int, int>, cudaGraphExec_t> graphs;
-  // multi-GPU
+  // multi-GPU: tail 0 = one rank (k_reduce_adam), 1 = NCCL (k_reduce, ncclAllReduce,
+  // k_adam), 2 = peer memory (k_reduce publishing into IPC-mapped exchange buffers,
+  // k_peer_adam summing them and updating)
   void* comm_handle = nullptr;
   int rank = 0, world = 1;
+  int tail_mode = 0;
+  DevBuf<uint8_t> peer_mem;          // [2][n_comm] f32 exchange buffers, then kMaxRanks u64 flags
+  int64_t n_comm = 0;
+  float* peer_xchg[kMaxRanks] = {};  // every rank's exchange buffer (mapped; own = local)
+  unsigned long long* peer_flags[kMaxRanks] = {};
+  void* peer_ipc[kMaxRanks] = {};    // opened IPC mappings (closed on destroy)
+  DevBuf<int64_t> peer_seq;
+  DevBuf<unsigned int> peer_done;    // [0] k_reduce publish counter, [1] k_peer_adam completion
+  int split_part = -1;               // test hook: enqueue only the part before (0) / of (1) the peer wait
   bool planes_dirty = true;
   // pipeline depths (smem per CTA decides how many CTAs share an SM)
   int fwd_stages = std::min(kFwdStagesMax, env_int("SNN_FWD_STAGES", 2));
@@ -342,6 +353,8 @@ struct snn_engine {
     if (device >= 0) cudaSetDevice(device);
     for (auto& g : graphs) cudaGraphExecDestroy(g.second);
     if (comm_handle && nccl().ok) nccl().CommDestroy(comm_handle);
+    for (void* p : peer_ipc)
+      if (p) cudaIpcCloseMemHandle(p);
     if (h_loss) cudaFreeHost(h_loss);
     if (h_acc) cudaFreeHost(h_acc);
     if (h_rows) cudaFreeHost(h_rows);
@@ -886,7 +899,29 @@ struct snn_engine {
   }
   // forward groups + readout + L bwd + wgrad + tail (fused reduce+Adam without a
   // communicator; reduce, adam with one -- the allreduce between them is NCCL's)
-  int launches_per_step() const { return int(fwd_groups().size()) + L + (comm_handle == nullptr ? 3 : 4); }
+  int launches_per_step() const { return int(fwd_groups().size()) + L + (tail_mode == 0 ? 3 : 4); }
+
+  // exchange buffers + flags of the peer tail (cudaMalloc'd: IPC-exportable)
+  void ensure_peer_mem() {
+    if (peer_mem.p) return;
+    n_comm = (int64_t(n_params) + 2 + L + 63) / 64 * 64;
+    peer_mem.alloc(size_t(2 * n_comm) * 4 + kMaxRanks * 8);
+    peer_seq.alloc(1);
+    peer_done.alloc(2);
+  }
+  unsigned long long* flags_of(uint8_t* base) const {
+    return reinterpret_cast<unsigned long long*>(base + size_t(2 * n_comm) * 4);
+  }
+  void set_peers(int r, int w, uint8_t* const* bases) {
+    for (int q = 0; q < w; ++q) {
+      peer_xchg[q] = reinterpret_cast<float*>(bases[q]);
+      peer_flags[q] = flags_of(bases[q]);
+    }
+    rank = r;
+    world = w;
+    tail_mode = 2;
+    clear_graphs();
+  }
 
   std::vector<std::string> launch_names;
   std::vector<cudaEvent_t> prof_ev;
@@ -903,9 +938,31 @@ struct snn_engine {
   }
 
   // One step.  sched_mode: rows = sched[*sched_slot] (advanced by the step tail).
+  // Peer tail: cross-rank gradient sum over mapped peer memory + the update.
+  void enqueue_peer_tail(int update, std::vector<cudaEvent_t>* evs, bool sched_mode) {
+    PeerArgs pa{};
+    for (int q = 0; q < world; ++q) pa.xchg[q] = peer_xchg[q];
+    pa.flags = peer_flags[rank];
+    pa.n_comm = n_comm;
+    pa.seq = peer_seq.p;
+    pa.done = peer_done.p + 1;
+    pa.grads_out = comm.p;
+    pa.rows_slot = sched_mode ? sched_slot.p : nullptr;
+    pa.step = step.p;
+    pa.world = world;
+    AdamArgs a = adam_args(update);
+    launch(k_peer_adam, dim3(unsigned((n_params + 255) / 256)), dim3(256), 0, pa, a);
+    mark(evs, "peer_adam", -1);
+  }
+
   void enqueue_body(const Dataset& ds, int update, std::vector<cudaEvent_t>* evs = nullptr,
                     bool sched_mode = false) {
     launch_names.clear();
+    if (tail_mode == 2 && split_part == 1) {  // test hook: only the tail of a split step
+      if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
+      enqueue_peer_tail(update, evs, sched_mode);
+      return;
+    }
     const uint32_t* rows_p = sched_mode ? sched.p : rows_cur.p;
     const int64_t* slot_p = sched_mode ? sched_slot.p : nullptr;
     if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
@@ -1065,7 +1122,16 @@ struct snn_engine {
       r.f_min = cfg.f_min; r.f_max = cfg.f_max;
       r.lambda_low = cfg.lambda_low; r.lambda_high = cfg.lambda_high;
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
-      if (update && comm_handle == nullptr) {
+      if (tail_mode == 2) {
+        r.xchg = reinterpret_cast<float*>(peer_mem.p);
+        r.n_comm = n_comm;
+        r.seq = peer_seq.p;
+        for (int q = 0; q < world; ++q) r.peer_flags[q] = peer_flags[q];
+        r.rank = rank;
+        r.world = world;
+        r.done = peer_done.p;
+      }
+      if (update && tail_mode == 0) {
         // no communicator: no allreduce between reduction and update -> one kernel
         AdamArgs a = adam_args(1);
         long long* tclk = debug && size_t(blocks) * kClkStride <= clk_region()
@@ -1075,8 +1141,14 @@ struct snn_engine {
         mark(evs, "reduce_adam", -1);
         return;
       }
-      launch(k_reduce, dim3(blocks), dim3(256), 0, r);
-      mark(evs, "reduce", -1);
+      if (split_part != 1) {
+        launch(k_reduce, dim3(blocks), dim3(256), 0, r);
+        mark(evs, "reduce", -1);
+      }
+    }
+    if (tail_mode == 2) {
+      if (split_part != 0) enqueue_peer_tail(update, evs, sched_mode);
+      return;
     }
     if (comm_handle != nullptr) {
       const int rc = nccl().AllReduce(comm.p, comm.p, n_params + 2 + mon_layers.size(), /*ncclFloat32*/ 7,
@@ -1839,6 +1911,7 @@ snn_status snn_comm_init(snn_engine* e, const uint8_t id[128], int32_t rank, int
   return guard(e, [&] {
     // world == 1 still creates a (single-rank) communicator: the step then runs the
     // multi-rank tail (k_reduce -> ncclAllReduce -> k_adam), testable on one GPU
+    if (e->tail_mode == 2) fail(SNN_ERR_STATE, "engine already runs the peer-memory tail");
     NcclApi& api = nccl();
     if (!api.ok) fail(SNN_ERR_CUDA, "libnccl.so.2 not loadable");
     UniqueId u;
@@ -1849,7 +1922,83 @@ snn_status snn_comm_init(snn_engine* e, const uint8_t id[128], int32_t rank, int
     e->comm_handle = comm;
     e->rank = rank;
     e->world = world;
+    e->tail_mode = 1;
     e->clear_graphs();
+  });
+}
+
+snn_status snn_peer_handle(snn_engine* e, uint8_t handle[64]) {
+  if (!e || !handle) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    e->ensure_peer_mem();
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, e->peer_mem.p));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+snn_status snn_peer_open(snn_engine* e, int32_t rank, int32_t world, const uint8_t* handles) {
+  if (!e || !handles || world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (e->comm_handle) fail(SNN_ERR_STATE, "engine already has an NCCL communicator");
+    e->ensure_peer_mem();
+    uint8_t* bases[kMaxRanks] = {};
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) {
+        bases[q] = e->peer_mem.p;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + size_t(q) * 64, 64);
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      e->peer_ipc[q] = p;
+      bases[q] = static_cast<uint8_t*>(p);
+    }
+    e->set_peers(rank, world, bases);
+  });
+}
+
+snn_status snn_peer_attach_local(snn_engine* const* engines, int32_t world) {
+  if (!engines || world < 1 || world > kMaxRanks) return SNN_ERR_ARGUMENT;
+  for (int q = 0; q < world; ++q)
+    if (!engines[q]) return SNN_ERR_ARGUMENT;
+  snn_status st = SNN_OK;
+  uint8_t* bases[kMaxRanks] = {};
+  for (int q = 0; q < world && st == SNN_OK; ++q)
+    st = guard(engines[q], [&] {
+      if (engines[q]->device != engines[0]->device) fail(SNN_ERR_ARGUMENT, "ranks on different devices");
+      if (engines[q]->n_params != engines[0]->n_params) fail(SNN_ERR_ARGUMENT, "ranks differ in network");
+      engines[q]->ensure_peer_mem();
+      bases[q] = engines[q]->peer_mem.p;
+    });
+  for (int q = 0; q < world && st == SNN_OK; ++q)
+    st = guard(engines[q], [&] { engines[q]->set_peers(q, world, bases); });
+  return st;
+}
+
+snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t part, float* loss,
+                                double* accuracy) {
+  if (!e || (part != 0 && part != 1) || (part == 0 && !rows)) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (e->tail_mode != 2) fail(SNN_ERR_STATE, "split steps need the peer tail");
+    if (e->data.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    struct Reset {
+      snn_engine* e;
+      ~Reset() { e->split_part = -1; }
+    } reset{e};
+    e->split_part = part;
+    if (part == 0) {
+      e->set_rows_host(rows, e->data);
+      e->ensure_bc_capacity();
+      e->enqueue_body(e->data, 1);
+      CK(cudaStreamSynchronize(e->stream));
+    } else {
+      e->enqueue_body(e->data, 1);
+      e->host_step += 1;
+      e->read_result(loss, accuracy);
+    }
   });
 }
 

@@ -32,6 +32,7 @@ using namespace sm100;
 
 constexpr int kMaxClasses = 32;
 constexpr int kMaxLayers = 9;  // Linear layers (hidden + readout)
+constexpr int kMaxRanks = 8;   // data-parallel ranks of the peer-memory tail (one NVSwitch box)
 // debug phase-timestamp record per CTA; [14]/[15] = globaltimer start/end
 constexpr int kClkStride = 48;  // [16, 48): per-k-block stamps (forward MMA thread)
 
@@ -1609,6 +1610,15 @@ struct ReduceArgs {
   int n_mon, hist_stride, reg_T;
   float mon_n[kMaxLayers];              // float(B_global * H) of each monitor
   float f_min, f_max, lambda_low, lambda_high;
+  // peer tail (ranks exchange gradients through IPC-mapped device memory): xchg is
+  // this rank's exchange buffer [2][n_comm] (nullptr otherwise), seq the exchange
+  // sequence number, peer_flags every rank's flag array [kMaxRanks] (mapped)
+  float* xchg;
+  int64_t n_comm;
+  const int64_t* seq;
+  unsigned long long* peer_flags[kMaxRanks];
+  int rank, world;
+  unsigned int* done;
 };
 
 // 8 KB of static shared scratch shared by the tail's block-wide helpers
@@ -1733,61 +1743,87 @@ __device__ __forceinline__ void loss_and_hits(const ReduceArgs& r, float& loss, 
 // fixed-order sum of the split-K partials (sum_partials_pair).  Next blocks: one warp per beta/bias element --
 // lanes take strided samples, then a fixed-shape tree (deterministic).  Last
 // block: loss sum in batch order (objective.hpp:57-72) + hits, step counter.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
   pdl_wait();
   const int tid = threadIdx.x;
+  // peer tail: this step's gradient goes to the exchange buffer of parity seq & 1
+  const int64_t seq = a.xchg != nullptr ? *reinterpret_cast<volatile const int64_t*>(a.seq) : 0;
+  float* __restrict__ gout = a.xchg != nullptr ? a.xchg + (seq & 1) * a.n_comm : a.grads;
+  const int vb_blocks = (a.n_vec + 7) / 8;
   if (int(blockIdx.x) < a.w_blocks) {
     // pairs stay converged: out-of-range / non-W pairs skip as a whole
     const int64_t i = int64_t(blockIdx.x) * kRedElemsPerBlock + (tid >> 1);
-    if (i >= a.n_params) return;
-    const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
-    if (en.kind != kEntryW) return;
-    const float g = sum_partials_pair(a, en, i - en.offset, tid & 1);
-    if ((tid & 1) == 0) a.grads[i] = g;
-    return;
-  }
-  const int vb_blocks = (a.n_vec + 7) / 8;
-  if (int(blockIdx.x) < a.w_blocks + vb_blocks) {
+    if (i < a.n_params) {
+      const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
+      if (en.kind == kEntryW) {
+        const float g = sum_partials_pair(a, en, i - en.offset, tid & 1);
+        if ((tid & 1) == 0) gout[i] = g;
+      }
+    }
+  } else if (int(blockIdx.x) < a.w_blocks + vb_blocks) {
     const int warp = tid >> 5, lane = tid & 31;
     const int v = (int(blockIdx.x) - a.w_blocks) * 8 + warp;
-    if (v >= a.n_vec) return;
-    const int64_t i = a.vec_index[v];
-    const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
-    const int64_t li = i - en.offset;
-    const float* __restrict__ src =
-        (en.kind == kEntryB ? a.dbias_part[en.layer] : a.dbeta_part[en.layer]) + li;
-    float g = 0.0f;
-    if (en.kind == kEntryBeta && en.beta_mode != 0) {
-      // scalar beta: every (b, n) partial; fixed beta: no gradient
-      if (en.beta_mode == 1)
-        for (int q = lane; q < a.B * en.cols; q += 32) g = __fadd_rn(g, __ldg(src + q));
-    } else {
-      for (int b = lane; b < a.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
-    if (lane == 0) {
-      if (en.kind == kEntryBeta) {
-        const float beta = a.params[i];
-        if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
+    if (v < a.n_vec) {
+      const int64_t i = a.vec_index[v];
+      const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
+      const int64_t li = i - en.offset;
+      const float* __restrict__ src =
+          (en.kind == kEntryB ? a.dbias_part[en.layer] : a.dbeta_part[en.layer]) + li;
+      float g = 0.0f;
+      if (en.kind == kEntryBeta && en.beta_mode != 0) {
+        // scalar beta: every (b, n) partial; fixed beta: no gradient
+        if (en.beta_mode == 1)
+          for (int q = lane; q < a.B * en.cols; q += 32) g = __fadd_rn(g, __ldg(src + q));
+      } else {
+        for (int b = lane; b < a.B; b += 32) g = __fadd_rn(g, __ldg(src + int64_t(b) * en.cols));
       }
-      a.grads[i] = g;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
+      if (lane == 0) {
+        if (en.kind == kEntryBeta) {
+          const float beta = a.params[i];
+          if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
+        }
+        gout[i] = g;
+      }
     }
-    return;
+  } else {
+    // loss / hits / step; activity regularizer values after them (summed over ranks
+    // by the allreduce or the peer tail, added to the loss by k_adam / k_result /
+    // k_peer_adam)
+    float loss;
+    int hits;
+    loss_and_hits(a, loss, hits);
+    if (tid == 0) {
+      gout[a.n_params] = loss;
+      gout[a.n_params + 1] = float(hits);
+      if (a.update && a.xchg == nullptr) *a.step += 1;  // peer tail: k_peer_adam advances it
+    }
+    for (int m = 0; m < a.n_mon; ++m) {
+      const float v = activity_value(a, m);
+      if (tid == 0) gout[a.n_params + 2 + m] = v;
+    }
   }
-  // loss / hits / step; activity regularizer values after them (summed over ranks
-  // by the allreduce, added to the loss by k_adam / k_result)
-  float loss;
-  int hits;
-  loss_and_hits(a, loss, hits);
+  if (a.xchg == nullptr) return;
+  // peer tail: once every block's stores are visible system-wide, the last block
+  // publishes seq + 1 into slot [rank] of every rank's flag array
+  __syncthreads();
   if (tid == 0) {
-    a.grads[a.n_params] = loss;
-    a.grads[a.n_params + 1] = float(hits);
-    if (a.update) *a.step += 1;
-  }
-  for (int m = 0; m < a.n_mon; ++m) {
-    const float v = activity_value(a, m);
-    if (tid == 0) a.grads[a.n_params + 2 + m] = v;
+    __threadfence_system();
+    if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+      *a.done = 0u;
+      __threadfence_system();
+      for (int q = 0; q < a.world; ++q) st_release_sys(a.peer_flags[q] + a.rank, (unsigned long long)(seq + 1));
+    }
   }
 }
 
@@ -1880,6 +1916,91 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   if (en.kind != kEntryW) return;
   const int64_t li = i - en.offset;
   refresh_planes(a, en.layer, li / en.cols, li % en.cols, p);
+}
+
+// Multi-rank step tail over peer memory: the cross-rank gradient sum and the
+// optimizer in one kernel (replaces ncclAllReduce + k_adam).  Every rank's k_reduce
+// wrote its local gradient, loss numerator, hits and regularizer values into its
+// exchange buffer of parity seq & 1 and published seq + 1 to every rank's flags.
+// Each block waits for all ranks' flags, then sums the W buffers element-wise in
+// ascending rank order with loads from the mapped peer buffers (deterministic, so
+// every rank computes bit-identical parameters), runs Adam / SGD and refreshes the
+// bf16 planes.  Double buffering is safe: a rank can only reuse a parity after every
+// rank has published the next sequence number, i.e. finished reading this one.
+struct PeerArgs {
+  const float* xchg[kMaxRanks];   // every rank's exchange buffer [2][n_comm] (mapped)
+  unsigned long long* flags;      // this rank's flag array (slot q written by rank q)
+  int64_t n_comm;
+  int64_t* seq;                   // exchange sequence number (advanced by the last block)
+  unsigned int* done;
+  float* grads_out;               // summed gradient, loss sum, hits (snn_get_grads)
+  int64_t* rows_slot;             // schedule mode: advanced once per update
+  int64_t* step;                  // the step counter (advanced once per update)
+  int world;
+};
+
+__global__ void __launch_bounds__(256) k_peer_adam(const __grid_constant__ PeerArgs p, AdamArgs a) {
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const int64_t seq = *reinterpret_cast<volatile const int64_t*>(p.seq);
+  const int64_t s = *reinterpret_cast<volatile const int64_t*>(a.step);  // bias corrections of step s+1
+  if (tid == 0) {
+    const unsigned long long target = (unsigned long long)(seq + 1);
+    for (int q = 0; q < p.world; ++q) {
+      const long long t0 = globaltimer();
+      while (ld_acquire_sys(p.flags + q) < target) {
+        if (globaltimer() - t0 > 20000000000ll) __trap();  // a rank died: fail instead of hanging
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t par = (seq & 1) * p.n_comm;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + tid;
+  if (i < a.n_params) {
+    float g = 0.0f;
+    for (int q = 0; q < p.world; ++q) g = __fadd_rn(g, __ldcv(p.xchg[q] + par + i));
+    p.grads_out[i] = g;
+    float pv = a.params[i];
+    if (a.update) pv = adam_one(a, i, g, a.bc[2 * s], a.bc[2 * s + 1]);
+    const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
+    if (en.kind == kEntryW && a.update) {
+      const int64_t li = i - en.offset;
+      refresh_planes(a, en.layer, li / en.cols, li % en.cols, pv);
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    // StepResult (optimize.hpp:143-147, :193-196) from the rank sums, same order
+    float ls = 0.0f, hs = 0.0f;
+    for (int q = 0; q < p.world; ++q) {
+      ls = __fadd_rn(ls, __ldcv(p.xchg[q] + par + a.n_params));
+      hs = __fadd_rn(hs, __ldcv(p.xchg[q] + par + a.n_params + 1));
+    }
+    p.grads_out[a.n_params] = ls;
+    p.grads_out[a.n_params + 1] = hs;
+    float l = __fdiv_rn(ls, a.loss_denom);
+    for (int m = 0; m < a.n_mon; ++m) {
+      float v = 0.0f;
+      for (int q = 0; q < p.world; ++q) v = __fadd_rn(v, __ldcv(p.xchg[q] + par + a.n_params + 2 + m));
+      l = __fadd_rn(l, v);  // optimize.hpp:185-191
+    }
+    *a.loss_out = l;
+    *a.acc_out = double(hs) / double(a.B_global);
+  }
+  // completion: the last block advances the exchange sequence and the step counters
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
+      *p.done = 0u;
+      *p.seq = seq + 1;
+      if (a.update) {
+        *p.step = s + 1;
+        if (p.rows_slot != nullptr) *p.rows_slot += 1;
+      }
+      __threadfence();
+    }
+  }
 }
 
 // Single-rank step tail: k_reduce + k_adam in one launch (no allreduce between

@@ -233,7 +233,8 @@ def lib() -> C.CDLL:
                  "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_evaluate", "snn_apply", "snn_save_checkpoint", "snn_load_checkpoint", "snn_sync", "snn_read_result",
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
-                 "snn_read_dataset", "snn_monitor_counts"):
+                 "snn_read_dataset", "snn_monitor_counts", "snn_peer_handle", "snn_peer_open",
+                 "snn_peer_attach_local", "snn_train_step_split"):
         if hasattr(L, name) or not os.environ.get("SNN_B200_ABI_ANY"):
             getattr(L, name).restype = C.c_int
     L.snn_launch_name.restype = C.c_char_p
@@ -543,6 +544,39 @@ class Engine:
     def comm_init(self, uid: bytes, rank: int, world: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self._check(self._L.snn_comm_init(self._h, buf, int(rank), int(world)))
+
+    # peer-memory data parallelism (the default multi-GPU tail; see snn_engine.h)
+    def peer_handle(self) -> bytes:
+        """This rank's exchange buffer as a 64-byte IPC handle."""
+        buf = (C.c_uint8 * 64)()
+        self._check(self._L.snn_peer_handle(self._h, buf))
+        return bytes(buf)
+
+    def peer_open(self, rank: int, world: int, handles):
+        """Map every rank's exchange buffer (handles in rank order, from peer_handle)."""
+        if len(handles) != world or any(len(h) != 64 for h in handles):
+            raise ArgumentError("peer_open: one 64-byte handle per rank")
+        buf = (C.c_uint8 * (64 * world)).from_buffer_copy(b"".join(handles))
+        self._check(self._L.snn_peer_open(self._h, int(rank), int(world), buf))
+
+    @staticmethod
+    def peer_attach_local(engines):
+        """Test hook: engines of one GPU as ranks 0..n-1 of the peer tail (drive them
+        with train_step_split so no kernel waits on a rank that has not run)."""
+        L = lib()
+        arr = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+        rc = L.snn_peer_attach_local(arr, len(engines))
+        if rc != 0:
+            engines[0]._check(rc)
+
+    def train_step_split(self, rows, part: int):
+        """part 0: forward .. local reduction (synchronised); part 1: cross-rank tail
+        -> (loss, accuracy)."""
+        loss, acc = C.c_float(), C.c_double()
+        r = np.ascontiguousarray(rows, np.uint32) if rows is not None else None
+        self._check(self._L.snn_train_step_split(self._h, _p(r, C.c_uint32) if r is not None else None,
+                                                 int(part), C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
 
     # ---------------------------------------------------------- diagnostics
     def debug(self, on: bool = True):

@@ -13,6 +13,15 @@ these rules:
   allreduce as the gradient; StepResult = (sum / B_global, hits / B_global);
 * every rank applies the identical Adam update to the identical reduced
   gradient, so parameter replicas stay bit-identical.
+
+Two device tails implement the exchange (engine.cu):
+
+* "peer" (default): every rank's k_reduce writes its local buffer (gradient,
+  loss numerator, hits, regularizer values) into an IPC-exported exchange
+  buffer and raises a flag on every rank; k_peer_adam waits for all flags and
+  sums the ranks' buffers by peer loads over NVLink in ascending rank order
+  (`peer_sum`), then updates -- the reduction and the optimizer in one kernel;
+* "nccl": k_reduce, ncclAllReduce (sum), k_adam.
 """
 from __future__ import annotations
 
@@ -28,6 +37,40 @@ def shard_rows(perm: np.ndarray, batch: int, rank: int, world: int, b_local: int
     gb = b_local * world
     start = batch * gb + rank * b_local
     return np.asarray(perm[start:start + b_local])
+
+
+def peer_sum(buffers):
+    """k_peer_adam's reduction: float32 sum of the ranks' buffers, ascending rank
+    order, starting from 0 -- the same bits on every rank."""
+    acc = np.zeros_like(np.asarray(buffers[0], np.float32))
+    for b in buffers:
+        acc = (acc + np.asarray(b, np.float32)).astype(np.float32)
+    return acc
+
+
+def exchange_handles(handle: bytes, rank: int, world: int, dist) -> list:
+    """All-gather every rank's 64-byte exchange-buffer handle, in rank order."""
+    if len(handle) != 64:
+        raise ValueError("peer handle must be 64 bytes")
+    got = [None] * world
+    dist.all_gather_object(got, (rank, bytes(handle)))
+    if [r for r, _ in got] != list(range(world)):
+        raise RuntimeError(f"handle exchange out of order: {[r for r, _ in got]}")
+    return [h for _, h in got]
+
+
+def setup_data_parallel(eng, rank: int, world: int, dist, tail: str = "peer") -> None:
+    """Join `eng` to the data-parallel group: tail "peer" (exchange buffers over
+    NVLink peer memory) or "nccl" (ncclAllReduce)."""
+    if tail == "peer":
+        eng.peer_open(rank, world, exchange_handles(eng.peer_handle(), rank, world, dist))
+    elif tail == "nccl":
+        from .engine import Engine
+        uid = [Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.comm_init(uid[0], rank, world)
+    else:
+        raise ValueError(f"unknown data-parallel tail {tail!r}")
 
 
 def combine_tail(loss_sums, hits, b_global: int):

@@ -92,3 +92,69 @@ def test_shard_rows_partition_the_global_batch():
         b_local = 8 // world if world <= 8 else 1
         rows = np.concatenate([shard_rows(perm, 1, r, world, b_local) for r in range(world)])
         assert np.array_equal(rows, perm[8:16])
+
+
+def _peer_worker(rank, port, out):
+    """The peer tail's rules on the CPU: every rank publishes its local buffer, every
+    rank gathers all of them (what k_peer_adam's peer loads see) and sums them in
+    ascending rank order (parallel.peer_sum), then applies Adam locally."""
+    import torch
+    from paper_2402_18994_b200.parallel import exchange_handles, peer_sum
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    # handle exchange: rank order, 64 bytes each
+    hs = exchange_handles(bytes([rank + 1]) * 64, rank, WORLD, dist)
+    assert hs == [bytes([q + 1]) * 64 for q in range(WORLD)]
+    orc = Lib("orc")
+    pk, y = _data(orc)
+    st = State(orc.init(NET, orc.key_child(orc.key_from_seed(0), 0)) * np.float32(3.0))
+    perm = orc.permutation(orc.key_child(orc.key_child(orc.key_from_seed(0), 1), 0), N)
+    b_global = B_LOCAL * WORLD
+    losses = []
+    for step in range(STEPS):
+        rows = shard_rows(perm, step, rank, WORLD, B_LOCAL)
+        o = orc.forward_backward(NET, st.params, pk[rows], T, y[rows])
+        scale = np.float32(B_LOCAL) / np.float32(b_global)
+        local = np.concatenate([o["grads"] * scale,
+                                [np.float32(o["loss"]) * np.float32(B_LOCAL), o["acc"] * B_LOCAL]])
+        bufs = [torch.zeros(local.size) for _ in range(WORLD)]
+        dist.all_gather(bufs, torch.from_numpy(local.astype(np.float32)))
+        red = peer_sum([b.numpy() for b in bufs])
+        losses.append(float(red[-2]) / b_global)
+        st.step = orc.adam(st.params, red[:-2].copy(), st.m, st.v, st.step)
+    out[rank] = (st.params.copy(), losses)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_peer_tail_rules_match_single_process(orc):
+    port = _free_port()
+    mgr = tmp.Manager()
+    out = mgr.dict()
+    tmp.spawn(_peer_worker, args=(port, out), nprocs=WORLD, join=True)
+    p0, l0 = out[0]
+    p1, l1 = out[1]
+    assert np.array_equal(p0, p1), "replicas diverged"
+    assert l0 == l1
+    pk, y = _data(orc)
+    st = State(orc.init(NET, orc.key_child(orc.key_from_seed(0), 0)) * np.float32(3.0))
+    perm = orc.permutation(orc.key_child(orc.key_child(orc.key_from_seed(0), 1), 0), N)
+    b_global = B_LOCAL * WORLD
+    for step in range(STEPS):
+        rows = perm[step * b_global:(step + 1) * b_global]
+        o = orc.forward_backward(NET, st.params, pk[rows], T, y[rows])
+        assert abs(o["loss"] - l0[step]) <= 1e-5 * abs(o["loss"])
+        st.step = orc.adam(st.params, o["grads"], st.m, st.v, st.step)
+    assert np.linalg.norm(p0 - st.params) / np.linalg.norm(st.params) <= 1e-6
+
+
+def test_peer_sum_is_rank_ordered_float32():
+    from paper_2402_18994_b200.parallel import peer_sum
+    bufs = [np.array([1e8, 1.0], np.float32), np.array([1.0, 1e8], np.float32),
+            np.array([-1e8, -1e8], np.float32)]
+    got = peer_sum(bufs)
+    want = np.array([(np.float32(1e8) + np.float32(1.0)) - np.float32(1e8),
+                     (np.float32(1.0) + np.float32(1e8)) - np.float32(1e8)], np.float32)
+    assert got.dtype == np.float32 and np.array_equal(got, want)

@@ -725,3 +725,128 @@ def test_monitor_spec_errors():
     eng = Engine(ok, TrainConfig(batch_size=2, f_min=0.6, f_max=0.3), 16)  # lambdas 0: unchecked
     with pytest.raises(ArgumentError):
         eng.monitor_counts(1)
+
+
+def test_single_rank_peer_tail_matches_fused_tail(orc):
+    """The peer-memory tail (k_reduce -> k_peer_adam) on one rank trains bit-identically
+    to the fused single-rank tail."""
+    net = Net(inp=30, hidden=(16, 12), classes=5)
+    x, y = orc.synth_raster(5, 8, 19, 30, 2)
+    pk = orc.pack_time(x)
+    e1, e2 = make_engine(net, 4, 19, seed=3), make_engine(net, 4, 19, seed=3)
+    e2.peer_open(0, 1, [e2.peer_handle()])
+    assert e2.launches_per_step == e1.launches_per_step + 1
+    for eng in (e1, e2):
+        eng.stage_dataset(pk, y)
+    for i in range(4):
+        rows = np.arange(4 * (i % 2), 4 * (i % 2) + 4, dtype=np.uint32)
+        assert e1.train_step(rows) == e2.train_step(rows)
+    assert np.array_equal(e1.get_params(), e2.get_params())
+    m1, v1, s1 = e1.get_opt_state()
+    m2, v2, s2 = e2.get_opt_state()
+    assert s1 == s2 == 4 and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+    assert e1.forward_backward(np.arange(4, dtype=np.uint32)) == e2.forward_backward(np.arange(4, dtype=np.uint32))
+    assert np.array_equal(e1.get_grads(), e2.get_grads())
+    # schedule mode (8-step graphs) through the peer tail
+    sched = np.arange(8 * 4, dtype=np.uint32) % 8
+    for eng in (e1, e2):
+        eng.upload_schedule(sched.reshape(8, 4))
+        eng.enqueue_steps(0, 8)
+        eng.sync()
+    assert np.array_equal(e1.get_params(), e2.get_params())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_tail_ranks_emulated_on_one_gpu(orc, world):
+    """`world` ranks of the peer tail on one GPU (B200_PROFILING: never let ranks
+    wait on each other as separate launches -- every rank runs its part before the
+    cross-rank wait, then every rank runs the tail).  Replicas stay bit-identical and
+    match full-global-batch training on the oracle."""
+    from paper_2402_18994_b200 import Engine
+    net = Net(inp=40, hidden=(24, 20), classes=5, act="superspike")
+    B, T, N = 4, 23, 48
+    x, y = orc.synth_raster(5, N, T, 40, 8)
+    pk = orc.pack_time(x)
+    engs = [make_engine(net, B, T, seed=5) for _ in range(world)]
+    Engine.peer_attach_local(engs)
+    p0 = engs[0].get_params() * np.float32(3.0)
+    for e in engs:
+        e.stage_dataset(pk, y)
+        e.set_params(p0)
+    st = State(p0.copy())
+    perm = orc.permutation(orc.key_from_seed(17), N)
+    for step in range(3):
+        gb = perm[step * B * world:(step + 1) * B * world].astype(np.uint32)
+        ref = orc.forward_backward(net, st.params, pk[gb], T, y[gb])
+        for r, e in enumerate(engs):
+            e.train_step_split(gb[r * B:(r + 1) * B], 0)
+        res = [e.train_step_split(None, 1) for e in engs]
+        assert all(r == res[0] for r in res), res
+        assert abs(res[0][0] - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+        assert res[0][1] == ref["acc"]
+        g = engs[0].get_grads()
+        check_grads(orc, net, g, ref["grads"])
+        for e in engs[1:]:
+            assert np.array_equal(e.get_grads(), g)
+        orc.train_step(net, st, pk[gb], T, y[gb])
+        params = [e.get_params() for e in engs]
+        assert all(np.array_equal(p, params[0]) for p in params), "replicas diverged"
+        if step == 0:
+            check_adam_step(orc, net, params[0], st.params, ref["grads"])
+        st.params = params[0].copy()  # follow the engine (Adam's sign flips on tiny grads)
+        m, v, s = engs[0].get_opt_state()
+        st.m, st.v, st.step = m, v, s
+
+
+def _ipc_rank(rank, port, out):
+    """One process per rank on GPU 0: real IPC handle export / all-gather / open, then
+    split steps with a barrier between the parts (every flag is set before any rank's
+    tail runs, so no kernel waits on a rank that has not run)."""
+    import os
+    import torch.distributed as dist
+    from oracle.pyoracle import Lib
+    from paper_2402_18994_b200.parallel import setup_data_parallel
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    orc = Lib("orc")
+    net = Net(inp=40, hidden=(24, 20), classes=5, act="superspike")
+    x, y = orc.synth_raster(5, 32, 23, 40, 8)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, 4, 23, seed=5)
+    setup_data_parallel(eng, rank, 2, dist, "peer")
+    eng.stage_dataset(pk, y)
+    eng.set_params(eng.get_params() * np.float32(3.0))
+    res = []
+    for step in range(3):
+        rows = np.arange(step * 8 + rank * 4, step * 8 + rank * 4 + 4, dtype=np.uint32)
+        eng.train_step_split(rows, 0)
+        dist.barrier()
+        res.append(eng.train_step_split(None, 1))
+        dist.barrier()
+    out[rank] = (res, eng.get_params(), eng.get_grads())
+    dist.destroy_process_group()
+
+
+def test_peer_tail_over_real_ipc_two_processes(orc):
+    import socket
+    import torch.multiprocessing as tmp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp.Manager().dict()
+    tmp.spawn(_ipc_rank, args=(port, out), nprocs=2, join=True)
+    (r0, p0, g0), (r1, p1, g1) = out[0], out[1]
+    assert r0 == r1 and np.array_equal(p0, p1) and np.array_equal(g0, g1)
+    # same three global batches on one in-process 8-sample engine
+    net = Net(inp=40, hidden=(24, 20), classes=5, act="superspike")
+    x, y = orc.synth_raster(5, 32, 23, 40, 8)
+    pk = orc.pack_time(x)
+    ref = make_engine(net, 8, 23, seed=5)
+    ref.stage_dataset(pk, y)
+    ref.set_params(ref.get_params() * np.float32(3.0))
+    for step in range(3):
+        l, a = ref.train_step(np.arange(step * 8, step * 8 + 8, dtype=np.uint32))
+        assert abs(l - r0[step][0]) <= REL_TOL * abs(l) and a == r0[step][1]
+    assert relnorm(p0, ref.get_params()) <= 1e-5
