@@ -160,6 +160,16 @@ snn_status snn_synth_dataset(snn_engine* e, size_t n, uint64_t seed);
 snn_status snn_read_dataset(snn_engine* e, size_t start, size_t n, uint8_t* packed,
                             int64_t* labels);
 
+/* .spkd container I/O (data.hpp:229-341): snn_load_container reads the
+ * reference's read_container format with its checks and error classes
+ * (FormatError with byte offsets, IoError) and stages it like
+ * snn_stage_dataset; the container's T must be the engine's and its per-step
+ * feature dims must flatten to the network input.  snn_save_container writes
+ * the staged dataset as [N, ceil(T/8), input] byte-for-byte like
+ * write_container. */
+snn_status snn_load_container(snn_engine* e, const char* path, size_t* n);
+snn_status snn_save_container(snn_engine* e, const char* path);
+
 /* permutation(master.child(1+epoch).child(0), n): the epoch shuffle of
  * train() (optimize.hpp:266-268, data.hpp:181-208, rng.hpp:78-87). */
 snn_status snn_epoch_permutation(snn_engine* e, size_t epoch, uint32_t* out, size_t n);

@@ -310,6 +310,17 @@ inline std::vector<float> apply(TrainState& st, const std::vector<std::uint32_t>
   return trace;
 }
 
+// read_container / write_container (data.hpp:229-341) straight into / out of the
+// engine's HBM-resident dataset; returns the number of examples staged.
+inline std::size_t load_container(TrainState& st, const std::string& path) {
+  std::size_t n = 0;
+  check(snn_load_container(st.engine(), path.c_str(), &n), st.engine());
+  return n;
+}
+inline void save_container(TrainState& st, const std::string& path) {
+  check(snn_save_container(st.engine(), path.c_str()), st.engine());
+}
+
 // ApplyResult.monitors entry of the monitor after hidden LIF `layer`: spike counts
 // [B][H] of the last forward (apply / step / evaluation batch).
 inline std::vector<float> monitor_counts(TrainState& st, int layer, std::size_t hidden) {

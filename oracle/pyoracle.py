@@ -274,6 +274,30 @@ class Lib:
             correct += r["acc"] * float(hi - lo)
         return correct / float(n)
 
+    def write_container(self, path: str, packed, original_t: int, labels) -> None:
+        """Reference write_container (data.hpp:272-293); ref library only."""
+        packed = np.ascontiguousarray(packed, np.uint8)
+        shape = np.array(packed.shape, np.uint64)
+        f = self._f("write_container")
+        f.restype = C.c_int
+        rc = f(path.encode(), _ptr(packed, C.c_uint8), _ptr(shape, C.c_uint64), C.c_int(packed.ndim),
+               C.c_uint32(original_t), _ptr(np.ascontiguousarray(labels, np.int64), C.c_int64))
+        if rc != 0:
+            raise ValueError("write_container failed")
+
+    def read_container(self, path: str, cap: int, n_cap: int):
+        """Reference read_container (data.hpp:295-339); ref library only."""
+        packed = np.zeros(cap, np.uint8)
+        labels = np.zeros(n_cap, np.int64)
+        t, n = C.c_uint32(), C.c_uint64()
+        f = self._f("read_container")
+        f.restype = C.c_int
+        rc = f(path.encode(), _ptr(packed, C.c_uint8), C.c_size_t(cap), _ptr(labels, C.c_int64),
+               C.c_size_t(n_cap), C.byref(t), C.byref(n))
+        if rc != 0:
+            raise ValueError(f"read_container failed rc={rc}")
+        return packed, labels[:n.value], t.value
+
     def write_checkpoint(self, net: Net, params, m, v, step: int, optimizer: str,
                          config_text: str, path: str) -> None:
         """Reference write_checkpoint (optimize.hpp:334-366); ref library only."""

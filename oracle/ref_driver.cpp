@@ -428,4 +428,37 @@ int ref_write_checkpoint(const orc_net* n, const float* params, const float* m,
   }
 }
 
+// write_container / read_container (data.hpp:229-341): golden .spkd fixtures.
+// shape = the packed tensor's [N, ceil(T/8), features...] (ndim entries).
+int ref_write_container(const char* path, const uint8_t* packed, const uint64_t* shape, int ndim,
+                        uint32_t original_t, const int64_t* labels) {
+  try {
+    PackedDataset d;
+    Shape s(shape, shape + ndim);
+    d.x = Tensor<std::uint8_t>(s);
+    std::memcpy(d.x.data(), packed, d.x.size());
+    d.y.assign(labels, labels + shape[0]);
+    d.original_t = original_t;
+    write_container(path, d);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+int ref_read_container(const char* path, uint8_t* packed, size_t cap, int64_t* labels,
+                       size_t label_cap, uint32_t* original_t, uint64_t* n) {
+  try {
+    const PackedDataset d = read_container(path);
+    if (d.x.size() > cap || d.y.size() > label_cap) return 2;
+    std::memcpy(packed, d.x.data(), d.x.size());
+    std::copy(d.y.begin(), d.y.end(), labels);
+    *original_t = uint32_t(d.original_t);
+    *n = d.y.size();
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -1853,6 +1853,103 @@ snn_status snn_read_dataset(snn_engine* e, size_t start, size_t n, uint8_t* pack
   });
 }
 
+// .spkd container (data.hpp:229-341): little-endian header, i32 labels, packed payload.
+snn_status snn_load_container(snn_engine* e, const char* path, size_t* n_out) {
+  if (!e || !path) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(SNN_ERR_IO, "cannot open for reading: %s", path);
+    std::unique_ptr<FILE, int (*)(FILE*)> hold(f, std::fclose);
+    size_t off = 0;
+    auto take = [&](void* p, size_t n) {  // io_read (data.hpp:255-263)
+      const size_t got = std::fread(p, 1, n, f);
+      if (got != n) fail(SNN_ERR_FORMAT, "container truncated at byte offset %zu", off + got);
+      off += n;
+    };
+    char magic[4];
+    take(magic, 4);
+    if (std::memcmp(magic, "SPKD", 4) != 0) fail(SNN_ERR_FORMAT, "bad magic at byte offset 0");
+    uint32_t version;
+    take(&version, 4);
+    if (version != 1) fail(SNN_ERR_FORMAT, "unsupported container version %u at byte offset 4", version);
+    uint8_t dtype, order;
+    take(&dtype, 1);
+    if (dtype != 0) fail(SNN_ERR_FORMAT, "unknown dtype %u at byte offset 8", unsigned(dtype));
+    take(&order, 1);
+    if (order != 0) fail(SNN_ERR_FORMAT, "unknown bit order %u at byte offset 9", unsigned(order));
+    uint16_t reserved;
+    take(&reserved, 2);
+    uint32_t original_t, ndim;
+    take(&original_t, 4);
+    take(&ndim, 4);
+    if (ndim < 2 || ndim > 16) fail(SNN_ERR_FORMAT, "implausible ndim %u at byte offset 16", ndim);
+    std::vector<uint64_t> shape(ndim);
+    for (auto& d : shape) take(&d, 8);
+    if (shape[1] != (uint64_t(original_t) + 7) / 8)
+      fail(SNN_ERR_FORMAT, "packed time extent %llu inconsistent with T=%u", (unsigned long long)shape[1],
+           original_t);
+    uint64_t n_labels;
+    take(&n_labels, 8);
+    if (n_labels != shape[0])
+      fail(SNN_ERR_FORMAT, "label count %llu does not match N=%llu", (unsigned long long)n_labels,
+           (unsigned long long)shape[0]);
+    // the engine's shape: T and the flattened per-step features (a Linear flattens, network.hpp:133-138)
+    uint64_t feat = 1;
+    for (uint32_t i = 2; i < ndim; ++i) feat *= shape[i];
+    if (int64_t(original_t) != e->T)
+      fail(SNN_ERR_FORMAT, "unpack_time: container T=%u, engine T=%d", original_t, e->T);
+    if (feat != uint64_t(e->IN))
+      fail(SNN_ERR_SHAPE, "container has %llu features per step, network input %d", (unsigned long long)feat,
+           e->IN);
+    if (n_labels == 0) fail(SNN_ERR_ARGUMENT, "empty container");
+    std::vector<int32_t> lab32(n_labels);
+    take(lab32.data(), n_labels * 4);
+    std::vector<int64_t> lab(lab32.begin(), lab32.end());
+    std::vector<uint8_t> x(size_t(n_labels) * shape[1] * feat);
+    take(x.data(), x.size());
+    e->stage(e->data, x.data(), size_t(n_labels), lab.data());
+    if (n_out) *n_out = size_t(n_labels);
+  });
+}
+
+snn_status snn_save_container(snn_engine* e, const char* path) {
+  if (!e || !path) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    const size_t n = e->data.n;
+    if (n == 0) fail(SNN_ERR_STATE, "no dataset staged");
+    const int tp8 = (e->T + 7) / 8;
+    std::vector<uint8_t> x(n * size_t(tp8) * e->IN);
+    std::vector<int64_t> lab(n);
+    const snn_status st = snn_read_dataset(e, 0, n, x.data(), lab.data());
+    if (st != SNN_OK) fail(st, "%s", e->err.c_str());
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(SNN_ERR_IO, "cannot open for writing: %s", path);
+    std::unique_ptr<FILE, int (*)(FILE*)> hold(f, std::fclose);
+    bool ok = true;
+    auto put = [&](const void* p, size_t b) { ok = ok && std::fwrite(p, 1, b, f) == b; };
+    const uint32_t version = 1, T = uint32_t(e->T), ndim = 3;
+    const uint8_t zero8 = 0;
+    const uint16_t zero16 = 0;
+    put("SPKD", 4);
+    put(&version, 4);
+    put(&zero8, 1);   // dtype u8
+    put(&zero8, 1);   // MSB-first
+    put(&zero16, 2);  // reserved
+    put(&T, 4);
+    put(&ndim, 4);
+    const uint64_t shape[3] = {uint64_t(n), uint64_t(tp8), uint64_t(e->IN)};
+    put(shape, sizeof(shape));
+    const uint64_t nl = n;
+    put(&nl, 8);
+    for (int64_t l : lab) {
+      const int32_t v = int32_t(l);
+      put(&v, 4);
+    }
+    put(x.data(), x.size());
+    if (!ok) fail(SNN_ERR_IO, "short write: %s", path);
+  });
+}
+
 snn_status snn_epoch_permutation(snn_engine* e, size_t epoch, uint32_t* out, size_t n) {
   if (!e || !out) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {

@@ -234,7 +234,8 @@ def lib() -> C.CDLL:
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
                  "snn_read_dataset", "snn_monitor_counts", "snn_peer_handle", "snn_peer_open",
-                 "snn_peer_attach_local", "snn_train_step_split"):
+                 "snn_peer_attach_local", "snn_train_step_split", "snn_load_container",
+                 "snn_save_container"):
         if hasattr(L, name) or not os.environ.get("SNN_B200_ABI_ANY"):
             getattr(L, name).restype = C.c_int
     L.snn_launch_name.restype = C.c_char_p
@@ -471,6 +472,16 @@ class Engine:
         self._check(self._L.snn_apply(self._h, _p(r, C.c_uint32), _p(out, C.c_float),
                                       C.c_size_t(out.size)))
         return out
+
+    def load_container(self, path: str) -> int:
+        """read_container (data.hpp:295-339) of a .spkd file, staged in HBM; returns N."""
+        n = C.c_size_t()
+        self._check(self._L.snn_load_container(self._h, str(path).encode(), C.byref(n)))
+        return n.value
+
+    def save_container(self, path: str):
+        """write_container (data.hpp:272-293) of the staged dataset."""
+        self._check(self._L.snn_save_container(self._h, str(path).encode()))
 
     def monitor_counts(self, layer: int) -> np.ndarray:
         """ApplyResult.monitors entry of the monitor after hidden LIF `layer`: spike

@@ -149,6 +149,16 @@ def activity_fixture(ref: Lib):
     np.savez_compressed(os.path.join(GOLD, "activity.npz"), **vals)
 
 
+def container_fixture(ref: Lib):
+    """.spkd containers written by the reference's write_container (data.hpp:229-293):
+    a flat [N, ceil(T/8), 40] dataset and the same bytes as [N, ceil(T/8), 5, 8]."""
+    x, y = ref.synth_raster(5, 6, 21, 40, 29)
+    pk = ref.pack_time(x)
+    ref.write_container(os.path.join(GOLD, "flat.spkd"), pk, 21, y)
+    ref.write_container(os.path.join(GOLD, "multi.spkd"), pk.reshape(6, 3, 5, 8), 21, y)
+    np.savez_compressed(os.path.join(GOLD, "spkd.npz"), packed=pk, y=y, t=21)
+
+
 SHIFT_NET = Net(inp=40, hidden=(24,), classes=5, bias=True, act="superspike", unroll=3)
 SHIFT_OPTS = {"one_axis": dict(max_shift=3, shift_axes=(2,)),
               "two_axes": dict(max_shift=5, shift_axes=(2, -1))}
@@ -237,6 +247,8 @@ if __name__ == "__main__":
         opts_fixture(ref)
     if only in (None, "ckpt"):
         checkpoint_fixture(ref)
+    if only in (None, "spkd"):
+        container_fixture(ref)
     if only in (None, "activity"):
         activity_fixture(ref)
     if only in (None, "shift"):

@@ -850,3 +850,44 @@ def test_peer_tail_over_real_ipc_two_processes(orc):
         l, a = ref.train_step(np.arange(step * 8, step * 8 + 8, dtype=np.uint32))
         assert abs(l - r0[step][0]) <= REL_TOL * abs(l) and a == r0[step][1]
     assert relnorm(p0, ref.get_params()) <= 1e-5
+
+
+def test_container_load_save_matches_reference_files(golden, tmp_path):
+    """.spkd I/O (data.hpp:229-341) against files written by the reference's own
+    write_container: load stages the same bytes (flat and [N, T', 5, 8] feature
+    shapes), save reproduces the reference's file byte for byte."""
+    import os
+    g = golden("spkd")
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    net = Net(inp=40, hidden=(16,), classes=5)
+    eng = make_engine(net, 2, int(g["t"]))
+    for name in ("flat.spkd", "multi.spkd"):
+        assert eng.load_container(os.path.join(gold, name)) == 6
+        pk, y = eng.read_dataset(0, 6)
+        assert np.array_equal(pk, g["packed"]) and np.array_equal(y, g["y"])
+    out = tmp_path / "saved.spkd"
+    eng.save_container(str(out))
+    assert out.read_bytes() == open(os.path.join(gold, "flat.spkd"), "rb").read()
+
+
+def test_container_errors_match_reference_classes(tmp_path):
+    import os
+    from paper_2402_18994_b200 import FormatError, IoError, ShapeError
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    raw = open(os.path.join(gold, "flat.spkd"), "rb").read()
+    eng = make_engine(Net(inp=40, hidden=(16,), classes=5), 2, 21)
+    with pytest.raises(IoError):
+        eng.load_container(str(tmp_path / "missing.spkd"))
+    cases = {"magic": b"SPKX" + raw[4:], "version": raw[:4] + b"\x02" + raw[5:],
+             "truncated": raw[:-7], "dtype": raw[:8] + b"\x01" + raw[9:]}
+    for name, data in cases.items():
+        p = tmp_path / f"{name}.spkd"
+        p.write_bytes(data)
+        with pytest.raises(FormatError):
+            eng.load_container(str(p))
+    other_t = make_engine(Net(inp=40, hidden=(16,), classes=5), 2, 30)
+    with pytest.raises(FormatError):
+        other_t.load_container(os.path.join(gold, "flat.spkd"))
+    other_in = make_engine(Net(inp=41, hidden=(16,), classes=5), 2, 21)
+    with pytest.raises(ShapeError):
+        other_in.load_container(os.path.join(gold, "flat.spkd"))

@@ -411,3 +411,16 @@ def test_activity_regularizer_rejects_bad_band(orc):
     # lambdas zero: the band is never checked (the regularizer is not called)
     orc.forward_backward(net, g["params"], g["packed"], int(g["t"]), g["y"],
                          opts=Opts(f_min=0.5, f_max=0.2))
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
+def test_container_fixtures_read_back_by_reference():
+    """tests/golden/*.spkd are the reference's write_container output; its own
+    read_container returns the packed bytes and labels of spkd.npz."""
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    g = np.load(os.path.join(gold, "spkd.npz"))
+    ref = Lib("ref")
+    for name in ("flat.spkd", "multi.spkd"):
+        pk, y, t = ref.read_container(os.path.join(gold, name), 4096, 64)
+        assert t == int(g["t"]) and np.array_equal(y, g["y"])
+        assert np.array_equal(pk[:g["packed"].size], g["packed"].ravel())
