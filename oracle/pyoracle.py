@@ -30,7 +30,11 @@ class _Net(C.Structure):
                 ("bias", C.c_int), ("threshold", C.c_float), ("act", C.c_int),
                 ("slope", C.c_float), ("aux", C.c_float), ("unroll", C.c_int),
                 ("beta_mode", C.c_int * 9), ("fixed_beta", C.c_float * 9),
-                ("monitor", C.c_int * 8)]
+                ("monitor", C.c_int * 8), ("cell", C.c_int * 8)]
+
+# hidden cell kinds: "lif" (neuron.hpp:127-136) | "alif" (declared restatement,
+# spiketrain_oracle.h -- not in the reference)
+CELLS = {"lif": 0, "alif": 1}
 
 BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 
@@ -88,6 +92,8 @@ class Net:
     fixed_beta: tuple = ()
     # hidden LIF layers followed by a MonitorLayer (indices into hidden)
     monitor: tuple = ()
+    # cell kind per hidden layer ("lif" | "alif"); missing entries are "lif"
+    cell: tuple = ()
 
     def c(self) -> _Net:
         s, a = DEFAULT_SLOPE[self.act]
@@ -108,6 +114,8 @@ class Net:
             n.fixed_beta[i] = self.fixed_beta[i] if i < len(self.fixed_beta) else 0.5
         for i in self.monitor:
             n.monitor[i] = 1
+        for i, c in enumerate(self.cell):
+            n.cell[i] = CELLS[c]
         return n
 
 

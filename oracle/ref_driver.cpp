@@ -40,6 +40,8 @@ NetworkSpec make_spec(const orc_net* n) {
   NetworkSpec s;
   s.input_shape = {std::size_t(n->in)};
   for (int l = 0; l < n->n_hidden; ++l) {
+    // the reference has LIF / LI cells only: no ALIF to drive
+    if (n->cell[l] != 0) throw std::invalid_argument("ALIF cells are not part of the reference");
     s.layers.push_back(LinearLayer{std::size_t(n->hidden[l]), n->bias != 0});
     LIFLayer lif;
     lif.activation = act_desc(n);

@@ -128,8 +128,12 @@ void orc_unpack_time(const uint8_t* packed, size_t n, size_t t, size_t f,
 /* Parameter layout (network.hpp:164-226): per hidden block w, [b], beta;
  * then readout w, [b], beta.  Normalised ids: Linear 2j, cell 2j+1.        */
 
+static int is_alif(const orc_net* net, int l) { return l < net->n_hidden && net->cell[l] == 1; }
+
 int orc_entry_count(const orc_net* net) {
-  return (net->n_hidden + 1) * (net->bias ? 3 : 2);
+  int n = (net->n_hidden + 1) * (net->bias ? 3 : 2);
+  for (int l = 0; l < net->n_hidden; ++l) n += is_alif(net, l);
+  return n;
 }
 
 /* beta entry size of cell l (l == n_hidden: the readout) */
@@ -158,11 +162,12 @@ void orc_entry_layout(const orc_net* net, size_t* offsets, size_t* sizes,
   int e = 0;
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    const size_t sz[3] = {k * h, h, beta_size(net, l, h)};
-    const char* leaf[3] = {"w", "b", "beta"};
-    const int lid[3] = {lin_id(net, l), lin_id(net, l), lin_id(net, l) + 1};
-    for (int q = 0; q < 3; ++q) {
+    const size_t sz[4] = {k * h, h, beta_size(net, l, h), h};
+    const char* leaf[4] = {"w", "b", "beta", "gamma"};
+    const int lid[4] = {lin_id(net, l), lin_id(net, l), lin_id(net, l) + 1, lin_id(net, l) + 1};
+    for (int q = 0; q < 4; ++q) {
       if (q == 1 && !net->bias) continue;
+      if (q == 3 && !is_alif(net, l)) continue;
       if (offsets) offsets[e] = off;
       if (sizes) sizes[e] = sz[q];
       if (names) snprintf(names[e], 16, "l%d.%s", lid[q], leaf[q]);
@@ -176,13 +181,13 @@ size_t orc_param_count(const orc_net* net) {
   size_t n = 0;
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    n += k * h + beta_size(net, l, h) + (net->bias ? h : 0);
+    n += k * h + beta_size(net, l, h) + (net->bias ? h : 0) + (is_alif(net, l) ? h : 0);
   }
   return n;
 }
 
 typedef struct {
-  size_t w, b, beta; /* offsets; b == SIZE_MAX when no bias */
+  size_t w, b, beta, gamma; /* offsets; b == SIZE_MAX when no bias, gamma when not ALIF */
 } layer_off;
 
 static void layer_offsets(const orc_net* net, layer_off* lo) {
@@ -199,6 +204,11 @@ static void layer_offsets(const orc_net* net, layer_off* lo) {
     }
     lo[l].beta = off;
     off += beta_size(net, l, h);
+    lo[l].gamma = (size_t)-1;
+    if (is_alif(net, l)) {
+      lo[l].gamma = off;
+      off += h;
+    }
   }
 }
 
@@ -219,6 +229,8 @@ void orc_init(const orc_net* net, uint64_t key, float* params) {
     else /* PerNeuron [h] or LearnableScalar [] from the same key */
       orc_truncated_normal(orc_key_child(lk_cell, 2), beta_size(net, l, h), 0.5f, 0.25f,
                            params + lo[l].beta);
+    if (is_alif(net, l)) /* declared ALIF: gamma ~ TN(0.5, 0.25) from child 3 */
+      orc_truncated_normal(orc_key_child(lk_cell, 3), h, 0.5f, 0.25f, params + lo[l].gamma);
   }
 }
 
@@ -343,6 +355,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
   /* activations a[l] = input of layer l as float rows [M, in_l] */
   float* act[ORC_MAX_HIDDEN + 1];
   float* vst[ORC_MAX_HIDDEN]; /* membrane entering step t, [B,T,H] */
+  float* ast[ORC_MAX_HIDDEN] = {0}; /* ALIF: adaptation entering step t, [B,T,H] */
   {
     const size_t in = (size_t)net->in;
     uint8_t* xb = (uint8_t*)malloc(M * in);
@@ -361,6 +374,34 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
     vst[l] = (float*)malloc(M * H * sizeof(float));
     const float* beta = params + lo[l].beta;
     const size_t bs = net->beta_mode[l] == 0 ? 1 : 0; /* scalar beta broadcasts */
+    if (is_alif(net, l)) {
+      /* declared ALIF (spiketrain_oracle.h): threshold theta + a, reset by it */
+      const float* gam = params + lo[l].gamma;
+      ast[l] = (float*)malloc(M * H * sizeof(float));
+      for (size_t b = 0; b < B; ++b)
+        for (size_t n = 0; n < H; ++n) {
+          const float vb = clip01(beta[n * bs]);
+          const float gc = clip01(gam[n]);
+          const float omg = 1.0f - gc;
+          float v = 0.0f, a = 0.0f;
+          for (size_t t = 0; t < T; ++t) {
+            const size_t idx = (b * T + t) * H + n;
+            vst[l][idx] = v;
+            ast[l][idx] = a;
+            const float th = theta + a;
+            const float pre = v - th;
+            const float s = pre >= 0.0f ? 1.0f : 0.0f;
+            const float m = v * vb;
+            const float ai = m + cur[idx];
+            const float r = s * th;
+            v = ai - r;
+            const float ma = a * gc;
+            const float sa = omg * s;
+            a = ma + sa;
+            act[l + 1][idx] = s;
+          }
+        }
+    } else
     /* lif_step_taped (neuron.hpp:127-136), per timestep */
     for (size_t b = 0; b < B; ++b)
       for (size_t n = 0; n < H; ++n) {
@@ -572,6 +613,40 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
       const size_t bs = mode == 0 ? 1 : 0;
       const float* V = vst[hl];
       float* dIh = (float*)malloc(M * H * sizeof(float));
+      if (is_alif(net, hl)) {
+        /* declared ALIF reverse: gv = d/dv_{t+1}, ga = d/da_{t+1}, t descending.
+         *   dI_t = gv ; gs = (dS + (-gv) th) + ga (1 - gc) ; gp = gs g(pre)
+         *   gv' = gv bc + gp ; ga' = ((ga gc) - gp) - s gv
+         *   dgamma += ga (a_t - s) (clip mask), per neuron over (b, t) in b-major,
+         *   t-descending order; dbeta from dI and V below, exactly as for LIF. */
+        const float* gam = params + lo[hl].gamma;
+        float* ggam = grads + lo[hl].gamma;
+        const float* Av = ast[hl];
+        float* sg = (float*)calloc(H, sizeof(float));
+        for (size_t b = 0; b < B; ++b)
+          for (size_t n = 0; n < H; ++n) {
+            const float vb = clip01(beta[n * bs]);
+            const float gc = clip01(gam[n]);
+            const float omg = 1.0f - gc;
+            float gv = 0.0f, ga = 0.0f;
+            for (size_t t = T; t-- > 0;) {
+              const size_t idx = (b * T + t) * H + n;
+              dIh[idx] = gv;
+              const float th = theta + Av[idx];
+              const float pre = V[idx] - th;
+              const float s = pre >= 0.0f ? 1.0f : 0.0f;
+              const float gs = (dS[idx] + (-gv) * th) + ga * omg;
+              const float gp = gs * surrogate(net, pre);
+              sg[n] += ga * (Av[idx] - s);
+              const float ngv = gv * vb + gp;
+              ga = (ga * gc - gp) - s * gv;
+              gv = ngv;
+            }
+          }
+        for (size_t n = 0; n < H; ++n)
+          if (gam[n] > 0.0f && gam[n] < 1.0f) ggam[n] += sg[n];
+        free(sg);
+      } else {
       for (size_t b = 0; b < B; ++b)
         for (size_t n = 0; n < H; ++n) {
           const float vb = clip01(beta[n * bs]);
@@ -586,6 +661,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
             G = G * vb + gpre;                /* mul_bcast, add_scalar */
           }
         }
+      }
       {
         float* gvb = (float*)malloc(H * sizeof(float));
         for (size_t t = T - 1; t-- > 0 && mode != 2;) {
@@ -610,6 +686,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
 
   for (int l = 0; l <= L; ++l) free(act[l]);
   for (int l = 0; l < L; ++l) free(vst[l]);
+  for (int l = 0; l < L; ++l) free(ast[l]);
   for (int l = 0; l < L; ++l) free(dcount[l]);
   free(i3);
   free(trace);

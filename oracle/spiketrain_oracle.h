@@ -65,6 +65,21 @@ typedef struct orc_net {
    * monitor takes a normalised layer id, so every later layer's id -- its
    * init key child(id) and entry names -- moves up by one.                 */
   int monitor[ORC_MAX_HIDDEN];
+  /* Cell kind of hidden layer l: 0 LIF (neuron.hpp:127-136), 1 ALIF.
+   *
+   * ALIF is NOT in the reference: this is a
+   * DECLARED restatement -- parity unpinned against the reference.  It follows
+   * the adaptive-threshold LIF of Spyx (the paper's library; the
+   * LSNN form of Bellec et al. 2018) written in the reference's LIF op order:
+   *   th = theta + a ;  pre = v - th ;  s = [pre >= 0]
+   *   v' = ((v * bc) + I) - s * th        (bc = clip01(beta))
+   *   a' = (a * gc) + (1 - gc) * s        (gc = clip01(gamma), a_0 = 0)
+   * The cell carries a second per-neuron entry "l{id}.gamma" after "l{id}.beta",
+   * initialised TN(0.5, 0.25, +-2 sigma) from child(cell_key, 3) (beta uses
+   * child 2).  The backward is the exact reverse of these ops (surrogate on pre,
+   * reset and threshold paths differentiated); tests/test_alif_oracle.py pins it
+   * against torch autograd of the same forward.                            */
+  int cell[ORC_MAX_HIDDEN];
 } orc_net;
 
 /* Parameter entries in NetworkParams order (network.hpp:231-286). */
