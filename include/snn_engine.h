@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 5
+#define SNN_ABI_VERSION 6
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -77,7 +77,15 @@ typedef struct snn_network_desc {
    * monitor takes a normalised layer id, so the entry names and init keys of
    * every later layer move up by one (network.hpp:231-286). */
   int32_t monitor[SNN_MAX_HIDDEN];
+  /* Cell kind of hidden layer l (snn_cell).  SNN_CELL_ALIF is a DECLARED cell that
+   * the reference does not have: threshold theta + a, reset by
+   * it, a' = a*clip01(gamma) + (1 - clip01(gamma))*s, with a second per-neuron entry
+   * "l{id}.gamma" after "l{id}.beta" (init TN(0.5, 0.25) from child(cell_key, 3)).
+   * Its checker is the restatement in oracle/spiketrain_oracle.h.  Zero = LIF. */
+  int32_t cell[SNN_MAX_HIDDEN];
 } snn_network_desc;
+
+typedef enum snn_cell { SNN_CELL_LIF = 0, SNN_CELL_ALIF = 1 } snn_cell;
 
 /* TrainConfig subset that reaches the step (optimize.hpp:116-133). */
 typedef struct snn_train_config {
@@ -270,7 +278,9 @@ snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t par
  *         1: membrane V (entering step t)           [B][T][H]
  *         2: spikes (0/1 as u8)                     [B][T][H]
  *         3: readout trace                          [B][T][C]
- *         4: dS (grad of spikes) of hidden `layer`  [B][T][H]  */
+ *         4: dS (grad of spikes) of hidden `layer`  [B][T][H]
+ *         5: per-kernel phase clocks (tests/clk_probe.py)
+ *         6: ALIF adaptation a (entering step t)    [B][T][H]  */
 snn_status snn_debug_enable(snn_engine* e, int32_t on);
 snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* host, size_t bytes);
 

@@ -5,7 +5,7 @@ behind the C ABI in include/snn_engine.h; this package is the Python mirror of
 the reference interface used by the tests and bench.py.
 """
 from .engine import (  # noqa: F401
-    ActivationDesc, ArgumentError, ConfigError, ContractError, DeviceError, Engine, Error,
+    ActivationDesc, ALIFLayer, ArgumentError, ConfigError, ContractError, DeviceError, Engine, Error,
     FormatError, IoError, LIFLayer, LILayer, LinearLayer, MonitorLayer, NetworkSpec, ShapeError,
     SpecError,
     StateError, TrainConfig, UnsupportedError, default_activation_desc, lib, normalize,

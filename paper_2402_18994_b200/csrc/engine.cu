@@ -280,6 +280,7 @@ struct snn_engine {
   DevBuf<__nv_bfloat16> wb[kMaxLayers];
   // activations
   DevBuf<float> V[SNN_MAX_HIDDEN];
+  DevBuf<float> Aad[SNN_MAX_HIDDEN], dgamma[SNN_MAX_HIDDEN];  // ALIF adaptation trace, d gamma partials
   DevBuf<uint32_t> s_np[SNN_MAX_HIDDEN], s_tp[SNN_MAX_HIDDEN];
   DevBuf<__nv_bfloat16> di[kMaxLayers];  // per Linear j: dI of its output
   DevBuf<float> dbeta[kMaxLayers], dbias[kMaxLayers];
@@ -391,6 +392,9 @@ struct snn_engine {
       fail(SNN_ERR_ARGUMENT, "activation slope must be positive");
     for (int l = 0; l <= n.n_hidden; ++l)
       if (n.beta_mode[l] < 0 || n.beta_mode[l] > 2) fail(SNN_ERR_ARGUMENT, "unknown beta mode");
+    for (int l = 0; l < SNN_MAX_HIDDEN; ++l)
+      if (n.cell[l] != SNN_CELL_LIF && (n.cell[l] != SNN_CELL_ALIF || l >= n.n_hidden))
+        fail(SNN_ERR_SPEC, "hidden layer %d: unknown cell kind %d", l, n.cell[l]);
     if (n.activation == SNN_ACT_BOXCAR && !(n.aux > 0.0f))
       fail(SNN_ERR_ARGUMENT, "boxcar: width and height must be positive");
     if (cfg.batch_size < 1) fail(SNN_ERR_ARGUMENT, "train: batch size 0");
@@ -518,6 +522,10 @@ struct snn_engine {
       const size_t bsz = bm == 0 ? size_t(N[j]) : 1;
       entries.push_back({"l" + std::to_string(cell) + ".beta", kEntryBeta, j, 1, N[j], off, bsz, bm});
       off += bsz;
+      if (alif(j)) {  // declared ALIF cell: adaptation decay after beta (oracle/spiketrain_oracle.h)
+        entries.push_back({"l" + std::to_string(cell) + ".gamma", kEntryGamma, j, 1, N[j], off, size_t(N[j])});
+        off += N[j];
+      }
     }
     n_params = off;
   }
@@ -539,6 +547,10 @@ struct snn_engine {
     const size_t rows = size_t(B) * T_pad;
     for (int l = 0; l < L; ++l) {
       V[l].alloc(rows * H_pad[l], false);
+      if (alif(l)) {
+        Aad[l].alloc(rows * H_pad[l], false);
+        dgamma[l].alloc(size_t(B) * H[l]);
+      }
       s_np[l].alloc(rows * (H_pad[l] / 32));
       s_tp[l].alloc(size_t(H_pad[l]) * (rows / 32));
     }
@@ -584,6 +596,12 @@ struct snn_engine {
                     k_lif_bwd<4, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
+    for (auto fn : {k_lif_bwd<0, false, true>, k_lif_bwd<1, false, true>, k_lif_bwd<2, false, true>,
+                    k_lif_bwd<3, false, true>, k_lif_bwd<4, false, true>, k_lif_bwd<0, true, true>,
+                    k_lif_bwd<1, true, true>, k_lif_bwd<2, true, true>, k_lif_bwd<3, true, true>,
+                    k_lif_bwd<4, true, true>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(bwd_smem_bytes(TT, 2, true))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(kWgSmemLaunch)));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -632,6 +650,7 @@ struct snn_engine {
     for (int i = 0; i < j && i < L; ++i) id += net.monitor[i] ? 1 : 0;
     return id;
   }
+  bool alif(int l) const { return l < L && net.cell[l] == SNN_CELL_ALIF; }
   bool reg_on() const {
     if (cfg.lambda_low == 0.0f && cfg.lambda_high == 0.0f) return false;
     for (int l = 0; l < L; ++l)
@@ -653,6 +672,9 @@ struct snn_engine {
           h[e.offset] = net.fixed_beta[e.layer];  // Tensor::scalar(fixed_beta)
         else  // per-neuron [H] or LearnableScalar [] from the same key
           hostrng::truncated_normal(hostrng::child(lk, 2), e.size, 0.5f, 0.25f, h.data() + e.offset);
+      } else if (e.kind == kEntryGamma) {  // declared ALIF: gamma ~ TN(0.5, 0.25) from child 3
+        const uint64_t lk = hostrng::child(key, uint64_t(lin_id(e.layer) + 1));
+        hostrng::truncated_normal(hostrng::child(lk, 3), e.size, 0.5f, 0.25f, h.data() + e.offset);
       }
     }
     upload_params(h.data());
@@ -861,8 +883,24 @@ struct snn_engine {
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   }
 
+  template <bool kAlif>
+  void launch_bwd_alif(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
+                       const CUtensorMap& to, const BwdArgs& bw) {
+    const bool reg = bw.hist != nullptr;
+    switch (act) {
+      case 1: launch(reg ? k_lif_bwd<1, true, kAlif> : k_lif_bwd<1, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 2: launch(reg ? k_lif_bwd<2, true, kAlif> : k_lif_bwd<2, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 3: launch(reg ? k_lif_bwd<3, true, kAlif> : k_lif_bwd<3, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 4: launch(reg ? k_lif_bwd<4, true, kAlif> : k_lif_bwd<4, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      default: launch(reg ? k_lif_bwd<0, true, kAlif> : k_lif_bwd<0, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+    }
+  }
   void launch_bwd(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
                   const CUtensorMap& to, const BwdArgs& bw) {
+    if (bw.gamma != nullptr) {  // declared ALIF cell
+      launch_bwd_alif<true>(act, grid, smem, tw, td, to, bw);
+      return;
+    }
     if (bw.hist != nullptr) {  // monitored layer with the activity regularizer on
       switch (act) {
         case 1: launch(k_lif_bwd<1, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
@@ -984,6 +1022,8 @@ struct snn_engine {
         ly.s_np = s_np[l + i].p;
         ly.s_tp = s_tp[l + i].p;
         ly.dbg_i = debug ? dbg_i[l + i].p : nullptr;
+        ly.gamma = alif(l + i) ? params.p + entry_of(kEntryGamma, l + i).offset : nullptr;
+        ly.a_out = alif(l + i) ? Aad[l + i].p : nullptr;
         ly.K_pad = K_pad[l + i]; ly.H = H[l + i]; ly.H_pad = H_pad[l + i];
         fm.m[i] = tm_wt[l + i];
       }
@@ -1044,6 +1084,11 @@ struct snn_engine {
       bw.dbeta_part = dbeta[l].p;
       bw.dbias_part = net.bias ? dbias[l].p : nullptr;
       bw.dbg_ds = debug ? dbg_ds[l].p : nullptr;
+      if (alif(l)) {
+        bw.a_in = Aad[l].p;
+        bw.gamma = params.p + entry_of(kEntryGamma, l).offset;
+        bw.dgamma_part = dgamma[l].p;
+      }
       bw.dbg_clk = debug ? dbg_clk.p + size_t(1 + L + l) * clk_region() : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
@@ -1057,7 +1102,7 @@ struct snn_engine {
           bw.f_min = cfg.f_min; bw.f_max = cfg.f_max;
           bw.lambda_low = cfg.lambda_low; bw.lambda_high = cfg.lambda_high;
         }
-      launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages),
+      launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages, alif(l)),
                  tm_wb[l + 1], tm_di_k[l + 1], tm_di_out[l], bw);
       mark(evs, "lif_bwd", l);
     }
@@ -1100,6 +1145,7 @@ struct snn_engine {
         r.splits[j] = splits_w[j];
         r.dbeta_part[j] = dbeta[j].p;
         r.dbias_part[j] = net.bias ? dbias[j].p : nullptr;
+        r.dgamma_part[j] = alif(j) ? dgamma[j].p : nullptr;
       }
       r.vec_index = vec_index.p;
       r.n_vec = n_vec;
@@ -2127,9 +2173,12 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
     const size_t need = size_t(B) * T * H * elem;
     if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
     const size_t rows = size_t(B) * T_pad;
-    if (which == 0 || which == 1 || which == 4) {
+    if (which == 6 && !e->alif(layer)) fail(SNN_ERR_ARGUMENT, "layer %d is not an ALIF cell", layer);
+    if (which == 0 || which == 1 || which == 4 || which == 6) {
       std::vector<float> buf(rows * Hp);
-      const float* src = which == 0 ? e->dbg_i[layer].p : (which == 1 ? e->V[layer].p : e->dbg_ds[layer].p);
+      const float* src = which == 0 ? e->dbg_i[layer].p
+                         : which == 1 ? e->V[layer].p
+                         : which == 6 ? e->Aad[layer].p : e->dbg_ds[layer].p;
       CK(cudaMemcpy(buf.data(), src, buf.size() * 4, cudaMemcpyDeviceToHost));
       float* out = static_cast<float*>(host);
       for (int b = 0; b < B; ++b)

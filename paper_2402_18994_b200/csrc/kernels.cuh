@@ -173,6 +173,8 @@ struct FwdLayer {
   uint32_t* s_np;         // [B][T_pad][H_pad/32]
   uint32_t* s_tp;         // [H_pad][B*T_pad/32]
   float* dbg_i;           // optional [B][T_pad][H_pad] raw projection
+  const float* gamma;     // ALIF (declared cell): adaptation decay [H]; nullptr = LIF
+  float* a_out;           // ALIF: adaptation entering step t [B][T_pad][H_pad]
   int K_pad, H, H_pad;
 };
 // A launch runs n_layers consecutive hidden layers.  n_layers > 1 (fused) needs
@@ -263,6 +265,38 @@ __device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, fl
     const float m = __fmul_rn(v, vb);
     const float ai = __fadd_rn(m, I);
     v = __fsub_rn(ai, sp ? theta : 0.0f);
+    const uint32_t bal = __ballot_sync(0xffffffffu, sp);
+    myword = (lane == j) ? bal : myword;
+    tmask |= uint32_t(sp) << j;
+  }
+}
+
+// 32 steps of the DECLARED ALIF cell (not in the reference; oracle/spiketrain_oracle.h
+// states it, op order bit-identical to the oracle):
+//   th = theta + a ; pre = v - th ; s = pre >= 0 ; v = ((v * bc) + I) - s * th ;
+//   a = (a * gc) + (1 - gc) * s
+// V and the adaptation a are stored before each step (state entering step t).
+__device__ __forceinline__ void alif_chunk(const uint32_t (&r)[32], float* vp, float* ap, float* dp,
+                                           int hpad, int nvalid, float vb, float gc, float bn,
+                                           bool has_bias, float theta, int lane, float& v, float& ad,
+                                           uint32_t& myword, uint32_t& tmask) {
+  const float omg = __fsub_rn(1.0f, gc);
+  myword = 0u;
+  tmask = 0u;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    float I = __uint_as_float(r[j]);
+    if (has_bias) I = __fadd_rn(I, bn);
+    if (dp != nullptr && j < nvalid) dp[size_t(j) * hpad] = I;
+    vp[size_t(j) * hpad] = v;
+    ap[size_t(j) * hpad] = ad;
+    const float th = __fadd_rn(theta, ad);
+    const float pre = __fsub_rn(v, th);
+    const bool sp = pre >= 0.0f && j < nvalid;
+    const float m = __fmul_rn(v, vb);
+    const float ai = __fadd_rn(m, I);
+    v = __fsub_rn(ai, sp ? th : 0.0f);
+    ad = __fadd_rn(__fmul_rn(ad, gc), sp ? omg : 0.0f);
     const uint32_t bal = __ballot_sync(0xffffffffu, sp);
     myword = (lane == j) ? bal : myword;
     tmask |= uint32_t(sp) << j;
@@ -511,6 +545,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float vb = clip01(n < ly.H ? ly.beta[n * ly.beta_stride] : 0.0f);
       const float bn = (ly.bias != nullptr && n < ly.H) ? ly.bias[n] : 0.0f;
       const size_t hw = size_t(ly.H_pad) / 32;
+      const bool alif = ly.gamma != nullptr;
+      const float gc = (alif && n < ly.H) ? clip01(ly.gamma[n]) : 0.0f;
+      float ad = 0.0f;  // ALIF adaptation state
       // fused: lane j writes the next layer's B row t0+j (its quadrant's 32 spikes
       // of that step, from the ballot word) into stage q/2's B part
       const bool feed = li + 1 < a.n_layers;
@@ -530,7 +567,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint32_t myword = 0u, tmask = 0u;
           if (t0 < a.T) {
             float* vp = ly.v_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
-            if (ly.bias != nullptr || ly.dbg_i != nullptr || t0 + 32 > a.T)
+            if (alif)
+              alif_chunk(r, vp, ly.a_out + (vp - ly.v_out),
+                         ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
+                         min(32, a.T - t0), vb, gc, bn, ly.bias != nullptr, a.theta, lane, v, ad,
+                         myword, tmask);
+            else if (ly.bias != nullptr || ly.dbg_i != nullptr || t0 + 32 > a.T)
               lif_chunk<true>(r, vp, ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
                               a.T - t0, vb, bn, a.theta, lane, v, myword, tmask);
             else
@@ -881,6 +923,10 @@ struct BwdArgs {
   const uint32_t* s_tp;        // this layer's spikes, time-packed [H_pad][B*T_pad/32]
   unsigned int* hist;          // [T+1] (sample, neuron) count histogram for the loss value
   float reg_gs, f_min, f_max, lambda_low, lambda_high;  // reg_gs = 2 / (B_global*H * T)
+  // ALIF (kAlif launches only; declared cell, oracle/spiketrain_oracle.h)
+  const float* a_in;           // adaptation entering step t [B][T_pad][H_pad]
+  const float* gamma;          // [H]
+  float* dgamma_part;          // [B][H]
 };
 
 // d loss / d count of one (sample, neuron) (objective.hpp:208-227): with g = 1,
@@ -983,12 +1029,103 @@ __device__ __forceinline__ void bwd_replay(const uint32_t (&r)[16], const float 
   }
 }
 
+// ALIF reverse step (declared cell; the exact reverse of alif_chunk's ops, same
+// statement order as the oracle): with gv = d/dv_{t+1}, ga = d/da_{t+1}
+//   th = theta + a ; s = (v - th) >= 0 ; g = g(v - th)
+//   gs = (dS + (-gv) th) + ga (1 - gc) ; gp = gs g
+//   gv' = gv bc + gp ; ga' = ((ga gc) - gp) - s gv
+// Linear in (gv, ga): the compose pass builds the 2x2 affine map of 16 steps,
+//   [gv'; ga'] = [[bc - th g, (1-gc) g], [th g - s, gc - (1-gc) g]] [gv; ga] + g dS [1; -1]
+template <int kAct, bool kTail>
+__device__ __forceinline__ void bwd_compose_alif(const uint32_t (&r)[16], const float (&vr)[16],
+                                                 const float (&ar)[16], int nval, float vb, float gc,
+                                                 float omg, float theta, const BwdArgs& a,
+                                                 float (&P)[4], float (&q)[2]) {
+#pragma unroll
+  for (int e = 15; e >= 0; --e) {
+    if (kTail && e >= nval) continue;
+    const float th = __fadd_rn(theta, ar[e]);
+    const float pre = __fsub_rn(vr[e], th);
+    const float sp = pre >= 0.0f ? 1.0f : 0.0f;
+    const float g = surrogate_t<kAct>(a.slope, a.aux, pre);
+    const float tg = th * g, og = omg * g;
+    const float m00 = vb - tg, m01 = og, m10 = tg - sp, m11 = gc - og;
+    const float c = g * __uint_as_float(r[e]);
+    const float p00 = m00 * P[0] + m01 * P[2], p01 = m00 * P[1] + m01 * P[3];
+    const float p10 = m10 * P[0] + m11 * P[2], p11 = m10 * P[1] + m11 * P[3];
+    const float q0 = m00 * q[0] + m01 * q[1] + c, q1 = m10 * q[0] + m11 * q[1] - c;
+    P[0] = p00; P[1] = p01; P[2] = p10; P[3] = p11;
+    q[0] = q0; q[1] = q1;
+  }
+}
+template <int kAct, bool kTail>
+__device__ __forceinline__ void bwd_replay_alif(const uint32_t (&r)[16], const float (&vr)[16],
+                                                const float (&ar)[16], int nval, float vb, float gc,
+                                                float omg, float theta, const BwdArgs& a, float& gv,
+                                                float& ga, float& db, float& dbias, float& dgam,
+                                                float (&x)[16]) {
+#pragma unroll
+  for (int e = 15; e >= 0; --e) {
+    if (kTail && e >= nval) {
+      x[e] = 0.0f;
+      continue;
+    }
+    const float th = __fadd_rn(theta, ar[e]);
+    const float pre = __fsub_rn(vr[e], th);
+    const float sp = pre >= 0.0f ? 1.0f : 0.0f;
+    const float g = surrogate_t<kAct>(a.slope, a.aux, pre);
+    const float gs = __fadd_rn(__fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gv, th)), __fmul_rn(ga, omg));
+    const float gp = __fmul_rn(gs, g);
+    x[e] = gv;
+    db = __fadd_rn(db, __fmul_rn(gv, vr[e]));
+    dbias = __fadd_rn(dbias, gv);
+    dgam = __fadd_rn(dgam, __fmul_rn(ga, __fsub_rn(ar[e], sp)));
+    const float ngv = __fadd_rn(__fmul_rn(gv, vb), gp);
+    ga = __fsub_rn(__fsub_rn(__fmul_rn(ga, gc), gp), __fmul_rn(sp, gv));
+    gv = ngv;
+  }
+}
+
 // dS of 16 steps + the monitor's per-(sample, neuron) term (two gradient
 // contributions to the stacked spikes: commutative, so the reference's order
 // does not matter)
 __device__ __forceinline__ void add_dcount(uint32_t (&r)[16], float term) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__fadd_rn(__uint_as_float(r[e]), term));
+}
+
+// dI of 16 steps as 3 bf16 planes: staged in smem (one t-tile, SW128 layout of
+// tm_out; tl = step within the tile) or stored straight to the planes (drow = the
+// neuron's row at the chunk's first step, plane = plane stride in elements).
+__device__ __forceinline__ void bwd_store_di16(const float (&x)[16], bool stage_out, uint8_t* smem,
+                                               int tl, int q, int lane, int TT,
+                                               __nv_bfloat16* drow, size_t plane) {
+  uint32_t ph_[8], pm_[8], pl_[8];
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) split3_pack(x[e], x[e + 1], ph_[e / 2], pm_[e / 2], pl_[e / 2]);
+  if (stage_out) {
+    const uint32_t row = uint32_t(q * 32 + lane);
+    const uint32_t base = smem_u32(smem) + uint32_t(tl >> 6) * 16384u + row * 128u;
+    const uint32_t j0 = uint32_t(tl & 63) >> 3;
+    const uint32_t o0 = ((j0 ^ (row & 7u)) << 4), o1 = (((j0 + 1u) ^ (row & 7u)) << 4);
+    const uint32_t pstride = uint32_t(TT / 64) * 16384u;
+    st_shared_v4(base + o0, make_uint4(ph_[0], ph_[1], ph_[2], ph_[3]));
+    st_shared_v4(base + o1, make_uint4(ph_[4], ph_[5], ph_[6], ph_[7]));
+    st_shared_v4(base + pstride + o0, make_uint4(pm_[0], pm_[1], pm_[2], pm_[3]));
+    st_shared_v4(base + pstride + o1, make_uint4(pm_[4], pm_[5], pm_[6], pm_[7]));
+    st_shared_v4(base + 2 * pstride + o0, make_uint4(pl_[0], pl_[1], pl_[2], pl_[3]));
+    st_shared_v4(base + 2 * pstride + o1, make_uint4(pl_[4], pl_[5], pl_[6], pl_[7]));
+  } else {
+    uint4* dh = reinterpret_cast<uint4*>(drow);
+    uint4* dm = reinterpret_cast<uint4*>(drow + plane);
+    uint4* dl = reinterpret_cast<uint4*>(drow + 2 * plane);
+    dh[0] = make_uint4(ph_[0], ph_[1], ph_[2], ph_[3]);
+    dh[1] = make_uint4(ph_[4], ph_[5], ph_[6], ph_[7]);
+    dm[0] = make_uint4(pm_[0], pm_[1], pm_[2], pm_[3]);
+    dm[1] = make_uint4(pm_[4], pm_[5], pm_[6], pm_[7]);
+    dl[0] = make_uint4(pl_[0], pl_[1], pl_[2], pl_[3]);
+    dl[1] = make_uint4(pl_[4], pl_[5], pl_[6], pl_[7]);
+  }
 }
 
 #ifndef SNN_BWD_EXP
@@ -1000,13 +1137,15 @@ constexpr int kBwdThreads = kBwdScanThreads + 32;  // + control warp (lane 0 TMA
 __host__ __device__ constexpr uint32_t bwd_stage_bytes(int TT) {
   return 3 * kPlaneTile + 3 * uint32_t(TT) * 128u;
 }
-__host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages) {
-  return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256 + 3 * 4 * kBwdScanThreads;
+// segment exchange floats per scan thread: LIF (A, Bc, G); ALIF (P 2x2, q 2, G 2)
+__host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages, bool alif = false) {
+  return uint32_t(stages) * bwd_stage_bytes(TT) + 1024 + 256 + (alif ? 8 : 3) * 4 * kBwdScanThreads;
 }
 
 // kReg: the layer feeds a monitor and the activity regularizer is on -- every
 // step's dS gains d loss / d count of its (sample, neuron) (sum_axis1 backward).
-template <int kAct, bool kReg = false>
+// kAlif: the layer is the declared ALIF cell (two-state reverse scan, 2x2 maps).
+template <int kAct, bool kReg = false, bool kAlif = false>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
               const __grid_constant__ CUtensorMap tm_out, BwdArgs a) {
@@ -1035,7 +1174,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   // one t-tile: TT more columns cache the membranes V between the two scan passes
-  const bool vcache = a.NT == 1;
+  const bool vcache = a.NT == 1 && !kAlif;
   const uint32_t tmem_cols = vcache ? acc_cols(2 * a.TT, 1) : acc_cols(a.TT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
 
@@ -1109,6 +1248,146 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       }
     }
     __syncwarp();
+  } else if constexpr (kAlif) {
+    // ALIF scan warps (declared cell): the same segment structure as the LIF path
+    // below with the two-state reverse step -- each segment composes its 2x2 affine
+    // map (bwd_compose_alif), the maps are chained through smem, then every segment
+    // replays its steps in the oracle's statement order (bwd_replay_alif).  V and
+    // the adaptation a are read from HBM / L2 in both passes (no TMEM cache).
+    const int q = warp & 3, sg = warp >> 2;
+    const int sidx = sg * 128 + q * 32 + lane;
+    const int n = nt * 128 + q * 32 + lane;
+    const float vb = clip01(n < a.H ? a.beta[n * a.beta_stride] : 0.0f);
+    const float gc = n < a.H ? clip01(a.gamma[n]) : 0.0f;
+    const float omg = __fsub_rn(1.0f, gc);
+    const float theta = a.theta;
+    const size_t plane = size_t(a.H_pad) * cols_total;
+    __nv_bfloat16* __restrict__ drow = a.di_planes + size_t(n) * cols_total + size_t(b) * a.T_pad;
+    const float* __restrict__ vrow = a.v_in + size_t(b) * a.T_pad * a.H_pad + n;
+    const float* __restrict__ arow = a.a_in + size_t(b) * a.T_pad * a.H_pad + n;
+    const int seg_len = a.TT / kBwdSeg;
+    const bool stage_out = a.NT == 1;
+    float* xP = reinterpret_cast<float*>(smem + S * stage_bytes + 256);  // [4][256]
+    float* xQ = xP + 4 * kBwdScanThreads;                                 // [2][256]
+    float* xG = xQ + 2 * kBwdScanThreads;                                 // [2][256]
+    const int last = (kBwdSeg - 1) * 128 + q * 32 + lane;
+    float cv = 0.0f, ca = 0.0f;  // (gv, ga) entering the t-tile from above
+    float db = 0.0f, dbias = 0.0f, dgam = 0.0f;
+    float rterm = 0.0f;
+    if constexpr (kReg) {
+      int count = -1;
+      if (n < a.H) {
+        const int wpb = a.T_pad / 32;
+        const uint32_t* w = a.s_tp + size_t(n) * (size_t(a.B) * wpb) + size_t(b) * wpb;
+        count = 0;
+        for (int i = 0; i < wpb; ++i) count += __popc(__ldg(w + i));
+        rterm = activity_dcount(a, count);
+      }
+      if (sg == 0) {
+        const unsigned peers = __match_any_sync(0xffffffffu, count);
+        if (count >= 0 && lane == __ffs(peers) - 1) atomicAdd(a.hist + count, unsigned(__popc(peers)));
+      }
+    }
+    for (int j = 0; j < a.NT; ++j) {
+      const int tt = a.NT - 1 - j, buf = j % nbuf;
+      const int t_lo = tt * a.TT + sg * seg_len;
+      const int t_hi = min(t_lo + seg_len, a.T);
+      const uint32_t tcol = tmem + (uint32_t(q * 32) << 16) + buf * a.TT + sg * seg_len;
+      mbar_wait(&acc_full[buf], (j / nbuf) & 1);
+      tc_fence_after();
+      const float* vseg = vrow + size_t(t_lo) * a.H_pad;
+      const float* aseg = arow + size_t(t_lo) * a.H_pad;
+      const int top = seg_len - 16;
+      float P[4] = {1.0f, 0.0f, 0.0f, 1.0f}, Q[2] = {0.0f, 0.0f};
+      for (int c0 = top; c0 >= 0; c0 -= 16) {
+        const int nval = t_hi - (t_lo + c0);
+        if (nval <= 0) continue;
+        float vr[16], ar[16];
+        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
+        load_v16(aseg + size_t(c0) * a.H_pad, a.H_pad, nval, ar);
+        uint32_t r[16];
+        tmem_ld16(tcol + c0, r);
+        tmem_ld_wait();
+        if constexpr (kReg) add_dcount(r, rterm);
+        if (nval >= 16) bwd_compose_alif<kAct, false>(r, vr, ar, 16, vb, gc, omg, theta, a, P, Q);
+        else bwd_compose_alif<kAct, true>(r, vr, ar, nval, vb, gc, omg, theta, a, P, Q);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xP[i * kBwdScanThreads + sidx] = P[i];
+      xQ[sidx] = Q[0];
+      xQ[kBwdScanThreads + sidx] = Q[1];
+      if (sg == kBwdSeg - 1) {
+        xG[sidx] = cv;
+        xG[kBwdScanThreads + sidx] = ca;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      float gv = xG[last], ga = xG[kBwdScanThreads + last];
+      for (int s2 = kBwdSeg - 1; s2 > sg; --s2) {
+        const int o = s2 * 128 + q * 32 + lane;
+        const float ngv = xP[o] * gv + xP[kBwdScanThreads + o] * ga + xQ[o];
+        ga = xP[2 * kBwdScanThreads + o] * gv + xP[3 * kBwdScanThreads + o] * ga + xQ[kBwdScanThreads + o];
+        gv = ngv;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      for (int c0 = top; c0 >= 0; c0 -= 16) {
+        const int nval = t_hi - (t_lo + c0);
+        if (nval <= 0) continue;
+        float vr[16], ar[16];
+        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
+        load_v16(aseg + size_t(c0) * a.H_pad, a.H_pad, nval, ar);
+        uint32_t r[16];
+        tmem_ld16(tcol + c0, r);
+        tmem_ld_wait();
+        if constexpr (kReg) add_dcount(r, rterm);
+        if (a.dbg_ds != nullptr) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < nval)
+              a.dbg_ds[(size_t(b) * a.T_pad + t_lo + c0 + e) * a.H_pad + n] = __uint_as_float(r[e]);
+        }
+        float x[16];
+        if (nval >= 16) bwd_replay_alif<kAct, false>(r, vr, ar, 16, vb, gc, omg, theta, a, gv, ga, db, dbias, dgam, x);
+        else bwd_replay_alif<kAct, true>(r, vr, ar, nval, vb, gc, omg, theta, a, gv, ga, db, dbias, dgam, x);
+        bwd_store_di16(x, stage_out, smem, sg * seg_len + c0, q, lane, a.TT, drow + t_lo + c0, plane);
+      }
+      if (sg == 0) {
+        xG[last] = gv;
+        xG[kBwdScanThreads + last] = ga;
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      if (stage_out) fence_async_smem();
+      asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+      cv = xG[last];
+      ca = xG[kBwdScanThreads + last];
+      if (stage_out && threadIdx.x == 0) {
+        for (int p = 0; p < 3; ++p)
+          for (int h = 0; h < a.TT / 64; ++h)
+            tma_store_2d(&tm_out, smem + (p * (a.TT / 64) + h) * 16384, b * a.T_pad + h * 64,
+                         p * a.H_pad + nt * 128);
+        bulk_commit();
+      }
+    }
+    // per-segment beta / bias / gamma partials combined in a fixed order
+    if (sg > 0) {
+      xP[sidx] = db;
+      xP[kBwdScanThreads + sidx] = dbias;
+      xP[2 * kBwdScanThreads + sidx] = dgam;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
+    if (sg == 0) {
+      for (int s2 = 1; s2 < kBwdSeg; ++s2) {
+        const int o = s2 * 128 + q * 32 + lane;
+        db = __fadd_rn(db, xP[o]);
+        dbias = __fadd_rn(dbias, xP[kBwdScanThreads + o]);
+        dgam = __fadd_rn(dgam, xP[2 * kBwdScanThreads + o]);
+      }
+      if (n < a.H) {
+        a.dbeta_part[size_t(b) * a.H + n] = db;
+        a.dgamma_part[size_t(b) * a.H + n] = dgam;
+        if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * a.H + n] = dbias;
+      }
+    }
   } else {
     // Scan warps: quadrant q (TMEM lanes 32q..32q+31 = neurons), time segment sg
     // of each t-tile.  G' = (bc - theta g) G + g dS is linear in G, so each
@@ -1574,7 +1853,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 // K6  gradient assembly, Adam and operand-plane refresh.
 // One thread per flat parameter in NetworkParams order (network.hpp:164-226).
 // ============================================================================
-enum EntryKind : int32_t { kEntryW = 0, kEntryB = 1, kEntryBeta = 2 };
+// kEntryGamma: the declared ALIF cell's adaptation decay [H] (layer = hidden index)
+enum EntryKind : int32_t { kEntryW = 0, kEntryB = 1, kEntryBeta = 2, kEntryGamma = 3 };
 
 struct Entry {
   int32_t kind, layer;    // layer = Linear index j (W, b) or cell index (beta)
@@ -1583,7 +1863,7 @@ struct Entry {
   int64_t offset;         // into the flat vector
 };
 
-constexpr int kMaxEntries = 3 * 9;
+constexpr int kMaxEntries = 4 * 9;
 
 struct ReduceArgs {
   Entry entries[kMaxEntries];
@@ -1593,6 +1873,7 @@ struct ReduceArgs {
   int M_pad[kMaxLayers], N_pad[kMaxLayers], splits[kMaxLayers];
   const float* dbeta_part[kMaxLayers];  // per cell j: [B][N]
   const float* dbias_part[kMaxLayers];  // per Linear j: [B][N]
+  const float* dgamma_part[kMaxLayers]; // per ALIF cell j: [B][N]
   const int32_t* vec_index;             // flat indices of the beta / bias entries
   int n_vec;
   const float* params;                  // for the clip mask
@@ -1777,7 +2058,8 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
       const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
       const int64_t li = i - en.offset;
       const float* __restrict__ src =
-          (en.kind == kEntryB ? a.dbias_part[en.layer] : a.dbeta_part[en.layer]) + li;
+          (en.kind == kEntryB ? a.dbias_part[en.layer]
+                              : en.kind == kEntryGamma ? a.dgamma_part[en.layer] : a.dbeta_part[en.layer]) + li;
       float g = 0.0f;
       if (en.kind == kEntryBeta && en.beta_mode != 0) {
         // scalar beta: every (b, n) partial; fixed beta: no gradient
@@ -1789,7 +2071,7 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
       if (lane == 0) {
-        if (en.kind == kEntryBeta) {
+        if (en.kind == kEntryBeta || en.kind == kEntryGamma) {
           const float beta = a.params[i];
           if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
         }
@@ -2047,7 +2329,8 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
       const Entry en = r.entries[find_entry(r.entries, r.n_entries, i)];
       const int64_t li = i - en.offset;
       const float* __restrict__ src =
-          (en.kind == kEntryB ? r.dbias_part[en.layer] : r.dbeta_part[en.layer]) + li;
+          (en.kind == kEntryB ? r.dbias_part[en.layer]
+                              : en.kind == kEntryGamma ? r.dgamma_part[en.layer] : r.dbeta_part[en.layer]) + li;
       float g = 0.0f;
       if (en.kind == kEntryBeta && en.beta_mode != 0) {
         // scalar beta: every (b, n) partial (mul_bcast backward, autodiff.hpp:191-205);
@@ -2060,7 +2343,7 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) g = __fadd_rn(g, __shfl_xor_sync(0xffffffffu, g, off));
       if (lane == 0) {
-        if (en.kind == kEntryBeta) {
+        if (en.kind == kEntryBeta || en.kind == kEntryGamma) {
           const float beta = r.params[i];
           if (!(beta > 0.0f && beta < 1.0f)) g = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
         }

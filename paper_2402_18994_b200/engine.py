@@ -73,6 +73,15 @@ class LIFLayer:
 
 
 @dataclass
+class ALIFLayer(LIFLayer):
+    """Adaptive-threshold LIF -- a DECLARED cell, not in the reference (SPEC.md:373,
+    :382): threshold theta + a, reset by it, a' = a*clip01(gamma) + (1-clip01(gamma))*s,
+    with a per-neuron "l{id}.gamma" entry after "l{id}.beta" (Spyx's ALIF in the
+    reference's LIF op order; checker: oracle/spiketrain_oracle.h).  gamma is always
+    per neuron and trainable; beta_mode applies to beta."""
+
+
+@dataclass
 class LILayer:
     beta_mode: str = "per_neuron"
     fixed_beta: float = 0.5
@@ -114,7 +123,7 @@ class TrainConfig:
     lambda_high: float = 0.0
 
 
-ABI_VERSION = 5  # SNN_ABI_VERSION in include/snn_engine.h
+ABI_VERSION = 6  # SNN_ABI_VERSION in include/snn_engine.h
 
 
 class _NetDesc(C.Structure):
@@ -122,7 +131,7 @@ class _NetDesc(C.Structure):
                 ("classes", C.c_int32), ("bias", C.c_int32), ("threshold", C.c_float),
                 ("activation", C.c_int32), ("slope", C.c_float), ("aux", C.c_float),
                 ("beta_mode", C.c_int32 * 9), ("fixed_beta", C.c_float * 9),
-                ("monitor", C.c_int32 * 8)]
+                ("monitor", C.c_int32 * 8), ("cell", C.c_int32 * 8)]
 
 
 BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
@@ -160,7 +169,7 @@ def normalize(spec: NetworkSpec) -> dict:
     monitor = [m // 2 - 1 for m in monitor]  # index of the hidden LIF block
     if len(layers) < 4 or len(layers) % 2:
         raise UnsupportedError("engine supports [Linear, LIF]*k + Linear + LI")
-    hidden, act, thr, bias, modes, fixed = [], None, None, None, [], []
+    hidden, act, thr, bias, modes, fixed, cells = [], None, None, None, [], [], []
     for i in range(0, len(layers) - 2, 2):
         lin, cell = layers[i], layers[i + 1]
         if not isinstance(lin, LinearLayer) or not isinstance(cell, LIFLayer):
@@ -174,6 +183,7 @@ def normalize(spec: NetworkSpec) -> dict:
         act, thr, bias = cell.activation, cell.threshold, lin.bias
         hidden.append(int(lin.out))
         modes.append(cell.beta_mode)
+        cells.append("alif" if isinstance(cell, ALIFLayer) else "lif")
         fixed.append(float(cell.fixed_beta))
     lin, cell = layers[-2], layers[-1]
     if not isinstance(lin, LinearLayer) or not isinstance(cell, LILayer):
@@ -187,14 +197,17 @@ def normalize(spec: NetworkSpec) -> dict:
     return dict(input=inp, hidden=hidden, classes=int(lin.out), bias=bool(bias),
                 threshold=float(thr), activation=act.name, slope=float(act.slope),
                 aux=float(act.aux), beta_mode=modes + [cell.beta_mode],
-                fixed_beta=fixed + [float(cell.fixed_beta)], monitor=monitor)
+                fixed_beta=fixed + [float(cell.fixed_beta)], monitor=monitor, cell=cells)
 
 
-def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False) -> NetworkSpec:
-    """The BASELINE network: 700-H1-H2-20, LIF, arctan k=2, nobias."""
+def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False,
+             cell="lif") -> NetworkSpec:
+    """The BASELINE network: 700-H1-H2-20, LIF, arctan k=2, nobias (PAPER.md:122);
+    cell="alif" gives BASELINE config 2's adaptive-threshold variant."""
     layers = []
+    kind = ALIFLayer if cell == "alif" else LIFLayer
     for h in hidden:
-        layers += [LinearLayer(h, bias), LIFLayer(default_activation_desc(act))]
+        layers += [LinearLayer(h, bias), kind(default_activation_desc(act))]
     layers += [LinearLayer(classes, bias), LILayer()]
     return NetworkSpec([inp], layers)
 
@@ -275,6 +288,8 @@ class Engine:
             n.fixed_beta[i] = fb
         for m in d["monitor"]:
             n.monitor[m] = 1
+        for i, k in enumerate(d["cell"]):
+            n.cell[i] = 1 if k == "alif" else 0
         c = _TrainCfg()
         c.batch_size = int(cfg.batch_size)
         c.time_steps = int(time_steps)
@@ -594,7 +609,7 @@ class Engine:
         self._check(self._L.snn_debug_enable(self._h, int(on)))
 
     def fetch(self, which: str, layer: int = 0) -> np.ndarray:
-        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5}[which]
+        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5, "A": 6}[which]
         B, T = self.batch_size, self.time_steps
         if which == "clk":
             out = np.empty((3 + 2 * len(self.desc["hidden"]), max(B * 4, 4096), 48), np.int64)

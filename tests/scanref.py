@@ -66,3 +66,29 @@ def lif_backward(dS, V, beta, theta, act, k, aux):
         gpre = gs * surrogate(act, k, aux, pre)
         G = (G * vb + gpre).astype(F)
     return dI
+
+
+def alif_forward(I, beta, gamma, theta):
+    """Declared ALIF cell (oracle/spiketrain_oracle.h), same op order:
+    I [B,T,H] f32 -> (V, a entering each step, spikes u8)."""
+    B, T, H = I.shape
+    vb = clip01(beta.astype(F))
+    gc = clip01(gamma.astype(F))
+    omg = (F(1) - gc).astype(F)
+    theta = F(theta)
+    v = np.zeros((B, H), F)
+    a = np.zeros((B, H), F)
+    V = np.empty_like(I)
+    A = np.empty_like(I)
+    S = np.empty(I.shape, np.uint8)
+    for t in range(T):
+        V[:, t] = v
+        A[:, t] = a
+        th = (theta + a).astype(F)
+        pre = (v - th).astype(F)
+        s = pre >= F(0)
+        ai = (v * vb + I[:, t]).astype(F)
+        v = (ai - s.astype(F) * th).astype(F)
+        a = (a * gc + omg * s.astype(F)).astype(F)
+        S[:, t] = s
+    return V, A, S

@@ -35,6 +35,13 @@ def make_engine(net: Net, B, T, seed=0, lr=1e-3, **cfg):
             layer.threshold = net.threshold
             if net.slope is not None:
                 layer.activation.slope = net.slope
+    if net.cell:  # declared ALIF cells (oracle/spiketrain_oracle.h)
+        from paper_2402_18994_b200 import ALIFLayer
+        hid = [i for i, layer in enumerate(spec.layers) if type(layer).__name__ == "LIFLayer"]
+        for i, kind in zip(hid, net.cell):
+            if kind == "alif":
+                old = spec.layers[i]
+                spec.layers[i] = ALIFLayer(old.activation, old.threshold, old.beta_mode, old.fixed_beta)
     if net.monitor:  # MonitorLayer after the listed hidden LIF layers
         from paper_2402_18994_b200 import MonitorLayer
         for m in sorted(net.monitor, reverse=True):
@@ -891,3 +898,84 @@ def test_container_errors_match_reference_classes(tmp_path):
     other_in = make_engine(Net(inp=41, hidden=(16,), classes=5), 2, 21)
     with pytest.raises(ShapeError):
         other_in.load_container(os.path.join(gold, "flat.spkd"))
+
+
+# ---------------------------------------------------------------------------
+# Declared ALIF cell (BASELINE config 2; not in the reference -- the checker is
+# the oracle's restatement, itself pinned to float64 autograd in
+# tests/test_alif_oracle.py).  Forward V / a / spikes bit-exact given the GPU's
+# projection; loss and gradients (gamma included) within the north_star bar.
+ALIF_CASES = [
+    ("alif-tiny", Net(inp=30, hidden=(16, 12), classes=5, act="superspike", cell=("alif", "alif")), 6, 19, 3.0),
+    ("alif-c2-shape", Net(act="superspike", cell=("alif", "alif")), 8, 128, 2.0),
+    ("alif-lif-T200", Net(inp=64, hidden=(128, 128), classes=10, cell=("alif", "lif")), 3, 200, 2.0),
+    ("alif-bias-3hidden", Net(inp=50, hidden=(64, 48, 32), classes=6, act="triangular", bias=True,
+                              cell=("lif", "alif", "alif")), 4, 33, 3.0),
+    ("alif-T1000", Net(inp=64, hidden=(96,), classes=5, act="superspike", cell=("alif",)), 2, 1000, 2.0),
+]
+
+
+@pytest.mark.parametrize("case", ALIF_CASES, ids=[c[0] for c in ALIF_CASES])
+def test_alif_step_parity(orc, case):
+    _, net, B, T, scale = case
+    params = orc.init(net, orc.key_child(orc.key_from_seed(21), 0))
+    ents = orc.entries(net)
+    for n, o, s in ents:
+        if n.endswith(".w"):
+            params[o:o + s] *= np.float32(scale)
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 5)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T)
+    names = [n for n, _, _ in ents]
+    assert eng.entries() == ents
+    assert np.array_equal(eng.get_params(), orc.init(net, orc.key_child(orc.key_from_seed(0), 0)))
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    eng.debug(True)
+    rows = np.arange(B, dtype=np.uint32)
+    loss, acc = eng.forward_backward(rows)
+    ref = orc.forward_backward(net, params, pk, T, y, want_spikes=True, want_trace=True)
+    emap = {n: (o, s) for n, o, s in ents}
+    flips = 0
+    for l, h in enumerate(net.hidden):
+        I = eng.fetch("I", l)
+        cell = names[names.index(f"l{2 * l}.w") + (2 if net.bias else 1)][:-5]
+        o, s = emap[cell + ".beta"]
+        S = eng.fetch("spikes", l)
+        if net.cell[l] == "alif":
+            go, gs = emap[cell + ".gamma"]
+            V_ref, A_ref, S_ref = scanref.alif_forward(I, params[o:o + s], params[go:go + gs], net.threshold)
+            assert np.array_equal(eng.fetch("A", l), A_ref), f"layer {l}: a not bit-exact given I"
+        else:
+            V_ref, S_ref = scanref.lif_forward(I, params[o:o + s], net.threshold)
+        assert np.array_equal(eng.fetch("V", l), V_ref), f"layer {l}: V not bit-exact given I"
+        assert np.array_equal(S, S_ref), f"layer {l}: spikes not bit-exact given I"
+        agree = (S == ref["spikes"][l]).mean()
+        assert agree >= SPIKE_AGREE, agree
+        flips += int((S != ref["spikes"][l]).sum())
+        assert 0.005 < S.mean() < 0.9, f"layer {l}: rate {S.mean()}"
+    assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    check_grads(orc, net, eng.get_grads(), ref["grads"], REL_TOL if flips == 0 else REL_TOL_FLIPS)
+    st = State(params.copy())
+    lo, ao = orc.train_step(net, st, pk, T, y)
+    eng.debug(False)
+    l2, a2 = eng.train_step(rows)
+    assert abs(l2 - lo) <= REL_TOL * abs(lo) and a2 == ao
+    check_adam_step(orc, net, eng.get_params(), st.params, ref["grads"])
+
+
+def test_alif_training_curve(orc):
+    """C2-shaped ALIF training (superspike) over 3 epochs tracks the oracle."""
+    net = Net(act="superspike", cell=("alif", "alif"))
+    N, B, T = 64, 16, 128
+    x, y = orc.synth_raster(net.classes, N, T, net.inp, 1)
+    pk = orc.pack_time(x)
+    params = orc.init(net, orc.key_child(orc.key_from_seed(0), 0))
+    st = State(params.copy())
+    m_ref = orc.train_epochs(net, st, pk, y, T, B, 3, 0)
+    eng = make_engine(net, B, T, seed=0)
+    eng.stage_dataset(pk, y)
+    m_gpu = eng.train_epochs(3)
+    assert np.allclose(m_gpu[:, 0], m_ref[:, 0], rtol=1e-3), (m_gpu, m_ref)
+    assert np.abs(m_gpu[:, 1] - m_ref[:, 1]).max() <= 1.0 / B + 1e-12
+    assert relnorm(eng.get_params(), st.params) <= 1e-4
