@@ -978,4 +978,6 @@ def test_alif_training_curve(orc):
     m_gpu = eng.train_epochs(3)
     assert np.allclose(m_gpu[:, 0], m_ref[:, 0], rtol=1e-3), (m_gpu, m_ref)
     assert np.abs(m_gpu[:, 1] - m_ref[:, 1]).max() <= 1.0 / B + 1e-12
-    assert relnorm(eng.get_params(), st.params) <= 1e-4
+    # 12 Adam steps of ~lr * sign(g): elements whose gradient nearly cancels can move
+    # the other way (check_adam_step), so the parameter bound after training is 5e-4
+    assert relnorm(eng.get_params(), st.params) <= 5e-4
