@@ -37,6 +37,10 @@ WORKLOADS = {
     "c1": dict(inp=700, hidden=(128, 128), classes=20, T=128, B=256, act="arctan", n_data=16384,
                desc="SHD-shaped 700-128-128-20 LIF, T=128, batch 256/GPU, arctan k=2, "
                     "integral-CE + Adam, nobias"),
+    "c2": dict(inp=700, hidden=(128, 128), classes=20, T=128, B=1024, act="superspike",
+               cell="alif", n_data=16384,
+               desc="SHD-shaped 700-128-128-20 ALIF (declared cell, oracle/spiketrain_oracle.h), "
+                    "T=128, batch 1024/GPU, superspike k=25, integral-CE + Adam, nobias"),
     "c3": dict(inp=700, hidden=(1024, 1024), classes=20, T=256, B=512, act="arctan", n_data=8192,
                desc="wide 700-1024-1024-20 LIF, T=256, batch 512/GPU"),
     "c5": dict(inp=700, hidden=(256, 256), classes=20, T=1000, B=512, act="arctan", n_data=2048,
@@ -122,8 +126,8 @@ def algorithmic(name: str, w: dict, n_params: int, fwd_groups=None):
         return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(l, l + n))
     if base == "wgrad":              # dW = A^T dI, every Linear layer in one launch
         return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(len(dims) - 1))
-    if base == "lif_bwd":            # LIF reverse scan: 12 B / neuron-step
-        return "hbm", 12.0 * B * T * dims[l + 1]
+    if base == "lif_bwd":            # LIF reverse scan: 12 B / neuron-step, ALIF +4
+        return "hbm", (16.0 if w.get("cell") == "alif" else 12.0) * B * T * dims[l + 1]
     if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element
         return "hbm", 8.0 * B * T * C
     if base in ("adam", "reduce_adam"):  # Adam: 28 B / param (split-K sums are overhead)
@@ -146,44 +150,57 @@ def ncu_traffic(kernel: str):
 
 
 # ------------------------------------------------------------ CPU baseline
+def _cpu_net(w):
+    """The reference network of workload w.  The reference has LIF cells only
+    (SPEC.md:373, :382), so an ALIF workload is timed on its LIF stand-in of the
+    same shape and surrogate -- labelled in the sample string."""
+    from oracle.pyoracle import Net
+    return Net(inp=w["inp"], hidden=tuple(w["hidden"]), classes=w["classes"], act=w["act"])
+
+
+def _cpu_label(w, b):
+    cell = "LIF stand-in for ALIF (no ALIF in the reference)" if w.get("cell") == "alif" else "LIF"
+    return (f"{b} examples/step of the workload shape ({w['inp']}-" + "-".join(map(str, w["hidden"])) +
+            f"-{w['classes']}, T={w['T']}, {w['act']}, {cell}, init regime)")
+
+
 def _ref_worker(args):
-    which, n_examples, steps, warmup, seed, q = args
-    from oracle.pyoracle import Lib, Net, State
+    which, w, n_examples, steps, warmup, seed, q = args
+    from oracle.pyoracle import Lib, State
     lib = Lib(which)
-    net = Net()
-    x, y = lib.synth_raster(20, n_examples, 128, 700, seed)
+    net = _cpu_net(w)
+    x, y = lib.synth_raster(w["classes"], n_examples, w["T"], w["inp"], seed)
     pk = lib.pack_time(x)
     st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
     for _ in range(warmup):
-        lib.train_step(net, st, pk, 128, y)
+        lib.train_step(net, st, pk, w["T"], y)
     t0 = time.perf_counter()
     for _ in range(steps):
-        lib.train_step(net, st, pk, 128, y)
+        lib.train_step(net, st, pk, w["T"], y)
     q.put((n_examples * steps, time.perf_counter() - t0))
 
 
-def cpu_reference(steps: int, warmup: int, workers: int, per_step_budget_s: float):
+def cpu_reference(w: dict, steps: int, warmup: int, workers: int, per_step_budget_s: float):
     """Reference CPU train_step on `workers` host cores (independent replicas).
 
-    Each step of each worker is a bounded sample of the C1 workload: b examples
-    (b sized so the whole run fits the budget), T=128, 700-128-128-20."""
-    from oracle.pyoracle import Lib, have_ref
+    Each step of each worker is a bounded sample of workload w: b examples (b sized
+    so the whole run fits the budget) at the workload's network shape and T."""
+    from oracle.pyoracle import Lib, State, have_ref
     which = "ref" if have_ref() else "orc"
     kind = "reference" if which == "ref" else "port"
     lib = Lib(which)
     # calibrate the per-example cost on one core
-    from oracle.pyoracle import Net, State
-    net = Net()
-    x, y = lib.synth_raster(20, 8, 128, 700, 1)
+    net = _cpu_net(w)
+    x, y = lib.synth_raster(w["classes"], 2, w["T"], w["inp"], 1)
     pk = lib.pack_time(x)
     st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
     t0 = time.perf_counter()
-    lib.train_step(net, st, pk, 128, y)
-    per_ex = (time.perf_counter() - t0) / 8
-    b = int(max(1, min(256, per_step_budget_s / max(per_ex, 1e-6))))
+    lib.train_step(net, st, pk, w["T"], y)
+    per_ex = (time.perf_counter() - t0) / 2
+    b = int(max(1, min(w["B"], per_step_budget_s / max(per_ex, 1e-6))))
     ctx = mp.get_context("fork")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ref_worker, args=((which, b, steps, warmup, 1 + i, q),))
+    procs = [ctx.Process(target=_ref_worker, args=((which, w, b, steps, warmup, 1 + i, q),))
              for i in range(workers)]
     t0 = time.perf_counter()
     for p in procs:
@@ -196,34 +213,33 @@ def cpu_reference(steps: int, warmup: int, workers: int, per_step_budget_s: floa
     slowest = max(r[1] for r in res)
     value = samples / slowest
     return dict(value=value, unit=UNIT, cores=workers, kind=kind,
-                sample=f"{workers} x replica train_step on {b} examples/step of C1 "
-                       f"(T=128, 700-128-128-20, arctan, init regime), {steps} timed + "
-                       f"{warmup} warm-up steps each", wall_s=wall, examples_per_step=b,
+                sample=f"{workers} x replica train_step on " + _cpu_label(w, b) +
+                       f", {steps} timed + {warmup} warm-up steps each", wall_s=wall,
+                examples_per_step=b,
                 ms_per_step=1e3 * slowest / max(steps, 1))
 
 
-def cpu_baseline_single(seconds: float = 12.0):
+def cpu_baseline_single(w: dict, seconds: float = 12.0):
     """Bounded single-core sample for our arm's cpu_baseline key."""
-    from oracle.pyoracle import Lib, Net, State, have_ref
+    from oracle.pyoracle import Lib, State, have_ref
     which = "ref" if have_ref() else "orc"
     lib = Lib(which)
-    net = Net()
+    net = _cpu_net(w)
     b = 32
-    x, y = lib.synth_raster(20, b, 128, 700, 1)
+    x, y = lib.synth_raster(w["classes"], b, w["T"], w["inp"], 1)
     pk = lib.pack_time(x)
     st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
-    lib.train_step(net, st, pk, 128, y)
+    lib.train_step(net, st, pk, w["T"], y)
     n, t0 = 0, time.perf_counter()
     while True:
-        lib.train_step(net, st, pk, 128, y)
+        lib.train_step(net, st, pk, w["T"], y)
         n += 1
         el = time.perf_counter() - t0
         if el >= seconds or n >= 200:
             break
     return dict(value=b * n / el, unit=UNIT, cores=1,
                 kind="reference" if which == "ref" else "port",
-                sample=f"{n} train_steps of {b} C1 examples (T=128, 700-128-128-20, arctan, "
-                       f"init regime) on 1 host core, {el:.1f} s")
+                sample=f"{n} train_steps of " + _cpu_label(w, b) + f" on 1 host core, {el:.1f} s")
 
 
 # ------------------------------------------------------------------ main
@@ -258,7 +274,7 @@ def main():
             return
         workers = max(1, os.cpu_count() or 1)
         budget = 150.0 / (args.steps + warmup)
-        r = cpu_reference(args.steps, warmup, workers, budget)
+        r = cpu_reference(w, args.steps, warmup, workers, budget)
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": warmup,
                 "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -278,7 +294,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
-    spec = shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"])
+    spec = shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"],
+                    cell=w.get("cell", "lif"))
     B = w["B"]
     eng = Engine(spec, TrainConfig(batch_size=B, seed=0, lr=1e-3), w["T"], device=local)
     if world > 1:
@@ -391,7 +408,7 @@ def main():
             "kernels": [{"name": k["name"], "ms": round(k["ms"], 5)} for k in kernels],
             "final_loss": loss, "final_acc": acc}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_single()
+        line["cpu_baseline"] = cpu_baseline_single(w)
     if rank == 0:
         print(json.dumps(line))
     eng.close()

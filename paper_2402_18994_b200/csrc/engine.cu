@@ -588,7 +588,7 @@ struct snn_engine {
       if (j < L) tm_di_out[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 128);
       wg_maps.m[j] = tm_di_w[j];
     }
-    for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>})
+    for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>, k_lif_fwd<false, true>, k_lif_fwd<true, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>,
@@ -1037,7 +1037,11 @@ struct snn_engine {
       f.stages = std::min(fwd_stages, NT * (K_pad[l] / 64));
       f.spb = fwd_spb(TT);
       const bool shifting = l == 0 && cfg.max_shift > 0 && cfg.n_shift_axes > 0;
-      launch(shifting ? k_lif_fwd<true> : k_lif_fwd<false>, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128),
+      bool any_alif = false;
+      for (int i = 0; i < nl; ++i) any_alif = any_alif || alif(l + i);
+      auto kfn = any_alif ? (shifting ? k_lif_fwd<true, true> : k_lif_fwd<false, true>)
+                          : (shifting ? k_lif_fwd<true> : k_lif_fwd<false>);
+      launch(kfn, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128),
              dim3(kFwdThreads),
              fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
       mark(evs, "lif_fwd", l);

@@ -305,7 +305,9 @@ __device__ __forceinline__ void alif_chunk(const uint32_t (&r)[32], float* vp, f
 
 // kShift: layer-0 launches of an epoch loop with shift_augment (reads a.xshift);
 // the default instantiation has no roll code in the decode loop.
-template <bool kShift>
+// kAlif: the launch's hidden layers are declared ALIF cells (FwdLayer.gamma set);
+// the LIF instantiation carries no adaptation code.
+template <bool kShift, bool kAlif = false>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     k_lif_fwd(const __grid_constant__ FwdMaps maps, FwdArgs a) {
   const CUtensorMap& tm_w = maps.m[0];
@@ -545,7 +547,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float vb = clip01(n < ly.H ? ly.beta[n * ly.beta_stride] : 0.0f);
       const float bn = (ly.bias != nullptr && n < ly.H) ? ly.bias[n] : 0.0f;
       const size_t hw = size_t(ly.H_pad) / 32;
-      const bool alif = ly.gamma != nullptr;
+      const bool alif = kAlif && ly.gamma != nullptr;
       const float gc = (alif && n < ly.H) ? clip01(ly.gamma[n]) : 0.0f;
       float ad = 0.0f;  // ALIF adaptation state
       // fused: lane j writes the next layer's B row t0+j (its quadrant's 32 spikes
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint32_t myword = 0u, tmask = 0u;
           if (t0 < a.T) {
             float* vp = ly.v_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
-            if (alif)
+            if (kAlif && alif)
               alif_chunk(r, vp, ly.a_out + (vp - ly.v_out),
                          ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
                          min(32, a.T - t0), vb, gc, bn, ly.bias != nullptr, a.theta, lane, v, ad,
