@@ -32,9 +32,9 @@ class _Net(C.Structure):
                 ("beta_mode", C.c_int * 9), ("fixed_beta", C.c_float * 9),
                 ("monitor", C.c_int * 8), ("cell", C.c_int * 8)]
 
-# hidden cell kinds: "lif" (neuron.hpp:127-136) | "alif" (declared restatement,
-# spiketrain_oracle.h -- not in the reference)
-CELLS = {"lif": 0, "alif": 1}
+# hidden cell kinds: "lif" (neuron.hpp:127-136) | "alif" | "rlif" (declared
+# restatements, spiketrain_oracle.h -- not in the reference)
+CELLS = {"lif": 0, "alif": 1, "rlif": 2}
 
 BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
 

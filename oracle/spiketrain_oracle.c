@@ -129,10 +129,15 @@ void orc_unpack_time(const uint8_t* packed, size_t n, size_t t, size_t f,
  * then readout w, [b], beta.  Normalised ids: Linear 2j, cell 2j+1.        */
 
 static int is_alif(const orc_net* net, int l) { return l < net->n_hidden && net->cell[l] == 1; }
+static int is_rlif(const orc_net* net, int l) { return l < net->n_hidden && net->cell[l] == 2; }
+/* the declared cells' extra entry after beta: ALIF gamma [h], RLIF rec [h][h] */
+static size_t extra_size(const orc_net* net, int l, size_t h) {
+  return is_alif(net, l) ? h : is_rlif(net, l) ? h * h : 0;
+}
 
 int orc_entry_count(const orc_net* net) {
   int n = (net->n_hidden + 1) * (net->bias ? 3 : 2);
-  for (int l = 0; l < net->n_hidden; ++l) n += is_alif(net, l);
+  for (int l = 0; l < net->n_hidden; ++l) n += extra_size(net, l, 1) ? 1 : 0;
   return n;
 }
 
@@ -162,12 +167,12 @@ void orc_entry_layout(const orc_net* net, size_t* offsets, size_t* sizes,
   int e = 0;
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    const size_t sz[4] = {k * h, h, beta_size(net, l, h), h};
-    const char* leaf[4] = {"w", "b", "beta", "gamma"};
+    const size_t sz[4] = {k * h, h, beta_size(net, l, h), extra_size(net, l, h)};
+    const char* leaf[4] = {"w", "b", "beta", is_rlif(net, l) ? "rec" : "gamma"};
     const int lid[4] = {lin_id(net, l), lin_id(net, l), lin_id(net, l) + 1, lin_id(net, l) + 1};
     for (int q = 0; q < 4; ++q) {
       if (q == 1 && !net->bias) continue;
-      if (q == 3 && !is_alif(net, l)) continue;
+      if (q == 3 && !sz[3]) continue;
       if (offsets) offsets[e] = off;
       if (sizes) sizes[e] = sz[q];
       if (names) snprintf(names[e], 16, "l%d.%s", lid[q], leaf[q]);
@@ -181,13 +186,14 @@ size_t orc_param_count(const orc_net* net) {
   size_t n = 0;
   for (int l = 0; l <= net->n_hidden; ++l) {
     const size_t k = (size_t)layer_in(net, l), h = (size_t)layer_out(net, l);
-    n += k * h + beta_size(net, l, h) + (net->bias ? h : 0) + (is_alif(net, l) ? h : 0);
+    n += k * h + beta_size(net, l, h) + (net->bias ? h : 0) + extra_size(net, l, h);
   }
   return n;
 }
 
 typedef struct {
-  size_t w, b, beta, gamma; /* offsets; b == SIZE_MAX when no bias, gamma when not ALIF */
+  size_t w, b, beta, gamma; /* offsets; b == SIZE_MAX when no bias, gamma (ALIF gamma or
+                               RLIF rec) when the cell has no extra entry */
 } layer_off;
 
 static void layer_offsets(const orc_net* net, layer_off* lo) {
@@ -205,9 +211,9 @@ static void layer_offsets(const orc_net* net, layer_off* lo) {
     lo[l].beta = off;
     off += beta_size(net, l, h);
     lo[l].gamma = (size_t)-1;
-    if (is_alif(net, l)) {
+    if (extra_size(net, l, h)) {
       lo[l].gamma = off;
-      off += h;
+      off += extra_size(net, l, h);
     }
   }
 }
@@ -231,6 +237,9 @@ void orc_init(const orc_net* net, uint64_t key, float* params) {
                            params + lo[l].beta);
     if (is_alif(net, l)) /* declared ALIF: gamma ~ TN(0.5, 0.25) from child 3 */
       orc_truncated_normal(orc_key_child(lk_cell, 3), h, 0.5f, 0.25f, params + lo[l].gamma);
+    if (is_rlif(net, l)) /* declared RLIF: rec ~ TN(0, 1/sqrt(h)) from child 4 */
+      orc_truncated_normal(orc_key_child(lk_cell, 4), h * h, 0.0f, 1.0f / sqrtf((float)h),
+                           params + lo[l].gamma);
   }
 }
 
@@ -374,7 +383,41 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
     vst[l] = (float*)malloc(M * H * sizeof(float));
     const float* beta = params + lo[l].beta;
     const size_t bs = net->beta_mode[l] == 0 ? 1 : 0; /* scalar beta broadcasts */
-    if (is_alif(net, l)) {
+    if (is_rlif(net, l)) {
+      /* declared RLIF (spiketrain_oracle.h): every neuron's spike of step t first,
+       * then fb_j = sum_i s_i rec[i][j] over spiking i ascending (a zero-skip
+       * matmul row, ops.hpp:163-172), v' = (((v bc) + I) + fb) - s theta */
+      const float* rec = params + lo[l].gamma;
+      float* vv = (float*)malloc(H * sizeof(float));
+      float* fb = (float*)malloc(H * sizeof(float));
+      for (size_t b = 0; b < B; ++b) {
+        for (size_t n = 0; n < H; ++n) vv[n] = 0.0f;
+        for (size_t t = 0; t < T; ++t) {
+          const size_t row = (b * T + t) * H;
+          for (size_t n = 0; n < H; ++n) {
+            vst[l][row + n] = vv[n];
+            const float pre = vv[n] + (-theta);
+            act[l + 1][row + n] = pre >= 0.0f ? 1.0f : 0.0f;
+            fb[n] = 0.0f;
+          }
+          for (size_t i = 0; i < H; ++i) {
+            if (act[l + 1][row + i] == 0.0f) continue;
+            const float* ri = rec + i * H;
+            for (size_t j = 0; j < H; ++j) fb[j] += ri[j];
+          }
+          for (size_t n = 0; n < H; ++n) {
+            const float vb = clip01(beta[n * bs]);
+            const float m = vv[n] * vb;
+            const float ai = m + cur[row + n];
+            const float af = ai + fb[n];
+            const float r = act[l + 1][row + n] * theta;
+            vv[n] = af - r;
+          }
+        }
+      }
+      free(vv);
+      free(fb);
+    } else if (is_alif(net, l)) {
       /* declared ALIF (spiketrain_oracle.h): threshold theta + a, reset by it */
       const float* gam = params + lo[l].gamma;
       ast[l] = (float*)malloc(M * H * sizeof(float));
@@ -613,7 +656,46 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
       const size_t bs = mode == 0 ? 1 : 0;
       const float* V = vst[hl];
       float* dIh = (float*)malloc(M * H * sizeof(float));
-      if (is_alif(net, hl)) {
+      if (is_rlif(net, hl)) {
+        /* declared RLIF reverse, per sample, t descending (G = d/dv_{t+1}):
+         *   dI_t = G ; rc_i = sum_j rec[i][j] G_j (j ascending)
+         *   gs = (dS + (-G) theta) + rc ; G' = G bc + gs g(v_t - theta)
+         *   drec[i][j] += s_i(t) G_j (b, t ascending after the sweep: the
+         *   spikes x dI product of the layer with itself, like matmul_tn) */
+        const float* rec = params + lo[hl].gamma;
+        float* grec = grads + lo[hl].gamma;
+        const float* Sx = act[hl + 1];
+        float* G = (float*)malloc(H * sizeof(float));
+        float* G2 = (float*)malloc(H * sizeof(float));
+        for (size_t b = 0; b < B; ++b) {
+          for (size_t n = 0; n < H; ++n) G[n] = 0.0f;
+          for (size_t t = T; t-- > 0;) {
+            const size_t row = (b * T + t) * H;
+            for (size_t i = 0; i < H; ++i) {
+              dIh[row + i] = G[i];
+              const float* ri = rec + i * H;
+              float rc = 0.0f;
+              for (size_t j = 0; j < H; ++j) rc += ri[j] * G[j];
+              const float vb = clip01(beta[i * bs]);
+              const float gs = (dS[row + i] + (-G[i]) * theta) + rc;
+              const float pre = V[row + i] + (-theta);
+              G2[i] = G[i] * vb + gs * surrogate(net, pre);
+            }
+            for (size_t i = 0; i < H; ++i) G[i] = G2[i];
+          }
+        }
+        for (size_t r = 0; r < M; ++r) {
+          const float* sr = Sx + r * H;
+          const float* gr = dIh + r * H;
+          for (size_t i = 0; i < H; ++i) {
+            if (sr[i] == 0.0f) continue;
+            float* o = grec + i * H;
+            for (size_t j = 0; j < H; ++j) o[j] += gr[j];
+          }
+        }
+        free(G);
+        free(G2);
+      } else if (is_alif(net, hl)) {
         /* declared ALIF reverse: gv = d/dv_{t+1}, ga = d/da_{t+1}, t descending.
          *   dI_t = gv ; gs = (dS + (-gv) th) + ga (1 - gc) ; gp = gs g(pre)
          *   gv' = gv bc + gp ; ga' = ((ga gc) - gp) - s gv

@@ -65,7 +65,7 @@ typedef struct orc_net {
    * monitor takes a normalised layer id, so every later layer's id -- its
    * init key child(id) and entry names -- moves up by one.                 */
   int monitor[ORC_MAX_HIDDEN];
-  /* Cell kind of hidden layer l: 0 LIF (neuron.hpp:127-136), 1 ALIF.
+  /* Cell kind of hidden layer l: 0 LIF (neuron.hpp:127-136), 1 ALIF, 2 RLIF.
    *
    * ALIF is NOT in the reference: this is a
    * DECLARED restatement -- parity unpinned against the reference.  It follows
@@ -78,7 +78,17 @@ typedef struct orc_net {
    * initialised TN(0.5, 0.25, +-2 sigma) from child(cell_key, 3) (beta uses
    * child 2).  The backward is the exact reverse of these ops (surrogate on pre,
    * reset and threshold paths differentiated); tests/test_alif_oracle.py pins it
-   * against torch autograd of the same forward.                            */
+   * against torch autograd of the same forward.
+   *
+   * RLIF is likewise NOT in the reference (feed-forward only, network.hpp:16,
+   * SPEC.md:382, :456): a DECLARED restatement of Spyx's recurrent LIF in the
+   * reference's LIF op order -- parity unpinned against the reference:
+   *   pre = v - theta ; s = [pre >= 0] ; fb_j = sum_i s_i rec[i][j]
+   *   v' = (((v * bc) + I) + fb) - s * theta
+   * fb sums the rows of the spiking neurons in ascending i (the zero-skip
+   * matmul order, ops.hpp:163-172).  Entry "l{id}.rec" [H][H] (row = source
+   * neuron) after "l{id}.beta", init TN(0, 1/sqrt(H), +-2 sigma) from
+   * child(cell_key, 4).  Pinned against torch autograd like ALIF.          */
   int cell[ORC_MAX_HIDDEN];
 } orc_net;
 

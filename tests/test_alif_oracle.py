@@ -1,6 +1,7 @@
-"""Pins the oracle's DECLARED ALIF cell (CPU only).
+"""Pins the oracle's DECLARED ALIF and RLIF cells (CPU only).
 
-ALIF is not in the reference, so there is no
+ALIF and RLIF are not in the reference,
+so there is no
 reference output to pin it to.  The oracle's restatement
 (oracle/spiketrain_oracle.h, `cell`) is pinned instead against an independent
 derivation: torch autograd (float64) of the same declared forward equations,
@@ -61,8 +62,10 @@ def _autograd(net: Net, entries, params, x, y, k, aux):
             cur = cur + P[lin + ".b"]
         beta = P[cell + ".beta"]
         bc = torch.clamp(beta, 0.0, 1.0).expand(h) if beta.numel() == 1 else torch.clamp(beta, 0.0, 1.0)
-        alif = (net.cell + ("lif",) * 8)[l] == "alif"
+        kind = (net.cell + ("lif",) * 8)[l]
+        alif = kind == "alif"
         gc = torch.clamp(P[cell + ".gamma"], 0.0, 1.0) if alif else None
+        rec = P[cell + ".rec"].reshape(h, h) if kind == "rlif" else None
         v = torch.zeros(B, h, dtype=torch.float64)
         a = torch.zeros(B, h, dtype=torch.float64)
         out = []
@@ -70,6 +73,8 @@ def _autograd(net: Net, entries, params, x, y, k, aux):
             th = net.threshold + a if alif else torch.full_like(v, net.threshold)
             s = _Spike.apply(v - th, net.act, k, aux)
             v = v * bc + cur[:, t] - s * th
+            if rec is not None:
+                v = v + s @ rec
             if alif:
                 a = a * gc + (1.0 - gc) * s
             out.append(s)
@@ -99,6 +104,9 @@ CASES = [
     dict(hidden=(24, 16), cell=("alif", "lif"), act="arctan", bias=True),
     dict(hidden=(20,), cell=("alif",), act="triangular", beta_mode=("scalar", "per_neuron")),
     dict(hidden=(16, 16, 12), cell=("lif", "alif", "alif"), act="boxcar", threshold=0.8),
+    dict(hidden=(24, 16), cell=("rlif", "rlif"), act="superspike"),
+    dict(hidden=(20, 18), cell=("rlif", "lif"), act="arctan", bias=True, beta_mode=("scalar",)),
+    dict(hidden=(16, 16, 12), cell=("alif", "rlif", "lif"), act="triangular"),
 ]
 
 
@@ -111,7 +119,7 @@ def test_alif_oracle_matches_autograd(orc, case):
     x = (rng.random((B, T, net.inp)) < 0.25).astype(np.uint8)
     y = rng.integers(0, net.classes, B).astype(np.int64)
     entries = orc.entries(net)
-    assert any(n.endswith(".gamma") for n, _, _ in entries)
+    assert any(n.endswith((".gamma", ".rec")) for n, _, _ in entries)
     params = orc.init(net, orc.key_child(orc.key_from_seed(case), 0))
     # louder weights so every layer spikes (and adapts) at a healthy rate
     for n, o, s in entries:
@@ -129,7 +137,7 @@ def test_alif_oracle_matches_autograd(orc, case):
         gr, go = g[o:o + s], ref["grads"][o:o + s].astype(np.float64)
         den = max(np.linalg.norm(gr), 1e-8)
         assert np.linalg.norm(go - gr) / den <= 2e-5, (n, np.linalg.norm(go - gr) / den)
-    gam = [o for n, o, s in entries if n.endswith(".gamma")]
+    gam = [o for n, o, s in entries if n.endswith((".gamma", ".rec"))]
     assert any(np.abs(ref["grads"][o:o + 4]).max() > 0 for o in gam)
 
 
@@ -171,5 +179,43 @@ def test_alif_without_adaptation_is_lif(orc):
     assert np.array_equal(a["spikes"][0], b["spikes"][0])
     for n, o, s in ea:
         if not n.endswith(".gamma"):
+            lo, ls = el[n]
+            assert np.array_equal(a["grads"][o:o + s], b["grads"][lo:lo + ls]), n
+
+
+def test_rlif_entries_and_init(orc):
+    net = Net(inp=10, hidden=(8, 6), classes=3, cell=("lif", "rlif"))
+    e = orc.entries(net)
+    assert [(n, sz) for n, _, sz in e] == [("l0.w", 80), ("l1.beta", 8), ("l2.w", 48), ("l3.beta", 6),
+                                          ("l3.rec", 36), ("l4.w", 18), ("l5.beta", 3)]
+    p = orc.init(net, 77)
+    cell_key = orc.key_child(77, 3)
+    _, o, s = e[4]
+    assert np.array_equal(p[o:o + s], orc.truncated_normal(orc.key_child(cell_key, 4), 36, 0.0,
+                                                          np.float32(1.0) / np.sqrt(np.float32(6))))
+
+
+def test_rlif_zero_recurrence_is_lif(orc):
+    """rec = 0 makes RLIF the reference LIF bit for bit (fb = 0 adds exactly)."""
+    lif = Net(inp=30, hidden=(16,), classes=4)
+    rl = Net(inp=30, hidden=(16,), classes=4, cell=("rlif",))
+    B, T = 5, 25
+    rng = np.random.default_rng(8)
+    pk = orc.pack_time((rng.random((B, T, 30)) < 0.3).astype(np.uint8))
+    y = rng.integers(0, 4, B).astype(np.int64)
+    p = orc.init(lif, 5) * np.float32(2.5)
+    el = {n: (o, s) for n, o, s in orc.entries(lif)}
+    pr = np.zeros(orc.param_count(rl), np.float32)
+    er = orc.entries(rl)
+    for n, o, s in er:
+        if n in el:
+            lo, ls = el[n]
+            pr[o:o + s] = p[lo:lo + ls]
+    a = orc.forward_backward(rl, pr, pk, T, y, want_spikes=True)
+    b = orc.forward_backward(lif, p, pk, T, y, want_spikes=True)
+    assert a["loss"] == b["loss"]
+    assert np.array_equal(a["spikes"][0], b["spikes"][0])
+    for n, o, s in er:
+        if n in el:
             lo, ls = el[n]
             assert np.array_equal(a["grads"][o:o + s], b["grads"][lo:lo + ls]), n
