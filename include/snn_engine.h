@@ -85,7 +85,11 @@ typedef struct snn_network_desc {
   int32_t cell[SNN_MAX_HIDDEN];
 } snn_network_desc;
 
-typedef enum snn_cell { SNN_CELL_LIF = 0, SNN_CELL_ALIF = 1 } snn_cell;
+/* SNN_CELL_RLIF is likewise DECLARED (the reference is feed-forward only, network.hpp:16,
+ * SPEC.md:382): pre = v - theta, s = [pre >= 0], fb_j = sum_i s_i rec[i][j] (spiking i
+ * ascending), v' = (((v*clip01(beta)) + I) + fb) - s*theta, with an entry "l{id}.rec"
+ * [H][H] after "l{id}.beta" (init TN(0, 1/sqrt(H)) from child(cell_key, 4)); H <= 1024. */
+typedef enum snn_cell { SNN_CELL_LIF = 0, SNN_CELL_ALIF = 1, SNN_CELL_RLIF = 2 } snn_cell;
 
 /* TrainConfig subset that reaches the step (optimize.hpp:116-133). */
 typedef struct snn_train_config {

@@ -6,7 +6,7 @@ the reference interface used by the tests and bench.py.
 """
 from .engine import (  # noqa: F401
     ActivationDesc, ALIFLayer, ArgumentError, ConfigError, ContractError, DeviceError, Engine, Error,
-    FormatError, IoError, LIFLayer, LILayer, LinearLayer, MonitorLayer, NetworkSpec, ShapeError,
+    FormatError, IoError, LIFLayer, LILayer, LinearLayer, MonitorLayer, NetworkSpec, RLIFLayer, ShapeError,
     SpecError,
     StateError, TrainConfig, UnsupportedError, default_activation_desc, lib, normalize,
     shd_spec, train_step,

@@ -281,6 +281,10 @@ struct snn_engine {
   // activations
   DevBuf<float> V[SNN_MAX_HIDDEN];
   DevBuf<float> Aad[SNN_MAX_HIDDEN], dgamma[SNN_MAX_HIDDEN];  // ALIF adaptation trace, d gamma partials
+  // RLIF: projection I, dS, and the f32 transpose of rec per layer; the rec weight
+  // gradient is an extra wgrad layer j = rec_j[l] in [L+1, NJ) (rec_l[j] = l)
+  DevBuf<float> Ibuf[SNN_MAX_HIDDEN], dsbuf[SNN_MAX_HIDDEN], rec_t[SNN_MAX_HIDDEN];
+  int NJ = 0, rec_j[SNN_MAX_HIDDEN]{}, rec_l[kMaxLayers]{};
   DevBuf<uint32_t> s_np[SNN_MAX_HIDDEN], s_tp[SNN_MAX_HIDDEN];
   DevBuf<__nv_bfloat16> di[kMaxLayers];  // per Linear j: dI of its output
   DevBuf<float> dbeta[kMaxLayers], dbias[kMaxLayers];
@@ -393,7 +397,8 @@ struct snn_engine {
     for (int l = 0; l <= n.n_hidden; ++l)
       if (n.beta_mode[l] < 0 || n.beta_mode[l] > 2) fail(SNN_ERR_ARGUMENT, "unknown beta mode");
     for (int l = 0; l < SNN_MAX_HIDDEN; ++l)
-      if (n.cell[l] != SNN_CELL_LIF && (n.cell[l] != SNN_CELL_ALIF || l >= n.n_hidden))
+      if (n.cell[l] != SNN_CELL_LIF &&
+          ((n.cell[l] != SNN_CELL_ALIF && n.cell[l] != SNN_CELL_RLIF) || l >= n.n_hidden))
         fail(SNN_ERR_SPEC, "hidden layer %d: unknown cell kind %d", l, n.cell[l]);
     if (n.activation == SNN_ACT_BOXCAR && !(n.aux > 0.0f))
       fail(SNN_ERR_ARGUMENT, "boxcar: width and height must be positive");
@@ -446,6 +451,21 @@ struct snn_engine {
       M_pad_w[j] = rup(K[j], 128);
       n_tile_w[j] = j < L ? 128 : 64;
     }
+    // declared RLIF cells: d rec = S_l^T dI_l is one more weight-gradient layer
+    NJ = L + 1;
+    for (int l = 0; l < L; ++l) {
+      rec_j[l] = -1;
+      if (!rlif(l)) continue;
+      if (NJ >= kMaxLayers) fail(SNN_ERR_UNSUPPORTED, "too many RLIF layers for %d hidden", L);
+      if (H_pad[l] > 1024) fail(SNN_ERR_UNSUPPORTED, "RLIF layer %d: width %d > 1024", l, H[l]);
+      const int j = NJ++;
+      rec_j[l] = j;
+      rec_l[j] = l;
+      K[j] = N[j] = H[l];
+      K_pad[j] = N_pad[j] = H_pad[l];
+      M_pad_w[j] = rup(H[l], 128);
+      n_tile_w[j] = 128;
+    }
     const size_t ro_smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
     if (ro_smem > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "readout working set too large");
     if (size_t(T) * C * 4 > 200 * 1024) fail(SNN_ERR_UNSUPPORTED, "T * classes too large");
@@ -470,7 +490,7 @@ struct snn_engine {
       wg_mg_max = std::min(wg_mg_max, env_int("SNN_WG_MG", kWgMgMax));  // M-tiles per CTA cap
       double fixed[kMaxLayers], per_unit[kMaxLayers], units[kMaxLayers];
       const double iters = double(B) * (T_pad / 64);
-      for (int j = 0; j <= L; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         const int m_tiles = M_pad_w[j] / 128, n_tiles = N_pad[j] / n_tile_w[j];
         // mg: TMEM columns (mg * n_tile <= 512), the 2-stage smem cap, and the epilogue
         // staging of mg f32 tiles (mg * 128 padded rows) within the budget
@@ -494,16 +514,16 @@ struct snn_engine {
         return std::max(1, std::min(B, int(std::ceil(per_unit[j] / room))));
       };
       double lo = 0, hi = 1e12;
-      for (int j = 0; j <= L; ++j) lo = std::max(lo, fixed[j]);
+      for (int j = 0; j < NJ; ++j) lo = std::max(lo, fixed[j]);
       for (int rep = 0; rep < 100; ++rep) {
         const double mid = 0.5 * (lo + hi);
         double ctas = 0;
-        for (int j = 0; j <= L; ++j) ctas += units[j] * splits_for(mid, j);
+        for (int j = 0; j < NJ; ++j) ctas += units[j] * splits_for(mid, j);
         if (ctas <= sms) hi = mid; else lo = mid;
       }
-      for (int j = 0; j <= L; ++j) splits_w[j] = splits_for(hi, j);
+      for (int j = 0; j < NJ; ++j) splits_w[j] = splits_for(hi, j);
       if (const char* v = std::getenv("SNN_WG_SPLIT_SAMPLES"))
-        for (int j = 0; j <= L; ++j) splits_w[j] = std::max(1, B / std::max(1, std::atoi(v)));
+        for (int j = 0; j < NJ; ++j) splits_w[j] = std::max(1, B / std::max(1, std::atoi(v)));
     }
     // parameter entries (network.hpp:210-226 order)
     entries.clear();
@@ -525,6 +545,11 @@ struct snn_engine {
       if (alif(j)) {  // declared ALIF cell: adaptation decay after beta (oracle/spiketrain_oracle.h)
         entries.push_back({"l" + std::to_string(cell) + ".gamma", kEntryGamma, j, 1, N[j], off, size_t(N[j])});
         off += N[j];
+      }
+      if (rlif(j)) {  // declared RLIF cell: recurrent weight [H][H] after beta (a W of layer rec_j)
+        entries.push_back({"l" + std::to_string(cell) + ".rec", kEntryW, rec_j[j], N[j], N[j], off,
+                           size_t(N[j]) * N[j]});
+        off += size_t(N[j]) * N[j];
       }
     }
     n_params = off;
@@ -550,6 +575,11 @@ struct snn_engine {
       if (alif(l)) {
         Aad[l].alloc(rows * H_pad[l], false);
         dgamma[l].alloc(size_t(B) * H[l]);
+      }
+      if (rlif(l)) {
+        Ibuf[l].alloc(rows * H_pad[l], false);
+        dsbuf[l].alloc(rows * H_pad[l], false);
+        rec_t[l].alloc(size_t(H[l]) * H_pad[l]);
       }
       s_np[l].alloc(rows * (H_pad[l] / 32));
       s_tp[l].alloc(size_t(H_pad[l]) * (rows / 32));
@@ -588,12 +618,19 @@ struct snn_engine {
       if (j < L) tm_di_out[j] = make_map(di[j].p, uint64_t(3) * N_pad[j], rows, 128);
       wg_maps.m[j] = tm_di_w[j];
     }
+    for (int j = L + 1; j < NJ; ++j) {
+      partial[j].alloc(size_t(splits_w[j]) * M_pad_w[j] * N_pad[j], false);
+      wg_maps.m[j] = tm_di_w[rec_l[j]];  // d rec: the RLIF layer's own dI planes
+    }
     for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>, k_lif_fwd<false, true>, k_lif_fwd<true, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>,
                     k_lif_bwd<0, true>, k_lif_bwd<1, true>, k_lif_bwd<2, true>, k_lif_bwd<3, true>,
                     k_lif_bwd<4, true>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(bwd_smem_bytes(TT, 2))));
+    for (auto fn : {k_lif_bwd<0, false, false, true>, k_lif_bwd<0, true, false, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     for (auto fn : {k_lif_bwd<0, false, true>, k_lif_bwd<1, false, true>, k_lif_bwd<2, false, true>,
@@ -651,6 +688,7 @@ struct snn_engine {
     return id;
   }
   bool alif(int l) const { return l < L && net.cell[l] == SNN_CELL_ALIF; }
+  bool rlif(int l) const { return l < L && net.cell[l] == SNN_CELL_RLIF; }
   bool reg_on() const {
     if (cfg.lambda_low == 0.0f && cfg.lambda_high == 0.0f) return false;
     for (int l = 0; l < L; ++l)
@@ -662,7 +700,11 @@ struct snn_engine {
     // network.hpp:231-286: layer i key rng.child(i); W ~ TN(child(0)); beta ~ TN(child(2))
     std::vector<float> h(n_params, 0.0f);
     for (const auto& e : entries) {
-      if (e.kind == kEntryW) {
+      if (e.kind == kEntryW && e.layer > L) {  // declared RLIF rec ~ TN(0, 1/sqrt(H)) from child 4
+        const uint64_t lk = hostrng::child(key, uint64_t(lin_id(rec_l[e.layer]) + 1));
+        const float sd = 1.0f / std::sqrt(float(e.rows));
+        hostrng::truncated_normal(hostrng::child(lk, 4), e.size, 0.0f, sd, h.data() + e.offset);
+      } else if (e.kind == kEntryW) {
         const uint64_t lk = hostrng::child(key, uint64_t(lin_id(e.layer)));
         const float sd = 1.0f / std::sqrt(float(e.rows));
         hostrng::truncated_normal(hostrng::child(lk, 0), e.size, 0.0f, sd, h.data() + e.offset);
@@ -707,6 +749,10 @@ struct snn_engine {
       a.planes[j].wb = wb[j].p;
       a.planes[j].K_pad = K_pad[j];
       a.planes[j].N_pad = N_pad[j];
+    }
+    for (int j = L + 1; j < NJ; ++j) {  // RLIF rec: f32 transpose for k_rlif_bwd
+      a.planes[j].wt = rec_t[rec_l[j]].p;
+      a.planes[j].wt_ld = H_pad[rec_l[j]];
     }
     a.params = params.p;
     a.m = m.p;
@@ -883,6 +929,37 @@ struct snn_engine {
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   }
 
+  // samples per k_rlif_bwd CTA: rec^T is re-read from L2 once per step per CTA, so
+  // CTAs share it across kSB samples while the grid still covers the SMs
+  int rlif_sb() const { return B >= 4 * 148 ? 4 : B >= 2 * 148 ? 2 : 1; }
+  template <int kAct>
+  void launch_rlif_bwd_sb(int sb, const RlifBwdArgs& ra, int hp) {
+    const size_t smem = size_t(2) * sb * hp * sizeof(float);
+    if (sb == 4) launch(k_rlif_bwd<kAct, 4>, dim3((B + 3) / 4), dim3(hp), smem, ra);
+    else if (sb == 2) launch(k_rlif_bwd<kAct, 2>, dim3((B + 1) / 2), dim3(hp), smem, ra);
+    else launch(k_rlif_bwd<kAct, 1>, dim3(B), dim3(hp), smem, ra);
+  }
+  void launch_rlif_bwd(int l) {
+    RlifBwdArgs ra{};
+    ra.ds = dsbuf[l].p;
+    ra.v_in = V[l].p;
+    ra.beta = params.p + entry_of(kEntryBeta, l).offset;
+    ra.beta_stride = net.beta_mode[l] == 0 ? 1 : 0;
+    ra.rec_t = rec_t[l].p;
+    ra.di_planes = di[l].p;
+    ra.dbeta_part = dbeta[l].p;
+    ra.dbias_part = net.bias ? dbias[l].p : nullptr;
+    ra.B = B; ra.T = T; ra.T_pad = T_pad; ra.H = H[l]; ra.H_pad = H_pad[l];
+    ra.theta = net.threshold; ra.slope = net.slope; ra.aux = net.aux;
+    const int sb = rlif_sb();
+    switch (net.activation) {
+      case 1: launch_rlif_bwd_sb<1>(sb, ra, H_pad[l]); break;
+      case 2: launch_rlif_bwd_sb<2>(sb, ra, H_pad[l]); break;
+      case 3: launch_rlif_bwd_sb<3>(sb, ra, H_pad[l]); break;
+      case 4: launch_rlif_bwd_sb<4>(sb, ra, H_pad[l]); break;
+      default: launch_rlif_bwd_sb<0>(sb, ra, H_pad[l]); break;
+    }
+  }
   template <bool kAlif>
   void launch_bwd_alif(int act, dim3 grid, size_t smem, const CUtensorMap& tw, const CUtensorMap& td,
                        const CUtensorMap& to, const BwdArgs& bw) {
@@ -928,8 +1005,11 @@ struct snn_engine {
     std::vector<std::pair<int, int>> g;
     for (int l = 0; l < L;) {
       int nl = 1;
-      if (fwd_fuse && NT == 1 && H_pad[l] == 128 && K_pad[l] >= 128 && fwd_stages >= 2)
-        while (l + nl < L && nl < kFwdFuseMax && H_pad[l + nl] == 128 && K_pad[l + nl] == 128) ++nl;
+      // RLIF layers run their recurrent scan in a separate kernel: never fused
+      if (fwd_fuse && NT == 1 && H_pad[l] == 128 && K_pad[l] >= 128 && fwd_stages >= 2 && !rlif(l))
+        while (l + nl < L && nl < kFwdFuseMax && H_pad[l + nl] == 128 && K_pad[l + nl] == 128 &&
+               !rlif(l + nl))
+          ++nl;
       g.emplace_back(l, nl);
       l += nl;
     }
@@ -937,7 +1017,15 @@ struct snn_engine {
   }
   // forward groups + readout + L bwd + wgrad + tail (fused reduce+Adam without a
   // communicator; reduce, adam with one -- the allreduce between them is NCCL's)
-  int launches_per_step() const { return int(fwd_groups().size()) + L + (tail_mode == 0 ? 3 : 4); }
+  int n_rlif() const {
+    int c = 0;
+    for (int l = 0; l < L; ++l) c += rlif(l) ? 1 : 0;
+    return c;
+  }
+  // + the RLIF recurrent scans (one forward, one backward per RLIF layer)
+  int launches_per_step() const {
+    return int(fwd_groups().size()) + L + (tail_mode == 0 ? 3 : 4) + 2 * n_rlif();
+  }
 
   // exchange buffers + flags of the peer tail (cudaMalloc'd: IPC-exportable)
   void ensure_peer_mem() {
@@ -1024,6 +1112,7 @@ struct snn_engine {
         ly.dbg_i = debug ? dbg_i[l + i].p : nullptr;
         ly.gamma = alif(l + i) ? params.p + entry_of(kEntryGamma, l + i).offset : nullptr;
         ly.a_out = alif(l + i) ? Aad[l + i].p : nullptr;
+        ly.i_out = rlif(l + i) ? Ibuf[l + i].p : nullptr;
         ly.K_pad = K_pad[l + i]; ly.H = H[l + i]; ly.H_pad = H_pad[l + i];
         fm.m[i] = tm_wt[l + i];
       }
@@ -1045,6 +1134,20 @@ struct snn_engine {
              dim3(kFwdThreads),
              fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
       mark(evs, "lif_fwd", l);
+      if (nl == 1 && rlif(l)) {  // declared RLIF: the recurrent scan over the projection
+        RlifFwdArgs ra{};
+        ra.i_in = Ibuf[l].p;
+        ra.beta = params.p + entry_of(kEntryBeta, l).offset;
+        ra.beta_stride = net.beta_mode[l] == 0 ? 1 : 0;
+        ra.rec = params.p + entry_of(kEntryW, rec_j[l]).offset;
+        ra.v_out = V[l].p;
+        ra.s_np = s_np[l].p;
+        ra.s_tp = s_tp[l].p;
+        ra.B = B; ra.T = T; ra.T_pad = T_pad; ra.H = H[l]; ra.H_pad = H_pad[l];
+        ra.theta = net.threshold;
+        launch(k_rlif_fwd, dim3(B), dim3(H_pad[l]), 0, ra);
+        mark(evs, "rlif_fwd", l);
+      }
     }
     // readout + loss + LI backward
     {
@@ -1106,6 +1209,16 @@ struct snn_engine {
           bw.f_min = cfg.f_min; bw.f_max = cfg.f_max;
           bw.lambda_low = cfg.lambda_low; bw.lambda_high = cfg.lambda_high;
         }
+      if (rlif(l)) {  // declared RLIF: dS on tcgen05, then the recurrent reverse scan
+        bw.ds_out = dsbuf[l].p;
+        launch(bw.hist != nullptr ? k_lif_bwd<0, true, false, true> : k_lif_bwd<0, false, false, true>,
+               dim3(B, H_pad[l] / 128), dim3(kBwdThreads), bwd_smem_bytes(TT, bw.stages), tm_wb[l + 1],
+               tm_di_k[l + 1], tm_di_out[l], bw);
+        mark(evs, "ds", l);
+        launch_rlif_bwd(l);
+        mark(evs, "rlif_bwd", l);
+        continue;
+      }
       launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages, alif(l)),
                  tm_wb[l + 1], tm_di_k[l + 1], tm_di_out[l], bw);
       mark(evs, "lif_bwd", l);
@@ -1113,7 +1226,6 @@ struct snn_engine {
     // weight gradients: one launch over every Linear layer (split-K partials)
     {
       WgradArgs w{};
-      w.n_layers = L + 1;
       w.x = ds.x.p;
       w.rows = rows_p;
       w.rows_slot = slot_p;
@@ -1122,9 +1234,10 @@ struct snn_engine {
       w.in_features = IN;
       w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * clk_region() : nullptr;
       int blocks = 0;
-      for (int j = 0; j <= L; ++j) {
+      w.n_layers = NJ;  // + one d rec layer per RLIF cell (A = its own spikes)
+      for (int j = 0; j < NJ; ++j) {
         WgradLayer& g = w.layer[j];
-        g.s_tp = j > 0 ? s_tp[j - 1].p : nullptr;
+        g.s_tp = j > L ? s_tp[rec_l[j]].p : j > 0 ? s_tp[j - 1].p : nullptr;
         g.partial = partial[j].p;
         g.kind = j == 0 ? 0 : 1;
         g.M_pad = M_pad_w[j]; g.N_pad = N_pad[j]; g.n_tile = n_tile_w[j]; g.splits = splits_w[j];
@@ -1142,6 +1255,12 @@ struct snn_engine {
       ReduceArgs r{};
       fill_entries(r.entries, &r.n_entries);
       r.n_params = int64_t(n_params);
+      for (int j = L + 1; j < NJ; ++j) {
+        r.partial[j] = partial[j].p;
+        r.M_pad[j] = M_pad_w[j];
+        r.N_pad[j] = N_pad[j];
+        r.splits[j] = splits_w[j];
+      }
       for (int j = 0; j <= L; ++j) {
         r.partial[j] = partial[j].p;
         r.M_pad[j] = M_pad_w[j];
@@ -2180,9 +2299,10 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
     if (which == 6 && !e->alif(layer)) fail(SNN_ERR_ARGUMENT, "layer %d is not an ALIF cell", layer);
     if (which == 0 || which == 1 || which == 4 || which == 6) {
       std::vector<float> buf(rows * Hp);
-      const float* src = which == 0 ? e->dbg_i[layer].p
+      const bool rl = e->rlif(layer);  // RLIF: the projection / dS buffers of the step itself
+      const float* src = which == 0 ? (rl ? e->Ibuf[layer].p : e->dbg_i[layer].p)
                          : which == 1 ? e->V[layer].p
-                         : which == 6 ? e->Aad[layer].p : e->dbg_ds[layer].p;
+                         : which == 6 ? e->Aad[layer].p : (rl ? e->dsbuf[layer].p : e->dbg_ds[layer].p);
       CK(cudaMemcpy(buf.data(), src, buf.size() * 4, cudaMemcpyDeviceToHost));
       float* out = static_cast<float*>(host);
       for (int b = 0; b < B; ++b)

@@ -175,6 +175,8 @@ struct FwdLayer {
   float* dbg_i;           // optional [B][T_pad][H_pad] raw projection
   const float* gamma;     // ALIF (declared cell): adaptation decay [H]; nullptr = LIF
   float* a_out;           // ALIF: adaptation entering step t [B][T_pad][H_pad]
+  float* i_out;           // RLIF: projection only -- I (+ bias) [B][T_pad][H_pad] for
+                          // k_rlif_fwd (no scan, no spikes); nullptr otherwise
   int K_pad, H, H_pad;
 };
 // A launch runs n_layers consecutive hidden layers.  n_layers > 1 (fused) needs
@@ -566,6 +568,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tmem_ld32(tmem + (uint32_t(q * 32) << 16) + buf * NTOT + sm * a.TT + c * 32, r);
           tmem_ld_wait();
           const int t0 = tt * a.TT + c * 32;
+          if (ly.i_out != nullptr) {  // RLIF layer: the recurrent scan runs in k_rlif_fwd
+            float* ip = ly.i_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float I = __uint_as_float(r[j]);
+              ip[size_t(j) * ly.H_pad] = ly.bias != nullptr ? __fadd_rn(I, bn) : I;
+            }
+            continue;
+          }
           uint32_t myword = 0u, tmask = 0u;
           if (t0 < a.T) {
             float* vp = ly.v_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
@@ -929,6 +940,8 @@ struct BwdArgs {
   const float* a_in;           // adaptation entering step t [B][T_pad][H_pad]
   const float* gamma;          // [H]
   float* dgamma_part;          // [B][H]
+  // RLIF (kDsOnly launches): dS of this layer [B][T_pad][H_pad] for k_rlif_bwd
+  float* ds_out;
 };
 
 // d loss / d count of one (sample, neuron) (objective.hpp:208-227): with g = 1,
@@ -938,6 +951,27 @@ __device__ __forceinline__ float activity_dcount(const BwdArgs& a, int count) {
   const float xl = __fsub_rn(a.f_min, r), xh = __fsub_rn(r, a.f_max);
   const float dl = xl > 0.0f ? xl : 0.0f, dh = xh > 0.0f ? xh : 0.0f;
   return __fmul_rn(a.reg_gs, __fsub_rn(__fmul_rn(a.lambda_high, dh), __fmul_rn(a.lambda_low, dl)));
+}
+
+// Monitored layer with the activity regularizer (kReg launches): the spike count
+// of (sample b, neuron n) over the window (monitor_activity, neuron.hpp:106-114)
+// from the time-packed raster, its d loss / d count, and -- segment 0 only -- one
+// histogram entry per (sample, neuron), warp-aggregated, for the loss value.
+__device__ __forceinline__ float monitor_term(const BwdArgs& a, int b, int n, int sg, int lane) {
+  int count = -1;
+  float rterm = 0.0f;
+  if (n < a.H) {
+    const int wpb = a.T_pad / 32;
+    const uint32_t* w = a.s_tp + size_t(n) * (size_t(a.B) * wpb) + size_t(b) * wpb;
+    count = 0;
+    for (int i = 0; i < wpb; ++i) count += __popc(__ldg(w + i));
+    rterm = activity_dcount(a, count);
+  }
+  if (sg == 0) {
+    const unsigned peers = __match_any_sync(0xffffffffu, count);
+    if (count >= 0 && lane == __ffs(peers) - 1) atomicAdd(a.hist + count, unsigned(__popc(peers)));
+  }
+  return rterm;
 }
 
 // Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
@@ -1147,7 +1181,9 @@ __host__ __device__ constexpr uint32_t bwd_smem_bytes(int TT, int stages, bool a
 // kReg: the layer feeds a monitor and the activity regularizer is on -- every
 // step's dS gains d loss / d count of its (sample, neuron) (sum_axis1 backward).
 // kAlif: the layer is the declared ALIF cell (two-state reverse scan, 2x2 maps).
-template <int kAct, bool kReg = false, bool kAlif = false>
+// kDsOnly: the layer is the declared RLIF cell -- only dS (+ the monitor term) is
+// written (a.ds_out); its recurrent reverse scan is k_rlif_bwd.
+template <int kAct, bool kReg = false, bool kAlif = false, bool kDsOnly = false>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_lif_bwd(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_di,
               const __grid_constant__ CUtensorMap tm_out, BwdArgs a) {
@@ -1176,7 +1212,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   // one t-tile: TT more columns cache the membranes V between the two scan passes
-  const bool vcache = a.NT == 1 && !kAlif;
+  const bool vcache = a.NT == 1 && !kAlif && !kDsOnly;
   const uint32_t tmem_cols = vcache ? acc_cols(2 * a.TT, 1) : acc_cols(a.TT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
 
@@ -1250,6 +1286,29 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       }
     }
     __syncwarp();
+  } else if constexpr (kDsOnly) {
+    const int q = warp & 3, sg = warp >> 2;
+    const int n = nt * 128 + q * 32 + lane;
+    const int seg_len = a.TT / kBwdSeg;
+    const float rterm = kReg ? monitor_term(a, b, n, sg, lane) : 0.0f;
+    for (int j = 0; j < a.NT; ++j) {
+      const int tt = a.NT - 1 - j, buf = j % nbuf;
+      const int t_lo = tt * a.TT + sg * seg_len;
+      const uint32_t tcol = tmem + (uint32_t(q * 32) << 16) + buf * a.TT + sg * seg_len;
+      mbar_wait(&acc_full[buf], (j / nbuf) & 1);
+      tc_fence_after();
+      for (int c0 = 0; c0 < seg_len; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tcol + c0, r);
+        tmem_ld_wait();
+        if constexpr (kReg) add_dcount(r, rterm);
+        float* dp = a.ds_out + (size_t(b) * a.T_pad + t_lo + c0) * a.H_pad + n;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dp[size_t(e) * a.H_pad] = __uint_as_float(r[e]);
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+    }
   } else if constexpr (kAlif) {
     // ALIF scan warps (declared cell): the same segment structure as the LIF path
     // below with the two-state reverse step -- each segment composes its 2x2 affine
@@ -1275,21 +1334,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     const int last = (kBwdSeg - 1) * 128 + q * 32 + lane;
     float cv = 0.0f, ca = 0.0f;  // (gv, ga) entering the t-tile from above
     float db = 0.0f, dbias = 0.0f, dgam = 0.0f;
-    float rterm = 0.0f;
-    if constexpr (kReg) {
-      int count = -1;
-      if (n < a.H) {
-        const int wpb = a.T_pad / 32;
-        const uint32_t* w = a.s_tp + size_t(n) * (size_t(a.B) * wpb) + size_t(b) * wpb;
-        count = 0;
-        for (int i = 0; i < wpb; ++i) count += __popc(__ldg(w + i));
-        rterm = activity_dcount(a, count);
-      }
-      if (sg == 0) {
-        const unsigned peers = __match_any_sync(0xffffffffu, count);
-        if (count >= 0 && lane == __ffs(peers) - 1) atomicAdd(a.hist + count, unsigned(__popc(peers)));
-      }
-    }
+    const float rterm = kReg ? monitor_term(a, b, n, sg, lane) : 0.0f;
     for (int j = 0; j < a.NT; ++j) {
       const int tt = a.NT - 1 - j, buf = j % nbuf;
       const int t_lo = tt * a.TT + sg * seg_len;
@@ -1852,6 +1897,183 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 }
 
 // ============================================================================
+// K2r / K3r  the DECLARED RLIF cell (not in the reference; oracle/spiketrain_oracle.h).
+// The input projection I = A W runs on tcgen05 in k_lif_fwd (FwdLayer.i_out: no
+// scan); the recurrence couples every neuron of a sample at every step, so the
+// scan is its own kernel: one CTA per sample, one thread per neuron.
+//   forward : s_t from the incoming v; fb_j = sum over spiking i ascending of
+//             rec[i][j] (exact: the oracle's zero-skip row order); the spiking set
+//             of a step is the block's warp ballots (smem, double-buffered, one
+//             barrier per step); v' = (((v bc) + I) + fb) - s theta.
+//   backward: dS from k_lif_bwd<., ., false, true> (dS only); per step t
+//             descending rc_i = sum_j rec[i][j] G_j over the CTA's kSB samples
+//             (rec^T rows coalesced over i, G broadcast from smem),
+//             gs = (dS + (-G) theta) + rc ; G' = G bc + gs g(v - theta);
+//             dI = G as bf16 planes, beta / bias partials per sample.
+// d rec = S^T dI of the layer with itself runs in k_wgrad as an extra layer.
+// ============================================================================
+struct RlifFwdArgs {
+  const float* i_in;      // [B][T_pad][H_pad] projection (+ bias)
+  const float* beta;      // [H] or one value (beta_stride 0)
+  int beta_stride;
+  const float* rec;       // [H][H] (row = source neuron), the parameter itself
+  float* v_out;           // [B][T_pad][H_pad]
+  uint32_t* s_np;         // [B][T_pad][H_pad/32]
+  uint32_t* s_tp;         // [H_pad][B*T_pad/32]
+  int B, T, T_pad, H, H_pad;
+  float theta;
+};
+
+__global__ void __launch_bounds__(1024) k_rlif_fwd(RlifFwdArgs a) {
+  __shared__ uint32_t words[2][32];
+  pdl_wait();
+  const int b = blockIdx.x, n = threadIdx.x, lane = n & 31, w = n >> 5;
+  const int nw = a.H_pad / 32;
+  const float vb = clip01(n < a.H ? a.beta[n * a.beta_stride] : 0.0f);
+  const float theta = a.theta, ntheta = -a.theta;
+  const float* __restrict__ ip = a.i_in + size_t(b) * a.T_pad * a.H_pad + n;
+  float* __restrict__ vp = a.v_out + size_t(b) * a.T_pad * a.H_pad + n;
+  const size_t tp_words = size_t(a.B) * a.T_pad / 32;
+  const float* __restrict__ recn = a.rec + (n < a.H ? n : 0);  // column n
+  float v = 0.0f;
+  uint32_t tmask = 0u;
+  float I = __ldg(ip);
+  for (int t = 0; t < a.T_pad; ++t) {
+    const float In = t + 1 < a.T_pad ? __ldg(ip + size_t(t + 1) * a.H_pad) : 0.0f;
+    vp[size_t(t) * a.H_pad] = v;
+    const bool sp = __fadd_rn(v, ntheta) >= 0.0f && n < a.H && t < a.T;
+    const uint32_t bal = __ballot_sync(0xffffffffu, sp);
+    if (lane == 0) {
+      words[t & 1][w] = bal;
+      a.s_np[(size_t(b) * a.T_pad + t) * nw + w] = bal;
+    }
+    tmask |= uint32_t(sp) << (t & 31);
+    if ((t & 31) == 31) {
+      a.s_tp[size_t(n) * tp_words + size_t(b) * (a.T_pad / 32) + t / 32] = tmask;
+      tmask = 0u;
+    }
+    __syncthreads();
+    float fb = 0.0f;
+    if (n < a.H) {
+      for (int q = 0; q < nw; ++q) {
+        uint32_t m = words[t & 1][q];
+        while (m != 0u) {
+          // up to 8 sources per round: the loads issue before the ordered adds
+          float xs[8];
+          int k = 0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (m != 0u) {
+              const int i = q * 32 + __ffs(m) - 1;
+              m &= m - 1u;
+              xs[u] = __ldg(recn + size_t(i) * a.H);
+              k = u + 1;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u < k) fb = __fadd_rn(fb, xs[u]);
+        }
+      }
+    }
+    const float ai = __fadd_rn(__fmul_rn(v, vb), I);
+    v = __fsub_rn(__fadd_rn(ai, fb), sp ? theta : 0.0f);
+    I = In;
+  }
+  pdl_launch_dependents();
+}
+
+struct RlifBwdArgs {
+  const float* ds;             // [B][T_pad][H_pad] dS of this layer
+  const float* v_in;           // [B][T_pad][H_pad]
+  const float* beta;
+  int beta_stride;
+  const float* rec_t;          // [H][H_pad]: rec_t[j][i] = rec[i][j] (refreshed by Adam)
+  __nv_bfloat16* di_planes;    // out: dI planes [3][H_pad][B*T_pad]
+  float* dbeta_part;           // [B][H]
+  float* dbias_part;           // [B][H] or nullptr
+  int B, T, T_pad, H, H_pad;
+  float theta, slope, aux;
+};
+
+template <int kAct, int kSB>
+__global__ void __launch_bounds__(1024) k_rlif_bwd(RlifBwdArgs a) {
+  extern __shared__ float gsm[];  // [2][kSB][H_pad]: G of every neuron, this step
+  pdl_wait();
+  const int b0 = blockIdx.x * kSB, i = threadIdx.x;
+  const bool live = i < a.H;
+  const float vb = clip01(live ? a.beta[i * a.beta_stride] : 0.0f);
+  const float theta = a.theta;
+  const size_t cols_total = size_t(a.B) * a.T_pad;
+  const size_t plane = size_t(a.H_pad) * cols_total;
+  const float* __restrict__ rt = a.rec_t + i;
+  float G[kSB], db[kSB], dbias[kSB];
+#pragma unroll
+  for (int s = 0; s < kSB; ++s) G[s] = db[s] = dbias[s] = 0.0f;
+  int par = 0;
+  for (int c0 = a.T_pad - 16; c0 >= 0; c0 -= 16) {
+    float x[kSB][16];
+#pragma unroll
+    for (int e = 15; e >= 0; --e) {
+      const int t = c0 + e;
+#pragma unroll
+      for (int s = 0; s < kSB; ++s) {
+        gsm[(par * kSB + s) * a.H_pad + i] = G[s];
+        x[s][e] = G[s];
+      }
+      if (t >= a.T) {  // padded steps: G stays 0, dI 0
+        par ^= 1;
+        continue;
+      }
+      float dS[kSB], V[kSB];
+#pragma unroll
+      for (int s = 0; s < kSB; ++s) {
+        const size_t idx = (size_t(b0 + s) * a.T_pad + t) * a.H_pad + i;
+        dS[s] = b0 + s < a.B ? __ldg(a.ds + idx) : 0.0f;
+        V[s] = b0 + s < a.B ? __ldg(a.v_in + idx) : 0.0f;
+      }
+      __syncthreads();
+      float rc[kSB];
+#pragma unroll
+      for (int s = 0; s < kSB; ++s) rc[s] = 0.0f;
+      if (live) {
+        const float* gp = gsm + par * kSB * a.H_pad;
+#pragma unroll 4
+        for (int j = 0; j < a.H; ++j) {
+          const float r = __ldg(rt + size_t(j) * a.H_pad);
+#pragma unroll
+          for (int s = 0; s < kSB; ++s) rc[s] = __fadd_rn(rc[s], __fmul_rn(r, gp[s * a.H_pad + j]));
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < kSB; ++s) {
+        const float gi = G[s];
+        const float gs = __fadd_rn(__fadd_rn(dS[s], __fmul_rn(-gi, theta)), rc[s]);
+        const float g = surrogate_t<kAct>(a.slope, a.aux, __fadd_rn(V[s], -theta));
+        db[s] = __fadd_rn(db[s], __fmul_rn(gi, V[s]));
+        dbias[s] = __fadd_rn(dbias[s], gi);
+        G[s] = live ? __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g)) : 0.0f;
+      }
+      par ^= 1;
+    }
+#pragma unroll
+    for (int s = 0; s < kSB; ++s)
+      if (b0 + s < a.B)
+        bwd_store_di16(x[s], false, nullptr, 0, 0, 0, 0,
+                       a.di_planes + size_t(i) * cols_total + size_t(b0 + s) * a.T_pad + c0, plane);
+  }
+  if (live) {
+#pragma unroll
+    for (int s = 0; s < kSB; ++s)
+      if (b0 + s < a.B) {
+        a.dbeta_part[size_t(b0 + s) * a.H + i] = db[s];
+        if (a.dbias_part != nullptr) a.dbias_part[size_t(b0 + s) * a.H + i] = dbias[s];
+      }
+  }
+  pdl_launch_dependents();
+}
+
+// ============================================================================
 // K6  gradient assembly, Adam and operand-plane refresh.
 // One thread per flat parameter in NetworkParams order (network.hpp:164-226).
 // ============================================================================
@@ -2114,6 +2336,8 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
 struct PlaneTarget {
   __nv_bfloat16* wb;  // operand planes [3][K_pad][N_pad] (forward MN-major A, backward K-major A)
   int K_pad, N_pad;
+  float* wt;          // RLIF rec: f32 transpose [N][wt_ld] for k_rlif_bwd (else nullptr)
+  int wt_ld;
 };
 
 struct AdamArgs {
@@ -2170,6 +2394,7 @@ __device__ __forceinline__ float adam_one(const AdamArgs& a, int64_t i, float g,
 // (consecutive n -> consecutive addresses: coalesced).
 __device__ __forceinline__ void refresh_planes(const AdamArgs& a, int layer, int64_t k, int64_t n, float p) {
   const PlaneTarget pt = a.planes[layer];
+  if (pt.wt != nullptr) pt.wt[n * pt.wt_ld + k] = p;
   if (pt.wb == nullptr) return;
   __nv_bfloat16 h, mi, lo;
   split3(p, h, mi, lo);

@@ -82,6 +82,15 @@ class ALIFLayer(LIFLayer):
 
 
 @dataclass
+class RLIFLayer(LIFLayer):
+    """Recurrent LIF -- a DECLARED cell, not in the reference (feed-forward only,
+    network.hpp:16): fb_j = sum_i s_i rec[i][j] over the step's spiking
+    neurons, v' = (((v*bc) + I) + fb) - s*theta, with an "l{id}.rec" [H][H] entry after
+    "l{id}.beta" (Spyx's RLIF in the reference's LIF op order; checker:
+    oracle/spiketrain_oracle.h).  Width <= 1024."""
+
+
+@dataclass
 class LILayer:
     beta_mode: str = "per_neuron"
     fixed_beta: float = 0.5
@@ -183,7 +192,8 @@ def normalize(spec: NetworkSpec) -> dict:
         act, thr, bias = cell.activation, cell.threshold, lin.bias
         hidden.append(int(lin.out))
         modes.append(cell.beta_mode)
-        cells.append("alif" if isinstance(cell, ALIFLayer) else "lif")
+        cells.append("alif" if isinstance(cell, ALIFLayer) else
+                     "rlif" if isinstance(cell, RLIFLayer) else "lif")
         fixed.append(float(cell.fixed_beta))
     lin, cell = layers[-2], layers[-1]
     if not isinstance(lin, LinearLayer) or not isinstance(cell, LILayer):
@@ -205,7 +215,7 @@ def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False,
     """The BASELINE network: 700-H1-H2-20, LIF, arctan k=2, nobias (PAPER.md:122);
     cell="alif" gives BASELINE config 2's adaptive-threshold variant."""
     layers = []
-    kind = ALIFLayer if cell == "alif" else LIFLayer
+    kind = {"lif": LIFLayer, "alif": ALIFLayer, "rlif": RLIFLayer}[cell]
     for h in hidden:
         layers += [LinearLayer(h, bias), kind(default_activation_desc(act))]
     layers += [LinearLayer(classes, bias), LILayer()]
@@ -289,7 +299,7 @@ class Engine:
         for m in d["monitor"]:
             n.monitor[m] = 1
         for i, k in enumerate(d["cell"]):
-            n.cell[i] = 1 if k == "alif" else 0
+            n.cell[i] = {"lif": 0, "alif": 1, "rlif": 2}[k]
         c = _TrainCfg()
         c.batch_size = int(cfg.batch_size)
         c.time_steps = int(time_steps)

@@ -92,3 +92,27 @@ def alif_forward(I, beta, gamma, theta):
         a = (a * gc + omg * s.astype(F)).astype(F)
         S[:, t] = s
     return V, A, S
+
+
+def rlif_forward(I, beta, rec, theta):
+    """Declared RLIF cell (oracle/spiketrain_oracle.h), same op order: fb sums the
+    rows of rec [H][H] of the spiking neurons in ascending order.
+    I [B,T,H] f32 -> (V entering each step, spikes u8)."""
+    B, T, H = I.shape
+    vb = clip01(beta.astype(F))
+    theta = F(theta)
+    rec = rec.reshape(H, H).astype(F)
+    v = np.zeros((B, H), F)
+    V = np.empty_like(I)
+    S = np.empty(I.shape, np.uint8)
+    zero = np.zeros((B, H), F)
+    for t in range(T):
+        V[:, t] = v
+        s = (v + (-theta)) >= F(0)
+        fb = np.zeros((B, H), F)
+        for i in np.nonzero(s.any(axis=0))[0]:
+            fb = (fb + np.where(s[:, i:i + 1], rec[i][None, :], zero)).astype(F)
+        ai = (v * vb + I[:, t]).astype(F)
+        v = ((ai + fb).astype(F) - s.astype(F) * theta).astype(F)
+        S[:, t] = s
+    return V, S

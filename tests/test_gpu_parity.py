@@ -35,13 +35,14 @@ def make_engine(net: Net, B, T, seed=0, lr=1e-3, **cfg):
             layer.threshold = net.threshold
             if net.slope is not None:
                 layer.activation.slope = net.slope
-    if net.cell:  # declared ALIF cells (oracle/spiketrain_oracle.h)
-        from paper_2402_18994_b200 import ALIFLayer
+    if net.cell:  # declared ALIF / RLIF cells (oracle/spiketrain_oracle.h)
+        from paper_2402_18994_b200 import ALIFLayer, RLIFLayer
         hid = [i for i, layer in enumerate(spec.layers) if type(layer).__name__ == "LIFLayer"]
         for i, kind in zip(hid, net.cell):
-            if kind == "alif":
+            if kind != "lif":
                 old = spec.layers[i]
-                spec.layers[i] = ALIFLayer(old.activation, old.threshold, old.beta_mode, old.fixed_beta)
+                cls = ALIFLayer if kind == "alif" else RLIFLayer
+                spec.layers[i] = cls(old.activation, old.threshold, old.beta_mode, old.fixed_beta)
     if net.monitor:  # MonitorLayer after the listed hidden LIF layers
         from paper_2402_18994_b200 import MonitorLayer
         for m in sorted(net.monitor, reverse=True):
@@ -981,3 +982,74 @@ def test_alif_training_curve(orc):
     # 12 Adam steps of ~lr * sign(g): elements whose gradient nearly cancels can move
     # the other way (check_adam_step), so the parameter bound after training is 5e-4
     assert relnorm(eng.get_params(), st.params) <= 5e-4
+
+
+# ---------------------------------------------------------------------------
+# Declared RLIF cell (BASELINE config 4; not in the reference -- checker: the
+# oracle's restatement, pinned to float64 autograd in tests/test_alif_oracle.py).
+# Forward V / spikes bit-exact given the GPU's projection (the feedback sum runs
+# over the spiking sources in the oracle's ascending order); loss and gradients
+# (rec included) within the north_star bar.
+RLIF_CASES = [
+    ("rlif-tiny", Net(inp=30, hidden=(16, 12), classes=5, cell=("rlif", "rlif")), 6, 19, 3.0),
+    ("rlif-c4-shape", Net(hidden=(512, 512), act="arctan", cell=("rlif", "rlif")), 3, 128, 2.0),
+    ("lif-rlif-T200-bias", Net(inp=64, hidden=(128, 96), classes=8, act="superspike", bias=True,
+                               cell=("lif", "rlif")), 3, 200, 2.0),
+    ("rlif-alif-3hidden", Net(inp=50, hidden=(64, 48, 32), classes=6, act="triangular",
+                              cell=("rlif", "alif", "lif")), 4, 33, 3.0),
+]
+
+
+@pytest.mark.parametrize("case", RLIF_CASES, ids=[c[0] for c in RLIF_CASES])
+def test_rlif_step_parity(orc, case):
+    _, net, B, T, scale = case
+    params = orc.init(net, orc.key_child(orc.key_from_seed(31), 0))
+    ents = orc.entries(net)
+    for n, o, s in ents:
+        if n.endswith(".w"):
+            params[o:o + s] *= np.float32(scale)
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 5)
+    pk = orc.pack_time(x)
+    eng = make_engine(net, B, T)
+    names = [n for n, _, _ in ents]
+    assert eng.entries() == ents
+    assert np.array_equal(eng.get_params(), orc.init(net, orc.key_child(orc.key_from_seed(0), 0)))
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    eng.debug(True)
+    rows = np.arange(B, dtype=np.uint32)
+    loss, acc = eng.forward_backward(rows)
+    ref = orc.forward_backward(net, params, pk, T, y, want_spikes=True, want_trace=True)
+    emap = {n: (o, s) for n, o, s in ents}
+    flips = 0
+    for l, h in enumerate(net.hidden):
+        I = eng.fetch("I", l)
+        cell = names[names.index(f"l{2 * l}.w") + (2 if net.bias else 1)][:-5]
+        o, s = emap[cell + ".beta"]
+        S = eng.fetch("spikes", l)
+        if net.cell[l] == "rlif":
+            ro, rs = emap[cell + ".rec"]
+            V_ref, S_ref = scanref.rlif_forward(I, params[o:o + s], params[ro:ro + rs], net.threshold)
+        elif net.cell[l] == "alif":
+            go, gs = emap[cell + ".gamma"]
+            V_ref, _, S_ref = scanref.alif_forward(I, params[o:o + s], params[go:go + gs], net.threshold)
+        else:
+            V_ref, S_ref = scanref.lif_forward(I, params[o:o + s], net.threshold)
+        assert np.array_equal(eng.fetch("V", l), V_ref), f"layer {l}: V not bit-exact given I"
+        assert np.array_equal(S, S_ref), f"layer {l}: spikes not bit-exact given I"
+        agree = (S == ref["spikes"][l]).mean()
+        assert agree >= SPIKE_AGREE, agree
+        flips += int((S != ref["spikes"][l]).sum())
+        assert 0.005 < S.mean() < 0.9, f"layer {l}: rate {S.mean()}"
+    assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
+    check_grads(orc, net, eng.get_grads(), ref["grads"], REL_TOL if flips == 0 else REL_TOL_FLIPS)
+    st = State(params.copy())
+    lo, ao = orc.train_step(net, st, pk, T, y)
+    eng.debug(False)
+    l2, a2 = eng.train_step(rows)
+    assert abs(l2 - lo) <= REL_TOL * abs(lo) and a2 == ao
+    check_adam_step(orc, net, eng.get_params(), st.params, ref["grads"])
+    # a second step runs on the Adam-refreshed rec^T (k_rlif_bwd's copy)
+    l3, _ = eng.train_step(rows)
+    lo3, _ = orc.train_step(net, st, pk, T, y)
+    assert abs(l3 - lo3) <= 1e-3 * abs(lo3)
