@@ -43,6 +43,10 @@ WORKLOADS = {
                     "T=128, batch 1024/GPU, superspike k=25, integral-CE + Adam, nobias"),
     "c3": dict(inp=700, hidden=(1024, 1024), classes=20, T=256, B=512, act="arctan", n_data=8192,
                desc="wide 700-1024-1024-20 LIF, T=256, batch 512/GPU"),
+    "c4": dict(inp=700, hidden=(512, 512), classes=20, T=128, B=256, act="arctan", cell="rlif",
+               n_data=8192,
+               desc="recurrent 700-512-512-20 RLIF (declared cell, oracle/spiketrain_oracle.h), "
+                    "T=128, batch 256/GPU (B unstated in BASELINE; SURVEY §8), arctan k=2"),
     "c5": dict(inp=700, hidden=(256, 256), classes=20, T=1000, B=512, act="arctan", n_data=2048,
                desc="long-sequence 700-256-256-20 LIF, T=1000, batch 512/GPU"),
 }
@@ -130,6 +134,12 @@ def algorithmic(name: str, w: dict, n_params: int, fwd_groups=None):
         return "hbm", (16.0 if w.get("cell") == "alif" else 12.0) * B * T * dims[l + 1]
     if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element
         return "hbm", 8.0 * B * T * C
+    if base == "rlif_fwd":           # recurrent scan: read I, write V (+ spike bits) per neuron-step
+        return "hbm", 8.125 * B * T * dims[l + 1]
+    if base == "rlif_bwd":           # recurrent reverse scan: the per-step rec^T GEMV, 2 H^2 flop / sample-step
+        return "hbm", 12.0 * B * T * dims[l + 1]
+    if base == "ds":                 # dS GEMM only (RLIF layers): read dI planes, write dS f32
+        return "hbm", 4.0 * B * T * dims[l + 1]
     if base in ("adam", "reduce_adam"):  # Adam: 28 B / param (split-K sums are overhead)
         return "hbm", 28.0 * n_params
     return "hbm", 0.0
@@ -159,7 +169,8 @@ def _cpu_net(w):
 
 
 def _cpu_label(w, b):
-    cell = "LIF stand-in for ALIF (no ALIF in the reference)" if w.get("cell") == "alif" else "LIF"
+    cell = {"alif": "LIF stand-in for ALIF (no ALIF in the reference)",
+            "rlif": "LIF stand-in for RLIF (no recurrent cell in the reference)"}.get(w.get("cell"), "LIF")
     return (f"{b} examples/step of the workload shape ({w['inp']}-" + "-".join(map(str, w["hidden"])) +
             f"-{w['classes']}, T={w['T']}, {w['act']}, {cell}, init regime)")
 

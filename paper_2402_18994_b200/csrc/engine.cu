@@ -622,7 +622,8 @@ struct snn_engine {
       partial[j].alloc(size_t(splits_w[j]) * M_pad_w[j] * N_pad[j], false);
       wg_maps.m[j] = tm_di_w[rec_l[j]];  // d rec: the RLIF layer's own dI planes
     }
-    for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>, k_lif_fwd<false, true>, k_lif_fwd<true, true>})
+    for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>, k_lif_fwd<false, true>, k_lif_fwd<true, true>,
+                    k_lif_fwd<false, false, true>, k_lif_fwd<true, false, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>,
@@ -630,6 +631,17 @@ struct snn_engine {
                     k_lif_bwd<4, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
+    {
+      CK(cudaFuncSetAttribute(k_rlif_fwd_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
+      CK(cudaFuncSetAttribute(k_rlif_fwd_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+      for (auto fn : {k_rlif_bwd_cl<0>, k_rlif_bwd_cl<1>, k_rlif_bwd_cl<2>, k_rlif_bwd_cl<3>, k_rlif_bwd_cl<4>})
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
+      for (int l = 0; l < L; ++l)
+        if (rlif(l) && rlif_cluster(l)) {
+          rl_sb_fwd[l] = rlif_pick_sb(l, true);
+          rl_sb_bwd[l] = rlif_pick_sb(l, false);
+        }
+    }
     for (auto fn : {k_lif_bwd<0, false, false, true>, k_lif_bwd<0, true, false, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
@@ -929,6 +941,62 @@ struct snn_engine {
     CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   }
 
+  // kernel launch on a cluster of cx CTAs along x (the RLIF cluster scans)
+  template <typename... KArgs, typename... Args>
+  void launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, int cx, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = unsigned(cx);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  }
+  // samples per cluster of the RLIF cluster scans: the smallest that keeps every
+  // cluster of the grid co-resident (one wave; cudaOccupancyMaxActiveClusters)
+  static constexpr int kRlSmemMax = 227 * 1024;
+  int rl_sb_fwd[SNN_MAX_HIDDEN]{}, rl_sb_bwd[SNN_MAX_HIDDEN]{};
+  int rlif_pick_sb(int l, bool fwd) {
+    const int NS = H_pad[l] / kRlCl;
+    int best = 0;
+    for (int sb = kRlSPT; sb <= kRlSBMax; sb += kRlSPT) {
+      const size_t smem = fwd ? rlif_fwd_cl_smem(H[l], H_pad[l], sb) : rlif_bwd_cl_smem(H[l], H_pad[l], sb);
+      const int threads = fwd ? NS * sb / kRlFPT : NS * sb / kRlSPT;
+      if (smem > size_t(kRlSmemMax) || threads > (fwd ? 1024 : 512)) break;
+      const int clusters = (B + sb - 1) / sb;
+      cudaLaunchConfig_t c{};
+      c.gridDim = dim3(kRlCl, unsigned(clusters));
+      c.blockDim = dim3(unsigned(threads));
+      c.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kRlCl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      c.attrs = at;
+      c.numAttrs = 1;
+      int active = 0;
+      if (fwd) CK(cudaOccupancyMaxActiveClusters(&active, k_rlif_fwd_cl, &c));
+      else CK(cudaOccupancyMaxActiveClusters(&active, k_rlif_bwd_cl<0>, &c));
+      best = sb;
+      if (clusters <= active) break;
+    }
+    if (best == 0) fail(SNN_ERR_UNSUPPORTED, "RLIF layer %d: no cluster configuration fits", l);
+    return best;
+  }
+  // RLIF scans on a cluster (rec slice in smem) when the slices are whole warps
+  // and fit: H_pad 256 or 512 (SNN_RLIF_CL=1 forces the single-CTA kernels)
+  bool rlif_cluster(int l) const {
+    return env_int("SNN_RLIF_CL", 2) == 2 && (H_pad[l] == 256 || H_pad[l] == 512);
+  }
   // samples per k_rlif_bwd CTA: rec^T is re-read from L2 once per step per CTA, so
   // CTAs share it across kSB samples while the grid still covers the SMs
   int rlif_sb() const { return B >= 4 * 148 ? 4 : B >= 2 * 148 ? 2 : 1; }
@@ -951,6 +1019,21 @@ struct snn_engine {
     ra.dbias_part = net.bias ? dbias[l].p : nullptr;
     ra.B = B; ra.T = T; ra.T_pad = T_pad; ra.H = H[l]; ra.H_pad = H_pad[l];
     ra.theta = net.threshold; ra.slope = net.slope; ra.aux = net.aux;
+    if (rlif_cluster(l)) {
+      const int sb = rl_sb_bwd[l];
+      ra.sb = sb;
+      const dim3 grid(kRlCl, unsigned((B + sb - 1) / sb));
+      const dim3 block(unsigned(H_pad[l] / kRlCl * (sb / kRlSPT)));
+      const size_t smem = rlif_bwd_cl_smem(H[l], H_pad[l], sb);
+      switch (net.activation) {
+        case 1: launch_cluster(k_rlif_bwd_cl<1>, grid, block, smem, kRlCl, ra); break;
+        case 2: launch_cluster(k_rlif_bwd_cl<2>, grid, block, smem, kRlCl, ra); break;
+        case 3: launch_cluster(k_rlif_bwd_cl<3>, grid, block, smem, kRlCl, ra); break;
+        case 4: launch_cluster(k_rlif_bwd_cl<4>, grid, block, smem, kRlCl, ra); break;
+        default: launch_cluster(k_rlif_bwd_cl<0>, grid, block, smem, kRlCl, ra); break;
+      }
+      return;
+    }
     const int sb = rlif_sb();
     switch (net.activation) {
       case 1: launch_rlif_bwd_sb<1>(sb, ra, H_pad[l]); break;
@@ -1128,8 +1211,9 @@ struct snn_engine {
       const bool shifting = l == 0 && cfg.max_shift > 0 && cfg.n_shift_axes > 0;
       bool any_alif = false;
       for (int i = 0; i < nl; ++i) any_alif = any_alif || alif(l + i);
-      auto kfn = any_alif ? (shifting ? k_lif_fwd<true, true> : k_lif_fwd<false, true>)
-                          : (shifting ? k_lif_fwd<true> : k_lif_fwd<false>);
+      auto kfn = rlif(l) ? (shifting ? k_lif_fwd<true, false, true> : k_lif_fwd<false, false, true>)
+                 : any_alif ? (shifting ? k_lif_fwd<true, true> : k_lif_fwd<false, true>)
+                            : (shifting ? k_lif_fwd<true> : k_lif_fwd<false>);
       launch(kfn, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128),
              dim3(kFwdThreads),
              fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
@@ -1145,7 +1229,14 @@ struct snn_engine {
         ra.s_tp = s_tp[l].p;
         ra.B = B; ra.T = T; ra.T_pad = T_pad; ra.H = H[l]; ra.H_pad = H_pad[l];
         ra.theta = net.threshold;
-        launch(k_rlif_fwd, dim3(B), dim3(H_pad[l]), 0, ra);
+        if (rlif_cluster(l)) {
+          const int sb = rl_sb_fwd[l];
+          ra.sb = sb;
+          launch_cluster(k_rlif_fwd_cl, dim3(kRlCl, unsigned((B + sb - 1) / sb)),
+                         dim3(unsigned(H_pad[l] / kRlCl * sb / kRlFPT)), rlif_fwd_cl_smem(H[l], H_pad[l], sb),
+                         kRlCl, ra);
+        } else
+          launch(k_rlif_fwd, dim3(B), dim3(H_pad[l]), 0, ra);
         mark(evs, "rlif_fwd", l);
       }
     }

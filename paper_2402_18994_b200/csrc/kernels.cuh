@@ -309,7 +309,8 @@ __device__ __forceinline__ void alif_chunk(const uint32_t (&r)[32], float* vp, f
 // the default instantiation has no roll code in the decode loop.
 // kAlif: the launch's hidden layers are declared ALIF cells (FwdLayer.gamma set);
 // the LIF instantiation carries no adaptation code.
-template <bool kShift, bool kAlif = false>
+// kProj: a single RLIF layer -- the epilogue only stores the projection (FwdLayer.i_out).
+template <bool kShift, bool kAlif = false, bool kProj = false>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     k_lif_fwd(const __grid_constant__ FwdMaps maps, FwdArgs a) {
   const CUtensorMap& tm_w = maps.m[0];
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tmem_ld32(tmem + (uint32_t(q * 32) << 16) + buf * NTOT + sm * a.TT + c * 32, r);
           tmem_ld_wait();
           const int t0 = tt * a.TT + c * 32;
-          if (ly.i_out != nullptr) {  // RLIF layer: the recurrent scan runs in k_rlif_fwd
+          if (kProj) {  // RLIF layer: the recurrent scan runs in k_rlif_fwd
             float* ip = ly.i_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -1921,6 +1922,7 @@ struct RlifFwdArgs {
   uint32_t* s_np;         // [B][T_pad][H_pad/32]
   uint32_t* s_tp;         // [H_pad][B*T_pad/32]
   int B, T, T_pad, H, H_pad;
+  int sb;                 // cluster form: samples per cluster
   float theta;
 };
 
@@ -1993,6 +1995,7 @@ struct RlifBwdArgs {
   float* dbeta_part;           // [B][H]
   float* dbias_part;           // [B][H] or nullptr
   int B, T, T_pad, H, H_pad;
+  int sb;                      // cluster form: samples per cluster
   float theta, slope, aux;
 };
 
@@ -2066,6 +2069,237 @@ __global__ void __launch_bounds__(1024) k_rlif_bwd(RlifBwdArgs a) {
 #pragma unroll
     for (int s = 0; s < kSB; ++s)
       if (b0 + s < a.B) {
+        a.dbeta_part[size_t(b0 + s) * a.H + i] = db[s];
+        if (a.dbias_part != nullptr) a.dbias_part[size_t(b0 + s) * a.H + i] = dbias[s];
+      }
+  }
+  pdl_launch_dependents();
+}
+
+// ---------------------------------------------------------------------------
+// Cluster forms of the RLIF scans (256 <= H_pad <= 512): the H neurons of a
+// sample group are split over a cluster of kRlCl CTAs, each keeping its slice of
+// rec in shared memory (128 KB at H = 512) instead of re-reading it from L2 every
+// step; the per-step exchange (spike words forward, G backward) goes to every
+// CTA of the cluster through DSMEM stores, then one cluster barrier per step
+// (it also retires the double-buffered exchange slot of the step before).
+constexpr int kRlCl = 8;      // CTAs per cluster = neuron slices
+constexpr int kRlSBMax = 32;  // samples per cluster (runtime a.sb <= this, multiple of 4)
+constexpr int kRlSPT = 4;     // backward: samples per thread
+constexpr int kRlFPT = 2;     // forward: samples per thread
+__host__ __device__ constexpr size_t rlif_fwd_cl_smem(int H, int H_pad, int sb) {
+  return size_t(H) * (H_pad / kRlCl) * 4 + size_t(2) * sb * (H_pad / 32) * 4;
+}
+__host__ __device__ constexpr size_t rlif_bwd_cl_smem(int H, int H_pad, int sb) {
+  return size_t(H) * (H_pad / kRlCl) * 4 + size_t(2) * H_pad * sb * 4;
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float x, float y, float z, float w) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x), "f"(y), "f"(z),
+               "f"(w)
+               : "memory");
+}
+
+// Forward: CTA c of the cluster owns output neurons [c NS, (c+1) NS) of a.sb
+// samples; thread = (neuron, kRlFPT samples s, s + sb/kRlFPT, ...).  Its smem
+// holds rec[:, slice] (rows i).  Same statements and ascending source order as
+// k_rlif_fwd: bit-identical.
+__global__ void __launch_bounds__(1024) k_rlif_fwd_cl(RlifFwdArgs a) {
+  extern __shared__ __align__(16) float rsm[];
+  const int NS = a.H_pad / kRlCl, nw = a.H_pad / 32, SB = a.sb, SBT = a.sb / kRlFPT;
+  float* recs = rsm;                                                     // [H][NS]
+  uint32_t* words = reinterpret_cast<uint32_t*>(rsm + size_t(a.H) * NS);  // [2][SB][nw]
+  const uint32_t crank = cluster_ctarank();
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int jl = tid % NS, s0 = tid / NS;
+  const int j = int(crank) * NS + jl;
+  pdl_wait();
+  for (int idx = tid; idx < a.H * NS; idx += blockDim.x) {
+    const int i = idx / NS, c = int(crank) * NS + idx % NS;
+    recs[idx] = c < a.H ? a.rec[size_t(i) * a.H + c] : 0.0f;
+  }
+  const float vb = clip01(j < a.H ? a.beta[j * a.beta_stride] : 0.0f);
+  const float theta = a.theta, ntheta = -a.theta;
+  const size_t tp_words = size_t(a.B) * a.T_pad / 32;
+  const int wi = (int(crank) * NS + (jl & ~31)) / 32;  // this warp's spike word
+  int b[kRlFPT];
+  bool bl[kRlFPT];
+  const float* ip[kRlFPT];
+  float* vp[kRlFPT];
+  float v[kRlFPT], I[kRlFPT];
+  uint32_t tmask[kRlFPT];
+#pragma unroll
+  for (int u = 0; u < kRlFPT; ++u) {
+    b[u] = blockIdx.y * SB + s0 + u * SBT;
+    bl[u] = b[u] < a.B;
+    const size_t base = (size_t(bl[u] ? b[u] : 0) * a.T_pad) * a.H_pad + j;
+    ip[u] = a.i_in + base;
+    vp[u] = a.v_out + base;
+    v[u] = 0.0f;
+    tmask[u] = 0u;
+    I[u] = bl[u] ? __ldg(ip[u]) : 0.0f;
+  }
+  cluster_sync_all();
+  for (int t = 0; t < a.T_pad; ++t) {
+    const int par = t & 1;
+    bool sp[kRlFPT];
+    float In[kRlFPT];
+#pragma unroll
+    for (int u = 0; u < kRlFPT; ++u) {
+      In[u] = (bl[u] && t + 1 < a.T_pad) ? __ldg(ip[u] + size_t(t + 1) * a.H_pad) : 0.0f;
+      if (bl[u]) vp[u][size_t(t) * a.H_pad] = v[u];
+      sp[u] = __fadd_rn(v[u], ntheta) >= 0.0f && j < a.H && t < a.T && bl[u];
+      const uint32_t bal = __ballot_sync(0xffffffffu, sp[u]);
+      const uint32_t slot = smem_u32(words + (par * SB + s0 + u * SBT) * nw + wi);
+      if (lane < kRlCl) st_cluster_u32(map_rank(slot, uint32_t(lane)), bal);  // lane r -> rank r
+      if (lane == 0 && bl[u]) a.s_np[(size_t(b[u]) * a.T_pad + t) * nw + wi] = bal;
+      tmask[u] |= uint32_t(sp[u]) << (t & 31);
+      if ((t & 31) == 31) {
+        if (bl[u]) a.s_tp[size_t(j) * tp_words + size_t(b[u]) * (a.T_pad / 32) + t / 32] = tmask[u];
+        tmask[u] = 0u;
+      }
+    }
+    cluster_sync_all();
+#pragma unroll
+    for (int u = 0; u < kRlFPT; ++u) {
+      float fb = 0.0f;
+      const uint32_t* wp = words + (par * SB + s0 + u * SBT) * nw;
+      for (int q = 0; q < nw; ++q) {
+        uint32_t m = wp[q];
+        while (m != 0u) {
+          const int i = q * 32 + __ffs(m) - 1;
+          m &= m - 1u;
+          fb = __fadd_rn(fb, recs[i * NS + jl]);
+        }
+      }
+      const float ai = __fadd_rn(__fmul_rn(v[u], vb), I[u]);
+      v[u] = __fsub_rn(__fadd_rn(ai, fb), sp[u] ? theta : 0.0f);
+      I[u] = In[u];
+    }
+  }
+  pdl_launch_dependents();
+}
+
+// Backward: CTA c owns source neurons i in [c NS, (c+1) NS) -- rec[slice, :] in smem
+// as recs[j][il] (conflict-free over il) -- and thread = (neuron, kRlSPT samples).
+// Per step: rc over every j from the exchanged G of this step (smem, broadcast;
+// fused multiply-adds: the backward is held to the 1e-4 bar, not bit-exactness),
+// the reverse LIF step, then G' of its neuron to every CTA's exchange slot.
+// The next step's dS / V are loaded while this step's rc sum runs.
+template <int kAct>
+__global__ void __launch_bounds__(512) k_rlif_bwd_cl(RlifBwdArgs a) {
+  extern __shared__ __align__(16) float rsm[];
+  const int NS = a.H_pad / kRlCl, SB = a.sb;
+  float* recs = rsm;                             // [H][NS]
+  float* gbuf = rsm + size_t(a.H) * NS;          // [2][H_pad][SB]
+  const uint32_t crank = cluster_ctarank();
+  const int tid = threadIdx.x;
+  const int il = tid % NS, sg = tid / NS;
+  const int i = int(crank) * NS + il;
+  const bool live = i < a.H;
+  const int b0 = blockIdx.y * SB + sg * kRlSPT;
+  pdl_wait();
+  for (int idx = tid; idx < a.H * NS; idx += blockDim.x) {
+    const int jj = idx / NS, c = int(crank) * NS + idx % NS;
+    recs[idx] = a.rec_t[size_t(jj) * a.H_pad + c];  // rec[c][jj] (0 for padded c)
+  }
+  for (int idx = tid; idx < 2 * a.H_pad * SB; idx += blockDim.x) gbuf[idx] = 0.0f;
+  const float vb = clip01(live ? a.beta[i * a.beta_stride] : 0.0f);
+  const float theta = a.theta;
+  const size_t cols_total = size_t(a.B) * a.T_pad;
+  const size_t plane = size_t(a.H_pad) * cols_total;
+  const uint32_t gslot = smem_u32(gbuf + size_t(i) * SB + sg * kRlSPT);
+  // sample s of the thread: element (t) at base + s * sstride + t * H_pad (s < nok)
+  const int nok = max(0, min(kRlSPT, a.B - b0));
+  const size_t sstride = size_t(a.T_pad) * a.H_pad;
+  const size_t rbase = size_t(nok > 0 ? b0 : 0) * sstride + i;
+  cluster_sync_all();
+  float G[kRlSPT], db[kRlSPT], dbias[kRlSPT], dSn[kRlSPT], Vn[kRlSPT];
+#pragma unroll
+  for (int s = 0; s < kRlSPT; ++s) {
+    G[s] = db[s] = dbias[s] = 0.0f;
+    const size_t o = rbase + s * sstride + size_t(a.T - 1) * a.H_pad;
+    dSn[s] = s < nok ? __ldg(a.ds + o) : 0.0f;
+    Vn[s] = s < nok ? __ldg(a.v_in + o) : 0.0f;
+  }
+  int par = 0;
+  for (int c0 = a.T_pad - 8; c0 >= 0; c0 -= 8) {
+    float x[kRlSPT][8];
+#pragma unroll
+    for (int e = 7; e >= 0; --e) {
+      const int t = c0 + e;
+#pragma unroll
+      for (int s = 0; s < kRlSPT; ++s) x[s][e] = G[s];
+      if (t >= a.T) continue;  // padded steps: G stays 0 (uniform over the cluster)
+      float dS[kRlSPT], V[kRlSPT];
+#pragma unroll
+      for (int s = 0; s < kRlSPT; ++s) {
+        dS[s] = dSn[s];
+        V[s] = Vn[s];
+        const size_t o = rbase + s * sstride + size_t(t - 1) * a.H_pad;
+        dSn[s] = (s < nok && t > 0) ? __ldg(a.ds + o) : 0.0f;
+        Vn[s] = (s < nok && t > 0) ? __ldg(a.v_in + o) : 0.0f;
+      }
+      float rc0 = 0.0f, rc1 = 0.0f, rc2 = 0.0f, rc3 = 0.0f;
+      const float* gp = gbuf + size_t(par) * a.H_pad * SB + sg * kRlSPT;
+#pragma unroll 8
+      for (int jj = 0; jj < a.H; ++jj) {
+        const float r = recs[jj * NS + il];
+        const float4 g4 = *reinterpret_cast<const float4*>(gp + jj * SB);
+        rc0 = __fmaf_rn(r, g4.x, rc0);
+        rc1 = __fmaf_rn(r, g4.y, rc1);
+        rc2 = __fmaf_rn(r, g4.z, rc2);
+        rc3 = __fmaf_rn(r, g4.w, rc3);
+      }
+      const float rc[kRlSPT] = {rc0, rc1, rc2, rc3};
+#pragma unroll
+      for (int s = 0; s < kRlSPT; ++s) {
+        const float gi = G[s];
+        const float gs = __fadd_rn(__fadd_rn(dS[s], __fmul_rn(-gi, theta)), rc[s]);
+        const float g = surrogate_t<kAct>(a.slope, a.aux, __fadd_rn(V[s], -theta));
+        db[s] = __fadd_rn(db[s], __fmul_rn(gi, V[s]));
+        dbias[s] = __fadd_rn(dbias[s], gi);
+        G[s] = live ? __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g)) : 0.0f;
+      }
+      const uint32_t dst = gslot + uint32_t((par ^ 1) * a.H_pad * SB) * 4u;
+#pragma unroll
+      for (int r = 0; r < kRlCl; ++r) st_cluster_v4(map_rank(dst, uint32_t(r)), G[0], G[1], G[2], G[3]);
+      cluster_sync_all();
+      par ^= 1;
+    }
+    if (live) {
+#pragma unroll
+      for (int s = 0; s < kRlSPT; ++s)
+        if (s < nok) {  // 8 steps of dI as 3 bf16 planes: one 16-byte store per plane
+          uint32_t h[4], m[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) split3_pack(x[s][e], x[s][e + 1], h[e / 2], m[e / 2], lo[e / 2]);
+          uint4* d = reinterpret_cast<uint4*>(a.di_planes + size_t(i) * cols_total + size_t(b0 + s) * a.T_pad + c0);
+          d[0] = make_uint4(h[0], h[1], h[2], h[3]);
+          d[plane / 8] = make_uint4(m[0], m[1], m[2], m[3]);
+          d[plane / 4] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int s = 0; s < kRlSPT; ++s)
+      if (s < nok) {
         a.dbeta_part[size_t(b0 + s) * a.H + i] = db[s];
         if (a.dbias_part != nullptr) a.dbias_part[size_t(b0 + s) * a.H + i] = dbias[s];
       }

@@ -23,7 +23,8 @@ def main():
     ap.add_argument("--config", default="c1")
     args = ap.parse_args()
     w = WORKLOADS[args.config]
-    eng = Engine(shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"]),
+    eng = Engine(shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"],
+                          cell=w.get("cell", "lif")),
                  TrainConfig(batch_size=w["B"], seed=0), w["T"])
     eng.synth_dataset(w["n_data"], seed=1)
     perm = eng.epoch_permutation(0, w["n_data"])

@@ -997,6 +997,9 @@ RLIF_CASES = [
                                cell=("lif", "rlif")), 3, 200, 2.0),
     ("rlif-alif-3hidden", Net(inp=50, hidden=(64, 48, 32), classes=6, act="triangular",
                               cell=("rlif", "alif", "lif")), 4, 33, 3.0),
+    # cluster scans (H_pad 256): two sample groups of the cluster, the second partial
+    ("rlif-256-cluster", Net(inp=100, hidden=(250,), classes=6, act="boxcar", bias=True,
+                             cell=("rlif",)), 20, 70, 2.0),
 ]
 
 
