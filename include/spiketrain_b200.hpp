@@ -82,12 +82,18 @@ struct LinearLayer {
 };
 enum class BetaMode { PerNeuron, LearnableScalar, Fixed };  // neuron.hpp:24
 
+// B200 extension (not in the reference): the DECLARED adaptive-threshold and
+// recurrent cells of BASELINE configs 2 and 4 (snn_engine.h snn_cell; checker
+// oracle/spiketrain_oracle.h).  The default keeps the reference's LIF.
+enum class CellKind { LIF = SNN_CELL_LIF, ALIF = SNN_CELL_ALIF, RLIF = SNN_CELL_RLIF };
+
 struct LIFLayer {
   std::vector<std::size_t> shape;
   ActivationDesc activation = {"superspike", 25.0, 0.0};
   BetaMode beta_mode = BetaMode::PerNeuron;
   double fixed_beta = 0.5;
   double threshold = 1.0;
+  CellKind cell = CellKind::LIF;  // extension field, last so reference aggregate inits still work
 };
 struct LILayer {
   std::vector<std::size_t> shape;
@@ -196,6 +202,7 @@ inline snn_network_desc describe(const NetworkSpec& spec) {
     d.aux = float(lif->activation.aux);
     d.beta_mode[i] = int32_t(lif->beta_mode);
     d.fixed_beta[i] = float(lif->fixed_beta);
+    d.cell[i] = int32_t(lif->cell);
   }
   const auto* lin = std::get_if<LinearLayer>(&s.layers[s.layers.size() - 2]);
   if (!lin || !std::holds_alternative<LILayer>(s.layers.back()))

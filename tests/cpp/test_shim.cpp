@@ -70,6 +70,24 @@ int main() {
     std::printf("toy: loss %.4f -> %.4f, acc %.3f, steps %llu\n", r.metrics.front().loss,
                 r.metrics.back().loss, r.metrics.back().accuracy, (unsigned long long)r.step);
   }
+  // the declared ALIF / RLIF cells (B200 extension) train the same toy problem
+  for (auto kind : {st::CellKind::ALIF, st::CellKind::RLIF}) {
+    const auto data = toy_data(16, 16, rng::from_seed(703));
+    st::TrainConfig cfg;
+    cfg.epochs = 30;
+    cfg.batch_size = 8;
+    cfg.lr = 5e-3;
+    cfg.seed = 1;
+    auto spec = toy_spec();
+    st::LIFLayer cell;
+    cell.cell = kind;
+    spec.layers[1] = cell;
+    const auto r = st::train(spec, cfg, data);
+    CHECK(r.metrics.back().loss < r.metrics.front().loss);
+    CHECK(r.metrics.back().accuracy >= 0.75);
+    std::printf("toy %s: loss %.4f -> %.4f, acc %.3f\n", kind == st::CellKind::ALIF ? "alif" : "rlif",
+                r.metrics.front().loss, r.metrics.back().loss, r.metrics.back().accuracy);
+  }
   // cmd_eval after training (commands.hpp:144-169): the trained toy separates its
   // own data; evaluation is forward only (no optimizer step)
   {
