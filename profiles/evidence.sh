@@ -1,6 +1,9 @@
 # Round-end evidence run on one B200 (gpurun): GPU tests, smoke, bench lines (C1 headline, C2, C4),
-# the reference arm, the ncu launch list and full captures of one training step.
+# the reference arm, the ncu launch list and full captures of one training step (summarised on
+# the box; only the C1 report is kept so gpurun_out stays under the 64 MiB copy-back limit).
+#   gpurun --timeout 2400 -- 'bash profiles/evidence.sh r01g'
 mkdir -p gpurun_out
+TAG=${1:-r01g}
 set -x
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
@@ -9,6 +12,13 @@ python bench.py --config c2 --steps 1000 > gpurun_out/bench_c2.json 2> gpurun_ou
 python bench.py --config c4 --steps 100 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/ref_c1.json 2> gpurun_out/ref_c1.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c1.csv python bench.py --steps 2 --warmup 3 --e2e-steps 2 --profile-steps 2 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --import-source on --clock-control none -c 7 -o gpurun_out/step_c1 python tests/prof_step.py --warmup 3 --steps 1 > gpurun_out/ncu_full.log 2>&1
-ncu --set full --import-source on --clock-control none -c 9 -o gpurun_out/step_c2 python tests/prof_step.py --warmup 3 --steps 1 --config c2 > gpurun_out/ncu_full2.log 2>&1
-tail -2 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log | tail -2
+ncu --set full --import-source on --clock-control none -c 8 -o gpurun_out/step_c1 python tests/prof_step.py --warmup 3 --steps 1 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none -c 9 -o gpurun_out/step_c2 python tests/prof_step.py --warmup 3 --steps 1 --config c2 > gpurun_out/ncu_full2.log 2>&1
+ncu --set full --clock-control none -c 11 -o gpurun_out/step_c4 python tests/prof_step.py --warmup 3 --steps 1 --config c4 > gpurun_out/ncu_full4.log 2>&1
+python profiles/summarize_ncu.py gpurun_out/step_c1.ncu-rep ${TAG} && mv profiles/${TAG}_ncu.json gpurun_out/
+python profiles/summarize_ncu.py gpurun_out/step_c2.ncu-rep ${TAG}_c2 && mv profiles/${TAG}_c2_ncu.json gpurun_out/
+python profiles/summarize_ncu.py gpurun_out/step_c4.ncu-rep ${TAG}_c4 && mv profiles/${TAG}_c4_ncu.json gpurun_out/
+rm -f gpurun_out/step_c2.ncu-rep gpurun_out/step_c4.ncu-rep
+du -sh gpurun_out/*
+tail -2 gpurun_out/pytest_gpu.log
+tail -1 gpurun_out/smoke.log

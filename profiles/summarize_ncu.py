@@ -53,7 +53,8 @@ def main(rep, tag):
                     pass
         tot = sum(stalls.values()) or 1.0
         top = sorted(stalls.items(), key=lambda x: -x[1])[:4]
-        ent = {"name": name, "duration_us": dur * (1e-3 if du == "ns" else 1.0),
+        ent = {"name": name, "duration_us": dur * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                                                    "msecond": 1e3}.get(du, 1.0),
                "dram_bytes": dram,
                "achieved_occupancy_pct": val(r, "sm__warps_active.avg.pct_of_peak_sustained_active")[0],
                "top_stalls": {k: round(v / tot, 3) for k, v in top}}
