@@ -636,6 +636,8 @@ struct snn_engine {
       CK(cudaFuncSetAttribute(k_rlif_fwd_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
       for (auto fn : {k_rlif_bwd_cl<0>, k_rlif_bwd_cl<1>, k_rlif_bwd_cl<2>, k_rlif_bwd_cl<3>, k_rlif_bwd_cl<4>})
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
+      for (auto fn : {k_rlif_bwd_tc<0>, k_rlif_bwd_tc<1>, k_rlif_bwd_tc<2>, k_rlif_bwd_tc<3>, k_rlif_bwd_tc<4>})
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rlif_bwd_tc_smem())));
       for (int l = 0; l < L; ++l)
         if (rlif(l) && rlif_cluster(l)) {
           rl_sb_fwd[l] = rlif_pick_sb(l, true);
@@ -994,6 +996,8 @@ struct snn_engine {
   }
   // RLIF scans on a cluster (rec slice in smem) when the slices are whole warps
   // and fit: H_pad 256 or 512 (SNN_RLIF_CL=1 forces the single-CTA kernels)
+  // the reverse scan's recurrent product on tcgen05 (SNN_RLIF_TC=1 keeps the FP32 form)
+  bool rlif_tc(int l) const { return env_int("SNN_RLIF_TC", 2) == 2 && H_pad[l] == 512; }
   bool rlif_cluster(int l) const {
     return env_int("SNN_RLIF_CL", 2) == 2 && (H_pad[l] == 256 || H_pad[l] == 512);
   }
@@ -1014,11 +1018,23 @@ struct snn_engine {
     ra.beta = params.p + entry_of(kEntryBeta, l).offset;
     ra.beta_stride = net.beta_mode[l] == 0 ? 1 : 0;
     ra.rec_t = rec_t[l].p;
+    ra.rec = params.p + entry_of(kEntryW, rec_j[l]).offset;
     ra.di_planes = di[l].p;
     ra.dbeta_part = dbeta[l].p;
     ra.dbias_part = net.bias ? dbias[l].p : nullptr;
     ra.B = B; ra.T = T; ra.T_pad = T_pad; ra.H = H[l]; ra.H_pad = H_pad[l];
     ra.theta = net.threshold; ra.slope = net.slope; ra.aux = net.aux;
+    if (rlif_tc(l)) {  // tcgen05 recurrent product (H_pad = 512)
+      const dim3 grid(kRlCl, unsigned((B + kRtN - 1) / kRtN));
+      switch (net.activation) {
+        case 1: launch_cluster(k_rlif_bwd_tc<1>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
+        case 2: launch_cluster(k_rlif_bwd_tc<2>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
+        case 3: launch_cluster(k_rlif_bwd_tc<3>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
+        case 4: launch_cluster(k_rlif_bwd_tc<4>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
+        default: launch_cluster(k_rlif_bwd_tc<0>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
+      }
+      return;
+    }
     if (rlif_cluster(l)) {
       const int sb = rl_sb_bwd[l];
       ra.sb = sb;

@@ -1991,6 +1991,7 @@ struct RlifBwdArgs {
   const float* beta;
   int beta_stride;
   const float* rec_t;          // [H][H_pad]: rec_t[j][i] = rec[i][j] (refreshed by Adam)
+  const float* rec;            // [H][H] the parameter (k_rlif_bwd_tc builds its bf16 planes)
   __nv_bfloat16* di_planes;    // out: dI planes [3][H_pad][B*T_pad]
   float* dbeta_part;           // [B][H]
   float* dbias_part;           // [B][H] or nullptr
@@ -2305,6 +2306,288 @@ __global__ void __launch_bounds__(512) k_rlif_bwd_cl(RlifBwdArgs a) {
       }
   }
   pdl_launch_dependents();
+}
+
+// ---------------------------------------------------------------------------
+// K3t  k_rlif_bwd_tc: the RLIF reverse scan with the per-step recurrent product on
+// tcgen05 (H_pad = 512).  Cluster of 8 CTAs x kRtN samples; CTA c owns the 64
+// source neurons of slice c.  Per step t (descending):
+//   rc[i][s] = sum_j rec[i][j] G_j(t+1)[s] as ONE M=128 x N=2 kRtN x K=512 chain:
+//   A = [rec_hi; rec_lo] of the slice stacked along M (bf16, K-major SW128, resident
+//   in smem), B = [G_hi; G_lo] of every neuron stacked along N, so
+//     D[il][s] + D[il][kRtN + s] + D[64 + il][s] = hi.hi + hi.lo + lo.hi
+//   (~2^-16 relative per product; the backward is held to the 1e-4 gradient bar;
+//   lo.lo in D[64 + il][kRtN + s] is added too).  Warps 0-1 read the hi rows (TMEM
+//   lanes 0-63), warps 2-3 the lo rows; they swap the partial sums of the other
+//   half's samples through smem, then thread (neuron, half) runs the reverse LIF step
+//   for kRtN/2 samples and writes G(t) as hi / lo bf16 into a local staging copy of
+//   its k-block of B (the slice is exactly k-block c, same SW128 layout).  One
+//   thread pushes the 4 KB k-block to every CTA with bulk shared->shared copies
+//   (TMA engine) completing the receiver's mbarrier transaction count -- no cluster
+//   barrier per step.  B is double-buffered: a CTA can only produce G(t) after every
+//   CTA's G(t+1) arrived, i.e. after every CTA finished the MMA that read the
+//   buffer it overwrites (and so did every copy out of a staging parity).
+// ---------------------------------------------------------------------------
+constexpr int kRtN = 16;                          // samples per cluster
+constexpr int kRtH = kRtN / 4;                    // samples per epilogue thread
+constexpr int kRtEpiWarps = 8;                    // warps 0-7 epilogue (0-3 also read TMEM)
+constexpr int kRtMmaWarp = kRtEpiWarps;           // warp 8: MMA issue + copies
+constexpr int kRtThreads = 32 * (kRtEpiWarps + 1);
+constexpr uint32_t kRtAPlane = 8u * 128u * 128u;  // 8 k-blocks x 128 rows (hi; lo) x 128 B
+constexpr uint32_t kRtSlice = 2u * kRtN * 128u;   // one k-block of B: [G_hi; G_lo] rows x 128 B
+constexpr uint32_t kRtBBuf = 8u * kRtSlice;       // 8 k-blocks
+__host__ __device__ constexpr size_t rlif_bwd_tc_smem() {
+  return 1024 + size_t(kRtAPlane) + 2 * size_t(kRtBBuf) + 2 * size_t(kRtSlice) + 2 * 64 * kRtN * 4 + 256;
+}
+// local shared -> remote shared bulk copy (TMA engine), completing tx bytes on the
+// receiver's mbarrier
+__device__ __forceinline__ void bulk_s2s(uint32_t rdst, uint32_t src, uint32_t bytes, uint32_t rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   rdst),
+               "r"(src), "r"(bytes), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+      "@P1 bra DONEC;\n\t"
+      "bra LAB_WAITC;\n\t"
+      "DONEC:\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+#ifndef SNN_RT_EXP
+#define SNN_RT_EXP 0  // timing experiments only: 1 no MMA, 2 no cross-CTA wait / copies, 3 no reverse step
+#endif
+template <int kAct>
+__global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
+  extern __shared__ uint8_t rt_raw[];
+  uint8_t* sm = align1024(rt_raw);
+  uint8_t* Ap = sm;                                    // [8 kb][128 rows][128 B]
+  uint8_t* Bp = sm + kRtAPlane;                        // [2 bufs][8 kb][2 kRtN rows][128 B]
+  uint8_t* gst = Bp + 2 * kRtBBuf;                     // [2 parities][2 kRtN rows][128 B]
+  float* xsum = reinterpret_cast<float*>(gst + 2 * kRtSlice);  // [2: hi, lo rows][64 neurons][kRtN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xsum + 2 * 64 * kRtN);  // [2] B buffer landed
+  uint64_t* dfull = full + 2;                          // MMA chain of the step done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
+  const uint32_t crank = cluster_ctarank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b0 = blockIdx.y * kRtN;
+  const int nok = max(0, min(kRtN, a.B - b0));
+  constexpr uint32_t kBytesPerStep = 8u * kRtSlice;  // every CTA's k-block
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(dfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<32>(tslot);
+  pdl_wait();
+  // A: row r < 64 = hi of neuron crank*64 + r, row 64 + r = its lo; K = source j
+  for (int idx = tid; idx < 64 * 64; idx += kRtThreads) {  // (neuron row, 8-element chunk of K)
+    const int il = idx / 64, ck = idx % 64, kb = ck / 8, c = ck % 8;
+    const int i = int(crank) * 64 + il;
+    uint32_t h[4], q[4];  // hi = bf16(x), lo = bf16(x - hi): ~16 significant bits together
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const int j = ck * 8 + e;
+      const float x0 = (i < a.H && j < a.H) ? a.rec[size_t(i) * a.H + j] : 0.0f;
+      const float x1 = (i < a.H && j + 1 < a.H) ? a.rec[size_t(i) * a.H + j + 1] : 0.0f;
+      const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+      const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
+      const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
+      h[e / 2] = (uint32_t(__bfloat16_as_ushort(h1)) << 16) | __bfloat16_as_ushort(h0);
+      q[e / 2] = (uint32_t(__bfloat16_as_ushort(l1)) << 16) | __bfloat16_as_ushort(l0);
+    }
+    const uint32_t kbo = uint32_t(kb) * 16384u;
+    st_shared_v4(smem_u32(Ap + kbo + sw128_off(uint32_t(il), uint32_t(c))), make_uint4(h[0], h[1], h[2], h[3]));
+    st_shared_v4(smem_u32(Ap + kbo + sw128_off(uint32_t(64 + il), uint32_t(c))), make_uint4(q[0], q[1], q[2], q[3]));
+  }
+  for (int idx = tid; idx < int(2 * kRtBBuf / 16); idx += kRtThreads)
+    st_shared_v4(smem_u32(Bp) + uint32_t(idx) * 16u, make_uint4(0u, 0u, 0u, 0u));
+  fence_async_smem();
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and B zeroed in every CTA before any copy
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  // epilogue: warp w < 4 reads TMEM lanes 32 w .. 32 w + 31 (rows 0-63 hi, 64-127 lo) and
+  // publishes the row sums of all samples; then warp w < 8 runs neuron il = 32 (w & 1) +
+  // lane for samples hs*kRtH .. (hs = w >> 1, a quarter of the cluster's samples)
+  const bool epi = warp < kRtEpiWarps;
+  const int il = 32 * (warp & 1) + lane, hs = warp >> 1;
+  const int i = int(crank) * 64 + il;
+  const bool live = epi && i < a.H;
+  const float vb = clip01(live ? a.beta[i * a.beta_stride] : 0.0f);
+  const float theta = a.theta;
+  const size_t cols_total = size_t(a.B) * a.T_pad;
+  const size_t plane = size_t(a.H_pad) * cols_total;
+  const size_t sstride = size_t(a.T_pad) * a.H_pad;
+  const int sb0 = hs * kRtH;  // first sample of this thread
+  const int nmine = max(0, min(kRtH, nok - sb0));
+  const size_t rbase = size_t(b0 + sb0) * sstride + (live ? i : 0);
+  float G[kRtH], db[kRtH], dbias[kRtH], dSn[kRtH], Vn[kRtH];
+#pragma unroll
+  for (int s = 0; s < kRtH; ++s) {
+    G[s] = db[s] = dbias[s] = 0.0f;
+    const size_t o = rbase + s * sstride + size_t(a.T - 1) * a.H_pad;
+    dSn[s] = (live && s < nmine) ? __ldg(a.ds + o) : 0.0f;
+    Vn[s] = (live && s < nmine) ? __ldg(a.v_in + o) : 0.0f;
+  }
+  const uint32_t stg_col = uint32_t(il & 7) * 2u;
+  const uint32_t idesc = idesc_bf16(128, 2 * kRtN, false, false);
+  uint32_t fph[2] = {0u, 0u}, dph = 0u;
+  int p = 0;
+  bool first = true;
+#if SNN_RT_EXP == 4
+  __shared__ long long tclk[16][8];
+  int nstep = 0;
+  const bool probe = blockIdx.x == 0 && blockIdx.y == 0;
+#define RT_CLK(k) if (probe && nstep < 16) tclk[nstep][k] = globaltimer();
+#else
+#define RT_CLK(k)
+#endif
+  for (int c0 = a.T_pad - 4; c0 >= 0; c0 -= 4) {
+    float x[kRtH][4];
+#pragma unroll
+    for (int e = 3; e >= 0; --e) {
+      const int t = c0 + e;
+#pragma unroll
+      for (int s = 0; s < kRtH; ++s) x[s][e] = G[s];
+      if (t >= a.T) continue;  // padded steps: uniform over the cluster
+      if (warp == kRtMmaWarp) {
+        if (elect_one()) {
+          RT_CLK(0)
+          if (!first && SNN_RT_EXP != 2) {
+            mbar_wait_cluster(&full[p], fph[p]);
+            fph[p] ^= 1u;
+          }
+          RT_CLK(1)
+          // B arrived by bulk copies (async proxy) and A was fenced once: no proxy fence here
+          tc_fence_after();
+          if (t > 0 && SNN_RT_EXP != 2) mbar_arrive_expect_tx(&full[p ^ 1], kBytesPerStep);
+          // descriptors advance by (byte offset >> 4) in their start-address field
+          const uint64_t ad0 = sdesc_sw128(smem_u32(Ap), 16, 1024);
+          const uint64_t bd0 = sdesc_sw128(smem_u32(Bp) + uint32_t(p) * kRtBBuf, 16, 1024);
+#pragma unroll
+          for (int kb = 0; kb < (SNN_RT_EXP == 1 ? 0 : 8); ++kb) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              umma_bf16(tmem, ad0 + uint64_t((kb * 16384 + ks * 32) >> 4),
+                        bd0 + uint64_t((kb * int(kRtSlice) + ks * 32) >> 4), idesc, (kb | ks) != 0);
+          }
+          umma_commit(dfull);
+          RT_CLK(2)
+        }
+        __syncwarp();
+      }
+      first = false;
+      mbar_wait(dfull, dph);
+      if (tid == 0) { RT_CLK(3) }
+      dph ^= 1u;
+      tc_fence_after();
+      if (epi) {
+        if (warp < 4) {  // row sums D[row][s] + D[row][kRtN + s] of every sample -> smem
+          uint32_t r[32];
+          tmem_ld32(tmem + (uint32_t(warp * 32) << 16), r);
+          tmem_ld_wait();
+          float* xs = xsum + (warp >> 1) * (64 * kRtN) + il * kRtN;
+#pragma unroll
+          for (int s = 0; s < kRtN; s += 4)
+            *reinterpret_cast<float4*>(xs + s) =
+                make_float4(__uint_as_float(r[s]) + __uint_as_float(r[kRtN + s]),
+                            __uint_as_float(r[s + 1]) + __uint_as_float(r[kRtN + s + 1]),
+                            __uint_as_float(r[s + 2]) + __uint_as_float(r[kRtN + s + 2]),
+                            __uint_as_float(r[s + 3]) + __uint_as_float(r[kRtN + s + 3]));
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kRtEpiWarps) : "memory");
+        if (tid == 0) { RT_CLK(4) }
+        if (SNN_RT_EXP != 3) {
+          const float4 hs4 = *reinterpret_cast<const float4*>(xsum + il * kRtN + sb0);
+          const float4 ls4 = *reinterpret_cast<const float4*>(xsum + 64 * kRtN + il * kRtN + sb0);
+          const float hsum[4] = {hs4.x, hs4.y, hs4.z, hs4.w}, lsum[4] = {ls4.x, ls4.y, ls4.z, ls4.w};
+#pragma unroll
+          for (int s = 0; s < kRtH; ++s) {
+            const float rc = hsum[s] + lsum[s];
+            const float dS = dSn[s], V = Vn[s];
+            const size_t o = rbase + s * sstride + size_t(t - 1) * a.H_pad;
+            dSn[s] = (live && s < nmine && t > 0) ? __ldg(a.ds + o) : 0.0f;
+            Vn[s] = (live && s < nmine && t > 0) ? __ldg(a.v_in + o) : 0.0f;
+            const float gi = G[s];
+            const float gs = __fadd_rn(__fadd_rn(dS, __fmul_rn(-gi, theta)), rc);
+            const float g = surrogate_t<kAct>(a.slope, a.aux, __fadd_rn(V, -theta));
+            db[s] = __fadd_rn(db[s], __fmul_rn(gi, V));
+            dbias[s] = __fadd_rn(dbias[s], gi);
+            G[s] = live ? __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g)) : 0.0f;
+            if (t > 0) {  // G(t) as hi / lo bf16 into staging parity p ^ 1: rows s / kRtN + s
+              const __nv_bfloat16 h = __float2bfloat16_rn(G[s]);
+              const __nv_bfloat16 lo = __float2bfloat16_rn(G[s] - __bfloat162float(h));
+              const uint32_t base = uint32_t(p ^ 1) * kRtSlice + stg_col;
+              const uint32_t c = uint32_t(il >> 3);
+              *reinterpret_cast<__nv_bfloat16*>(gst + base + sw128_off(uint32_t(sb0 + s), c)) = h;
+              *reinterpret_cast<__nv_bfloat16*>(gst + base + sw128_off(uint32_t(kRtN + sb0 + s), c)) = lo;
+            }
+          }
+        }
+        fence_async_smem();  // staging -> visible to the bulk copies
+        if (tid == 0) { RT_CLK(5) }
+      }
+      tc_fence_before();
+      __syncthreads();  // G(t) staged; D read before the next MMA chain; xsum reusable
+      if (tid == 0) { RT_CLK(6) }
+      if (warp == kRtMmaWarp && t > 0 && SNN_RT_EXP != 2 && lane < kRlCl) {
+        // G(t) of this slice (k-block crank) to every CTA's B buffer p ^ 1: lane r -> rank r
+        const uint32_t src = smem_u32(gst) + uint32_t(p ^ 1) * kRtSlice;
+        const uint32_t dst = smem_u32(Bp) + uint32_t(p ^ 1) * kRtBBuf + crank * kRtSlice;
+        const uint32_t bar = smem_u32(full) + 8u * uint32_t(p ^ 1);
+        bulk_s2s(map_rank(dst, uint32_t(lane)), src, kRtSlice, map_rank(bar, uint32_t(lane)));
+        if (lane == 0) { RT_CLK(7) }
+      }
+      p ^= 1;
+#if SNN_RT_EXP == 4
+      ++nstep;
+#endif
+    }
+    if (live) {
+#pragma unroll
+      for (int s = 0; s < kRtH; ++s)
+        if (s < nmine) {  // 4 steps of dI as 3 bf16 planes: one 8-byte store per plane
+          uint32_t h[2], m[2], lo[2];
+          split3_pack(x[s][0], x[s][1], h[0], m[0], lo[0]);
+          split3_pack(x[s][2], x[s][3], h[1], m[1], lo[1]);
+          uint2* d = reinterpret_cast<uint2*>(a.di_planes + size_t(i) * cols_total + size_t(b0 + sb0 + s) * a.T_pad + c0);
+          d[0] = make_uint2(h[0], h[1]);
+          d[plane / 4] = make_uint2(m[0], m[1]);
+          d[plane / 2] = make_uint2(lo[0], lo[1]);
+        }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int s = 0; s < kRtH; ++s)
+      if (s < nmine) {
+        a.dbeta_part[size_t(b0 + sb0 + s) * a.H + i] = db[s];
+        if (a.dbias_part != nullptr) a.dbias_part[size_t(b0 + sb0 + s) * a.H + i] = dbias[s];
+      }
+  }
+#if SNN_RT_EXP == 4
+  if (probe && tid == 0)
+    for (int k = 1; k < 16; ++k)
+      printf("step %d: wait_full %lld mma %lld dfull %lld ld+swap %lld compute %lld sync %lld copies %lld | step %lld\n", k,
+             tclk[k][1] - tclk[k][0], tclk[k][2] - tclk[k][1], tclk[k][3] - tclk[k][2], tclk[k][4] - tclk[k][3],
+             tclk[k][5] - tclk[k][4], tclk[k][6] - tclk[k][5], tclk[k][7] - tclk[k][6], tclk[k][0] - tclk[k - 1][0]);
+#endif
+  pdl_launch_dependents();
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while a peer may still address its smem
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<32>(tmem);
+  }
 }
 
 // ============================================================================

@@ -764,20 +764,24 @@ def test_single_rank_peer_tail_matches_fused_tail(orc):
     assert np.array_equal(e1.get_params(), e2.get_params())
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_tail_ranks_emulated_on_one_gpu(orc, world):
+@pytest.mark.parametrize("world,cell", [(2, ()), (3, ()), (2, ("alif", "rlif"))],
+                         ids=["2ranks", "3ranks", "2ranks-alif-rlif"])
+def test_peer_tail_ranks_emulated_on_one_gpu(orc, world, cell):
     """`world` ranks of the peer tail on one GPU (B200_PROFILING: never let ranks
     wait on each other as separate launches -- every rank runs its part before the
     cross-rank wait, then every rank runs the tail).  Replicas stay bit-identical and
     match full-global-batch training on the oracle."""
     from paper_2402_18994_b200 import Engine
-    net = Net(inp=40, hidden=(24, 20), classes=5, act="superspike")
+    net = Net(inp=40, hidden=(24, 20), classes=5, act="superspike", cell=cell)
     B, T, N = 4, 23, 48
     x, y = orc.synth_raster(5, N, T, 40, 8)
     pk = orc.pack_time(x)
     engs = [make_engine(net, B, T, seed=5) for _ in range(world)]
     Engine.peer_attach_local(engs)
-    p0 = engs[0].get_params() * np.float32(3.0)
+    p0 = engs[0].get_params()
+    for name, off, size in orc.entries(net):  # louder weights (gamma / beta keep their init)
+        if name.endswith((".w", ".rec")):
+            p0[off:off + size] *= np.float32(3.0)
     for e in engs:
         e.stage_dataset(pk, y)
         e.set_params(p0)
