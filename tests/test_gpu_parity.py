@@ -1060,3 +1060,48 @@ def test_rlif_step_parity(orc, case):
     l3, _ = eng.train_step(rows)
     lo3, _ = orc.train_step(net, st, pk, T, y)
     assert abs(l3 - lo3) <= 1e-3 * abs(lo3)
+
+
+def test_declared_cells_checkpoint_apply_monitor(orc, tmp_path):
+    """The declared cells through the rest of the API: .spkc save / load with the
+    gamma and rec entries (resume bit-exact), apply, evaluate, a monitored ALIF layer
+    with the activity regularizer, and SGD."""
+    from paper_2402_18994_b200 import ShapeError
+    net = Net(inp=40, hidden=(24, 256), classes=5, act="superspike", cell=("alif", "rlif"),
+              monitor=(0,))
+    B, T = 16, 30
+    x, y = orc.synth_raster(5, 32, T, 40, 4)
+    pk = orc.pack_time(x)
+    kw = dict(optimizer="sgd", lambda_low=0.5, lambda_high=0.5, f_min=0.05, f_max=0.2)
+    a = make_engine(net, B, T, seed=3, **kw)
+    a.stage_dataset(pk, y)
+    p0 = a.get_params()
+    for n, o, s in orc.entries(net):
+        if n.endswith(".w"):
+            p0[o:o + s] *= np.float32(3.0)
+    a.set_params(p0)
+    rows = [np.arange(16 * (i % 2), 16 * (i % 2) + 16, dtype=np.uint32) for i in range(5)]
+    for r in rows[:2]:
+        a.train_step(r)
+    path = str(tmp_path / "cells.spkc")
+    a.save_checkpoint(path, "declared cells")
+    b = make_engine(net, B, T, seed=11, **kw)
+    b.stage_dataset(pk, y)
+    assert b.load_checkpoint(path) == "declared cells"
+    assert np.array_equal(a.get_params(), b.get_params())
+    for r in rows[2:]:
+        assert a.train_step(r) == b.train_step(r)
+    assert np.array_equal(a.get_params(), b.get_params())
+    # forward-only entries on the trained declared network agree with the oracle
+    params = a.get_params()
+    ref = orc.forward_backward(net, params, pk[rows[0]], T, y[rows[0]], want_grads=False,
+                               want_trace=True, want_spikes=True)
+    assert relnorm(a.apply(rows[0]), ref["trace"]) <= REL_TOL
+    counts = a.monitor_counts(0)
+    assert (counts == ref["spikes"][0].sum(axis=1)).mean() >= 0.999
+    acc, loss = a.evaluate(np.arange(32, dtype=np.uint32))
+    assert 0.0 <= acc <= 1.0 and np.isfinite(loss)
+    # a LIF network cannot load the declared network's checkpoint (entry shapes differ)
+    c = make_engine(Net(inp=40, hidden=(24, 256), classes=5, monitor=(0,)), B, T)
+    with pytest.raises(ShapeError):
+        c.load_checkpoint(path)
