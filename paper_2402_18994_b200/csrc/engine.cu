@@ -632,8 +632,8 @@ struct snn_engine {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     {
-      CK(cudaFuncSetAttribute(k_rlif_fwd_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
-      CK(cudaFuncSetAttribute(k_rlif_fwd_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+      for (auto fn : {k_rlif_fwd_cl<1>, k_rlif_fwd_cl<2>})
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
       for (auto fn : {k_rlif_bwd_cl<0>, k_rlif_bwd_cl<1>, k_rlif_bwd_cl<2>, k_rlif_bwd_cl<3>, k_rlif_bwd_cl<4>})
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
       for (auto fn : {k_rlif_bwd_tc<0>, k_rlif_bwd_tc<1>, k_rlif_bwd_tc<2>, k_rlif_bwd_tc<3>, k_rlif_bwd_tc<4>})
@@ -964,14 +964,14 @@ struct snn_engine {
   }
   // samples per cluster of the RLIF cluster scans: the smallest that keeps every
   // cluster of the grid co-resident (one wave; cudaOccupancyMaxActiveClusters)
-  static constexpr int kRlSmemMax = 227 * 1024;
+  static constexpr int kRlSmemMax = 220 * 1024;
   int rl_sb_fwd[SNN_MAX_HIDDEN]{}, rl_sb_bwd[SNN_MAX_HIDDEN]{};
   int rlif_pick_sb(int l, bool fwd) {
     const int NS = H_pad[l] / kRlCl;
     int best = 0;
     for (int sb = kRlSPT; sb <= kRlSBMax; sb += kRlSPT) {
       const size_t smem = fwd ? rlif_fwd_cl_smem(H[l], H_pad[l], sb) : rlif_bwd_cl_smem(H[l], H_pad[l], sb);
-      const int threads = fwd ? NS * sb / kRlFPT : NS * sb / kRlSPT;
+      const int threads = fwd ? 32 * sb / kRlFPT : NS * sb / kRlSPT;
       if (smem > size_t(kRlSmemMax) || threads > (fwd ? 1024 : 512)) break;
       const int clusters = (B + sb - 1) / sb;
       cudaLaunchConfig_t c{};
@@ -986,7 +986,7 @@ struct snn_engine {
       c.attrs = at;
       c.numAttrs = 1;
       int active = 0;
-      if (fwd) CK(cudaOccupancyMaxActiveClusters(&active, k_rlif_fwd_cl, &c));
+      if (fwd) CK(cudaOccupancyMaxActiveClusters(&active, NS == 64 ? k_rlif_fwd_cl<2> : k_rlif_fwd_cl<1>, &c));
       else CK(cudaOccupancyMaxActiveClusters(&active, k_rlif_bwd_cl<0>, &c));
       best = sb;
       if (clusters <= active) break;
@@ -1248,9 +1248,9 @@ struct snn_engine {
         if (rlif_cluster(l)) {
           const int sb = rl_sb_fwd[l];
           ra.sb = sb;
-          launch_cluster(k_rlif_fwd_cl, dim3(kRlCl, unsigned((B + sb - 1) / sb)),
-                         dim3(unsigned(H_pad[l] / kRlCl * sb / kRlFPT)), rlif_fwd_cl_smem(H[l], H_pad[l], sb),
-                         kRlCl, ra);
+          launch_cluster(H_pad[l] == 512 ? k_rlif_fwd_cl<2> : k_rlif_fwd_cl<1>,
+                         dim3(kRlCl, unsigned((B + sb - 1) / sb)), dim3(unsigned(32 * sb / kRlFPT)),
+                         rlif_fwd_cl_smem(H[l], H_pad[l], sb), kRlCl, ra);
         } else
           launch(k_rlif_fwd, dim3(B), dim3(H_pad[l]), 0, ra);
         mark(evs, "rlif_fwd", l);

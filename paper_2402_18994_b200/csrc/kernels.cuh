@@ -2089,7 +2089,9 @@ constexpr int kRlSBMax = 32;  // samples per cluster (runtime a.sb <= this, mult
 constexpr int kRlSPT = 4;     // backward: samples per thread
 constexpr int kRlFPT = 2;     // forward: samples per thread
 __host__ __device__ constexpr size_t rlif_fwd_cl_smem(int H, int H_pad, int sb) {
-  return size_t(H) * (H_pad / kRlCl) * 4 + size_t(2) * sb * (H_pad / 32) * 4;
+  // rec slice + double-buffered spike words + 2 mbarriers + per-warp source lists
+  return size_t(H) * (H_pad / kRlCl) * 4 + size_t(2) * sb * (H_pad / 32) * 4 + 16 +
+         size_t(sb / kRlFPT) * kRlFPT * H_pad * 2;
 }
 __host__ __device__ constexpr size_t rlif_bwd_cl_smem(int H, int H_pad, int sb) {
   return size_t(H) * (H_pad / kRlCl) * 4 + size_t(2) * H_pad * sb * 4;
@@ -2110,90 +2112,195 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// remote shared store that completes 4 tx bytes on the receiver's mbarrier
+__device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAITW:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+      "@P1 bra DONEW;\n\t"
+      "bra LAB_WAITW;\n\t"
+      "DONEW:\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float x, float y, float z, float w) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x), "f"(y), "f"(z),
                "f"(w)
                : "memory");
 }
 
+#ifndef SNN_RT_EXP
+#define SNN_RT_EXP 0  // timing experiments only (RLIF scans): 1 no MMA, 2 no cross-CTA wait /
+                      // copies, 3 no reverse step, 4 / 5 backward / forward phase clocks
+#endif
 // Forward: CTA c of the cluster owns output neurons [c NS, (c+1) NS) of a.sb
-// samples; thread = (neuron, kRlFPT samples s, s + sb/kRlFPT, ...).  Its smem
-// holds rec[:, slice] (rows i).  Same statements and ascending source order as
-// k_rlif_fwd: bit-identical.
+// samples.  Lane l of a warp owns neurons l + 32 h (h < kNPT = NS / 32) of one
+// sample group (kRlFPT samples s, s + sb/kRlFPT, ...); its smem holds rec[:, slice]
+// as recs[i][kNPT l + h], so one vector load per spiking source feeds all its
+// neurons.  Same statements and ascending source order as k_rlif_fwd: bit-identical.
+template <int kNPT>
 __global__ void __launch_bounds__(1024) k_rlif_fwd_cl(RlifFwdArgs a) {
   extern __shared__ __align__(16) float rsm[];
-  const int NS = a.H_pad / kRlCl, nw = a.H_pad / 32, SB = a.sb, SBT = a.sb / kRlFPT;
-  float* recs = rsm;                                                     // [H][NS]
+  constexpr int NS = 32 * kNPT;
+  const int nw = a.H_pad / 32, SB = a.sb, SBT = a.sb / kRlFPT;
+  float* recs = rsm;                                                     // [H][NS] permuted
   uint32_t* words = reinterpret_cast<uint32_t*>(rsm + size_t(a.H) * NS);  // [2][SB][nw]
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(words + 2 * SB * nw);     // [2] words of a step landed
   const uint32_t crank = cluster_ctarank();
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int jl = tid % NS, s0 = tid / NS;
-  const int j = int(crank) * NS + jl;
+  const int tid = threadIdx.x, lane = tid & 31, s0 = tid >> 5;
+  // this warp's ascending spiking-source lists, one per sample it owns
+  uint16_t* slist = reinterpret_cast<uint16_t*>(wfull + 2) + size_t(s0) * kRlFPT * a.H_pad;
+  if (tid == 0) {
+    mbar_init(&wfull[0], 1);
+    mbar_init(&wfull[1], 1);
+    fence_barrier_init();
+  }
   pdl_wait();
   for (int idx = tid; idx < a.H * NS; idx += blockDim.x) {
-    const int i = idx / NS, c = int(crank) * NS + idx % NS;
+    const int i = idx / NS, q = idx % NS;                    // q = kNPT l + h
+    const int c = int(crank) * NS + (q / kNPT) + 32 * (q % kNPT);
     recs[idx] = c < a.H ? a.rec[size_t(i) * a.H + c] : 0.0f;
   }
-  const float vb = clip01(j < a.H ? a.beta[j * a.beta_stride] : 0.0f);
   const float theta = a.theta, ntheta = -a.theta;
   const size_t tp_words = size_t(a.B) * a.T_pad / 32;
-  const int wi = (int(crank) * NS + (jl & ~31)) / 32;  // this warp's spike word
+  int j[kNPT];
+  float vb[kNPT];
+#pragma unroll
+  for (int h = 0; h < kNPT; ++h) {
+    j[h] = int(crank) * NS + lane + 32 * h;
+    vb[h] = clip01(j[h] < a.H ? a.beta[j[h] * a.beta_stride] : 0.0f);
+  }
+  const int wi0 = int(crank) * kNPT;  // the slice's first spike word
   int b[kRlFPT];
   bool bl[kRlFPT];
-  const float* ip[kRlFPT];
-  float* vp[kRlFPT];
-  float v[kRlFPT], I[kRlFPT];
-  uint32_t tmask[kRlFPT];
+  size_t base[kRlFPT];
+  float v[kRlFPT][kNPT], I[kRlFPT][kNPT];
+  uint32_t tmask[kRlFPT][kNPT];
 #pragma unroll
   for (int u = 0; u < kRlFPT; ++u) {
     b[u] = blockIdx.y * SB + s0 + u * SBT;
     bl[u] = b[u] < a.B;
-    const size_t base = (size_t(bl[u] ? b[u] : 0) * a.T_pad) * a.H_pad + j;
-    ip[u] = a.i_in + base;
-    vp[u] = a.v_out + base;
-    v[u] = 0.0f;
-    tmask[u] = 0u;
-    I[u] = bl[u] ? __ldg(ip[u]) : 0.0f;
+    base[u] = (size_t(bl[u] ? b[u] : 0) * a.T_pad) * a.H_pad;
+#pragma unroll
+    for (int h = 0; h < kNPT; ++h) {
+      v[u][h] = 0.0f;
+      tmask[u][h] = 0u;
+      I[u][h] = bl[u] ? __ldg(a.i_in + base[u] + j[h]) : 0.0f;
+    }
   }
-  cluster_sync_all();
+  cluster_sync_all();  // every CTA's barriers initialised before any remote store
+  // per step the spike words go to every CTA with st.async completing the receiver's
+  // mbarrier (SB * nw words per step) -- no cluster barrier, no fence over the
+  // step's global stores.  Slot reuse two steps later is safe: a CTA sends step t+2
+  // only after receiving every CTA's step t+1 words, each sent after its step t gather.
+  const uint32_t step_bytes = uint32_t(SB * nw) * 4u;
+  const uint32_t wbar0 = smem_u32(wfull);
+#if SNN_RT_EXP == 5
+  __shared__ long long fclk[24][4];
+  const bool fprobe = blockIdx.x == 0 && blockIdx.y == 0 && tid == 0;
+#define RF_CLK(k) if (fprobe && t < 24) fclk[t][k] = globaltimer();
+#else
+#define RF_CLK(k)
+#endif
   for (int t = 0; t < a.T_pad; ++t) {
     const int par = t & 1;
-    bool sp[kRlFPT];
-    float In[kRlFPT];
+    RF_CLK(0)
+    if (tid == 0) mbar_arrive_expect_tx(&wfull[par], step_bytes);
+    bool sp[kRlFPT][kNPT];
+    float In[kRlFPT][kNPT];
 #pragma unroll
-    for (int u = 0; u < kRlFPT; ++u) {
-      In[u] = (bl[u] && t + 1 < a.T_pad) ? __ldg(ip[u] + size_t(t + 1) * a.H_pad) : 0.0f;
-      if (bl[u]) vp[u][size_t(t) * a.H_pad] = v[u];
-      sp[u] = __fadd_rn(v[u], ntheta) >= 0.0f && j < a.H && t < a.T && bl[u];
-      const uint32_t bal = __ballot_sync(0xffffffffu, sp[u]);
-      const uint32_t slot = smem_u32(words + (par * SB + s0 + u * SBT) * nw + wi);
-      if (lane < kRlCl) st_cluster_u32(map_rank(slot, uint32_t(lane)), bal);  // lane r -> rank r
-      if (lane == 0 && bl[u]) a.s_np[(size_t(b[u]) * a.T_pad + t) * nw + wi] = bal;
-      tmask[u] |= uint32_t(sp[u]) << (t & 31);
-      if ((t & 31) == 31) {
-        if (bl[u]) a.s_tp[size_t(j) * tp_words + size_t(b[u]) * (a.T_pad / 32) + t / 32] = tmask[u];
-        tmask[u] = 0u;
-      }
-    }
-    cluster_sync_all();
+    for (int u = 0; u < kRlFPT; ++u)
 #pragma unroll
-    for (int u = 0; u < kRlFPT; ++u) {
-      float fb = 0.0f;
-      const uint32_t* wp = words + (par * SB + s0 + u * SBT) * nw;
-      for (int q = 0; q < nw; ++q) {
-        uint32_t m = wp[q];
-        while (m != 0u) {
-          const int i = q * 32 + __ffs(m) - 1;
-          m &= m - 1u;
-          fb = __fadd_rn(fb, recs[i * NS + jl]);
+      for (int h = 0; h < kNPT; ++h) {
+        const size_t o = base[u] + size_t(t) * a.H_pad + j[h];
+        In[u][h] = (bl[u] && t + 1 < a.T_pad) ? __ldg(a.i_in + o + a.H_pad) : 0.0f;
+        if (bl[u]) a.v_out[o] = v[u][h];
+        sp[u][h] = __fadd_rn(v[u][h], ntheta) >= 0.0f && j[h] < a.H && t < a.T && bl[u];
+        const uint32_t bal = __ballot_sync(0xffffffffu, sp[u][h]);
+        const uint32_t slot = smem_u32(words + (par * SB + s0 + u * SBT) * nw + wi0 + h);
+        if (lane < kRlCl)  // lane r -> rank r
+          st_async_u32(map_rank(slot, uint32_t(lane)), bal, map_rank(wbar0 + 8u * uint32_t(par), uint32_t(lane)));
+        if (lane == 0 && bl[u]) a.s_np[(size_t(b[u]) * a.T_pad + t) * nw + wi0 + h] = bal;
+        tmask[u][h] |= uint32_t(sp[u][h]) << (t & 31);
+        if ((t & 31) == 31) {
+          if (bl[u]) a.s_tp[size_t(j[h]) * tp_words + size_t(b[u]) * (a.T_pad / 32) + t / 32] = tmask[u][h];
+          tmask[u][h] = 0u;
         }
       }
-      const float ai = __fadd_rn(__fmul_rn(v[u], vb), I[u]);
-      v[u] = __fsub_rn(__fadd_rn(ai, fb), sp[u] ? theta : 0.0f);
-      I[u] = In[u];
+    RF_CLK(1)
+    mbar_wait_acq_cluster(&wfull[par], uint32_t(t >> 1) & 1u);
+    RF_CLK(2)
+#pragma unroll
+    for (int u = 0; u < kRlFPT; ++u) {
+      float fb[kNPT];
+#pragma unroll
+      for (int h = 0; h < kNPT; ++h) fb[h] = 0.0f;
+      // the warp turns the sample's words into an ascending source list once (lane q
+      // expands word q at its exclusive prefix), then every lane walks the list
+      const uint32_t* wp = words + (par * SB + s0 + u * SBT) * nw;
+      uint16_t* li = slist + u * a.H_pad;
+      const uint32_t wq = lane < nw ? wp[lane] : 0u;
+      const int cq = __popc(wq);
+      int pre = cq;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, pre, d);
+        if (lane >= d) pre += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      pre -= cq;
+      for (uint32_t m = wq; m != 0u; m &= m - 1u) li[pre++] = uint16_t(lane * 32 + __ffs(m) - 1);
+      __syncwarp();
+      int k = 0;
+      for (; k + 4 <= total; k += 4) {
+        const uint2 q4 = *reinterpret_cast<const uint2*>(li + k);  // 4 indices, broadcast
+        const int i4[4] = {int(q4.x & 0xFFFFu), int(q4.x >> 16), int(q4.y & 0xFFFFu), int(q4.y >> 16)};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if constexpr (kNPT == 2) {
+            const float2 r2 = *reinterpret_cast<const float2*>(recs + i4[e] * NS + 2 * lane);
+            fb[0] = __fadd_rn(fb[0], r2.x);
+            fb[1] = __fadd_rn(fb[1], r2.y);
+          } else {
+            fb[0] = __fadd_rn(fb[0], recs[i4[e] * NS + lane]);
+          }
+        }
+      }
+      for (; k < total; ++k) {
+        const int i = li[k];
+        if constexpr (kNPT == 2) {
+          const float2 r2 = *reinterpret_cast<const float2*>(recs + i * NS + 2 * lane);
+          fb[0] = __fadd_rn(fb[0], r2.x);
+          fb[1] = __fadd_rn(fb[1], r2.y);
+        } else {
+          fb[0] = __fadd_rn(fb[0], recs[i * NS + lane]);
+        }
+      }
+      __syncwarp();  // the list is rebuilt next step
+#pragma unroll
+      for (int h = 0; h < kNPT; ++h) {
+        const float ai = __fadd_rn(__fmul_rn(v[u][h], vb[h]), I[u][h]);
+        v[u][h] = __fsub_rn(__fadd_rn(ai, fb[h]), sp[u][h] ? theta : 0.0f);
+        I[u][h] = In[u][h];
+      }
     }
+    RF_CLK(3)
   }
+#if SNN_RT_EXP == 5
+  if (fprobe)
+    for (int k = 1; k < 24; ++k)
+      printf("fwd step %d: send %lld wait %lld gather %lld | step %lld\n", k, fclk[k][1] - fclk[k][0],
+             fclk[k][2] - fclk[k][1], fclk[k][3] - fclk[k][2], fclk[k][0] - fclk[k - 1][0]);
+#endif
   pdl_launch_dependents();
+  cluster_sync_all();  // no CTA leaves while a peer may still address its smem
 }
 
 // Backward: CTA c owns source neurons i in [c NS, (c+1) NS) -- rec[slice, :] in smem
@@ -2360,9 +2467,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-#ifndef SNN_RT_EXP
-#define SNN_RT_EXP 0  // timing experiments only: 1 no MMA, 2 no cross-CTA wait / copies, 3 no reverse step
-#endif
 template <int kAct>
 __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
   extern __shared__ uint8_t rt_raw[];
