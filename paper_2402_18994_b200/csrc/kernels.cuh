@@ -2435,16 +2435,35 @@ __global__ void __launch_bounds__(512) k_rlif_bwd_cl(RlifBwdArgs a) {
 //   CTA's G(t+1) arrived, i.e. after every CTA finished the MMA that read the
 //   buffer it overwrites (and so did every copy out of a staging parity).
 // ---------------------------------------------------------------------------
-constexpr int kRtN = 16;                          // samples per cluster
+constexpr int kRtN = 24;                          // samples per cluster (11 clusters at B=256: one wave)
 constexpr int kRtH = kRtN / 4;                    // samples per epilogue thread
 constexpr int kRtEpiWarps = 8;                    // warps 0-7 epilogue (0-3 also read TMEM)
 constexpr int kRtMmaWarp = kRtEpiWarps;           // warp 8: MMA issue + copies
 constexpr int kRtThreads = 32 * (kRtEpiWarps + 1);
-constexpr uint32_t kRtAPlane = 8u * 128u * 128u;  // 8 k-blocks x 128 rows (hi; lo) x 128 B
 constexpr uint32_t kRtSlice = 2u * kRtN * 128u;   // one k-block of B: [G_hi; G_lo] rows x 128 B
 constexpr uint32_t kRtBBuf = 8u * kRtSlice;       // 8 k-blocks
+constexpr uint32_t kRtACol = 256;                 // A = [rec_hi; rec_lo] in TMEM columns 256..511
 __host__ __device__ constexpr size_t rlif_bwd_tc_smem() {
-  return 1024 + size_t(kRtAPlane) + 2 * size_t(kRtBBuf) + 2 * size_t(kRtSlice) + 2 * 64 * kRtN * 4 + 256;
+  return 1024 + 2 * size_t(kRtBBuf) + 2 * size_t(kRtSlice) + 2 * 64 * kRtN * 4 + 256;
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T (A-in-TMEM form: row m on lane m, K pairs per column)
+__device__ __forceinline__ void umma_bf16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
 }
 // local shared -> remote shared bulk copy (TMA engine), completing tx bytes on the
 // receiver's mbarrier
@@ -2471,8 +2490,7 @@ template <int kAct>
 __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
   extern __shared__ uint8_t rt_raw[];
   uint8_t* sm = align1024(rt_raw);
-  uint8_t* Ap = sm;                                    // [8 kb][128 rows][128 B]
-  uint8_t* Bp = sm + kRtAPlane;                        // [2 bufs][8 kb][2 kRtN rows][128 B]
+  uint8_t* Bp = sm;                                    // [2 bufs][8 kb][2 kRtN rows][128 B]
   uint8_t* gst = Bp + 2 * kRtBBuf;                     // [2 parities][2 kRtN rows][128 B]
   float* xsum = reinterpret_cast<float*>(gst + 2 * kRtSlice);  // [2: hi, lo rows][64 neurons][kRtN]
   uint64_t* full = reinterpret_cast<uint64_t*>(xsum + 2 * 64 * kRtN);  // [2] B buffer landed
@@ -2489,27 +2507,35 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
     mbar_init(dfull, 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<32>(tslot);
+  if (warp == 0) tmem_alloc<512>(tslot);
   pdl_wait();
-  // A: row r < 64 = hi of neuron crank*64 + r, row 64 + r = its lo; K = source j
-  for (int idx = tid; idx < 64 * 64; idx += kRtThreads) {  // (neuron row, 8-element chunk of K)
-    const int il = idx / 64, ck = idx % 64, kb = ck / 8, c = ck % 8;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // A into TMEM: lane r of warps 0-3 = row r; r < 64 hi of neuron crank*64 + r, r >= 64
+  // its lo (hi = bf16(x), lo = bf16(x - hi): ~16 significant bits together); K = source
+  // j as bf16 pairs, column kRtACol + j / 2
+  if (warp < 4) {
+    const int r = 32 * warp + lane, il = r & 63;
     const int i = int(crank) * 64 + il;
-    uint32_t h[4], q[4];  // hi = bf16(x), lo = bf16(x - hi): ~16 significant bits together
+    const float* __restrict__ row = a.rec + size_t(i < a.H ? i : 0) * a.H;
+    for (int c = 0; c < 8; ++c) {
+      uint32_t v[32];
 #pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      const int j = ck * 8 + e;
-      const float x0 = (i < a.H && j < a.H) ? a.rec[size_t(i) * a.H + j] : 0.0f;
-      const float x1 = (i < a.H && j + 1 < a.H) ? a.rec[size_t(i) * a.H + j + 1] : 0.0f;
-      const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
-      const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
-      const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
-      h[e / 2] = (uint32_t(__bfloat16_as_ushort(h1)) << 16) | __bfloat16_as_ushort(h0);
-      q[e / 2] = (uint32_t(__bfloat16_as_ushort(l1)) << 16) | __bfloat16_as_ushort(l0);
+      for (int e = 0; e < 32; ++e) {
+        const int j = c * 64 + 2 * e;
+        const float x0 = (i < a.H && j < a.H) ? __ldg(row + j) : 0.0f;
+        const float x1 = (i < a.H && j + 1 < a.H) ? __ldg(row + j + 1) : 0.0f;
+        __nv_bfloat16 y0 = __float2bfloat16_rn(x0), y1 = __float2bfloat16_rn(x1);
+        if (r >= 64) {
+          y0 = __float2bfloat16_rn(x0 - __bfloat162float(y0));
+          y1 = __float2bfloat16_rn(x1 - __bfloat162float(y1));
+        }
+        v[e] = (uint32_t(__bfloat16_as_ushort(y1)) << 16) | __bfloat16_as_ushort(y0);
+      }
+      tmem_st32(*tslot + (uint32_t(32 * warp) << 16) + kRtACol + uint32_t(c) * 32u, v);
     }
-    const uint32_t kbo = uint32_t(kb) * 16384u;
-    st_shared_v4(smem_u32(Ap + kbo + sw128_off(uint32_t(il), uint32_t(c))), make_uint4(h[0], h[1], h[2], h[3]));
-    st_shared_v4(smem_u32(Ap + kbo + sw128_off(uint32_t(64 + il), uint32_t(c))), make_uint4(q[0], q[1], q[2], q[3]));
+    tmem_st_wait();
   }
   for (int idx = tid; idx < int(2 * kRtBBuf / 16); idx += kRtThreads)
     st_shared_v4(smem_u32(Bp) + uint32_t(idx) * 16u, make_uint4(0u, 0u, 0u, 0u));
@@ -2574,15 +2600,14 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
           // B arrived by bulk copies (async proxy) and A was fenced once: no proxy fence here
           tc_fence_after();
           if (t > 0 && SNN_RT_EXP != 2) mbar_arrive_expect_tx(&full[p ^ 1], kBytesPerStep);
-          // descriptors advance by (byte offset >> 4) in their start-address field
-          const uint64_t ad0 = sdesc_sw128(smem_u32(Ap), 16, 1024);
+          // B descriptor advances by (byte offset >> 4); A (TMEM) by 8 columns per K=16
           const uint64_t bd0 = sdesc_sw128(smem_u32(Bp) + uint32_t(p) * kRtBBuf, 16, 1024);
 #pragma unroll
           for (int kb = 0; kb < (SNN_RT_EXP == 1 ? 0 : 8); ++kb) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              umma_bf16(tmem, ad0 + uint64_t((kb * 16384 + ks * 32) >> 4),
-                        bd0 + uint64_t((kb * int(kRtSlice) + ks * 32) >> 4), idesc, (kb | ks) != 0);
+              umma_bf16_ta(tmem, tmem + kRtACol + uint32_t((kb * 4 + ks) * 8),
+                           bd0 + uint64_t((kb * int(kRtSlice) + ks * 32) >> 4), idesc, (kb | ks) != 0);
           }
           umma_commit(dfull);
           RT_CLK(2)
@@ -2596,9 +2621,17 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
       tc_fence_after();
       if (epi) {
         if (warp < 4) {  // row sums D[row][s] + D[row][kRtN + s] of every sample -> smem
-          uint32_t r[32];
-          tmem_ld32(tmem + (uint32_t(warp * 32) << 16), r);
-          tmem_ld_wait();
+          uint32_t r[2 * kRtN];
+          {
+            uint32_t r0[32], r1[16];
+            tmem_ld32(tmem + (uint32_t(warp * 32) << 16), r0);
+            tmem_ld16(tmem + (uint32_t(warp * 32) << 16) + 32u, r1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) r[e] = r0[e];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[32 + e] = r1[e];
+          }
           float* xs = xsum + (warp >> 1) * (64 * kRtN) + il * kRtN;
 #pragma unroll
           for (int s = 0; s < kRtN; s += 4)
@@ -2611,9 +2644,14 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kRtEpiWarps) : "memory");
         if (tid == 0) { RT_CLK(4) }
         if (SNN_RT_EXP != 3) {
-          const float4 hs4 = *reinterpret_cast<const float4*>(xsum + il * kRtN + sb0);
-          const float4 ls4 = *reinterpret_cast<const float4*>(xsum + 64 * kRtN + il * kRtN + sb0);
-          const float hsum[4] = {hs4.x, hs4.y, hs4.z, hs4.w}, lsum[4] = {ls4.x, ls4.y, ls4.z, ls4.w};
+          float hsum[kRtH], lsum[kRtH];
+#pragma unroll
+          for (int s2 = 0; s2 < kRtH; s2 += 2) {
+            const float2 h2 = *reinterpret_cast<const float2*>(xsum + il * kRtN + sb0 + s2);
+            const float2 l2 = *reinterpret_cast<const float2*>(xsum + 64 * kRtN + il * kRtN + sb0 + s2);
+            hsum[s2] = h2.x; hsum[s2 + 1] = h2.y;
+            lsum[s2] = l2.x; lsum[s2 + 1] = l2.y;
+          }
 #pragma unroll
           for (int s = 0; s < kRtH; ++s) {
             const float rc = hsum[s] + lsum[s];
@@ -2690,7 +2728,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
   cluster_sync_all();  // no CTA leaves while a peer may still address its smem
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<32>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
