@@ -195,6 +195,14 @@ snn_status snn_train_step(snn_engine* e, const uint32_t* rows, float* loss, doub
  * with a HOST packed batch [batch_size][ceil(T/8)][input] and int64 targets. */
 snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
                                  const int64_t* targets, float* loss, double* accuracy);
+/* The reference's train() loop over host batches (optimize.hpp:260-299, one train_step
+ * per batch) with the uploads pipelined: n_steps packed batches back to back in host
+ * memory ([n_steps][B][ceil(T/8)][input], pinned for overlap) and their targets
+ * [n_steps][B].  Batch k+1 is DMA'd and re-laid out on a copy stream while step k runs;
+ * every step's StepResult is read back (losses / accuracies [n_steps], may be NULL).
+ * Same results as n_steps calls of snn_train_step_packed. */
+snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const int64_t* targets,
+                                  size_t n_steps, float* losses, double* accuracies);
 
 /* Forward + loss + reverse sweep without the optimizer update (gradients are
  * then readable with snn_get_grads). */

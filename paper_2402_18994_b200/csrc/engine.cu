@@ -364,6 +364,14 @@ struct snn_engine {
     if (h_acc) cudaFreeHost(h_acc);
     if (h_rows) cudaFreeHost(h_rows);
     if (pinned) cudaFreeHost(pinned);
+    if (plab_host) cudaFreeHost(plab_host);
+    if (pres_loss) cudaFreeHost(pres_loss);
+    if (pres_acc) cudaFreeHost(pres_acc);
+    for (int s = 0; s < 2; ++s) {
+      if (ev_ready[s]) cudaEventDestroy(ev_ready[s]);
+      if (ev_used[s]) cudaEventDestroy(ev_used[s]);
+    }
+    if (cstream) cudaStreamDestroy(cstream);
     for (auto& g : prof_graphs) cudaGraphExecDestroy(g.second);
     for (auto& ev : prof_ev) cudaEventDestroy(ev);
     if (stream) cudaStreamDestroy(stream);
@@ -893,6 +901,70 @@ struct snn_engine {
     const size_t out = n * size_t(tp8_pad) * IN_pad;
     k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, stream>>>(raw_in.p, ds.x.p, int64_t(n), tp8,
                                                                    tp8_pad, IN, IN_pad);
+    CK(cudaGetLastError());
+  }
+
+  // Pipelined host batches (snn_train_steps_packed): two device slots; a copy stream
+  // DMAs batch k+1 (pinned caller memory) and re-lays it out while the step graph of
+  // batch k runs; per-step loss / accuracy are read back into pinned memory.
+  cudaStream_t cstream = nullptr;
+  Dataset pslot[2];
+  DevBuf<uint8_t> praw[2];
+  cudaEvent_t ev_ready[2] = {}, ev_used[2] = {};
+  int32_t* plab_host = nullptr;     // pinned [steps][B] labels of the call
+  size_t plab_cap = 0;
+  float* pres_loss = nullptr;       // pinned per-step results
+  double* pres_acc = nullptr;
+  size_t pres_cap = 0;
+  void pipe_init(size_t steps) {
+    const int tp8 = (T + 7) / 8, tp8_pad = T_pad / 8;
+    if (!cstream) {
+      CK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+      for (int s = 0; s < 2; ++s) {
+        CK(cudaEventCreateWithFlags(&ev_ready[s], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_used[s], cudaEventDisableTiming));
+        praw[s].alloc(size_t(B) * tp8 * IN, false);
+        pslot[s].x.alloc(size_t(B) * tp8_pad * IN_pad, false);
+        pslot[s].labels.alloc(size_t(B), false);
+        pslot[s].n = size_t(B);
+        CK(cudaEventRecord(ev_used[s], stream));
+      }
+    }
+    if (steps > plab_cap) {
+      if (plab_host) cudaFreeHost(plab_host);
+      plab_host = nullptr;
+      CK(cudaMallocHost(&plab_host, sizeof(int32_t) * B * steps));
+      plab_cap = steps;
+    }
+    if (steps > pres_cap) {
+      if (pres_loss) cudaFreeHost(pres_loss);
+      if (pres_acc) cudaFreeHost(pres_acc);
+      pres_loss = nullptr;
+      pres_acc = nullptr;
+      CK(cudaMallocHost(&pres_loss, sizeof(float) * steps));
+      CK(cudaMallocHost(&pres_acc, sizeof(double) * steps));
+      pres_cap = steps;
+    }
+  }
+  // batch k into slot k & 1 on the copy stream (after the graph that last read the slot)
+  void pipe_stage(size_t k, const uint8_t* packed, const int64_t* labels) {
+    const int tp8 = (T + 7) / 8, tp8_pad = T_pad / 8;
+    const int sl = int(k & 1);
+    const size_t raw = size_t(B) * tp8 * IN;
+    CK(cudaStreamWaitEvent(cstream, ev_used[sl], 0));
+    static const int pipe_exp = env_int("SNN_PIPE_EXP", 1) - 1;  // timing experiment: 1 = no batch H2D
+    if (pipe_exp != 1) CK(cudaMemcpyAsync(praw[sl].p, packed + k * raw, raw, cudaMemcpyHostToDevice, cstream));
+    // labels from the call's pinned copy (filled and checked up front): no host wait
+    CK(cudaMemcpyAsync(pslot[sl].labels.p, plab_host + k * size_t(B), sizeof(int32_t) * B,
+                       cudaMemcpyHostToDevice, cstream));
+    CK(cudaEventRecord(ev_ready[sl], cstream));
+  }
+  // the step's re-layout of slot sl on the compute stream, right before its graph
+  void pipe_relayout(int sl) {
+    const int tp8 = (T + 7) / 8, tp8_pad = T_pad / 8;
+    const size_t out = size_t(B) * tp8_pad * IN_pad;
+    k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, stream>>>(praw[sl].p, pslot[sl].x.p, int64_t(B), tp8,
+                                                                    tp8_pad, IN, IN_pad);
     CK(cudaGetLastError());
   }
 
@@ -1937,6 +2009,41 @@ snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
       if (++calls % 200 == 0)
         std::fprintf(stderr, "e2e host us/step: stage %.1f  launch %.1f  wait+result %.1f\n", acc[0] / calls,
                      acc[1] / calls, acc[2] / calls);
+    }
+  });
+}
+
+snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const int64_t* targets,
+                                  size_t n_steps, float* losses, double* accuracies) {
+  if (!e || !packed || !targets) return SNN_ERR_ARGUMENT;
+  return guard(e, [&] {
+    if (n_steps == 0) return;
+    e->pipe_init(n_steps);
+    e->ensure_bc_capacity(n_steps);
+    std::vector<uint32_t> rows(size_t(e->B));
+    for (int i = 0; i < e->B; ++i) rows[size_t(i)] = uint32_t(i);
+    e->set_rows_host(rows.data(), e->pslot[0]);
+    CK(cudaStreamSynchronize(e->stream));  // the pinned label / result arrays are free
+    for (size_t i = 0; i < n_steps * size_t(e->B); ++i) {
+      if (targets[i] < 0 || targets[i] >= e->C)
+        fail(SNN_ERR_ARGUMENT, "target %lld outside [0,%d)", (long long)targets[i], e->C);
+      e->plab_host[i] = int32_t(targets[i]);
+    }
+    e->pipe_stage(0, packed, targets);
+    for (size_t k = 0; k < n_steps; ++k) {
+      const int sl = int(k & 1);
+      CK(cudaStreamWaitEvent(e->stream, e->ev_ready[sl], 0));
+      e->pipe_relayout(sl);
+      e->launch(e->pslot[sl], 1);
+      CK(cudaEventRecord(e->ev_used[sl], e->stream));
+      if (k + 1 < n_steps) e->pipe_stage(k + 1, packed, targets);  // runs while step k does
+      CK(cudaMemcpyAsync(e->pres_loss + k, e->result_loss.p, sizeof(float), cudaMemcpyDeviceToHost, e->stream));
+      CK(cudaMemcpyAsync(e->pres_acc + k, e->result_acc.p, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    }
+    CK(cudaStreamSynchronize(e->stream));
+    for (size_t k = 0; k < n_steps; ++k) {
+      if (losses) losses[k] = e->pres_loss[k];
+      if (accuracies) accuracies[k] = e->pres_acc[k];
     }
   });
 }

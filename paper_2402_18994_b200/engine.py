@@ -252,7 +252,7 @@ def lib() -> C.CDLL:
     for name in ("snn_engine_create", "snn_param_count", "snn_entry_count", "snn_entry_info",
                  "snn_set_params", "snn_get_params", "snn_init_params", "snn_get_opt_state",
                  "snn_set_opt_state", "snn_get_grads", "snn_stage_dataset", "snn_train_step",
-                 "snn_train_step_packed", "snn_forward_backward", "snn_train_epochs",
+                 "snn_train_step_packed", "snn_train_steps_packed", "snn_forward_backward", "snn_train_epochs",
                  "snn_upload_schedule", "snn_enqueue_step", "snn_enqueue_steps", "snn_evaluate", "snn_apply", "snn_save_checkpoint", "snn_load_checkpoint", "snn_sync", "snn_read_result",
                  "snn_nccl_unique_id", "snn_comm_init", "snn_debug_enable", "snn_debug_fetch",
                  "snn_synth_dataset", "snn_epoch_permutation", "snn_profile_steps",
@@ -462,6 +462,24 @@ class Engine:
         self._check(self._L.snn_train_step_packed(self._h, _p(packed_x, C.c_uint8),
                                                   _p(t, C.c_int64), C.byref(loss), C.byref(acc)))
         return loss.value, acc.value
+
+    def train_steps_packed(self, packed_x: np.ndarray, targets) -> tuple[np.ndarray, np.ndarray]:
+        """train() over host batches with pipelined uploads: packed_x [n_steps, B, ceil(T/8),
+        input] (pinned memory overlaps the copies), targets [n_steps, B] -> per-step
+        (losses, accuracies); same results as n_steps train_step_packed calls."""
+        packed_x = np.ascontiguousarray(packed_x, np.uint8)
+        t = np.ascontiguousarray(targets, np.int64)
+        n = packed_x.shape[0]
+        if packed_x.ndim != 4 or packed_x.shape[1] != self.batch_size or t.shape != (n, self.batch_size):
+            raise ArgumentError("train_steps_packed: need [n_steps, B, ceil(T/8), input] and [n_steps, B]")
+        if packed_x.shape[2] != (self.time_steps + 7) // 8:
+            raise FormatError("unpack_time: packed extent inconsistent with T")
+        losses = np.zeros(n, np.float32)
+        accs = np.zeros(n, np.float64)
+        self._check(self._L.snn_train_steps_packed(self._h, _p(packed_x, C.c_uint8), _p(t, C.c_int64),
+                                                   C.c_size_t(n), _p(losses, C.c_float),
+                                                   _p(accs, C.c_double)))
+        return losses, accs
 
     def train_epochs(self, epochs: int) -> np.ndarray:
         metrics = np.zeros((epochs, 2), np.float64)

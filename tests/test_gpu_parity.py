@@ -1105,3 +1105,27 @@ def test_declared_cells_checkpoint_apply_monitor(orc, tmp_path):
     c = make_engine(Net(inp=40, hidden=(24, 256), classes=5, monitor=(0,)), B, T)
     with pytest.raises(ShapeError):
         c.load_checkpoint(path)
+
+
+def test_pipelined_host_batches_match_per_step_calls(orc):
+    """snn_train_steps_packed (uploads of batch k+1 overlapped with step k) gives the same
+    bits as one train_step_packed call per batch, losses and parameters."""
+    import torch
+    net = Net(inp=70, hidden=(40, 24), classes=7, act="superspike")
+    B, T, K = 8, 45, 5
+    x, y = orc.synth_raster(7, B * K, T, 70, 9)
+    pk = orc.pack_time(x).reshape(K, B, -1, 70)
+    yk = y.reshape(K, B)
+    pinned = torch.empty(pk.shape, dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[...] = pk
+    a = make_engine(net, B, T, seed=4)
+    b = make_engine(net, B, T, seed=4)
+    la, aa = a.train_steps_packed(pinned.numpy(), yk)
+    ref = [b.train_step_packed(pk[k], yk[k]) for k in range(K)]
+    assert [float(v) for v in la] == [r[0] for r in ref]
+    assert [float(v) for v in aa] == [r[1] for r in ref]
+    assert np.array_equal(a.get_params(), b.get_params())
+    # a second call continues the same optimizer state (pageable memory works too)
+    la2, _ = a.train_steps_packed(pk[:2], yk[:2])
+    assert [float(v) for v in la2] == [b.train_step_packed(pk[k], yk[k])[0] for k in range(2)]
+    assert np.array_equal(a.get_params(), b.get_params())
