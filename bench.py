@@ -29,7 +29,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-E2E_CHUNK = 20  # host batches per snn_train_steps_packed call in the e2e leg
+E2E_CHUNK = int(os.environ.get("SNN_E2E_CHUNK", "20"))  # host batches per snn_train_steps_packed call in the e2e leg
 METRIC = "SNN train samples/sec (fwd+bwd+Adam, SHD shape) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "samples/s"
 

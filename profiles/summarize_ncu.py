@@ -14,7 +14,7 @@ import sys
 NAMES = {"k_lif_fwd": "lif_fwd", "k_readout": "readout", "k_lif_bwd": "lif_bwd",
          "k_wgrad": "wgrad", "k_reduce_adam": "reduce_adam", "k_reduce": "reduce", "k_adam": "adam",
          "k_rlif_fwd": "rlif_fwd", "k_rlif_fwd_cl": "rlif_fwd", "k_rlif_bwd": "rlif_bwd",
-         "k_rlif_bwd_cl": "rlif_bwd", "k_peer_adam": "peer_adam"}
+         "k_rlif_bwd_cl": "rlif_bwd", "k_rlif_bwd_tc": "rlif_bwd", "k_peer_adam": "peer_adam"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6}
 
 
