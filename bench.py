@@ -313,7 +313,16 @@ def main():
     if world > 1:
         # gradient exchange: peer-memory tail (default) or NCCL (SNN_DP_TAIL=nccl)
         from paper_2402_18994_b200.parallel import setup_data_parallel
-        setup_data_parallel(eng, rank, world, dist, os.environ.get("SNN_DP_TAIL", "peer"))
+        tail = os.environ.get("SNN_DP_TAIL", "peer")
+        if tail == "peer":
+            # the peer tail maps every rank's buffer over NVLink; every rank takes the same
+            # decision from the (symmetric) peer-access matrix of the node's GPUs
+            n_local = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+            if not all(torch.cuda.can_device_access_peer(i, j)
+                       for i in range(n_local) for j in range(n_local) if i != j):
+                tail = "nccl"
+        config["dp_tail"] = tail
+        setup_data_parallel(eng, rank, world, dist, tail)
     n_data = w["n_data"]
     eng.synth_dataset(n_data, seed=1)
     # schedule: the reference epoch shuffle, this rank's contiguous slice of each global batch
