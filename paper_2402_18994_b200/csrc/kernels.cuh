@@ -1213,7 +1213,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   // one t-tile: TT more columns cache the membranes V between the two scan passes
-  const bool vcache = a.NT == 1 && !kAlif && !kDsOnly;
+  const bool vcache = a.NT == 1 && !kDsOnly;
   const uint32_t tmem_cols = vcache ? acc_cols(2 * a.TT, 1) : acc_cols(a.TT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
 
@@ -1347,12 +1347,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const float* aseg = arow + size_t(t_lo) * a.H_pad;
       const int top = seg_len - 16;
       float P[4] = {1.0f, 0.0f, 0.0f, 1.0f}, Q[2] = {0.0f, 0.0f};
+      // one t-tile: the membranes are cached in TMEM columns TT.. between the passes
+      const uint32_t vcol = tmem + (uint32_t(q * 32) << 16) + a.TT + sg * seg_len;
       for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
         if (nval <= 0) continue;
         float vr[16], ar[16];
         load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
         load_v16(aseg + size_t(c0) * a.H_pad, a.H_pad, nval, ar);
+        if (vcache) tmem_st16(vcol + c0, vr);
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
         tmem_ld_wait();
@@ -1360,6 +1363,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         if (nval >= 16) bwd_compose_alif<kAct, false>(r, vr, ar, 16, vb, gc, omg, theta, a, P, Q);
         else bwd_compose_alif<kAct, true>(r, vr, ar, nval, vb, gc, omg, theta, a, P, Q);
       }
+      if (vcache) tmem_st_wait();
 #pragma unroll
       for (int i = 0; i < 4; ++i) xP[i * kBwdScanThreads + sidx] = P[i];
       xQ[sidx] = Q[0];
@@ -1381,11 +1385,20 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         const int nval = t_hi - (t_lo + c0);
         if (nval <= 0) continue;
         float vr[16], ar[16];
-        load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
         load_v16(aseg + size_t(c0) * a.H_pad, a.H_pad, nval, ar);
         uint32_t r[16];
-        tmem_ld16(tcol + c0, r);
-        tmem_ld_wait();
+        if (vcache) {
+          uint32_t vv[16];
+          tmem_ld16(vcol + c0, vv);
+          tmem_ld16(tcol + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) vr[e] = __uint_as_float(vv[e]);
+        } else {
+          load_v16(vseg + size_t(c0) * a.H_pad, a.H_pad, nval, vr);
+          tmem_ld16(tcol + c0, r);
+          tmem_ld_wait();
+        }
         if constexpr (kReg) add_dcount(r, rterm);
         if (a.dbg_ds != nullptr) {
 #pragma unroll
