@@ -2594,6 +2594,20 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
 #else
 #define RT_CLK(k)
 #endif
+  // dI of a 4-step chunk as 3 bf16 planes (one 8-byte store per plane); the previous
+  // chunk's samples are flushed one or two per step of the next chunk, so no step
+  // carries every store (each step's exchange waits on the slowest CTA)
+  auto flush = [&](const float (&xs)[4], int s, int cb) {
+    uint32_t h[2], m[2], lo[2];
+    split3_pack(xs[0], xs[1], h[0], m[0], lo[0]);
+    split3_pack(xs[2], xs[3], h[1], m[1], lo[1]);
+    uint2* d = reinterpret_cast<uint2*>(a.di_planes + size_t(i) * cols_total + size_t(b0 + sb0 + s) * a.T_pad + cb);
+    d[0] = make_uint2(h[0], h[1]);
+    d[plane / 4] = make_uint2(m[0], m[1]);
+    d[plane / 2] = make_uint2(lo[0], lo[1]);
+  };
+  float xp[kRtH][4];
+  int cprev = -1;
   for (int c0 = a.T_pad - 4; c0 >= 0; c0 -= 4) {
     float x[kRtH][4];
 #pragma unroll
@@ -2601,6 +2615,11 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
       const int t = c0 + e;
 #pragma unroll
       for (int s = 0; s < kRtH; ++s) x[s][e] = G[s];
+      if (live && cprev >= 0) {
+#pragma unroll
+        for (int s = 0; s < kRtH; ++s)
+          if (s % 4 == 3 - e && s < nmine) flush(xp[s], s, cprev);
+      }
       if (t >= a.T) continue;  // padded steps: uniform over the cluster
       if (warp == kRtMmaWarp) {
         if (elect_one()) {
@@ -2707,19 +2726,16 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_rlif_bwd_tc(RlifBwdArgs a) {
       ++nstep;
 #endif
     }
-    if (live) {
 #pragma unroll
-      for (int s = 0; s < kRtH; ++s)
-        if (s < nmine) {  // 4 steps of dI as 3 bf16 planes: one 8-byte store per plane
-          uint32_t h[2], m[2], lo[2];
-          split3_pack(x[s][0], x[s][1], h[0], m[0], lo[0]);
-          split3_pack(x[s][2], x[s][3], h[1], m[1], lo[1]);
-          uint2* d = reinterpret_cast<uint2*>(a.di_planes + size_t(i) * cols_total + size_t(b0 + sb0 + s) * a.T_pad + c0);
-          d[0] = make_uint2(h[0], h[1]);
-          d[plane / 4] = make_uint2(m[0], m[1]);
-          d[plane / 2] = make_uint2(lo[0], lo[1]);
-        }
-    }
+    for (int s = 0; s < kRtH; ++s)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) xp[s][e] = x[s][e];
+    cprev = c0;
+  }
+  if (live && cprev >= 0) {
+#pragma unroll
+    for (int s = 0; s < kRtH; ++s)
+      if (s < nmine) flush(xp[s], s, cprev);
   }
   if (live) {
 #pragma unroll
