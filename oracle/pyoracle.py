@@ -18,10 +18,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libspiketrain_ref.so")
 
-ACTS = {"custom": 0, "superspike": 1, "triangular": 2, "arctan": 3, "boxcar": 4}
+# "sigmoid" is DECLARED (not in the reference catalogue; spiketrain_oracle.h):
+# custom(heaviside, d/dx sigmoid(kx)), k = 25 by default
+ACTS = {"custom": 0, "superspike": 1, "triangular": 2, "arctan": 3, "boxcar": 4,
+        "sigmoid": 5}
 DEFAULT_SLOPE = {"custom": (0.0, 0.0), "superspike": (25.0, 0.0),
                  "triangular": (0.5, 0.0), "arctan": (2.0, 0.0),
-                 "boxcar": (2.0, 0.5)}
+                 "boxcar": (2.0, 0.5), "sigmoid": (25.0, 0.0)}
 
 
 class _Net(C.Structure):
@@ -157,6 +160,24 @@ class Lib:
         f("train_epochs").restype = C.c_int
         f("train_epochs_ex").restype = C.c_int
         self._f = f
+        if hasattr(L, self.p + "forward_backward_forced"):
+            f("forward_backward_forced").restype = C.c_int
+
+    def set_threads(self, n: int) -> None:
+        """Host threads for big shapes (the C restatement only; bit-identical for any n)."""
+        fn = getattr(self.lib, self.p + "set_threads", None)
+        if fn is not None:
+            fn(C.c_int(int(n)))
+
+    def surrogate(self, act: str, x, slope=None, aux=None):
+        """g(x) elementwise; for the ref library through the reference's own tape."""
+        s, a = DEFAULT_SLOPE[act]
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.zeros_like(x)
+        self._f("surrogate")(C.c_int(ACTS[act]), C.c_float(s if slope is None else slope),
+                             C.c_float(a if aux is None else aux), _ptr(x, C.c_float),
+                             C.c_size_t(x.size), _ptr(out, C.c_float))
+        return out
 
     # ---- rng -----------------------------------------------------------
     def key_from_seed(self, s):
@@ -229,7 +250,9 @@ class Lib:
 
     def forward_backward(self, net: Net, params, packed, t, targets,
                          want_grads=True, want_spikes=False, want_trace=False,
-                         want_v=False, opts: "Opts | None" = None):
+                         want_v=False, opts: "Opts | None" = None, forced=None):
+        """forced: optional list of per-layer u8 rasters [B,T,H] (teacher forcing,
+        orc_forward_backward_forced; the C restatement only)."""
         n = net.c()
         oc = opts.c() if opts is not None else None
         B = packed.shape[0]
@@ -243,12 +266,23 @@ class Lib:
         spikes = np.zeros(nsp, np.uint8) if want_spikes else None
         vtr = np.zeros(nsp, np.float32) if want_v else None
         trace = np.zeros((B, t, net.classes), np.float32) if want_trace else None
-        rc = self._f("forward_backward_ex")(
-            C.byref(n), C.byref(oc) if oc is not None else None, _ptr(params, C.c_float),
-            _ptr(packed, C.c_uint8),
-            C.c_size_t(B), C.c_size_t(t), _ptr(targets, C.c_int64), C.byref(loss),
-            C.byref(acc), _ptr(grads, C.c_float), _ptr(spikes, C.c_uint8),
-            _ptr(vtr, C.c_float), _ptr(trace, C.c_float))
+        if forced is None:
+            rc = self._f("forward_backward_ex")(
+                C.byref(n), C.byref(oc) if oc is not None else None, _ptr(params, C.c_float),
+                _ptr(packed, C.c_uint8),
+                C.c_size_t(B), C.c_size_t(t), _ptr(targets, C.c_int64), C.byref(loss),
+                C.byref(acc), _ptr(grads, C.c_float), _ptr(spikes, C.c_uint8),
+                _ptr(vtr, C.c_float), _ptr(trace, C.c_float))
+        else:
+            fr = np.ascontiguousarray(np.concatenate(
+                [np.asarray(f, np.uint8).reshape(-1) for f in forced]))
+            assert fr.size == nsp, "forced rasters must cover every hidden layer"
+            rc = self._f("forward_backward_forced")(
+                C.byref(n), C.byref(oc) if oc is not None else None, _ptr(params, C.c_float),
+                _ptr(packed, C.c_uint8), C.c_size_t(B), C.c_size_t(t),
+                _ptr(targets, C.c_int64), _ptr(fr, C.c_uint8), C.byref(loss),
+                C.byref(acc), _ptr(grads, C.c_float), _ptr(spikes, C.c_uint8),
+                _ptr(vtr, C.c_float), _ptr(trace, C.c_float))
         if rc != 0:
             raise ValueError(f"forward_backward failed rc={rc}")
         out = {"loss": loss.value, "acc": acc.value}

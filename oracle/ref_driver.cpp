@@ -24,6 +24,9 @@ namespace {
 ActivationDesc act_desc(const orc_net* n) {
   static const char* names[] = {"custom", "superspike", "triangular", "arctan",
                                 "boxcar"};
+  // sigmoid is not in make_activation's catalogue (surrogate.hpp:140-148): the
+  // reference reaches it only through custom() (ref_surrogate_vjp below)
+  if (n->act < 0 || n->act > 4) throw std::invalid_argument("surrogate outside the reference catalogue");
   ActivationDesc d;
   d.name = names[n->act];
   d.slope = double(n->slope);
@@ -462,5 +465,48 @@ int ref_read_container(const char* path, uint8_t* packed, size_t cap, int64_t* l
     return 1;
   }
 }
+
+// The declared sigmoid surrogate (ORC_ACT_SIGMOID, spiketrain_oracle.h) as a
+// caller would add it to the reference: custom(heaviside, bwd) with bwd the
+// derivative of sigmoid(kx) (surrogate.hpp:45-57).
+static SpikingActivation<float> sigmoid_activation(float k) {
+  return custom<float>(nullptr, [k](const Tensor<float>& x) {
+    Tensor<float> out(x.shape());
+    for (std::size_t i = 0; i < x.size(); ++i) {
+      const float s = 1.0f / (1.0f + std::exp(-(k * x[i])));
+      out[i] = (k * s) * (1.0f - s);
+    }
+    return out;
+  });
+}
+
+// g(x) through the reference's own tape: leaf x -> spike(tape, x, act)
+// (surrogate.hpp:124-129, register_custom autodiff.hpp:389-413) -> sum, so the
+// leaf gradient is 1 * g(x) exactly.  act 0..4 via make_activation, 5 =
+// sigmoid through custom().
+void ref_surrogate(int act, float slope, float aux, const float* x, size_t n, float* out) {
+  static const char* names[] = {"custom", "superspike", "triangular", "arctan", "boxcar"};
+  SpikingActivation<float> a;
+  if (act == 5) {
+    a = sigmoid_activation(slope);
+  } else {
+    ActivationDesc d;
+    d.name = names[act];
+    d.slope = double(slope);
+    d.aux = double(aux);
+    a = make_activation<float>(d);
+  }
+  Tape<float> tape;
+  Tensor<float> xt(Shape{n});
+  std::memcpy(xt.data(), x, n * sizeof(float));
+  auto xi = tape.leaf(xt);
+  auto y = spike(tape, xi, a);
+  auto l = tape.sum(y);
+  tape.backward(l);
+  Tensor<float> g = tape.grad(xi);
+  std::memcpy(out, g.data(), n * sizeof(float));
+}
+
+void ref_set_threads(int) {}  // the reference is single-threaded (ops.hpp:12-14)
 
 }  // extern "C"

@@ -14,6 +14,14 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Host threads for the big-shape parity tests (orc_set_threads; default 1).
+ * Every parallel loop below splits OUTPUT elements (rows, samples, neurons or
+ * weight rows) across threads and keeps each element's own accumulation in the
+ * reference order, so results are bit-identical for any thread count
+ * (tests/test_oracle.py::test_threads_are_bit_identical). */
+static int g_threads = 1;
+void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+
 /* ------------------------------------------------------------------------ */
 /* RNG: rng.hpp:20-48 (mix64, from_seed, bits, child), :62-64 (uniform01). */
 
@@ -246,9 +254,8 @@ void orc_init(const orc_net* net, uint64_t key, float* params) {
 /* ------------------------------------------------------------------------ */
 /* Surrogates (surrogate.hpp:59-120), evaluated in float like SpikingActivation<float>. */
 
-static float surrogate(const orc_net* net, float x) {
-  const float k = net->slope;
-  switch (net->act) {
+static float surrogate_k(int act, float k, float aux, float x) {
+  switch (act) {
     case ORC_ACT_SUPERSPIKE: {
       const float d = 1.0f + k * fabsf(x);
       return 1.0f / (d * d);
@@ -262,10 +269,23 @@ static float surrogate(const orc_net* net, float x) {
       return 1.0f / (1.0f + u * u);
     }
     case ORC_ACT_BOXCAR:
-      return fabsf(x) <= k / 2.0f ? net->aux : 0.0f;
+      return fabsf(x) <= k / 2.0f ? aux : 0.0f;
+    case ORC_ACT_SIGMOID: {
+      /* declared (spiketrain_oracle.h): k sig(kx) (1 - sig(kx)) */
+      const float sg = 1.0f / (1.0f + expf(-(k * x)));
+      return (k * sg) * (1.0f - sg);
+    }
     default:
       return 1.0f;
   }
+}
+
+static float surrogate(const orc_net* net, float x) {
+  return surrogate_k(net->act, net->slope, net->aux, x);
+}
+
+void orc_surrogate(int act, float slope, float aux, const float* x, size_t n, float* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = surrogate_k(act, slope, aux, x[i]);
 }
 
 /* clip(beta, 0, 1) = std::min(1, std::max(0, beta)) (ops.hpp clip). */
@@ -281,6 +301,7 @@ static float clip01(float b) {
 /* matmul (ops.hpp:147-174): rows x k times k x n, zero-skip on a. */
 static void matmul_rows(const float* a, size_t rows, size_t k, const float* w,
                         size_t n, const float* bias, float* out) {
+#pragma omp parallel for schedule(static) num_threads(g_threads)
   for (size_t r = 0; r < rows; ++r) {
     float* o = out + r * n;
     for (size_t j = 0; j < n; ++j) o[j] = 0.0f;
@@ -338,11 +359,35 @@ int orc_forward_backward(const orc_net* net, const float* params,
                                  acc_out, grads, spikes_out, vtrace_out, trace_out);
 }
 
+static int fb_impl(const orc_net* net, const orc_train_opts* opts,
+                   const float* params, const uint8_t* packed, size_t B,
+                   size_t T, const int64_t* targets, float* loss_out,
+                   double* acc_out, float* grads, uint8_t* spikes_out,
+                   float* vtrace_out, float* trace_out, const uint8_t* forced);
+
 int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
                             const float* params, const uint8_t* packed, size_t B,
                             size_t T, const int64_t* targets, float* loss_out,
                             double* acc_out, float* grads, uint8_t* spikes_out,
                             float* vtrace_out, float* trace_out) {
+  return fb_impl(net, opts, params, packed, B, T, targets, loss_out, acc_out, grads,
+                 spikes_out, vtrace_out, trace_out, NULL);
+}
+
+int orc_forward_backward_forced(const orc_net* net, const orc_train_opts* opts,
+                                const float* params, const uint8_t* packed, size_t B,
+                                size_t T, const int64_t* targets, const uint8_t* forced,
+                                float* loss_out, double* acc_out, float* grads,
+                                uint8_t* spikes_out, float* vtrace_out, float* trace_out) {
+  return fb_impl(net, opts, params, packed, B, T, targets, loss_out, acc_out, grads,
+                 spikes_out, vtrace_out, trace_out, forced);
+}
+
+static int fb_impl(const orc_net* net, const orc_train_opts* opts,
+                   const float* params, const uint8_t* packed, size_t B,
+                   size_t T, const int64_t* targets, float* loss_out,
+                   double* acc_out, float* grads, uint8_t* spikes_out,
+                   float* vtrace_out, float* trace_out, const uint8_t* forced) {
   if (!opts) opts = &k_default_opts;
   if (opts->loss == 1 && (opts->rate_hi < 0.0f || opts->rate_hi > 1.0f ||
                           opts->rate_lo < 0.0f || opts->rate_lo > 1.0f))
@@ -388,8 +433,11 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
        * then fb_j = sum_i s_i rec[i][j] over spiking i ascending (a zero-skip
        * matmul row, ops.hpp:163-172), v' = (((v bc) + I) + fb) - s theta */
       const float* rec = params + lo[l].gamma;
+#pragma omp parallel num_threads(g_threads)
+      {
       float* vv = (float*)malloc(H * sizeof(float));
       float* fb = (float*)malloc(H * sizeof(float));
+#pragma omp for schedule(static)
       for (size_t b = 0; b < B; ++b) {
         for (size_t n = 0; n < H; ++n) vv[n] = 0.0f;
         for (size_t t = 0; t < T; ++t) {
@@ -397,7 +445,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
           for (size_t n = 0; n < H; ++n) {
             vst[l][row + n] = vv[n];
             const float pre = vv[n] + (-theta);
-            act[l + 1][row + n] = pre >= 0.0f ? 1.0f : 0.0f;
+            act[l + 1][row + n] = (forced ? forced[sp_off + row + n] != 0 : pre >= 0.0f) ? 1.0f : 0.0f;
             fb[n] = 0.0f;
           }
           for (size_t i = 0; i < H; ++i) {
@@ -417,10 +465,12 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
       }
       free(vv);
       free(fb);
+      }
     } else if (is_alif(net, l)) {
       /* declared ALIF (spiketrain_oracle.h): threshold theta + a, reset by it */
       const float* gam = params + lo[l].gamma;
       ast[l] = (float*)malloc(M * H * sizeof(float));
+#pragma omp parallel for schedule(static) num_threads(g_threads)
       for (size_t b = 0; b < B; ++b)
         for (size_t n = 0; n < H; ++n) {
           const float vb = clip01(beta[n * bs]);
@@ -433,7 +483,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
             ast[l][idx] = a;
             const float th = theta + a;
             const float pre = v - th;
-            const float s = pre >= 0.0f ? 1.0f : 0.0f;
+            const float s = (forced ? forced[sp_off + idx] != 0 : pre >= 0.0f) ? 1.0f : 0.0f;
             const float m = v * vb;
             const float ai = m + cur[idx];
             const float r = s * th;
@@ -446,6 +496,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
         }
     } else
     /* lif_step_taped (neuron.hpp:127-136), per timestep */
+#pragma omp parallel for schedule(static) num_threads(g_threads)
     for (size_t b = 0; b < B; ++b)
       for (size_t n = 0; n < H; ++n) {
         const float vb = clip01(beta[n * bs]);
@@ -454,7 +505,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
           const size_t idx = (b * T + t) * H + n;
           vst[l][idx] = v;
           const float pre = v + (-theta);
-          const float s = pre >= 0.0f ? 1.0f : 0.0f;
+          const float s = (forced ? forced[sp_off + idx] != 0 : pre >= 0.0f) ? 1.0f : 0.0f;
           const float m = v * vb;
           const float a = m + cur[idx];
           const float r = s * theta;
@@ -613,19 +664,33 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
         /* matmul_tn over block rows (b, s) ascending (ops.hpp:203-222) */
         memset(D, 0, K * N * sizeof(float));
         memset(db, 0, N * sizeof(float));
-        for (size_t b = 0; b < B; ++b)
-          for (size_t t = t0; t < t1; ++t) {
-            const size_t r = b * T + t;
-            const float* ar = A + r * K;
-            const float* gr = g_out + r * N;
-            for (size_t kk = 0; kk < K; ++kk) {
-              const float av = ar[kk];
-              if (av == 0.0f) continue;
-              float* o = D + kk * N;
-              for (size_t j = 0; j < N; ++j) o[j] += av * gr[j];
-            }
-            for (size_t j = 0; j < N; ++j) db[j] += gr[j];
+        /* threads own disjoint row ranges of D; each element still sums the
+         * block's rows (b, t) in ascending order */
+        {
+          const size_t nth = (size_t)g_threads < K ? (size_t)g_threads : K;
+#pragma omp parallel for schedule(static, 1) num_threads(g_threads)
+          for (size_t th = 0; th < nth; ++th) {
+            const size_t k0 = K * th / nth, k1 = K * (th + 1) / nth;
+            for (size_t b = 0; b < B; ++b)
+              for (size_t t = t0; t < t1; ++t) {
+                const size_t r = b * T + t;
+                const float* ar = A + r * K;
+                const float* gr = g_out + r * N;
+                for (size_t kk = k0; kk < k1; ++kk) {
+                  const float av = ar[kk];
+                  if (av == 0.0f) continue;
+                  float* o = D + kk * N;
+                  for (size_t j = 0; j < N; ++j) o[j] += av * gr[j];
+                }
+              }
           }
+        }
+        if (net->bias)
+          for (size_t b = 0; b < B; ++b)
+            for (size_t t = t0; t < t1; ++t) {
+              const float* gr = g_out + (b * T + t) * N;
+              for (size_t j = 0; j < N; ++j) db[j] += gr[j];
+            }
         for (size_t i = 0; i < K * N; ++i) gW[i] += D[i];
         if (net->bias)
           for (size_t j = 0; j < N; ++j) grads[lo[l].b + j] += db[j];
@@ -636,6 +701,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
       /* dS = matmul_nt(g, W) (ops.hpp:178-199), then the LIF reverse scan. */
       const size_t H = K;
       float* dS = (float*)malloc(M * H * sizeof(float));
+#pragma omp parallel for schedule(static) num_threads(g_threads)
       for (size_t r = 0; r < M; ++r) {
         const float* gr = g_out + r * N;
         for (size_t kk = 0; kk < H; ++kk) {
@@ -665,8 +731,11 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
         const float* rec = params + lo[hl].gamma;
         float* grec = grads + lo[hl].gamma;
         const float* Sx = act[hl + 1];
+#pragma omp parallel num_threads(g_threads)
+        {
         float* G = (float*)malloc(H * sizeof(float));
         float* G2 = (float*)malloc(H * sizeof(float));
+#pragma omp for schedule(static)
         for (size_t b = 0; b < B; ++b) {
           for (size_t n = 0; n < H; ++n) G[n] = 0.0f;
           for (size_t t = T; t-- > 0;) {
@@ -684,17 +753,19 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
             for (size_t i = 0; i < H; ++i) G[i] = G2[i];
           }
         }
-        for (size_t r = 0; r < M; ++r) {
-          const float* sr = Sx + r * H;
-          const float* gr = dIh + r * H;
-          for (size_t i = 0; i < H; ++i) {
-            if (sr[i] == 0.0f) continue;
-            float* o = grec + i * H;
+        free(G);
+        free(G2);
+        }
+        /* rows of drec split across threads, each summing r ascending */
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+        for (size_t i = 0; i < H; ++i) {
+          float* o = grec + i * H;
+          for (size_t r = 0; r < M; ++r) {
+            if (Sx[r * H + i] == 0.0f) continue;
+            const float* gr = dIh + r * H;
             for (size_t j = 0; j < H; ++j) o[j] += gr[j];
           }
         }
-        free(G);
-        free(G2);
       } else if (is_alif(net, hl)) {
         /* declared ALIF reverse: gv = d/dv_{t+1}, ga = d/da_{t+1}, t descending.
          *   dI_t = gv ; gs = (dS + (-gv) th) + ga (1 - gc) ; gp = gs g(pre)
@@ -705,8 +776,10 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
         float* ggam = grads + lo[hl].gamma;
         const float* Av = ast[hl];
         float* sg = (float*)calloc(H, sizeof(float));
-        for (size_t b = 0; b < B; ++b)
-          for (size_t n = 0; n < H; ++n) {
+        const float* Sx = act[hl + 1];
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+        for (size_t n = 0; n < H; ++n)
+          for (size_t b = 0; b < B; ++b) {
             const float vb = clip01(beta[n * bs]);
             const float gc = clip01(gam[n]);
             const float omg = 1.0f - gc;
@@ -716,7 +789,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
               dIh[idx] = gv;
               const float th = theta + Av[idx];
               const float pre = V[idx] - th;
-              const float s = pre >= 0.0f ? 1.0f : 0.0f;
+              const float s = Sx[idx];  /* = [pre >= 0] unless teacher-forced */
               const float gs = (dS[idx] + (-gv) * th) + ga * omg;
               const float gp = gs * surrogate(net, pre);
               sg[n] += ga * (Av[idx] - s);
@@ -729,6 +802,7 @@ int orc_forward_backward_ex(const orc_net* net, const orc_train_opts* opts,
           if (gam[n] > 0.0f && gam[n] < 1.0f) ggam[n] += sg[n];
         free(sg);
       } else {
+#pragma omp parallel for schedule(static) num_threads(g_threads)
       for (size_t b = 0; b < B; ++b)
         for (size_t n = 0; n < H; ++n) {
           const float vb = clip01(beta[n * bs]);

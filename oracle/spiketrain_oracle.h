@@ -34,8 +34,24 @@ enum orc_act {
   ORC_ACT_SUPERSPIKE = 1, /* 1/(1+k|x|)^2                     (surrogate.hpp:59-73) */
   ORC_ACT_TRIANGULAR = 2, /* max(0, 1-|kx|)                   (surrogate.hpp:75-88) */
   ORC_ACT_ARCTAN = 3,     /* 1/(1+(pi k x/2)^2)               (surrogate.hpp:90-104) */
-  ORC_ACT_BOXCAR = 4      /* h on |x|<=w/2                    (surrogate.hpp:106-120) */
+  ORC_ACT_BOXCAR = 4,     /* h on |x|<=w/2                    (surrogate.hpp:106-120) */
+  /* DECLARED, not in the reference catalogue (SPEC.md:283 lists sigmoid as
+   * "addable via custom()"; config.hpp:487-490 rejects the name): the
+   * backward a caller passes to custom(fwd = heaviside, bwd), surrogate.hpp:45-57,
+   *   s = 1 / (1 + exp(-(k x))) ;  g = (k s) (1 - s)      (k = slope, default 25)
+   * i.e. d/dx sigmoid(kx) (the snnTorch / Zenke & Vogels form).  Pinned at the
+   * op level against the reference's own custom() + register_custom tape
+   * closure (ref_surrogate_vjp, tests/test_oracle.py); the network path is the
+   * reference-pinned surrogate plumbing with this g.                          */
+  ORC_ACT_SIGMOID = 5
 };
+
+/* Host threads for the big-shape parity tests (default 1).  Results are
+ * bit-identical for every thread count: threads split output elements only. */
+void orc_set_threads(int n);
+
+/* g(x) of a surrogate, elementwise (act = enum orc_act). */
+void orc_surrogate(int act, float slope, float aux, const float* x, size_t n, float* out);
 
 /*
  * Feed-forward SNN of the shape every BASELINE config uses:
@@ -169,6 +185,19 @@ int orc_train_epochs_ex(const orc_net* net, const orc_train_opts* opts, float* p
                         float* m, float* v, uint64_t* step, const uint8_t* packed,
                         const int64_t* y, size_t n, size_t t_steps, size_t batch,
                         size_t epochs, uint64_t seed, float lr, double* metrics);
+/* Teacher-forced forward_backward (TEST-ONLY diagnostic): identical to
+ * orc_forward_backward_ex except that every hidden cell's spike s_t is taken
+ * from `forced` (layer-major u8 rasters [sum_l B*T*hidden[l]], the layout of
+ * spikes_out) instead of [v - th >= 0]; membranes, resets, surrogates and all
+ * gradients then follow those spikes.  Fed the GPU's own rasters it isolates
+ * the gradient error of the kernels from the legitimate effect of a spike
+ * that flipped on an fp32 near-tie.                                           */
+int orc_forward_backward_forced(const orc_net* net, const orc_train_opts* opts,
+                                const float* params, const uint8_t* packed, size_t batch,
+                                size_t t_steps, const int64_t* targets, const uint8_t* forced,
+                                float* loss, double* acc, float* grads,
+                                uint8_t* spikes, float* vtrace, float* trace);
+
 /* sgd_update over a flat buffer (optimize.hpp:69-84): m doubles as momentum. */
 void orc_sgd(float* p, const float* g, float* m, size_t n, uint64_t* step,
              float lr, float momentum);

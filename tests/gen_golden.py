@@ -227,6 +227,19 @@ def beta_modes_fixture(ref: Lib):
                         v3=st.v)
 
 
+def surrogate_fixture(ref: Lib):
+    """g(x) of every surrogate through the reference's own tape (spike() over
+    register_custom, surrogate.hpp:124-129): the five catalogue entries via
+    make_activation and the declared sigmoid via custom(heaviside, bwd)."""
+    x = np.concatenate([np.linspace(-3, 3, 601, dtype=np.float32),
+                        np.array([0.0, -0.0, 1e-8, -1e-8, 40.0, -40.0, 1e4, -1e4], np.float32)])
+    out = {"x": x}
+    for act in ("custom", "superspike", "triangular", "arctan", "boxcar", "sigmoid"):
+        out[act] = ref.surrogate(act, x)
+        out[act + "_k5"] = ref.surrogate(act, x, slope=5.0, aux=0.25)
+    np.savez_compressed(os.path.join(GOLD, "surrogates.npz"), **out)
+
+
 if __name__ == "__main__":
     if not have_ref():
         Lib.__init__  # noqa: B018
@@ -255,4 +268,6 @@ if __name__ == "__main__":
         shift_fixture(ref)
     if only in (None, "betamodes"):
         beta_modes_fixture(ref)
+    if only in (None, "surrogates"):
+        surrogate_fixture(ref)
     print("golden fixtures written to", GOLD)

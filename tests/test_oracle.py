@@ -424,3 +424,85 @@ def test_container_fixtures_read_back_by_reference():
         pk, y, t = ref.read_container(os.path.join(gold, name), 4096, 64)
         assert t == int(g["t"]) and np.array_equal(y, g["y"])
         assert np.array_equal(pk[:g["packed"].size], g["packed"].ravel())
+
+
+ACT_NAMES = ("custom", "superspike", "triangular", "arctan", "boxcar", "sigmoid")
+
+
+@pytest.mark.parametrize("act", ACT_NAMES)
+def test_surrogate_golden_bit_exact(orc, golden, act):
+    """g(x) of every surrogate == the reference's own tape (spike() over
+    register_custom) bit for bit; sigmoid is the declared custom() backward
+    (spiketrain_oracle.h ORC_ACT_SIGMOID), fixture tests/golden/surrogates.npz."""
+    g = golden("surrogates")
+    assert np.array_equal(orc.surrogate(act, g["x"]), g[act])
+    assert np.array_equal(orc.surrogate(act, g["x"], slope=5.0, aux=0.25), g[act + "_k5"])
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref needs /root/reference")
+def test_surrogate_vs_reference_tape_live(orc):
+    ref = Lib("ref")
+    x = np.random.default_rng(3).normal(0, 2, 5000).astype(np.float32)
+    for act in ACT_NAMES:
+        assert np.array_equal(orc.surrogate(act, x), ref.surrogate(act, x)), act
+
+
+def test_sigmoid_surrogate_is_dsigmoid():
+    """The declared formula is d/dx sigmoid(kx), finite everywhere."""
+    from oracle.pyoracle import Lib as _L
+    o = _L("orc")
+    x = np.linspace(-5, 5, 1001).astype(np.float32)
+    k = 25.0
+    s = 1.0 / (1.0 + np.exp(-k * x.astype(np.float64)))
+    np.testing.assert_allclose(o.surrogate("sigmoid", x), k * s * (1 - s), rtol=1e-5, atol=2e-6)  # f32 tails round s to 1
+    big = np.array([1e4, -1e4, 80.0, -80.0], np.float32)
+    assert np.isfinite(o.surrogate("sigmoid", big)).all()
+
+
+THREAD_NETS = [
+    ("lif", Net(inp=40, hidden=(24, 20), classes=4, bias=True, act="superspike", unroll=5)),
+    ("alif", Net(inp=40, hidden=(24, 20), classes=4, cell=("alif", "lif"), unroll=7)),
+    ("rlif", Net(inp=40, hidden=(24, 20), classes=4, cell=("rlif", "alif"), act="sigmoid")),
+]
+
+
+@pytest.mark.parametrize("case", THREAD_NETS, ids=[c[0] for c in THREAD_NETS])
+def test_threads_are_bit_identical(case):
+    """orc_set_threads(n) splits output elements only: any n gives the same bits."""
+    _, net = case
+    o = Lib("orc")
+    p = o.init(net, o.key_child(o.key_from_seed(4), 0)) * np.float32(3.0)
+    x, y = o.synth_raster(net.classes, 13, 29, net.inp, 2)
+    pk = o.pack_time(x)
+    outs = []
+    for n in (1, 3, 8):
+        o.set_threads(n)
+        outs.append(o.forward_backward(net, p, pk, 29, y, want_spikes=True, want_trace=True))
+    o.set_threads(1)
+    for r in outs[1:]:
+        assert r["loss"] == outs[0]["loss"]
+        assert np.array_equal(r["grads"], outs[0]["grads"])
+        assert np.array_equal(r["trace"], outs[0]["trace"])
+
+
+@pytest.mark.parametrize("case", THREAD_NETS, ids=[c[0] for c in THREAD_NETS])
+def test_forced_with_own_spikes_is_identity(orc, case):
+    """Teacher forcing with the oracle's own rasters reproduces the free run bit
+    for bit; forcing a different raster changes it (the mode is live)."""
+    _, net = case
+    p = orc.init(net, orc.key_child(orc.key_from_seed(4), 0)) * np.float32(3.0)
+    x, y = orc.synth_raster(net.classes, 7, 29, net.inp, 2)
+    pk = orc.pack_time(x)
+    free = orc.forward_backward(net, p, pk, 29, y, want_spikes=True, want_trace=True, want_v=True)
+    assert sum(int(s.sum()) for s in free["spikes"]) > 0
+    forced = orc.forward_backward(net, p, pk, 29, y, want_spikes=True, want_trace=True,
+                                  want_v=True, forced=free["spikes"])
+    assert forced["loss"] == free["loss"]
+    assert np.array_equal(forced["grads"], free["grads"])
+    for a, b in zip(forced["spikes"], free["spikes"]):
+        assert np.array_equal(a, b)
+    flip = [s.copy() for s in free["spikes"]]
+    flip[0][0, 3, :] ^= 1
+    other = orc.forward_backward(net, p, pk, 29, y, want_spikes=True, forced=flip)
+    assert np.array_equal(other["spikes"][0], flip[0])
+    assert not np.array_equal(other["grads"], free["grads"])
