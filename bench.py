@@ -7,7 +7,8 @@ train_step over one batch drawn from an HBM-resident synthetic dataset that
 is larger than L2 (16384 examples, 184 MB staged), fresh rows every step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...   (data-parallel, weak scaling)
+    torchrun --nproc-per-node N bench.py --gpus N ...   (data-parallel; started bare with
+                                                         --gpus N it launches the N ranks itself)
 
 Prints ONE JSON line on rank 0.  The `reference` arm times the reference's own
 CPU train_step (oracle/_ref, built from /root/reference) on the host cores.
@@ -42,8 +43,12 @@ WORKLOADS = {
                cell="alif", n_data=16384,
                desc="SHD-shaped 700-128-128-20 ALIF (declared cell, oracle/spiketrain_oracle.h), "
                     "T=128, batch 1024/GPU, superspike k=25, integral-CE + Adam, nobias"),
-    "c3": dict(inp=700, hidden=(1024, 1024), classes=20, T=256, B=512, act="arctan", n_data=8192,
-               desc="wide 700-1024-1024-20 LIF, T=256, batch 512/GPU"),
+    # BASELINE configs[2]: global batch 4096 sharded over the N GPUs (strong scaling)
+    "c3": dict(inp=700, hidden=(1024, 1024), classes=20, T=256, B=4096, global_batch=True,
+               act="arctan", n_data=16384,
+               desc="wide 700-1024-1024-20 LIF, T=256, global batch 4096 sharded over the GPUs"),
+    "c3w": dict(inp=700, hidden=(1024, 1024), classes=20, T=256, B=512, act="arctan", n_data=8192,
+                desc="wide 700-1024-1024-20 LIF, T=256, batch 512/GPU (weak scaling)"),
     "c4": dict(inp=700, hidden=(512, 512), classes=20, T=128, B=256, act="arctan", cell="rlif",
                n_data=8192,
                desc="recurrent 700-512-512-20 RLIF (declared cell, oracle/spiketrain_oracle.h), "
@@ -54,96 +59,126 @@ WORKLOADS = {
 
 
 def peaks():
+    """(HBM GB/s, dense bf16 TFLOP/s burst, source): the burst figures, since each
+    kernel is timed alone (a few tens of us) inside the profiling graph."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         p = json.load(open(path))
-        return float(p["hbm_gbs"]), float(p["bf16_tflops_sustained"]), "measured"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json hbm_gbs, bf16_tflops burst)"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons during the timed region: NVML polled every 2 ms
+    on a thread, plus explicit samples (`mark()`) taken while the enqueued steps
+    are running, so even a region of a few ms carries samples."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.lines = []
-        self.proc = None
+        self.samples = []
+        self._stop = threading.Event()
+        self._h = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self._h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def mark(self):
+        if self._h is None:
+            return
+        try:
+            nv = self._nv
+            self.samples.append((nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)))
+        except Exception:
+            pass
+
+    def _poll(self):
+        while not self._stop.wait(0.002):
+            self.mark()
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._h is not None:
+            self.thread.join(1.0)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower() in ("active", "1", "yes"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": reasons,
+                "samples": len(sm), "source": "NVML (2 ms poll + samples while the steps run)"}
 
 
 # ------------------------------------------------------------------ roofline
-def algorithmic(name: str, w: dict, n_params: int, fwd_groups=None):
-    """(bound, work per launch) from SURVEY.md §8(d) per-unit figures.  fwd_groups:
-    Engine.forward_launches -- a fused forward launch does every layer it covers."""
-    B, T, C = w["B"], w["T"], w["classes"]
+def algorithmic(name: str, w: dict, n_params: int, fwd_groups=None, B=None):
+    """Algorithmic work per launch from SURVEY.md §8(d)'s per-unit figures:
+    {"tensor": flops, "hbm": bytes} (either may be 0).  A fused GEMM + scan launch
+    carries both; the binding one is the larger fraction of its peak.
+    fwd_groups: Engine.forward_launches -- a fused forward launch does every layer
+    it covers."""
+    B = B or w["B"]
+    T, C = w["T"], w["classes"]
     dims = [w["inp"], *w["hidden"], C]
+    alif = w.get("cell") == "alif"
     base, _, idx = name.partition("[")
     l = int(idx.rstrip("]")) if idx else 0
-    if base == "lif_fwd":            # I = A W over all T: 2 B T K N flops per layer
+    if base == "lif_fwd":
+        # GEMM: I = A W over all T, 2 B T K N flop per layer.  Scan: 8.125 B per
+        # neuron-step (I f32 in, V f32 out, 1 spike bit; ALIF +4 B for a), plus the
+        # first layer's packed input bits (1 bit per (b, t, i))
         n = dict(fwd_groups or []).get(l, 1)
-        return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(l, l + n))
+        fl = sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(l, l + n))
+        by = sum((12.125 if alif else 8.125) * B * T * dims[j + 1] for j in range(l, l + n))
+        by += B * T * dims[l] / 8.0 if l == 0 else 0.0
+        return {"tensor": fl, "hbm": by}
     if base == "wgrad":              # dW = A^T dI, every Linear layer in one launch
-        return "tensor", sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(len(dims) - 1))
-    if base == "lif_bwd":            # LIF reverse scan: 12 B / neuron-step, ALIF +4 (SURVEY §8d)
-        return "hbm", (16.0 if w.get("cell") == "alif" else 12.0) * B * T * dims[l + 1]
+        return {"tensor": sum(2.0 * B * T * dims[j] * dims[j + 1] for j in range(len(dims) - 1)),
+                "hbm": 0.0}
+    if base == "lif_bwd":            # dS GEMM (layers >= 1 get dS from the next layer) + reverse scan
+        return {"tensor": 2.0 * B * T * dims[l + 1] * dims[l + 2],
+                "hbm": (16.0 if alif else 12.0) * B * T * dims[l + 1]}
     if base == "readout":            # LI fwd 4 B + bwd 4 B per readout element
-        return "hbm", 8.0 * B * T * C
+        return {"tensor": 0.0, "hbm": 8.0 * B * T * C}
     if base == "rlif_fwd":           # recurrent scan: read I, write V (+ spike bits) per neuron-step
-        return "hbm", 8.125 * B * T * dims[l + 1]
-    if base == "rlif_bwd":           # recurrent reverse scan: the per-step rec^T GEMV, 2 H^2 flop / sample-step
-        return "hbm", 12.0 * B * T * dims[l + 1]
-    if base == "ds":                 # dS GEMM only (RLIF layers): read dI planes, write dS f32
-        return "hbm", 4.0 * B * T * dims[l + 1]
-    if base in ("adam", "reduce_adam"):  # Adam: 28 B / param (split-K sums are overhead)
-        return "hbm", 28.0 * n_params
-    return "hbm", 0.0
+        return {"tensor": 0.0, "hbm": 8.125 * B * T * dims[l + 1]}
+    if base == "rlif_bwd":           # recurrent reverse scan (+ the per-step rec product, 2 H^2 / sample-step)
+        return {"tensor": 2.0 * B * T * dims[l + 1] ** 2, "hbm": 12.0 * B * T * dims[l + 1]}
+    if base == "ds":                 # dS GEMM only (RLIF layers)
+        return {"tensor": 2.0 * B * T * dims[l + 1] * dims[l + 2], "hbm": 0.0}
+    if base in ("adam", "reduce_adam", "peer_adam"):  # Adam: 28 B / param
+        return {"tensor": 0.0, "hbm": 28.0 * n_params}
+    return {"tensor": 0.0, "hbm": 0.0}
+
+
+def roofline_of(k: dict, hbm_peak: float, tf_peak: float) -> dict:
+    """Both fractions of one launch (burst peaks: a kernel timed alone); the
+    binding one is the larger."""
+    sec = k["ms"] / 1e3
+    out = {}
+    if k["work"]["tensor"] > 0:
+        a = k["work"]["tensor"] / sec / 1e12
+        out["tensor"] = {"achieved": a, "peak": tf_peak, "unit": "TFLOP/s", "frac": a / tf_peak,
+                         "work_per_launch": k["work"]["tensor"]}
+    if k["work"]["hbm"] > 0:
+        a = k["work"]["hbm"] / sec / 1e9
+        out["hbm"] = {"achieved": a, "peak": hbm_peak, "unit": "GB/s", "frac": a / hbm_peak,
+                      "work_per_launch": k["work"]["hbm"]}
+    return out
 
 
 def ncu_traffic(kernel: str):
@@ -231,8 +266,21 @@ def cpu_reference(w: dict, steps: int, warmup: int, workers: int, per_step_budge
                 ms_per_step=1e3 * slowest / max(steps, 1))
 
 
-def cpu_baseline_single(w: dict, seconds: float = 12.0):
-    """Bounded single-core sample for our arm's cpu_baseline key."""
+def host_cpu() -> dict:
+    model = None
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def cpu_baseline_single(w: dict, seconds: float = 12.0, params=None, regime="init"):
+    """Bounded single-core sample for our arm's cpu_baseline key.  params: the
+    regime's parameters (None = the reference init, seed 0).  The reference skips
+    zero inputs (ops.hpp:168, :216), so a spiking (warm) network costs it more."""
     from oracle.pyoracle import Lib, State, have_ref
     which = "ref" if have_ref() else "orc"
     lib = Lib(which)
@@ -240,7 +288,8 @@ def cpu_baseline_single(w: dict, seconds: float = 12.0):
     b = 32
     x, y = lib.synth_raster(w["classes"], b, w["T"], w["inp"], 1)
     pk = lib.pack_time(x)
-    st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)))
+    st = State(lib.init(net, lib.key_child(lib.key_from_seed(0), 0)) if params is None
+               else np.array(params, np.float32))
     lib.train_step(net, st, pk, w["T"], y)
     n, t0 = 0, time.perf_counter()
     while True:
@@ -251,7 +300,8 @@ def cpu_baseline_single(w: dict, seconds: float = 12.0):
             break
     return dict(value=b * n / el, unit=UNIT, cores=1,
                 kind="reference" if which == "ref" else "port",
-                sample=f"{n} train_steps of " + _cpu_label(w, b) + f" on 1 host core, {el:.1f} s")
+                sample=f"{n} train_steps of " + _cpu_label(w, b).replace("init regime", f"{regime} regime")
+                       + f" on 1 host core, {el:.1f} s")
 
 
 # ------------------------------------------------------------------ main
@@ -269,9 +319,25 @@ def main():
     warmup = max(3, args.warmup)
     w = WORKLOADS[args.config]
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # started bare with --gpus N: launch the N ranks ourselves (one process per GPU)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if w.get("global_batch"):
+        if w["B"] % world:
+            raise SystemExit(f"{args.config}: global batch {w['B']} not divisible by {world} ranks")
+        w = dict(w, B=w["B"] // world)
+    scaling = "strong" if w.get("global_batch") else "weak"
     config = {"workload": f"{args.config}: {w['desc']}", "global_batch": w["B"] * world,
               "seq_len": w["T"], "network": f"{w['inp']}-" + "-".join(map(str, w["hidden"])) +
               f"-{w['classes']}", "parallelism": f"dp{world}",
@@ -289,7 +355,7 @@ def main():
         r = cpu_reference(w, args.steps, warmup, workers, budget)
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": warmup,
-                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth_raster seed 1)",
                 "config": config,
                 "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -317,9 +383,10 @@ def main():
         if tail == "peer":
             # the peer tail maps every rank's buffer over NVLink; every rank takes the same
             # decision from the (symmetric) peer-access matrix of the node's GPUs
+            # (multi-node jobs always take NCCL: IPC handles do not cross nodes)
             n_local = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-            if not all(torch.cuda.can_device_access_peer(i, j)
-                       for i in range(n_local) for j in range(n_local) if i != j):
+            if n_local != world or not all(torch.cuda.can_device_access_peer(i, j)
+                                           for i in range(n_local) for j in range(n_local) if i != j):
                 tail = "nccl"
         config["dp_tail"] = tail
         setup_data_parallel(eng, rank, world, dist, tail)
@@ -356,6 +423,7 @@ def main():
     with ClockSampler(local) as clocks:
         t_start.record(stream)
         eng.enqueue_steps(warmup, args.steps)
+        clocks.mark()                      # the enqueued steps are running now
         t_end.record(stream)
         eng.sync()
         torch.cuda.synchronize()
@@ -389,7 +457,7 @@ def main():
     # the train() form over host batches: snn_train_steps_packed uploads batch k+1 while
     # step k runs; every step's batch is DMA'd from pinned memory and every StepResult
     # read back inside the timed region (calls of E2E_CHUNK steps)
-    chunk = min(E2E_CHUNK, args.e2e_steps)
+    chunk = max(2, min(E2E_CHUNK, args.e2e_steps, (20 * 512) // B))  # bounds the pinned batch set
     seq = np.arange(chunk) % nb
     stream_batches = torch.empty((chunk, B) + tuple(packed_host.shape[1:]), dtype=torch.uint8,
                                  pin_memory=True).numpy()
@@ -417,24 +485,23 @@ def main():
     hbm_peak, tf_peak, peak_src = peaks()
     kernels = []
     for name, kms in prof:
-        bound, work = algorithmic(name, w, eng.n_params, eng.forward_launches)
-        kernels.append({"name": name, "ms": kms, "bound": bound, "work": work})
+        k = {"name": name, "ms": kms,
+             "work": algorithmic(name, w, eng.n_params, eng.forward_launches, B)}
+        k["roofline"] = roofline_of(k, hbm_peak, tf_peak)
+        kernels.append(k)
     dom = max(kernels, key=lambda k: k["ms"])
-    if dom["bound"] == "tensor":
-        achieved = dom["work"] / (dom["ms"] / 1e3) / 1e12
-        peak, unit = tf_peak, "TFLOP/s"
-    else:
-        achieved = dom["work"] / (dom["ms"] / 1e3) / 1e9
-        peak, unit = hbm_peak, "GB/s"
-    roofline = {"kernel": dom["name"], "bound": dom["bound"], "achieved": achieved, "peak": peak,
-                "unit": unit, "frac": achieved / peak, "traffic": ncu_traffic(dom["name"]),
-                "peak_source": f"{peak_src} ({'bf16_tflops_sustained' if dom['bound'] == 'tensor' else 'hbm_gbs'})",
-                "work_per_launch": dom["work"],
-                "share_of_step": dom["ms"] / sum(k["ms"] for k in kernels)}
+    both = dom["roofline"]
+    bound = max(both, key=lambda b: both[b]["frac"])
+    roofline = {"kernel": dom["name"], "bound": bound, "achieved": both[bound]["achieved"],
+                "peak": both[bound]["peak"], "unit": both[bound]["unit"],
+                "frac": both[bound]["frac"], "traffic": ncu_traffic(dom["name"]),
+                "peak_source": peak_src, "work_per_launch": both[bound]["work_per_launch"],
+                "share_of_step": dom["ms"] / sum(k["ms"] for k in kernels),
+                "fractions": {b: round(v["frac"], 4) for b, v in both.items()}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (synth_raster seed 1, generated in HBM bit-identical to the "
                     "reference), random-init weights (reference init, seed 0)",
             "config": config, "clocks": clocks.summary(),
@@ -449,10 +516,18 @@ def main():
                                               "D2H loss/acc, host sync every step"}},
             "gpu_launches": eng.launches_per_step * args.steps,
             "roofline": roofline,
-            "kernels": [{"name": k["name"], "ms": round(k["ms"], 5)} for k in kernels],
+            "kernels": [{"name": k["name"], "ms": round(k["ms"], 5),
+                         **{b: round(v["frac"], 4) for b, v in k["roofline"].items()}}
+                        for k in kernels],
             "final_loss": loss, "final_acc": acc}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_single(w)
+        line["cpu_baseline"]["host"] = host_cpu()
+        gold = os.path.join(ROOT, "tests", "golden", "c1.npz")
+        if args.config == "c1" and os.path.exists(gold):
+            # warm regime: the reference's own C1 checkpoint after 3 epochs
+            warm = cpu_baseline_single(w, params=np.load(gold)["warm_params"], regime="warm")
+            line["cpu_baseline"]["warm"] = {k: warm[k] for k in ("value", "unit", "cores", "sample")}
     if rank == 0:
         print(json.dumps(line))
     eng.close()

@@ -46,7 +46,12 @@ typedef enum snn_activation {
   SNN_ACT_SUPERSPIKE = 1,
   SNN_ACT_TRIANGULAR = 2,
   SNN_ACT_ARCTAN = 3,
-  SNN_ACT_BOXCAR = 4
+  SNN_ACT_BOXCAR = 4,
+  /* DECLARED, not in the reference catalogue ("addable via
+   * custom()"; config.hpp:487-490 rejects the name): custom(heaviside, bwd)
+   * with bwd = d/dx sigmoid(kx) = k e / (1 + e)^2, e = exp(-k |x|) (the
+   * cancellation-free form of k s (1 - s)); slope k default 25.              */
+  SNN_ACT_SIGMOID = 5
 } snn_activation;
 
 /*
@@ -292,7 +297,9 @@ snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t par
  *         3: readout trace                          [B][T][C]
  *         4: dS (grad of spikes) of hidden `layer`  [B][T][H]
  *         5: per-kernel phase clocks (tests/clk_probe.py)
- *         6: ALIF adaptation a (entering step t)    [B][T][H]  */
+ *         6: ALIF adaptation a (entering step t)    [B][T][H]
+ *         7: dI of Linear `layer` (0..L, L = readout; hi + (mid + lo) of
+ *            its three bf16 planes)                 [B][T][H or C]  */
 snn_status snn_debug_enable(snn_engine* e, int32_t on);
 snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* host, size_t bytes);
 

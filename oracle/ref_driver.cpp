@@ -473,8 +473,8 @@ static SpikingActivation<float> sigmoid_activation(float k) {
   return custom<float>(nullptr, [k](const Tensor<float>& x) {
     Tensor<float> out(x.shape());
     for (std::size_t i = 0; i < x.size(); ++i) {
-      const float s = 1.0f / (1.0f + std::exp(-(k * x[i])));
-      out[i] = (k * s) * (1.0f - s);
+      const float e = std::exp(-(k * std::fabs(x[i])));
+      out[i] = (k * e) / ((1.0f + e) * (1.0f + e));
     }
     return out;
   });

@@ -271,9 +271,9 @@ static float surrogate_k(int act, float k, float aux, float x) {
     case ORC_ACT_BOXCAR:
       return fabsf(x) <= k / 2.0f ? aux : 0.0f;
     case ORC_ACT_SIGMOID: {
-      /* declared (spiketrain_oracle.h): k sig(kx) (1 - sig(kx)) */
-      const float sg = 1.0f / (1.0f + expf(-(k * x)));
-      return (k * sg) * (1.0f - sg);
+      /* declared (spiketrain_oracle.h): k e / (1 + e)^2, e = exp(-k|x|) */
+      const float e = expf(-(k * fabsf(x)));
+      return (k * e) / ((1.0f + e) * (1.0f + e));
     }
     default:
       return 1.0f;

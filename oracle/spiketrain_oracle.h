@@ -38,8 +38,10 @@ enum orc_act {
   /* DECLARED, not in the reference catalogue (SPEC.md:283 lists sigmoid as
    * "addable via custom()"; config.hpp:487-490 rejects the name): the
    * backward a caller passes to custom(fwd = heaviside, bwd), surrogate.hpp:45-57,
-   *   s = 1 / (1 + exp(-(k x))) ;  g = (k s) (1 - s)      (k = slope, default 25)
-   * i.e. d/dx sigmoid(kx) (the snnTorch / Zenke & Vogels form).  Pinned at the
+   *   e = exp(-(k |x|)) ;  g = (k e) / ((1 + e) (1 + e))   (k = slope, default 25)
+   * i.e. d/dx sigmoid(kx) = k s (1 - s) (the snnTorch / Zenke & Vogels form),
+   * written in the cancellation-free form: k s (1 - s) with s -> 1 loses every
+   * digit of 1 - s, so two fp32 implementations would disagree in the tails.  Pinned at the
    * op level against the reference's own custom() + register_custom tape
    * closure (ref_surrogate_vjp, tests/test_oracle.py); the network path is the
    * reference-pinned surrogate plumbing with this g.                          */

@@ -141,7 +141,12 @@ struct DevBuf {
     n = count;
     if (count == 0) return;
     CK(cudaMalloc(&p, count * sizeof(T)));
-    if (zero) CK(cudaMemset(p, 0, count * sizeof(T)));
+    if (zero) {
+      // the legacy stream is not ordered with the engine's non-blocking stream:
+      // finish the fill before any engine work can touch the buffer
+      CK(cudaMemsetAsync(p, 0, count * sizeof(T), cudaStreamLegacy));
+      CK(cudaStreamSynchronize(cudaStreamLegacy));
+    }
   }
   void free() {
     if (p) cudaFree(p);
@@ -399,7 +404,7 @@ struct snn_engine {
     for (int l = 0; l < n.n_hidden; ++l)
       if (n.hidden[l] < 1) fail(SNN_ERR_SPEC, "layer %d: zero width", 2 * l);
     if (!(n.threshold > 0.0f)) fail(SNN_ERR_UNSUPPORTED, "LIF threshold must be > 0");
-    if (n.activation < 0 || n.activation > 4) fail(SNN_ERR_ARGUMENT, "unknown activation");
+    if (n.activation < 0 || n.activation > 5) fail(SNN_ERR_ARGUMENT, "unknown activation");
     if (n.activation != SNN_ACT_CUSTOM && !(n.slope > 0.0f))
       fail(SNN_ERR_ARGUMENT, "activation slope must be positive");
     for (int l = 0; l <= n.n_hidden; ++l)
@@ -634,17 +639,19 @@ struct snn_engine {
                     k_lif_fwd<false, false, true>, k_lif_fwd<true, false, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
-    for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>,
+    for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>, k_lif_bwd<5>,
                     k_lif_bwd<0, true>, k_lif_bwd<1, true>, k_lif_bwd<2, true>, k_lif_bwd<3, true>,
-                    k_lif_bwd<4, true>})
+                    k_lif_bwd<4, true>, k_lif_bwd<5, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     {
       for (auto fn : {k_rlif_fwd_cl<1>, k_rlif_fwd_cl<2>})
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
-      for (auto fn : {k_rlif_bwd_cl<0>, k_rlif_bwd_cl<1>, k_rlif_bwd_cl<2>, k_rlif_bwd_cl<3>, k_rlif_bwd_cl<4>})
+      for (auto fn : {k_rlif_bwd_cl<0>, k_rlif_bwd_cl<1>, k_rlif_bwd_cl<2>, k_rlif_bwd_cl<3>, k_rlif_bwd_cl<4>,
+                      k_rlif_bwd_cl<5>})
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRlSmemMax));
-      for (auto fn : {k_rlif_bwd_tc<0>, k_rlif_bwd_tc<1>, k_rlif_bwd_tc<2>, k_rlif_bwd_tc<3>, k_rlif_bwd_tc<4>})
+      for (auto fn : {k_rlif_bwd_tc<0>, k_rlif_bwd_tc<1>, k_rlif_bwd_tc<2>, k_rlif_bwd_tc<3>, k_rlif_bwd_tc<4>,
+                      k_rlif_bwd_tc<5>})
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rlif_bwd_tc_smem())));
       for (int l = 0; l < L; ++l)
         if (rlif(l) && rlif_cluster(l)) {
@@ -656,9 +663,9 @@ struct snn_engine {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2))));
     for (auto fn : {k_lif_bwd<0, false, true>, k_lif_bwd<1, false, true>, k_lif_bwd<2, false, true>,
-                    k_lif_bwd<3, false, true>, k_lif_bwd<4, false, true>, k_lif_bwd<0, true, true>,
-                    k_lif_bwd<1, true, true>, k_lif_bwd<2, true, true>, k_lif_bwd<3, true, true>,
-                    k_lif_bwd<4, true, true>})
+                    k_lif_bwd<3, false, true>, k_lif_bwd<4, false, true>, k_lif_bwd<5, false, true>,
+                    k_lif_bwd<0, true, true>, k_lif_bwd<1, true, true>, k_lif_bwd<2, true, true>,
+                    k_lif_bwd<3, true, true>, k_lif_bwd<4, true, true>, k_lif_bwd<5, true, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2, true))));
     CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1109,6 +1116,7 @@ struct snn_engine {
         case 2: launch_cluster(k_rlif_bwd_tc<2>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
         case 3: launch_cluster(k_rlif_bwd_tc<3>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
         case 4: launch_cluster(k_rlif_bwd_tc<4>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
+        case 5: launch_cluster(k_rlif_bwd_tc<5>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
         default: launch_cluster(k_rlif_bwd_tc<0>, grid, dim3(kRtThreads), rlif_bwd_tc_smem(), kRlCl, ra); break;
       }
       return;
@@ -1124,6 +1132,7 @@ struct snn_engine {
         case 2: launch_cluster(k_rlif_bwd_cl<2>, grid, block, smem, kRlCl, ra); break;
         case 3: launch_cluster(k_rlif_bwd_cl<3>, grid, block, smem, kRlCl, ra); break;
         case 4: launch_cluster(k_rlif_bwd_cl<4>, grid, block, smem, kRlCl, ra); break;
+        case 5: launch_cluster(k_rlif_bwd_cl<5>, grid, block, smem, kRlCl, ra); break;
         default: launch_cluster(k_rlif_bwd_cl<0>, grid, block, smem, kRlCl, ra); break;
       }
       return;
@@ -1134,6 +1143,7 @@ struct snn_engine {
       case 2: launch_rlif_bwd_sb<2>(sb, ra, H_pad[l]); break;
       case 3: launch_rlif_bwd_sb<3>(sb, ra, H_pad[l]); break;
       case 4: launch_rlif_bwd_sb<4>(sb, ra, H_pad[l]); break;
+      case 5: launch_rlif_bwd_sb<5>(sb, ra, H_pad[l]); break;
       default: launch_rlif_bwd_sb<0>(sb, ra, H_pad[l]); break;
     }
   }
@@ -1146,6 +1156,7 @@ struct snn_engine {
       case 2: launch(reg ? k_lif_bwd<2, true, kAlif> : k_lif_bwd<2, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       case 3: launch(reg ? k_lif_bwd<3, true, kAlif> : k_lif_bwd<3, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       case 4: launch(reg ? k_lif_bwd<4, true, kAlif> : k_lif_bwd<4, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 5: launch(reg ? k_lif_bwd<5, true, kAlif> : k_lif_bwd<5, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       default: launch(reg ? k_lif_bwd<0, true, kAlif> : k_lif_bwd<0, false, kAlif>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
     }
   }
@@ -1161,6 +1172,7 @@ struct snn_engine {
         case 2: launch(k_lif_bwd<2, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
         case 3: launch(k_lif_bwd<3, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
         case 4: launch(k_lif_bwd<4, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+        case 5: launch(k_lif_bwd<5, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
         default: launch(k_lif_bwd<0, true>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       }
       return;
@@ -1170,6 +1182,7 @@ struct snn_engine {
       case 2: launch(k_lif_bwd<2>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       case 3: launch(k_lif_bwd<3>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       case 4: launch(k_lif_bwd<4>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 5: launch(k_lif_bwd<5>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
       default: launch(k_lif_bwd<0>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
     }
   }
@@ -2508,6 +2521,26 @@ snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* ho
       const size_t need = size_t(B) * T * e->C * sizeof(float);
       if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
       CK(cudaMemcpy(host, e->dbg_trace.p, need, cudaMemcpyDeviceToHost));
+      return;
+    }
+    if (which == 7) {  // dI of Linear `layer` (0..L; L = readout), from its three bf16 planes
+      if (layer < 0 || layer > e->L) fail(SNN_ERR_ARGUMENT, "layer %d", layer);
+      const int W = layer < e->L ? e->H[layer] : e->C, Np = e->N_pad[layer];
+      const size_t need = size_t(B) * T * W * sizeof(float);
+      if (bytes != need) fail(SNN_ERR_SHAPE, "need %zu bytes", need);
+      const size_t rows = size_t(B) * T_pad;
+      std::vector<uint16_t> buf(size_t(3) * Np * rows);
+      CK(cudaMemcpy(buf.data(), e->di[layer].p, buf.size() * 2, cudaMemcpyDeviceToHost));
+      auto f = [](uint16_t h) { uint32_t u = uint32_t(h) << 16; float x; std::memcpy(&x, &u, 4); return x; };
+      float* out = static_cast<float*>(host);
+      for (int b = 0; b < B; ++b)
+        for (int t = 0; t < T; ++t)
+          for (int n = 0; n < W; ++n) {
+            const size_t r = size_t(b) * T_pad + t;
+            const float hi = f(buf[size_t(n) * rows + r]), mi = f(buf[(size_t(Np) + n) * rows + r]),
+                        lo = f(buf[(size_t(2) * Np + n) * rows + r]);
+            out[(size_t(b) * T + t) * W + n] = hi + (mi + lo);
+          }
       return;
     }
     if (layer < 0 || layer >= e->L) fail(SNN_ERR_ARGUMENT, "layer %d", layer);

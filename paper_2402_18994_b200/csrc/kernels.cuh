@@ -49,28 +49,6 @@ __device__ __forceinline__ float clip01(float b) {
   return lo < 1.0f ? lo : 1.0f;
 }
 
-// Surrogate derivative g(x) in float, operation order of surrogate.hpp:59-120.
-__device__ __forceinline__ float surrogate(int act, float k, float aux, float x) {
-  switch (act) {
-    case 1: {  // superspike
-      const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
-      return __fdiv_rn(1.0f, __fmul_rn(d, d));
-    }
-    case 2: {  // triangular
-      const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
-      return 0.0f < r ? r : 0.0f;
-    }
-    case 3: {  // arctan: u = pi*k*x/2
-      const float u = __fdiv_rn(__fmul_rn(__fmul_rn(3.14159265358979f, k), x), 2.0f);
-      return __fdiv_rn(1.0f, __fadd_rn(1.0f, __fmul_rn(u, u)));
-    }
-    case 4:  // boxcar (width = k, height = aux)
-      return fabsf(x) <= __fdiv_rn(k, 2.0f) ? aux : 0.0f;
-    default:  // custom straight-through
-      return 1.0f;
-  }
-}
-
 // 8 bytes each 0/1 (byte e = element e) -> 8 bf16 {0,1} packed into 4 u32.
 __device__ __forceinline__ uint4 expand_bytes01(uint64_t m) {
   // bytes are 0/1: x0xFF -> 0x00/0xFF masks (no carries), PRMT duplicates each
@@ -992,6 +970,14 @@ __device__ __forceinline__ float surrogate_t(float k, float aux, float x) {
     return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
   } else if constexpr (kAct == 4) {  // boxcar
     return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
+  } else if constexpr (kAct == 5) {
+    // sigmoid, DECLARED (not in the reference catalogue): the
+    // backward a caller hands to custom(heaviside, bwd), surrogate.hpp:45-57,
+    // g = k s (1 - s) = (k e) / ((1 + e)(1 + e)), e = exp(-k |x|): the
+    // cancellation-free form of oracle/spiketrain_oracle.h (accurate expf)
+    const float e = expf(-__fmul_rn(k, fabsf(x)));
+    const float d = __fadd_rn(1.0f, e);
+    return __fdiv_rn(__fmul_rn(k, e), __fmul_rn(d, d));
   } else {  // custom straight-through
     return 1.0f;
   }

@@ -39,7 +39,10 @@ _STATUS = {1: ShapeError, 2: ArgumentError, 3: ContractError, 4: StateError, 5: 
            6: IoError, 7: SpecError, 8: ConfigError, 9: UnsupportedError, 10: DeviceError}
 
 # ------------------------------------------------------------- spec types
-ACTIVATIONS = {"custom": 0, "superspike": 1, "triangular": 2, "arctan": 3, "boxcar": 4}
+# "sigmoid" is DECLARED (not in the reference catalogue): the
+# custom(heaviside, k s (1 - s)) backward of oracle/spiketrain_oracle.h
+ACTIVATIONS = {"custom": 0, "superspike": 1, "triangular": 2, "arctan": 3, "boxcar": 4,
+               "sigmoid": 5}
 
 
 @dataclass
@@ -52,7 +55,7 @@ class ActivationDesc:
 
 def default_activation_desc(name: str) -> ActivationDesc:
     table = {"custom": (0.0, 0.0), "superspike": (25.0, 0.0), "triangular": (0.5, 0.0),
-             "arctan": (2.0, 0.0), "boxcar": (2.0, 0.5)}
+             "arctan": (2.0, 0.0), "boxcar": (2.0, 0.5), "sigmoid": (25.0, 0.0)}
     if name not in table:
         raise ArgumentError(f"unknown activation: {name}")
     return ActivationDesc(name, *table[name])
@@ -450,14 +453,26 @@ class Engine:
                                                  C.byref(acc)))
         return loss.value, acc.value
 
+    def _check_packed(self, packed_x: np.ndarray, time_axis: int):
+        """Full shape check before the C ABI reads B * ceil(T/8) * input bytes per step:
+        [..., B, ceil(T/8), input] with exactly time_axis + 2 dims (unpack_time's
+        FormatError for the time extent, data.hpp:131-134; ShapeError otherwise)."""
+        if packed_x.ndim != time_axis + 2:
+            raise ShapeError(f"packed batch: {packed_x.ndim} dims, need {time_axis + 2}")
+        if packed_x.shape[time_axis] != (self.time_steps + 7) // 8:
+            raise FormatError(f"unpack_time: packed extent {packed_x.shape[time_axis]} "
+                              f"inconsistent with T={self.time_steps}")
+        if packed_x.shape[time_axis + 1] != self.desc["input"]:
+            raise ShapeError(f"packed batch: {packed_x.shape[time_axis + 1]} features, "
+                             f"the network takes {self.desc['input']}")
+
     def train_step_packed(self, packed_x: np.ndarray, targets) -> tuple[float, float]:
         """train_step(st, packed_x, T, targets) (optimize.hpp:152-156)."""
         packed_x = np.ascontiguousarray(packed_x, np.uint8)
         t = np.ascontiguousarray(targets, np.int64)
+        self._check_packed(packed_x, 1)
         if packed_x.shape[0] != self.batch_size or t.size != self.batch_size:
             raise ArgumentError(f"targets: {t.size} labels for batch {packed_x.shape[0]}")
-        if packed_x.shape[1] != (self.time_steps + 7) // 8:
-            raise FormatError("unpack_time: packed extent inconsistent with T")
         loss, acc = C.c_float(), C.c_double()
         self._check(self._L.snn_train_step_packed(self._h, _p(packed_x, C.c_uint8),
                                                   _p(t, C.c_int64), C.byref(loss), C.byref(acc)))
@@ -470,10 +485,9 @@ class Engine:
         packed_x = np.ascontiguousarray(packed_x, np.uint8)
         t = np.ascontiguousarray(targets, np.int64)
         n = packed_x.shape[0]
-        if packed_x.ndim != 4 or packed_x.shape[1] != self.batch_size or t.shape != (n, self.batch_size):
+        self._check_packed(packed_x, 2)
+        if packed_x.shape[1] != self.batch_size or t.shape != (n, self.batch_size):
             raise ArgumentError("train_steps_packed: need [n_steps, B, ceil(T/8), input] and [n_steps, B]")
-        if packed_x.shape[2] != (self.time_steps + 7) // 8:
-            raise FormatError("unpack_time: packed extent inconsistent with T")
         losses = np.zeros(n, np.float32)
         accs = np.zeros(n, np.float64)
         self._check(self._L.snn_train_steps_packed(self._h, _p(packed_x, C.c_uint8), _p(t, C.c_int64),
@@ -637,11 +651,11 @@ class Engine:
         self._check(self._L.snn_debug_enable(self._h, int(on)))
 
     def fetch(self, which: str, layer: int = 0) -> np.ndarray:
-        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5, "A": 6}[which]
+        idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5, "A": 6, "dI": 7}[which]
         B, T = self.batch_size, self.time_steps
         if which == "clk":
             out = np.empty((3 + 2 * len(self.desc["hidden"]), max(B * 4, 4096), 48), np.int64)
-        elif which == "trace":
+        elif which == "trace" or (which == "dI" and layer == len(self.desc["hidden"])):
             out = np.empty((B, T, self.desc["classes"]), np.float32)
         else:
             H = self.desc["hidden"][layer]

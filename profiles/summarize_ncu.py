@@ -58,12 +58,18 @@ def main(rep, tag):
                "dram_bytes": dram,
                "achieved_occupancy_pct": val(r, "sm__warps_active.avg.pct_of_peak_sustained_active")[0],
                "top_stalls": {k: round(v / tot, 3) for k, v in top}}
-        for k in ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
-                  "TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
-                  "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
-                  "lts__t_bytes.sum.per_second", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"):
-            if k in hdr:
-                ent[k] = val(r, k)[0]
+        # tensor pipe: sm__pipe_tensor_cycles_active (% of elapsed cycles the tcgen05
+        # pipe is busy, all plane MMAs counted) and the UTCHMMA bf16->fp32 op counters
+        # (the TPC.TriageCompute *_realtime variants are not the tcgen05 pipe)
+        for k in hdr:
+            if (k.startswith("sm__pipe_tensor_cycles_active.") or
+                    k.startswith("sm__ops_path_tensor_op_utchmma") or
+                    k in ("lts__t_bytes.sum.per_second", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+                          "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed")):
+                v = val(r, k)[0]
+                if v is not None:
+                    ent[k] = v
+        ent["tensor_pipe_pct"] = ent.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")
         out["kernels"].append(ent)
         out["dram_bytes_per_launch"][name] = dram
     # backward launches run top-down: the first lif_bwd launch is the last hidden layer
@@ -74,7 +80,7 @@ def main(rep, tag):
     out["dram_bytes_per_launch"] = {k["name"]: k["dram_bytes"] for k in out["kernels"]}
     json.dump(out, open(f"profiles/{tag}_ncu.json", "w"), indent=1)
     for k in out["kernels"]:
-        tp = k.get("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
+        tp = k.get("tensor_pipe_pct")
         print(f"{k['name']:14s} {k['duration_us']:8.1f} us  dram {k['dram_bytes']/1e6:8.2f} MB  "
               f"occ {k['achieved_occupancy_pct']:.1f}%  tensor-pipe {tp}%  {k['top_stalls']}")
 

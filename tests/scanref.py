@@ -26,6 +26,10 @@ def surrogate(act, k, aux, x):
     if act == "arctan":
         u = PI_F * k * x / F(2)
         return (F(1) / (F(1) + u * u)).astype(F)
+    if act == "sigmoid":  # declared (oracle/spiketrain_oracle.h): k e / (1 + e)^2, e = exp(-k|x|)
+        e = np.exp(-(k * np.abs(x))).astype(F)
+        d = (F(1) + e).astype(F)
+        return ((k * e) / (d * d)).astype(F)
     if act == "boxcar":
         return np.where(np.abs(x) <= k / F(2), F(aux), F(0)).astype(F)
     return np.ones_like(x, dtype=F)

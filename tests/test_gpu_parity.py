@@ -15,10 +15,6 @@ pytestmark = pytest.mark.gpu
 
 SPIKE_AGREE = 0.9999
 REL_TOL = 1e-4
-# When the >= 99.99 %-agreeing rasters still differ by a few flipped spikes (fp32
-# accumulation order near threshold, long T), a flip legitimately changes the
-# downstream gradient; the per-tensor bound is then 5e-4 (Parity).
-REL_TOL_FLIPS = 5e-4
 
 
 def relnorm(a, b):
@@ -61,7 +57,7 @@ def check_adam_step(orc, net, p_gpu, p_ref, g_ref, lr=1e-3):
     whose gradient nearly cancels (|g| tiny next to its tensor) can legitimately move
     the other way when the fp32 sums round differently; every other element must
     agree to 1e-6 relative (and the update itself is bit-exact given the gradient,
-    test_c1_golden)."""
+    test_gpu_benched_shapes.py::test_adam_bit_exact_given_gradient)."""
     d = np.abs(p_gpu - p_ref)
     for name, off, size in orc.entries(net):
         sl = slice(off, off + size)
@@ -82,6 +78,8 @@ CASES = [
     ("c1-shape", Net(), 8, 128, 2.0),
     # three hidden layers in one fused forward launch (inp >= 128, H <= 128, T <= 128)
     ("3hidden-fused", Net(inp=150, hidden=(64, 48, 32), classes=6, act="superspike"), 5, 50, 3.0),
+    # declared sigmoid surrogate (custom(heaviside, k s (1 - s)), oracle/spiketrain_oracle.h)
+    ("sigmoid", Net(inp=60, hidden=(96, 40), classes=8, act="sigmoid"), 5, 45, 3.0),
 ]
 
 
@@ -112,11 +110,8 @@ def test_step_parity(orc, case):
         assert (S == ref["spikes"][l]).mean() >= SPIKE_AGREE
     assert relnorm(eng.fetch("trace"), ref["trace"]) <= REL_TOL
     check_grads(orc, net, eng.get_grads(), ref["grads"])
-    # the backward scan given the GPU's own dS is bit-exact too
-    for l, h in enumerate(net.hidden):
-        o, s = ents[f"l{2 * l + 1}.beta"]
-        dS = eng.fetch("dS", l)
-        assert np.isfinite(dS).all()
+    # the backward scan given the GPU's own dS: tests/test_gpu_benched_shapes.py
+    # (test_backward_scan_given_ds) checks dI against scanref.lif_backward
     # one optimizer step
     st = State(params.copy())
     lo, ao = orc.train_step(net, st, pk, T, y)
@@ -215,6 +210,13 @@ def test_errors_map_to_reference_classes(orc):
     eng.stage_dataset(pk, y)
     with pytest.raises(ArgumentError):
         eng.train_step(np.array([0, 5], np.uint32))    # row outside the dataset
+    from paper_2402_18994_b200 import ShapeError
+    with pytest.raises(ShapeError):
+        eng.train_step_packed(pk[:, :, :29], y)        # feature count != network input
+    with pytest.raises(ShapeError):
+        eng.train_step_packed(pk.reshape(2, -1), y)    # not [B, ceil(T/8), input]
+    with pytest.raises(FormatError):
+        eng.train_steps_packed(pk[None, :, :2], y[None])   # packed extent != ceil(T/8)
 
 
 def test_determinism(orc):
@@ -252,11 +254,17 @@ def test_baseline_shapes(orc, case):
     ref = orc.forward_backward(net, params, pk, T, y, want_spikes=True)
     assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
     flips = 0
+    S = [eng.fetch("spikes", l) for l in range(2)]
     for l in range(2):
-        S = eng.fetch("spikes", l)
-        assert (S == ref["spikes"][l]).mean() >= SPIKE_AGREE
-        flips += int((S != ref["spikes"][l]).sum())
-    check_grads(orc, net, eng.get_grads(), ref["grads"], REL_TOL if flips == 0 else REL_TOL_FLIPS)
+        assert (S[l] == ref["spikes"][l]).mean() >= SPIKE_AGREE
+        flips += int((S[l] != ref["spikes"][l]).sum())
+    if flips == 0:
+        check_grads(orc, net, eng.get_grads(), ref["grads"])
+    else:
+        # a flipped fp32 near-tie legitimately moves the gradient: the 1e-4 bar is
+        # applied to the teacher-forced oracle replaying the GPU's own rasters
+        forced = orc.forward_backward(net, params, pk, T, y, forced=S)
+        check_grads(orc, net, eng.get_grads(), forced["grads"])
 
 
 def test_device_synth_is_bit_exact(orc):
@@ -960,7 +968,12 @@ def test_alif_step_parity(orc, case):
         flips += int((S != ref["spikes"][l]).sum())
         assert 0.005 < S.mean() < 0.9, f"layer {l}: rate {S.mean()}"
     assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
-    check_grads(orc, net, eng.get_grads(), ref["grads"], REL_TOL if flips == 0 else REL_TOL_FLIPS)
+    if flips == 0:
+        check_grads(orc, net, eng.get_grads(), ref["grads"])
+    else:  # 1e-4 against the teacher-forced oracle (the GPU's own rasters)
+        Sg = [eng.fetch("spikes", l) for l in range(len(net.hidden))]
+        check_grads(orc, net, eng.get_grads(),
+                    orc.forward_backward(net, params, pk, T, y, forced=Sg)["grads"])
     st = State(params.copy())
     lo, ao = orc.train_step(net, st, pk, T, y)
     eng.debug(False)
@@ -1049,7 +1062,12 @@ def test_rlif_step_parity(orc, case):
         flips += int((S != ref["spikes"][l]).sum())
         assert 0.005 < S.mean() < 0.9, f"layer {l}: rate {S.mean()}"
     assert abs(loss - ref["loss"]) <= REL_TOL * abs(ref["loss"])
-    check_grads(orc, net, eng.get_grads(), ref["grads"], REL_TOL if flips == 0 else REL_TOL_FLIPS)
+    if flips == 0:
+        check_grads(orc, net, eng.get_grads(), ref["grads"])
+    else:  # 1e-4 against the teacher-forced oracle (the GPU's own rasters)
+        Sg = [eng.fetch("spikes", l) for l in range(len(net.hidden))]
+        check_grads(orc, net, eng.get_grads(),
+                    orc.forward_backward(net, params, pk, T, y, forced=Sg)["grads"])
     st = State(params.copy())
     lo, ao = orc.train_step(net, st, pk, T, y)
     eng.debug(False)
