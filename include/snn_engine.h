@@ -271,20 +271,26 @@ snn_status snn_comm_init(snn_engine* e, const uint8_t id[128], int32_t rank, int
  * NCCL allreduce + update): each rank exports its exchange buffer with
  * snn_peer_handle (a 64-byte cudaIpcMemHandle_t), the caller all-gathers the
  * handles (bench.py: torch.distributed.all_gather_object) and every rank calls
- * snn_peer_open with all of them in rank order.  A step then ends with k_reduce
- * (local gradient + loss into the exchange buffer, a release flag to every rank)
- * and k_peer_adam (wait for all flags, sum the ranks' buffers by peer loads in
- * rank order, Adam/SGD, planes, StepResult) -- bit-identical replicas, no NCCL.
- * world <= 8 (one NVSwitch box). */
+ * snn_peer_open with all of them in rank order.  A step then ends, owner-computes,
+ * with k_reduce (local gradient + loss into the exchange buffer, release flag A
+ * to every rank), k_peer_owner (rank r waits for all A flags, sums ITS parameter
+ * slice [r n/W, (r+1) n/W) over the ranks' buffers by peer loads in rank order,
+ * Adam/SGD on that slice -- m, v sharded with the owner -- result into its own
+ * buffer, release flag B to every rank) and k_peer_gather (wait for all B flags,
+ * copy every slice from its owner, planes, StepResult): ~2 n (W-1)/W floats read
+ * per rank per step, bit-identical replicas, no NCCL.  snn_get_opt_state and
+ * checkpoints pull the other owners' m / v slices back first.  A peer that never
+ * publishes (SNN_PEER_TIMEOUT_S, default 20 s) raises SNN_ERR_CUDA on the next
+ * result read instead of hanging.  world <= 8, one node (IPC handles). */
 snn_status snn_peer_handle(snn_engine* e, uint8_t handle[64]);
 snn_status snn_peer_open(snn_engine* e, int32_t rank, int32_t world, const uint8_t* handles);
 /* Test hooks for the peer tail with fewer GPUs than ranks (B200_PROFILING: ranks
  * whose kernels wait on one another must not run as separate launches on one
  * GPU): attach `world` engines of ONE device as ranks 0..world-1 through plain
- * device pointers, and split a step into its part before the cross-rank wait
- * (part 0: forward .. k_reduce, synchronised) and the tail (part 1: k_peer_adam,
- * StepResult).  Running part 0 on every rank before any part 1 means no kernel
- * ever waits on a rank that has not run. */
+ * device pointers, and split a step at its cross-rank waits (part 0: forward ..
+ * k_reduce; part 1: k_peer_owner; part 2: k_peer_gather -> StepResult).  Running
+ * each part on every rank before any rank's next part means no kernel ever waits
+ * on a rank that has not run. */
 snn_status snn_peer_attach_local(snn_engine* const* engines, int32_t world);
 snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t part, float* loss,
                                 double* accuracy);

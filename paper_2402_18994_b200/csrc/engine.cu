@@ -329,19 +329,22 @@ struct snn_engine {
   // g consecutive schedule steps (rows from sched[*sched_slot])
   std::map<std::tuple<const void*, int, int>, cudaGraphExec_t> graphs;
   // multi-GPU: tail 0 = one rank (k_reduce_adam), 1 = NCCL (k_reduce, ncclAllReduce,
-  // k_adam), 2 = peer memory (k_reduce publishing into IPC-mapped exchange buffers,
-  // k_peer_adam summing them and updating)
+  // k_adam), 2 = peer memory, owner-computes (k_reduce publishing into IPC-mapped
+  // exchange buffers, k_peer_owner updating this rank's slice, k_peer_gather)
   void* comm_handle = nullptr;
   int rank = 0, world = 1;
   int tail_mode = 0;
   DevBuf<uint8_t> peer_mem;          // [2][n_comm] f32 exchange buffers, then kMaxRanks u64 flags
   int64_t n_comm = 0;
   float* peer_xchg[kMaxRanks] = {};  // every rank's exchange buffer (mapped; own = local)
-  unsigned long long* peer_flags[kMaxRanks] = {};
+  unsigned long long* peer_flags[kMaxRanks] = {};    // every rank's A flags (k_reduce published)
+  unsigned long long* peer_flags_b[kMaxRanks] = {};  // every rank's B flags (owner phase done)
   void* peer_ipc[kMaxRanks] = {};    // opened IPC mappings (closed on destroy)
   DevBuf<int64_t> peer_seq;
-  DevBuf<unsigned int> peer_done;    // [0] k_reduce publish counter, [1] k_peer_adam completion
-  int split_part = -1;               // test hook: enqueue only the part before (0) / of (1) the peer wait
+  DevBuf<unsigned int> peer_done;    // completion counters: [0] k_reduce, [1] k_peer_owner, [2] k_peer_gather
+  DevBuf<unsigned int> peer_timeout; // set by a peer wait that gave up (checked on every result read)
+  int split_part = -1;               // test hook: enqueue only part 0 (body + k_reduce), 1 (owner
+                                     // phase) or 2 (gather) of a peer-tail step
   bool planes_dirty = true;
   // pipeline depths (smem per CTA decides how many CTAs share an SM)
   int fwd_stages = std::min(kFwdStagesMax, env_int("SNN_FWD_STAGES", 2));
@@ -357,6 +360,10 @@ struct snn_engine {
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
     return (v && *v) ? std::max(1, std::atoi(v)) : d;
+  }
+  static double env_double(const char* k, double d) {
+    const char* v = std::getenv(k);
+    return (v && *v && std::atof(v) > 0.0) ? std::atof(v) : d;
   }
 
   ~snn_engine() {
@@ -1214,24 +1221,28 @@ struct snn_engine {
   }
   // + the RLIF recurrent scans (one forward, one backward per RLIF layer)
   int launches_per_step() const {
-    return int(fwd_groups().size()) + L + (tail_mode == 0 ? 3 : 4) + 2 * n_rlif();
+    return int(fwd_groups().size()) + L + (tail_mode == 0 ? 3 : tail_mode == 1 ? 4 : 5) + 2 * n_rlif();
   }
 
   // exchange buffers + flags of the peer tail (cudaMalloc'd: IPC-exportable)
   void ensure_peer_mem() {
     if (peer_mem.p) return;
     n_comm = (int64_t(n_params) + 2 + L + 63) / 64 * 64;
-    peer_mem.alloc(size_t(2 * n_comm) * 4 + kMaxRanks * 8);
+    // [2] grad regions | [2] result regions | m mirror | v mirror (f32, n_comm each),
+    // then the A and B flag arrays (kMaxRanks u64 each); see k_peer_owner
+    peer_mem.alloc(size_t(6 * n_comm) * 4 + 2 * kMaxRanks * 8);
     peer_seq.alloc(1);
-    peer_done.alloc(2);
+    peer_done.alloc(3);
+    peer_timeout.alloc(1);
   }
   unsigned long long* flags_of(uint8_t* base) const {
-    return reinterpret_cast<unsigned long long*>(base + size_t(2 * n_comm) * 4);
+    return reinterpret_cast<unsigned long long*>(base + size_t(6 * n_comm) * 4);
   }
   void set_peers(int r, int w, uint8_t* const* bases) {
     for (int q = 0; q < w; ++q) {
       peer_xchg[q] = reinterpret_cast<float*>(bases[q]);
       peer_flags[q] = flags_of(bases[q]);
+      peer_flags_b[q] = flags_of(bases[q]) + kMaxRanks;
     }
     rank = r;
     world = w;
@@ -1257,24 +1268,60 @@ struct snn_engine {
   // Peer tail: cross-rank gradient sum over mapped peer memory + the update.
   void enqueue_peer_tail(int update, std::vector<cudaEvent_t>* evs, bool sched_mode) {
     PeerArgs pa{};
-    for (int q = 0; q < world; ++q) pa.xchg[q] = peer_xchg[q];
-    pa.flags = peer_flags[rank];
+    for (int q = 0; q < world; ++q) {
+      pa.xchg[q] = peer_xchg[q];
+      pa.peer_flags_b[q] = peer_flags_b[q];
+    }
+    pa.flags_a = peer_flags[rank];
+    pa.flags_b = peer_flags_b[rank];
     pa.n_comm = n_comm;
     pa.seq = peer_seq.p;
     pa.done = peer_done.p + 1;
+    pa.timeout = peer_timeout.p;
     pa.grads_out = comm.p;
     pa.rows_slot = sched_mode ? sched_slot.p : nullptr;
     pa.step = step.p;
+    pa.rank = rank;
     pa.world = world;
+    pa.spin_ns = (long long)(1e9 * env_double("SNN_PEER_TIMEOUT_S", 20.0));
     AdamArgs a = adam_args(update);
-    launch(k_peer_adam, dim3(unsigned((n_params + 255) / 256)), dim3(256), 0, pa, a);
-    mark(evs, "peer_adam", -1);
+    const int64_t slice = peer_slice_lo(int64_t(n_params), rank + 1, world) -
+                          peer_slice_lo(int64_t(n_params), rank, world);
+    if (split_part != 2) {
+      launch(k_peer_owner, dim3(unsigned(std::max<int64_t>(1, (slice + 255) / 256))), dim3(256), 0, pa, a);
+      mark(evs, "peer_owner", -1);
+    }
+    if (split_part != 1) {
+      launch(k_peer_gather, dim3(unsigned((n_params + 255) / 256)), dim3(256), 0, pa, a);
+      mark(evs, "peer_gather", -1);
+    }
+  }
+  // the owner phase keeps m / v of this rank's slice only (ZeRO-1 style) and mirrors
+  // them into the exchange buffer: pull every other owner's slice back in
+  void sync_opt_from_owners() {
+    if (tail_mode != 2) return;
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) continue;
+      const int64_t lo = peer_slice_lo(int64_t(n_params), q, world);
+      const int64_t hi = peer_slice_lo(int64_t(n_params), q + 1, world);
+      if (hi <= lo) continue;
+      CK(cudaMemcpyAsync(m.p + lo, peer_xchg[q] + peer_m_off(n_comm) + lo, size_t(hi - lo) * 4,
+                         cudaMemcpyDeviceToDevice, stream));
+      CK(cudaMemcpyAsync(v.p + lo, peer_xchg[q] + peer_v_off(n_comm) + lo, size_t(hi - lo) * 4,
+                         cudaMemcpyDeviceToDevice, stream));
+    }
+  }
+  void check_peer_timeout() {
+    if (tail_mode != 2 || !peer_timeout.p) return;
+    unsigned int t = 0;
+    CK(cudaMemcpy(&t, peer_timeout.p, 4, cudaMemcpyDeviceToHost));
+    if (t) fail(SNN_ERR_CUDA, "peer tail: a rank did not publish within SNN_PEER_TIMEOUT_S");
   }
 
   void enqueue_body(const Dataset& ds, int update, std::vector<cudaEvent_t>* evs = nullptr,
                     bool sched_mode = false) {
     launch_names.clear();
-    if (tail_mode == 2 && split_part == 1) {  // test hook: only the tail of a split step
+    if (tail_mode == 2 && split_part >= 1) {  // test hook: only a tail part of a split step
       if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
       enqueue_peer_tail(update, evs, sched_mode);
       return;
@@ -1508,7 +1555,7 @@ struct snn_engine {
         mark(evs, "reduce_adam", -1);
         return;
       }
-      if (split_part != 1) {
+      if (split_part < 1) {
         launch(k_reduce, dim3(blocks), dim3(256), 0, r);
         mark(evs, "reduce", -1);
       }
@@ -1652,6 +1699,7 @@ struct snn_engine {
     CK(cudaMemcpyAsync(h_loss, result_loss.p, sizeof(float), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(h_acc, result_acc.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    check_peer_timeout();
     if (loss) *loss = *h_loss;
     if (acc) *acc = *h_acc;
   }
@@ -1835,6 +1883,7 @@ snn_status snn_save_checkpoint(snn_engine* e, const char* path, const char* conf
     const size_t n = e->n_params;
     std::vector<float> p(n), m(n), v(n);
     int64_t step = 0;
+    e->sync_opt_from_owners();
     CK(cudaMemcpyAsync(p.data(), e->params.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaMemcpyAsync(m.data(), e->m.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaMemcpyAsync(v.data(), e->v.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1953,6 +2002,7 @@ snn_status snn_get_opt_state(snn_engine* e, float* m, float* v, uint64_t* step, 
   if (!e) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
     check_n(e, n);
+    e->sync_opt_from_owners();
     if (m) CK(cudaMemcpyAsync(m, e->m.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
     if (v) CK(cudaMemcpyAsync(v, e->v.p, n * 4, cudaMemcpyDeviceToHost, e->stream));
     int64_t s = 0;
@@ -1972,6 +2022,11 @@ snn_status snn_set_opt_state(snn_engine* e, const float* m, const float* v, uint
     CK(cudaMemcpyAsync(e->m.p, m, n * 4, cudaMemcpyHostToDevice, e->stream));
     CK(cudaMemcpyAsync(e->v.p, v, n * 4, cudaMemcpyHostToDevice, e->stream));
     CK(cudaMemcpyAsync(e->step.p, &s, 8, cudaMemcpyHostToDevice, e->stream));
+    if (e->tail_mode == 2) {  // the mirrors other ranks pull from (sync_opt_from_owners)
+      float* x = e->peer_xchg[e->rank];
+      CK(cudaMemcpyAsync(x + peer_m_off(e->n_comm), m, n * 4, cudaMemcpyHostToDevice, e->stream));
+      CK(cudaMemcpyAsync(x + peer_v_off(e->n_comm), v, n * 4, cudaMemcpyHostToDevice, e->stream));
+    }
     CK(cudaStreamSynchronize(e->stream));
     e->host_step = s;
     e->ensure_bc_capacity();
@@ -2479,7 +2534,7 @@ snn_status snn_peer_attach_local(snn_engine* const* engines, int32_t world) {
 
 snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t part, float* loss,
                                 double* accuracy) {
-  if (!e || (part != 0 && part != 1) || (part == 0 && !rows)) return SNN_ERR_ARGUMENT;
+  if (!e || part < 0 || part > 2 || (part == 0 && !rows)) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
     if (e->tail_mode != 2) fail(SNN_ERR_STATE, "split steps need the peer tail");
     if (e->data.n == 0) fail(SNN_ERR_STATE, "no dataset staged");
@@ -2491,6 +2546,9 @@ snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t par
     if (part == 0) {
       e->set_rows_host(rows, e->data);
       e->ensure_bc_capacity();
+      e->enqueue_body(e->data, 1);
+      CK(cudaStreamSynchronize(e->stream));
+    } else if (part == 1) {
       e->enqueue_body(e->data, 1);
       CK(cudaStreamSynchronize(e->stream));
     } else {

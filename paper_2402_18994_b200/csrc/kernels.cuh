@@ -2979,14 +2979,14 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
   } else {
     // loss / hits / step; activity regularizer values after them (summed over ranks
     // by the allreduce or the peer tail, added to the loss by k_adam / k_result /
-    // k_peer_adam)
+    // k_peer_gather)
     float loss;
     int hits;
     loss_and_hits(a, loss, hits);
     if (tid == 0) {
       gout[a.n_params] = loss;
       gout[a.n_params + 1] = float(hits);
-      if (a.update && a.xchg == nullptr) *a.step += 1;  // peer tail: k_peer_adam advances it
+      if (a.update && a.xchg == nullptr) *a.step += 1;  // peer tail: k_peer_gather advances it
     }
     for (int m = 0; m < a.n_mon; ++m) {
       const float v = activity_value(a, m);
@@ -3101,51 +3101,122 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   refresh_planes(a, en.layer, li / en.cols, li % en.cols, p);
 }
 
-// Multi-rank step tail over peer memory: the cross-rank gradient sum and the
-// optimizer in one kernel (replaces ncclAllReduce + k_adam).  Every rank's k_reduce
-// wrote its local gradient, loss numerator, hits and regularizer values into its
-// exchange buffer of parity seq & 1 and published seq + 1 to every rank's flags.
-// Each block waits for all ranks' flags, then sums the W buffers element-wise in
-// ascending rank order with loads from the mapped peer buffers (deterministic, so
-// every rank computes bit-identical parameters), runs Adam / SGD and refreshes the
-// bf16 planes.  Double buffering is safe: a rank can only reuse a parity after every
-// rank has published the next sequence number, i.e. finished reading this one.
+// Multi-rank step tail over peer memory, OWNER-COMPUTES (replaces ncclAllReduce +
+// k_adam).  Every rank's k_reduce wrote its local gradient, loss numerator, hits
+// and regularizer values into its exchange buffer (grad region, parity seq & 1)
+// and published seq + 1 into flag array A of every rank.  Rank r owns the flat
+// parameter slice [r n / W, (r + 1) n / W):
+//   k_peer_owner  waits for every rank's A flag, sums its slice over the ranks'
+//                 grad regions in ascending rank order (deterministic), runs Adam /
+//                 SGD on it (m, v are owner-sharded, ZeRO-1 style), writes the new
+//                 parameters (and m, v) into its own result region and the summed
+//                 gradient back over its own grad slice, then publishes seq + 1 into
+//                 flag array B of every rank;
+//   k_peer_gather waits for every rank's B flag and copies each parameter from its
+//                 owner's result region (local or mapped peer memory), refreshes the
+//                 bf16 operand planes and the summed gradient.
+// Each rank reads ~2 (W-1)/W n floats over NVLink per step: O(n), not O(W n), and
+// every rank holds the same bits (each element is computed by exactly one owner).
+// Reuse of a parity is race-free: a rank rewrites grad region p two steps later,
+// after its own gather of the next step, i.e. after every owner published that
+// step's B flag (so every owner has finished reading region p); it rewrites
+// result region p after its owner phase two steps later, which waits for every
+// rank's A flag of that step, i.e. for every rank's gather of the step before.
 struct PeerArgs {
-  const float* xchg[kMaxRanks];   // every rank's exchange buffer [2][n_comm] (mapped)
-  unsigned long long* flags;      // this rank's flag array (slot q written by rank q)
+  float* xchg[kMaxRanks];          // every rank's exchange buffer (mapped; own = local)
+  unsigned long long* flags_a;     // this rank's A flags (slot q written by rank q's k_reduce)
+  unsigned long long* flags_b;     // this rank's B flags (slot q written by rank q's owner phase)
+  unsigned long long* peer_flags_b[kMaxRanks];  // every rank's B flag array
   int64_t n_comm;
-  int64_t* seq;                   // exchange sequence number (advanced by the last block)
-  unsigned int* done;
-  float* grads_out;               // summed gradient, loss sum, hits (snn_get_grads)
-  int64_t* rows_slot;             // schedule mode: advanced once per update
-  int64_t* step;                  // the step counter (advanced once per update)
-  int world;
+  int64_t* seq;                    // exchange sequence number (advanced by k_peer_gather)
+  unsigned int* done;              // completion counters: [0] owner phase, [1] gather
+  unsigned int* timeout;           // set to 1 (not a trap) when a peer never published
+  float* grads_out;                // summed gradient, loss sum, hits (snn_get_grads)
+  int64_t* rows_slot;              // schedule mode: advanced once per update
+  int64_t* step;                   // the step counter (advanced once per update)
+  int rank, world;
+  long long spin_ns;               // peer wait limit (SNN_PEER_TIMEOUT_S)
 };
-
-__global__ void __launch_bounds__(256) k_peer_adam(const __grid_constant__ PeerArgs p, AdamArgs a) {
-  pdl_wait();
-  const int tid = threadIdx.x;
-  const int64_t seq = *reinterpret_cast<volatile const int64_t*>(p.seq);
-  const int64_t s = *reinterpret_cast<volatile const int64_t*>(a.step);  // bias corrections of step s+1
-  if (tid == 0) {
-    const unsigned long long target = (unsigned long long)(seq + 1);
+// region offsets (floats) inside one rank's exchange buffer
+__host__ __device__ inline int64_t peer_grad_off(int64_t n_comm, int par) { return par * n_comm; }
+__host__ __device__ inline int64_t peer_res_off(int64_t n_comm, int par) { return (2 + par) * n_comm; }
+__host__ __device__ inline int64_t peer_m_off(int64_t n_comm) { return 4 * n_comm; }
+__host__ __device__ inline int64_t peer_v_off(int64_t n_comm) { return 5 * n_comm; }
+__host__ __device__ inline int64_t peer_slice_lo(int64_t n, int r, int w) { return n * r / w; }
+__device__ __forceinline__ int peer_owner(int64_t i, int64_t n, int w) {
+  int q = int((i * w) / n);  // first guess; fix the floor-division edge
+  while (q + 1 < w && peer_slice_lo(n, q + 1, w) <= i) ++q;
+  while (q > 0 && peer_slice_lo(n, q, w) > i) --q;
+  return q;
+}
+// thread 0 of the block spins until every rank's flag reached `target`; on a
+// timeout it raises the device error flag (the host reports it) instead of
+// trapping, and the block proceeds (the step's results are then invalid)
+__device__ __forceinline__ void peer_wait_all(const PeerArgs& p, const unsigned long long* flags,
+                                              unsigned long long target) {
+  if (threadIdx.x == 0) {
     for (int q = 0; q < p.world; ++q) {
       const long long t0 = globaltimer();
-      while (ld_acquire_sys(p.flags + q) < target) {
-        if (globaltimer() - t0 > 20000000000ll) __trap();  // a rank died: fail instead of hanging
+      while (ld_acquire_sys(flags + q) < target) {
+        if (globaltimer() - t0 > p.spin_ns) {
+          atomicExch(p.timeout, 1u);
+          break;
+        }
         __nanosleep(64);
       }
     }
   }
   __syncthreads();
-  const int64_t par = (seq & 1) * p.n_comm;
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + tid;
-  if (i < a.n_params) {
+}
+
+__global__ void __launch_bounds__(256) k_peer_owner(const __grid_constant__ PeerArgs p, AdamArgs a) {
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const int64_t seq = *reinterpret_cast<volatile const int64_t*>(p.seq);
+  const int64_t s = *reinterpret_cast<volatile const int64_t*>(a.step);  // bias corrections of step s+1
+  const int par = int(seq & 1);
+  peer_wait_all(p, p.flags_a, (unsigned long long)(seq + 1));
+  const int64_t lo = peer_slice_lo(a.n_params, p.rank, p.world);
+  const int64_t hi = peer_slice_lo(a.n_params, p.rank + 1, p.world);
+  const int64_t i = lo + int64_t(blockIdx.x) * blockDim.x + tid;
+  float* own = p.xchg[p.rank];
+  if (i < hi) {
     float g = 0.0f;
-    for (int q = 0; q < p.world; ++q) g = __fadd_rn(g, __ldcv(p.xchg[q] + par + i));
-    p.grads_out[i] = g;
+    for (int q = 0; q < p.world; ++q) g = __fadd_rn(g, __ldcv(p.xchg[q] + peer_grad_off(p.n_comm, par) + i));
     float pv = a.params[i];
     if (a.update) pv = adam_one(a, i, g, a.bc[2 * s], a.bc[2 * s + 1]);
+    own[peer_grad_off(p.n_comm, par) + i] = g;  // only this rank reads its own slice
+    own[peer_res_off(p.n_comm, par) + i] = pv;
+    own[peer_m_off(p.n_comm) + i] = a.m[i];
+    own[peer_v_off(p.n_comm) + i] = a.v[i];
+  }
+  // publish: once every block's stores are visible system-wide, the last block
+  // writes seq + 1 into slot [rank] of every rank's B flags
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
+      *p.done = 0u;
+      __threadfence_system();
+      for (int q = 0; q < p.world; ++q) st_release_sys(p.peer_flags_b[q] + p.rank, (unsigned long long)(seq + 1));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_peer_gather(const __grid_constant__ PeerArgs p, AdamArgs a) {
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const int64_t seq = *reinterpret_cast<volatile const int64_t*>(p.seq);
+  const int64_t s = *reinterpret_cast<volatile const int64_t*>(a.step);
+  const int par = int(seq & 1);
+  peer_wait_all(p, p.flags_b, (unsigned long long)(seq + 1));
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + tid;
+  if (i < a.n_params) {
+    const int q = peer_owner(i, a.n_params, p.world);
+    const float* src = p.xchg[q];
+    const float pv = __ldcv(src + peer_res_off(p.n_comm, par) + i);
+    p.grads_out[i] = __ldcv(src + peer_grad_off(p.n_comm, par) + i);
+    if (q != p.rank) a.params[i] = pv;
     const Entry en = a.entries[find_entry(a.entries, a.n_entries, i)];
     if (en.kind == kEntryW && a.update) {
       const int64_t li = i - en.offset;
@@ -3154,17 +3225,18 @@ __global__ void __launch_bounds__(256) k_peer_adam(const __grid_constant__ PeerA
   }
   if (blockIdx.x == 0 && tid == 0) {
     // StepResult (optimize.hpp:143-147, :193-196) from the rank sums, same order
+    const int64_t g0 = peer_grad_off(p.n_comm, par) + a.n_params;
     float ls = 0.0f, hs = 0.0f;
     for (int q = 0; q < p.world; ++q) {
-      ls = __fadd_rn(ls, __ldcv(p.xchg[q] + par + a.n_params));
-      hs = __fadd_rn(hs, __ldcv(p.xchg[q] + par + a.n_params + 1));
+      ls = __fadd_rn(ls, __ldcv(p.xchg[q] + g0));
+      hs = __fadd_rn(hs, __ldcv(p.xchg[q] + g0 + 1));
     }
     p.grads_out[a.n_params] = ls;
     p.grads_out[a.n_params + 1] = hs;
     float l = __fdiv_rn(ls, a.loss_denom);
     for (int m = 0; m < a.n_mon; ++m) {
       float v = 0.0f;
-      for (int q = 0; q < p.world; ++q) v = __fadd_rn(v, __ldcv(p.xchg[q] + par + a.n_params + 2 + m));
+      for (int q = 0; q < p.world; ++q) v = __fadd_rn(v, __ldcv(p.xchg[q] + g0 + 2 + m));
       l = __fadd_rn(l, v);  // optimize.hpp:185-191
     }
     *a.loss_out = l;
@@ -3174,8 +3246,8 @@ __global__ void __launch_bounds__(256) k_peer_adam(const __grid_constant__ PeerA
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
-      *p.done = 0u;
+    if (atomicAdd(p.done + 1, 1u) == gridDim.x - 1) {
+      p.done[1] = 0u;
       *p.seq = seq + 1;
       if (a.update) {
         *p.step = s + 1;

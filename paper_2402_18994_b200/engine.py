@@ -638,8 +638,8 @@ class Engine:
             engines[0]._check(rc)
 
     def train_step_split(self, rows, part: int):
-        """part 0: forward .. local reduction (synchronised); part 1: cross-rank tail
-        -> (loss, accuracy)."""
+        """part 0: forward .. local reduction (synchronised); part 1: owner phase
+        (this rank's parameter slice, synchronised); part 2: gather -> (loss, accuracy)."""
         loss, acc = C.c_float(), C.c_double()
         r = np.ascontiguousarray(rows, np.uint32) if rows is not None else None
         self._check(self._L.snn_train_step_split(self._h, _p(r, C.c_uint32) if r is not None else None,

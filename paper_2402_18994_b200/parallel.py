@@ -11,16 +11,22 @@ these rules:
   SUM over ranks of the local gradients is the full-batch gradient;
 * the loss numerator (sum of lse - logit_y) and the hit count ride in the same
   allreduce as the gradient; StepResult = (sum / B_global, hits / B_global);
-* every rank applies the identical Adam update to the identical reduced
-  gradient, so parameter replicas stay bit-identical.
+* with the NCCL tail every rank applies the identical Adam update to the
+  identical reduced gradient; with the peer tail each parameter is updated by
+  exactly one owner rank and copied to the others -- either way the parameter
+  replicas stay bit-identical.
 
 Two device tails implement the exchange (engine.cu):
 
-* "peer" (default): every rank's k_reduce writes its local buffer (gradient,
-  loss numerator, hits, regularizer values) into an IPC-exported exchange
-  buffer and raises a flag on every rank; k_peer_adam waits for all flags and
-  sums the ranks' buffers by peer loads over NVLink in ascending rank order
-  (`peer_sum`), then updates -- the reduction and the optimizer in one kernel;
+* "peer" (default, owner-computes): every rank's k_reduce writes its local
+  buffer (gradient, loss numerator, hits, regularizer values) into an
+  IPC-exported exchange buffer and raises flag A on every rank; rank r owns
+  the flat parameter slice [r n / W, (r+1) n / W) (`owner_slice`):
+  k_peer_owner waits for all A flags, sums its slice over the ranks' buffers by
+  peer loads over NVLink in ascending rank order (`peer_sum`), runs Adam on it
+  (m / v sharded with the owner, ZeRO-1 style) and raises flag B; k_peer_gather
+  waits for all B flags and copies every slice from its owner.  Each rank reads
+  about 2 n (W-1)/W floats per step -- O(n), not O(W n);
 * "nccl": k_reduce, ncclAllReduce (sum), k_adam.
 """
 from __future__ import annotations
@@ -37,6 +43,11 @@ def shard_rows(perm: np.ndarray, batch: int, rank: int, world: int, b_local: int
     gb = b_local * world
     start = batch * gb + rank * b_local
     return np.asarray(perm[start:start + b_local])
+
+
+def owner_slice(n: int, rank: int, world: int) -> tuple[int, int]:
+    """[lo, hi) of the flat parameters rank `rank` updates (kernels.cuh peer_slice_lo)."""
+    return n * rank // world, n * (rank + 1) // world
 
 
 def peer_sum(buffers):

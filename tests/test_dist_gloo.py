@@ -95,11 +95,13 @@ def test_shard_rows_partition_the_global_batch():
 
 
 def _peer_worker(rank, port, out):
-    """The peer tail's rules on the CPU: every rank publishes its local buffer, every
-    rank gathers all of them (what k_peer_adam's peer loads see) and sums them in
-    ascending rank order (parallel.peer_sum), then applies Adam locally."""
+    """The owner-computes peer tail's rules on the CPU: every rank publishes its local
+    buffer; rank r sums ITS slice (parallel.owner_slice) over all ranks' buffers in
+    ascending rank order (parallel.peer_sum, what k_peer_owner's peer loads see),
+    runs Adam on that slice only (m / v sharded with the owner), and every rank then
+    gathers the updated slices from their owners (k_peer_gather)."""
     import torch
-    from paper_2402_18994_b200.parallel import exchange_handles, peer_sum
+    from paper_2402_18994_b200.parallel import exchange_handles, owner_slice, peer_sum
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -120,9 +122,19 @@ def _peer_worker(rank, port, out):
                                 [np.float32(o["loss"]) * np.float32(B_LOCAL), o["acc"] * B_LOCAL]])
         bufs = [torch.zeros(local.size) for _ in range(WORLD)]
         dist.all_gather(bufs, torch.from_numpy(local.astype(np.float32)))
-        red = peer_sum([b.numpy() for b in bufs])
-        losses.append(float(red[-2]) / b_global)
-        st.step = orc.adam(st.params, red[:-2].copy(), st.m, st.v, st.step)
+        n = st.params.size
+        lo, hi = owner_slice(n, rank, WORLD)
+        red = peer_sum([b.numpy()[lo:hi] for b in bufs])          # my slice only
+        tail = peer_sum([b.numpy()[n:] for b in bufs])             # loss numerator, hits
+        losses.append(float(tail[0]) / b_global)
+        mine = st.params[lo:hi].copy()
+        m, v = st.m[lo:hi].copy(), st.v[lo:hi].copy()
+        orc.adam(mine, red.copy(), m, v, st.step)
+        st.m[lo:hi], st.v[lo:hi] = m, v                             # only the owner's are valid
+        st.step += 1
+        sl = [None] * WORLD
+        dist.all_gather_object(sl, mine)
+        st.params = np.concatenate(sl).astype(np.float32)
     out[rank] = (st.params.copy(), losses)
     dist.barrier()
     dist.destroy_process_group()

@@ -744,14 +744,14 @@ def test_monitor_spec_errors():
 
 
 def test_single_rank_peer_tail_matches_fused_tail(orc):
-    """The peer-memory tail (k_reduce -> k_peer_adam) on one rank trains bit-identically
-    to the fused single-rank tail."""
+    """The peer-memory tail (k_reduce -> k_peer_owner -> k_peer_gather) on one rank
+    trains bit-identically to the fused single-rank tail."""
     net = Net(inp=30, hidden=(16, 12), classes=5)
     x, y = orc.synth_raster(5, 8, 19, 30, 2)
     pk = orc.pack_time(x)
     e1, e2 = make_engine(net, 4, 19, seed=3), make_engine(net, 4, 19, seed=3)
     e2.peer_open(0, 1, [e2.peer_handle()])
-    assert e2.launches_per_step == e1.launches_per_step + 1
+    assert e2.launches_per_step == e1.launches_per_step + 2
     for eng in (e1, e2):
         eng.stage_dataset(pk, y)
     for i in range(4):
@@ -800,7 +800,9 @@ def test_peer_tail_ranks_emulated_on_one_gpu(orc, world, cell):
         ref = orc.forward_backward(net, st.params, pk[gb], T, y[gb])
         for r, e in enumerate(engs):
             e.train_step_split(gb[r * B:(r + 1) * B], 0)
-        res = [e.train_step_split(None, 1) for e in engs]
+        for e in engs:                      # owner phase: each rank updates its slice
+            e.train_step_split(None, 1)
+        res = [e.train_step_split(None, 2) for e in engs]   # gather the owners' slices
         assert all(r == res[0] for r in res), res
         assert abs(res[0][0] - ref["loss"]) <= REL_TOL * abs(ref["loss"])
         assert res[0][1] == ref["acc"]
@@ -842,7 +844,9 @@ def _ipc_rank(rank, port, out):
         rows = np.arange(step * 8 + rank * 4, step * 8 + rank * 4 + 4, dtype=np.uint32)
         eng.train_step_split(rows, 0)
         dist.barrier()
-        res.append(eng.train_step_split(None, 1))
+        eng.train_step_split(None, 1)
+        dist.barrier()
+        res.append(eng.train_step_split(None, 2))
         dist.barrier()
     out[rank] = (res, eng.get_params(), eng.get_grads())
     dist.destroy_process_group()
