@@ -296,7 +296,9 @@ snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t par
                                 double* accuracy);
 
 /* Diagnostics: raw intermediate tensors of the last forward_backward when
- * enabled (costs extra HBM writes; off by default).
+ * enabled (costs extra HBM writes; off by default).  snn_debug_enable(e, 1):
+ * tensors + per-CTA clock stamps; (e, 2): clock stamps only (the kernels keep
+ * their production code paths); (e, 0): off.
  *   which 0: projection I of hidden layer `layer`   [B][T][H]
  *         1: membrane V (entering step t)           [B][T][H]
  *         2: spikes (0/1 as u8)                     [B][T][H]

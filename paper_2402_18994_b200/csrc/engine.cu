@@ -132,6 +132,21 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
   return m;
 }
 
+// 2-D f32 tensor [rows][cols], box {32 cols, 128 rows}, 128B swizzle (wgrad partials).
+CUtensorMap make_map_f32(const void* base, uint64_t rows, uint64_t cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SNN_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (%d)", int(r));
+  return m;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -279,6 +294,9 @@ struct snn_engine {
   int64_t host_step = 0;               // host mirror of *step (advanced per update launch)
   DevBuf<int64_t> sched_slot;          // schedule mode: slot of the next step (device counter)
   DevBuf<unsigned int> tail_done;      // completion counter of k_reduce_adam
+  DevBuf<unsigned int> wg_tile_cnt;    // fused tail: per output tile arrival counters
+  DevBuf<unsigned int> wg_done;        // fused tail: k_wgrad completion counter
+  int wg_blocks = 0, wg_tiles = 0, sm_count = 148;
   size_t slot_expected = ~size_t(0);   // host mirror of *sched_slot
   // bf16 operand planes of every Linear W [3][K_pad][N_pad] (hi/mid/lo split of the
   // f32 master): MN-major A of the forward GEMM, K-major A of the backward dS GEMM
@@ -318,7 +336,8 @@ struct snn_engine {
   CUtensorMap tm_di_out[kMaxLayers];  // hidden dI planes, 128-row boxes (K3 TMA stores)
   WgradMaps wg_maps;
   // debug
-  bool debug = false;
+  bool debug = false;   // capture intermediate tensors (+ clock stamps)
+  bool clocks = false;  // clock stamps
   DevBuf<float> dbg_i[SNN_MAX_HIDDEN], dbg_ds[SNN_MAX_HIDDEN], dbg_trace;
   // evaluation graphs (update flag): kEval = forward + readout, kEvalTrace = + the
   // readout trace [B][T][C] into eval_trace (apply, network.hpp:435-448)
@@ -503,6 +522,7 @@ struct snn_engine {
       if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess &&
           dev_sms > 0)
         sms = dev_sms;
+      sm_count = sms;
       const double budget = double(kWgBarrierOffset);
       const double xrun = double(wg_xrun_bytes(IN_pad));
       // mg cap: 2 stages of (mg A tiles + 3 B planes + dataset run) must fit
@@ -585,6 +605,17 @@ struct snn_engine {
     step.alloc(1);
     sched_slot.alloc(1);
     tail_done.alloc(1);
+    {
+      wg_blocks = 0;
+      wg_tiles = 0;
+      for (int j = 0; j < NJ; ++j) {
+        const int units = (M_pad_w[j] / 128 + mg_w[j] - 1) / mg_w[j] * (N_pad[j] / n_tile_w[j]);
+        wg_tiles += units;
+        wg_blocks += units * splits_w[j];
+      }
+      wg_tile_cnt.alloc(size_t(wg_tiles));
+      wg_done.alloc(1);
+    }
     grow_bc(1 << 20);
     for (int j = 0; j < L; ++j) {
     }
@@ -642,6 +673,8 @@ struct snn_engine {
       partial[j].alloc(size_t(splits_w[j]) * M_pad_w[j] * N_pad[j], false);
       wg_maps.m[j] = tm_di_w[rec_l[j]];  // d rec: the RLIF layer's own dI planes
     }
+    for (int j = 0; j < NJ; ++j)  // fused tail: TMA tensor stores of the f32 partials
+      wg_maps.pm[j] = make_map_f32(partial[j].p, uint64_t(splits_w[j]) * M_pad_w[j], uint64_t(N_pad[j]));
     for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>, k_lif_fwd<false, true>, k_lif_fwd<true, true>,
                     k_lif_fwd<false, false, true>, k_lif_fwd<true, false, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -675,7 +708,9 @@ struct snn_engine {
                     k_lif_bwd<3, true, true>, k_lif_bwd<4, true, true>, k_lif_bwd<5, true, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               int(bwd_smem_bytes(TT, 2, true))));
-    CK(cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_wgrad<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(kWgSmemLaunch)));
+    CK(cudaFuncSetAttribute(k_wgrad<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(kWgSmemLaunch)));
     CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(200 * 1024)));
@@ -1220,8 +1255,12 @@ struct snn_engine {
     return c;
   }
   // + the RLIF recurrent scans (one forward, one backward per RLIF layer)
+  // one rank: the step tail runs inside k_wgrad when its grid fits one wave (the
+  // tile waits need every CTA co-resident), else k_reduce_adam
+  bool fused_tail() const { return tail_mode == 0 && wg_blocks <= sm_count; }
   int launches_per_step() const {
-    return int(fwd_groups().size()) + L + (tail_mode == 0 ? 3 : tail_mode == 1 ? 4 : 5) + 2 * n_rlif();
+    return int(fwd_groups().size()) + L + (tail_mode == 0 ? (fused_tail() ? 2 : 3) : tail_mode == 1 ? 4 : 5) +
+           2 * n_rlif();
   }
 
   // exchange buffers + flags of the peer tail (cudaMalloc'd: IPC-exportable)
@@ -1354,7 +1393,7 @@ struct snn_engine {
         fm.m[i] = tm_wt[l + i];
       }
       f.n_layers = nl;
-      f.dbg_clk = debug ? dbg_clk.p + size_t(1 + l) * clk_region() : nullptr;
+      f.dbg_clk = clocks ? dbg_clk.p + size_t(1 + l) * clk_region() : nullptr;
       f.B = B; f.T = T; f.T_pad = T_pad; f.TT = TT; f.NT = NT;
       f.in_kind = l == 0 ? 0 : 1;
       f.xshift = l == 0 ? xshift.p : nullptr;
@@ -1411,7 +1450,7 @@ struct snn_engine {
       r.dbeta_part = dbeta[L].p;
       r.dbias_part = net.bias ? dbias[L].p : nullptr;
       r.dbg_trace = update == kEvalTrace ? eval_trace.p : (debug ? dbg_trace.p : nullptr);
-      r.dbg_clk = debug ? dbg_clk.p : nullptr;
+      r.dbg_clk = clocks ? dbg_clk.p : nullptr;
       r.exp_mode = exp_mode;
       r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
       r.inv_b = 1.0f / float(B_global());
@@ -1441,7 +1480,7 @@ struct snn_engine {
         bw.gamma = params.p + entry_of(kEntryGamma, l).offset;
         bw.dgamma_part = dgamma[l].p;
       }
-      bw.dbg_clk = debug ? dbg_clk.p + size_t(1 + L + l) * clk_region() : nullptr;
+      bw.dbg_clk = clocks ? dbg_clk.p + size_t(1 + L + l) * clk_region() : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
       bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
@@ -1467,33 +1506,6 @@ struct snn_engine {
       launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages, alif(l)),
                  tm_wb[l + 1], tm_di_k[l + 1], tm_di_out[l], bw);
       mark(evs, "lif_bwd", l);
-    }
-    // weight gradients: one launch over every Linear layer (split-K partials)
-    {
-      WgradArgs w{};
-      w.x = ds.x.p;
-      w.rows = rows_p;
-      w.rows_slot = slot_p;
-      w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
-      w.xshift = xshift.p;
-      w.in_features = IN;
-      w.dbg_clk = debug ? dbg_clk.p + size_t(1 + 2 * L) * clk_region() : nullptr;
-      int blocks = 0;
-      w.n_layers = NJ;  // + one d rec layer per RLIF cell (A = its own spikes)
-      for (int j = 0; j < NJ; ++j) {
-        WgradLayer& g = w.layer[j];
-        g.s_tp = j > L ? s_tp[rec_l[j]].p : j > 0 ? s_tp[j - 1].p : nullptr;
-        g.partial = partial[j].p;
-        g.kind = j == 0 ? 0 : 1;
-        g.M_pad = M_pad_w[j]; g.N_pad = N_pad[j]; g.n_tile = n_tile_w[j]; g.splits = splits_w[j];
-        g.m_tiles = M_pad_w[j] / 128; g.n_tiles = N_pad[j] / n_tile_w[j];
-        g.mg = mg_w[j]; g.m_groups = (g.m_tiles + g.mg - 1) / g.mg;
-        g.stages = wg_stages_l[j];
-        g.block_start = blocks;
-        blocks += g.m_groups * g.n_tiles * g.splits;
-      }
-      launch(k_wgrad, dim3(blocks), dim3(kWgThreads), kWgSmemLaunch, wg_maps, w);
-      mark(evs, "wgrad", -1);
     }
     // gradient assembly (+ loss sum, hits, step counter)
     {
@@ -1536,6 +1548,7 @@ struct snn_engine {
       r.f_min = cfg.f_min; r.f_max = cfg.f_max;
       r.lambda_low = cfg.lambda_low; r.lambda_high = cfg.lambda_high;
       const int blocks = r.w_blocks + (n_vec + 7) / 8 + 1;
+      const bool fused = update && fused_tail();
       if (tail_mode == 2) {
         r.xchg = reinterpret_cast<float*>(peer_mem.p);
         r.n_comm = n_comm;
@@ -1545,10 +1558,60 @@ struct snn_engine {
         r.world = world;
         r.done = peer_done.p;
       }
+      // weight gradients: one launch over every Linear layer (split-K partials); with
+      // the fused tail it also reduces them, updates and writes the StepResult
+      {
+        WgradArgs w{};
+        w.x = ds.x.p;
+        w.rows = rows_p;
+        w.rows_slot = slot_p;
+        w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
+        w.xshift = xshift.p;
+        w.in_features = IN;
+        w.dbg_clk = clocks ? dbg_clk.p + size_t(1 + 2 * L) * clk_region() : nullptr;
+        int blocks = 0;
+        w.n_layers = NJ;  // + one d rec layer per RLIF cell (A = its own spikes)
+        for (int j = 0; j < NJ; ++j) {
+          WgradLayer& g = w.layer[j];
+          g.s_tp = j > L ? s_tp[rec_l[j]].p : j > 0 ? s_tp[j - 1].p : nullptr;
+          g.partial = partial[j].p;
+          g.kind = j == 0 ? 0 : 1;
+          g.M_pad = M_pad_w[j]; g.N_pad = N_pad[j]; g.n_tile = n_tile_w[j]; g.splits = splits_w[j];
+          g.m_tiles = M_pad_w[j] / 128; g.n_tiles = N_pad[j] / n_tile_w[j];
+          g.mg = mg_w[j]; g.m_groups = (g.m_tiles + g.mg - 1) / g.mg;
+          g.stages = wg_stages_l[j];
+          g.block_start = blocks;
+          blocks += g.m_groups * g.n_tiles * g.splits;
+        }
+        if (fused) {
+          WgradTail tl{};
+          tl.tile_cnt = wg_tile_cnt.p;
+          tl.done = wg_done.p;
+          tl.rows_slot = sched_mode ? sched_slot.p : nullptr;
+          tl.n_tiles_total = wg_tiles;
+          int tb = 0;
+          for (int j = 0; j < NJ; ++j) {
+            const EntryHost* we = nullptr;
+            for (const auto& en : entries)
+              if (en.kind == kEntryW && en.layer == j) we = &en;
+            tl.w_off[j] = int64_t(we->offset);
+            tl.rows[j] = we->rows;
+            tl.cols[j] = we->cols;
+            tl.tile_base[j] = tb;
+            tb += w.layer[j].m_groups * w.layer[j].n_tiles;
+          }
+          launch(k_wgrad<true>, dim3(blocks), dim3(kWgThreads), kWgSmemLaunch, wg_maps, w, r, adam_args(1), tl);
+          mark(evs, "wgrad", -1);
+          return;
+        }
+        launch(k_wgrad<false>, dim3(blocks), dim3(kWgThreads), kWgSmemLaunch, wg_maps, w, r, AdamArgs{},
+               WgradTail{});
+        mark(evs, "wgrad", -1);
+      }
       if (update && tail_mode == 0) {
         // no communicator: no allreduce between reduction and update -> one kernel
         AdamArgs a = adam_args(1);
-        long long* tclk = debug && size_t(blocks) * kClkStride <= clk_region()
+        long long* tclk = clocks && size_t(blocks) * kClkStride <= clk_region()
                               ? dbg_clk.p + size_t(2 + 2 * L) * clk_region() : nullptr;
         launch(k_reduce_adam, dim3(blocks), dim3(256), 0, r, a, tail_done.p,
                sched_mode ? sched_slot.p : (int64_t*)nullptr, tclk);
@@ -1710,8 +1773,12 @@ struct snn_engine {
     read_result(loss, acc);
   }
 
-  void set_debug(bool on) {
+  // level 0 off, 1 tensors + clock stamps, 2 clock stamps only (kernels run their
+  // production code paths: no capture stores)
+  void set_debug(int level) {
+    const bool on = level == 1;
     debug = on;
+    clocks = level != 0;
     const size_t rows = size_t(B) * T_pad;
     for (int l = 0; l < L; ++l) {
       if (on) {
@@ -1724,7 +1791,7 @@ struct snn_engine {
     }
     if (on) dbg_trace.alloc(size_t(B) * T * C); else dbg_trace.free();
     // clock stamps: slot 0 readout [B][8], slots 1..L fwd, L+1..2L bwd ([B*8 ctas][8] each)
-    if (on) dbg_clk.alloc(size_t(3 + 2 * L) * clk_region()); else dbg_clk.free();
+    if (clocks) dbg_clk.alloc(size_t(3 + 2 * L) * clk_region()); else dbg_clk.free();
     clear_graphs();
   }
 };
@@ -2561,13 +2628,13 @@ snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t par
 
 snn_status snn_debug_enable(snn_engine* e, int32_t on) {
   if (!e) return SNN_ERR_ARGUMENT;
-  return guard(e, [&] { e->set_debug(on != 0); });
+  return guard(e, [&] { e->set_debug(on == 2 ? 2 : on != 0 ? 1 : 0); });
 }
 
 snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* host, size_t bytes) {
   if (!e || !host) return SNN_ERR_ARGUMENT;
   return guard(e, [&] {
-    if (!e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
+    if (which == 5 ? !e->clocks : !e->debug) fail(SNN_ERR_STATE, "debug capture not enabled");
     const int B = e->B, T = e->T, T_pad = e->T_pad;
     if (which == 5) {
       const size_t need = size_t(3 + 2 * e->L) * e->clk_region() * sizeof(long long);

@@ -540,8 +540,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int g = li * a.NT + tt;  // accumulator use (fused: one per layer)
         const int buf = g % nbuf;
         mbar_wait(&acc_full[buf], (g / nbuf) & 1);
+        __syncwarp();  // reconverge after the per-thread spin: the scan's ballots then
+                       // compile to plain VOTEs (no WARPSYNC.COLLECTIVE emulation)
         tc_fence_after();
         if (clk != nullptr && threadIdx.x == 0 && tt == 0 && li == 0) clk[1] = clock64();
+        if (clk != nullptr && threadIdx.x == 0 && tt == 0 && li < 4) clk[8 + 2 * li] = clock64();
         for (int c = 0; c < a.TT / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(tmem + (uint32_t(q * 32) << 16) + buf * NTOT + sm * a.TT + c * 32, r);
@@ -584,6 +587,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);
       }
+      if (clk != nullptr && threadIdx.x == 0 && li < 4) clk[9 + 2 * li] = clock64();
       if (feed) {
         fence_async_smem();  // B tiles -> visible to the tensor core
         tc_fence_before();   // TMEM reads of this layer done before the next MMA
@@ -1623,280 +1627,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 }
 
 // ============================================================================
-// K5  k_wgrad: partial[s][k][n] = sum_{rows in split s} A[k][row] * dI[row][n]
-// A binary (dataset time bits or time-packed spikes), exact in bf16 (K-major,
-// decoded by warps 0-3); dI as 3 bf16 planes via TMA (MN-major).  Epilogue
-// writes f32 partials; k_reduce sums them in fixed order (deterministic).
-// grid (M_pad/128, N_pad/N_TILE, splits); block 192.
-// ============================================================================
-struct WgradLayer {
-  const uint32_t* s_tp;    // kind 1: time-packed spikes [K_pad][B*T_pad/32]
-  float* partial;          // [splits][M_pad][N_pad]
-  int kind, M_pad, N_pad, n_tile, splits, m_tiles, n_tiles, block_start;
-  int mg, m_groups;        // m-tiles per CTA (share every dI stage), groups
-  int stages;              // pipeline depth for this layer's stage size
-};
-// B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
-struct WgradArgs {
-  WgradLayer layer[kMaxLayers];
-  int n_layers;
-  const uint8_t* x;        // kind 0: staged dataset
-  const uint32_t* rows;    // kind 0: [B]
-  const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
-  long long* dbg_clk;      // optional [blocks][kClkStride] phase timestamps
-  const int32_t* xshift;   // kind 0: batch roll along the features (shift_augment)
-  int B, T_pad, x_row_stride, in_features;
-};
-struct WgradMaps {
-  CUtensorMap m[kMaxLayers];
-};
-
-constexpr int kWgStagesMax = 6;
-constexpr int kWgMgMax = 4;
-#ifndef SNN_WG_EXP
-#define SNN_WG_EXP 0  // timing experiments (tests/clk_probe.py only): 1 no decode, 2 one dI plane, 3 no MMA
-#endif
-// A-operand producers: kWgProdWarps warps; thread p decodes row p % 128 of every
-// M-tile, time half p / 128 (64 steps per stage = 2 halves of 32)
-constexpr int kWgProdWarps = 8;
-constexpr int kWgProd = 32 * kWgProdWarps;
-constexpr int kWgThreads = kWgProd + 64;  // + TMA warp + MMA warp
-__host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile, int mg) {
-  return uint32_t(mg) * kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // mg A tiles + 3 B planes
-}
-__host__ __device__ constexpr uint32_t wg_xrun_bytes(int x_row_stride) {
-  return (8u * uint32_t(x_row_stride) + 1023) & ~1023u;
-}
-__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages, int x_row_stride) {
-  return uint32_t(stages) * (wg_stage_bytes(n_tile, mg) + wg_xrun_bytes(x_row_stride)) + 1024 + 256;
-}
-// epilogue staging row stride (f32 row of n_tile + 16 bytes of bank padding)
-__host__ __device__ constexpr uint32_t wg_epi_row_stride(int n_tile) { return uint32_t(n_tile) * 4u + 16u; }
-// the launch always requests the full carve-out: barriers at kWgBarrierOffset
-constexpr uint32_t kWgSmemLaunch = 227 * 1024;
-
-// barriers at a fixed offset past the largest per-layer stage footprint
-constexpr uint32_t kWgBarrierOffset = 227 * 1024 - 2048;
-
-// One launch for every Linear layer: block -> (layer, m-group, n-tile, split).
-// A CTA accumulates mg M-tiles (mg x n_tile TMEM columns) so each dI stage
-// loaded by TMA feeds mg MMAs.
-__global__ void __launch_bounds__(kWgThreads, 1)
-    k_wgrad(const __grid_constant__ WgradMaps maps, WgradArgs args) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  long long* clk = args.dbg_clk != nullptr ? args.dbg_clk + size_t(blockIdx.x) * kClkStride : nullptr;
-  if (clk != nullptr && threadIdx.x == 0) {
-    clk[0] = clock64();
-    clk[6] = globaltimer();
-  }
-  int li = 0;
-  while (li + 1 < args.n_layers && int(blockIdx.x) >= args.layer[li + 1].block_start) ++li;
-  const WgradLayer a = args.layer[li];
-  const CUtensorMap* tm_di = &maps.m[li];
-  const int local = int(blockIdx.x) - a.block_start;
-  const int mgi = local % a.m_groups, ntile = (local / a.m_groups) % a.n_tiles;
-  const int split = local / (a.m_groups * a.n_tiles);
-  const int mt0 = mgi * a.mg;
-  const int nm = min(a.mg, a.m_tiles - mt0);  // M-tiles of this CTA
-  const int S = a.stages;
-  const uint32_t stage_bytes = wg_stage_bytes(a.n_tile, a.mg);
-  const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: n_tile rows x 64 cols
-  // kind 0: the dataset bytes of one (sample, 64-step block) are one contiguous
-  // run of 8 * x_row_stride bytes -> one bulk copy per stage into xbuf
-  const uint32_t xbytes = a.kind == 0 ? 8u * uint32_t(args.x_row_stride) : 0u;
-  uint8_t* xbuf = smem + S * stage_bytes;
-  // barriers live at the end of the (max-sized) dynamic smem, past every layer's stages
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgBarrierOffset);
-  uint64_t* empty = full + S;
-  uint64_t* xfull = empty + S;
-  uint64_t* acc_full = xfull + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tq_per_b = args.T_pad / 64;
-  const int b0 = int((long long)args.B * split / a.splits);
-  const int b1 = int((long long)args.B * (split + 1) / a.splits);
-  const int total = (b1 - b0) * tq_per_b;
-  const uint32_t tmem_cols = tmem_cols_for(a.mg * a.n_tile, 1);
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1 + kWgProd);
-      mbar_init(&empty[s], 1);
-      mbar_init(&xfull[s], 1);
-    }
-    mbar_init(&acc_full[0], 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  pdl_wait();
-  if (clk != nullptr && threadIdx.x == 0) clk[1] = clock64();
-  const uint32_t tmem = *tmem_slot;
-  if (warp == kWgProdWarps) {
-    if (elect_one()) {
-      tma_prefetch(tm_di);
-      const uint32_t* rows = batch_rows(args.rows, args.rows_slot, args.B);
-      for (int it = 0; it < total; ++it) {
-        const int s = it % S, ph = (it / S) & 1;
-        const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
-        mbar_wait(&empty[s], ph ^ 1);
-        if (a.kind == 0) {
-          mbar_arrive_expect_tx(&xfull[s], xbytes);
-          bulk_load(xbuf + s * ((xbytes + 1023) & ~1023u),
-                    args.x + (size_t(rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride,
-                    xbytes, &xfull[s]);
-        }
-#if SNN_WG_EXP == 2
-        constexpr int kLoadPlanes = 1;  // timing experiment only
-#else
-        constexpr int kLoadPlanes = 3;
-#endif
-        mbar_arrive_expect_tx(&full[s], kLoadPlanes * ptile);
-        uint8_t* Bp = smem + s * stage_bytes + a.mg * kPlaneTile;
-        for (int p = 0; p < kLoadPlanes; ++p)
-          tma_load_2d(Bp + p * ptile, tm_di, &full[s], bb * args.T_pad + tq * 64,
-                      p * a.N_pad + ntile * a.n_tile);
-      }
-    }
-    __syncwarp();
-  } else if (warp == kWgProdWarps + 1) {
-    const uint32_t idesc = idesc_bf16(128, a.n_tile, false, false);
-    if (elect_one()) {
-      for (int it = 0; it < total; ++it) {
-        const int s = it % S, ph = (it / S) & 1;
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        if (clk != nullptr && it == 0) clk[2] = clock64();
-        const uint32_t A = smem_u32(smem + s * stage_bytes);
-        const uint32_t Bp = A + a.mg * kPlaneTile;
-#pragma unroll
-        for (int ks = 0; ks < (SNN_WG_EXP == 3 ? 0 : 4); ++ks) {
-          for (int m = 0; m < nm; ++m) {
-            const uint64_t ad = sdesc_sw128(A + m * kPlaneTile + ks * 32, 16, 1024);
-#pragma unroll
-            for (int p = 2; p >= 0; --p) {
-              const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
-              umma_bf16(tmem + m * a.n_tile, ad, bd, idesc, (it | ks | (2 - p)) != 0);
-            }
-          }
-        }
-        umma_commit(&empty[s]);
-      }
-      umma_commit(&acc_full[0]);
-      if (clk != nullptr) clk[3] = clock64();
-    }
-    __syncwarp();
-  } else {
-    // A producers: nm tiles [128 k-rows][64 time cols], K-major SW128.  Thread p:
-    // row p % 128 of every tile, 16-byte chunks 4h..4h+3 (h = p / 128: 32 steps).
-    // kind 0 decodes the bulk-copied dataset bytes from smem; kind 1 loads the
-    // time-packed spike word (L2-resident) one stage ahead.
-    const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
-    auto fetch = [&](int it, int m) -> uint32_t {
-      const int k = (mt0 + m) * 128 + row;
-      if (a.kind == 0 || it >= total || m >= nm) return 0u;
-      const int bb = b0 + it / tq_per_b, tq = it % tq_per_b;
-      return __ldg(a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) +
-                   size_t(bb) * (args.T_pad / 32) + tq * 2 + h);
-    };
-    uint32_t cur[kWgMgMax], nxt[kWgMgMax];
-    const int xsh = (a.kind == 0 && args.xshift != nullptr) ? *args.xshift : 0;
-#pragma unroll
-    for (int m = 0; m < kWgMgMax; ++m) cur[m] = fetch(0, m);
-    for (int it = 0; it < total; ++it) {
-      const int s = it % S, ph = (it / S) & 1;
-#pragma unroll
-      for (int m = 0; m < kWgMgMax; ++m) nxt[m] = fetch(it + 1, m);
-      mbar_wait(&empty[s], ph ^ 1);
-      if (a.kind == 0) {
-        mbar_wait(&xfull[s], ph);
-        const uint8_t* xs = xbuf + s * ((xbytes + 1023) & ~1023u) + 4 * h * args.x_row_stride;
-#pragma unroll
-        for (int m = 0; m < kWgMgMax; ++m) {
-          if (m >= nm) break;
-          const int k = (mt0 + m) * 128 + row;
-          // rolled feature k reads staged feature (k - xsh) mod in (shift_augment)
-          int src = k;
-          if (xsh != 0)
-            src = k >= args.in_features ? args.x_row_stride : (k >= xsh ? k - xsh : k - xsh + args.in_features);
-          uint32_t v = 0;
-          if (src < args.x_row_stride) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v |= uint32_t(xs[j * args.x_row_stride + src]) << (8 * j);
-          }
-          cur[m] = v;
-        }
-      }
-      const uint32_t A = smem_u32(smem + s * stage_bytes);
-#pragma unroll
-      for (int m = 0; m < (SNN_WG_EXP == 1 ? 0 : kWgMgMax); ++m) {
-        if (m >= nm) break;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t byte = (cur[m] >> (8 * j)) & 0xFFu;
-          st_shared_v4(A + m * kPlaneTile + sw128_off(row, 4 * h + j),
-                       a.kind == 0 ? expand_bits_msb(byte) : expand_bits_lsb(byte));
-        }
-      }
-      fence_async_smem();
-      mbar_arrive(&full[s]);
-#pragma unroll
-      for (int m = 0; m < kWgMgMax; ++m) cur[m] = nxt[m];
-    }
-    // epilogue: TMEM -> smem (row per thread, rows padded by 16 bytes so the 8
-    // rows of a quarter-warp hit distinct banks) -> one 1-D bulk store per row.
-    // Warp w reads TMEM lanes 32 (w % 4)..; the two halves split the columns.
-    mbar_wait(&acc_full[0], 0);
-    tc_fence_after();
-    if (clk != nullptr && threadIdx.x == 0) clk[4] = clock64();
-    const uint32_t row_bytes = uint32_t(a.n_tile) * 4u;
-    const uint32_t row_stride = wg_epi_row_stride(a.n_tile);
-    const int nc = a.n_tile / 32, c0 = h * nc / 2, c1 = (h + 1) * nc / 2;
-    for (int m = 0; m < nm; ++m) {
-      uint8_t* srow = smem + (size_t(m) * 128 + row) * row_stride;  // stages are free now
-      for (int c = c0; c < c1; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + (uint32_t((warp & 3) * 32) << 16) + m * a.n_tile + c * 32, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint4 v4 = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-          if (total == 0) v4 = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(srow + c * 128 + j * 16) = v4;
-        }
-      }
-    }
-    fence_async_smem();
-    asm volatile("bar.sync 1, %0;" ::"r"(kWgProd) : "memory");
-    if (h == 0) {
-      for (int m = 0; m < nm; ++m) {
-        const int k = (mt0 + m) * 128 + row;
-        bulk_store(a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile,
-                   smem + (size_t(m) * 128 + row) * row_stride, row_bytes);
-      }
-      bulk_commit_wait_all();
-    }
-    tc_fence_before();
-  }
-  pdl_launch_dependents();
-  __syncthreads();
-  if (clk != nullptr && threadIdx.x == 0) {
-    clk[5] = clock64();
-    clk[7] = globaltimer();
-    clk[14] = clk[6];
-    clk[15] = clk[7];
-  }
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc_any(tmem_cols, tmem);
-  }
-}
-
-// ============================================================================
 // K2r / K3r  the DECLARED RLIF cell (not in the reference; oracle/spiketrain_oracle.h).
 // The input projection I = A W runs on tcgen05 in k_lif_fwd (FwdLayer.i_out: no
 // scan); the recurrence couples every neuron of a sample at every step, so the
@@ -2811,14 +2541,17 @@ __device__ __forceinline__ uint32_t* tail_scratch() {
 // value in double with a fixed-shape tree (deterministic; the reference's running
 // float sum over (b, n) differs by rounding only), then the histogram is zeroed
 // for the next step.  Whole block calls; thread 0 holds the value.
-__device__ __forceinline__ float activity_value(const ReduceArgs& r, int m) {
-  double* s_lo = reinterpret_cast<double*>(tail_scratch());
-  double* s_hi = s_lo + 256;
+// scratch: >= 4 KB of shared memory; nthr: the calling threads (ids 0..nthr-1, a
+// power of two, synchronised with named barrier 1)
+__device__ __forceinline__ void bar1(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory"); }
+__device__ __forceinline__ float activity_value(const ReduceArgs& r, int m, uint32_t* scratch, int nthr) {
+  double* s_lo = reinterpret_cast<double*>(scratch);
+  double* s_hi = s_lo + nthr;
   const int tid = threadIdx.x;
-  __syncthreads();  // the scratch may still be read by the previous helper
+  bar1(nthr);  // the scratch may still be read by the previous helper
   unsigned int* h = r.hist + size_t(m) * r.hist_stride;
   double lo = 0.0, hi = 0.0;
-  for (int c = tid; c <= r.reg_T; c += blockDim.x) {
+  for (int c = tid; c <= r.reg_T; c += nthr) {
     const unsigned k = h[c];
     if (k == 0u) continue;
     const float rate = __fdiv_rn(float(c), float(r.reg_T));
@@ -2829,19 +2562,19 @@ __device__ __forceinline__ float activity_value(const ReduceArgs& r, int m) {
   }
   s_lo[tid] = lo;
   s_hi[tid] = hi;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+  bar1(nthr);
+  for (int w = nthr / 2; w > 0; w >>= 1) {
     if (tid < w) {
       s_lo[tid] += s_lo[tid + w];
       s_hi[tid] += s_hi[tid + w];
     }
-    __syncthreads();
+    bar1(nthr);
   }
   const float n = r.mon_n[m];
   const float v = __fadd_rn(__fmul_rn(r.lambda_low, __fdiv_rn(float(s_lo[0]), n)),
                             __fmul_rn(r.lambda_high, __fdiv_rn(float(s_hi[0]), n)));
-  __syncthreads();
-  for (int c = tid; c <= r.reg_T; c += blockDim.x) h[c] = 0u;
+  bar1(nthr);
+  for (int c = tid; c <= r.reg_T; c += nthr) h[c] = 0u;
   return v;
 }
 
@@ -2893,26 +2626,27 @@ constexpr int kRedElemsPerBlock = 128;  // W elements per 256-thread block (lane
 // per-sample CE terms (objective.hpp:57-72) or the per-(sample, class) rate-MSE
 // terms (objective.hpp:150-157) -- and the hit count.  Whole block calls; thread
 // 0 holds the results.
-__device__ __forceinline__ void loss_and_hits(const ReduceArgs& r, float& loss, int& hits) {
-  float* sl = reinterpret_cast<float*>(tail_scratch());
-  int* sc = reinterpret_cast<int*>(tail_scratch() + 1024);
+__device__ __forceinline__ void loss_and_hits(const ReduceArgs& r, float& loss, int& hits,
+                                              uint32_t* scratch, int nthr) {
+  float* sl = reinterpret_cast<float*>(scratch);
+  int* sc = reinterpret_cast<int*>(scratch + 1024);
   const int tid = threadIdx.x;
   const float* terms = r.loss_terms != nullptr ? r.loss_terms : r.loss_b;
   loss = 0.0f;
   hits = 0;
   for (int b0 = 0; b0 < r.n_loss_terms; b0 += 1024) {
     const int nb = min(1024, r.n_loss_terms - b0);
-    __syncthreads();
-    for (int i = tid; i < nb; i += blockDim.x) sl[i] = terms[b0 + i];
-    __syncthreads();
+    bar1(nthr);
+    for (int i = tid; i < nb; i += nthr) sl[i] = terms[b0 + i];
+    bar1(nthr);
     if (tid == 0)
       for (int i = 0; i < nb; ++i) loss = __fadd_rn(loss, sl[i]);
   }
   for (int b0 = 0; b0 < r.B; b0 += 1024) {
     const int nb = min(1024, r.B - b0);
-    __syncthreads();
-    for (int i = tid; i < nb; i += blockDim.x) sc[i] = r.correct_b[b0 + i];
-    __syncthreads();
+    bar1(nthr);
+    for (int i = tid; i < nb; i += nthr) sc[i] = r.correct_b[b0 + i];
+    bar1(nthr);
     if (tid == 0)
       for (int i = 0; i < nb; ++i) hits += sc[i];
   }
@@ -2982,14 +2716,14 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     // k_peer_gather)
     float loss;
     int hits;
-    loss_and_hits(a, loss, hits);
+    loss_and_hits(a, loss, hits, tail_scratch(), 256);
     if (tid == 0) {
       gout[a.n_params] = loss;
       gout[a.n_params + 1] = float(hits);
       if (a.update && a.xchg == nullptr) *a.step += 1;  // peer tail: k_peer_gather advances it
     }
     for (int m = 0; m < a.n_mon; ++m) {
-      const float v = activity_value(a, m);
+      const float v = activity_value(a, m, tail_scratch(), 256);
       if (tid == 0) gout[a.n_params + 2 + m] = v;
     }
   }
@@ -3258,6 +2992,537 @@ __global__ void __launch_bounds__(256) k_peer_gather(const __grid_constant__ Pee
   }
 }
 
+// ============================================================================
+// K5  k_wgrad: partial[s][k][n] = sum_{rows in split s} A[k][row] * dI[row][n]
+// A binary (dataset time bits or time-packed spikes), exact in bf16 (K-major,
+// decoded by warps 0-3); dI as 3 bf16 planes via TMA (MN-major).  Epilogue
+// writes f32 partials; k_reduce sums them in fixed order (deterministic).
+// grid (M_pad/128, N_pad/N_TILE, splits); block 192.
+// ============================================================================
+struct WgradLayer {
+  const uint32_t* s_tp;    // kind 1: time-packed spikes [K_pad][B*T_pad/32]
+  float* partial;          // [splits][M_pad][N_pad]
+  int kind, M_pad, N_pad, n_tile, splits, m_tiles, n_tiles, block_start;
+  int mg, m_groups;        // m-tiles per CTA (share every dI stage), groups
+  int stages;              // pipeline depth for this layer's stage size
+};
+// B operand: dI planes [3][N_pad][B*T_pad] (K-major rows = output neurons)
+struct WgradArgs {
+  WgradLayer layer[kMaxLayers];
+  int n_layers;
+  const uint8_t* x;        // kind 0: staged dataset
+  const uint32_t* rows;    // kind 0: [B]
+  const int64_t* rows_slot;  // schedule mode: rows += *rows_slot * B (else nullptr)
+  long long* dbg_clk;      // optional [blocks][kClkStride] phase timestamps
+  const int32_t* xshift;   // kind 0: batch roll along the features (shift_augment)
+  int B, T_pad, x_row_stride, in_features;
+};
+struct WgradMaps {
+  CUtensorMap m[kMaxLayers];   // dI planes (B operand)
+  CUtensorMap pm[kMaxLayers];  // fused tail: f32 partials [splits*M_pad][N_pad], box 32 x 128, SW128
+};
+
+constexpr int kWgStagesMax = 6;
+constexpr int kWgMgMax = 4;
+#ifndef SNN_WG_EXP
+#define SNN_WG_EXP 0  // timing experiments (tests/clk_probe.py only): 1 no decode, 2 one dI plane, 3 no MMA
+#endif
+// A-operand producers: kWgProdWarps warps; thread p decodes row p % 128 of every
+// M-tile, time half p / 128 (64 steps per stage = 2 halves of 32)
+constexpr int kWgProdWarps = 8;
+constexpr int kWgProd = 32 * kWgProdWarps;
+constexpr int kWgThreads = kWgProd + 64;  // + TMA warp + MMA warp
+__host__ __device__ constexpr uint32_t wg_stage_bytes(int n_tile, int mg) {
+  return uint32_t(mg) * kPlaneTile + 3 * uint32_t(n_tile) * 128u;  // mg A tiles + 3 B planes
+}
+__host__ __device__ constexpr uint32_t wg_xrun_bytes(int x_row_stride) {
+  return (8u * uint32_t(x_row_stride) + 1023) & ~1023u;
+}
+__host__ __device__ constexpr uint32_t wg_smem_bytes(int n_tile, int mg, int stages, int x_row_stride) {
+  return uint32_t(stages) * (wg_stage_bytes(n_tile, mg) + wg_xrun_bytes(x_row_stride)) + 1024 + 256;
+}
+// epilogue staging row stride (f32 row of n_tile + 16 bytes of bank padding)
+__host__ __device__ constexpr uint32_t wg_epi_row_stride(int n_tile) { return uint32_t(n_tile) * 4u + 16u; }
+// the launch always requests the full carve-out: barriers at kWgBarrierOffset
+constexpr uint32_t kWgSmemLaunch = 227 * 1024;
+
+// barriers at a fixed offset past the largest per-layer stage footprint
+constexpr uint32_t kWgBarrierOffset = 227 * 1024 - 2048;
+constexpr uint32_t kWgRedBarOffset = kWgBarrierOffset + 1024;  // fused tail: partial-load barrier
+
+// Fused step tail (one rank, training step): after its partial is written, every
+// CTA of an output tile waits on the tile's arrival counter (all of the launch's
+// CTAs are co-resident: the split model keeps the grid within one wave), then the
+// tile's S CTAs each take 1/S of its elements, sum the S partials in ascending
+// split order (deterministic, L2-resident), run Adam / SGD and refresh the bf16
+// planes; the beta / bias / gamma entries are spread over the CTAs (one warp per
+// element), block 0 sums the loss / hits / regularizer (StepResult), and the last
+// CTA to finish advances the step and schedule counters and re-arms the tile
+// counters.  Replaces k_reduce_adam and its launch.
+struct WgradTail {
+  unsigned int* tile_cnt;     // per output tile (zeroed; re-armed by the last CTA)
+  unsigned int* done;         // CTA completion counter
+  int64_t* rows_slot;         // schedule mode: advanced once per step (else nullptr)
+  int n_tiles_total;
+  int64_t w_off[kMaxLayers];  // flat offset of each layer's W entry
+  int rows[kMaxLayers], cols[kMaxLayers];  // K[j], N[j] (unpadded)
+  int tile_base[kMaxLayers];  // first tile id of each layer
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Producer threads (kWgProd, named barrier 1) of one CTA after its accumulator is
+// staged in smem (rows m*128 + r, padded row stride): write the partial, wait for
+// the tile, reduce 1/S of it + Adam, the CTA's share of the vector entries, and
+// (block 0) the loss / hits / StepResult.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// the fused tail's batch reductions that need no weight gradient: beta / bias /
+// gamma entries (one warp per element, spread over the CTAs) and, in block 0, the
+// loss / hits / regularizer (StepResult); scratch: 8 KB of free shared memory
+__device__ __forceinline__ void wgrad_vec_and_loss(const ReduceArgs& rd, const AdamArgs& ad, float bc1,
+                                                   float bc2, uint8_t* scratch_smem, long long* clk) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (clk != nullptr && tid == 0) clk[10] = clock64();
+  // 4. beta / bias / gamma entries: one warp per element, spread over the CTAs
+  for (int v = int(blockIdx.x) * kWgProdWarps + warp; v < rd.n_vec; v += int(gridDim.x) * kWgProdWarps) {
+    const int64_t i = rd.vec_index[v];
+    const Entry en = rd.entries[find_entry(rd.entries, rd.n_entries, i)];
+    const int64_t li = i - en.offset;
+    const float* __restrict__ src =
+        (en.kind == kEntryB ? rd.dbias_part[en.layer]
+                            : en.kind == kEntryGamma ? rd.dgamma_part[en.layer] : rd.dbeta_part[en.layer]) + li;
+    float gs = 0.0f;
+    // lane-strided partials, 8 loads in flight per lane, summed in the same order
+    // as k_reduce_adam's loop (lane's samples ascending), then the warp tree
+    const int cnt = (en.kind == kEntryBeta && en.beta_mode != 0) ? (en.beta_mode == 1 ? rd.B * en.cols : 0)
+                                                                 : rd.B;
+    const int64_t stride = (en.kind == kEntryBeta && en.beta_mode != 0) ? 1 : en.cols;
+    for (int q0 = lane; q0 < cnt; q0 += 32 * 8) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = q0 + 32 * u < cnt ? __ldcg(src + int64_t(q0 + 32 * u) * stride) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + 32 * u < cnt) gs = __fadd_rn(gs, x[u]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) gs = __fadd_rn(gs, __shfl_xor_sync(0xffffffffu, gs, off));
+    if (lane == 0) {
+      if (en.kind == kEntryBeta || en.kind == kEntryGamma) {
+        const float beta = rd.params[i];
+        if (!(beta > 0.0f && beta < 1.0f)) gs = 0.0f;  // clip01 gradient (autodiff.hpp:353-355)
+      }
+      rd.grads[i] = gs;
+      adam_one(ad, i, gs, bc1, bc2);
+    }
+  }
+  if (clk != nullptr && tid == 0) clk[11] = clock64();
+  // 5. block 0: loss sum in batch order (objective.hpp:57-72) + hits -> StepResult
+  if (blockIdx.x == 0) {
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(scratch_smem);
+    bar1(kWgProd);
+    float loss;
+    int hits;
+    loss_and_hits(rd, loss, hits, scratch, kWgProd);
+    float l = __fdiv_rn(loss, ad.loss_denom);
+    for (int m = 0; m < rd.n_mon; ++m) {  // optimize.hpp:185-191
+      const float v = activity_value(rd, m, scratch, kWgProd);
+      if (tid == 0) {
+        rd.grads[rd.n_params + 2 + m] = v;
+        l = __fadd_rn(l, v);
+      }
+    }
+    if (tid == 0) {
+      rd.grads[rd.n_params] = loss;
+      rd.grads[rd.n_params + 1] = float(hits);
+      *ad.loss_out = l;
+      *ad.acc_out = double(hits) / double(ad.B_global);
+    }
+  }
+}
+
+__device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j, const CUtensorMap* pmap,
+                                                  int split, int mt0, int nm, int ntile, uint8_t* smem,
+                                                  const ReduceArgs& rd, const AdamArgs& ad,
+                                                  const WgradTail& tl, int64_t s, long long* clk) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt4 = a.n_tile / 4, ncg = a.n_tile / 32;
+  const int S = a.splits;
+  const int unit = mt0 / a.mg + (a.m_tiles + a.mg - 1) / a.mg * ntile;
+  const int tile = tl.tile_base[j] + unit;
+  // 1. own partial by TMA tensor stores from the SW128 staging; once the writes are
+  //    performed, arrive on the tile counter and wait for the tile's other splits
+  if (tid == 0) {
+    for (int m = 0; m < nm; ++m)
+      for (int c = 0; c < ncg; ++c)
+        tma_store_2d(pmap, smem + size_t(m * ncg + c) * 16384, ntile * a.n_tile + c * 32,
+                     split * a.M_pad + (mt0 + m) * 128);
+    bulk_commit();
+  }
+  const float bc1 = ad.bc[2 * s], bc2 = ad.bc[2 * s + 1];
+  // while the stores drain and the tile's other splits finish: the work that does
+  // not depend on the weight gradients (beta / bias / gamma, loss / StepResult)
+  wgrad_vec_and_loss(rd, ad, bc1, bc2, smem + size_t(nm) * ncg * 16384, clk);
+  if (tid == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (clk != nullptr) clk[8] = clock64();
+    fence_proxy_async_global();
+    __threadfence();
+    atomicAdd(tl.tile_cnt + tile, 1u);
+    while (ld_acquire_gpu_u32(tl.tile_cnt + tile) < unsigned(S)) __nanosleep(32);
+    fence_proxy_async_global();  // the bulk loads below see the other splits' partials
+    if (clk != nullptr) clk[9] = clock64();
+  }
+  bar1(kWgProd);
+  // 2. this CTA's rows [r0, r1) of the tile, in chunks of cr rows: every split's
+  //    rows are bulk-loaded into smem [split][row][n_tile], summed in the order of
+  //    k_reduce's sum_partials_pair (splits [0, S/2) and [S/2, S) ascending, then
+  //    the halves added: forward_backward and a train step see the same bits),
+  //    then Adam / SGD and the bf16 plane refresh per element
+  const int R = nm * 128;
+  const int r0 = R * split / S, r1 = R * (split + 1) / S;
+  const uint32_t rowb = uint32_t(a.n_tile) * 4u;
+  const int cr = max(1, min(r1 - r0, int((kWgBarrierOffset - 1024) / (uint32_t(S) * rowb))));
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(smem + kWgRedBarOffset);
+  const int rows_j = tl.rows[j], cols_j = tl.cols[j];
+  const bool contig = a.n_tiles == 1;  // a tile's rows are one contiguous run per split
+  int phase = 0;
+  for (int c = r0; c < r1; c += cr, phase ^= 1) {
+    const int nr = min(cr, r1 - c);
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(rbar, uint32_t(S) * uint32_t(nr) * rowb);
+      __syncwarp();
+      const int n_copies = contig ? S : S * nr;
+      for (int q = lane; q < n_copies; q += 32) {
+        const int sp = contig ? q : q / nr, rr = contig ? 0 : q % nr;
+        const float* src = a.partial + (size_t(sp) * a.M_pad + mt0 * 128 + c + rr) * a.N_pad +
+                           size_t(ntile) * a.n_tile;
+        bulk_load(smem + (size_t(sp) * cr + rr) * rowb, src, contig ? uint32_t(nr) * rowb : rowb, rbar);
+      }
+    }
+    mbar_wait(rbar, phase);
+    if (clk != nullptr && tid == 0 && c == r0) clk[12] = clock64();
+    for (int g = tid; g < nr * nt4; g += kWgProd) {
+      const int rr = g / nt4, c4 = g % nt4;
+      const int k = mt0 * 128 + c + rr, n0 = ntile * a.n_tile + 4 * c4;
+      if (k >= rows_j || n0 >= cols_j) continue;
+      const int64_t i0 = tl.w_off[j] + int64_t(k) * cols_j + n0;
+      const int nv = min(4, cols_j - n0);
+      float p0[4], m0[4], v0[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < nv) {
+          p0[e] = ad.params[i0 + e];
+          m0[e] = ad.m[i0 + e];
+          v0[e] = ad.v[i0 + e];
+        }
+      const float4* col = reinterpret_cast<const float4*>(smem + size_t(rr) * rowb) + c4;
+      const size_t sstep = size_t(cr) * rowb / 16;  // float4s between splits
+      float4 acc[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int s1 = (q + 1) * S / 2;
+        for (int sp = q * S / 2; sp < s1; sp += 8) {
+          float4 x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (sp + u < s1) x[u] = col[(sp + u) * sstep];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (sp + u < s1) {
+              a4.x = __fadd_rn(a4.x, x[u].x);
+              a4.y = __fadd_rn(a4.y, x[u].y);
+              a4.z = __fadd_rn(a4.z, x[u].z);
+              a4.w = __fadd_rn(a4.w, x[u].w);
+            }
+        }
+        acc[q] = a4;
+      }
+      const float gv[4] = {__fadd_rn(acc[0].x, acc[1].x), __fadd_rn(acc[0].y, acc[1].y),
+                           __fadd_rn(acc[0].z, acc[1].z), __fadd_rn(acc[0].w, acc[1].w)};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < nv) {
+          rd.grads[i0 + e] = gv[e];
+          refresh_planes(ad, j, k, n0 + e, adam_apply(ad, i0 + e, gv[e], p0[e], m0[e], v0[e], bc1, bc2));
+        }
+    }
+    bar1(kWgProd);  // the chunk's smem is reloaded next
+    if (clk != nullptr && tid == 0 && c == r0) clk[13] = clock64();
+  }
+}
+
+// One launch for every Linear layer: block -> (layer, m-group, n-tile, split), the
+// split index innermost (a tile's CTAs are consecutive).
+// A CTA accumulates mg M-tiles (mg x n_tile TMEM columns) so each dI stage
+// loaded by TMA feeds mg MMAs.  kFused: the one-rank step tail runs in the
+// epilogue (wgrad_fused_epilogue) instead of k_reduce_adam.
+template <bool kFused>
+__global__ void __launch_bounds__(kWgThreads, 1)
+    k_wgrad(const __grid_constant__ WgradMaps maps, WgradArgs args, const __grid_constant__ ReduceArgs rd,
+            const __grid_constant__ AdamArgs ad, const __grid_constant__ WgradTail tl) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  long long* clk = args.dbg_clk != nullptr ? args.dbg_clk + size_t(blockIdx.x) * kClkStride : nullptr;
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[0] = clock64();
+    clk[6] = globaltimer();
+  }
+  int li = 0;
+  while (li + 1 < args.n_layers && int(blockIdx.x) >= args.layer[li + 1].block_start) ++li;
+  const WgradLayer a = args.layer[li];
+  const CUtensorMap* tm_di = &maps.m[li];
+  const int local = int(blockIdx.x) - a.block_start;
+  const int split = local % a.splits, unit = local / a.splits;
+  const int mgi = unit % a.m_groups, ntile = unit / a.m_groups;
+  // fused tail: the step counter before any CTA can advance it (bias corrections)
+  const int64_t step0 = kFused ? *reinterpret_cast<volatile const int64_t*>(rd.step) : 0;
+  const int mt0 = mgi * a.mg;
+  const int nm = min(a.mg, a.m_tiles - mt0);  // M-tiles of this CTA
+  const int S = a.stages;
+  const uint32_t stage_bytes = wg_stage_bytes(a.n_tile, a.mg);
+  const uint32_t ptile = uint32_t(a.n_tile) * 128u;  // one plane: n_tile rows x 64 cols
+  // kind 0: the dataset bytes of one (sample, 64-step block) are one contiguous
+  // run of 8 * x_row_stride bytes -> one bulk copy per stage into xbuf
+  const uint32_t xbytes = a.kind == 0 ? 8u * uint32_t(args.x_row_stride) : 0u;
+  uint8_t* xbuf = smem + S * stage_bytes;
+  // barriers live at the end of the (max-sized) dynamic smem, past every layer's stages
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgBarrierOffset);
+  uint64_t* empty = full + S;
+  uint64_t* xfull = empty + S;
+  uint64_t* acc_full = xfull + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tq_per_b = args.T_pad / 64;
+  // split s takes iterations [it0, it1) of the (sample, 64-step block) sequence:
+  // finer than whole samples, so the splits of a tile finish closer together
+  const int iters_all = args.B * tq_per_b;
+  const int it0 = int((long long)iters_all * split / a.splits);
+  const int total = int((long long)iters_all * (split + 1) / a.splits) - it0;
+  const uint32_t tmem_cols = tmem_cols_for(a.mg * a.n_tile, 1);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1 + kWgProd);
+      mbar_init(&empty[s], 1);
+      mbar_init(&xfull[s], 1);
+    }
+    mbar_init(&acc_full[0], 1);
+    if (kFused) mbar_init(reinterpret_cast<uint64_t*>(smem + kWgRedBarOffset), 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc_any(tmem_cols, tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  if (clk != nullptr && threadIdx.x == 0) clk[1] = clock64();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == kWgProdWarps) {
+    if (elect_one()) {
+      tma_prefetch(tm_di);
+      const uint32_t* rows = batch_rows(args.rows, args.rows_slot, args.B);
+      for (int it = 0; it < total; ++it) {
+        const int s = it % S, ph = (it / S) & 1;
+        const int bb = (it0 + it) / tq_per_b, tq = (it0 + it) % tq_per_b;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (a.kind == 0) {
+          mbar_arrive_expect_tx(&xfull[s], xbytes);
+          bulk_load(xbuf + s * ((xbytes + 1023) & ~1023u),
+                    args.x + (size_t(rows[bb]) * (args.T_pad / 8) + tq * 8) * args.x_row_stride,
+                    xbytes, &xfull[s]);
+        }
+#if SNN_WG_EXP == 2
+        constexpr int kLoadPlanes = 1;  // timing experiment only
+#else
+        constexpr int kLoadPlanes = 3;
+#endif
+        mbar_arrive_expect_tx(&full[s], kLoadPlanes * ptile);
+        uint8_t* Bp = smem + s * stage_bytes + a.mg * kPlaneTile;
+        for (int p = 0; p < kLoadPlanes; ++p)
+          tma_load_2d(Bp + p * ptile, tm_di, &full[s], bb * args.T_pad + tq * 64,
+                      p * a.N_pad + ntile * a.n_tile);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kWgProdWarps + 1) {
+    const uint32_t idesc = idesc_bf16(128, a.n_tile, false, false);
+    if (elect_one()) {
+      for (int it = 0; it < total; ++it) {
+        const int s = it % S, ph = (it / S) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (clk != nullptr && it == 0) clk[2] = clock64();
+        const uint32_t A = smem_u32(smem + s * stage_bytes);
+        const uint32_t Bp = A + a.mg * kPlaneTile;
+#pragma unroll
+        for (int ks = 0; ks < (SNN_WG_EXP == 3 ? 0 : 4); ++ks) {
+          for (int m = 0; m < nm; ++m) {
+            const uint64_t ad = sdesc_sw128(A + m * kPlaneTile + ks * 32, 16, 1024);
+#pragma unroll
+            for (int p = 2; p >= 0; --p) {
+              const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
+              umma_bf16(tmem + m * a.n_tile, ad, bd, idesc, (it | ks | (2 - p)) != 0);
+            }
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&acc_full[0]);
+      if (clk != nullptr) clk[3] = clock64();
+    }
+    __syncwarp();
+  } else {
+    // A producers: nm tiles [128 k-rows][64 time cols], K-major SW128.  Thread p:
+    // row p % 128 of every tile, 16-byte chunks 4h..4h+3 (h = p / 128: 32 steps).
+    // kind 0 decodes the bulk-copied dataset bytes from smem; kind 1 loads the
+    // time-packed spike word (L2-resident) one stage ahead.
+    const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
+    auto fetch = [&](int it, int m) -> uint32_t {
+      const int k = (mt0 + m) * 128 + row;
+      if (a.kind == 0 || it >= total || m >= nm) return 0u;
+      const int bb = (it0 + it) / tq_per_b, tq = (it0 + it) % tq_per_b;
+      return __ldg(a.s_tp + size_t(k) * (size_t(args.B) * args.T_pad / 32) +
+                   size_t(bb) * (args.T_pad / 32) + tq * 2 + h);
+    };
+    uint32_t cur[kWgMgMax], nxt[kWgMgMax];
+    const int xsh = (a.kind == 0 && args.xshift != nullptr) ? *args.xshift : 0;
+#pragma unroll
+    for (int m = 0; m < kWgMgMax; ++m) cur[m] = fetch(0, m);
+    for (int it = 0; it < total; ++it) {
+      const int s = it % S, ph = (it / S) & 1;
+#pragma unroll
+      for (int m = 0; m < kWgMgMax; ++m) nxt[m] = fetch(it + 1, m);
+      mbar_wait(&empty[s], ph ^ 1);
+      if (a.kind == 0) {
+        mbar_wait(&xfull[s], ph);
+        const uint8_t* xs = xbuf + s * ((xbytes + 1023) & ~1023u) + 4 * h * args.x_row_stride;
+#pragma unroll
+        for (int m = 0; m < kWgMgMax; ++m) {
+          if (m >= nm) break;
+          const int k = (mt0 + m) * 128 + row;
+          // rolled feature k reads staged feature (k - xsh) mod in (shift_augment)
+          int src = k;
+          if (xsh != 0)
+            src = k >= args.in_features ? args.x_row_stride : (k >= xsh ? k - xsh : k - xsh + args.in_features);
+          uint32_t v = 0;
+          if (src < args.x_row_stride) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v |= uint32_t(xs[j * args.x_row_stride + src]) << (8 * j);
+          }
+          cur[m] = v;
+        }
+      }
+      const uint32_t A = smem_u32(smem + s * stage_bytes);
+#pragma unroll
+      for (int m = 0; m < (SNN_WG_EXP == 1 ? 0 : kWgMgMax); ++m) {
+        if (m >= nm) break;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t byte = (cur[m] >> (8 * j)) & 0xFFu;
+          st_shared_v4(A + m * kPlaneTile + sw128_off(row, 4 * h + j),
+                       a.kind == 0 ? expand_bits_msb(byte) : expand_bits_lsb(byte));
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(&full[s]);
+#pragma unroll
+      for (int m = 0; m < kWgMgMax; ++m) cur[m] = nxt[m];
+    }
+    // epilogue: TMEM -> smem (row per thread, rows padded by 16 bytes so the 8
+    // rows of a quarter-warp hit distinct banks) -> one 1-D bulk store per row.
+    // Warp w reads TMEM lanes 32 (w % 4)..; the two halves split the columns.
+    mbar_wait(&acc_full[0], 0);
+    tc_fence_after();
+    if (clk != nullptr && threadIdx.x == 0) clk[4] = clock64();
+    const uint32_t row_bytes = uint32_t(a.n_tile) * 4u;
+    const uint32_t row_stride = wg_epi_row_stride(a.n_tile);
+    const int nc = a.n_tile / 32, c0 = h * nc / 2, c1 = (h + 1) * nc / 2;
+    if constexpr (kFused) {
+      // SW128 staging for the TMA tensor stores: tile (m, 32-column group c) is
+      // 128 rows x 128 bytes, 16-byte chunk j of row r at chunk j ^ (r & 7)
+      for (int m = 0; m < nm; ++m)
+        for (int c = c0; c < c1; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + (uint32_t((warp & 3) * 32) << 16) + m * a.n_tile + c * 32, r);
+          tmem_ld_wait();
+          const uint32_t base = smem_u32(smem) + uint32_t(m * nc + c) * 16384u + uint32_t(row) * 128u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 v4 = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+            if (total == 0) v4 = make_uint4(0u, 0u, 0u, 0u);
+            st_shared_v4(base + ((uint32_t(j) ^ uint32_t(row & 7)) << 4), v4);
+          }
+        }
+      fence_async_smem();
+      asm volatile("bar.sync 1, %0;" ::"r"(kWgProd) : "memory");
+      wgrad_fused_epilogue(a, li, &maps.pm[li], split, mt0, nm, ntile, smem, rd, ad, tl, step0, clk);
+    }
+    for (int m = 0; m < (kFused ? 0 : nm); ++m) {
+      uint8_t* srow = smem + (size_t(m) * 128 + row) * row_stride;  // stages are free now
+      for (int c = c0; c < c1; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + (uint32_t((warp & 3) * 32) << 16) + m * a.n_tile + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint4 v4 = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          if (total == 0) v4 = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(srow + c * 128 + j * 16) = v4;
+        }
+      }
+    }
+    if constexpr (!kFused) {
+      fence_async_smem();
+      asm volatile("bar.sync 1, %0;" ::"r"(kWgProd) : "memory");
+      if (h == 0) {
+        for (int m = 0; m < nm; ++m) {
+          const int k = (mt0 + m) * 128 + row;
+          bulk_store(a.partial + (size_t(split) * a.M_pad + k) * a.N_pad + ntile * a.n_tile,
+                     smem + (size_t(m) * 128 + row) * row_stride, row_bytes);
+        }
+        bulk_commit_wait_all();
+      }
+    }
+    tc_fence_before();
+  }
+  pdl_launch_dependents();
+  __syncthreads();
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[5] = clock64();
+    clk[7] = globaltimer();
+    clk[14] = clk[6];
+    clk[15] = clk[7];
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc_any(tmem_cols, tmem);
+  }
+  if constexpr (kFused) {
+    // completion: the last CTA advances the step / schedule counters and re-arms
+    // the tile counters (every CTA has passed its tile wait by now)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(tl.done, 1u) == gridDim.x - 1) {
+        for (int t = 0; t < tl.n_tiles_total; ++t) tl.tile_cnt[t] = 0u;
+        *tl.done = 0u;
+        *rd.step = step0 + 1;
+        if (tl.rows_slot != nullptr) *tl.rows_slot += 1;
+        __threadfence();
+      }
+    }
+  }
+}
+
 // Single-rank step tail: k_reduce + k_adam in one launch (no allreduce between
 // them).  Same block roles and the same fixed-order sums as k_reduce, each
 // gradient consumed by Adam in the thread that produced it.  Every block reads
@@ -3328,10 +3593,10 @@ __global__ void __launch_bounds__(256) k_reduce_adam(ReduceArgs r, AdamArgs a, u
     // loss sum in batch order (objective.hpp:57-72) + hits -> StepResult
     float loss;
     int hits;
-    loss_and_hits(r, loss, hits);
+    loss_and_hits(r, loss, hits, tail_scratch(), 256);
     float l = __fdiv_rn(loss, a.loss_denom);
     for (int m = 0; m < r.n_mon; ++m) {  // loss = add(loss, regularizer) per monitor (optimize.hpp:185-191)
-      const float v = activity_value(r, m);
+      const float v = activity_value(r, m, tail_scratch(), 256);
       if (tid == 0) {
         r.grads[r.n_params + 2 + m] = v;
         l = __fadd_rn(l, v);

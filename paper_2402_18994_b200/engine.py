@@ -647,8 +647,9 @@ class Engine:
         return loss.value, acc.value
 
     # ---------------------------------------------------------- diagnostics
-    def debug(self, on: bool = True):
-        self._check(self._L.snn_debug_enable(self._h, int(on)))
+    def debug(self, on=True):
+        """True / 1: capture tensors + clock stamps; 2: clock stamps only."""
+        self._check(self._L.snn_debug_enable(self._h, 2 if on == 2 else int(bool(on))))
 
     def fetch(self, which: str, layer: int = 0) -> np.ndarray:
         idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5, "A": 6, "dI": 7}[which]

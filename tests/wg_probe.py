@@ -1,0 +1,32 @@
+"""Phase clocks of k_wgrad with the fused step tail (debug mode, C1): per CTA
+[prologue, first stage, MMA loop, commit->epilogue, TMEM->smem staging,
+vector entries, loss, TMA store drain, tile wait, first partial load, first chunk
+sum+Adam] in cycles."""
+import os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
+eng = Engine(shd_spec(), TrainConfig(batch_size=256, seed=0), 128)
+eng.synth_dataset(16384, seed=1)
+eng.debug(2)  # clock stamps only
+rows = np.arange(256, dtype=np.uint32)
+for _ in range(3):
+    eng.train_step(rows)
+clk = eng.fetch("clk")
+L = 2
+c = clk[1 + 2 * L]
+valid = c[:, 6] > 0
+c = c[valid]
+cols = [(1, 0), (2, 1), (3, 2), (4, 3), (10, 4), (11, 10), (8, 11), (9, 8), (12, 9), (13, 12)]
+d = np.stack([c[:, a] - c[:, b] for a, b in cols], 1)
+print("wgrad CTAs", valid.sum())
+print("  [prologue, first-stage, mma-loop, commit->epi, staging+vec, loss, store-drain, tile-wait, load, sum+adam] cycles")
+print("  median", np.median(d, 0).astype(int).tolist())
+print("  max   ", d.max(0).tolist())
+gt = c[:, 6:8]
+t0 = gt[:, 0].min()
+print(f"  start spread {(gt[:, 0].max() - t0) / 1e3:.1f} us, end {(gt[:, 1].min() - t0) / 1e3:.1f}..{(gt[:, 1].max() - t0) / 1e3:.1f} us")
+for blk in (0, 52, 53, 105, 106, 126, 127, len(c) - 1):
+    if blk < len(c):
+        print("  cta", blk, d[blk].tolist(), f"start {(gt[blk, 0] - t0) / 1e3:.1f} us")
