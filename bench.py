@@ -315,6 +315,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gemm-planes", type=int, default=3, choices=[1, 2, 3],
+                    help="bf16 operand planes per real GEMM operand: 3 = the fp32 path (default), "
+                         "2 = fast bf16x2 mode, 1 = bf16 (separate lines, own tolerances)")
     args = ap.parse_args()
     warmup = max(3, args.warmup)
     w = WORKLOADS[args.config]
@@ -346,6 +349,10 @@ def main():
                     f"staged) > 126 MB L2; fresh permuted rows every step, no L2 flush"}
     if world > 1:
         config["dp_tail"] = os.environ.get("SNN_DP_TAIL", "peer")  # gradient exchange (parallel.py)
+    dtype = {3: "f32", 2: "bf16x2", 1: "bf16"}[args.gemm_planes]
+    if args.gemm_planes != 3:
+        config["gemm_mode"] = (f"{dtype}: {args.gemm_planes} bf16 plane(s) per real GEMM operand "
+                               "(fast mode; tolerance in DESIGN.md)")
 
     if args.impl == "reference":
         if rank != 0:
@@ -375,7 +382,8 @@ def main():
     spec = shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"],
                     cell=w.get("cell", "lif"))
     B = w["B"]
-    eng = Engine(spec, TrainConfig(batch_size=B, seed=0, lr=1e-3), w["T"], device=local)
+    eng = Engine(spec, TrainConfig(batch_size=B, seed=0, lr=1e-3, gemm_planes=args.gemm_planes), w["T"],
+                 device=local)
     if world > 1:
         # gradient exchange: peer-memory tail (default) or NCCL (SNN_DP_TAIL=nccl)
         from paper_2402_18994_b200.parallel import setup_data_parallel
@@ -501,7 +509,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": dtype,
             "data": "synthetic (synth_raster seed 1, generated in HBM bit-identical to the "
                     "reference), random-init weights (reference init, seed 0)",
             "config": config, "clocks": clocks.summary(),

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 6
+#define SNN_ABI_VERSION 7
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -121,6 +121,13 @@ typedef struct snn_train_config {
    * squared hinge on the rates count/T outside [f_min, f_max]; both lambdas 0 = off
    * (then the band is not checked, like the reference). */
   float f_min, f_max, lambda_low, lambda_high;
+  /* GEMM precision mode (not a reference option): bf16 operand planes per real
+   * operand on the tensor cores.  0 or 3 = the fp32 path (x = hi + mid + lo, 2^-24:
+   * the north_star parity bar); 2 = fast mode (hi + mid, <= 2^-16 relative per
+   * operand; dS uses hi*hi + hi*mid + mid*hi); 1 = bf16 (hi only).  The sparse
+   * readout projection and every scan stay fp32 in all modes.  Fast modes are
+   * reported separately with their own measured tolerance. */
+  int32_t gemm_planes;
 } snn_train_config;
 
 typedef struct snn_engine snn_engine;

@@ -125,6 +125,7 @@ struct TrainConfig {
   double f_max = 1.0;
   double lambda_low = 0.0;
   double lambda_high = 0.0;
+  int gemm_planes = 3;            // engine option: 3 fp32 path, 2 fast (bf16x2), 1 bf16
   std::int64_t max_shift = 0;     // shift augmentation on packed batches
   std::vector<long> shift_axes;   // feature axis only (2 or -1)
   std::uint64_t seed = 0;
@@ -246,6 +247,7 @@ class TrainState {
     c.f_max = float(cfg.f_max);
     c.lambda_low = float(cfg.lambda_low);
     c.lambda_high = float(cfg.lambda_high);
+    c.gemm_planes = int32_t(cfg.gemm_planes);
     snn_engine* e = nullptr;
     check(snn_engine_create(&d, &c, device, &e), nullptr);
     eng_.reset(e);

@@ -272,6 +272,7 @@ class CopyPool {
 struct snn_engine {
   snn_network_desc net{};
   snn_train_config cfg{};
+  int planes = 3;  // bf16 operand planes per real GEMM operand (cfg.gemm_planes)
   int device = 0;
   std::string err;
 
@@ -469,6 +470,9 @@ struct snn_engine {
       if (cfg.max_shift > 0 && ax != 2 && ax != -1)
         fail(SNN_ERR_UNSUPPORTED, "shift axis %d: only the (flat) feature axis 2 / -1 is supported", ax);
     }
+    if (cfg.gemm_planes < 0 || cfg.gemm_planes > 3)
+      fail(SNN_ERR_ARGUMENT, "gemm_planes %d: 1, 2 or 3 (0 = default 3)", cfg.gemm_planes);
+    planes = cfg.gemm_planes == 0 ? 3 : cfg.gemm_planes;
     B = cfg.batch_size;
     T = cfg.time_steps;
     TT = T <= 64 ? 64 : 128;
@@ -1372,6 +1376,7 @@ struct snn_engine {
     for (const auto& grp : fwd_groups()) {
       const int l = grp.first, nl = grp.second;
       FwdArgs f{};
+      f.planes = planes;
       FwdMaps fm{};
       f.x = ds.x.p;
       f.rows = rows_p;
@@ -1468,6 +1473,7 @@ struct snn_engine {
     // hidden backward, top-down: dS on tcgen05 (readout-fed layer: K = classes)
     for (int l = L - 1; l >= 0; --l) {
       BwdArgs bw{};
+      bw.planes = planes;
       bw.v_in = V[l].p;
       bw.beta = params.p + entry_of(kEntryBeta, l).offset;
       bw.beta_stride = net.beta_mode[l] == 0 ? 1 : 0;
@@ -1562,6 +1568,7 @@ struct snn_engine {
       // the fused tail it also reduces them, updates and writes the StepResult
       {
         WgradArgs w{};
+        w.planes = planes;
         w.x = ds.x.p;
         w.rows = rows_p;
         w.rows_slot = slot_p;

@@ -175,6 +175,7 @@ struct FwdArgs {
   long long* dbg_clk;     // optional [gridDim.x*gridDim.y][kClkStride] phase timestamps
   const int32_t* xshift;  // layer 0: batch roll along the features, [0, in_features) (shift_augment)
   int B, T, T_pad, TT, NT, in_kind, stages, spb, in_features;
+  int planes;  // bf16 W planes multiplied (3: the fp32 path; 2 / 1: fast modes)
   float theta;
 };
 
@@ -375,13 +376,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                       xrun, &xfull[xb]);
         }
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile);
+        mbar_arrive_expect_tx(&full[s], uint32_t(a.planes) * kPlaneTile);
         uint8_t* A = smem + s * stage_bytes;
         // W planes [3][K_pad][H_pad] read MN-major: per plane two 64-neuron x 64-k boxes
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < a.planes; ++p)
           for (int h = 0; h < 2; ++h)
             tma_load_2d(A + p * kPlaneTile + h * 8192, &tm_w, &full[s], nt * 128 + h * 64,
                         p * K_pad0 + kb * 64);
+
       }
       // fused layers: once the previous GEMM is complete the stages are idle; the
       // next layer's W planes land in stage kb's A part while the scan runs
@@ -389,8 +391,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&acc_full[0], (li - 1) & 1);
         const int KBl = a.lay[li].K_pad / 64;
         for (int kb = 0; kb < KBl; ++kb) {
-          mbar_arrive_expect_tx(&lfull[kb], 3 * kPlaneTile);
-          for (int p = 0; p < 3; ++p)
+          mbar_arrive_expect_tx(&lfull[kb], uint32_t(a.planes) * kPlaneTile);
+          for (int p = 0; p < a.planes; ++p)
             for (int h = 0; h < 2; ++h)
               tma_load_2d(smem + kb * stage_bytes + p * kPlaneTile + h * 8192, &maps.m[li], &lfull[kb],
                           nt * 128 + h * 64, p * a.lay[li].K_pad + kb * 64);
@@ -416,13 +418,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bt = A + 3 * kPlaneTile;
         const uint32_t d = tmem + buf * NTOT;
+        if (a.planes == 3) {  // the fp32 path, fully unrolled
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
 #pragma unroll
-          for (int p = 2; p >= 0; --p) {
-            const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 2048, 8192, 1024);
-            umma_bf16(d, ad, bd, idesc, (kb | ks | (2 - p)) != 0);
+            for (int p = 2; p >= 0; --p) {
+              const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 2048, 8192, 1024);
+              umma_bf16(d, ad, bd, idesc, (kb | ks | (2 - p)) != 0);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
+            for (int p = a.planes - 1; p >= 0; --p) {
+              const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 2048, 8192, 1024);
+              umma_bf16(d, ad, bd, idesc, (kb | ks | (a.planes - 1 - p)) != 0);
+            }
           }
         }
         umma_commit(&empty[s]);
@@ -441,10 +454,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
-#pragma unroll
-            for (int p = 2; p >= 0; --p) {
+            for (int p = a.planes - 1; p >= 0; --p) {
               const uint64_t ad = sdesc_sw128(A + p * kPlaneTile + ks * 2048, 8192, 1024);
-              umma_bf16(tmem, ad, bd, idesc, (kb | ks | (2 - p)) != 0);
+              umma_bf16(tmem, ad, bd, idesc, (kb | ks | (a.planes - 1 - p)) != 0);
             }
           }
         }
@@ -663,14 +675,9 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
-  pdl_wait();
-  RO_CLK(0)
-  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
-  __shared__ int s_label;
-  if (tid == 0) s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
-  const float beta_l = lane < C ? a.beta[lane * a.beta_stride] : 0.0f;
+  // W [HL][C] is a parameter (written by the previous step's update, long complete):
+  // staged before the dependency wait, overlapping the forward kernel's tail
   {
-    // W rows padded to Cp floats (zeros in the padding) and the spike words
     const int nw = a.HL * C;
     if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
       const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
@@ -681,6 +688,14 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
         w[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
       }
     }
+  }
+  const float beta_l = lane < C ? a.beta[lane * a.beta_stride] : 0.0f;
+  pdl_wait();
+  RO_CLK(0)
+  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
+  __shared__ int s_label;
+  if (tid == 0) s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
+  {
     const uint4* __restrict__ ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
     for (int i = tid; i < T * hw / 4; i += kRoThreads) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
   }
@@ -914,6 +929,7 @@ struct BwdArgs {
   float* dbg_ds;               // optional [B][T_pad][H_pad]
   long long* dbg_clk;          // optional [gridDim.x*gridDim.y][8] phase timestamps
   int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
+  int planes;                  // bf16 planes per real operand (3: fp32 path)
   float theta, slope, aux;
   // activity regularizer on a monitored layer (kReg launches only)
   const uint32_t* s_tp;        // this layer's spikes, time-packed [H_pad][B*T_pad/32]
@@ -1235,10 +1251,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         const int s = it % S, ph = (it / S) & 1;
         const int tt = a.NT - 1 - it / KB, kb = it % KB;
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], 3 * kPlaneTile + 3 * btile);
+        mbar_arrive_expect_tx(&full[s], uint32_t(a.planes) * (kPlaneTile + btile));
         uint8_t* A = smem + s * stage_bytes;
         uint8_t* Bt = A + 3 * kPlaneTile;
-        for (int p = 0; p < 3; ++p) {
+        for (int p = 0; p < a.planes; ++p) {
           tma_load_2d(A + p * kPlaneTile, &tm_w, &full[s], kb * 64, p * a.H_pad + nt * 128);
           for (int h = 0; h < a.TT / 64; ++h)
             tma_load_2d(Bt + p * btile + h * 8192, &tm_di, &full[s],
@@ -1260,16 +1276,29 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bt = A + 3 * kPlaneTile;
         const uint32_t d = tmem + buf * a.TT;
-        // (pa, pb) plane products with pa + pb <= 2, smallest terms first
-        const int pa[6] = {2, 1, 0, 1, 0, 0};
-        const int pb[6] = {0, 1, 2, 0, 1, 0};
+        // (pa, pb) plane products with pa + pb <= planes - 1, smallest terms first:
+        // 6 for the fp32 path, 3 (hi.hi + hi.mid + mid.hi) for planes = 2, 1 for bf16
+        const int pa[10] = {2, 1, 0, 1, 0, 0, 1, 0, 0, 0};
+        const int pb[10] = {0, 1, 2, 0, 1, 0, 0, 1, 0, 0};
+        if (a.planes == 3) {  // the fp32 path, fully unrolled
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
+          for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            const uint64_t ad = sdesc_sw128(A + pa[q] * kPlaneTile + ks * 32, 16, 1024);
-            const uint64_t bd = sdesc_sw128(Bt + pb[q] * btile + ks * 2048, 8192, 1024);
-            umma_bf16(d, ad, bd, idesc, (kb | ks | q) != 0);
+            for (int q = 0; q < 6; ++q) {
+              const uint64_t ad = sdesc_sw128(A + pa[q] * kPlaneTile + ks * 32, 16, 1024);
+              const uint64_t bd = sdesc_sw128(Bt + pb[q] * btile + ks * 2048, 8192, 1024);
+              umma_bf16(d, ad, bd, idesc, (kb | ks | q) != 0);
+            }
+          }
+        } else {
+          const int q0 = a.planes == 2 ? 6 : 9, q1 = a.planes == 2 ? 9 : 10;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            for (int q = q0; q < q1; ++q) {
+              const uint64_t ad = sdesc_sw128(A + pa[q] * kPlaneTile + ks * 32, 16, 1024);
+              const uint64_t bd = sdesc_sw128(Bt + pb[q] * btile + ks * 2048, 8192, 1024);
+              umma_bf16(d, ad, bd, idesc, (kb | ks | (q - q0)) != 0);
+            }
           }
         }
         umma_commit(&empty[s]);
@@ -1412,7 +1441,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       cv = xG[last];
       ca = xG[kBwdScanThreads + last];
       if (stage_out && threadIdx.x == 0) {
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < a.planes; ++p)  // consumers read the first `planes` planes
           for (int h = 0; h < a.TT / 64; ++h)
             tma_store_2d(&tm_out, smem + (p * (a.TT / 64) + h) * 16384, b * a.T_pad + h * 64,
                          p * a.H_pad + nt * 128);
@@ -1588,7 +1617,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       asm volatile("bar.sync 1, %0;" ::"r"(kBwdScanThreads));
       Gcarry = xG[(kBwdSeg - 1) * 128 + q * 32 + lane];
       if (stage_out && threadIdx.x == 0) {
-        for (int p = 0; p < 3; ++p)
+        for (int p = 0; p < a.planes; ++p)  // consumers read the first `planes` planes
           for (int h = 0; h < a.TT / 64; ++h)
             tma_store_2d(&tm_out, smem + (p * (a.TT / 64) + h) * 16384, b * a.T_pad + h * 64,
                          p * a.H_pad + nt * 128);
@@ -3016,6 +3045,7 @@ struct WgradArgs {
   long long* dbg_clk;      // optional [blocks][kClkStride] phase timestamps
   const int32_t* xshift;   // kind 0: batch roll along the features (shift_augment)
   int B, T_pad, x_row_stride, in_features;
+  int planes;                // dI planes multiplied (3: fp32 path)
 };
 struct WgradMaps {
   CUtensorMap m[kMaxLayers];   // dI planes (B operand)
@@ -3342,9 +3372,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     xbytes, &xfull[s]);
         }
 #if SNN_WG_EXP == 2
-        constexpr int kLoadPlanes = 1;  // timing experiment only
+        const int kLoadPlanes = 1;  // timing experiment only
 #else
-        constexpr int kLoadPlanes = 3;
+        const int kLoadPlanes = args.planes;
 #endif
         mbar_arrive_expect_tx(&full[s], kLoadPlanes * ptile);
         uint8_t* Bp = smem + s * stage_bytes + a.mg * kPlaneTile;
@@ -3368,10 +3398,17 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         for (int ks = 0; ks < (SNN_WG_EXP == 3 ? 0 : 4); ++ks) {
           for (int m = 0; m < nm; ++m) {
             const uint64_t ad = sdesc_sw128(A + m * kPlaneTile + ks * 32, 16, 1024);
+            if (args.planes == 3) {
 #pragma unroll
-            for (int p = 2; p >= 0; --p) {
-              const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
-              umma_bf16(tmem + m * a.n_tile, ad, bd, idesc, (it | ks | (2 - p)) != 0);
+              for (int p = 2; p >= 0; --p) {
+                const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
+                umma_bf16(tmem + m * a.n_tile, ad, bd, idesc, (it | ks | (2 - p)) != 0);
+              }
+            } else {
+              for (int p = args.planes - 1; p >= 0; --p) {
+                const uint64_t bd = sdesc_sw128(Bp + p * ptile + ks * 32, 16, 1024);
+                umma_bf16(tmem + m * a.n_tile, ad, bd, idesc, (it | ks | (args.planes - 1 - p)) != 0);
+              }
             }
           }
         }

@@ -133,9 +133,11 @@ class TrainConfig:
     f_max: float = 1.0
     lambda_low: float = 0.0
     lambda_high: float = 0.0
+    gemm_planes: int = 3                 # engine option (not in the reference): 3 = fp32 path,
+                                         # 2 = fast bf16x2 planes, 1 = bf16 (snn_engine.h)
 
 
-ABI_VERSION = 6  # SNN_ABI_VERSION in include/snn_engine.h
+ABI_VERSION = 7  # SNN_ABI_VERSION in include/snn_engine.h
 
 
 class _NetDesc(C.Structure):
@@ -156,7 +158,7 @@ class _TrainCfg(C.Structure):
                 ("momentum", C.c_float), ("loss", C.c_int32), ("rate_hi", C.c_float),
                 ("rate_lo", C.c_float), ("max_shift", C.c_int32), ("n_shift_axes", C.c_int32),
                 ("shift_axes", C.c_int32 * 4), ("f_min", C.c_float), ("f_max", C.c_float),
-                ("lambda_low", C.c_float), ("lambda_high", C.c_float)]
+                ("lambda_low", C.c_float), ("lambda_high", C.c_float), ("gemm_planes", C.c_int32)]
 
 
 def normalize(spec: NetworkSpec) -> dict:
@@ -324,6 +326,7 @@ class Engine:
         c.max_shift, c.n_shift_axes = int(cfg.max_shift), len(axes)
         c.f_min, c.f_max = float(cfg.f_min), float(cfg.f_max)
         c.lambda_low, c.lambda_high = float(cfg.lambda_low), float(cfg.lambda_high)
+        c.gemm_planes = int(cfg.gemm_planes)
         for i, a in enumerate(axes):
             c.shift_axes[i] = a
         self._L = lib()

@@ -26,5 +26,7 @@ for l in (1, 0):
     print(f"bwd{l} [gemm, compose, chain, replay, combine, end] median", np.median(d, 0).astype(int).tolist())
 c = clk[0][:B]
 print("readout phases", np.median(np.diff(c[:, :8], axis=1), 0).astype(int).tolist())
+eng.debug(True)
+eng.train_step(rows)
 for l in range(2):
     print(f"layer {l} spike rate {eng.fetch('spikes', l).mean():.3f}")
