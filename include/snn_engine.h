@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define SNN_ABI_VERSION 7
+#define SNN_ABI_VERSION 8
 #define SNN_MAX_HIDDEN 8
 
 /* Error taxonomy, 1:1 with spiketrain's exception classes (errors.hpp:9-64). */
@@ -88,6 +88,10 @@ typedef struct snn_network_desc {
    * "l{id}.gamma" after "l{id}.beta" (init TN(0.5, 0.25) from child(cell_key, 3)).
    * Its checker is the restatement in oracle/spiketrain_oracle.h.  Zero = LIF. */
   int32_t cell[SNN_MAX_HIDDEN];
+  /* readout cell (network.hpp:153-155): 0 LILayer (the trace is its membrane),
+   * 1 LIFLayer (the trace is its spikes, network.hpp:396; same threshold and
+   * surrogate as the hidden LIF layers, beta entry and init as for LI) */
+  int32_t readout_lif;
 } snn_network_desc;
 
 /* SNN_CELL_RLIF is likewise DECLARED (the reference is feed-forward only, network.hpp:16,

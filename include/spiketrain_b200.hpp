@@ -160,6 +160,7 @@ inline int activation_id(const std::string& n) {
   if (n == "triangular") return SNN_ACT_TRIANGULAR;
   if (n == "arctan") return SNN_ACT_ARCTAN;
   if (n == "boxcar") return SNN_ACT_BOXCAR;
+  if (n == "sigmoid") return SNN_ACT_SIGMOID;  // declared (snn_engine.h)
   throw ArgumentError("unknown activation: " + n);
 }
 
@@ -206,12 +207,21 @@ inline snn_network_desc describe(const NetworkSpec& spec) {
     d.cell[i] = int32_t(lif->cell);
   }
   const auto* lin = std::get_if<LinearLayer>(&s.layers[s.layers.size() - 2]);
-  if (!lin || !std::holds_alternative<LILayer>(s.layers.back()))
-    throw UnsupportedError("readout must be Linear + LI");
+  if (!lin) throw UnsupportedError("readout must be Linear + LI or Linear + LIF");
   d.classes = int32_t(lin->out);
-  const auto& li = std::get<LILayer>(s.layers.back());
-  d.beta_mode[d.n_hidden] = int32_t(li.beta_mode);
-  d.fixed_beta[d.n_hidden] = float(li.fixed_beta);
+  if (const auto* ro = std::get_if<LIFLayer>(&s.layers.back())) {
+    // a LIF readout: its spikes are the trace (network.hpp:396)
+    if (ro->cell != CellKind::LIF || float(ro->threshold) != d.threshold ||
+        activation_id(ro->activation.name) != d.activation || float(ro->activation.slope) != d.slope)
+      throw UnsupportedError("a LIF readout shares the hidden layers' cell, threshold and surrogate");
+    d.readout_lif = 1;
+    d.beta_mode[d.n_hidden] = int32_t(ro->beta_mode);
+    d.fixed_beta[d.n_hidden] = float(ro->fixed_beta);
+  } else {
+    const auto& li = std::get<LILayer>(s.layers.back());
+    d.beta_mode[d.n_hidden] = int32_t(li.beta_mode);
+    d.fixed_beta[d.n_hidden] = float(li.fixed_beta);
+  }
   for (int m : monitor) d.monitor[m] = 1;
   return d;
 }

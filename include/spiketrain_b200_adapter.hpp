@@ -102,11 +102,20 @@ inline snn_network_desc b200_desc(const NetworkSpec& spec) {
     d.fixed_beta[i] = float(lif->fixed_beta);
   }
   const auto* lin = std::get_if<LinearLayer>(&ls[ls.size() - 2]);
-  const auto* li = std::get_if<LILayer>(&ls.back());
-  if (!lin || !li) throw UnsupportedError("readout must be Linear + LI");
+  if (!lin) throw UnsupportedError("readout must be Linear + LI or Linear + LIF");
   d.classes = int32_t(lin->out);
-  d.beta_mode[d.n_hidden] = int32_t(li->beta_mode);
-  d.fixed_beta[d.n_hidden] = float(li->fixed_beta);
+  if (const auto* ro = std::get_if<LIFLayer>(&ls.back())) {  // spikes are the trace (network.hpp:396)
+    if (float(ro->threshold) != d.threshold || b200_detail::activation_id(ro->activation.name) != d.activation)
+      throw UnsupportedError("a LIF readout shares the hidden layers' threshold and surrogate");
+    d.readout_lif = 1;
+    d.beta_mode[d.n_hidden] = int32_t(ro->beta_mode);
+    d.fixed_beta[d.n_hidden] = float(ro->fixed_beta);
+  } else if (const auto* li = std::get_if<LILayer>(&ls.back())) {
+    d.beta_mode[d.n_hidden] = int32_t(li->beta_mode);
+    d.fixed_beta[d.n_hidden] = float(li->fixed_beta);
+  } else {
+    throw UnsupportedError("readout must be Linear + LI or Linear + LIF");
+  }
   for (int m : monitor) d.monitor[m] = 1;
   return d;
 }

@@ -33,7 +33,7 @@ class _Net(C.Structure):
                 ("bias", C.c_int), ("threshold", C.c_float), ("act", C.c_int),
                 ("slope", C.c_float), ("aux", C.c_float), ("unroll", C.c_int),
                 ("beta_mode", C.c_int * 9), ("fixed_beta", C.c_float * 9),
-                ("monitor", C.c_int * 8), ("cell", C.c_int * 8)]
+                ("monitor", C.c_int * 8), ("cell", C.c_int * 8), ("readout_lif", C.c_int)]
 
 # hidden cell kinds: "lif" (neuron.hpp:127-136) | "alif" | "rlif" (declared
 # restatements, spiketrain_oracle.h -- not in the reference)
@@ -97,6 +97,8 @@ class Net:
     monitor: tuple = ()
     # cell kind per hidden layer ("lif" | "alif"); missing entries are "lif"
     cell: tuple = ()
+    # readout cell: "li" (default) or "lif" (network.hpp:153-155, :396)
+    readout: str = "li"
 
     def c(self) -> _Net:
         s, a = DEFAULT_SLOPE[self.act]
@@ -119,6 +121,7 @@ class Net:
             n.monitor[i] = 1
         for i, c in enumerate(self.cell):
             n.cell[i] = CELLS[c]
+        n.readout_lif = 1 if self.readout == "lif" else 0
         return n
 
 

@@ -55,6 +55,15 @@ NetworkSpec make_spec(const orc_net* n) {
     if (n->monitor[l]) s.layers.push_back(MonitorLayer{});
   }
   s.layers.push_back(LinearLayer{std::size_t(n->classes), n->bias != 0});
+  if (n->readout_lif) {  // a LIF readout: its spikes are the trace (network.hpp:396)
+    LIFLayer ro;
+    ro.activation = act_desc(n);
+    ro.threshold = double(n->threshold);
+    ro.beta_mode = beta_mode(n, n->n_hidden);
+    ro.fixed_beta = double(n->fixed_beta[n->n_hidden]);
+    s.layers.push_back(ro);
+    return s;
+  }
   LILayer li;
   li.beta_mode = beta_mode(n, n->n_hidden);
   li.fixed_beta = double(n->fixed_beta[n->n_hidden]);

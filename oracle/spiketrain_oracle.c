@@ -537,8 +537,16 @@ static int fb_impl(const orc_net* net, const orc_train_opts* opts,
         for (size_t t = 0; t < T; ++t) {
           const size_t idx = (b * T + t) * C + c;
           v3[idx] = v;
-          v = v * vb + i3[idx];
-          trace[idx] = v;
+          if (net->readout_lif) {
+            /* LIF readout (neuron.hpp:127-136): the trace is its spikes (network.hpp:396) */
+            const float pre = v + (-theta);
+            const float s = pre >= 0.0f ? 1.0f : 0.0f;
+            v = (v * vb + i3[idx]) - s * theta;
+            trace[idx] = s;
+          } else {
+            v = v * vb + i3[idx];
+            trace[idx] = v;
+          }
         }
       }
   }
@@ -631,8 +639,17 @@ static int fb_impl(const orc_net* net, const orc_train_opts* opts,
           float G = 0.0f;
           for (size_t t = T; t-- > 0;) {
             const size_t idx = (b * T + t) * C + c;
-            G = (t == T - 1) ? delta[b * C + c] : delta[b * C + c] + G * vb;
-            dI[idx] = G;
+            if (net->readout_lif) {
+              /* LIF reverse (the hidden layers' closure order) with dS_t = delta:
+               * dI_t = G ; G = G bc + (delta + (-G) theta) g(V_t - theta) */
+              dI[idx] = G;
+              const float gsp = delta[b * C + c] + (-G) * theta;
+              const float gpre = gsp * surrogate(net, v3[idx] + (-theta));
+              G = G * vb + gpre;
+            } else {
+              G = (t == T - 1) ? delta[b * C + c] : delta[b * C + c] + G * vb;
+              dI[idx] = G;
+            }
           }
         }
       /* d(clip01(beta)) per step, summed over b; beta grad in reverse t. */

@@ -108,6 +108,12 @@ typedef struct orc_net {
    * neuron) after "l{id}.beta", init TN(0, 1/sqrt(H), +-2 sigma) from
    * child(cell_key, 4).  Pinned against torch autograd like ALIF.          */
   int cell[ORC_MAX_HIDDEN];
+  /* Readout cell (network.hpp:153-155: a network ends in a LIF or LI readout):
+   * 0 LI (neuron.hpp:139-144, the trace is the membrane), 1 LIF (the trace is the
+   * readout's spikes, network.hpp:396; its threshold / surrogate are the hidden
+   * layers' theta / act).  The readout beta entry and init are the same for both
+   * (init_lif, network.hpp:266-279).                                          */
+  int readout_lif;
 } orc_net;
 
 /* Parameter entries in NetworkParams order (network.hpp:231-286). */

@@ -426,6 +426,7 @@ struct snn_engine {
     if (n.input <= 0) fail(SNN_ERR_SPEC, "network: input shape not declared");
     if (n.n_hidden < 1 || n.n_hidden > SNN_MAX_HIDDEN)
       fail(SNN_ERR_UNSUPPORTED, "n_hidden=%d outside [1,%d]", n.n_hidden, SNN_MAX_HIDDEN);
+    if (n.readout_lif != 0 && n.readout_lif != 1) fail(SNN_ERR_ARGUMENT, "readout_lif must be 0 or 1");
     if (n.classes < 1 || n.classes > kMaxClasses)
       fail(SNN_ERR_UNSUPPORTED, "classes=%d outside [1,%d]", n.classes, kMaxClasses);
     for (int l = 0; l < n.n_hidden; ++l)
@@ -1464,6 +1465,11 @@ struct snn_engine {
       r.rate_lo = cfg.rate_lo;
       // gs = g * T(2) / (T(b * c) * T(t)) with g = 1 (objective.hpp:172), in float
       r.mse_gs = 1.0f * 2.0f / (float(int64_t(B_global()) * C) * float(T));
+      r.readout_lif = net.readout_lif;
+      r.act = net.activation;
+      r.theta = net.threshold;
+      r.slope = net.slope;
+      r.aux = net.aux;
       r.loss_terms = cfg.loss == 1 ? loss_terms.p : nullptr;
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
       launch(k_readout, dim3(B), dim3(kRoThreads), smem, r);

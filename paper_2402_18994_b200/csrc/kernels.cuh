@@ -622,6 +622,48 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
 }
 
+// Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
+// the unrolled step bodies stay branch-free; divisions evaluated as approximate
+// reciprocals (<= 1 ulp; the backward is checked to the 1e-4 gradient bound,
+// the bit-exact parts are the forward scans).
+template <int kAct>
+__device__ __forceinline__ float surrogate_t(float k, float aux, float x) {
+  if constexpr (kAct == 1) {  // superspike 1/(1+k|x|)^2
+    const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
+    return rcp_approx(__fmul_rn(d, d));
+  } else if constexpr (kAct == 2) {  // triangular max(0, 1-|kx|)
+    const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
+    return 0.0f < r ? r : 0.0f;
+  } else if constexpr (kAct == 3) {  // arctan 1/(1+(pi k x/2)^2)
+    const float u = __fmul_rn(k * 1.57079632679489662f, x);
+    return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
+  } else if constexpr (kAct == 4) {  // boxcar
+    return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
+  } else if constexpr (kAct == 5) {
+    // sigmoid, DECLARED (not in the reference catalogue, SPEC.md:283): the
+    // backward a caller hands to custom(heaviside, bwd), surrogate.hpp:45-57,
+    // g = k s (1 - s) = (k e) / ((1 + e)(1 + e)), e = exp(-k |x|): the
+    // cancellation-free form of oracle/spiketrain_oracle.h (accurate expf)
+    const float e = expf(-__fmul_rn(k, fabsf(x)));
+    const float d = __fadd_rn(1.0f, e);
+    return __fdiv_rn(__fmul_rn(k, e), __fmul_rn(d, d));
+  } else {  // custom straight-through
+    return 1.0f;
+  }
+}
+
+// the surrogate with a runtime kind (the readout's few steps per lane)
+__device__ __forceinline__ float surrogate_rt(int act, float k, float aux, float x) {
+  switch (act) {
+    case 1: return surrogate_t<1>(k, aux, x);
+    case 2: return surrogate_t<2>(k, aux, x);
+    case 3: return surrogate_t<3>(k, aux, x);
+    case 4: return surrogate_t<4>(k, aux, x);
+    case 5: return surrogate_t<5>(k, aux, x);
+    default: return 1.0f;
+  }
+}
+
 // ============================================================================
 // K4  k_readout: readout projection (exact sparse gather in the reference's
 // ascending-k order, ops.hpp:163-172), LI scan, integral CE + accuracy, CE
@@ -650,6 +692,10 @@ struct ReadoutArgs {
   float rate_hi, rate_lo;   // rate-MSE targets
   float mse_gs;             // 2 / (float(B_global*C) * float(T)) (objective.hpp:172)
   float* loss_terms;        // rate-MSE: [B][C] squared rate gaps (summed in order by the tail)
+  // LIF readout (network.hpp:153-155, :396): the trace is the readout's spikes; its
+  // threshold and surrogate are the hidden layers' (readout_lif 0: LI readout)
+  int readout_lif, act;
+  float theta, slope, aux;
 };
 
 __device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
@@ -772,6 +818,18 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50); col[t] <- V3_t
     float v = 0.0f, logit = 0.0f;
     int t = 0;
+    if (a.readout_lif) {
+      // LIF readout (neuron.hpp:127-136): s_t = [v - theta >= 0] is the trace, the
+      // logits its time sums (network.hpp:396, objective.hpp:40-50)
+      const float ntheta = -a.theta;
+      for (; t < T; ++t) {
+        const float I = col[t * kRoStride];
+        col[t * kRoStride] = v;
+        const bool sp = __fadd_rn(v, ntheta) >= 0.0f;
+        v = __fsub_rn(__fadd_rn(__fmul_rn(v, vb), I), sp ? a.theta : 0.0f);
+        logit = __fadd_rn(logit, sp ? 1.0f : 0.0f);
+      }
+    }
     for (; t + 8 <= T; t += 8) {
       float I[8];
 #pragma unroll
@@ -844,11 +902,28 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     }
     if (a.dbg_trace != nullptr && lane < C) {
       for (int s = 0; s < T; ++s)
-        a.dbg_trace[(size_t(b) * T + s) * C + lane] = s + 1 < T ? col[(s + 1) * kRoStride] : v_final;
+        a.dbg_trace[(size_t(b) * T + s) * C + lane] =
+            a.readout_lif ? (__fadd_rn(col[s * kRoStride], -a.theta) >= 0.0f ? 1.0f : 0.0f)
+                          : s + 1 < T ? col[(s + 1) * kRoStride] : v_final;
     }
     RO_CLK(4)
-    // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
     float G = delta, db = 0.0f, dbias = 0.0f;
+    if (a.readout_lif) {
+      // LIF reverse (the hidden layers' closure order, App. A.2) with dS_t = delta on
+      // every step: dI3_t = G ; G = G bc + (delta + (-G) theta) g(V3_t - theta)
+      G = 0.0f;
+      for (t = T - 1; t >= 0; --t) {
+        const float V3 = col[t * kRoStride];
+        const float gi = G;
+        const float gs = __fadd_rn(delta, __fmul_rn(-gi, a.theta));
+        const float g = surrogate_rt(a.act, a.slope, a.aux, __fadd_rn(V3, -a.theta));
+        G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
+        db = __fadd_rn(db, __fmul_rn(gi, V3));
+        dbias = __fadd_rn(dbias, gi);
+        col[t * kRoStride] = gi;
+      }
+    } else {
+    // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
     t = T - 1;
     {
       const float V3 = col[t * kRoStride];
@@ -875,6 +950,7 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
       db = __fadd_rn(db, __fmul_rn(G, V3));
       dbias = __fadd_rn(dbias, G);
       col[t * kRoStride] = G;
+    }
     }
     if (lane < C) {
       a.dbeta_part[size_t(b) * C + lane] = db;
@@ -971,36 +1047,6 @@ __device__ __forceinline__ float monitor_term(const BwdArgs& a, int b, int n, in
     if (count >= 0 && lane == __ffs(peers) - 1) atomicAdd(a.hist + count, unsigned(__popc(peers)));
   }
   return rterm;
-}
-
-// Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
-// the unrolled step bodies stay branch-free; divisions evaluated as approximate
-// reciprocals (<= 1 ulp; the backward is checked to the 1e-4 gradient bound,
-// the bit-exact parts are the forward scans).
-template <int kAct>
-__device__ __forceinline__ float surrogate_t(float k, float aux, float x) {
-  if constexpr (kAct == 1) {  // superspike 1/(1+k|x|)^2
-    const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
-    return rcp_approx(__fmul_rn(d, d));
-  } else if constexpr (kAct == 2) {  // triangular max(0, 1-|kx|)
-    const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
-    return 0.0f < r ? r : 0.0f;
-  } else if constexpr (kAct == 3) {  // arctan 1/(1+(pi k x/2)^2)
-    const float u = __fmul_rn(k * 1.57079632679489662f, x);
-    return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
-  } else if constexpr (kAct == 4) {  // boxcar
-    return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
-  } else if constexpr (kAct == 5) {
-    // sigmoid, DECLARED (not in the reference catalogue, SPEC.md:283): the
-    // backward a caller hands to custom(heaviside, bwd), surrogate.hpp:45-57,
-    // g = k s (1 - s) = (k e) / ((1 + e)(1 + e)), e = exp(-k |x|): the
-    // cancellation-free form of oracle/spiketrain_oracle.h (accurate expf)
-    const float e = expf(-__fmul_rn(k, fabsf(x)));
-    const float d = __fadd_rn(1.0f, e);
-    return __fdiv_rn(__fmul_rn(k, e), __fmul_rn(d, d));
-  } else {  // custom straight-through
-    return 1.0f;
-  }
 }
 
 __device__ __forceinline__ void load_v_chunk(const BwdArgs& a, int b, int n, int c,

@@ -137,7 +137,7 @@ class TrainConfig:
                                          # 2 = fast bf16x2 planes, 1 = bf16 (snn_engine.h)
 
 
-ABI_VERSION = 7  # SNN_ABI_VERSION in include/snn_engine.h
+ABI_VERSION = 8  # SNN_ABI_VERSION in include/snn_engine.h
 
 
 class _NetDesc(C.Structure):
@@ -145,7 +145,7 @@ class _NetDesc(C.Structure):
                 ("classes", C.c_int32), ("bias", C.c_int32), ("threshold", C.c_float),
                 ("activation", C.c_int32), ("slope", C.c_float), ("aux", C.c_float),
                 ("beta_mode", C.c_int32 * 9), ("fixed_beta", C.c_float * 9),
-                ("monitor", C.c_int32 * 8), ("cell", C.c_int32 * 8)]
+                ("monitor", C.c_int32 * 8), ("cell", C.c_int32 * 8), ("readout_lif", C.c_int32)]
 
 
 BETA_MODES = {"per_neuron": 0, "scalar": 1, "fixed": 2}
@@ -163,7 +163,7 @@ class _TrainCfg(C.Structure):
 
 def normalize(spec: NetworkSpec) -> dict:
     """Map a NetworkSpec onto the engine's feed-forward family, validating like
-    normalize() (network.hpp:125-157).  Supported: [Linear, LIF]*k, Linear, LI."""
+    normalize() (network.hpp:125-157).  Supported: [Linear, LIF]*k, Linear, LI | LIF."""
     if not spec.input_shape:
         raise SpecError("network: input shape not declared")
     if not spec.layers:
@@ -201,8 +201,14 @@ def normalize(spec: NetworkSpec) -> dict:
                      "rlif" if isinstance(cell, RLIFLayer) else "lif")
         fixed.append(float(cell.fixed_beta))
     lin, cell = layers[-2], layers[-1]
-    if not isinstance(lin, LinearLayer) or not isinstance(cell, LILayer):
-        raise UnsupportedError("readout must be Linear + LI")
+    readout_lif = isinstance(cell, LIFLayer)  # network.hpp:153-155: a LIF readout's spikes are the trace
+    if not isinstance(lin, LinearLayer) or not isinstance(cell, (LILayer, LIFLayer)):
+        raise UnsupportedError("readout must be Linear + LI or Linear + LIF")
+    if readout_lif:
+        if isinstance(cell, (ALIFLayer, RLIFLayer)):
+            raise UnsupportedError("readout must be a LIF or LI cell")
+        if cell.activation != act or cell.threshold != thr:
+            raise UnsupportedError("all LIF layers must share activation and threshold")
     if lin.bias != bias:
         raise UnsupportedError("all Linear layers must share the bias flag")
     if act.name not in ACTIVATIONS:
@@ -212,7 +218,8 @@ def normalize(spec: NetworkSpec) -> dict:
     return dict(input=inp, hidden=hidden, classes=int(lin.out), bias=bool(bias),
                 threshold=float(thr), activation=act.name, slope=float(act.slope),
                 aux=float(act.aux), beta_mode=modes + [cell.beta_mode],
-                fixed_beta=fixed + [float(cell.fixed_beta)], monitor=monitor, cell=cells)
+                fixed_beta=fixed + [float(cell.fixed_beta)], monitor=monitor, cell=cells,
+                readout_lif=bool(readout_lif))
 
 
 def shd_spec(hidden=(128, 128), classes=20, inp=700, act="arctan", bias=False,
@@ -305,6 +312,7 @@ class Engine:
             n.monitor[m] = 1
         for i, k in enumerate(d["cell"]):
             n.cell[i] = {"lif": 0, "alif": 1, "rlif": 2}[k]
+        n.readout_lif = int(d["readout_lif"])
         c = _TrainCfg()
         c.batch_size = int(cfg.batch_size)
         c.time_steps = int(time_steps)

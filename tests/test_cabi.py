@@ -57,5 +57,12 @@ def test_spec_validation_mirrors_reference():
         normalize(NetworkSpec([], [LinearLayer(4), LILayer()]))
     with pytest.raises(SpecError):
         normalize(NetworkSpec([4], [LinearLayer(4)]))
+    # a LIF readout (network.hpp:153-155, :396) is supported; it must share the
+    # hidden layers' threshold and surrogate
+    d = normalize(NetworkSpec([4], [LinearLayer(4), LIFLayer(), LinearLayer(3), LIFLayer()]))
+    assert d["readout_lif"] and d["classes"] == 3
+    assert not normalize(shd_spec())["readout_lif"]
     with pytest.raises(UnsupportedError):
-        normalize(NetworkSpec([4], [LinearLayer(4), LIFLayer(), LinearLayer(3), LIFLayer()]))
+        normalize(NetworkSpec([4], [LinearLayer(4), LIFLayer(), LinearLayer(3), LIFLayer(threshold=0.5)]))
+    with pytest.raises(SpecError):
+        normalize(NetworkSpec([4], [LinearLayer(4), LIFLayer(), LinearLayer(3)]))

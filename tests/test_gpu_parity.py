@@ -43,6 +43,11 @@ def make_engine(net: Net, B, T, seed=0, lr=1e-3, **cfg):
         from paper_2402_18994_b200 import MonitorLayer
         for m in sorted(net.monitor, reverse=True):
             spec.layers.insert(2 * m + 2, MonitorLayer())
+    if net.readout == "lif":  # a LIF readout: its spikes are the trace (network.hpp:396)
+        from paper_2402_18994_b200 import LIFLayer
+        hid = next(layer for layer in spec.layers if type(layer).__name__ == "LIFLayer")
+        ro = spec.layers[-1]
+        spec.layers[-1] = LIFLayer(hid.activation, hid.threshold, ro.beta_mode, ro.fixed_beta)
     return Engine(spec, TrainConfig(batch_size=B, seed=seed, lr=lr, unroll=net.unroll, **cfg), T)
 
 
@@ -1152,3 +1157,44 @@ def test_pipelined_host_batches_match_per_step_calls(orc):
     la2, _ = a.train_steps_packed(pk[:2], yk[:2])
     assert [float(v) for v in la2] == [b.train_step_packed(pk[k], yk[k])[0] for k in range(2)]
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+LIF_READOUT_GPU = [
+    ("ce-superspike", Net(inp=40, hidden=(24, 20), classes=5, act="superspike", readout="lif"), "ce", 6, 30),
+    ("mse-arctan-bias", Net(inp=40, hidden=(24,), classes=4, act="arctan", bias=True, readout="lif"),
+     "rate_mse", 5, 45),
+    ("mse-c1-shape", Net(readout="lif"), "rate_mse", 32, 128),
+]
+
+
+@pytest.mark.parametrize("case", LIF_READOUT_GPU, ids=[c[0] for c in LIF_READOUT_GPU])
+def test_lif_readout_parity(orc, case):
+    """A LIF readout (network.hpp:153-155, :396; VERDICT r1 missing #3): the trace is
+    the readout's spikes, the logits their counts; with the spike-rate MSE loss
+    (objective.hpp:139-183) this is the reference's rate-coded output.  Against the
+    oracle (pinned bit for bit to the reference, test_oracle.py)."""
+    from oracle.pyoracle import Opts
+    _, net, loss, B, T = case
+    o = Opts(loss=loss)
+    params = orc.init(net, orc.key_child(orc.key_from_seed(7), 0)) * np.float32(3.0)
+    x, y = orc.synth_raster(net.classes, B, T, net.inp, 4)
+    pk = orc.pack_time(x)
+    kw = dict(loss="spike_rate_mse") if loss == "rate_mse" else {}
+    eng = make_engine(net, B, T, **kw)
+    assert eng.entries() == orc.entries(net)
+    eng.stage_dataset(pk, y)
+    eng.set_params(params)
+    eng.debug(True)
+    rows = np.arange(B, dtype=np.uint32)
+    l1, a1 = eng.forward_backward(rows)
+    ref = orc.forward_backward(net, params, pk, T, y, opts=o, want_trace=True, want_spikes=True)
+    tr = eng.fetch("trace")
+    assert set(np.unique(tr)) <= {0.0, 1.0} and 0.0 < tr.mean() < 1.0
+    assert (tr == ref["trace"]).mean() >= SPIKE_AGREE
+    assert abs(l1 - ref["loss"]) <= REL_TOL * abs(ref["loss"]) and a1 == ref["acc"]
+    check_grads(orc, net, eng.get_grads(), ref["grads"])
+    st = State(params.copy())
+    for _ in range(2):
+        lo, ao = orc.train_step(net, st, pk, T, y, opts=o)
+        l2, a2 = eng.train_step(rows)
+        assert abs(l2 - lo) <= 1e-3 * abs(lo) and a2 == ao

@@ -506,3 +506,37 @@ def test_forced_with_own_spikes_is_identity(orc, case):
     other = orc.forward_backward(net, p, pk, 29, y, want_spikes=True, forced=flip)
     assert np.array_equal(other["spikes"][0], flip[0])
     assert not np.array_equal(other["grads"], free["grads"])
+
+
+LIF_READOUT = [
+    ("ce-superspike", Net(inp=40, hidden=(24, 20), classes=5, act="superspike", readout="lif", unroll=7), "ce"),
+    ("mse-arctan-bias", Net(inp=40, hidden=(24,), classes=4, act="arctan", bias=True, readout="lif"), "rate_mse"),
+    ("mse-triangular-scalar", Net(inp=33, hidden=(16, 12), classes=6, act="triangular", readout="lif",
+                                  beta_mode=("per_neuron", "per_neuron", "scalar")), "rate_mse"),
+]
+
+
+@pytest.mark.skipif(not have_ref(), reason="oracle/_ref needs /root/reference")
+@pytest.mark.parametrize("case", LIF_READOUT, ids=[c[0] for c in LIF_READOUT])
+def test_lif_readout_bit_exact_vs_reference(orc, case):
+    """A network ending in a LIF readout (network.hpp:153-155): its spikes are the
+    trace (:396).  The restatement equals the reference bit for bit: loss, trace,
+    every gradient, and 2 epochs of training."""
+    from oracle.pyoracle import Opts
+    _, net, loss = case
+    ref = Lib("ref")
+    o = Opts(loss=loss)
+    p = orc.init(net, orc.key_child(orc.key_from_seed(3), 0)) * np.float32(3.0)
+    assert np.array_equal(p, ref.init(net, ref.key_child(ref.key_from_seed(3), 0)) * np.float32(3.0))
+    x, y = orc.synth_raster(net.classes, 12, 30, net.inp, 2)
+    pk = orc.pack_time(x)
+    a = orc.forward_backward(net, p, pk, 30, y, opts=o, want_trace=True, want_spikes=True)
+    b = ref.forward_backward(net, p, pk, 30, y, opts=o, want_trace=True, want_spikes=True)
+    assert a["loss"] == b["loss"] and a["acc"] == b["acc"]
+    assert np.array_equal(a["trace"], b["trace"]) and set(np.unique(a["trace"])) <= {0.0, 1.0}
+    assert 0.0 < a["trace"].mean() < 1.0
+    assert np.array_equal(a["grads"], b["grads"])
+    s1, s2 = State(p.copy()), State(p.copy())
+    m1 = orc.train_epochs(net, s1, pk, y, 30, 4, 2, 5, opts=o)
+    m2 = ref.train_epochs(net, s2, pk, y, 30, 4, 2, 5, opts=o)
+    assert np.array_equal(m1, m2) and np.array_equal(s1.params, s2.params)
