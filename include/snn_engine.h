@@ -320,6 +320,11 @@ snn_status snn_train_step_split(snn_engine* e, const uint32_t* rows, int32_t par
  *         7: dI of Linear `layer` (0..L, L = readout; hi + (mid + lo) of
  *            its three bf16 planes)                 [B][T][H or C]  */
 snn_status snn_debug_enable(snn_engine* e, int32_t on);
+/* With SNN_GUARD=1 in the environment when buffers are allocated, every device
+ * buffer of the process carries 4 KB of a known byte pattern past its end;
+ * this checks them all (SNN_ERR_CONTRACT names the first overwritten one) and
+ * returns how many buffers were checked (0 when guards are off). */
+snn_status snn_debug_check_guards(snn_engine* e, int32_t* checked);
 snn_status snn_debug_fetch(snn_engine* e, int32_t which, int32_t layer, void* host, size_t bytes);
 
 #ifdef __cplusplus

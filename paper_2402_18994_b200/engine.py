@@ -662,6 +662,13 @@ class Engine:
         """True / 1: capture tensors + clock stamps; 2: clock stamps only."""
         self._check(self._L.snn_debug_enable(self._h, 2 if on == 2 else int(bool(on))))
 
+    def check_guards(self) -> int:
+        """SNN_GUARD=1: verify the out-of-bounds guard bytes of every device buffer
+        (raises ContractError on an overwrite); returns the number checked."""
+        n = C.c_int32()
+        self._check(self._L.snn_debug_check_guards(self._h, C.byref(n)))
+        return n.value
+
     def fetch(self, which: str, layer: int = 0) -> np.ndarray:
         idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5, "A": 6, "dI": 7}[which]
         B, T = self.batch_size, self.time_steps
