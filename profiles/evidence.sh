@@ -1,15 +1,21 @@
-# Round-end evidence run on one B200 (gpurun): GPU tests, smoke, bench lines (C1 headline, C2, C4),
-# the reference arm, the ncu launch list and full captures of one training step (summarised on
-# the box; only the C1 report is kept so gpurun_out stays under the 64 MiB copy-back limit).
-#   gpurun --timeout 2400 -- 'bash profiles/evidence.sh r01g'
+# Round evidence on one B200 (gpurun): GPU tests, smoke, bench lines (C1 headline + fast
+# modes, C2, C3 at global batch 4096, C4, C5), the reference arm, the ncu launch list of the
+# C1 bench and full captures of one step (C1, C2, C4), summarised on the box; only the C1
+# report is kept so gpurun_out stays under the copy-back limit.
+#   gpurun --timeout 3000 -- 'bash profiles/evidence.sh r02a'
 mkdir -p gpurun_out
-TAG=${1:-r01g}
+TAG=${1:-r02}
 set -x
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 python bench.py > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
+python bench.py --gemm-planes 2 --no-cpu-baseline > gpurun_out/bench_c1_bf16x2.json 2> gpurun_out/bench_c1_bf16x2.err
+python bench.py --gemm-planes 1 --no-cpu-baseline > gpurun_out/bench_c1_bf16.json 2> gpurun_out/bench_c1_bf16.err
 python bench.py --config c2 --steps 1000 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
-python bench.py --config c4 --steps 100 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+python bench.py --config c3 --steps 20 --warmup 3 --e2e-steps 4 --profile-steps 2 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+python bench.py --config c3 --steps 20 --warmup 3 --e2e-steps 4 --profile-steps 2 --gemm-planes 2 --no-cpu-baseline > gpurun_out/bench_c3_bf16x2.json 2> gpurun_out/bench_c3_bf16x2.err
+python bench.py --config c4 --steps 100 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+python bench.py --config c5 --steps 100 --e2e-steps 20 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/ref_c1.json 2> gpurun_out/ref_c1.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c1.csv python bench.py --steps 2 --warmup 3 --e2e-steps 2 --profile-steps 2 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -c 8 -o gpurun_out/step_c1 python tests/prof_step.py --warmup 3 --steps 1 > gpurun_out/ncu_full.log 2>&1
