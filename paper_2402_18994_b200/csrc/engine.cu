@@ -1409,6 +1409,40 @@ struct snn_engine {
     const uint32_t* rows_p = sched_mode ? sched.p : rows_cur.p;
     const int64_t* slot_p = sched_mode ? sched_slot.p : nullptr;
     if (evs) CK(cudaEventRecordWithFlags((*evs)[0], stream, cudaEventRecordExternal));
+    // readout arguments (K4)
+    ReadoutArgs ro_args{};
+    {
+      ReadoutArgs& r = ro_args;
+      r.s_in = s_np[L - 1].p;
+      r.rows = rows_p;
+      r.rows_slot = slot_p;
+      r.labels = ds.labels.p;
+      r.w = params.p + entry_of(kEntryW, L).offset;
+      r.bias = net.bias ? params.p + entry_of(kEntryB, L).offset : nullptr;
+      r.beta = params.p + entry_of(kEntryBeta, L).offset;
+    r.beta_stride = net.beta_mode[L] == 0 ? 1 : 0;
+      r.d3_planes = di[L].p;
+      r.loss_b = loss_b.p;
+      r.correct_b = correct_b.p;
+      r.dbeta_part = dbeta[L].p;
+      r.dbias_part = net.bias ? dbias[L].p : nullptr;
+      r.dbg_trace = update == kEvalTrace ? eval_trace.p : (debug ? dbg_trace.p : nullptr);
+      r.dbg_clk = clocks ? dbg_clk.p : nullptr;
+      r.exp_mode = exp_mode;
+      r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
+      r.inv_b = 1.0f / float(B_global());
+      r.loss_kind = cfg.loss;
+      r.rate_hi = cfg.rate_hi;
+      r.rate_lo = cfg.rate_lo;
+      // gs = g * T(2) / (T(b * c) * T(t)) with g = 1 (objective.hpp:172), in float
+      r.mse_gs = 1.0f * 2.0f / (float(int64_t(B_global()) * C) * float(T));
+      r.readout_lif = net.readout_lif;
+      r.act = net.activation;
+      r.theta = net.threshold;
+      r.slope = net.slope;
+      r.aux = net.aux;
+      r.loss_terms = cfg.loss == 1 ? loss_terms.p : nullptr;
+    }
     // forward: one launch per group of consecutive hidden layers (fwd_groups)
     for (const auto& grp : fwd_groups()) {
       const int l = grp.first, nl = grp.second;
@@ -1477,36 +1511,7 @@ struct snn_engine {
     }
     // readout + loss + LI backward
     {
-      ReadoutArgs r{};
-      r.s_in = s_np[L - 1].p;
-      r.rows = rows_p;
-      r.rows_slot = slot_p;
-      r.labels = ds.labels.p;
-      r.w = params.p + entry_of(kEntryW, L).offset;
-      r.bias = net.bias ? params.p + entry_of(kEntryB, L).offset : nullptr;
-      r.beta = params.p + entry_of(kEntryBeta, L).offset;
-    r.beta_stride = net.beta_mode[L] == 0 ? 1 : 0;
-      r.d3_planes = di[L].p;
-      r.loss_b = loss_b.p;
-      r.correct_b = correct_b.p;
-      r.dbeta_part = dbeta[L].p;
-      r.dbias_part = net.bias ? dbias[L].p : nullptr;
-      r.dbg_trace = update == kEvalTrace ? eval_trace.p : (debug ? dbg_trace.p : nullptr);
-      r.dbg_clk = clocks ? dbg_clk.p : nullptr;
-      r.exp_mode = exp_mode;
-      r.B = B; r.T = T; r.T_pad = T_pad; r.HL = H[L - 1]; r.HL_pad = H_pad[L - 1]; r.C = C;
-      r.inv_b = 1.0f / float(B_global());
-      r.loss_kind = cfg.loss;
-      r.rate_hi = cfg.rate_hi;
-      r.rate_lo = cfg.rate_lo;
-      // gs = g * T(2) / (T(b * c) * T(t)) with g = 1 (objective.hpp:172), in float
-      r.mse_gs = 1.0f * 2.0f / (float(int64_t(B_global()) * C) * float(T));
-      r.readout_lif = net.readout_lif;
-      r.act = net.activation;
-      r.theta = net.threshold;
-      r.slope = net.slope;
-      r.aux = net.aux;
-      r.loss_terms = cfg.loss == 1 ? loss_terms.p : nullptr;
+      const ReadoutArgs r = ro_args;
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
       launch(k_readout, dim3(B), dim3(kRoThreads), smem, r);
       mark(evs, "readout", -1);

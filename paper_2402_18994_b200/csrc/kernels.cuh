@@ -134,6 +134,395 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
+// Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
+// the unrolled step bodies stay branch-free; divisions evaluated as approximate
+// reciprocals (<= 1 ulp; the backward is checked to the 1e-4 gradient bound,
+// the bit-exact parts are the forward scans).
+template <int kAct>
+__device__ __forceinline__ float surrogate_t(float k, float aux, float x) {
+  if constexpr (kAct == 1) {  // superspike 1/(1+k|x|)^2
+    const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
+    return rcp_approx(__fmul_rn(d, d));
+  } else if constexpr (kAct == 2) {  // triangular max(0, 1-|kx|)
+    const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
+    return 0.0f < r ? r : 0.0f;
+  } else if constexpr (kAct == 3) {  // arctan 1/(1+(pi k x/2)^2)
+    const float u = __fmul_rn(k * 1.57079632679489662f, x);
+    return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
+  } else if constexpr (kAct == 4) {  // boxcar
+    return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
+  } else if constexpr (kAct == 5) {
+    // sigmoid, DECLARED (not in the reference catalogue, SPEC.md:283): the
+    // backward a caller hands to custom(heaviside, bwd), surrogate.hpp:45-57,
+    // g = k s (1 - s) = (k e) / ((1 + e)(1 + e)), e = exp(-k |x|): the
+    // cancellation-free form of oracle/spiketrain_oracle.h (accurate expf)
+    const float e = expf(-__fmul_rn(k, fabsf(x)));
+    const float d = __fadd_rn(1.0f, e);
+    return __fdiv_rn(__fmul_rn(k, e), __fmul_rn(d, d));
+  } else {  // custom straight-through
+    return 1.0f;
+  }
+}
+
+// the surrogate with a runtime kind (the readout's few steps per lane)
+__device__ __forceinline__ float surrogate_rt(int act, float k, float aux, float x) {
+  switch (act) {
+    case 1: return surrogate_t<1>(k, aux, x);
+    case 2: return surrogate_t<2>(k, aux, x);
+    case 3: return surrogate_t<3>(k, aux, x);
+    case 4: return surrogate_t<4>(k, aux, x);
+    case 5: return surrogate_t<5>(k, aux, x);
+    default: return 1.0f;
+  }
+}
+
+// ============================================================================
+// K4  k_readout: readout projection (exact sparse gather in the reference's
+// ascending-k order, ops.hpp:163-172), LI scan, integral CE + accuracy, CE
+// backward and the closed-form LI reverse scan (App. A.3).  grid B, block 128.
+// ============================================================================
+struct ReadoutArgs {
+  const uint32_t* s_in;     // neuron-packed spikes of the last hidden layer
+  const uint32_t* rows;     // [B]
+  const int64_t* rows_slot; // schedule mode: rows += *rows_slot * B (else nullptr)
+  const int32_t* labels;    // dataset labels [N]
+  const float* w;           // readout W [HL][C] f32 (master)
+  const float* bias;        // [C] or nullptr
+  const float* beta;        // [C] (or one value: beta_stride 0)
+  int beta_stride;
+  __nv_bfloat16* d3_planes; // [3][64][B*T_pad] (class rows, (b,t) contiguous)
+  float* loss_b;            // [B] lse - logit_y
+  int32_t* correct_b;       // [B]
+  float* dbeta_part;        // [B][C]
+  float* dbias_part;        // [B][C] or nullptr
+  float* dbg_trace;         // optional [B][T][C]
+  long long* dbg_clk;       // optional [B][8] phase timestamps (clock64)
+  int exp_mode;             // 0: exp/log evaluated in fp64 then rounded; 1: expf/logf
+  int B, T, T_pad, HL, HL_pad, C;
+  float inv_b;              // 1/B_global (objective.hpp:104)
+  int loss_kind;            // 0 integral CE, 1 spike-rate MSE (objective.hpp:139-183)
+  float rate_hi, rate_lo;   // rate-MSE targets
+  float mse_gs;             // 2 / (float(B_global*C) * float(T)) (objective.hpp:172)
+  float* loss_terms;        // rate-MSE: [B][C] squared rate gaps (summed in order by the tail)
+  // LIF readout (network.hpp:153-155, :396): the trace is the readout's spikes; its
+  // threshold and surrogate are the hidden layers' (readout_lif 0: LI readout)
+  int readout_lif, act;
+  float theta, slope, aux;
+};
+
+__device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
+__device__ __forceinline__ float log_cr(float x) { return float(log(double(x))); }
+
+// readout scratch: W [HL][C] | spike words [T][HL_pad/32] | per-(t, class) column
+// buffer [T][33] (one column per lane; stride 33 keeps both the per-step rows
+// written by the projection and the per-class columns read by the scans free
+// of bank conflicts)
+constexpr int kRoStride = 33;
+constexpr int kRoThreads = 256;  // projection: 2 lanes per time step (class groups split)
+__host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
+  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4 + 16;
+}
+
+// The readout of sample b by a group of G threads (gt = index in the group, G a
+// multiple of 64, named barrier `bar`); k_readout runs one group per CTA.  rsm:
+// readout_smem_bytes of scratch; w_ready: W is already staged in rsm (the kernel
+// loads it before its dependency wait).  (Running this in the tail of the fused
+// forward launch, one group per sample, was measured slower: the forward's
+// 448-thread register budget slows every phase 1.2-8x.)
+__device__ __forceinline__ void readout_sample(const ReadoutArgs& a, int b, float* rsm, int gt, int G,
+                                               int bar, bool w_ready) {
+  const int C = a.C, T = a.T;
+  const int hw = a.HL_pad / 32;
+  const int Cp = (C + 3) & ~3;
+  float* w = rsm;                                                      // [HL][Cp]
+  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * Cp);  // [T][hw]
+  float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
+  const int tid = gt, warp = gt >> 5, lane = gt & 31;
+  auto sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory"); };
+#define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
+  if (!w_ready) {
+    const int nw = a.HL * C;
+    if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
+      const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
+      for (int i = tid; i < nw / 4; i += G) reinterpret_cast<float4*>(w)[i] = __ldg(src + i);
+    } else {
+      for (int i = tid; i < a.HL * Cp; i += G) {
+        const int k = i / Cp, c = i % Cp;
+        w[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
+      }
+    }
+  }
+  const float beta_l = lane < C ? a.beta[lane * a.beta_stride] : 0.0f;
+  RO_CLK(0)
+  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
+  int* s_label = reinterpret_cast<int*>(buf + size_t(T) * kRoStride);
+  if (tid == 0) *s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
+  {
+    // the spike words of this sample (written by the forward: plain loads, not the
+    // non-coherent __ldg path, since the fused forward reads words it just stored)
+    const uint4* ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
+    for (int i = tid; i < T * hw / 4; i += G) reinterpret_cast<uint4*>(spk)[i] = ss[i];
+  }
+  sync();
+  RO_CLK(1)
+  // projection (ops.hpp:163-172 order: ascending k, zero skip): a lane pair per
+  // time step, lane h of the pair owning the 4-class groups j = 2jj + h (acc in
+  // registers; the pair walks the same spike bits).  W rows live in smem padded to
+  // Cp = C rounded up to 4 floats; the row of the next spike is loaded while the
+  // current one is added, so a burst of spikes costs the add chain, not one smem
+  // round trip per spike.
+  constexpr int kGroups = kMaxClasses / 8;  // 4-class groups per lane
+  const int h = tid & 1;
+  for (int t = tid >> 1; t < T; t += G / 2) {
+    float acc[kGroups][4];
+#pragma unroll
+    for (int jj = 0; jj < kGroups; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0.0f;
+    const uint32_t* words = spk + t * hw;
+    int wi = 0;
+    uint32_t bits = words[0];
+    auto next_k = [&]() -> int {
+      while (bits == 0u) {
+        if (++wi >= hw) return -1;
+        bits = words[wi];
+      }
+      const int i = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      return wi * 32 + i;
+    };
+    float4 cur[kGroups];
+    int k = next_k();
+    if (k >= 0) {
+      const float4* wr = reinterpret_cast<const float4*>(w + k * Cp) + h;
+#pragma unroll
+      for (int jj = 0; jj < kGroups; ++jj)
+        if (4 * (2 * jj + h) < C) cur[jj] = wr[2 * jj];
+    }
+    while (k >= 0) {
+      const int kn = next_k();
+      float4 nxt[kGroups];
+      if (kn >= 0) {
+        const float4* wr = reinterpret_cast<const float4*>(w + kn * Cp) + h;
+#pragma unroll
+        for (int jj = 0; jj < kGroups; ++jj)
+          if (4 * (2 * jj + h) < C) nxt[jj] = wr[2 * jj];
+      }
+#pragma unroll
+      for (int jj = 0; jj < kGroups; ++jj) {
+        const int c0 = 4 * (2 * jj + h);
+        if (c0 + 0 < C) acc[jj][0] = __fadd_rn(acc[jj][0], cur[jj].x);
+        if (c0 + 1 < C) acc[jj][1] = __fadd_rn(acc[jj][1], cur[jj].y);
+        if (c0 + 2 < C) acc[jj][2] = __fadd_rn(acc[jj][2], cur[jj].z);
+        if (c0 + 3 < C) acc[jj][3] = __fadd_rn(acc[jj][3], cur[jj].w);
+      }
+#pragma unroll
+      for (int jj = 0; jj < kGroups; ++jj) cur[jj] = nxt[jj];
+      k = kn;
+    }
+#pragma unroll
+    for (int jj = 0; jj < kGroups; ++jj)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = 4 * (2 * jj + h) + e;
+        float vout = 0.0f;
+        if (c < C) vout = a.bias != nullptr ? __fadd_rn(acc[jj][e], a.bias[c]) : acc[jj][e];
+        buf[t * kRoStride + c] = vout;  // c < 32: classes >= C are zero
+      }
+  }
+  sync();
+  RO_CLK(2)
+  if (warp == 0) {
+    float* col = buf + lane;
+    const float vb = lane < C ? clip01(beta_l) : 0.0f;
+    // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50); col[t] <- V3_t
+    float v = 0.0f, logit = 0.0f;
+    int t = 0;
+    if (a.readout_lif) {
+      // LIF readout (neuron.hpp:127-136): s_t = [v - theta >= 0] is the trace, the
+      // logits its time sums (network.hpp:396, objective.hpp:40-50)
+      const float ntheta = -a.theta;
+      for (; t < T; ++t) {
+        const float I = col[t * kRoStride];
+        col[t * kRoStride] = v;
+        const bool sp = __fadd_rn(v, ntheta) >= 0.0f;
+        v = __fsub_rn(__fadd_rn(__fmul_rn(v, vb), I), sp ? a.theta : 0.0f);
+        logit = __fadd_rn(logit, sp ? 1.0f : 0.0f);
+      }
+    }
+    for (; t + 8 <= T; t += 8) {
+      float I[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * kRoStride];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        col[(t + e) * kRoStride] = v;
+        v = __fadd_rn(__fmul_rn(v, vb), I[e]);
+        logit = __fadd_rn(logit, v);
+      }
+    }
+    for (; t < T; ++t) {
+      const float I = col[t * kRoStride];
+      col[t * kRoStride] = v;
+      v = __fadd_rn(__fmul_rn(v, vb), I);
+      logit = __fadd_rn(logit, v);
+    }
+    const float v_final = v;
+    RO_CLK(3)
+    // softmax CE, sequential order of objective.hpp:53-73.  The class values are
+    // gathered with independent shuffles first; only the max / sum chains are serial.
+    float lg[kMaxClasses];
+#pragma unroll
+    for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, logit, j);
+    float mx = lg[0];
+#pragma unroll
+    for (int j = 1; j < kMaxClasses; ++j)
+      if (j < C) mx = (mx < lg[j]) ? lg[j] : mx;
+    const float xd = __fsub_rn(logit, mx);
+    const float ex = (lane < C && a.loss_kind == 0) ? (a.exp_mode ? expf(xd) : exp_cr(xd)) : 0.0f;
+#pragma unroll
+    for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, ex, j);
+    float z = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kMaxClasses; ++j)
+      if (j < C) z = __fadd_rn(z, lg[j]);
+    const int y = *s_label;
+    const float logit_y = __shfl_sync(0xffffffffu, logit, y);
+    // argmax, ties to the lowest index (objective.hpp:126-131)
+    float bv = lane < C ? logit : -INFINITY;
+    int bi = lane < C ? lane : 1 << 30;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      if (a.loss_kind == 0)
+        a.loss_b[b] = __fsub_rn(__fadd_rn(mx, a.exp_mode ? logf(z) : log_cr(z)), logit_y);
+      a.correct_b[b] = (bi == y) ? 1 : 0;
+    }
+    float delta = 0.0f;
+    if (lane < C) {
+      if (a.loss_kind == 1) {
+        // spike_rate_mse (objective.hpp:139-183): r = counts / T, d = r - target;
+        // the loss term d*d and the cotangent gs*d on every step
+        const float r = __fdiv_rn(logit, float(T));
+        const float d = __fsub_rn(r, lane == y ? a.rate_hi : a.rate_lo);
+        a.loss_terms[size_t(b) * C + lane] = __fmul_rn(d, d);
+        delta = __fmul_rn(a.mse_gs, d);
+      } else {
+        float d = __fdiv_rn(ex, z);
+        if (lane == y) d = __fsub_rn(d, 1.0f);
+        delta = __fmul_rn(d, a.inv_b);
+      }
+    }
+    if (a.dbg_trace != nullptr && lane < C) {
+      for (int s = 0; s < T; ++s)
+        a.dbg_trace[(size_t(b) * T + s) * C + lane] =
+            a.readout_lif ? (__fadd_rn(col[s * kRoStride], -a.theta) >= 0.0f ? 1.0f : 0.0f)
+                          : s + 1 < T ? col[(s + 1) * kRoStride] : v_final;
+    }
+    RO_CLK(4)
+    float G = delta, db = 0.0f, dbias = 0.0f;
+    if (a.readout_lif) {
+      // LIF reverse (the hidden layers' closure order, App. A.2) with dS_t = delta on
+      // every step: dI3_t = G ; G = G bc + (delta + (-G) theta) g(V3_t - theta)
+      G = 0.0f;
+      for (t = T - 1; t >= 0; --t) {
+        const float V3 = col[t * kRoStride];
+        const float gi = G;
+        const float gs = __fadd_rn(delta, __fmul_rn(-gi, a.theta));
+        const float g = surrogate_rt(a.act, a.slope, a.aux, __fadd_rn(V3, -a.theta));
+        G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
+        db = __fadd_rn(db, __fmul_rn(gi, V3));
+        dbias = __fadd_rn(dbias, gi);
+        col[t * kRoStride] = gi;
+      }
+    } else {
+    // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
+    t = T - 1;
+    {
+      const float V3 = col[t * kRoStride];
+      db = __fmul_rn(G, V3);
+      dbias = G;
+      col[t * kRoStride] = G;
+    }
+    --t;
+    for (; t >= 7; t -= 8) {
+      float V3[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * kRoStride];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        G = __fadd_rn(delta, __fmul_rn(G, vb));
+        db = __fadd_rn(db, __fmul_rn(G, V3[e]));
+        dbias = __fadd_rn(dbias, G);
+        col[(t - e) * kRoStride] = G;
+      }
+    }
+    for (; t >= 0; --t) {
+      const float V3 = col[t * kRoStride];
+      G = __fadd_rn(delta, __fmul_rn(G, vb));
+      db = __fadd_rn(db, __fmul_rn(G, V3));
+      dbias = __fadd_rn(dbias, G);
+      col[t * kRoStride] = G;
+    }
+    }
+    if (lane < C) {
+      a.dbeta_part[size_t(b) * C + lane] = db;
+      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
+    }
+    RO_CLK(5)
+  }
+  sync();
+  RO_CLK(6)
+  // dI3 as three bf16 planes [3][64][B*T_pad] (class rows, (b,t) contiguous)
+  const int chunks = (T + 7) / 8;
+  const size_t cols = size_t(a.B) * a.T_pad;
+  const size_t plane = size_t(64) * cols;
+  for (int u = tid; u < C * chunks; u += G) {
+    const int c = u / chunks, t0 = (u % chunks) * 8;
+    uint32_t hp[4], mp[4], lp[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float g0 = t0 + e < T ? buf[(t0 + e) * kRoStride + c] : 0.0f;
+      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * kRoStride + c] : 0.0f;
+      split3_pack(g0, g1, hp[e / 2], mp[e / 2], lp[e / 2]);
+    }
+    const size_t off = size_t(c) * cols + size_t(b) * a.T_pad + t0;
+    *reinterpret_cast<uint4*>(a.d3_planes + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+    *reinterpret_cast<uint4*>(a.d3_planes + plane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
+    *reinterpret_cast<uint4*>(a.d3_planes + 2 * plane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+  }
+  sync();
+  RO_CLK(7)
+  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 15] = globaltimer();
+#undef RO_CLK
+}
+
+__global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
+  extern __shared__ float rsm[];
+  // W [HL][C] is a parameter (written by the previous step's update, long complete):
+  // staged before the dependency wait, overlapping the forward kernel's tail
+  {
+    const int C = a.C, Cp = (C + 3) & ~3, nw = a.HL * C;
+    if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
+      const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
+      for (int i = threadIdx.x; i < nw / 4; i += kRoThreads) reinterpret_cast<float4*>(rsm)[i] = __ldg(src + i);
+    } else {
+      for (int i = threadIdx.x; i < a.HL * Cp; i += kRoThreads) {
+        const int k = i / Cp, c = i % Cp;
+        rsm[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
+      }
+    }
+  }
+  pdl_wait();
+  readout_sample(a, blockIdx.x, rsm, threadIdx.x, kRoThreads, 1, true);
+  pdl_launch_dependents();
+}
+
 // ============================================================================
 // K1  k_lif_fwd: I^T[n][t] = sum_k Wt[n][k] * A[t][k] on tcgen05 (3 bf16 planes
 // of W, binary A exact in bf16), then the LIF scan epilogue straight from TMEM.
@@ -183,6 +572,7 @@ constexpr int kFwdStagesMax = 2;
 constexpr int kFwdSpbMax = 2;
 constexpr int kFwdScanWarps = 4 * kFwdSpbMax;
 constexpr int kFwdThreads = 32 * (kFwdScanWarps + 4 + 2);
+
 constexpr uint32_t kPlaneTile = 128 * 128;  // 128 rows x 64 bf16 = 16 KB
 
 __host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT, int spb) {
@@ -620,369 +1010,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tc_fence_after();
     tmem_dealloc_any(tmem_cols, tmem);
   }
-}
-
-// Surrogate for the backward sweep (surrogate.hpp:59-120), compile-time kind so
-// the unrolled step bodies stay branch-free; divisions evaluated as approximate
-// reciprocals (<= 1 ulp; the backward is checked to the 1e-4 gradient bound,
-// the bit-exact parts are the forward scans).
-template <int kAct>
-__device__ __forceinline__ float surrogate_t(float k, float aux, float x) {
-  if constexpr (kAct == 1) {  // superspike 1/(1+k|x|)^2
-    const float d = __fadd_rn(1.0f, __fmul_rn(k, fabsf(x)));
-    return rcp_approx(__fmul_rn(d, d));
-  } else if constexpr (kAct == 2) {  // triangular max(0, 1-|kx|)
-    const float r = __fsub_rn(1.0f, fabsf(__fmul_rn(k, x)));
-    return 0.0f < r ? r : 0.0f;
-  } else if constexpr (kAct == 3) {  // arctan 1/(1+(pi k x/2)^2)
-    const float u = __fmul_rn(k * 1.57079632679489662f, x);
-    return rcp_approx(__fadd_rn(1.0f, __fmul_rn(u, u)));
-  } else if constexpr (kAct == 4) {  // boxcar
-    return fabsf(x) <= __fmul_rn(k, 0.5f) ? aux : 0.0f;
-  } else if constexpr (kAct == 5) {
-    // sigmoid, DECLARED (not in the reference catalogue, SPEC.md:283): the
-    // backward a caller hands to custom(heaviside, bwd), surrogate.hpp:45-57,
-    // g = k s (1 - s) = (k e) / ((1 + e)(1 + e)), e = exp(-k |x|): the
-    // cancellation-free form of oracle/spiketrain_oracle.h (accurate expf)
-    const float e = expf(-__fmul_rn(k, fabsf(x)));
-    const float d = __fadd_rn(1.0f, e);
-    return __fdiv_rn(__fmul_rn(k, e), __fmul_rn(d, d));
-  } else {  // custom straight-through
-    return 1.0f;
-  }
-}
-
-// the surrogate with a runtime kind (the readout's few steps per lane)
-__device__ __forceinline__ float surrogate_rt(int act, float k, float aux, float x) {
-  switch (act) {
-    case 1: return surrogate_t<1>(k, aux, x);
-    case 2: return surrogate_t<2>(k, aux, x);
-    case 3: return surrogate_t<3>(k, aux, x);
-    case 4: return surrogate_t<4>(k, aux, x);
-    case 5: return surrogate_t<5>(k, aux, x);
-    default: return 1.0f;
-  }
-}
-
-// ============================================================================
-// K4  k_readout: readout projection (exact sparse gather in the reference's
-// ascending-k order, ops.hpp:163-172), LI scan, integral CE + accuracy, CE
-// backward and the closed-form LI reverse scan (App. A.3).  grid B, block 128.
-// ============================================================================
-struct ReadoutArgs {
-  const uint32_t* s_in;     // neuron-packed spikes of the last hidden layer
-  const uint32_t* rows;     // [B]
-  const int64_t* rows_slot; // schedule mode: rows += *rows_slot * B (else nullptr)
-  const int32_t* labels;    // dataset labels [N]
-  const float* w;           // readout W [HL][C] f32 (master)
-  const float* bias;        // [C] or nullptr
-  const float* beta;        // [C] (or one value: beta_stride 0)
-  int beta_stride;
-  __nv_bfloat16* d3_planes; // [3][64][B*T_pad] (class rows, (b,t) contiguous)
-  float* loss_b;            // [B] lse - logit_y
-  int32_t* correct_b;       // [B]
-  float* dbeta_part;        // [B][C]
-  float* dbias_part;        // [B][C] or nullptr
-  float* dbg_trace;         // optional [B][T][C]
-  long long* dbg_clk;       // optional [B][8] phase timestamps (clock64)
-  int exp_mode;             // 0: exp/log evaluated in fp64 then rounded; 1: expf/logf
-  int B, T, T_pad, HL, HL_pad, C;
-  float inv_b;              // 1/B_global (objective.hpp:104)
-  int loss_kind;            // 0 integral CE, 1 spike-rate MSE (objective.hpp:139-183)
-  float rate_hi, rate_lo;   // rate-MSE targets
-  float mse_gs;             // 2 / (float(B_global*C) * float(T)) (objective.hpp:172)
-  float* loss_terms;        // rate-MSE: [B][C] squared rate gaps (summed in order by the tail)
-  // LIF readout (network.hpp:153-155, :396): the trace is the readout's spikes; its
-  // threshold and surrogate are the hidden layers' (readout_lif 0: LI readout)
-  int readout_lif, act;
-  float theta, slope, aux;
-};
-
-__device__ __forceinline__ float exp_cr(float x) { return float(exp(double(x))); }
-__device__ __forceinline__ float log_cr(float x) { return float(log(double(x))); }
-
-// readout scratch: W [HL][C] | spike words [T][HL_pad/32] | per-(t, class) column
-// buffer [T][33] (one column per lane; stride 33 keeps both the per-step rows
-// written by the projection and the per-class columns read by the scans free
-// of bank conflicts)
-constexpr int kRoStride = 33;
-constexpr int kRoThreads = 256;  // projection: 2 lanes per time step (class groups split)
-__host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
-}
-
-__global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
-  extern __shared__ float rsm[];
-  const int C = a.C, T = a.T;
-  const int hw = a.HL_pad / 32;
-  const int Cp = (C + 3) & ~3;
-  float* w = rsm;                                                      // [HL][Cp]
-  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * Cp);  // [T][hw]
-  float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
-  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-#define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
-  // W [HL][C] is a parameter (written by the previous step's update, long complete):
-  // staged before the dependency wait, overlapping the forward kernel's tail
-  {
-    const int nw = a.HL * C;
-    if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
-      const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
-      for (int i = tid; i < nw / 4; i += kRoThreads) reinterpret_cast<float4*>(w)[i] = __ldg(src + i);
-    } else {
-      for (int i = tid; i < a.HL * Cp; i += kRoThreads) {
-        const int k = i / Cp, c = i % Cp;
-        w[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
-      }
-    }
-  }
-  const float beta_l = lane < C ? a.beta[lane * a.beta_stride] : 0.0f;
-  pdl_wait();
-  RO_CLK(0)
-  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
-  __shared__ int s_label;
-  if (tid == 0) s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
-  {
-    const uint4* __restrict__ ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
-    for (int i = tid; i < T * hw / 4; i += kRoThreads) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
-  }
-  __syncthreads();
-  RO_CLK(1)
-  // projection (ops.hpp:163-172 order: ascending k, zero skip): a lane pair per
-  // time step, lane h of the pair owning the 4-class groups j = 2jj + h (acc in
-  // registers; the pair walks the same spike bits).  W rows live in smem padded to
-  // Cp = C rounded up to 4 floats; the row of the next spike is loaded while the
-  // current one is added, so a burst of spikes costs the add chain, not one smem
-  // round trip per spike.
-  constexpr int kGroups = kMaxClasses / 8;  // 4-class groups per lane
-  const int h = tid & 1;
-  for (int t = tid >> 1; t < T; t += kRoThreads / 2) {
-    float acc[kGroups][4];
-#pragma unroll
-    for (int jj = 0; jj < kGroups; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0.0f;
-    const uint32_t* words = spk + t * hw;
-    int wi = 0;
-    uint32_t bits = words[0];
-    auto next_k = [&]() -> int {
-      while (bits == 0u) {
-        if (++wi >= hw) return -1;
-        bits = words[wi];
-      }
-      const int i = __ffs(bits) - 1;
-      bits &= bits - 1u;
-      return wi * 32 + i;
-    };
-    float4 cur[kGroups];
-    int k = next_k();
-    if (k >= 0) {
-      const float4* wr = reinterpret_cast<const float4*>(w + k * Cp) + h;
-#pragma unroll
-      for (int jj = 0; jj < kGroups; ++jj)
-        if (4 * (2 * jj + h) < C) cur[jj] = wr[2 * jj];
-    }
-    while (k >= 0) {
-      const int kn = next_k();
-      float4 nxt[kGroups];
-      if (kn >= 0) {
-        const float4* wr = reinterpret_cast<const float4*>(w + kn * Cp) + h;
-#pragma unroll
-        for (int jj = 0; jj < kGroups; ++jj)
-          if (4 * (2 * jj + h) < C) nxt[jj] = wr[2 * jj];
-      }
-#pragma unroll
-      for (int jj = 0; jj < kGroups; ++jj) {
-        const int c0 = 4 * (2 * jj + h);
-        if (c0 + 0 < C) acc[jj][0] = __fadd_rn(acc[jj][0], cur[jj].x);
-        if (c0 + 1 < C) acc[jj][1] = __fadd_rn(acc[jj][1], cur[jj].y);
-        if (c0 + 2 < C) acc[jj][2] = __fadd_rn(acc[jj][2], cur[jj].z);
-        if (c0 + 3 < C) acc[jj][3] = __fadd_rn(acc[jj][3], cur[jj].w);
-      }
-#pragma unroll
-      for (int jj = 0; jj < kGroups; ++jj) cur[jj] = nxt[jj];
-      k = kn;
-    }
-#pragma unroll
-    for (int jj = 0; jj < kGroups; ++jj)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int c = 4 * (2 * jj + h) + e;
-        float vout = 0.0f;
-        if (c < C) vout = a.bias != nullptr ? __fadd_rn(acc[jj][e], a.bias[c]) : acc[jj][e];
-        buf[t * kRoStride + c] = vout;  // c < 32: classes >= C are zero
-      }
-  }
-  __syncthreads();
-  RO_CLK(2)
-  if (warp == 0) {
-    float* col = buf + lane;
-    const float vb = lane < C ? clip01(beta_l) : 0.0f;
-    // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50); col[t] <- V3_t
-    float v = 0.0f, logit = 0.0f;
-    int t = 0;
-    if (a.readout_lif) {
-      // LIF readout (neuron.hpp:127-136): s_t = [v - theta >= 0] is the trace, the
-      // logits its time sums (network.hpp:396, objective.hpp:40-50)
-      const float ntheta = -a.theta;
-      for (; t < T; ++t) {
-        const float I = col[t * kRoStride];
-        col[t * kRoStride] = v;
-        const bool sp = __fadd_rn(v, ntheta) >= 0.0f;
-        v = __fsub_rn(__fadd_rn(__fmul_rn(v, vb), I), sp ? a.theta : 0.0f);
-        logit = __fadd_rn(logit, sp ? 1.0f : 0.0f);
-      }
-    }
-    for (; t + 8 <= T; t += 8) {
-      float I[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * kRoStride];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        col[(t + e) * kRoStride] = v;
-        v = __fadd_rn(__fmul_rn(v, vb), I[e]);
-        logit = __fadd_rn(logit, v);
-      }
-    }
-    for (; t < T; ++t) {
-      const float I = col[t * kRoStride];
-      col[t * kRoStride] = v;
-      v = __fadd_rn(__fmul_rn(v, vb), I);
-      logit = __fadd_rn(logit, v);
-    }
-    const float v_final = v;
-    RO_CLK(3)
-    // softmax CE, sequential order of objective.hpp:53-73.  The class values are
-    // gathered with independent shuffles first; only the max / sum chains are serial.
-    float lg[kMaxClasses];
-#pragma unroll
-    for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, logit, j);
-    float mx = lg[0];
-#pragma unroll
-    for (int j = 1; j < kMaxClasses; ++j)
-      if (j < C) mx = (mx < lg[j]) ? lg[j] : mx;
-    const float xd = __fsub_rn(logit, mx);
-    const float ex = (lane < C && a.loss_kind == 0) ? (a.exp_mode ? expf(xd) : exp_cr(xd)) : 0.0f;
-#pragma unroll
-    for (int j = 0; j < kMaxClasses; ++j) lg[j] = __shfl_sync(0xffffffffu, ex, j);
-    float z = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kMaxClasses; ++j)
-      if (j < C) z = __fadd_rn(z, lg[j]);
-    const int y = s_label;
-    const float logit_y = __shfl_sync(0xffffffffu, logit, y);
-    // argmax, ties to the lowest index (objective.hpp:126-131)
-    float bv = lane < C ? logit : -INFINITY;
-    int bi = lane < C ? lane : 1 << 30;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      if (a.loss_kind == 0)
-        a.loss_b[b] = __fsub_rn(__fadd_rn(mx, a.exp_mode ? logf(z) : log_cr(z)), logit_y);
-      a.correct_b[b] = (bi == y) ? 1 : 0;
-    }
-    float delta = 0.0f;
-    if (lane < C) {
-      if (a.loss_kind == 1) {
-        // spike_rate_mse (objective.hpp:139-183): r = counts / T, d = r - target;
-        // the loss term d*d and the cotangent gs*d on every step
-        const float r = __fdiv_rn(logit, float(T));
-        const float d = __fsub_rn(r, lane == y ? a.rate_hi : a.rate_lo);
-        a.loss_terms[size_t(b) * C + lane] = __fmul_rn(d, d);
-        delta = __fmul_rn(a.mse_gs, d);
-      } else {
-        float d = __fdiv_rn(ex, z);
-        if (lane == y) d = __fsub_rn(d, 1.0f);
-        delta = __fmul_rn(d, a.inv_b);
-      }
-    }
-    if (a.dbg_trace != nullptr && lane < C) {
-      for (int s = 0; s < T; ++s)
-        a.dbg_trace[(size_t(b) * T + s) * C + lane] =
-            a.readout_lif ? (__fadd_rn(col[s * kRoStride], -a.theta) >= 0.0f ? 1.0f : 0.0f)
-                          : s + 1 < T ? col[(s + 1) * kRoStride] : v_final;
-    }
-    RO_CLK(4)
-    float G = delta, db = 0.0f, dbias = 0.0f;
-    if (a.readout_lif) {
-      // LIF reverse (the hidden layers' closure order, App. A.2) with dS_t = delta on
-      // every step: dI3_t = G ; G = G bc + (delta + (-G) theta) g(V3_t - theta)
-      G = 0.0f;
-      for (t = T - 1; t >= 0; --t) {
-        const float V3 = col[t * kRoStride];
-        const float gi = G;
-        const float gs = __fadd_rn(delta, __fmul_rn(-gi, a.theta));
-        const float g = surrogate_rt(a.act, a.slope, a.aux, __fadd_rn(V3, -a.theta));
-        G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
-        db = __fadd_rn(db, __fmul_rn(gi, V3));
-        dbias = __fadd_rn(dbias, gi);
-        col[t * kRoStride] = gi;
-      }
-    } else {
-    // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
-    t = T - 1;
-    {
-      const float V3 = col[t * kRoStride];
-      db = __fmul_rn(G, V3);
-      dbias = G;
-      col[t * kRoStride] = G;
-    }
-    --t;
-    for (; t >= 7; t -= 8) {
-      float V3[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * kRoStride];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        G = __fadd_rn(delta, __fmul_rn(G, vb));
-        db = __fadd_rn(db, __fmul_rn(G, V3[e]));
-        dbias = __fadd_rn(dbias, G);
-        col[(t - e) * kRoStride] = G;
-      }
-    }
-    for (; t >= 0; --t) {
-      const float V3 = col[t * kRoStride];
-      G = __fadd_rn(delta, __fmul_rn(G, vb));
-      db = __fadd_rn(db, __fmul_rn(G, V3));
-      dbias = __fadd_rn(dbias, G);
-      col[t * kRoStride] = G;
-    }
-    }
-    if (lane < C) {
-      a.dbeta_part[size_t(b) * C + lane] = db;
-      if (a.dbias_part != nullptr) a.dbias_part[size_t(b) * C + lane] = dbias;
-    }
-    RO_CLK(5)
-  }
-  pdl_launch_dependents();
-  __syncthreads();
-  RO_CLK(6)
-  // dI3 as three bf16 planes [3][64][B*T_pad] (class rows, (b,t) contiguous)
-  const int chunks = (T + 7) / 8;
-  const size_t cols = size_t(a.B) * a.T_pad;
-  const size_t plane = size_t(64) * cols;
-  for (int u = tid; u < C * chunks; u += kRoThreads) {
-    const int c = u / chunks, t0 = (u % chunks) * 8;
-    uint32_t hp[4], mp[4], lp[4];
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      const float g0 = t0 + e < T ? buf[(t0 + e) * kRoStride + c] : 0.0f;
-      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * kRoStride + c] : 0.0f;
-      split3_pack(g0, g1, hp[e / 2], mp[e / 2], lp[e / 2]);
-    }
-    const size_t off = size_t(c) * cols + size_t(b) * a.T_pad + t0;
-    *reinterpret_cast<uint4*>(a.d3_planes + off) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-    *reinterpret_cast<uint4*>(a.d3_planes + plane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
-    *reinterpret_cast<uint4*>(a.d3_planes + 2 * plane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
-  }
-  __syncthreads();
-  RO_CLK(7)
-  if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 15] = globaltimer();
-#undef RO_CLK
 }
 
 // ============================================================================
@@ -3233,6 +3260,33 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
   const int S = a.splits;
   const int unit = mt0 / a.mg + (a.m_tiles + a.mg - 1) / a.mg * ntile;
   const int tile = tl.tile_base[j] + unit;
+  // 2. this CTA's rows [r0, r1) of the tile, in chunks of cr rows: every split's
+  //    rows are bulk-loaded into smem [split][row][n_tile], summed in the order of
+  //    k_reduce's sum_partials_pair (splits [0, S/2) and [S/2, S) ascending, then
+  //    the halves added: forward_backward and a train step see the same bits),
+  //    then Adam / SGD and the bf16 plane refresh per element
+  const int R = nm * 128;
+  const int r0 = R * split / S, r1 = R * (split + 1) / S;
+  const uint32_t rowb = uint32_t(a.n_tile) * 4u;
+  const int cr = max(1, min(r1 - r0, int((kWgBarrierOffset - 1024) / (uint32_t(S) * rowb))));
+  // Adam's operands of this thread's first element group (the first chunk) do not
+  // depend on the partials: loaded before the tile wait so their latency hides in it
+  const int nr_first = min(cr, r1 - r0);
+  float pf_p[4] = {0.f, 0.f, 0.f, 0.f}, pf_m[4] = {0.f, 0.f, 0.f, 0.f}, pf_v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (tid < nr_first * nt4) {
+    const int k = mt0 * 128 + r0 + tid / nt4, n0 = ntile * a.n_tile + 4 * (tid % nt4);
+    if (k < tl.rows[j] && n0 < tl.cols[j]) {
+      const int64_t i0 = tl.w_off[j] + int64_t(k) * tl.cols[j] + n0;
+      const int nv = min(4, tl.cols[j] - n0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < nv) {
+          pf_p[e] = ad.params[i0 + e];
+          pf_m[e] = ad.m[i0 + e];
+          pf_v[e] = ad.v[i0 + e];
+        }
+    }
+  }
   // 1. own partial by TMA tensor stores from the SW128 staging; once the writes are
   //    performed, arrive on the tile counter and wait for the tile's other splits
   if (tid == 0) {
@@ -3257,15 +3311,6 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
     if (clk != nullptr) clk[9] = clock64();
   }
   bar1(kWgProd);
-  // 2. this CTA's rows [r0, r1) of the tile, in chunks of cr rows: every split's
-  //    rows are bulk-loaded into smem [split][row][n_tile], summed in the order of
-  //    k_reduce's sum_partials_pair (splits [0, S/2) and [S/2, S) ascending, then
-  //    the halves added: forward_backward and a train step see the same bits),
-  //    then Adam / SGD and the bf16 plane refresh per element
-  const int R = nm * 128;
-  const int r0 = R * split / S, r1 = R * (split + 1) / S;
-  const uint32_t rowb = uint32_t(a.n_tile) * 4u;
-  const int cr = max(1, min(r1 - r0, int((kWgBarrierOffset - 1024) / (uint32_t(S) * rowb))));
   uint64_t* rbar = reinterpret_cast<uint64_t*>(smem + kWgRedBarOffset);
   const int rows_j = tl.rows[j], cols_j = tl.cols[j];
   const bool contig = a.n_tiles == 1;  // a tile's rows are one contiguous run per split
@@ -3292,12 +3337,13 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
       const int64_t i0 = tl.w_off[j] + int64_t(k) * cols_j + n0;
       const int nv = min(4, cols_j - n0);
       float p0[4], m0[4], v0[4];
+      const bool pref = c == r0 && g == tid;  // prefetched before the tile wait
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (e < nv) {
-          p0[e] = ad.params[i0 + e];
-          m0[e] = ad.m[i0 + e];
-          v0[e] = ad.v[i0 + e];
+          p0[e] = pref ? pf_p[e] : ad.params[i0 + e];
+          m0[e] = pref ? pf_m[e] : ad.m[i0 + e];
+          v0[e] = pref ? pf_v[e] : ad.v[i0 + e];
         }
       const float4* col = reinterpret_cast<const float4*>(smem + size_t(rr) * rowb) + c4;
       const size_t sstep = size_t(cr) * rowb / 16;  // float4s between splits
