@@ -1031,8 +1031,9 @@ struct snn_engine {
       if (pres_acc) cudaFreeHost(pres_acc);
       pres_loss = nullptr;
       pres_acc = nullptr;
-      CK(cudaMallocHost(&pres_loss, sizeof(float) * steps));
-      CK(cudaMallocHost(&pres_acc, sizeof(double) * steps));
+      // mapped: the step's k_result_out writes straight into it
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&pres_loss), sizeof(float) * steps, cudaHostAllocMapped));
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&pres_acc), sizeof(double) * steps, cudaHostAllocMapped));
       pres_cap = steps;
     }
   }
@@ -1053,15 +1054,12 @@ struct snn_engine {
     // labels from the call's pinned copy (filled and checked up front): no host wait
     CK(cudaMemcpyAsync(pslot[sl].labels.p, plab_host + k * size_t(B), sizeof(int32_t) * B,
                        cudaMemcpyHostToDevice, cstream));
-    CK(cudaEventRecord(ev_ready[sl], cstream));
-  }
-  // the step's re-layout of slot sl on the compute stream, right before its graph
-  void pipe_relayout(int sl) {
-    const int tp8 = (T + 7) / 8, tp8_pad = T_pad / 8;
+    // re-layout on the copy stream too: it overlaps the previous step's graph
     const size_t out = size_t(B) * tp8_pad * IN_pad;
-    k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, stream>>>(praw[sl].p, pslot[sl].x.p, int64_t(B), tp8,
-                                                                    tp8_pad, IN, IN_pad);
+    k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, cstream>>>(praw[sl].p, pslot[sl].x.p, int64_t(B), tp8,
+                                                                     tp8_pad, IN, IN_pad);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(ev_ready[sl], cstream));
   }
 
   // Roll of the next batches along the features (read by the layer-0 forward and
@@ -2228,12 +2226,15 @@ snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const in
     for (size_t k = 0; k < n_steps; ++k) {
       const int sl = int(k & 1);
       CK(cudaStreamWaitEvent(e->stream, e->ev_ready[sl], 0));
-      e->pipe_relayout(sl);
       e->launch(e->pslot[sl], 1);
       CK(cudaEventRecord(e->ev_used[sl], e->stream));
       if (k + 1 < n_steps) e->pipe_stage(k + 1, packed, targets);  // runs while step k does
-      CK(cudaMemcpyAsync(e->pres_loss + k, e->result_loss.p, sizeof(float), cudaMemcpyDeviceToHost, e->stream));
-      CK(cudaMemcpyAsync(e->pres_acc + k, e->result_acc.p, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+      float* hl = nullptr;
+      double* ha = nullptr;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hl), e->pres_loss + k, 0));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ha), e->pres_acc + k, 0));
+      k_result_out<<<1, 1, 0, e->stream>>>(e->result_loss.p, e->result_acc.p, hl, ha);
+      CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(e->stream));
     for (size_t k = 0; k < n_steps; ++k) {

@@ -3802,24 +3802,37 @@ __global__ void k_synth(SynthArgs a) {
 }
 
 // Host-batch layout [n][tp8][IN] (reference packed, data.hpp:105-126) -> the
-// staged layout [n][tp8_pad][IN_pad], zero padded.  One thread per 4 output bytes.
+// staged layout [n][tp8_pad][IN_pad], zero padded.  One thread per 4 output bytes;
+// rows whose feature count is a multiple of 4 copy whole words (32-bit indexing:
+// a host batch is far below 4 GB).
 __global__ void k_relayout(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t n,
                            int tp8, int tp8_pad, int IN, int IN_pad) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t total = n * tp8_pad * IN_pad;
-  if (q * 4 >= total) return;
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t wpr = uint32_t(IN_pad) / 4;  // output words per row
+  const uint32_t row = q / wpr, w = q - row * wpr;
+  if (uint64_t(row) >= uint64_t(n) * tp8_pad) return;
+  const uint32_t g = row % uint32_t(tp8_pad), i = row / uint32_t(tp8_pad);
   uint32_t word = 0;
+  if (g < uint32_t(tp8)) {
+    const uint32_t src = (i * uint32_t(tp8) + g) * uint32_t(IN);  // first byte of the source row
+    if ((IN & 3) == 0) {
+      if (4 * w < uint32_t(IN)) word = *reinterpret_cast<const uint32_t*>(in + src + 4 * w);
+    } else {
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int64_t o = q * 4 + e;
-    const int k = int(o % IN_pad);
-    const int64_t rg = o / IN_pad;
-    const int g = int(rg % tp8_pad);
-    const int64_t i = rg / tp8_pad;
-    const uint32_t v = (k < IN && g < tp8) ? in[(i * tp8 + g) * IN + k] : 0u;
-    word |= v << (8 * e);
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t k = 4 * w + e;
+        if (k < uint32_t(IN)) word |= uint32_t(in[src + k]) << (8 * e);
+      }
+    }
   }
   reinterpret_cast<uint32_t*>(out)[q] = word;  // IN_pad is a multiple of 64
+}
+
+// StepResult of pipelined step k into mapped pinned host memory (no D2H copy on
+// the compute stream between steps).
+__global__ void k_result_out(const float* loss, const double* acc, float* host_loss, double* host_acc) {
+  *host_loss = *loss;
+  *host_acc = *acc;
 }
 
 // monitor_activity (neuron.hpp:106-114): counts[b][n] = spikes of (b, n) over the
