@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-E2E_CHUNK = int(os.environ.get("SNN_E2E_CHUNK", "20"))  # host batches per snn_train_steps_packed call in the e2e leg
+E2E_CHUNK = int(os.environ.get("SNN_E2E_CHUNK", "64"))  # host batches per snn_train_steps_packed call in the e2e leg
 METRIC = "SNN train samples/sec (fwd+bwd+Adam, SHD shape) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "samples/s"
 
@@ -312,7 +312,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=256)
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gemm-planes", type=int, default=3, choices=[1, 2, 3],
@@ -465,7 +465,7 @@ def main():
     # the train() form over host batches: snn_train_steps_packed uploads batch k+1 while
     # step k runs; every step's batch is DMA'd from pinned memory and every StepResult
     # read back inside the timed region (calls of E2E_CHUNK steps)
-    chunk = max(2, min(E2E_CHUNK, args.e2e_steps, (20 * 512) // B))  # bounds the pinned batch set
+    chunk = max(2, min(E2E_CHUNK, args.e2e_steps, (64 * 256) // B))  # bounds the pinned batch set
     seq = np.arange(chunk) % nb
     stream_batches = torch.empty((chunk, B) + tuple(packed_host.shape[1:]), dtype=torch.uint8,
                                  pin_memory=True).numpy()
