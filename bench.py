@@ -181,6 +181,41 @@ def roofline_of(k: dict, hbm_peak: float, tf_peak: float) -> dict:
     return out
 
 
+SPAN_STEPS = 8
+
+
+def kernel_spans(eng, w: dict, first_slot: int) -> dict:
+    """Per-kernel in-graph spans (ms) of the last step of an 8-step graph replayed with
+    clock stamps on (debug level 2: the kernels keep their production paths and each
+    CTA stores its globaltimer start / end): span = last CTA end - first CTA start.
+    Slots: readout 0, forward launch starting at layer l 1 + l, backward of layer l
+    1 + L + l, wgrad (+ the one-rank tail) 1 + 2 L."""
+    L = len(w["hidden"])
+    try:
+        eng.debug(2)
+        eng.enqueue_steps(first_slot, SPAN_STEPS)
+        eng.sync()
+        clk = eng.fetch("clk")
+    except Exception:
+        return {}
+    finally:
+        try:
+            eng.debug(False)
+        except Exception:
+            pass
+    slots = {"readout": 0, "wgrad": 1 + 2 * L}
+    for l in range(L):
+        slots[f"lif_fwd[{l}]"] = 1 + l
+        slots[f"lif_bwd[{l}]"] = 1 + L + l
+    out = {}
+    for name, sl in slots.items():
+        c = clk[sl]
+        v = c[:, 14] > 0
+        if v.any():
+            out[name] = float(c[v, 15].max() - c[v, 14].min()) / 1e6
+    return out
+
+
 def ncu_traffic(kernel: str):
     """dram bytes per launch for `kernel` from the committed ncu summary, if any."""
     for fn in sorted(os.listdir(os.path.join(ROOT, "profiles")) if os.path.isdir(
@@ -403,7 +438,7 @@ def main():
     # schedule: the reference epoch shuffle, this rank's contiguous slice of each global batch
     gb = B * world
     per_epoch = n_data // gb
-    total = warmup + args.steps
+    total = warmup + args.steps + SPAN_STEPS  # + the clock-stamped replay (kernel_spans)
     rows = np.empty((total, B), np.uint32)
     e = 0
     s = 0
@@ -490,10 +525,14 @@ def main():
 
     # --- per-kernel device times (graph with event nodes) -> roofline of the dominant kernel
     prof = eng.profile(args.profile_steps)
+    spans = kernel_spans(eng, w, warmup + args.steps)
     hbm_peak, tf_peak, peak_src = peaks()
     kernels = []
     for name, kms in prof:
-        k = {"name": name, "ms": kms,
+        # in-graph span (first CTA start .. last CTA end, globaltimer) when stamped;
+        # else the event-graph time (which adds a launch and a drain per kernel)
+        k = {"name": name, "ms": spans.get(name, kms), "ms_event_graph": kms,
+             "timing": "in-graph span" if name in spans else "event graph",
              "work": algorithmic(name, w, eng.n_params, eng.forward_launches, B)}
         k["roofline"] = roofline_of(k, hbm_peak, tf_peak)
         kernels.append(k)
@@ -524,7 +563,8 @@ def main():
                                               "D2H loss/acc, host sync every step"}},
             "gpu_launches": eng.launches_per_step * args.steps,
             "roofline": roofline,
-            "kernels": [{"name": k["name"], "ms": round(k["ms"], 5),
+            "kernels": [{"name": k["name"], "ms": round(k["ms"], 5), "timing": k["timing"],
+                         "ms_event_graph": round(k["ms_event_graph"], 5),
                          **{b: round(v["frac"], 4) for b, v in k["roofline"].items()}}
                         for k in kernels],
             "final_loss": loss, "final_acc": acc}
