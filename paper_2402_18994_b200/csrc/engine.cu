@@ -412,7 +412,7 @@ struct snn_engine {
   int bwd_stages = env_int("SNN_BWD_STAGES", 1);
   int exp_mode = env_int("SNN_EXP_MODE", 1) - 1;  // default 0 = fp64-rounded exp/log
   int wg_stages_cap = env_int("SNN_WG_STAGES", kWgStagesMax);
-  int pdl = env_int("SNN_PDL", 1) - 1;  // programmatic dependent launch (measured slower: off)
+  int pdl = env_int("SNN_PDL", 2) - 1;  // programmatic dependent launch: same device step, +3 % e2e (r02)
   static int env_int(const char* k, int d) {
     const char* v = std::getenv(k);
     return (v && *v) ? std::max(1, std::atoi(v)) : d;
