@@ -220,27 +220,26 @@ __device__ __forceinline__ float log_cr(float x) { return float(log(double(x)));
 constexpr int kRoStride = 33;
 constexpr int kRoThreads = 256;  // projection: 2 lanes per time step (class groups split)
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4 + 16;
+  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
 }
 
-// The readout of sample b by a group of G threads (gt = index in the group, G a
-// multiple of 64, named barrier `bar`); k_readout runs one group per CTA.  rsm:
-// readout_smem_bytes of scratch; w_ready: W is already staged in rsm (the kernel
-// loads it before its dependency wait).  (Running this in the tail of the fused
-// forward launch, one group per sample, was measured slower: the forward's
-// 448-thread register budget slows every phase 1.2-8x.)
-__device__ __forceinline__ void readout_sample(const ReadoutArgs& a, int b, float* rsm, int gt, int G,
-                                               int bar, bool w_ready) {
+// (Running the readout in the tail of the fused forward launch, one group of warps
+// per sample, was measured slower: the forward's 448-thread register budget slowed
+// every readout phase 1.2-8x.)
+__global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
+  extern __shared__ float rsm[];
   const int C = a.C, T = a.T;
   const int hw = a.HL_pad / 32;
   const int Cp = (C + 3) & ~3;
   float* w = rsm;                                                      // [HL][Cp]
   uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * Cp);  // [T][hw]
   float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
-  const int tid = gt, warp = gt >> 5, lane = gt & 31;
-  auto sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory"); };
+  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int G = kRoThreads;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
-  if (!w_ready) {
+  // W [HL][C] is a parameter (written by the previous step's update, long complete):
+  // staged before the dependency wait, overlapping the forward kernel's tail
+  {
     const int nw = a.HL * C;
     if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
       const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
@@ -253,17 +252,17 @@ __device__ __forceinline__ void readout_sample(const ReadoutArgs& a, int b, floa
     }
   }
   const float beta_l = lane < C ? a.beta[lane * a.beta_stride] : 0.0f;
+  pdl_wait();
   RO_CLK(0)
   if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
-  int* s_label = reinterpret_cast<int*>(buf + size_t(T) * kRoStride);
+  __shared__ int s_label[1];
   if (tid == 0) *s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
   {
-    // the spike words of this sample (written by the forward: plain loads, not the
-    // non-coherent __ldg path, since the fused forward reads words it just stored)
+    // the spike words of this sample (written by the forward kernel)
     const uint4* ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
-    for (int i = tid; i < T * hw / 4; i += G) reinterpret_cast<uint4*>(spk)[i] = ss[i];
+    for (int i = tid; i < T * hw / 4; i += G) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
   }
-  sync();
+  __syncthreads();
   RO_CLK(1)
   // projection (ops.hpp:163-172 order: ascending k, zero skip): a lane pair per
   // time step, lane h of the pair owning the 4-class groups j = 2jj + h (acc in
@@ -328,7 +327,7 @@ __device__ __forceinline__ void readout_sample(const ReadoutArgs& a, int b, floa
         buf[t * kRoStride + c] = vout;  // c < 32: classes >= C are zero
       }
   }
-  sync();
+  __syncthreads();
   RO_CLK(2)
   if (warp == 0) {
     float* col = buf + lane;
@@ -476,7 +475,8 @@ __device__ __forceinline__ void readout_sample(const ReadoutArgs& a, int b, floa
     }
     RO_CLK(5)
   }
-  sync();
+  pdl_launch_dependents();
+  __syncthreads();
   RO_CLK(6)
   // dI3 as three bf16 planes [3][64][B*T_pad] (class rows, (b,t) contiguous)
   const int chunks = (T + 7) / 8;
@@ -496,31 +496,10 @@ __device__ __forceinline__ void readout_sample(const ReadoutArgs& a, int b, floa
     *reinterpret_cast<uint4*>(a.d3_planes + plane + off) = make_uint4(mp[0], mp[1], mp[2], mp[3]);
     *reinterpret_cast<uint4*>(a.d3_planes + 2 * plane + off) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
   }
-  sync();
+  __syncthreads();
   RO_CLK(7)
   if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 15] = globaltimer();
 #undef RO_CLK
-}
-
-__global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
-  extern __shared__ float rsm[];
-  // W [HL][C] is a parameter (written by the previous step's update, long complete):
-  // staged before the dependency wait, overlapping the forward kernel's tail
-  {
-    const int C = a.C, Cp = (C + 3) & ~3, nw = a.HL * C;
-    if (Cp == C && (reinterpret_cast<uintptr_t>(a.w) & 15) == 0) {
-      const float4* __restrict__ src = reinterpret_cast<const float4*>(a.w);
-      for (int i = threadIdx.x; i < nw / 4; i += kRoThreads) reinterpret_cast<float4*>(rsm)[i] = __ldg(src + i);
-    } else {
-      for (int i = threadIdx.x; i < a.HL * Cp; i += kRoThreads) {
-        const int k = i / Cp, c = i % Cp;
-        rsm[i] = c < C ? __ldg(a.w + k * C + c) : 0.0f;
-      }
-    }
-  }
-  pdl_wait();
-  readout_sample(a, blockIdx.x, rsm, threadIdx.x, kRoThreads, 1, true);
-  pdl_launch_dependents();
 }
 
 // ============================================================================
