@@ -454,7 +454,13 @@ struct snn_engine {
 
   int B_global() const { return B * world; }
   // debug clock stamps: one region per kernel of the step, kClkStride per CTA
-  size_t clk_region() const { return size_t(std::max(4096, 4 * B)) * kClkStride; }
+  // clock-stamp rows per kernel slot: every CTA of the widest launch (backward grids are
+  // B x H_pad/128); tests/wg_probe.py etc. read it through snn_debug_fetch(5)
+  size_t clk_region() const {
+    int tiles = 4;
+    for (int l = 0; l < L; ++l) tiles = std::max(tiles, H_pad[l] / 128);
+    return size_t(std::max(4096, B * tiles)) * kClkStride;
+  }
 
   // ---------------------------------------------------------------- setup
   void validate_and_size() {

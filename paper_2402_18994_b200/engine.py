@@ -672,8 +672,9 @@ class Engine:
     def fetch(self, which: str, layer: int = 0) -> np.ndarray:
         idx = {"I": 0, "V": 1, "spikes": 2, "trace": 3, "dS": 4, "clk": 5, "A": 6, "dI": 7}[which]
         B, T = self.batch_size, self.time_steps
-        if which == "clk":
-            out = np.empty((3 + 2 * len(self.desc["hidden"]), max(B * 4, 4096), 48), np.int64)
+        if which == "clk":  # rows per slot: engine.cu clk_region()
+            tiles = max([4] + [(h + 127) // 128 for h in self.desc["hidden"]])
+            out = np.empty((3 + 2 * len(self.desc["hidden"]), max(B * tiles, 4096), 48), np.int64)
         elif which == "trace" or (which == "dI" and layer == len(self.desc["hidden"])):
             out = np.empty((B, T, self.desc["classes"]), np.float32)
         else:
