@@ -477,6 +477,18 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     loss, acc = eng.read_result()
+    ranks = None
+    if dist is not None:
+        # proof of participation: every rank's device, step counter and replica checksum
+        # (the data-parallel replicas must be bit-identical)
+        p = eng.get_params()
+        mine = {"rank": rank, "device": torch.cuda.get_device_name(local), "local_rank": local,
+                "steps_done": int(eng.get_opt_state()[2]),
+                "param_checksum": float(np.float64(p.astype(np.float64).sum()))}
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        ranks = {"world": world, "tail": config.get("dp_tail"), "per_rank": allr,
+                 "replicas_identical": len({r["param_checksum"] for r in allr}) == 1}
     ms_per_step = ms / args.steps
     value = gb * args.steps / (ms / 1e3)
 
@@ -562,6 +574,7 @@ def main():
                                       "path": "snn_train_step_packed: H2D, re-layout, step graph, "
                                               "D2H loss/acc, host sync every step"}},
             "gpu_launches": eng.launches_per_step * args.steps,
+            **({"ranks": ranks} if ranks is not None else {}),
             "roofline": roofline,
             "kernels": [{"name": k["name"], "ms": round(k["ms"], 5), "timing": k["timing"],
                          "ms_event_graph": round(k["ms_event_graph"], 5),
