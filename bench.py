@@ -187,7 +187,9 @@ SPAN_STEPS = 8
 def kernel_spans(eng, w: dict, first_slot: int) -> dict:
     """Per-kernel in-graph spans (ms) of the last step of an 8-step graph replayed with
     clock stamps on (debug level 2: the kernels keep their production paths and each
-    CTA stores its globaltimer start / end): span = last CTA end - first CTA start.
+    CTA stores its globaltimer once past its dependency wait, and at its end): span =
+    last CTA end - first CTA start (so a kernel launched early by PDL is not charged
+    for the time it waits on its predecessor).
     Slots: readout 0, forward launch starting at layer l 1 + l, backward of layer l
     1 + L + l, wgrad (+ the one-rank tail) 1 + 2 L."""
     L = len(w["hidden"])

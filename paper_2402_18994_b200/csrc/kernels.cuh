@@ -691,7 +691,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (clk != nullptr && threadIdx.x == 0) {
     clk[0] = clock64();
     clk[6] = globaltimer();
-    clk[14] = clk[6];
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     clk[4] = smid;
@@ -725,6 +724,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   pdl_wait();  // activations / planes of the previous kernels are visible from here
+  if (clk != nullptr && threadIdx.x == 0) clk[14] = globaltimer();  // span start: past the dependency wait
   const uint32_t tmem = *tmem_slot;
   const int dec_warp0 = kFwdScanWarps, tma_warp = kFwdScanWarps + 4, mma_warp = tma_warp + 1;
 
@@ -1264,10 +1264,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x, nt = blockIdx.y;
   long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * kClkStride : nullptr;
-  if (clk != nullptr && threadIdx.x == 0) {
-    clk[0] = clock64();
-    clk[14] = globaltimer();
-  }
+  if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;
   // one t-tile: TT more columns cache the membranes V between the two scan passes
@@ -1291,6 +1288,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   __syncthreads();
   tc_fence_after();
   pdl_wait();
+  if (clk != nullptr && threadIdx.x == 0) clk[14] = globaltimer();  // span start: past the dependency wait
   const uint32_t tmem = *tmem_slot;
   const int cols_total = a.B * a.T_pad;
 
@@ -3426,7 +3424,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   __syncthreads();
   tc_fence_after();
   pdl_wait();
-  if (clk != nullptr && threadIdx.x == 0) clk[1] = clock64();
+  if (clk != nullptr && threadIdx.x == 0) {
+    clk[1] = clock64();
+    clk[14] = globaltimer();  // span start: past the dependency wait
+  }
   const uint32_t tmem = *tmem_slot;
   if (warp == kWgProdWarps) {
     if (elect_one()) {
@@ -3608,7 +3609,6 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   if (clk != nullptr && threadIdx.x == 0) {
     clk[5] = clock64();
     clk[7] = globaltimer();
-    clk[14] = clk[6];
     clk[15] = clk[7];
   }
   if (warp == 0) {

@@ -4,7 +4,7 @@
 # report is kept so gpurun_out stays under the copy-back limit.
 #   gpurun --timeout 3000 -- 'bash profiles/evidence.sh r02a'
 mkdir -p gpurun_out
-TAG=${1:-r02}
+TAG=${1:-r02b}
 set -x
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
