@@ -1287,12 +1287,20 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  const int ctl_warp = kBwdScanThreads / 32;
+  // the first stage's W planes are parameters (last written by the previous step's
+  // update, complete before this step's forward passed its own wait): their TMA goes
+  // out before the dependency wait, overlapping the previous kernel's tail
+  if (warp == ctl_warp && lane == 0 && total > 0) {
+    mbar_arrive_expect_tx(&full[0], uint32_t(a.planes) * (kPlaneTile + btile));
+    for (int p = 0; p < a.planes; ++p)
+      tma_load_2d(smem + p * kPlaneTile, &tm_w, &full[0], 0, p * a.H_pad + nt * 128);
+  }
   pdl_wait();
   if (clk != nullptr && threadIdx.x == 0) clk[14] = globaltimer();  // span start: past the dependency wait
   const uint32_t tmem = *tmem_slot;
   const int cols_total = a.B * a.T_pad;
 
-  const int ctl_warp = kBwdScanThreads / 32;
   if (warp == ctl_warp) {
     if (lane == 0) {
       tma_prefetch(&tm_w);
@@ -1301,11 +1309,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         const int s = it % S, ph = (it / S) & 1;
         const int tt = a.NT - 1 - it / KB, kb = it % KB;
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], uint32_t(a.planes) * (kPlaneTile + btile));
+        if (it > 0) mbar_arrive_expect_tx(&full[s], uint32_t(a.planes) * (kPlaneTile + btile));
         uint8_t* A = smem + s * stage_bytes;
         uint8_t* Bt = A + 3 * kPlaneTile;
         for (int p = 0; p < a.planes; ++p) {
-          tma_load_2d(A + p * kPlaneTile, &tm_w, &full[s], kb * 64, p * a.H_pad + nt * 128);
+          if (it > 0) tma_load_2d(A + p * kPlaneTile, &tm_w, &full[s], kb * 64, p * a.H_pad + nt * 128);
           for (int h = 0; h < a.TT / 64; ++h)
             tma_load_2d(Bt + p * btile + h * 8192, &tm_di, &full[s],
                         b * a.T_pad + tt * a.TT + h * 64, p * a.K_pad + kb * 64);
@@ -2877,6 +2885,43 @@ __device__ __forceinline__ float adam_one(const AdamArgs& a, int64_t i, float g,
   return adam_apply(a, i, g, a.params[i], a.m[i], a.v[i], bc1, bc2);
 }
 
+// Four consecutive elements i0..i0+3 of a W entry of Linear `layer` at (k, n0..n0+3)
+// (i0 and n0 multiples of 4, no f32 transpose target): the same float ops as
+// adam_apply / refresh_planes, with 16-byte parameter / moment / gradient stores and
+// 8-byte plane stores.
+__device__ __forceinline__ void adam4_planes(const AdamArgs& a, float* grads, int layer, int64_t i0, int64_t k,
+                                             int64_t n0, const float (&g)[4], const float (&p0)[4],
+                                             const float (&m0)[4], const float (&v0)[4], float bc1, float bc2) {
+  float p[4], m[4], v[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (a.opt_kind == 1) {  // sgd_update (optimize.hpp:69-84)
+      m[e] = __fadd_rn(__fmul_rn(a.momentum, m0[e]), g[e]);
+      p[e] = __fsub_rn(p0[e], __fmul_rn(a.lr, m[e]));
+      v[e] = v0[e];
+    } else {
+      m[e] = __fadd_rn(__fmul_rn(a.b1, m0[e]), __fmul_rn(a.omb1, g[e]));
+      v[e] = __fadd_rn(__fmul_rn(a.b2, v0[e]), __fmul_rn(__fmul_rn(a.omb2, g[e]), g[e]));
+      const float mhat = __fdiv_rn(m[e], bc1);
+      const float vhat = __fdiv_rn(v[e], bc2);
+      p[e] = __fsub_rn(p0[e], __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps)));
+    }
+  }
+  *reinterpret_cast<float4*>(a.params + i0) = make_float4(p[0], p[1], p[2], p[3]);
+  *reinterpret_cast<float4*>(a.m + i0) = make_float4(m[0], m[1], m[2], m[3]);
+  if (a.opt_kind != 1) *reinterpret_cast<float4*>(a.v + i0) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(grads + i0) = make_float4(g[0], g[1], g[2], g[3]);
+  const PlaneTarget pt = a.planes[layer];
+  if (pt.wb == nullptr) return;
+  uint32_t h[4], mi[4], lo[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) split3_bits(p[e], h[e], mi[e], lo[e]);
+  const int64_t plane = int64_t(pt.K_pad) * pt.N_pad, idx = k * pt.N_pad + n0;
+  *reinterpret_cast<uint2*>(pt.wb + idx) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+  *reinterpret_cast<uint2*>(pt.wb + plane + idx) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
+  *reinterpret_cast<uint2*>(pt.wb + 2 * plane + idx) = make_uint2(lo[0] | (lo[1] << 16), lo[2] | (lo[3] << 16));
+}
+
 // bf16 operand planes of W element (k, n) of Linear `layer` from its f32 master
 // (consecutive n -> consecutive addresses: coalesced).
 __device__ __forceinline__ void refresh_planes(const AdamArgs& a, int layer, int64_t k, int64_t n, float p) {
@@ -3313,7 +3358,7 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
       if (k >= rows_j || n0 >= cols_j) continue;
       const int64_t i0 = tl.w_off[j] + int64_t(k) * cols_j + n0;
       const int nv = min(4, cols_j - n0);
-      float p0[4], m0[4], v0[4];
+      float p0[4] = {0.f, 0.f, 0.f, 0.f}, m0[4] = {0.f, 0.f, 0.f, 0.f}, v0[4] = {0.f, 0.f, 0.f, 0.f};
       const bool pref = c == r0 && g == tid;  // prefetched before the tile wait
 #pragma unroll
       for (int e = 0; e < 4; ++e)
@@ -3347,12 +3392,16 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
       }
       const float gv[4] = {__fadd_rn(acc[0].x, acc[1].x), __fadd_rn(acc[0].y, acc[1].y),
                            __fadd_rn(acc[0].z, acc[1].z), __fadd_rn(acc[0].w, acc[1].w)};
+      if (nv == 4 && (i0 & 3) == 0 && ad.planes[j].wt == nullptr) {
+        adam4_planes(ad, rd.grads, j, i0, k, n0, gv, p0, m0, v0, bc1, bc2);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (e < nv) {
-          rd.grads[i0 + e] = gv[e];
-          refresh_planes(ad, j, k, n0 + e, adam_apply(ad, i0 + e, gv[e], p0[e], m0[e], v0[e], bc1, bc2));
-        }
+        for (int e = 0; e < 4; ++e)
+          if (e < nv) {
+            rd.grads[i0 + e] = gv[e];
+            refresh_planes(ad, j, k, n0 + e, adam_apply(ad, i0 + e, gv[e], p0[e], m0[e], v0[e], bc1, bc2));
+          }
+      }
     }
     bar1(kWgProd);  // the chunk's smem is reloaded next
     if (clk != nullptr && tid == 0 && c == r0) clk[13] = clock64();
