@@ -217,10 +217,14 @@ __device__ __forceinline__ float log_cr(float x) { return float(log(double(x)));
 // buffer [T][33] (one column per lane; stride 33 keeps both the per-step rows
 // written by the projection and the per-class columns read by the scans free
 // of bank conflicts)
-constexpr int kRoStride = 33;
 constexpr int kRoThreads = 256;  // projection: 2 lanes per time step (class groups split)
+// per-(t, class) column buffer row stride: odd (conflict-free for both the projection's
+// rows and the scans' columns) and > C, so column C is a scratch column the scan lanes
+// >= C share
+__host__ __device__ constexpr int readout_row_stride(int C) { return (C + 1) | 1; }
+// W [HL][Cp] | [T][row stride] column buffer (the spike words are read from L2)
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * (HL_pad / 32) + size_t(T) * kRoStride) * 4;
+  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * readout_row_stride(C)) * 4;
 }
 
 // (Running the readout in the tail of the fused forward launch, one group of warps
@@ -231,9 +235,11 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   const int C = a.C, T = a.T;
   const int hw = a.HL_pad / 32;
   const int Cp = (C + 3) & ~3;
-  float* w = rsm;                                                      // [HL][Cp]
-  uint32_t* spk = reinterpret_cast<uint32_t*>(w + size_t(a.HL) * Cp);  // [T][hw]
-  float* buf = reinterpret_cast<float*>(spk + size_t(T) * hw);         // [T][kRoStride]
+  const int rs = readout_row_stride(C);
+  float* w = rsm;                       // [HL][Cp]
+  float* buf = w + size_t(a.HL) * Cp;   // [T][rs]
+  // the spike words of this sample (written by the forward kernel; read from L2)
+  const uint32_t* spk = a.s_in + size_t(blockIdx.x) * a.T_pad * hw;
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int G = kRoThreads;
 #define RO_CLK(k) if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + (k)] = clock64();
@@ -257,11 +263,6 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
   __shared__ int s_label[1];
   if (tid == 0) *s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
-  {
-    // the spike words of this sample (written by the forward kernel)
-    const uint4* ss = reinterpret_cast<const uint4*>(a.s_in + size_t(b) * a.T_pad * hw);
-    for (int i = tid; i < T * hw / 4; i += G) reinterpret_cast<uint4*>(spk)[i] = __ldg(ss + i);
-  }
   __syncthreads();
   RO_CLK(1)
   // projection (ops.hpp:163-172 order: ascending k, zero skip): a lane pair per
@@ -278,11 +279,11 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     for (int jj = 0; jj < kGroups; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0.0f;
     const uint32_t* words = spk + t * hw;
     int wi = 0;
-    uint32_t bits = words[0];
+    uint32_t bits = __ldg(words);
     auto next_k = [&]() -> int {
       while (bits == 0u) {
         if (++wi >= hw) return -1;
-        bits = words[wi];
+        bits = __ldg(words + wi);
       }
       const int i = __ffs(bits) - 1;
       bits &= bits - 1u;
@@ -324,13 +325,13 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
         const int c = 4 * (2 * jj + h) + e;
         float vout = 0.0f;
         if (c < C) vout = a.bias != nullptr ? __fadd_rn(acc[jj][e], a.bias[c]) : acc[jj][e];
-        buf[t * kRoStride + c] = vout;  // c < 32: classes >= C are zero
+        if (c < rs) buf[t * rs + c] = vout;  // classes >= C (the scratch column) are zero
       }
   }
   __syncthreads();
   RO_CLK(2)
   if (warp == 0) {
-    float* col = buf + lane;
+    float* col = buf + (lane < C ? lane : C);  // lanes >= C share the scratch column
     const float vb = lane < C ? clip01(beta_l) : 0.0f;
     // LI scan (neuron.hpp:139-144) + time_sum (objective.hpp:40-50); col[t] <- V3_t
     float v = 0.0f, logit = 0.0f;
@@ -340,8 +341,8 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
       // logits its time sums (network.hpp:396, objective.hpp:40-50)
       const float ntheta = -a.theta;
       for (; t < T; ++t) {
-        const float I = col[t * kRoStride];
-        col[t * kRoStride] = v;
+        const float I = col[t * rs];
+        col[t * rs] = v;
         const bool sp = __fadd_rn(v, ntheta) >= 0.0f;
         v = __fsub_rn(__fadd_rn(__fmul_rn(v, vb), I), sp ? a.theta : 0.0f);
         logit = __fadd_rn(logit, sp ? 1.0f : 0.0f);
@@ -350,17 +351,17 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     for (; t + 8 <= T; t += 8) {
       float I[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * kRoStride];
+      for (int e = 0; e < 8; ++e) I[e] = col[(t + e) * rs];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        col[(t + e) * kRoStride] = v;
+        col[(t + e) * rs] = v;
         v = __fadd_rn(__fmul_rn(v, vb), I[e]);
         logit = __fadd_rn(logit, v);
       }
     }
     for (; t < T; ++t) {
-      const float I = col[t * kRoStride];
-      col[t * kRoStride] = v;
+      const float I = col[t * rs];
+      col[t * rs] = v;
       v = __fadd_rn(__fmul_rn(v, vb), I);
       logit = __fadd_rn(logit, v);
     }
@@ -420,8 +421,8 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     if (a.dbg_trace != nullptr && lane < C) {
       for (int s = 0; s < T; ++s)
         a.dbg_trace[(size_t(b) * T + s) * C + lane] =
-            a.readout_lif ? (__fadd_rn(col[s * kRoStride], -a.theta) >= 0.0f ? 1.0f : 0.0f)
-                          : s + 1 < T ? col[(s + 1) * kRoStride] : v_final;
+            a.readout_lif ? (__fadd_rn(col[s * rs], -a.theta) >= 0.0f ? 1.0f : 0.0f)
+                          : s + 1 < T ? col[(s + 1) * rs] : v_final;
     }
     RO_CLK(4)
     float G = delta, db = 0.0f, dbias = 0.0f;
@@ -430,43 +431,43 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
       // every step: dI3_t = G ; G = G bc + (delta + (-G) theta) g(V3_t - theta)
       G = 0.0f;
       for (t = T - 1; t >= 0; --t) {
-        const float V3 = col[t * kRoStride];
+        const float V3 = col[t * rs];
         const float gi = G;
         const float gs = __fadd_rn(delta, __fmul_rn(-gi, a.theta));
         const float g = surrogate_rt(a.act, a.slope, a.aux, __fadd_rn(V3, -a.theta));
         G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
         db = __fadd_rn(db, __fmul_rn(gi, V3));
         dbias = __fadd_rn(dbias, gi);
-        col[t * kRoStride] = gi;
+        col[t * rs] = gi;
       }
     } else {
     // LI reverse scan: G_t = delta + G_{t+1} bc ; dI3_t = G_t ; dbeta += G_t V3_t
     t = T - 1;
     {
-      const float V3 = col[t * kRoStride];
+      const float V3 = col[t * rs];
       db = __fmul_rn(G, V3);
       dbias = G;
-      col[t * kRoStride] = G;
+      col[t * rs] = G;
     }
     --t;
     for (; t >= 7; t -= 8) {
       float V3[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * kRoStride];
+      for (int e = 0; e < 8; ++e) V3[e] = col[(t - e) * rs];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         G = __fadd_rn(delta, __fmul_rn(G, vb));
         db = __fadd_rn(db, __fmul_rn(G, V3[e]));
         dbias = __fadd_rn(dbias, G);
-        col[(t - e) * kRoStride] = G;
+        col[(t - e) * rs] = G;
       }
     }
     for (; t >= 0; --t) {
-      const float V3 = col[t * kRoStride];
+      const float V3 = col[t * rs];
       G = __fadd_rn(delta, __fmul_rn(G, vb));
       db = __fadd_rn(db, __fmul_rn(G, V3));
       dbias = __fadd_rn(dbias, G);
-      col[t * kRoStride] = G;
+      col[t * rs] = G;
     }
     }
     if (lane < C) {
@@ -487,8 +488,8 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
     uint32_t hp[4], mp[4], lp[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const float g0 = t0 + e < T ? buf[(t0 + e) * kRoStride + c] : 0.0f;
-      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * kRoStride + c] : 0.0f;
+      const float g0 = t0 + e < T ? buf[(t0 + e) * rs + c] : 0.0f;
+      const float g1 = t0 + e + 1 < T ? buf[(t0 + e + 1) * rs + c] : 0.0f;
       split3_pack(g0, g1, hp[e / 2], mp[e / 2], lp[e / 2]);
     }
     const size_t off = size_t(c) * cols + size_t(b) * a.T_pad + t0;
