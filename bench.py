@@ -466,6 +466,11 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        # hold the stream with a ~25 ms device spin so the start event fires only after
+        # the whole timed region is enqueued: host-side stalls (GIL hand-off to the
+        # sampler thread) stay out of the device-timed region
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(50_000_000)
         t_start.record(stream)
         eng.enqueue_steps(warmup, args.steps)
         clocks.mark()                      # the enqueued steps are running now

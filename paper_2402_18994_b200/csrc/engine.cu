@@ -486,6 +486,8 @@ struct snn_engine {
     if (n.activation == SNN_ACT_BOXCAR && !(n.aux > 0.0f))
       fail(SNN_ERR_ARGUMENT, "boxcar: width and height must be positive");
     if (cfg.batch_size < 1) fail(SNN_ERR_ARGUMENT, "train: batch size 0");
+    if (cfg.batch_size > 65535)  // one grid dimension carries the samples
+      fail(SNN_ERR_UNSUPPORTED, "batch size per rank above 65535 (split it over ranks or steps)");
     if (cfg.time_steps < 1) fail(SNN_ERR_ARGUMENT, "apply: zero timesteps");
     if (cfg.unroll < 1) fail(SNN_ERR_ARGUMENT, "apply: unroll must be >= 1");
     if (cfg.optimizer != 0 && cfg.optimizer != 1) fail(SNN_ERR_ARGUMENT, "train_step: unknown optimizer");
@@ -1487,7 +1489,7 @@ struct snn_engine {
       auto kfn = rlif(l) ? (shifting ? k_lif_fwd<true, false, true> : k_lif_fwd<false, false, true>)
                  : any_alif ? (shifting ? k_lif_fwd<true, true> : k_lif_fwd<false, true>)
                             : (shifting ? k_lif_fwd<true> : k_lif_fwd<false>);
-      launch(kfn, dim3((B + f.spb - 1) / f.spb, H_pad[l] / 128),
+      launch(kfn, dim3(H_pad[l] / 128, (B + f.spb - 1) / f.spb),
              dim3(kFwdThreads),
              fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
       mark(evs, "lif_fwd", l);
@@ -1553,14 +1555,14 @@ struct snn_engine {
       if (rlif(l)) {  // declared RLIF: dS on tcgen05, then the recurrent reverse scan
         bw.ds_out = dsbuf[l].p;
         launch(bw.hist != nullptr ? k_lif_bwd<0, true, false, true> : k_lif_bwd<0, false, false, true>,
-               dim3(B, H_pad[l] / 128), dim3(kBwdThreads), bwd_smem_bytes(TT, bw.stages), tm_wb[l + 1],
+               dim3(H_pad[l] / 128, B), dim3(kBwdThreads), bwd_smem_bytes(TT, bw.stages), tm_wb[l + 1],
                tm_di_k[l + 1], tm_di_out[l], bw);
         mark(evs, "ds", l);
         launch_rlif_bwd(l);
         mark(evs, "rlif_bwd", l);
         continue;
       }
-      launch_bwd(net.activation, dim3(B, H_pad[l] / 128), bwd_smem_bytes(TT, bw.stages, alif(l)),
+      launch_bwd(net.activation, dim3(H_pad[l] / 128, B), bwd_smem_bytes(TT, bw.stages, alif(l)),
                  tm_wb[l + 1], tm_di_k[l + 1], tm_di_out[l], bw);
       mark(evs, "lif_bwd", l);
     }
@@ -1779,6 +1781,8 @@ struct snn_engine {
     cudaGraphExec_t ex;
     CK(cudaGraphInstantiate(&ex, g, 0));
     CK(cudaGraphDestroy(g));
+    // upload now: a first launch would otherwise upload inside the caller's (timed) stream work
+    CK(cudaGraphUpload(ex, stream));
     graphs[key] = ex;
     return ex;
   }

@@ -686,9 +686,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b0 = blockIdx.x * SPB, nt = blockIdx.y;
+  // grid (H_pad / 128, sample groups): a sample group's neuron tiles run together
+  const int sg = blockIdx.y, b0 = sg * SPB, nt = blockIdx.x;
   const int nsamp = min(SPB, a.B - b0);
-  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * kClkStride : nullptr;
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(nt) * gridDim.y + sg) * kClkStride : nullptr;
   if (clk != nullptr && threadIdx.x == 0) {
     clk[0] = clock64();
     clk[6] = globaltimer();
@@ -699,7 +700,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int KB = K_pad0 / 64;
   const int total = a.NT * KB;
   // k-block order rotated per CTA: concurrent CTAs stream different W tiles
-  const int rot = int(blockIdx.x) % KB;
+  const int rot = sg % KB;
   const uint32_t tmem_cols = tmem_cols_for(NTOT, a.NT);
   const int nbuf = a.NT > 1 ? 2 : 1;
   const int scan_threads = 128 * nsamp;
@@ -1263,8 +1264,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   float* xG = xB + kBwdScanThreads;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x, nt = blockIdx.y;
-  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(blockIdx.y) * gridDim.x + b) * kClkStride : nullptr;
+  // grid (H_pad / 128, B): the neuron tiles of one sample are adjacent in launch
+  // order, so the sample's dI planes come from HBM once and from L2 for the others
+  const int b = blockIdx.y, nt = blockIdx.x;
+  long long* clk = a.dbg_clk != nullptr ? a.dbg_clk + (size_t(nt) * a.B + b) * kClkStride : nullptr;
   if (clk != nullptr && threadIdx.x == 0) clk[0] = clock64();
   const int KB = a.K_pad / 64;
   const int total = a.NT * KB;

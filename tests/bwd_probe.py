@@ -10,7 +10,7 @@ from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec  # noqa: E402
 w = WORKLOADS[os.environ.get("PROBE_CFG", "c3w")]
 B = int(os.environ.get("PROBE_B", str(w["B"])))
 eng = Engine(shd_spec(hidden=w["hidden"], classes=w["classes"], inp=w["inp"], act=w["act"]),
-             TrainConfig(batch_size=B, seed=0), w["T"])
+             TrainConfig(batch_size=B, seed=0, gemm_planes=int(os.environ.get("PROBE_PLANES", "3"))), w["T"])
 eng.synth_dataset(2 * B, seed=1)
 rows = np.arange(B, dtype=np.uint32)
 for _ in range(20):
