@@ -761,8 +761,8 @@ struct snn_engine {
                             int(kWgSmemLaunch)));
     CK(cudaFuncSetAttribute(k_wgrad<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(kWgSmemLaunch)));
-    CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(200 * 1024)));
+    for (auto fn : {k_readout<1>, k_readout<2>, k_readout<3>, k_readout<4>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(200 * 1024)));
     {
       std::vector<int32_t> vi;
       for (const auto& en : entries)
@@ -1519,7 +1519,9 @@ struct snn_engine {
     {
       const ReadoutArgs r = ro_args;
       const size_t smem = readout_smem_bytes(H[L - 1], H_pad[L - 1], T, C);
-      launch(k_readout, dim3(B), dim3(kRoThreads), smem, r);
+      const int ng = readout_groups(C);
+      launch(ng == 1 ? k_readout<1> : ng == 2 ? k_readout<2> : ng == 3 ? k_readout<3> : k_readout<4>,
+             dim3(B), dim3(kRoThreads), smem, r);
       mark(evs, "readout", -1);
     }
     if (update >= kEval) return;  // evaluation: forward + readout only (apply, cmd_eval)

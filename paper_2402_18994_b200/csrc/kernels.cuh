@@ -222,19 +222,24 @@ constexpr int kRoThreads = 256;  // projection: 2 lanes per time step (class gro
 // rows and the scans' columns) and > C, so column C is a scratch column the scan lanes
 // >= C share
 __host__ __device__ constexpr int readout_row_stride(int C) { return (C + 1) | 1; }
-// W [HL][Cp] | [T][row stride] column buffer (the spike words are read from L2)
+// 4-class groups per lane of the projection's lane pair (template parameter of k_readout)
+__host__ __device__ constexpr int readout_groups(int C) { return (C + 7) / 8; }
+// W [HL][Cp] (Cp = 8 * groups: rows zero-padded so every lane adds whole float4 groups)
+// | [T][row stride] column buffer (the spike words are read from L2)
 __host__ __device__ inline size_t readout_smem_bytes(int HL, int HL_pad, int T, int C) {
-  return (size_t(HL) * ((C + 3) & ~3) + size_t(T) * readout_row_stride(C)) * 4;
+  return (size_t(HL) * 8 * readout_groups(C) + size_t(T) * readout_row_stride(C)) * 4;
 }
 
 // (Running the readout in the tail of the fused forward launch, one group of warps
 // per sample, was measured slower: the forward's 448-thread register budget slowed
 // every readout phase 1.2-8x.)
+// kNG = readout_groups(C): each lane of a pair owns kNG 4-class groups
+template <int kNG>
 __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   extern __shared__ float rsm[];
   const int C = a.C, T = a.T;
   const int hw = a.HL_pad / 32;
-  const int Cp = (C + 3) & ~3;
+  constexpr int Cp = 8 * kNG;
   const int rs = readout_row_stride(C);
   float* w = rsm;                       // [HL][Cp]
   float* buf = w + size_t(a.HL) * Cp;   // [T][rs]
@@ -261,69 +266,82 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
   pdl_wait();
   RO_CLK(0)
   if (a.dbg_clk != nullptr && tid == 0) a.dbg_clk[b * kClkStride + 14] = globaltimer();
+  // the first spike-word chunk of this thread's first step, in flight across the label
+  // load (hw = HL_pad / 32 is a multiple of 4: whole 16-byte chunks)
+  const uint4 pre = (tid >> 1) < T ? __ldg(reinterpret_cast<const uint4*>(spk + (tid >> 1) * hw))
+                                   : make_uint4(0u, 0u, 0u, 0u);
   __shared__ int s_label[1];
   if (tid == 0) *s_label = a.labels[batch_rows(a.rows, a.rows_slot, a.B)[b]];
   __syncthreads();
   RO_CLK(1)
   // projection (ops.hpp:163-172 order: ascending k, zero skip): a lane pair per
   // time step, lane h of the pair owning the 4-class groups j = 2jj + h (acc in
-  // registers; the pair walks the same spike bits).  W rows live in smem padded to
-  // Cp = C rounded up to 4 floats; the row of the next spike is loaded while the
-  // current one is added, so a burst of spikes costs the add chain, not one smem
-  // round trip per spike.
-  constexpr int kGroups = kMaxClasses / 8;  // 4-class groups per lane
+  // registers; the pair walks the same spike bits).  W rows live in smem zero-padded
+  // to Cp = 8 kNG floats, so every lane adds whole groups with no per-class
+  // predicates (the padded classes' sums are never stored); the row of the next
+  // spike is loaded while the current one is added (two rows per trip, no register
+  // moves), so a burst of spikes costs the add chain, not one smem round trip each.
+  constexpr int kGroups = kNG;
   const int h = tid & 1;
   for (int t = tid >> 1; t < T; t += G / 2) {
     float acc[kGroups][4];
 #pragma unroll
     for (int jj = 0; jj < kGroups; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0.0f;
-    const uint32_t* words = spk + t * hw;
-    int wi = 0;
-    uint32_t bits = __ldg(words);
+    // the step's spike words in 16-byte chunks, the next chunk in flight while the
+    // current one is walked: one L2 round trip per step, not one per word
+    const uint4* words = reinterpret_cast<const uint4*>(spk + t * hw);
+    const int nq = hw >> 2;
+    uint4 cw = t == (tid >> 1) ? pre : __ldg(words);
+    uint4 nw = nq > 1 ? __ldg(words + 1) : make_uint4(0u, 0u, 0u, 0u);
+    int wi = 0;  // word index: chunk wi >> 2, word wi & 3 of it
+    uint32_t bits = cw.x;
     auto next_k = [&]() -> int {
       while (bits == 0u) {
         if (++wi >= hw) return -1;
-        bits = __ldg(words + wi);
+        const int sub = wi & 3;
+        if (sub == 0) {
+          cw = nw;
+          if ((wi >> 2) + 1 < nq) nw = __ldg(words + (wi >> 2) + 1);
+        }
+        bits = sub == 0 ? cw.x : sub == 1 ? cw.y : sub == 2 ? cw.z : cw.w;
       }
       const int i = __ffs(bits) - 1;
       bits &= bits - 1u;
       return wi * 32 + i;
     };
-    float4 cur[kGroups];
-    int k = next_k();
-    if (k >= 0) {
-      const float4* wr = reinterpret_cast<const float4*>(w + k * Cp) + h;
+    const float4* wbase = reinterpret_cast<const float4*>(w) + h;
+    auto load_row = [&](int k, float4 (&r)[kGroups]) {
+      const float4* wr = wbase + k * (Cp / 4);
 #pragma unroll
-      for (int jj = 0; jj < kGroups; ++jj)
-        if (4 * (2 * jj + h) < C) cur[jj] = wr[2 * jj];
-    }
-    while (k >= 0) {
-      const int kn = next_k();
-      float4 nxt[kGroups];
-      if (kn >= 0) {
-        const float4* wr = reinterpret_cast<const float4*>(w + kn * Cp) + h;
-#pragma unroll
-        for (int jj = 0; jj < kGroups; ++jj)
-          if (4 * (2 * jj + h) < C) nxt[jj] = wr[2 * jj];
-      }
+      for (int jj = 0; jj < kGroups; ++jj) r[jj] = wr[2 * jj];
+    };
+    auto add_row = [&](const float4 (&r)[kGroups]) {
 #pragma unroll
       for (int jj = 0; jj < kGroups; ++jj) {
-        const int c0 = 4 * (2 * jj + h);
-        if (c0 + 0 < C) acc[jj][0] = __fadd_rn(acc[jj][0], cur[jj].x);
-        if (c0 + 1 < C) acc[jj][1] = __fadd_rn(acc[jj][1], cur[jj].y);
-        if (c0 + 2 < C) acc[jj][2] = __fadd_rn(acc[jj][2], cur[jj].z);
-        if (c0 + 3 < C) acc[jj][3] = __fadd_rn(acc[jj][3], cur[jj].w);
+        acc[jj][0] = __fadd_rn(acc[jj][0], r[jj].x);
+        acc[jj][1] = __fadd_rn(acc[jj][1], r[jj].y);
+        acc[jj][2] = __fadd_rn(acc[jj][2], r[jj].z);
+        acc[jj][3] = __fadd_rn(acc[jj][3], r[jj].w);
       }
-#pragma unroll
-      for (int jj = 0; jj < kGroups; ++jj) cur[jj] = nxt[jj];
-      k = kn;
+    };
+    float4 ra[kGroups], rb[kGroups];
+    int k = next_k();
+    if (k >= 0) load_row(k, ra);
+    while (k >= 0) {
+      const int k1 = next_k();
+      if (k1 >= 0) load_row(k1, rb);
+      add_row(ra);
+      if (k1 < 0) break;
+      k = next_k();
+      if (k >= 0) load_row(k, ra);
+      add_row(rb);
     }
 #pragma unroll
     for (int jj = 0; jj < kGroups; ++jj)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int c = 4 * (2 * jj + h) + e;
-        float vout = 0.0f;
+        float vout = 0.0f;  // (classes >= C: padded W columns, sums discarded)
         if (c < C) vout = a.bias != nullptr ? __fadd_rn(acc[jj][e], a.bias[c]) : acc[jj][e];
         if (c < rs) buf[t * rs + c] = vout;  // classes >= C (the scratch column) are zero
       }

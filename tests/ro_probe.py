@@ -33,3 +33,12 @@ eng.sync()
 s1 = eng.fetch("spikes", 1)
 per = s1.sum(axis=(1, 2))
 print("layer-1 spikes per sample: median", int(np.median(per)), "max", int(per.max()), "rate", s1.mean())
+# per-step spike counts: a warp of the projection walks 16 steps, its loop runs the
+# max over them; a CTA's projection phase is its slowest warp
+cnt = s1.sum(axis=2)  # [B, T]
+T = cnt.shape[1]
+wmax = cnt[:, :T - T % 16].reshape(B, -1, 16).max(axis=2)
+print("per-step spikes: mean", cnt.mean(), "max", cnt.max(), "| per-warp max: median",
+      np.median(wmax), "| per-CTA max warp-max: median", np.median(wmax.max(1)))
+print("corr(projection cycles, CTA max warp-max)", np.corrcoef(d[:, 1], wmax.max(1))[0, 1],
+      "cycles per warp-max spike", np.median(d[:, 1] / np.maximum(wmax.max(1), 1)))
