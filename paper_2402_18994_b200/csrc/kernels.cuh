@@ -3231,10 +3231,9 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 }
 
 // the fused tail's batch reductions that need no weight gradient: beta / bias /
-// gamma entries (one warp per element, spread over the CTAs) and, in block 0, the
-// loss / hits / regularizer (StepResult); scratch: 8 KB of free shared memory
-__device__ __forceinline__ void wgrad_vec_and_loss(const ReduceArgs& rd, const AdamArgs& ad, float bc1,
-                                                   float bc2, uint8_t* scratch_smem, long long* clk) {
+// gamma entries (one warp per element, spread over the CTAs)
+__device__ __forceinline__ void wgrad_vec(const ReduceArgs& rd, const AdamArgs& ad, float bc1, float bc2,
+                                          long long* clk) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (clk != nullptr && tid == 0) clk[10] = clock64();
   // 4. beta / bias / gamma entries: one warp per element, spread over the CTAs
@@ -3271,7 +3270,12 @@ __device__ __forceinline__ void wgrad_vec_and_loss(const ReduceArgs& rd, const A
     }
   }
   if (clk != nullptr && tid == 0) clk[11] = clock64();
-  // 5. block 0: loss sum in batch order (objective.hpp:57-72) + hits -> StepResult
+}
+
+// block 0: loss sum in batch order (objective.hpp:57-72) + hits + regularizer ->
+// StepResult; scratch: 8 KB of free shared memory
+__device__ __forceinline__ void wgrad_loss(const ReduceArgs& rd, const AdamArgs& ad, uint8_t* scratch_smem) {
+  const int tid = threadIdx.x;
   if (blockIdx.x == 0) {
     uint32_t* scratch = reinterpret_cast<uint32_t*>(scratch_smem);
     bar1(kWgProd);
@@ -3342,14 +3346,18 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
   }
   const float bc1 = ad.bc[2 * s], bc2 = ad.bc[2 * s + 1];
   // while the stores drain and the tile's other splits finish: the work that does
-  // not depend on the weight gradients (beta / bias / gamma, loss / StepResult)
-  wgrad_vec_and_loss(rd, ad, bc1, bc2, smem + size_t(nm) * ncg * 16384, clk);
+  // not depend on the weight gradients (beta / bias / gamma, then block 0's loss /
+  // StepResult -- after this CTA's arrival, so the tile's other splits never wait on it)
+  wgrad_vec(rd, ad, bc1, bc2, clk);
   if (tid == 0) {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (clk != nullptr) clk[8] = clock64();
     fence_proxy_async_global();
     __threadfence();
     atomicAdd(tl.tile_cnt + tile, 1u);
+  }
+  wgrad_loss(rd, ad, smem + size_t(nm) * ncg * 16384);
+  if (tid == 0) {
     while (ld_acquire_gpu_u32(tl.tile_cnt + tile) < unsigned(S)) __nanosleep(32);
     fence_proxy_async_global();  // the bulk loads below see the other splits' partials
     if (clk != nullptr) clk[9] = clock64();

@@ -30,3 +30,15 @@ print(f"  start spread {(gt[:, 0].max() - t0) / 1e3:.1f} us, end {(gt[:, 1].min(
 for blk in (0, 52, 53, 105, 106, 126, 127, len(c) - 1):
     if blk < len(c):
         print("  cta", blk, d[blk].tolist(), f"start {(gt[blk, 0] - t0) / 1e3:.1f} us")
+if os.environ.get("PROBE_ALL"):
+    tot = c[:, 13] - c[:, 0]
+    for blk in range(len(c)):
+        print(f"  {blk:3d} loop {d[blk, 2]:6d} epi {int(c[blk, 13] - c[blk, 4]):6d} total {int(tot[blk]):6d} "
+              f"end {(gt[blk, 1] - t0) / 1e3:5.1f} us")
+if os.environ.get("PROBE_ALL"):
+    # absolute arrival on the tile counter (globaltimer start + clock64 delta at ~1.965 GHz)
+    arr = (gt[:, 0] - t0) / 1e3 + (c[:, 8] - c[:, 0]) / 1965.0
+    for lo, hi in ((0, 54), (54, 108), (108, 129), (129, len(c))):
+        o = np.argsort(arr[lo:hi])[::-1][:4] + lo
+        print(f"  CTAs [{lo},{hi}) latest arrivals", [(int(i), round(float(arr[i]), 1)) for i in o],
+              "median", round(float(np.median(arr[lo:hi])), 1))
