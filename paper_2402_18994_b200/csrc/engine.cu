@@ -222,9 +222,11 @@ struct EntryHost {
 };
 
 struct Dataset {
-  DevBuf<uint8_t> x;       // [n][T_pad/8][IN_pad]
+  DevBuf<uint8_t> x;       // [n][T_pad/8][row]
   DevBuf<int32_t> labels;  // [n]
   size_t n = 0;
+  int row = 0;             // bytes per packed time row: IN_pad (staged), or IN for a host
+                           // batch kept in the reference layout (Engine::raw_layout_ok); 0 = IN_pad
 };
 
 // Host memcpy split over a few persistent worker threads (the caller takes part).
@@ -359,6 +361,14 @@ struct snn_engine {
   int n_vec = 0;
   DevBuf<float> result_loss;
   DevBuf<double> result_acc;
+  // StepResult ring in mapped pinned memory, written by the one-rank fused tail at
+  // entry (step & (kRing - 1)): host-batch calls read it after their sync
+  static constexpr int64_t kRing = 4096;
+  float* ring_loss_h = nullptr;
+  double* ring_acc_h = nullptr;
+  float* ring_loss_d = nullptr;
+  double* ring_acc_d = nullptr;
+  bool ring_on() const { return tail_mode == 0 && fused_tail(); }
   float* h_loss = nullptr;
   double* h_acc = nullptr;
   uint32_t* h_rows = nullptr;
@@ -435,6 +445,8 @@ struct snn_engine {
     if (plab_host) cudaFreeHost(plab_host);
     if (pres_loss) cudaFreeHost(pres_loss);
     if (pres_acc) cudaFreeHost(pres_acc);
+    if (ring_loss_h) cudaFreeHost(ring_loss_h);
+    if (ring_acc_h) cudaFreeHost(ring_acc_h);
     for (int s = 0; s < 2; ++s) {
       if (ev_ready[s]) cudaEventDestroy(ev_ready[s]);
       if (ev_used[s]) cudaEventDestroy(ev_used[s]);
@@ -700,6 +712,12 @@ struct snn_engine {
     correct_b.alloc(B);
     result_loss.alloc(1);
     result_acc.alloc(1);
+    if (!ring_loss_h) {
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&ring_loss_h), sizeof(float) * kRing, cudaHostAllocMapped));
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&ring_acc_h), sizeof(double) * kRing, cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ring_loss_d), ring_loss_h, 0));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ring_acc_d), ring_acc_h, 0));
+    }
     rows_cur.alloc(B);
     xshift.alloc(1);
     CK(cudaMallocHost(&h_loss, sizeof(float)));
@@ -727,7 +745,7 @@ struct snn_engine {
     for (auto fn : {k_lif_fwd<false>, k_lif_fwd<true>, k_lif_fwd<false, true>, k_lif_fwd<true, true>,
                     k_lif_fwd<false, false, true>, k_lif_fwd<true, false, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(fwd_smem_bytes(TT, kFwdSpbMax, kFwdStagesMax, IN_pad))));
+                              227 * 1024));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>, k_lif_bwd<5>,
                     k_lif_bwd<0, true>, k_lif_bwd<1, true>, k_lif_bwd<2, true>, k_lif_bwd<3, true>,
                     k_lif_bwd<4, true>, k_lif_bwd<5, true>})
@@ -895,6 +913,9 @@ struct snn_engine {
     a.n_mon = int(mon_layers.size());
     a.loss_out = result_loss.p;
     a.acc_out = result_acc.p;
+    a.ring_loss = ring_loss_d;
+    a.ring_acc = ring_acc_d;
+    a.ring_mask = kRing - 1;
     return a;
   }
 
@@ -963,13 +984,16 @@ struct snn_engine {
       CK(cudaMallocHost(&pinned, lab_off + n * sizeof(int32_t)));
       pinned_bytes = lab_off + n * sizeof(int32_t);
     }
-    if (raw_in.n < raw) raw_in.alloc(raw, false);
+    const bool in_place = raw_layout_ok();
+    if (!in_place && raw_in.n < raw) raw_in.alloc(raw, false);
     if (ds.n != n) {
       ds.x.alloc(n * size_t(tp8_pad) * IN_pad, false);
       ds.labels.alloc(n, false);
       ds.n = n;
       clear_graphs();
     }
+    ds.row = in_place ? IN : IN_pad;
+    uint8_t* dst = in_place ? ds.x.p : raw_in.p;
     uint8_t* h = static_cast<uint8_t*>(pinned);
     // a caller batch that already lives in pinned (page-locked) memory is DMA'd as is
     cudaPointerAttributes pa{};
@@ -977,7 +1001,7 @@ struct snn_engine {
                                pa.type == cudaMemoryTypeHost;
     if (!caller_pinned) cudaGetLastError();  // clear a pageable-pointer query error
     if (caller_pinned) {
-      CK(cudaMemcpyAsync(raw_in.p, packed, raw, cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(dst, packed, raw, cudaMemcpyHostToDevice, stream));
     } else {
       if (!copy_pool) {  // created on the first pageable batch
         const unsigned hc = std::thread::hardware_concurrency();
@@ -990,17 +1014,26 @@ struct snn_engine {
       for (size_t off = 0; off < raw; off += per) {
         const size_t len = std::min(per, raw - off);
         copy_pool->copy(h + off, packed + off, len);
-        CK(cudaMemcpyAsync(raw_in.p + off, h + off, len, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(dst + off, h + off, len, cudaMemcpyHostToDevice, stream));
       }
     }
     int32_t* lab = reinterpret_cast<int32_t*>(h + lab_off);
     for (size_t i = 0; i < n; ++i) lab[i] = int32_t(labels[i]);
     CK(cudaMemcpyAsync(ds.labels.p, lab, n * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
-    const size_t out = n * size_t(tp8_pad) * IN_pad;
-    k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, stream>>>(raw_in.p, ds.x.p, int64_t(n), tp8,
-                                                                   tp8_pad, IN, IN_pad);
-    CK(cudaGetLastError());
+    if (!in_place) {
+      const size_t out = n * size_t(tp8_pad) * IN_pad;
+      k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, stream>>>(raw_in.p, ds.x.p, int64_t(n), tp8,
+                                                                     tp8_pad, IN, IN_pad);
+      CK(cudaGetLastError());
+    }
   }
+
+  // A host batch in the reference layout [n][ceil(T/8)][IN] is used in place (no
+  // k_relayout) when it already has the device's time extent and its rows suit the
+  // kernels' bulk copies / 4-byte decoder loads; features >= IN of the last 64-k
+  // block are masked in the decoders.
+  bool raw_layout_ok() const { return (T + 7) / 8 == T_pad / 8 && IN % 4 == 0; }
+  int row_of(const Dataset& ds) const { return ds.row > 0 ? ds.row : IN_pad; }
 
   // Pipelined host batches (snn_train_steps_packed): two device slots; a copy stream
   // DMAs batch k+1 (pinned caller memory) and re-lays it out while the step graph of
@@ -1021,8 +1054,9 @@ struct snn_engine {
       for (int s = 0; s < 2; ++s) {
         CK(cudaEventCreateWithFlags(&ev_ready[s], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_used[s], cudaEventDisableTiming));
-        praw[s].alloc(size_t(B) * tp8 * IN, false);
+        if (!raw_layout_ok()) praw[s].alloc(size_t(B) * tp8 * IN, false);
         pslot[s].x.alloc(size_t(B) * tp8_pad * IN_pad, false);
+        pslot[s].row = raw_layout_ok() ? IN : IN_pad;
         pslot[s].labels.alloc(size_t(B), false);
         pslot[s].n = size_t(B);
         CK(cudaEventRecord(ev_used[s], stream));
@@ -1053,20 +1087,24 @@ struct snn_engine {
     CK(cudaStreamWaitEvent(cstream, ev_used[sl], 0));
     // the batch in 4 DMA pieces (measured ~5 % faster end to end than one copy)
     static const int pipe_exp = env_int("SNN_PIPE_EXP", 1) - 1;  // timing experiment: 1 = no batch H2D
+    const bool in_place = raw_layout_ok();  // the DMA lands in the slot itself
+    uint8_t* dst = in_place ? pslot[sl].x.p : praw[sl].p;
     if (pipe_exp != 1) {
       const size_t per = ((raw + 3) / 4 + 15) & ~size_t(15);
       for (size_t off = 0; off < raw; off += per)
-        CK(cudaMemcpyAsync(praw[sl].p + off, packed + k * raw + off, std::min(per, raw - off),
+        CK(cudaMemcpyAsync(dst + off, packed + k * raw + off, std::min(per, raw - off),
                            cudaMemcpyHostToDevice, cstream));
     }
     // labels from the call's pinned copy (filled and checked up front): no host wait
     CK(cudaMemcpyAsync(pslot[sl].labels.p, plab_host + k * size_t(B), sizeof(int32_t) * B,
                        cudaMemcpyHostToDevice, cstream));
-    // re-layout on the copy stream too: it overlaps the previous step's graph
-    const size_t out = size_t(B) * tp8_pad * IN_pad;
-    k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, cstream>>>(praw[sl].p, pslot[sl].x.p, int64_t(B), tp8,
-                                                                     tp8_pad, IN, IN_pad);
-    CK(cudaGetLastError());
+    // otherwise re-laid out on the copy stream too: it overlaps the previous step's graph
+    if (!in_place) {
+      const size_t out = size_t(B) * tp8_pad * IN_pad;
+      k_relayout<<<unsigned((out / 4 + 255) / 256), 256, 0, cstream>>>(praw[sl].p, pslot[sl].x.p, int64_t(B),
+                                                                       tp8, tp8_pad, IN, IN_pad);
+      CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(ev_ready[sl], cstream));
   }
 
@@ -1456,6 +1494,7 @@ struct snn_engine {
       f.planes = planes;
       FwdMaps fm{};
       f.x = ds.x.p;
+      f.x_row = row_of(ds);
       f.rows = rows_p;
       f.rows_slot = slot_p;
       f.s_in = l > 0 ? s_np[l - 1].p : nullptr;
@@ -1491,7 +1530,7 @@ struct snn_engine {
                             : (shifting ? k_lif_fwd<true> : k_lif_fwd<false>);
       launch(kfn, dim3(H_pad[l] / 128, (B + f.spb - 1) / f.spb),
              dim3(kFwdThreads),
-             fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0), fm, f);
+             fwd_smem_bytes(TT, f.spb, f.stages, l == 0 ? K_pad[0] : 0, planes), fm, f);
       mark(evs, "lif_fwd", l);
       if (nl == 1 && rlif(l)) {  // declared RLIF: the recurrent scan over the projection
         RlifFwdArgs ra{};
@@ -1627,7 +1666,7 @@ struct snn_engine {
         w.x = ds.x.p;
         w.rows = rows_p;
         w.rows_slot = slot_p;
-        w.B = B; w.T_pad = T_pad; w.x_row_stride = IN_pad;
+        w.B = B; w.T_pad = T_pad; w.x_row_stride = row_of(ds);
         w.xshift = xshift.p;
         w.in_features = IN;
         w.dbg_clk = clocks ? dbg_clk.p + size_t(1 + 2 * L) * clk_region() : nullptr;
@@ -1830,11 +1869,21 @@ struct snn_engine {
     if (loss) *loss = *h_loss;
     if (acc) *acc = *h_acc;
   }
+  // after an update launch: the fused tail already wrote the StepResult into the
+  // mapped ring, so only the sync remains (no D2H copies)
+  void read_step_result(float* loss, double* acc) {
+    if (!ring_on()) return read_result(loss, acc);
+    CK(cudaStreamSynchronize(stream));
+    const int64_t r = (host_step - 1) & (kRing - 1);
+    if (loss) *loss = ring_loss_h[r];
+    if (acc) *acc = ring_acc_h[r];
+  }
 
   void step_rows(const uint32_t* rows, const Dataset& ds, int update, float* loss, double* acc) {
     set_rows_host(rows, ds);
     launch(ds, update);
-    read_result(loss, acc);
+    if (update) read_step_result(loss, acc);
+    else read_result(loss, acc);
   }
 
   // level 0 off, 1 tensors + clock stamps, 2 clock stamps only (kernels run their
@@ -2203,7 +2252,7 @@ snn_status snn_train_step_packed(snn_engine* e, const uint8_t* packed_batch,
     e->set_rows_host(rows.data(), e->scratch);
     e->launch(e->scratch, 1);
     const auto t2 = std::chrono::steady_clock::now();
-    e->read_result(loss, accuracy);
+    e->read_step_result(loss, accuracy);
     const auto t3 = std::chrono::steady_clock::now();
     if (trace) {  // host-side phase times of the e2e call (diagnostics)
       static double acc[3];
@@ -2234,6 +2283,19 @@ snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const in
         fail(SNN_ERR_ARGUMENT, "target %lld outside [0,%d)", (long long)targets[i], e->C);
       e->plab_host[i] = int32_t(targets[i]);
     }
+    // StepResults: the fused tail writes them into the mapped ring (read after a sync
+    // at least every kRing steps); other tails copy each one out with k_result_out
+    const bool ring = e->ring_on();
+    const int64_t s0 = e->host_step;
+    size_t read = 0;
+    auto drain = [&](size_t upto) {
+      CK(cudaStreamSynchronize(e->stream));
+      for (; read < upto; ++read) {
+        const int64_t r = (s0 + int64_t(read)) & (snn_engine::kRing - 1);
+        if (losses) losses[read] = ring ? e->ring_loss_h[r] : e->pres_loss[read];
+        if (accuracies) accuracies[read] = ring ? e->ring_acc_h[r] : e->pres_acc[read];
+      }
+    };
     e->pipe_stage(0, packed, targets);
     for (size_t k = 0; k < n_steps; ++k) {
       const int sl = int(k & 1);
@@ -2241,6 +2303,10 @@ snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const in
       e->launch(e->pslot[sl], 1);
       CK(cudaEventRecord(e->ev_used[sl], e->stream));
       if (k + 1 < n_steps) e->pipe_stage(k + 1, packed, targets);  // runs while step k does
+      if (ring) {
+        if (k + 1 - read == size_t(snn_engine::kRing)) drain(k + 1);
+        continue;
+      }
       float* hl = nullptr;
       double* ha = nullptr;
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hl), e->pres_loss + k, 0));
@@ -2248,11 +2314,7 @@ snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const in
       k_result_out<<<1, 1, 0, e->stream>>>(e->result_loss.p, e->result_acc.p, hl, ha);
       CK(cudaGetLastError());
     }
-    CK(cudaStreamSynchronize(e->stream));
-    for (size_t k = 0; k < n_steps; ++k) {
-      if (losses) losses[k] = e->pres_loss[k];
-      if (accuracies) accuracies[k] = e->pres_acc[k];
-    }
+    drain(n_steps);
   });
 }
 

@@ -562,26 +562,29 @@ struct FwdArgs {
   long long* dbg_clk;     // optional [gridDim.x*gridDim.y][kClkStride] phase timestamps
   const int32_t* xshift;  // layer 0: batch roll along the features, [0, in_features) (shift_augment)
   int B, T, T_pad, TT, NT, in_kind, stages, spb, in_features;
+  int x_row;              // layer 0: bytes per packed time row of the dataset (K_pad of the
+                          // staged layout, or in_features for a batch in the reference layout)
   int planes;  // bf16 W planes multiplied (3: the fp32 path; 2 / 1: fast modes)
   float theta;
 };
 
-constexpr int kFwdStagesMax = 2;
+constexpr int kFwdStagesMax = 4;
 constexpr int kFwdSpbMax = 2;
 constexpr int kFwdScanWarps = 4 * kFwdSpbMax;
 constexpr int kFwdThreads = 32 * (kFwdScanWarps + 4 + 2);
 
 constexpr uint32_t kPlaneTile = 128 * 128;  // 128 rows x 64 bf16 = 16 KB
 
-__host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT, int spb) {
-  return 3 * kPlaneTile + uint32_t(spb * TT) * 128u;
+__host__ __device__ constexpr uint32_t fwd_stage_bytes(int TT, int spb, int planes = 3) {
+  return uint32_t(planes) * kPlaneTile + uint32_t(spb * TT) * 128u;
 }
 // dataset run of one sample for one t-tile: TT/8 rows of K_pad bytes (layer 0)
 __host__ __device__ constexpr uint32_t fwd_xrun_bytes(int TT, int K_pad) {
   return uint32_t(TT / 8) * uint32_t(K_pad);
 }
-__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int spb, int stages, int x_kpad) {
-  return uint32_t(stages) * fwd_stage_bytes(TT, spb) +
+__host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int spb, int stages, int x_kpad,
+                                                      int planes = 3) {
+  return uint32_t(stages) * fwd_stage_bytes(TT, spb, planes) +
          2u * ((uint32_t(spb) * fwd_xrun_bytes(TT, x_kpad) + 1023) & ~1023u) + 1024 + 256;
 }
 // TMEM columns for N-wide accumulators, doubled when several t-tiles pipeline.
@@ -686,12 +689,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* smem = align1024(smem_raw);
   const int SPB = a.spb;
   const int NTOT = SPB * a.TT;  // MMA N (stacked samples)
-  const uint32_t stage_bytes = fwd_stage_bytes(a.TT, SPB);
+  const uint32_t stage_bytes = fwd_stage_bytes(a.TT, SPB, a.planes);
   const int S = a.stages;
-  // layer 0: each sample's dataset run for the current t-tile is bulk-copied
-  // into xbuf[tt % 2] (double-buffered across t-tiles)
-  const uint32_t xrun = a.in_kind == 0 ? fwd_xrun_bytes(a.TT, K_pad0) : 0u;
-  const uint32_t xbuf_bytes = (uint32_t(SPB) * xrun + 1023) & ~1023u;
+  // layer 0: each sample's dataset run for the current t-tile (TT/8 rows of x_row
+  // bytes, contiguous) is bulk-copied into xbuf[tt % 2] (double-buffered across t-tiles)
+  const uint32_t xrun = a.in_kind == 0 ? uint32_t(a.TT / 8) * uint32_t(a.x_row) : 0u;
+  const uint32_t xbuf_bytes =
+      a.in_kind == 0 ? (uint32_t(SPB) * fwd_xrun_bytes(a.TT, K_pad0) + 1023) & ~1023u : 0u;
   uint8_t* xbuf = smem + S * stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * xbuf_bytes);
   uint64_t* empty = full + S;
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mbar_arrive_expect_tx(&xfull[xb], uint32_t(nsamp) * xrun);
           for (int sm = 0; sm < nsamp; ++sm)
             bulk_load(xbuf + xb * xbuf_bytes + sm * xrun,
-                      a.x + (size_t(rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(K_pad0),
+                      a.x + (size_t(rows[b0 + sm]) * (a.T_pad / 8) + tt * (a.TT / 8)) * size_t(a.x_row),
                       xrun, &xfull[xb]);
         }
         mbar_wait(&empty[s], ph ^ 1);
@@ -805,7 +809,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (clk != nullptr && it < 32) clk[16 + it] = clock64();
         tc_fence_after();
         const uint32_t A = smem_u32(smem + s * stage_bytes);
-        const uint32_t Bt = A + 3 * kPlaneTile;
+        const uint32_t Bt = A + a.planes * kPlaneTile;
         const uint32_t d = tmem + buf * NTOT;
         if (a.planes == 3) {  // the fp32 path, fully unrolled
 #pragma unroll
@@ -839,7 +843,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           mbar_wait(&lfull[kb], (li - 1) & 1);
           tc_fence_after();
           const uint32_t A = smem_u32(smem + kb * stage_bytes);
-          const uint32_t Bt = A + 3 * kPlaneTile;
+          const uint32_t Bt = A + a.planes * kPlaneTile;
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
@@ -877,7 +881,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint64_t nxt0 = fetch(it + 1, tid), nxt1 = fetch(it + 1, tid + 128);
       if (a.in_kind == 0 && it % KB == 0) mbar_wait(&xfull[tt & 1], (tt >> 1) & 1);
       mbar_wait(&empty[s], ph ^ 1);
-      const uint32_t Bt = smem_u32(smem + s * stage_bytes + 3 * kPlaneTile);
+      const uint32_t Bt = smem_u32(smem + s * stage_bytes + a.planes * kPlaneTile);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int u = tid + 128 * h;
@@ -886,11 +890,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (a.in_kind == 0) {
           // dataset bytes [t/8][k] (bulk-copied), bit 7-(t%8): 8 k of one t-group -> 8 rows
           const int g = r >> 3, q = r & 7;
-          const uint8_t* xr = xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * K_pad0;
+          const uint8_t* xr = xbuf + (tt & 1) * xbuf_bytes + sm * xrun + g * a.x_row;
           uint64_t cur = 0ull;
           if (sm < nsamp) {
             if (!kShift || xsh == 0) {
-              cur = *reinterpret_cast<const uint64_t*>(xr + kb * 64 + q * 8);
+              // rows of the reference layout are only 4-byte aligned; features >= in
+              // of the last block belong to the next row there and are masked
+              const uint32_t* xw = reinterpret_cast<const uint32_t*>(xr + kb * 64 + q * 8);
+              cur = uint64_t(xw[0]) | (uint64_t(xw[1]) << 32);
+              const int nb = a.in_features - (kb * 64 + q * 8);
+              if (nb < 8) cur = nb <= 0 ? 0ull : cur & ((1ull << (8 * nb)) - 1ull);
             } else {
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -935,7 +944,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // fused: lane j writes the next layer's B row t0+j (its quadrant's 32 spikes
       // of that step, from the ballot word) into stage q/2's B part
       const bool feed = li + 1 < a.n_layers;
-      const uint32_t feed_b = smem_u32(smem + (q >> 1) * stage_bytes + 3 * kPlaneTile);
+      const uint32_t feed_b = smem_u32(smem + (q >> 1) * stage_bytes + a.planes * kPlaneTile);
       float v = 0.0f;
       for (int tt = 0; tt < a.NT; ++tt) {
         const int g = li * a.NT + tt;  // accumulator use (fused: one per layer)
@@ -2878,6 +2887,12 @@ struct AdamArgs {
   int opt_kind;              // 0 Adam, 1 SGD + momentum (optimize.hpp:69-84)
   float momentum;
   int n_mon;                 // activity regularizer values at grads[n_params + 2 + m]
+  // one-rank fused tail: every step's StepResult also goes to entry (step & ring_mask)
+  // of a host-mapped ring (host batches read it after their one sync: no per-step
+  // result kernel or copy); nullptr = off
+  float* ring_loss;
+  double* ring_acc;
+  int64_t ring_mask;
 };
 
 // Adam on one flat parameter (optimize.hpp:88-110); bias corrections of step s+1.
@@ -3274,7 +3289,8 @@ __device__ __forceinline__ void wgrad_vec(const ReduceArgs& rd, const AdamArgs& 
 
 // block 0: loss sum in batch order (objective.hpp:57-72) + hits + regularizer ->
 // StepResult; scratch: 8 KB of free shared memory
-__device__ __forceinline__ void wgrad_loss(const ReduceArgs& rd, const AdamArgs& ad, uint8_t* scratch_smem) {
+__device__ __forceinline__ void wgrad_loss(const ReduceArgs& rd, const AdamArgs& ad, uint8_t* scratch_smem,
+                                           int64_t step0) {
   const int tid = threadIdx.x;
   if (blockIdx.x == 0) {
     uint32_t* scratch = reinterpret_cast<uint32_t*>(scratch_smem);
@@ -3295,6 +3311,10 @@ __device__ __forceinline__ void wgrad_loss(const ReduceArgs& rd, const AdamArgs&
       rd.grads[rd.n_params + 1] = float(hits);
       *ad.loss_out = l;
       *ad.acc_out = double(hits) / double(ad.B_global);
+      if (ad.ring_loss != nullptr) {
+        ad.ring_loss[step0 & ad.ring_mask] = l;
+        ad.ring_acc[step0 & ad.ring_mask] = double(hits) / double(ad.B_global);
+      }
     }
   }
 }
@@ -3356,7 +3376,7 @@ __device__ __forceinline__ void wgrad_fused_epilogue(const WgradLayer& a, int j,
     __threadfence();
     atomicAdd(tl.tile_cnt + tile, 1u);
   }
-  wgrad_loss(rd, ad, smem + size_t(nm) * ncg * 16384);
+  wgrad_loss(rd, ad, smem + size_t(nm) * ncg * 16384, s);
   if (tid == 0) {
     while (ld_acquire_gpu_u32(tl.tile_cnt + tile) < unsigned(S)) __nanosleep(32);
     fence_proxy_async_global();  // the bulk loads below see the other splits' partials

@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
 B = int(os.environ.get("PROBE_B", "256"))
-eng = Engine(shd_spec(), TrainConfig(batch_size=B, seed=0), 128)
+eng = Engine(shd_spec(), TrainConfig(batch_size=B, seed=0, gemm_planes=int(os.environ.get("PROBE_PLANES", "3"))), 128)
 eng.synth_dataset(16384, seed=1)
 rows = np.arange(B, dtype=np.uint32)
 for _ in range(int(os.environ.get("PROBE_TRAIN", "300"))):   # trained-like spike rates
@@ -30,3 +30,9 @@ eng.debug(True)
 eng.train_step(rows)
 for l in range(2):
     print(f"layer {l} spike rate {eng.fetch('spikes', l).mean():.3f}")
+if os.environ.get("PROBE_KB"):
+    # MMA-warp time stamps at each k-block's full-barrier pass (clk[16 + it])
+    c = eng.fetch("clk")[1][: B // 2]
+    kbt = c[:, 16:16 + 11].astype(np.int64)
+    print("k-block issue deltas (median)", np.median(np.diff(kbt, axis=1), 0).astype(int).tolist(),
+          "first after start", int(np.median(kbt[:, 0] - c[:, 0])))

@@ -1198,3 +1198,38 @@ def test_lif_readout_parity(orc, case):
         lo, ao = orc.train_step(net, st, pk, T, y, opts=o)
         l2, a2 = eng.train_step(rows)
         assert abs(l2 - lo) <= 1e-3 * abs(lo) and a2 == ao
+
+
+RAW_LAYOUT = [
+    # (name, net, B, T, steps): IN % 4 == 0 and T_pad / 8 == ceil(T / 8), so host batches
+    # are used in the reference layout as DMA'd (row pitch IN, last block masked)
+    ("c1-shape", Net(), 16, 128, 3),
+    ("ring-wrap", Net(inp=40, hidden=(24, 20), classes=5), 2, 64, 4100),
+]
+
+
+@pytest.mark.parametrize("case", RAW_LAYOUT, ids=[c[0] for c in RAW_LAYOUT])
+def test_reference_layout_batches_match_staged_dataset(orc, case):
+    """Host batches kept in the reference layout [B][ceil(T/8)][IN] (no device re-layout;
+    the forward / wgrad decoders read rows of IN bytes and mask features >= IN of the last
+    64-k block) train bit-identically to the same rows of a staged [n][T_pad/8][IN_pad]
+    dataset; the StepResults of snn_train_steps_packed come from the mapped ring the fused
+    tail writes (more steps than the ring holds: drained mid-call)."""
+    import torch
+    _, net, B, T, K = case
+    x, y = orc.synth_raster(net.classes, B * K, T, net.inp, 5)
+    pk = orc.pack_time(x)
+    a = make_engine(net, B, T, seed=2)
+    b = make_engine(net, B, T, seed=2)
+    c = make_engine(net, B, T, seed=2)
+    b.stage_dataset(pk, y)
+    ref = [b.train_step(np.arange(k * B, (k + 1) * B, dtype=np.uint32)) for k in range(K)]
+    pinned = torch.empty((K, B) + pk.shape[1:], dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[...] = pk.reshape((K, B) + pk.shape[1:])
+    la, aa = a.train_steps_packed(pinned.numpy(), y.reshape(K, B))
+    assert [float(v) for v in la] == [r[0] for r in ref]
+    assert [float(v) for v in aa] == [r[1] for r in ref]
+    assert np.array_equal(a.get_params(), b.get_params())
+    n1 = min(K, 3)
+    lc = [c.train_step_packed(pk[k * B:(k + 1) * B], y[k * B:(k + 1) * B]) for k in range(n1)]
+    assert lc == ref[:n1]

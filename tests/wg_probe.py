@@ -7,7 +7,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2402_18994_b200 import Engine, TrainConfig, shd_spec
-eng = Engine(shd_spec(), TrainConfig(batch_size=256, seed=0), 128)
+eng = Engine(shd_spec(), TrainConfig(batch_size=256, seed=0, gemm_planes=int(os.environ.get("PROBE_PLANES", "3"))), 128)
 eng.synth_dataset(16384, seed=1)
 eng.debug(2)  # clock stamps only
 rows = np.arange(256, dtype=np.uint32)
