@@ -575,11 +575,13 @@ def main():
                     "d2h_bytes_per_step": d2h,
                     "path": f"snn_train_steps_packed (train() over host batches, {chunk} per call): "
                             "every step's pinned host batch (reference layout) -> H2D on a copy stream "
-                            "-> device re-layout, overlapped with the previous step's graph; every "
-                            "step's loss/acc D2H; one host sync per call",
+                            "into the step's device slot (used in place when ceil(T/8) = T_pad/8 and "
+                            "input % 4 == 0, else re-laid out there), overlapped with the previous "
+                            "step's graph; every step's loss/acc written by its own tail into mapped "
+                            "host memory (12 B D2H); one host sync per call",
                     "per_step_call": {"value": sync_value, "unit": UNIT,
-                                      "path": "snn_train_step_packed: H2D, re-layout, step graph, "
-                                              "D2H loss/acc, host sync every step"}},
+                                      "path": "snn_train_step_packed: H2D, step graph, loss/acc "
+                                              "into mapped host memory, host sync every step"}},
             "gpu_launches": eng.launches_per_step * args.steps,
             **({"ranks": ranks} if ranks is not None else {}),
             "roofline": roofline,
