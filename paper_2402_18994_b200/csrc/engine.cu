@@ -2299,14 +2299,12 @@ snn_status snn_train_steps_packed(snn_engine* e, const uint8_t* packed, const in
     e->pipe_stage(0, packed, targets);
     for (size_t k = 0; k < n_steps; ++k) {
       const int sl = int(k & 1);
+      if (ring && k + 1 - read > size_t(snn_engine::kRing)) drain(k);  // step k reuses an unread entry
       CK(cudaStreamWaitEvent(e->stream, e->ev_ready[sl], 0));
       e->launch(e->pslot[sl], 1);
       CK(cudaEventRecord(e->ev_used[sl], e->stream));
       if (k + 1 < n_steps) e->pipe_stage(k + 1, packed, targets);  // runs while step k does
-      if (ring) {
-        if (k + 1 - read == size_t(snn_engine::kRing)) drain(k + 1);
-        continue;
-      }
+      if (ring) continue;
       float* hl = nullptr;
       double* ha = nullptr;
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hl), e->pres_loss + k, 0));

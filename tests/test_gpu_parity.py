@@ -1204,6 +1204,7 @@ RAW_LAYOUT = [
     # (name, net, B, T, steps): IN % 4 == 0 and T_pad / 8 == ceil(T / 8), so host batches
     # are used in the reference layout as DMA'd (row pitch IN, last block masked)
     ("c1-shape", Net(), 16, 128, 3),
+    ("c1-shape-17", Net(), 16, 128, 17),
     ("ring-wrap", Net(inp=40, hidden=(24, 20), classes=5), 2, 64, 4100),
 ]
 
