@@ -569,6 +569,9 @@ struct FwdArgs {
 };
 
 constexpr int kFwdStagesMax = 4;
+#ifndef SNN_FWD_EXP
+#define SNN_FWD_EXP 0  // timing experiments only (A/B builds): 1 decoders skip their stores, 2 no MMAs
+#endif
 constexpr int kFwdSpbMax = 2;
 constexpr int kFwdScanWarps = 4 * kFwdSpbMax;
 constexpr int kFwdThreads = 32 * (kFwdScanWarps + 4 + 2);
@@ -769,10 +772,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                       xrun, &xfull[xb]);
         }
         mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], uint32_t(a.planes) * kPlaneTile);
+        mbar_arrive_expect_tx(&full[s], SNN_FWD_EXP == 3 ? 0u : uint32_t(a.planes) * kPlaneTile);
         uint8_t* A = smem + s * stage_bytes;
         // W planes [3][K_pad][H_pad] read MN-major: per plane two 64-neuron x 64-k boxes
-        for (int p = 0; p < a.planes; ++p)
+        for (int p = 0; p < (SNN_FWD_EXP == 3 ? 0 : a.planes); ++p)
           for (int h = 0; h < 2; ++h)
             tma_load_2d(A + p * kPlaneTile + h * 8192, &tm_w, &full[s], nt * 128 + h * 64,
                         p * K_pad0 + kb * 64);
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint32_t d = tmem + buf * NTOT;
         if (a.planes == 3) {  // the fp32 path, fully unrolled
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
+          for (int ks = 0; ks < (SNN_FWD_EXP == 2 ? 0 : 4); ++ks) {
             const uint64_t bd = sdesc_sw128(Bt + ks * 32, 16, 1024);
 #pragma unroll
             for (int p = 2; p >= 0; --p) {
@@ -910,7 +913,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < (SNN_FWD_EXP == 1 ? 0 : 8); ++j)
             st_shared_v4(Bt + sw128_off(sm * a.TT + 8 * g + j, q),
                          expand_bytes01((cur >> (7 - j)) & 0x0101010101010101ull));
         } else {
