@@ -4,7 +4,7 @@
 # report is kept so gpurun_out stays under the copy-back limit.
 #   gpurun --timeout 3000 -- 'bash profiles/evidence.sh r02a'
 mkdir -p gpurun_out
-TAG=${1:-r02b}
+TAG=${1:-r02c}
 set -x
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo PYTEST_EXIT $? >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
@@ -25,6 +25,10 @@ python profiles/summarize_ncu.py gpurun_out/step_c1.ncu-rep ${TAG} && mv profile
 python profiles/summarize_ncu.py gpurun_out/step_c2.ncu-rep ${TAG}_c2 && mv profiles/${TAG}_c2_ncu.json gpurun_out/
 python profiles/summarize_ncu.py gpurun_out/step_c4.ncu-rep ${TAG}_c4 && mv profiles/${TAG}_c4_ncu.json gpurun_out/
 rm -f gpurun_out/step_c2.ncu-rep gpurun_out/step_c4.ncu-rep
+# compute-sanitizer (racecheck / synccheck / memcheck over one C1 step), if the pool allows it
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tests/sanitize_step.py > gpurun_out/sanitize_$tool.log 2>&1; echo "EXIT $?" >> gpurun_out/sanitize_$tool.log
+done
 du -sh gpurun_out/*
 tail -2 gpurun_out/pytest_gpu.log
 tail -1 gpurun_out/smoke.log
