@@ -2,7 +2,7 @@
 # modes, C2, C3 at global batch 4096, C4, C5), the reference arm, the ncu launch list of the
 # C1 bench and full captures of one step (C1, C2, C4), summarised on the box; only the C1
 # report is kept so gpurun_out stays under the copy-back limit.
-#   gpurun --timeout 3000 -- 'bash profiles/evidence.sh r02a'
+#   gpurun --timeout 3000 -- 'bash profiles/evidence.sh r02c'
 mkdir -p gpurun_out
 TAG=${1:-r02c}
 set -x
