@@ -587,8 +587,10 @@ __host__ __device__ constexpr uint32_t fwd_xrun_bytes(int TT, int K_pad) {
 }
 __host__ __device__ constexpr uint32_t fwd_smem_bytes(int TT, int spb, int stages, int x_kpad,
                                                       int planes = 3) {
+  // stages | dataset runs | barriers (256) | per-scan-warp ballot rows (kFwdScanWarps x 32 words)
   return uint32_t(stages) * fwd_stage_bytes(TT, spb, planes) +
-         2u * ((uint32_t(spb) * fwd_xrun_bytes(TT, x_kpad) + 1023) & ~1023u) + 1024 + 256;
+         2u * ((uint32_t(spb) * fwd_xrun_bytes(TT, x_kpad) + 1023) & ~1023u) + 1024 + 256 +
+         uint32_t(kFwdScanWarps) * 128u;
 }
 // TMEM columns for N-wide accumulators, doubled when several t-tiles pipeline.
 __host__ __device__ constexpr uint32_t tmem_cols_for(int N, int NT) {
@@ -620,30 +622,38 @@ __device__ __forceinline__ void tmem_dealloc_any(uint32_t cols, uint32_t taddr) 
 //   pre = v - theta ; s = pre >= 0 ; v = ((v * bc) + I) - s * theta
 // kGeneral adds bias, a debug copy of I and a valid-step count (< 32 only in the
 // last chunk).  V is stored before each step (membrane entering step t).
-template <bool kGeneral>
-__device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, float* dp, int hpad,
+// The step's ballot (the 32 neurons' spikes of step j) goes to the warp's row of
+// shared words sbal (lane 0 stores it) and lane j reads word j back after the chunk:
+// one store per step instead of a per-step lane == j select.  kHpad > 0: the V row
+// stride as a constant (immediate store offsets); 0: runtime hpad.
+template <bool kGeneral, int kHpad = 0>
+__device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, float* dp, int hpad_rt,
                                           int nvalid, float vb, float bn, float theta, int lane,
-                                          float& v, uint32_t& myword, uint32_t& tmask) {
+                                          uint32_t* sbal, float& v, uint32_t& myword, uint32_t& tmask) {
+  const int hpad = kHpad > 0 ? kHpad : hpad_rt;
   const float ntheta = -theta;
-  myword = 0u;
+  const uint32_t sb = smem_u32(sbal);
   tmask = 0u;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     float I = __uint_as_float(r[j]);
     if (kGeneral) {
       I = __fadd_rn(I, bn);
-      if (dp != nullptr && j < nvalid) dp[size_t(j) * hpad] = I;
+      if (dp != nullptr && j < nvalid) dp[j * hpad] = I;
     }
-    vp[size_t(j) * hpad] = v;
+    vp[j * hpad] = v;
     const float pre = __fadd_rn(v, ntheta);
     const bool sp = kGeneral ? (pre >= 0.0f && j < nvalid) : (pre >= 0.0f);
     const float m = __fmul_rn(v, vb);
     const float ai = __fadd_rn(m, I);
     v = __fsub_rn(ai, sp ? theta : 0.0f);
     const uint32_t bal = __ballot_sync(0xffffffffu, sp);
-    myword = (lane == j) ? bal : myword;
-    tmask |= uint32_t(sp) << j;
+    if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sb + 4u * j), "r"(bal) : "memory");
+    if (sp) tmask |= 1u << j;
   }
+  __syncwarp();
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(myword) : "r"(sb + 4u * lane) : "memory");
+  __syncwarp();  // the row is rewritten by the next chunk
 }
 
 // 32 steps of the DECLARED ALIF cell (not in the reference; oracle/spiketrain_oracle.h
@@ -709,6 +719,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* lfull = xempty + 2;  // fused layers: W planes of k-block 0 / 1 landed
   uint64_t* bready = lfull + 2;  // fused layers: next layer's B tiles written by the scan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bready + 1);
+  uint32_t* sbal_all = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid (H_pad / 128, sample groups): a sample group's neuron tiles run together
@@ -982,9 +993,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                          myword, tmask);
             else if (ly.bias != nullptr || ly.dbg_i != nullptr || t0 + 32 > a.T)
               lif_chunk<true>(r, vp, ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
-                              a.T - t0, vb, bn, a.theta, lane, v, myword, tmask);
+                              a.T - t0, vb, bn, a.theta, lane, sbal_all + warp * 32, v, myword, tmask);
+            else if (ly.H_pad == 128)
+              lif_chunk<false, 128>(r, vp, nullptr, 128, 32, vb, 0.0f, a.theta, lane, sbal_all + warp * 32, v,
+                                    myword, tmask);
             else
-              lif_chunk<false>(r, vp, nullptr, ly.H_pad, 32, vb, 0.0f, a.theta, lane, v, myword, tmask);
+              lif_chunk<false>(r, vp, nullptr, ly.H_pad, 32, vb, 0.0f, a.theta, lane, sbal_all + warp * 32, v,
+                               myword, tmask);
           }
           // padded steps (t >= T): no spikes; V rows beyond T are never read
           ly.s_np[(size_t(b) * a.T_pad + t0 + lane) * hw + nt * 4 + q] = myword;
