@@ -661,20 +661,22 @@ __device__ __forceinline__ void lif_chunk(const uint32_t (&r)[32], float* vp, fl
 //   th = theta + a ; pre = v - th ; s = pre >= 0 ; v = ((v * bc) + I) - s * th ;
 //   a = (a * gc) + (1 - gc) * s
 // V and the adaptation a are stored before each step (state entering step t).
+template <int kHpad = 0>
 __device__ __forceinline__ void alif_chunk(const uint32_t (&r)[32], float* vp, float* ap, float* dp,
-                                           int hpad, int nvalid, float vb, float gc, float bn,
-                                           bool has_bias, float theta, int lane, float& v, float& ad,
-                                           uint32_t& myword, uint32_t& tmask) {
+                                           int hpad_rt, int nvalid, float vb, float gc, float bn,
+                                           bool has_bias, float theta, int lane, uint32_t* sbal, float& v,
+                                           float& ad, uint32_t& myword, uint32_t& tmask) {
+  const int hpad = kHpad > 0 ? kHpad : hpad_rt;
   const float omg = __fsub_rn(1.0f, gc);
-  myword = 0u;
+  const uint32_t sb = smem_u32(sbal);
   tmask = 0u;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     float I = __uint_as_float(r[j]);
     if (has_bias) I = __fadd_rn(I, bn);
-    if (dp != nullptr && j < nvalid) dp[size_t(j) * hpad] = I;
-    vp[size_t(j) * hpad] = v;
-    ap[size_t(j) * hpad] = ad;
+    if (dp != nullptr && j < nvalid) dp[j * hpad] = I;
+    vp[j * hpad] = v;
+    ap[j * hpad] = ad;
     const float th = __fadd_rn(theta, ad);
     const float pre = __fsub_rn(v, th);
     const bool sp = pre >= 0.0f && j < nvalid;
@@ -683,9 +685,12 @@ __device__ __forceinline__ void alif_chunk(const uint32_t (&r)[32], float* vp, f
     v = __fsub_rn(ai, sp ? th : 0.0f);
     ad = __fadd_rn(__fmul_rn(ad, gc), sp ? omg : 0.0f);
     const uint32_t bal = __ballot_sync(0xffffffffu, sp);
-    myword = (lane == j) ? bal : myword;
-    tmask |= uint32_t(sp) << j;
+    if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sb + 4u * j), "r"(bal) : "memory");
+    if (sp) tmask |= 1u << j;
   }
+  __syncwarp();  // ballots of the chunk -> lane j takes step j's word (as lif_chunk)
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(myword) : "r"(sb + 4u * lane) : "memory");
+  __syncwarp();
 }
 
 // kShift: layer-0 launches of an epoch loop with shift_augment (reads a.xshift);
@@ -986,11 +991,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint32_t myword = 0u, tmask = 0u;
           if (t0 < a.T) {
             float* vp = ly.v_out + (size_t(b) * a.T_pad + t0) * ly.H_pad + n;
-            if (kAlif && alif)
+            if (kAlif && alif && ly.H_pad == 128)
+              alif_chunk<128>(r, vp, ly.a_out + (vp - ly.v_out),
+                              ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, 128,
+                              min(32, a.T - t0), vb, gc, bn, ly.bias != nullptr, a.theta, lane,
+                              sbal_all + warp * 32, v, ad, myword, tmask);
+            else if (kAlif && alif)
               alif_chunk(r, vp, ly.a_out + (vp - ly.v_out),
                          ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
-                         min(32, a.T - t0), vb, gc, bn, ly.bias != nullptr, a.theta, lane, v, ad,
-                         myword, tmask);
+                         min(32, a.T - t0), vb, gc, bn, ly.bias != nullptr, a.theta, lane,
+                         sbal_all + warp * 32, v, ad, myword, tmask);
             else if (ly.bias != nullptr || ly.dbg_i != nullptr || t0 + 32 > a.T)
               lif_chunk<true>(r, vp, ly.dbg_i != nullptr ? ly.dbg_i + (vp - ly.v_out) : nullptr, ly.H_pad,
                               a.T - t0, vb, bn, a.theta, lane, sbal_all + warp * 32, v, myword, tmask);
@@ -1132,8 +1142,13 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void load_v16(const float* __restrict__ p, int hpad, int nval,
                                          float (&v)[16]) {
+  if (hpad == 128 && nval >= 16) {  // 128-wide layers, whole chunk: immediate offsets
 #pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = e < nval ? __ldg(p + size_t(e) * hpad) : 0.0f;
+    for (int e = 0; e < 16; ++e) v[e] = __ldg(p + e * 128);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = e < nval ? __ldg(p + size_t(e) * hpad) : 0.0f;
+  }
 }
 // affine map of 16 reverse steps: G' = (bc - theta g) G + g dS
 template <int kAct, bool kTail>
