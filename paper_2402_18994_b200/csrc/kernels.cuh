@@ -897,7 +897,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int it = 0; it < total; ++it) {
       const int s = it % S, ph = (it / S) & 1;
       const int tt = it / KB, kb = (it % KB + rot) % KB;
-      const uint64_t nxt0 = fetch(it + 1, tid), nxt1 = fetch(it + 1, tid + 128);
       if (a.in_kind == 0 && it % KB == 0) mbar_wait(&xfull[tt & 1], (tt >> 1) & 1);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t Bt = smem_u32(smem + s * stage_bytes + a.planes * kPlaneTile);
@@ -943,8 +942,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (a.in_kind == 0 && it % KB == KB - 1) mbar_arrive(&xempty[tt & 1]);
       fence_async_smem();
       mbar_arrive(&full[s]);
-      cur0 = nxt0;
-      cur1 = nxt1;
+      // next stage's spike words after the proxy fence (it would wait for them)
+      cur0 = fetch(it + 1, tid);
+      cur1 = fetch(it + 1, tid + 128);
     }
   } else if (warp / 4 < nsamp) {
     // ---------------- LIF scan epilogue: thread = neuron (TMEM lane) of sample warp/4
@@ -1630,17 +1630,19 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const int t_lo = tt * a.TT + sg * seg_len;               // first step of my segment
       const int t_hi = min(t_lo + seg_len, a.T);                // one past the last valid
       const uint32_t tcol = tmem + (uint32_t(q * 32) << 16) + buf * a.TT + sg * seg_len;
+      // the membranes of the segment's top sub-chunk do not depend on the GEMM: their
+      // loads are in flight across the accumulator wait
+      const float* vseg = vrow + size_t(t_lo) * a.H_pad;
+      const int top = seg_len - 16;
+      float vr[16], vn[16];
+      load_v16(vseg + size_t(top) * a.H_pad, a.H_pad, t_hi - (t_lo + top), vn);
       mbar_wait(&acc_full[buf], (j / nbuf) & 1);
       tc_fence_after();
       if (clk != nullptr && threadIdx.x == 0 && j == 0) clk[1] = clock64();
       // ---- pass 1: compose the segment's affine map, t descending.  The membranes
       // of the next 16-step sub-chunk are loaded while this one is processed.
       float A = 1.0f, Bc = 0.0f;
-      const float* vseg = vrow + size_t(t_lo) * a.H_pad;
-      const int top = seg_len - 16;
       const uint32_t vcol = tmem + (uint32_t(q * 32) << 16) + a.TT + sg * seg_len;  // V cache
-      float vr[16], vn[16];
-      load_v16(vseg + size_t(top) * a.H_pad, a.H_pad, t_hi - (t_lo + top), vn);
       for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
 #pragma unroll
