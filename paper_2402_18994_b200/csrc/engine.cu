@@ -625,6 +625,10 @@ struct snn_engine {
       for (int j = 0; j < NJ; ++j) splits_w[j] = splits_for(hi, j);
       if (const char* v = std::getenv("SNN_WG_SPLIT_SAMPLES"))
         for (int j = 0; j < NJ; ++j) splits_w[j] = std::max(1, B / std::max(1, std::atoi(v)));
+      if (std::getenv("SNN_PRINT_PLAN"))  // diagnostics: the weight-gradient split plan
+        for (int j = 0; j < NJ; ++j)
+          std::fprintf(stderr, "wgrad layer %d: m_tiles %d mg %d n_tiles %d splits %d stages %d\n", j,
+                       M_pad_w[j] / 128, mg_w[j], N_pad[j] / n_tile_w[j], splits_w[j], wg_stages_l[j]);
     }
     // parameter entries (network.hpp:210-226 order)
     entries.clear();

@@ -42,3 +42,12 @@ if os.environ.get("PROBE_ALL"):
         o = np.argsort(arr[lo:hi])[::-1][:4] + lo
         print(f"  CTAs [{lo},{hi}) latest arrivals", [(int(i), round(float(arr[i]), 1)) for i in o],
               "median", round(float(np.median(arr[lo:hi])), 1))
+if os.environ.get("PROBE_LAYERS"):
+    # per-layer loop / total cycles (layer ranges from the engine's split plan)
+    info = eng.wgrad_plan() if hasattr(eng, "wgrad_plan") else None
+    loop = c[:, 3] - c[:, 2]
+    tot = c[:, 13] - c[:, 0]
+    edges = [int(x) for x in os.environ["PROBE_LAYERS"].split(",")]
+    for lo, hi in zip(edges[:-1], edges[1:]):
+        print(f"  CTAs [{lo},{hi}) loop median {int(np.median(loop[lo:hi]))} max {int(loop[lo:hi].max())}"
+              f"  total median {int(np.median(tot[lo:hi]))} max {int(tot[lo:hi].max())}")
