@@ -324,7 +324,8 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
         acc[jj][3] = __fadd_rn(acc[jj][3], r[jj].w);
       }
     };
-    float4 ra[kGroups], rb[kGroups];
+    float4 ra[kGroups];
+    float4 rb[kGroups];
     int k = next_k();
     if (k >= 0) load_row(k, ra);
     while (k >= 0) {
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(kRoThreads) k_readout(ReadoutArgs a) {
         if (c < rs) buf[t * rs + c] = vout;  // classes >= C (the scratch column) are zero
       }
   }
+  if (a.dbg_clk != nullptr && lane == 0) a.dbg_clk[b * kClkStride + 16 + warp] = clock64();  // per warp
   __syncthreads();
   RO_CLK(2)
   if (warp == 0) {

@@ -42,3 +42,7 @@ print("per-step spikes: mean", cnt.mean(), "max", cnt.max(), "| per-warp max: me
       np.median(wmax), "| per-CTA max warp-max: median", np.median(wmax.max(1)))
 print("corr(projection cycles, CTA max warp-max)", np.corrcoef(d[:, 1], wmax.max(1))[0, 1],
       "cycles per warp-max spike", np.median(d[:, 1] / np.maximum(wmax.max(1), 1)))
+# per-warp end of the projection (clk[16 + warp]) relative to the phase start (clk[1])
+pw = clk[:, 16:24] - clk[:, 1:2]
+print("projection end per warp (median over CTAs)", np.median(pw, axis=0).astype(int).tolist(),
+      "max", pw.max(axis=0).tolist())
