@@ -1156,14 +1156,40 @@ __device__ __forceinline__ void load_v16(const float* __restrict__ p, int hpad, 
 template <int kAct, bool kTail>
 __device__ __forceinline__ void bwd_compose(const uint32_t (&r)[16], const float (&vr)[16], int nval,
                                             float vb, float theta, const BwdArgs& a, float& A,
-                                            float& Bc) {
+                                            float& Bc, float (&gout)[16]) {
 #pragma unroll
   for (int e = 15; e >= 0; --e) {
-    if (kTail && e >= nval) continue;
+    if (kTail && e >= nval) {
+      gout[e] = 0.0f;
+      continue;
+    }
     const float g = surrogate_t<kAct>(a.slope, a.aux, __fsub_rn(vr[e], theta));
+    gout[e] = g;
     const float at = vb - theta * g;
     Bc = at * Bc + g * __uint_as_float(r[e]);
     A = at * A;
+  }
+}
+// 16 reverse steps in the reference order with the surrogates the compose pass
+// computed (bit-identical values, read back from TMEM): dI_t = G ; gs = dS + (-G) theta ;
+// G = G bc + gs g ; dbeta += G V ; dbias += G
+template <bool kTail>
+__device__ __forceinline__ void bwd_replay_g(const uint32_t (&r)[16], const float (&vr)[16],
+                                             const uint32_t (&gr)[16], int nval, float vb, float theta,
+                                             float& G, float& db, float& dbias, float (&x)[16]) {
+#pragma unroll
+  for (int e = 15; e >= 0; --e) {
+    if (kTail && e >= nval) {
+      x[e] = 0.0f;
+      continue;
+    }
+    const float g = __uint_as_float(gr[e]);
+    const float gi = G;
+    const float gs = __fadd_rn(__uint_as_float(r[e]), __fmul_rn(-gi, theta));
+    G = __fadd_rn(__fmul_rn(gi, vb), __fmul_rn(gs, g));
+    x[e] = gi;
+    db = __fadd_rn(db, __fmul_rn(gi, vr[e]));
+    dbias = __fadd_rn(dbias, gi);
   }
 }
 // 16 reverse steps in the reference order: dI_t = G ; gs = dS + (-G) theta ;
@@ -1644,22 +1670,25 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       // ---- pass 1: compose the segment's affine map, t descending.  The membranes
       // of the next 16-step sub-chunk are loaded while this one is processed.
       float A = 1.0f, Bc = 0.0f;
-      const uint32_t vcol = tmem + (uint32_t(q * 32) << 16) + a.TT + sg * seg_len;  // V cache
+      // one t-tile: the surrogates of pass 1 are kept in spare TMEM columns for pass 3
+      // (which re-reads V from L2 for the dbeta sum only)
+      const uint32_t gcol = tmem + (uint32_t(q * 32) << 16) + a.TT + sg * seg_len;
       for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
 #pragma unroll
         for (int e = 0; e < 16; ++e) vr[e] = vn[e];
-        // next: c0 - 16, or (end of pass 1, no V cache) the top sub-chunk for pass 3
+        // next: c0 - 16, or (end of pass 1) the top sub-chunk for pass 3
         const int cn = c0 >= 16 ? c0 - 16 : top;
-        if (c0 >= 16 || !vcache) load_v16(vseg + size_t(cn) * a.H_pad, a.H_pad, t_hi - (t_lo + cn), vn);
-        if (vcache) tmem_st16(vcol + c0, vr);
+        load_v16(vseg + size_t(cn) * a.H_pad, a.H_pad, t_hi - (t_lo + cn), vn);
         if (nval <= 0) continue;
         uint32_t r[16];
         tmem_ld16(tcol + c0, r);
         tmem_ld_wait();
         if constexpr (kReg) add_dcount(r, rterm);
-        if (nval >= 16) bwd_compose<kAct, false>(r, vr, 16, vb, theta, a, A, Bc);
-        else bwd_compose<kAct, true>(r, vr, nval, vb, theta, a, A, Bc);
+        float gk[16];
+        if (nval >= 16) bwd_compose<kAct, false>(r, vr, 16, vb, theta, a, A, Bc, gk);
+        else bwd_compose<kAct, true>(r, vr, nval, vb, theta, a, A, Bc, gk);
+        if (vcache) tmem_st16(gcol + c0, gk);
       }
       if (vcache) tmem_st_wait();
       xA[sidx] = A;
@@ -1675,23 +1704,14 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       // ---- pass 3: exact-order replay of my segment
       for (int c0 = top; c0 >= 0; c0 -= 16) {
         const int nval = t_hi - (t_lo + c0);
-        uint32_t r[16];
-        if (vcache) {
-          if (nval <= 0) continue;
-          uint32_t vv[16];
-          tmem_ld16(vcol + c0, vv);
-          tmem_ld16(tcol + c0, r);
-          tmem_ld_wait();
+        uint32_t r[16], gv[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) vr[e] = __uint_as_float(vv[e]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) vr[e] = vn[e];
-          if (c0 >= 16) load_v16(vseg + size_t(c0 - 16) * a.H_pad, a.H_pad, t_hi - (t_lo + c0 - 16), vn);
-          if (nval <= 0) continue;
-          tmem_ld16(tcol + c0, r);
-          tmem_ld_wait();
-        }
+        for (int e = 0; e < 16; ++e) vr[e] = vn[e];
+        if (c0 >= 16) load_v16(vseg + size_t(c0 - 16) * a.H_pad, a.H_pad, t_hi - (t_lo + c0 - 16), vn);
+        if (nval <= 0) continue;
+        if (vcache) tmem_ld16(gcol + c0, gv);
+        tmem_ld16(tcol + c0, r);
+        tmem_ld_wait();
         if constexpr (kReg) add_dcount(r, rterm);
         if (a.dbg_ds != nullptr) {
 #pragma unroll
@@ -1700,8 +1720,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               a.dbg_ds[(size_t(b) * a.T_pad + t_lo + c0 + e) * a.H_pad + n] = __uint_as_float(r[e]);
         }
         float x[16];
-        if (nval >= 16) bwd_replay<kAct, false>(r, vr, 16, vb, theta, a, G, db, dbias, x);
-        else bwd_replay<kAct, true>(r, vr, nval, vb, theta, a, G, db, dbias, x);
+        if (vcache) {
+          if (nval >= 16) bwd_replay_g<false>(r, vr, gv, 16, vb, theta, G, db, dbias, x);
+          else bwd_replay_g<true>(r, vr, gv, nval, vb, theta, G, db, dbias, x);
+        } else {
+          if (nval >= 16) bwd_replay<kAct, false>(r, vr, 16, vb, theta, a, G, db, dbias, x);
+          else bwd_replay<kAct, true>(r, vr, nval, vb, theta, a, G, db, dbias, x);
+        }
         uint32_t ph_[8], pm_[8], pl_[8];
 #pragma unroll
         for (int e = 0; e < 16; e += 2) split3_pack(x[e], x[e + 1], ph_[e / 2], pm_[e / 2], pl_[e / 2]);
