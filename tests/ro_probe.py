@@ -12,8 +12,13 @@ eng.synth_dataset(16384, seed=1)
 perm = eng.epoch_permutation(0, 16384)
 sched = np.concatenate([perm[(i * B) % 16384:(i * B) % 16384 + B] for i in range(1200)]).astype(np.uint32)
 eng.upload_schedule(sched)
-eng.enqueue_steps(0, 1192)
-eng.sync()
+if os.environ.get("PROBE_LOAD"):   # A/B builds: the same trained state (and rasters) for each
+    eng.load_checkpoint(os.environ["PROBE_LOAD"])
+else:
+    eng.enqueue_steps(0, 1192)
+    eng.sync()
+    if os.environ.get("PROBE_SAVE"):
+        eng.save_checkpoint(os.environ["PROBE_SAVE"])
 eng.debug(2)
 eng.enqueue_steps(1192, 8)
 eng.sync()
