@@ -562,7 +562,7 @@ struct FwdArgs {
 
 constexpr int kFwdStagesMax = 4;
 #ifndef SNN_FWD_EXP
-#define SNN_FWD_EXP 0  // timing experiments only (A/B builds): 1 decoders skip their stores, 2 no MMAs
+#define SNN_FWD_EXP 0  // timing experiments only (A/B builds): 1 decoders skip their stores, 2 no MMAs, 3 no W loads
 #endif
 constexpr int kFwdSpbMax = 2;
 constexpr int kFwdScanWarps = 4 * kFwdSpbMax;
