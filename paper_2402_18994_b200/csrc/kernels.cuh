@@ -1132,25 +1132,15 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-template <int kHpad>
-__device__ __forceinline__ void load_v16_c(const float* __restrict__ p, float (&v)[16]) {
-#pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = __ldg(p + e * kHpad);
-}
 __device__ __forceinline__ void load_v16(const float* __restrict__ p, int hpad, int nval,
                                          float (&v)[16]) {
-  // whole chunks of the common widths: immediate offsets (no per-element address math)
-  if (nval >= 16) {
-    switch (hpad) {
-      case 128: load_v16_c<128>(p, v); return;
-      case 256: load_v16_c<256>(p, v); return;
-      case 512: load_v16_c<512>(p, v); return;
-      case 1024: load_v16_c<1024>(p, v); return;
-      default: break;
-    }
-  }
+  if (hpad == 128 && nval >= 16) {  // 128-wide layers, whole chunk: immediate offsets
 #pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = e < nval ? __ldg(p + size_t(e) * hpad) : 0.0f;
+    for (int e = 0; e < 16; ++e) v[e] = __ldg(p + e * 128);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = e < nval ? __ldg(p + size_t(e) * hpad) : 0.0f;
+  }
 }
 // affine map of 16 reverse steps: G' = (bc - theta g) G + g dS
 template <int kAct, bool kTail>
