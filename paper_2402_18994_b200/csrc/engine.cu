@@ -1586,7 +1586,7 @@ struct snn_engine {
       }
       bw.dbg_clk = clocks ? dbg_clk.p + size_t(1 + L + l) * clk_region() : nullptr;
       bw.B = B; bw.T = T; bw.T_pad = T_pad; bw.TT = TT; bw.NT = NT;
-      bw.K_pad = N_pad[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
+      bw.K_pad = N_pad[l + 1]; bw.K = N[l + 1]; bw.H = H[l]; bw.H_pad = H_pad[l]; bw.act = net.activation;
       bw.stages = std::min(bwd_stages, NT * (N_pad[l + 1] / 64));
       bw.theta = net.threshold; bw.slope = net.slope; bw.aux = net.aux;
       for (size_t m = 0; m < mon_layers.size(); ++m)

@@ -1060,6 +1060,8 @@ struct BwdArgs {
   float* dbg_ds;               // optional [B][T_pad][H_pad]
   long long* dbg_clk;          // optional [gridDim.x*gridDim.y][8] phase timestamps
   int B, T, T_pad, TT, NT, K_pad, H, H_pad, act, stages;
+  int K;                       // unpadded contraction width (next layer's neurons / classes):
+                               // 16-k MMA steps past it in the last k-block are skipped
   int planes;                  // bf16 planes per real operand (3: fp32 path)
   float theta, slope, aux;
   // activity regularizer on a monitored layer (kReg launches only)
@@ -1416,6 +1418,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         const uint32_t A = smem_u32(smem + s * stage_bytes);
         const uint32_t Bt = A + 3 * kPlaneTile;
         const uint32_t d = tmem + buf * a.TT;
+        // 16-k steps that hold data (the readout-fed layer: 20 classes of a 64-wide block)
+        const int ksn = kb == KB - 1 ? min(4, (a.K - kb * 64 + 15) / 16) : 4;
         // (pa, pb) plane products with pa + pb <= planes - 1, smallest terms first:
         // 6 for the fp32 path, 3 (hi.hi + hi.mid + mid.hi) for planes = 2, 1 for bf16
         const int pa[10] = {2, 1, 0, 1, 0, 0, 1, 0, 0, 0};
@@ -1423,6 +1427,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         if (a.planes == 3) {  // the fp32 path, fully unrolled
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
+            if (ks >= ksn) break;
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
               const uint64_t ad = sdesc_sw128(A + pa[q] * kPlaneTile + ks * 32, 16, 1024);
