@@ -751,6 +751,9 @@ struct snn_engine {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               227 * 1024));
     for (auto fn : {k_lif_bwd<0>, k_lif_bwd<1>, k_lif_bwd<2>, k_lif_bwd<3>, k_lif_bwd<4>, k_lif_bwd<5>,
+                    k_lif_bwd<0, false, false, false, 2>, k_lif_bwd<1, false, false, false, 2>,
+                    k_lif_bwd<2, false, false, false, 2>, k_lif_bwd<3, false, false, false, 2>,
+                    k_lif_bwd<4, false, false, false, 2>, k_lif_bwd<5, false, false, false, 2>,
                     k_lif_bwd<0, true>, k_lif_bwd<1, true>, k_lif_bwd<2, true>, k_lif_bwd<3, true>,
                     k_lif_bwd<4, true>, k_lif_bwd<5, true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1308,14 +1311,18 @@ struct snn_engine {
       }
       return;
     }
+    // plain LIF: several t-tiles take the 32-byte sector-store kernel
+    const bool one = bw.NT == 1;
+#define SNN_BWD_PLAIN(A) (one ? k_lif_bwd<A> : k_lif_bwd<A, false, false, false, 2>)
     switch (act) {
-      case 1: launch(k_lif_bwd<1>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
-      case 2: launch(k_lif_bwd<2>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
-      case 3: launch(k_lif_bwd<3>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
-      case 4: launch(k_lif_bwd<4>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
-      case 5: launch(k_lif_bwd<5>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
-      default: launch(k_lif_bwd<0>, grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 1: launch(SNN_BWD_PLAIN(1), grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 2: launch(SNN_BWD_PLAIN(2), grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 3: launch(SNN_BWD_PLAIN(3), grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 4: launch(SNN_BWD_PLAIN(4), grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      case 5: launch(SNN_BWD_PLAIN(5), grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
+      default: launch(SNN_BWD_PLAIN(0), grid, dim3(kBwdThreads), smem, tw, td, to, bw); break;
     }
+#undef SNN_BWD_PLAIN
   }
 
   // ---------------------------------------------------------------- step
